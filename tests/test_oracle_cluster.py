@@ -1,0 +1,96 @@
+"""Pins of the oracle's greedy drivers (Appendix E):
+certified clustering (P12: Algs 1-2 clusters have exact relative error
+<= eps), Alg. 3 never violates eps (P13,
+provable by F3), cover/determinism, and the paper's regimes on config 1."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import cluster as oc
+import synth
+
+
+def random_collection(seed, N=10, m=16, n=3, G=3, noise=0.02):
+    R = np.random.default_rng(seed)
+    U = [np.linalg.qr(R.standard_normal((m, 2)))[0] for _ in range(G)]
+    blocks = []
+    for i in range(N):
+        a = U[i % G] @ R.standard_normal((2, n)) * R.uniform(0.5, 2) + noise * R.standard_normal((m, n))
+        blocks.append(a)
+    return oracle.block_spectra(blocks)
+
+
+def check_cover(res, N):
+    assert sorted(np.concatenate([np.array(c) for c in res.clusters]).tolist()) == list(range(N))
+    for cid, c in enumerate(res.clusters):
+        for pos, b in enumerate(c):
+            assert res.assign[b] == cid and res.order[b] == pos
+
+
+def exact_rel(sp, members, r):
+    e2 = oracle.exact_groups(sp, [members], r)[0]
+    return np.sqrt(e2 / sum(sp.E[b] for b in members))
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("eps", [0.05, 0.2])
+@pytest.mark.parametrize("r", [2, 4])
+def test_certified_algorithms(seed, eps, r):
+    sp = random_collection(seed)
+    N = len(sp.A)
+    runs = [oc.cluster(sp, oc.MAX_NORM, r, eps)]
+    for srt in (oc.SORT_FROBENIUS, oc.SORT_RESIDUAL):
+        runs.append(oc.cluster(sp, oc.RESIDUAL_ALG, r, eps, srt))
+        runs.append(oc.cluster(sp, oc.APPROX, r, eps, srt))
+    for k, res in enumerate(runs):
+        check_cover(res, N)
+        for c, e2, tot in zip(res.clusters, res.err2, res.total):
+            if len(c) == 1:
+                continue
+            rel = exact_rel(sp, c, r)
+            assert rel <= eps + 1e-9, (k, c, rel)
+            # the certificate itself upper-bounds the exact error
+            assert rel <= np.sqrt(e2 / tot) + 1e-9
+
+
+def test_deterministic():
+    sp = random_collection(3)
+    a = oc.cluster(sp, oc.APPROX, 3, 0.1, oc.SORT_RESIDUAL)
+    b = oc.cluster(sp, oc.APPROX, 3, 0.1, oc.SORT_RESIDUAL)
+    assert a.clusters == b.clusters and a.err2 == b.err2
+
+
+def test_max_norm_spec_example():
+    """anchor energy 100 (4 cols), r = 4, eps = 0.05, two tail
+    blocks of energy 0.1 -> both merged (rel = sqrt(0.2/100.2) = 0.0447)."""
+    R = np.random.default_rng(0)
+    Q = np.linalg.qr(R.standard_normal((12, 6)))[0]
+    anchor = Q[:, :4] * 5.0                  # energy 4*25 = 100
+    t1 = Q[:, 4:5] * np.sqrt(0.1)
+    t2 = Q[:, 5:6] * np.sqrt(0.1) * 0.999
+    sp = oracle.block_spectra([anchor, t1, t2])
+    res = oc.cluster(sp, oc.MAX_NORM, 4, 0.05)
+    # head = anchor (width 4 = r); tail blocks are appended smallest first
+    assert res.clusters == [[0, 2, 1]]
+    assert abs(np.sqrt(res.err2[0] / res.total[0]) - np.sqrt(0.1999 / 100.1999)) < 1e-4
+
+
+def test_zero_blocks_merge_unconditionally():
+    R = np.random.default_rng(1)
+    A = R.standard_normal((8, 4))
+    sp = oracle.block_spectra([A, np.zeros((8, 2)), R.standard_normal((8, 4))])
+    res = oc.cluster(sp, oc.APPROX, 2, 0.01)
+    assert any(1 in c and len(c) > 1 for c in res.clusters)
+
+
+def test_config1_regimes():
+    """Config 1 (BASELINE configs[0]): residual-sort Alg. 3 recovers the 4
+    hidden groups at eps = 0.05 (SURVEY §8(d) simulated outcome)."""
+    col = synth.config1()
+    sp = oracle.block_spectra(col.blocks)
+    res = oc.cluster(sp, oc.APPROX, col.r, 0.05, oc.SORT_RESIDUAL)
+    assert len(res.clusters) == 4
+    for c in res.clusters:
+        assert len({int(col.groups[b]) for b in c}) == 1
+    for c in res.clusters:
+        assert exact_rel(sp, c, col.r) <= 0.05
