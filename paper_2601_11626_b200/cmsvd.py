@@ -1,0 +1,233 @@
+"""Thin ctypes binding of libcmsvd (include/cmsvd.h): argument marshalling
+only -- every step of the path runs in the library's CUDA kernels.  There is
+no CPU fallback: if the shared library or a CUDA device is missing, the calls
+raise.
+
+Torch is used only as plumbing: device tensors may be passed (their
+``data_ptr()`` goes to the C ABI with ``where=DEVICE``) and the context can
+borrow torch's current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcmsvd.so")
+
+OK, E_ARG, E_SHAPE, E_NONFINITE, E_STATE, E_NOCONV, E_CUDA, E_NOMEM = range(8)
+HOST, DEVICE = 0, 1
+WEYL, RESIDUAL, INCREMENTAL, ALL = 1, 2, 4, 7
+RAW, TRUNC = 0, 1
+ALG_MAX_NORM, ALG_RESIDUAL, ALG_APPROX = 0, 1, 2
+SORT_FROBENIUS, SORT_RESIDUAL = 0, 1
+
+EXPORTS = ["cmsvd_status_string", "cmsvd_last_error", "cmsvd_version", "cmsvd_create", "cmsvd_destroy",
+           "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_cluster", "cmsvd_launch_count"]
+
+
+class CmsvdError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_status_name(status)}: {msg}")
+        self.status = status
+
+
+class ClusterOpts(ctypes.Structure):
+    _fields_ = [("algorithm", ctypes.c_int32), ("sort", ctypes.c_int32), ("knn", ctypes.c_int32),
+                ("operand", ctypes.c_int32), ("r", ctypes.c_int32), ("eps", ctypes.c_double)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libcmsvd.so (raises if it is missing -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libcmsvd.so not built at {path}; run __graft_entry__.build()")
+    L = ctypes.CDLL(path)
+    vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32
+    L.cmsvd_status_string.restype = ctypes.c_char_p
+    L.cmsvd_status_string.argtypes = [ctypes.c_int]
+    L.cmsvd_last_error.restype = ctypes.c_char_p
+    L.cmsvd_last_error.argtypes = [vp]
+    L.cmsvd_version.restype = ctypes.c_char_p
+    L.cmsvd_version.argtypes = []
+    L.cmsvd_create.restype = ctypes.c_int
+    L.cmsvd_create.argtypes = [ctypes.c_int, vp, ctypes.POINTER(vp)]
+    L.cmsvd_destroy.restype = ctypes.c_int
+    L.cmsvd_destroy.argtypes = [vp]
+    L.cmsvd_register.restype = ctypes.c_int
+    L.cmsvd_register.argtypes = [vp, i64, i32, vp, vp, vp, ctypes.c_int]
+    L.cmsvd_block_spectra.restype = ctypes.c_int
+    L.cmsvd_block_spectra.argtypes = [vp, i32, vp, vp, vp]
+    L.cmsvd_pair_errors.restype = ctypes.c_int
+    L.cmsvd_pair_errors.argtypes = [vp, vp, i64, i32, u32, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]
+    L.cmsvd_cluster.restype = ctypes.c_int
+    L.cmsvd_cluster.argtypes = [vp, ctypes.POINTER(ClusterOpts), vp, vp, vp, vp, vp, vp]
+    L.cmsvd_launch_count.restype = i64
+    L.cmsvd_launch_count.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def _status_name(s: int) -> str:
+    try:
+        return load().cmsvd_status_string(s).decode()
+    except Exception:
+        return f"status {s}"
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return ctypes.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Context:
+    """One cmsvd context = one registered collection on one device/stream."""
+
+    def __init__(self, device: int = 0, stream=None):
+        L = load()
+        h = ctypes.c_void_p()
+        s = L.cmsvd_create(device, ctypes.c_void_p(stream) if stream else None, ctypes.byref(h))
+        if s != OK:
+            raise CmsvdError(s, "cmsvd_create failed (is a CUDA device visible?)")
+        self._h = h
+        self._L = L
+        self.count = 0
+        self.r = 0
+
+    def _check(self, s):
+        if s != OK:
+            raise CmsvdError(s, self._L.cmsvd_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.cmsvd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def launches(self) -> int:
+        return int(self._L.cmsvd_launch_count(self._h))
+
+    # -- cmsvd_register --------------------------------------------------
+    def register(self, blocks, where: int | None = None):
+        """blocks: (N, n, m) float32 array/tensor (block i column-major), or a
+        list of column-major m x n_i arrays (Fortran-ordered numpy or tensors
+        holding the transposed (n_i, m) layout)."""
+        if hasattr(blocks, "dim") and blocks.dim() == 3:          # torch tensor (N, n, m)
+            N, n, m = blocks.shape
+            dev = blocks.is_cuda
+            base = blocks.data_ptr()
+            stride = n * m * 4
+            ptrs = [base + i * stride for i in range(N)]
+            ns = np.full(N, n, np.int32)
+            keep = blocks
+        elif isinstance(blocks, np.ndarray) and blocks.ndim == 3:
+            blocks = np.ascontiguousarray(blocks, dtype=np.float32)
+            N, n, m = blocks.shape
+            dev = False
+            ptrs = [blocks.ctypes.data + i * n * m * 4 for i in range(N)]
+            ns = np.full(N, n, np.int32)
+            keep = blocks
+        else:
+            keep, ptrs, nl = [], [], []
+            dev = False
+            m = None
+            for b in blocks:
+                if hasattr(b, "data_ptr"):
+                    dev = b.is_cuda
+                    nn, mm = b.shape
+                    ptrs.append(b.data_ptr())
+                else:
+                    f = np.asfortranarray(b, dtype=np.float32)
+                    mm, nn = f.shape
+                    ptrs.append(f.ctypes.data)
+                    b = f
+                keep.append(b)
+                nl.append(nn)
+                m = mm
+            N = len(ptrs)
+            ns = np.array(nl, np.int32)
+        w = (DEVICE if dev else HOST) if where is None else where
+        arr = (ctypes.c_void_p * N)(*ptrs)
+        self._check(self._L.cmsvd_register(self._h, int(m), int(N), _ptr(ns), arr, None, w))
+        del keep
+        self.count = N
+        self.m = int(m)
+        return self
+
+    # -- cmsvd_block_spectra ---------------------------------------------
+    def block_spectra(self, r: int):
+        N = self.count
+        E = np.zeros(N)
+        sig = np.zeros((N, r), np.float32)
+        rank = np.zeros(N, np.int32)
+        self._check(self._L.cmsvd_block_spectra(self._h, int(r), _ptr(E), _ptr(sig), _ptr(rank)))
+        self.r = r
+        return E, sig, rank
+
+    # -- cmsvd_pair_errors -----------------------------------------------
+    def pair_errors(self, pairs, r: int | None = None, kinds: int = ALL, operand: int = RAW,
+                    want_sigma: bool = True, want_mu: bool = True, out=None):
+        """Host path: pairs (P,2) int32 numpy -> dict of numpy outputs.
+        Device path: pairs as an int32 CUDA tensor and ``out`` a dict of CUDA
+        tensors (err2 (P,3) f64, total (P,) f64, sigma_tilde/mu (P,r) f32)."""
+        r = self.r if r is None else r
+        if hasattr(pairs, "data_ptr") and pairs.is_cuda:
+            P = pairs.shape[0]
+            self._check(self._L.cmsvd_pair_errors(self._h, _ptr(pairs), P, r, kinds, operand, DEVICE,
+                                                  _ptr(out["err2"]), _ptr(out["total"]),
+                                                  _ptr(out.get("sigma_tilde")), _ptr(out.get("mu"))))
+            return out
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        P = pairs.shape[0]
+        err2 = np.zeros((P, 3))
+        total = np.zeros(P)
+        st = np.zeros((P, r), np.float32) if want_sigma else None
+        mu = np.zeros((P, r), np.float32) if want_mu else None
+        self._check(self._L.cmsvd_pair_errors(self._h, _ptr(pairs), P, r, kinds, operand, HOST, _ptr(err2),
+                                              _ptr(total), _ptr(st), _ptr(mu)))
+        return {"err2": err2, "total": total, "sigma_tilde": st, "mu": mu}
+
+    # -- cmsvd_cluster ---------------------------------------------------
+    def cluster(self, algorithm: int, eps: float, r: int | None = None, sort: int = SORT_FROBENIUS,
+                knn: int = 1, operand: int = RAW):
+        r = self.r if r is None else r
+        N = self.count
+        o = ClusterOpts(algorithm, sort, knn, operand, r, eps)
+        assign = np.zeros(N, np.int32)
+        order = np.zeros(N, np.int32)
+        K = ctypes.c_int32()
+        ce = np.zeros(N)
+        ct = np.zeros(N)
+        ne = ctypes.c_int64()
+        self._check(self._L.cmsvd_cluster(self._h, ctypes.byref(o), _ptr(assign), _ptr(order), ctypes.byref(K),
+                                          _ptr(ce), _ptr(ct), ctypes.byref(ne)))
+        k = K.value
+        clusters = [[] for _ in range(k)]
+        for b in np.argsort(order, kind="stable"):
+            clusters[assign[b]].append(int(b))
+        for c in clusters:
+            c.sort(key=lambda b: order[b])
+        return {"assign": assign, "order": order, "clusters": clusters, "err2": ce[:k], "total": ct[:k],
+                "n_evals": ne.value}

@@ -1,0 +1,144 @@
+// abi.cu -- the extern "C" boundary of libcmsvd (declared in include/cmsvd.h).
+// Every entry point converts C++/CUDA failures into a cmsvd_status plus a
+// per-context message; no exception crosses the ABI.
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+#include "engine.h"
+
+using namespace cmsvd;
+
+namespace cmsvd {
+__global__ void k_check_pairs(const int2* __restrict__ pairs, int64_t P, int count, int* bad) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int2 v = pairs[p];
+  if (v.x < 0 || v.x >= count || v.y < 0 || v.y >= count) atomicOr(bad, 1);
+}
+
+cudaError_t launch_check_pairs(Ctx& c, const int2* d_pairs, int64_t P, int count, int* d_bad) {
+  k_check_pairs<<<(unsigned)((P + 255) / 256), 256, 0, c.stream>>>(d_pairs, P, count, d_bad);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+}  // namespace cmsvd
+
+#define GUARD_CTX(ctx)                       \
+  if (!(ctx)) return CMSVD_E_ARG;            \
+  Ctx& c = (ctx)->c;                         \
+  c.err.clear();                             \
+  {                                          \
+    cudaError_t _e = cudaSetDevice(c.device); \
+    if (_e != cudaSuccess) return cuda_fail(c, _e, "cudaSetDevice"); \
+  }
+
+extern "C" {
+
+const char* cmsvd_status_string(cmsvd_status s) {
+  switch (s) {
+    case CMSVD_OK: return "CMSVD_OK";
+    case CMSVD_E_ARG: return "CMSVD_E_ARG";
+    case CMSVD_E_SHAPE: return "CMSVD_E_SHAPE";
+    case CMSVD_E_NONFINITE: return "CMSVD_E_NONFINITE";
+    case CMSVD_E_STATE: return "CMSVD_E_STATE";
+    case CMSVD_E_NOCONV: return "CMSVD_E_NOCONV";
+    case CMSVD_E_CUDA: return "CMSVD_E_CUDA";
+    case CMSVD_E_NOMEM: return "CMSVD_E_NOMEM";
+  }
+  return "CMSVD_E_UNKNOWN";
+}
+
+const char* cmsvd_last_error(cmsvd_ctx ctx) { return ctx ? ctx->c.err.c_str() : "NULL context"; }
+
+const char* cmsvd_version(void) { return "cmsvd 0.1 (sm_100a)"; }
+
+cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
+  if (!out) return CMSVD_E_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return CMSVD_E_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return CMSVD_E_CUDA;
+  cmsvd_ctx h = new (std::nothrow) cmsvd_ctx_s();
+  if (!h) return CMSVD_E_NOMEM;
+  h->c.device = device;
+  if (cuda_stream) {
+    h->c.stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete h;
+      return CMSVD_E_CUDA;
+    }
+    h->c.own_stream = true;
+  }
+  cudaDeviceGetAttribute(&h->c.sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (const char* env = getenv("CMSVD_WS_BYTES")) h->c.ws_budget = (size_t)atoll(env);
+  *out = h;
+  return CMSVD_OK;
+}
+
+cmsvd_status cmsvd_destroy(cmsvd_ctx ctx) {
+  if (!ctx) return CMSVD_OK;
+  Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  cudaStreamSynchronize(c.stream);
+  DevMem* bufs[] = {&c.arena, &c.d_E, &c.d_U, &c.d_sig, &c.d_Ftrunc, &c.d_sig32, &c.d_rank,
+                    &c.d_bdesc, &c.d_adesc_raw, &c.d_adesc_trunc, &c.d_meta64, &c.d_meta32};
+  for (DevMem* b : bufs) release(*b);
+  for (auto& b : c.ws) release(b);
+  for (auto& b : c.cws) release(b);
+  if (c.own_stream) cudaStreamDestroy(c.stream);
+  delete ctx;
+  return CMSVD_OK;
+}
+
+cmsvd_status cmsvd_register(cmsvd_ctx ctx, int64_t m, int32_t count, const int32_t* n, const float* const* blocks,
+                            const int64_t* ld, int where) {
+  GUARD_CTX(ctx);
+  try {
+    return do_register(c, m, count, n, blocks, ld, where);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "register: host allocation failed");
+  } catch (...) {
+    return fail(c, CMSVD_E_ARG, "register: unexpected exception");
+  }
+}
+
+cmsvd_status cmsvd_block_spectra(cmsvd_ctx ctx, int32_t r, double* energy, float* sigma, int32_t* rank_out) {
+  GUARD_CTX(ctx);
+  try {
+    return do_block_spectra(c, r, energy, sigma, rank_out);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "block_spectra: host allocation failed");
+  } catch (...) {
+    return fail(c, CMSVD_E_ARG, "block_spectra: unexpected exception");
+  }
+}
+
+cmsvd_status cmsvd_pair_errors(cmsvd_ctx ctx, const int32_t* pairs, int64_t P, int32_t r, uint32_t kinds, int operand,
+                               int where, double* err2, double* total, float* sigma_tilde, float* mu) {
+  GUARD_CTX(ctx);
+  try {
+    return do_pair_errors(c, pairs, P, r, kinds, operand, where, err2, total, sigma_tilde, mu);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "pair_errors: host allocation failed");
+  } catch (...) {
+    return fail(c, CMSVD_E_ARG, "pair_errors: unexpected exception");
+  }
+}
+
+cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_t* assign, int32_t* order,
+                           int32_t* n_clusters, double* cluster_err2, double* cluster_total, int64_t* n_evals) {
+  GUARD_CTX(ctx);
+  try {
+    return do_cluster(c, opts, assign, order, n_clusters, cluster_err2, cluster_total, n_evals);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "cluster: host allocation failed");
+  } catch (...) {
+    return fail(c, CMSVD_E_ARG, "cluster: unexpected exception");
+  }
+}
+
+int64_t cmsvd_launch_count(cmsvd_ctx ctx) { return ctx ? ctx->c.launches : 0; }
+
+}  // extern "C"

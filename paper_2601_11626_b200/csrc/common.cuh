@@ -1,0 +1,149 @@
+// common.cuh -- shared device helpers and the internal context of libcmsvd.
+// B200 (sm_100a) only.  Nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/cmsvd.h"
+
+
+namespace cmsvd {
+
+// Numerical-rank rule (reading A5): keep sigma_l > kTau * sigma_1.
+constexpr double kTau = 1e-5;
+constexpr int kThreads = 256;
+constexpr int kArenaAlign = 32;  // floats (128 B) between block starts
+
+// ---------------------------------------------------------------------------
+// Device-side descriptors
+// ---------------------------------------------------------------------------
+// A "base" of a candidate merge: a block (its left singular basis and
+// spectrum) or a cluster state of Alg. 2 / Alg. 3.
+struct BaseDesc {
+  const float* basis;   // m x q column-major (ld = m); first rr columns = tracked top-r basis
+  const double* spec;   // spectrum, non-increasing, ns entries (sigma(A_i) all / mu pool / sigma~)
+  int q;                // columns of the projection basis used by this evaluation
+  int rr;               // size of the tracked top-r part (incremental)
+  int ns;               // length of spec
+  int pad;
+  double E;             // energy ||.||_F^2 of the base
+  double tail_inc;      // E - sum_{l<rr} spec_l^2, computed as a sum of the dropped part (>= 0)
+  double rest_res;      // E - sum_{all l} spec_l^2 (energy not represented in spec, >= 0)
+  double tailw;         // E - sum_{l<r} spec_l^2 (Weyl), summed from the dropped part
+};
+
+// An appended operand F (RAW block or TRUNC factor).
+struct AppDesc {
+  const float* F;       // m x w column-major (ld = m)
+  int w;
+  int pad;
+  double E;             // full energy of the appended block
+  double extra;         // E - ||F||_F^2 for TRUNC (the dropped tail), 0 for RAW
+  double tailw;         // E - sum_{l<r} sigma_l^2 of the appended block (Weyl)
+};
+
+// One batched-GEMM problem for the SIMT kernels.
+struct GemmDesc {
+  const float* A; const float* B; const float* C0;  // C0: optional minuend (R = C0 - A B)
+  void* C;
+  int64_t lda, ldb, ldc, ldc0;
+  int M, N, K;
+  int sym;  // 1: C symmetric, only lower tiles computed and mirrored
+};
+
+// ---------------------------------------------------------------------------
+// Host-side context
+// ---------------------------------------------------------------------------
+struct DevMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int64_t launches = 0;
+  int sm_count = 148;
+
+  // collection
+  int64_t m = 0;
+  int32_t count = 0;
+  std::vector<int32_t> n;        // host copy
+  std::vector<int64_t> boff;     // arena offsets (floats)
+  int nmax = 0;
+  DevMem arena;                  // packed fp32 blocks
+  DevMem d_E;                    // fp64 energies
+  std::vector<double> E;         // host copy
+
+  // spectra (valid when spectra_r > 0)
+  int spectra_r = 0;
+  std::vector<int64_t> uoff;     // basis offsets (floats), block i basis m x k_i
+  std::vector<int32_t> kcols;    // k_i = min(m, n_i)
+  DevMem d_U;                    // fp32 left singular vectors
+  DevMem d_sig;                  // fp64 all singular values, count x nmax
+  std::vector<double> sig;       // host copy
+  std::vector<int32_t> rank, rr;
+  DevMem d_Ftrunc;               // fp32 TRUNC operands, m x min(r, k_i) each at foff
+  std::vector<int64_t> foff;
+  bool trunc_ready = false;
+  DevMem d_sig32, d_rank, d_bdesc, d_adesc_raw, d_adesc_trunc, d_meta64, d_meta32;
+
+  // workspaces (grow-only)
+  DevMem ws[16];
+  DevMem cws[16];  // cluster-driver state and scratch
+  size_t ws_budget = (size_t)8 << 30;  // bytes of pair workspace per chunk
+};
+
+// grow-only device buffer
+cudaError_t ensure(DevMem& b, size_t bytes);
+void release(DevMem& b);
+
+}  // namespace cmsvd
+
+struct cmsvd_ctx_s {
+  cmsvd::Ctx c;
+};
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+namespace cmsvd {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_sumf(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed tree); red must hold blockDim.x/32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    int nw = blockDim.x >> 5;
+    t = lane < nw ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+}  // namespace cmsvd

@@ -1,0 +1,394 @@
+// engine.cu -- host orchestration of libcmsvd: collection registration (S1),
+// block spectra (S2) and the batched pair-evaluation pipeline (S3-S9).
+// Everything runs on the context stream; host syncs only where a result must
+// be read back (status flags, host outputs).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "engine.h"
+#include "kernels.cuh"
+
+namespace cmsvd {
+
+cudaError_t ensure(DevMem& b, size_t bytes) {
+  if (bytes <= b.bytes && b.p) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  size_t want = bytes < 256 ? 256 : bytes;
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e != cudaSuccess) { b.p = nullptr; return e; }
+  b.bytes = want;
+  return cudaSuccess;
+}
+
+void release(DevMem& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+Status fail(Ctx& c, cmsvd_status s, const std::string& msg) {
+  c.err = msg;
+  return s;
+}
+
+Status cuda_fail(Ctx& c, cudaError_t e, const char* where) {
+  c.err = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? CMSVD_E_NOMEM : CMSVD_E_CUDA;
+}
+
+#define CK(expr, where)                                  \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(c, _e, where); \
+  } while (0)
+
+// Workspace slots
+enum { WS_PARTIAL = 0, WS_BAD, WS_META, WS_G, WS_V, WS_EV, WS_PERM, WS_STAT, WS_PAIR, WS_OUT, WS_A, WS_B, WS_C };
+
+// ---------------------------------------------------------------------------
+// S1: register
+// ---------------------------------------------------------------------------
+Status do_register(Ctx& c, int64_t m, int32_t count, const int32_t* n, const float* const* blocks, const int64_t* ld,
+                   int where) {
+  if (!n || !blocks) return fail(c, CMSVD_E_ARG, "register: n and blocks must be non-NULL");
+  if (where != CMSVD_HOST && where != CMSVD_DEVICE) return fail(c, CMSVD_E_ARG, "register: bad `where`");
+  if (m <= 0 || count <= 0) return fail(c, CMSVD_E_SHAPE, "register: m and count must be >= 1");
+  for (int32_t i = 0; i < count; ++i) {
+    if (n[i] <= 0) return fail(c, CMSVD_E_SHAPE, "register: n[" + std::to_string(i) + "] must be >= 1");
+    if (ld && ld[i] < m) return fail(c, CMSVD_E_SHAPE, "register: ld[" + std::to_string(i) + "] < m");
+    if (!blocks[i]) return fail(c, CMSVD_E_ARG, "register: blocks[" + std::to_string(i) + "] is NULL");
+  }
+  c.spectra_r = 0;
+  c.trunc_ready = false;
+  c.m = m;
+  c.count = count;
+  c.n.assign(n, n + count);
+  c.boff.resize(count + 1);
+  int64_t off = 0, maxlen = 0;
+  c.nmax = 0;
+  for (int32_t i = 0; i < count; ++i) {
+    c.boff[i] = off;
+    off += align_up((size_t)n[i] * m, kArenaAlign);
+    maxlen = std::max<int64_t>(maxlen, (int64_t)n[i] * m);
+    c.nmax = std::max(c.nmax, n[i]);
+  }
+  c.boff[count] = off;
+  CK(ensure(c.arena, (size_t)off * 4), "register: arena");
+  const cudaMemcpyKind kind = where == CMSVD_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  float* arena = (float*)c.arena.p;
+  for (int32_t i = 0; i < count; ++i) {
+    int64_t ldi = ld ? ld[i] : m;
+    if (ldi == m) {
+      CK(cudaMemcpyAsync(arena + c.boff[i], blocks[i], (size_t)n[i] * m * 4, kind, c.stream), "register: copy");
+    } else {
+      CK(cudaMemcpy2DAsync(arena + c.boff[i], (size_t)m * 4, blocks[i], (size_t)ldi * 4, (size_t)m * 4, n[i], kind,
+                           c.stream),
+         "register: copy2d");
+    }
+  }
+  // energies
+  const int mc = energy_max_chunks(maxlen);
+  std::vector<int64_t> meta(2 * count);
+  for (int32_t i = 0; i < count; ++i) {
+    meta[i] = c.boff[i];
+    meta[count + i] = (int64_t)n[i] * m;
+  }
+  CK(ensure(c.ws[WS_META], meta.size() * 8), "register: meta");
+  CK(ensure(c.ws[WS_PARTIAL], (size_t)count * mc * 8), "register: partial");
+  CK(ensure(c.ws[WS_BAD], 16), "register: flag");
+  CK(ensure(c.d_E, (size_t)count * 8), "register: E");
+  int64_t* d_meta = (int64_t*)c.ws[WS_META].p;
+  CK(cudaMemcpyAsync(d_meta, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, c.stream), "register: meta h2d");
+  CK(cudaMemsetAsync(c.ws[WS_BAD].p, 0, 4, c.stream), "register: memset");
+  CK(launch_energy(c, d_meta, d_meta + count, maxlen, (double*)c.ws[WS_PARTIAL].p, (int*)c.ws[WS_BAD].p,
+                   (double*)c.d_E.p),
+     "register: energy kernel");
+  c.E.resize(count);
+  int bad = 0;
+  CK(cudaMemcpyAsync(c.E.data(), c.d_E.p, (size_t)count * 8, cudaMemcpyDeviceToHost, c.stream), "register: E d2h");
+  CK(cudaMemcpyAsync(&bad, c.ws[WS_BAD].p, 4, cudaMemcpyDeviceToHost, c.stream), "register: flag d2h");
+  CK(cudaStreamSynchronize(c.stream), "register: sync");
+  if (bad) {
+    c.count = 0;
+    return fail(c, CMSVD_E_NONFINITE, "register: a block contains NaN or Inf");
+  }
+  return CMSVD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// S2: block spectra (tall-thin / square blocks with n_i <= min(m, 160))
+// ---------------------------------------------------------------------------
+Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t* rank_out) {
+  if (c.count <= 0) return fail(c, CMSVD_E_STATE, "block_spectra: no collection registered");
+  if (r < 1) return fail(c, CMSVD_E_ARG, "block_spectra: r must be >= 1");
+  const int64_t m = c.m;
+  const int N = c.count;
+  for (int i = 0; i < N; ++i) {
+    if (c.n[i] > m) return fail(c, CMSVD_E_SHAPE, "block_spectra: wide blocks (n_i > m) are not supported");
+    if (c.n[i] > kJacobiMax)
+      return fail(c, CMSVD_E_SHAPE, "block_spectra: n_i > " + std::to_string(kJacobiMax) + " not supported yet");
+  }
+  const int nmax = c.nmax;
+  c.kcols.assign(c.n.begin(), c.n.end());
+  c.uoff.resize(N + 1);
+  c.foff.resize(N + 1);
+  int64_t uo = 0, fo = 0;
+  for (int i = 0; i < N; ++i) {
+    c.uoff[i] = uo;
+    uo += align_up((size_t)c.kcols[i] * m, kArenaAlign);
+    c.foff[i] = fo;
+    fo += align_up((size_t)std::min(r, c.kcols[i]) * m, kArenaAlign);
+  }
+  c.uoff[N] = uo;
+  c.foff[N] = fo;
+  CK(ensure(c.d_U, (size_t)uo * 4), "spectra: U");
+  CK(ensure(c.d_Ftrunc, (size_t)fo * 4), "spectra: Ftrunc");
+  CK(ensure(c.d_sig, (size_t)N * nmax * 8), "spectra: sig");
+  CK(ensure(c.d_sig32, (size_t)N * r * 4), "spectra: sig32");
+  CK(ensure(c.d_rank, (size_t)N * 4), "spectra: rank");
+  CK(ensure(c.d_bdesc, (size_t)(N + 1) * sizeof(BaseDesc)), "spectra: bdesc");
+  CK(ensure(c.d_adesc_raw, (size_t)(N + 1) * sizeof(AppDesc)), "spectra: adesc");
+  CK(ensure(c.d_adesc_trunc, (size_t)(N + 1) * sizeof(AppDesc)), "spectra: adesc");
+  // metadata: boff, uoff, foff (int64), kcols, n (int32)
+  std::vector<int64_t> m64(3 * N);
+  std::vector<int32_t> m32(2 * N);
+  for (int i = 0; i < N; ++i) {
+    m64[i] = c.boff[i];
+    m64[N + i] = c.uoff[i];
+    m64[2 * N + i] = c.foff[i];
+    m32[i] = c.kcols[i];
+    m32[N + i] = c.n[i];
+  }
+  CK(ensure(c.d_meta64, m64.size() * 8), "spectra: meta");
+  CK(ensure(c.d_meta32, m32.size() * 4), "spectra: meta");
+  CK(cudaMemcpyAsync(c.d_meta64.p, m64.data(), m64.size() * 8, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
+  CK(cudaMemcpyAsync(c.d_meta32.p, m32.data(), m32.size() * 4, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
+  const int64_t* d_boff = (const int64_t*)c.d_meta64.p;
+  const int64_t* d_uoff = d_boff + N;
+  const int64_t* d_foff = d_boff + 2 * N;
+  const int* d_kcols = (const int*)c.d_meta32.p;
+  const int* d_ncols = d_kcols + N;
+  // Gram A_i^T A_i in fp64 (exact products of fp32 data)
+  const int64_t gstride = (int64_t)nmax * nmax;
+  CK(ensure(c.ws[WS_G], (size_t)N * gstride * 8), "spectra: G");
+  CK(ensure(c.ws[WS_V], (size_t)N * gstride * 8), "spectra: V");
+  CK(ensure(c.ws[WS_EV], (size_t)N * nmax * 8), "spectra: ev");
+  CK(ensure(c.ws[WS_PERM], (size_t)N * nmax * 4), "spectra: perm");
+  CK(ensure(c.ws[WS_STAT], (size_t)N * 4), "spectra: stat");
+  std::vector<GemmDesc> gd(N);
+  const float* arena = (const float*)c.arena.p;
+  double* G = (double*)c.ws[WS_G].p;
+  for (int i = 0; i < N; ++i) {
+    GemmDesc g{};
+    g.A = arena + c.boff[i]; g.lda = m; g.B = arena + c.boff[i]; g.ldb = m;
+    g.C = G + (int64_t)i * gstride; g.ldc = nmax; g.M = c.kcols[i]; g.N = c.kcols[i]; g.K = (int)m; g.sym = 1;
+    gd[i] = g;
+  }
+  CK(ensure(c.ws[WS_A], gd.size() * sizeof(GemmDesc)), "spectra: gd");
+  CK(cudaMemcpyAsync(c.ws[WS_A].p, gd.data(), gd.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice, c.stream),
+     "spectra: gd h2d");
+  CK(launch_gemm_tn(c, (const GemmDesc*)c.ws[WS_A].p, N, nmax, nmax, true), "spectra: gram");
+  // eigen-decomposition A_i^T A_i = V diag(lambda) V^T (values + vectors)
+  CK(launch_syev_jacobi(c, G, nmax, gstride, d_kcols, N, nmax, (double*)c.ws[WS_V].p, gstride,
+                        (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, nmax, (int*)c.ws[WS_STAT].p),
+     "spectra: jacobi");
+  std::vector<int> stat(N);
+  CK(cudaMemcpyAsync(stat.data(), c.ws[WS_STAT].p, (size_t)N * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
+  CK(cudaStreamSynchronize(c.stream), "spectra: sync");
+  for (int i = 0; i < N; ++i)
+    if (stat[i] < 0) return fail(c, CMSVD_E_NOCONV, "block_spectra: Jacobi did not converge for block " +
+                                                        std::to_string(i) + " (" + std::to_string(c.kcols[i]) + "x" +
+                                                        std::to_string(c.kcols[i]) + " Gram)");
+  k_spec_stats<<<(N + 127) / 128, 128, 0, c.stream>>>(
+      N, nmax, r, (const double*)c.ws[WS_EV].p, d_kcols, (const double*)c.d_E.p, (double*)c.d_sig.p,
+      (float*)c.d_sig32.p, (int*)c.d_rank.p, d_uoff, (const float*)c.d_U.p, d_boff, d_ncols, arena, d_foff,
+      (const float*)c.d_Ftrunc.p, (BaseDesc*)c.d_bdesc.p, (AppDesc*)c.d_adesc_raw.p, (AppDesc*)c.d_adesc_trunc.p,
+      kTau);
+  c.launches += 1;
+  CK(cudaGetLastError(), "spectra: stats");
+  {
+    dim3 g((unsigned)((m + kThreads - 1) / kThreads), nmax, N);
+    k_leftvec<<<g, kThreads, 0, c.stream>>>(m, arena, d_boff, d_kcols, (const double*)c.ws[WS_V].p, gstride,
+                                            (const int*)c.ws[WS_PERM].p, nmax, (const double*)c.d_sig.p,
+                                            (const int*)c.d_rank.p, (float*)c.d_U.p, d_uoff);
+    c.launches += 1;
+    CK(cudaGetLastError(), "spectra: leftvec");
+    dim3 g2((unsigned)((m + kThreads - 1) / kThreads), std::min(r, nmax), N);
+    k_trunc_operand<<<g2, kThreads, 0, c.stream>>>(m, (const BaseDesc*)c.d_bdesc.p, (const AppDesc*)c.d_adesc_trunc.p,
+                                                   (float*)c.d_Ftrunc.p);
+    c.launches += 1;
+    CK(cudaGetLastError(), "spectra: trunc");
+  }
+  // host copies
+  c.sig.resize((size_t)N * nmax);
+  c.rank.resize(N);
+  CK(cudaMemcpyAsync(c.sig.data(), c.d_sig.p, (size_t)N * nmax * 8, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
+  CK(cudaMemcpyAsync(c.rank.data(), c.d_rank.p, (size_t)N * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
+  if (sigma)
+    CK(cudaMemcpyAsync(sigma, c.d_sig32.p, (size_t)N * r * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
+  CK(cudaStreamSynchronize(c.stream), "spectra: sync");
+  c.rr.resize(N);
+  for (int i = 0; i < N; ++i) c.rr[i] = std::min(r, c.rank[i]);
+  if (energy) std::memcpy(energy, c.E.data(), (size_t)N * 8);
+  if (rank_out) std::memcpy(rank_out, c.rank.data(), (size_t)N * 4);
+  c.spectra_r = r;
+  return CMSVD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// S3-S9: batched pair evaluation on device-resident pairs and outputs.
+// ---------------------------------------------------------------------------
+Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kinds, const BaseDesc* d_bd,
+                     const AppDesc* d_ad, const Dims& dims, double* d_err2, double* d_total, float* d_st,
+                     float* d_mu) {
+  if (P <= 0) return CMSVD_OK;
+  const int64_t m = c.m;
+  const bool need_mat = (kinds & (CMSVD_RESIDUAL | CMSVD_INCREMENTAL)) != 0;
+  const bool full = (kinds & CMSVD_RESIDUAL) != 0;
+  const int QMAX = std::max(1, full ? dims.qmax : dims.rrmax);
+  const int WMAX = std::max(1, dims.wmax);
+  const int GMAX = std::max(1, dims.rrmax + dims.wmax);
+  size_t per_pair = 0;
+  if (need_mat) {
+    per_pair = align_up((size_t)QMAX * WMAX * 4, 256) + align_up((size_t)m * WMAX * 4, 256) +
+               2 * align_up((size_t)WMAX * WMAX * 8, 256) + align_up((size_t)GMAX * GMAX * 8, 256) +
+               4 * sizeof(GemmDesc) + 2 * (size_t)r * 8 + 64;
+  }
+  size_t budget = c.ws_budget;
+  int64_t chunk = P;
+  if (need_mat) chunk = std::max<int64_t>(1, std::min<int64_t>(P, (int64_t)(budget / per_pair)));
+  chunk = std::min<int64_t>(chunk, 65535);
+  for (int64_t p0 = 0; p0 < P; p0 += chunk) {
+    const int64_t Pc = std::min(chunk, P - p0);
+    const int2* pr = d_pairs + p0;
+    double *evG = nullptr, *evW = nullptr, *trG = nullptr, *trW = nullptr, *zn2 = nullptr;
+    int *cntG = nullptr, *cntW = nullptr;
+    if (need_mat) {
+      // carve the workspace
+      size_t off = 0;
+      auto carve = [&](size_t bytes) { size_t o = off; off += align_up(bytes, 256); return o; };
+      size_t oZ = carve((size_t)Pc * QMAX * WMAX * 4), oR = carve((size_t)Pc * m * WMAX * 4);
+      size_t oW = carve((size_t)Pc * WMAX * WMAX * 8), oZZ = carve((size_t)Pc * WMAX * WMAX * 8);
+      size_t oG = carve((size_t)Pc * GMAX * GMAX * 8);
+      size_t oD = carve((size_t)Pc * 4 * sizeof(GemmDesc));
+      size_t onG = carve((size_t)Pc * 4), onW = carve((size_t)Pc * 4), othr = carve((size_t)Pc * 8);
+      size_t oevG = carve((size_t)Pc * r * 8), oevW = carve((size_t)Pc * r * 8);
+      size_t ocG = carve((size_t)Pc * 4), ocW = carve((size_t)Pc * 4);
+      size_t otG = carve((size_t)Pc * 8), otW = carve((size_t)Pc * 8), ozn = carve((size_t)Pc * 8);
+      CK(ensure(c.ws[WS_PAIR], off), "pairs: workspace");
+      char* base = (char*)c.ws[WS_PAIR].p;
+      float* Z = (float*)(base + oZ);
+      float* R = (float*)(base + oR);
+      double* W = (double*)(base + oW);
+      double* ZZ = (double*)(base + oZZ);
+      double* Gm = (double*)(base + oG);
+      GemmDesc* dZ = (GemmDesc*)(base + oD);
+      GemmDesc* dR = dZ + Pc;
+      GemmDesc* dW = dR + Pc;
+      GemmDesc* dZZ = dW + Pc;
+      int* nG = (int*)(base + onG);
+      int* nW = (int*)(base + onW);
+      double* thrW = (double*)(base + othr);
+      evG = (double*)(base + oevG);
+      evW = (double*)(base + oevW);
+      cntG = (int*)(base + ocG);
+      cntW = (int*)(base + ocW);
+      trG = (double*)(base + otG);
+      trW = (double*)(base + otW);
+      zn2 = (double*)(base + ozn);
+      k_make_descs<<<(unsigned)((Pc + 255) / 256), 256, 0, c.stream>>>(pr, Pc, d_bd, d_ad, m, full ? 1 : 0, QMAX,
+                                                                       WMAX, GMAX, Z, R, W, ZZ, dZ, dR, dW, dZZ, nG,
+                                                                       nW, thrW, r);
+      c.launches += 1;
+      CK(cudaGetLastError(), "pairs: descs");
+      CK(launch_gemm_tn(c, dZ, (int)Pc, QMAX, WMAX, false), "pairs: Z = Q^T F");
+      CK(launch_gemm_nn_sub(c, dR, (int)Pc, (int)m, WMAX), "pairs: R = F - Q Z");
+      CK(launch_gemm_tn(c, dW, (int)Pc, WMAX, WMAX, true), "pairs: W = R^T R");
+      CK(launch_gemm_tn(c, dZZ, (int)Pc, WMAX, WMAX, true), "pairs: Z^T Z");
+      k_build_G<<<(unsigned)Pc, kThreads, 0, c.stream>>>(pr, d_bd, d_ad, QMAX, WMAX, GMAX, Z, W, ZZ, Gm, zn2);
+      c.launches += 1;
+      CK(cudaGetLastError(), "pairs: build G");
+      if (kinds & CMSVD_INCREMENTAL)
+        CK(launch_tridiag_topk(c, Gm, GMAX, (int64_t)GMAX * GMAX, nG, (int)Pc, GMAX, nullptr, r, evG, cntG, trG),
+           "pairs: eig(G)");
+      if (kinds & CMSVD_RESIDUAL)
+        CK(launch_tridiag_topk(c, W, WMAX, (int64_t)WMAX * WMAX, nW, (int)Pc, WMAX, thrW, r, evW, cntW, trW),
+           "pairs: eig(W)");
+    }
+    k_finalize<<<(unsigned)((Pc + 127) / 128), 128, 0, c.stream>>>(
+        pr, Pc, d_bd, d_ad, r, kinds, evG, cntG, trG, evW, cntW, trW, zn2, d_err2 + 3 * p0, d_total + p0,
+        d_st ? d_st + p0 * r : nullptr, d_mu ? d_mu + p0 * r : nullptr);
+    c.launches += 1;
+    CK(cudaGetLastError(), "pairs: finalize");
+  }
+  return CMSVD_OK;
+}
+
+Dims block_dims(const Ctx& c, int operand) {
+  Dims d;
+  for (int i = 0; i < c.count; ++i) {
+    d.qmax = std::max(d.qmax, c.rank[i]);
+    d.rrmax = std::max(d.rrmax, c.rr[i]);
+    d.wmax = std::max(d.wmax, operand == CMSVD_OPERAND_TRUNC ? c.rr[i] : c.n[i]);
+  }
+  return d;
+}
+
+Status do_pair_errors(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, uint32_t kinds, int operand, int where,
+                      double* err2, double* total, float* sigma_tilde, float* mu) {
+  if (P < 0) return fail(c, CMSVD_E_ARG, "pair_errors: P < 0");
+  if (P == 0) return CMSVD_OK;
+  if (!pairs || !err2 || !total) return fail(c, CMSVD_E_ARG, "pair_errors: pairs, err2 and total are required");
+  if (c.count <= 0 || c.spectra_r <= 0) return fail(c, CMSVD_E_STATE, "pair_errors: call block_spectra first");
+  if (r != c.spectra_r) return fail(c, CMSVD_E_STATE, "pair_errors: r differs from the block_spectra r");
+  if ((kinds & ~7u) != 0 || kinds == 0) return fail(c, CMSVD_E_ARG, "pair_errors: bad kinds mask");
+  if (operand != CMSVD_OPERAND_RAW && operand != CMSVD_OPERAND_TRUNC)
+    return fail(c, CMSVD_E_ARG, "pair_errors: bad operand");
+  if (where != CMSVD_HOST && where != CMSVD_DEVICE) return fail(c, CMSVD_E_ARG, "pair_errors: bad `where`");
+  const AppDesc* d_ad = (const AppDesc*)(operand == CMSVD_OPERAND_TRUNC ? c.d_adesc_trunc.p : c.d_adesc_raw.p);
+  const Dims dims = block_dims(c, operand);
+  if (where == CMSVD_HOST) {
+    for (int64_t p = 0; p < 2 * P; ++p)
+      if (pairs[p] < 0 || pairs[p] >= c.count)
+        return fail(c, CMSVD_E_SHAPE, "pair_errors: pair index out of range at entry " + std::to_string(p));
+    size_t off = 0;
+    size_t oP = off; off += align_up((size_t)P * 8, 256);
+    size_t oE = off; off += align_up((size_t)P * 24, 256);
+    size_t oT = off; off += align_up((size_t)P * 8, 256);
+    size_t oS = off; off += sigma_tilde ? align_up((size_t)P * r * 4, 256) : 0;
+    size_t oM = off; off += mu ? align_up((size_t)P * r * 4, 256) : 0;
+    CK(ensure(c.ws[WS_OUT], off), "pair_errors: io buffers");
+    char* b = (char*)c.ws[WS_OUT].p;
+    CK(cudaMemcpyAsync(b + oP, pairs, (size_t)P * 8, cudaMemcpyHostToDevice, c.stream), "pair_errors: h2d");
+    Status s = pair_eval_dev(c, (const int2*)(b + oP), P, r, kinds, (const BaseDesc*)c.d_bdesc.p, d_ad, dims,
+                             (double*)(b + oE), (double*)(b + oT), sigma_tilde ? (float*)(b + oS) : nullptr,
+                             mu ? (float*)(b + oM) : nullptr);
+    if (s != CMSVD_OK) return s;
+    CK(cudaMemcpyAsync(err2, b + oE, (size_t)P * 24, cudaMemcpyDeviceToHost, c.stream), "pair_errors: d2h");
+    CK(cudaMemcpyAsync(total, b + oT, (size_t)P * 8, cudaMemcpyDeviceToHost, c.stream), "pair_errors: d2h");
+    if (sigma_tilde)
+      CK(cudaMemcpyAsync(sigma_tilde, b + oS, (size_t)P * r * 4, cudaMemcpyDeviceToHost, c.stream), "pair_errors: d2h");
+    if (mu) CK(cudaMemcpyAsync(mu, b + oM, (size_t)P * r * 4, cudaMemcpyDeviceToHost, c.stream), "pair_errors: d2h");
+    CK(cudaStreamSynchronize(c.stream), "pair_errors: sync");
+    return CMSVD_OK;
+  }
+  // device-resident pairs / outputs: validate indices on device
+  CK(ensure(c.ws[WS_BAD], 16), "pair_errors: flag");
+  CK(cudaMemsetAsync(c.ws[WS_BAD].p, 0, 4, c.stream), "pair_errors: memset");
+  CK(launch_check_pairs(c, (const int2*)pairs, P, c.count, (int*)c.ws[WS_BAD].p), "pair_errors: check");
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, c.ws[WS_BAD].p, 4, cudaMemcpyDeviceToHost, c.stream), "pair_errors: flag d2h");
+  CK(cudaStreamSynchronize(c.stream), "pair_errors: sync");
+  if (bad) return fail(c, CMSVD_E_SHAPE, "pair_errors: a device pair index is out of range");
+  return pair_eval_dev(c, (const int2*)pairs, P, r, kinds, (const BaseDesc*)c.d_bdesc.p, d_ad, dims, err2, total,
+                       sigma_tilde, mu);
+}
+
+}  // namespace cmsvd

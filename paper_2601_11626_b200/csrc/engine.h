@@ -1,0 +1,33 @@
+// engine.h -- host-side entry points of the libcmsvd engine (used by abi.cu
+// and cluster.cu).
+#pragma once
+#include "common.cuh"
+
+namespace cmsvd {
+
+typedef cmsvd_status Status;
+
+constexpr int kJacobiMax = 160;  // largest block width handled by the smem Jacobi (S2)
+
+struct Dims {
+  int qmax = 0;   // projection-basis columns (full range)
+  int rrmax = 0;  // tracked top-r columns
+  int wmax = 0;   // appended-operand columns
+};
+
+Status fail(Ctx& c, cmsvd_status s, const std::string& msg);
+Status cuda_fail(Ctx& c, cudaError_t e, const char* where);
+
+Status do_register(Ctx& c, int64_t m, int32_t count, const int32_t* n, const float* const* blocks, const int64_t* ld,
+                   int where);
+Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t* rank_out);
+Status do_pair_errors(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, uint32_t kinds, int operand, int where,
+                      double* err2, double* total, float* sigma_tilde, float* mu);
+Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kinds, const BaseDesc* d_bd,
+                     const AppDesc* d_ad, const Dims& dims, double* d_err2, double* d_total, float* d_st, float* d_mu);
+Dims block_dims(const Ctx& c, int operand);
+cudaError_t launch_check_pairs(Ctx& c, const int2* d_pairs, int64_t P, int count, int* d_bad);
+Status do_cluster(Ctx& c, const cmsvd_cluster_opts* o, int32_t* assign, int32_t* order, int32_t* n_clusters,
+                  double* cluster_err2, double* cluster_total, int64_t* n_evals);
+
+}  // namespace cmsvd

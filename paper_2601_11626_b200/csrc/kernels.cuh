@@ -1,0 +1,48 @@
+// kernels.cuh -- launch wrappers of the libcmsvd kernels (host-callable).
+#pragma once
+#include "common.cuh"
+
+namespace cmsvd {
+
+// S1 energies
+cudaError_t launch_energy(Ctx& c, const int64_t* d_boff, const int64_t* d_blen, int64_t maxlen, double* d_partial,
+                          int* d_bad, double* d_E);
+int energy_max_chunks(int64_t maxlen);
+
+// SIMT batched GEMMs
+cudaError_t launch_gemm_tn(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN, bool fp64acc);
+cudaError_t launch_gemm_nn_sub(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN);
+
+// eigensolvers
+size_t syev_jacobi_smem(int nmax);
+cudaError_t launch_syev_jacobi(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns, int nprob,
+                               int nmax, double* Vws, int64_t stride_v, double* evals, int* perm, int64_t stride_out,
+                               int* status);
+size_t tridiag_smem(int nmax, int kw);
+cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
+                                int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
+                                double* trace);
+
+// pair pipeline kernels (k_pair.cu)
+__global__ void k_make_descs(const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int64_t m,
+                             int use_full_basis, int QMAX, int WMAX, int GMAX, float* Zws, float* Rws, double* Wws,
+                             double* ZZws, GemmDesc* dZ, GemmDesc* dR, GemmDesc* dW, GemmDesc* dZZ, int* nG, int* nW,
+                             double* thrW, int r);
+__global__ void k_build_G(const int2* pairs, const BaseDesc* bd, const AppDesc* ad, int QMAX, int WMAX, int GMAX,
+                          const float* Zws, const double* Wws, const double* ZZws, double* Gws, double* zn2);
+__global__ void k_finalize(const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int r, unsigned kinds,
+                           const double* evG, const int* cntG, const double* trG, const double* evW, const int* cntW,
+                           const double* trW, const double* zn2, double* err2, double* total, float* sigma_tilde,
+                           float* mu);
+__global__ void k_spec_stats(int count, int nmax, int r, const double* evals, const int* kcols, const double* E,
+                             double* sig, float* sig32, int* rank, const int64_t* uoff, const float* Ubase,
+                             const int64_t* boff, const int* ncols, const float* arena, const int64_t* foff,
+                             const float* Fbase, BaseDesc* bd, AppDesc* ad_raw, AppDesc* ad_trunc, double tau);
+__global__ void k_leftvec(int64_t m, const float* arena, const int64_t* boff, const int* kcols, const double* V,
+                          int64_t strideV, const int* perm, int nmax, const double* sig, const int* rank, float* U,
+                          const int64_t* uoff);
+cudaError_t launch_build_G1(Ctx& c, int rr, int w, const double* spec, const float* Z, int ldz, const double* ZZ,
+                            const double* WW, double* G);
+__global__ void k_trunc_operand(int64_t m, const BaseDesc* bd, const AppDesc* ad_trunc, float* Fbase);
+
+}  // namespace cmsvd
