@@ -103,8 +103,8 @@ static void hh_form_q(int64_t m, int64_t n, const double* A, int64_t lda, const 
 /* ------------------------------------------------------------------ */
 /* Cyclic one-sided (Hestenes) Jacobi on the columns of X (p x n).       */
 /* Rotate pair (a,b) iff |gamma| > tol * sqrt(alpha*beta) (A19, fp64 tol =  */
-/* max(p,8)*eps), until a */
-/* whole sweep rotates nothing.  On exit the columns of X are mutually   */
+/* max(p,8)*eps) and neither column is negligible (norm^2 <= tol^2 ||X||_F^2),*/
+/* until a whole sweep rotates nothing.  On exit the columns of X are mutually   */
 /* orthogonal: X = U diag(s), and V (n x n, may be NULL) accumulates the */
 /* rotations so that X_in V = X_out.                                     */
 /* ------------------------------------------------------------------ */
@@ -117,6 +117,13 @@ static int jacobi_onesided(int64_t p, int64_t n, double* X, int64_t ldx, double*
     for (int64_t j = 0; j < n; ++j)
       for (int64_t i = 0; i < n; ++i) V[i + j * ldv] = (i == j) ? 1.0 : 0.0;
   }
+  /* A column whose norm is below tol * ||X||_F is at the rounding level of
+     the matrix: its direction is meaningless and rotating it against the
+     others never meets the relative criterion (A19).  Such pairs are skipped. */
+  double fro2 = 0.0;
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < p; ++i) fro2 += X[i + j * ldx] * X[i + j * ldx];
+  const double negligible = tol * tol * fro2;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     int64_t rotated = 0;
     for (int64_t a = 0; a + 1 < n; ++a) {
@@ -130,6 +137,7 @@ static int jacobi_onesided(int64_t p, int64_t n, double* X, int64_t ldx, double*
           gamma += xa[i] * xb[i];
         }
         if (gamma == 0.0 || !(fabs(gamma) > tol * sqrt(alpha * beta))) continue;
+        if (alpha <= negligible || beta <= negligible) continue;
         double zeta = (beta - alpha) / (2.0 * gamma);
         double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         double c = 1.0 / sqrt(1.0 + t * t);

@@ -311,3 +311,20 @@ def test_clamp_and_single_block_weyl():
     EA, EB = np.sum(A * A), np.sum(B * B)
     assert abs(res.err2[0, 0] - min(EA, EB)) < 1e-11 * (EA + EB)
     assert np.all(res.err2[0] >= 0) and np.all(res.err2[0] <= res.total[0])
+
+
+@pytest.mark.parametrize("r", [1, 9, 18, 21])
+def test_zero_and_low_rank_blocks_vs_brute_force(r):
+    """Rank-deficient concatenations (a zero block, a rank-2 block) converge
+    and agree with LAPACK brute force on the plain definitions."""
+    R = rng(1000)
+    m, n = 34, 18
+    Z = np.zeros((m, n)); A = R.standard_normal((m, n)); L2 = R.standard_normal((m, 2)) @ R.standard_normal((2, n))
+    for X, Y in [(A, Z), (Z, A), (A, L2), (L2, A), (Z, Z)]:
+        sp, res = eval_pair([X, Y], r)
+        assert res.err2[0, 2] >= exact([X, Y], r) - 1e-10 * max(res.total[0], 1)
+        UA, sA, _ = np.linalg.svd(X, full_matrices=False)
+        rr = min(r, int(np.sum(sA > oracle.TAU * sA[0]))) if sA[0] > 0 else 0
+        st = np.linalg.svd(np.concatenate([UA[:, :rr] * sA[:rr], Y], 1), compute_uv=False)[:r]
+        st = np.pad(st, (0, r - st.size))
+        assert np.allclose(res.sigma_tilde[0], st, atol=1e-12 * max(1, st[0]))
