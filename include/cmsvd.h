@@ -178,6 +178,17 @@ cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_
  * bench's gpu_launches accounting). */
 int64_t cmsvd_launch_count(cmsvd_ctx ctx);
 
+/* Per-kernel-category timing with CUDA events recorded on the context stream
+ * around each launch group (for bench.py's live roofline).  enable != 0
+ * resets the accumulators and turns recording on; 0 turns it off. */
+cmsvd_status cmsvd_profile_enable(cmsvd_ctx ctx, int enable);
+
+/* Synchronises the context stream, then fills up to `max` categories:
+ * names[k] (static strings), ms[k] (summed event time), launches[k] (number
+ * of timed launch groups).  Any output may be NULL.  Returns the number of
+ * categories written (0 for a NULL context). */
+int32_t cmsvd_profile_read(cmsvd_ctx ctx, int32_t max, const char** names, double* ms, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

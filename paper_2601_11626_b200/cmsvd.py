@@ -25,7 +25,8 @@ ALG_MAX_NORM, ALG_RESIDUAL, ALG_APPROX = 0, 1, 2
 SORT_FROBENIUS, SORT_RESIDUAL = 0, 1
 
 EXPORTS = ["cmsvd_status_string", "cmsvd_last_error", "cmsvd_version", "cmsvd_create", "cmsvd_destroy",
-           "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_cluster", "cmsvd_launch_count"]
+           "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_cluster", "cmsvd_launch_count",
+           "cmsvd_profile_enable", "cmsvd_profile_read"]
 
 
 class CmsvdError(RuntimeError):
@@ -71,6 +72,10 @@ def load(path: str = LIB_PATH):
     L.cmsvd_cluster.argtypes = [vp, ctypes.POINTER(ClusterOpts), vp, vp, vp, vp, vp, vp]
     L.cmsvd_launch_count.restype = i64
     L.cmsvd_launch_count.argtypes = [vp]
+    L.cmsvd_profile_enable.restype = ctypes.c_int
+    L.cmsvd_profile_enable.argtypes = [vp, ctypes.c_int]
+    L.cmsvd_profile_read.restype = i32
+    L.cmsvd_profile_read.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_char_p), vp, vp]
     _lib = L
     return L
 
@@ -128,6 +133,19 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self._L.cmsvd_launch_count(self._h))
+
+    def profile(self, enable: bool = True):
+        """Reset and enable/disable per-kernel-category CUDA-event timing."""
+        self._check(self._L.cmsvd_profile_enable(self._h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """{category: (ms, launch_groups)} accumulated since profile(True)."""
+        mx = 64
+        names = (ctypes.c_char_p * mx)()
+        ms = np.zeros(mx)
+        cnt = np.zeros(mx, np.int64)
+        k = self._L.cmsvd_profile_read(self._h, mx, names, _ptr(ms), _ptr(cnt))
+        return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(k)}
 
     # -- cmsvd_register --------------------------------------------------
     def register(self, blocks, where: int | None = None):

@@ -87,6 +87,8 @@ cmsvd_status cmsvd_destroy(cmsvd_ctx ctx) {
   for (DevMem* b : bufs) release(*b);
   for (auto& b : c.ws) release(b);
   for (auto& b : c.cws) release(b);
+  prof_collect(c);
+  for (auto e : c.prof.pool) cudaEventDestroy(e);
   if (c.own_stream) cudaStreamDestroy(c.stream);
   delete ctx;
   return CMSVD_OK;
@@ -140,5 +142,27 @@ cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_
 }
 
 int64_t cmsvd_launch_count(cmsvd_ctx ctx) { return ctx ? ctx->c.launches : 0; }
+
+cmsvd_status cmsvd_profile_enable(cmsvd_ctx ctx, int enable) {
+  GUARD_CTX(ctx);
+  prof_collect(c);
+  c.prof.on = enable != 0;
+  for (int k = 0; k < PC_COUNT; ++k) { c.prof.ms[k] = 0.0; c.prof.launches[k] = 0; c.prof.work[k] = 0; }
+  return CMSVD_OK;
+}
+
+int32_t cmsvd_profile_read(cmsvd_ctx ctx, int32_t max, const char** names, double* ms, int64_t* launches) {
+  if (!ctx) return 0;
+  Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  prof_collect(c);
+  int32_t k = 0;
+  for (; k < PC_COUNT && k < max; ++k) {
+    if (names) names[k] = kProfNames[k];
+    if (ms) ms[k] = c.prof.ms[k];
+    if (launches) launches[k] = c.prof.launches[k];
+  }
+  return k;
+}
 
 }  // extern "C"

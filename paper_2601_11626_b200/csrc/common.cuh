@@ -62,8 +62,28 @@ struct DevMem {
   size_t bytes = 0;
 };
 
+// Per-kernel-category CUDA-event timing (cmsvd_profile_enable/read).
+enum ProfCat {
+  PC_ENERGY = 0, PC_SPEC_GRAM, PC_SPEC_EIG, PC_SPEC_MISC, PC_DESCS, PC_PROJ, PC_RESID, PC_GRAM_W, PC_GRAM_ZZ,
+  PC_BUILD_G, PC_EIG_G, PC_EIG_W, PC_FINALIZE, PC_CLUSTER, PC_COUNT
+};
+static const char* const kProfNames[PC_COUNT] = {
+  "energy", "spectra_gram", "spectra_eig", "spectra_misc", "pair_descs", "proj_Z", "resid_R", "gram_W",
+  "gram_ZZ", "build_G", "eig_G", "eig_W", "finalize", "cluster_misc"};
+
+struct Prof {
+  bool on = false;
+  struct Rec { int cat; cudaEvent_t a, b; int64_t work; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double ms[PC_COUNT] = {};
+  int64_t launches[PC_COUNT] = {};
+  int64_t work[PC_COUNT] = {};
+};
+
 struct Ctx {
   int device = 0;
+  Prof prof;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::string err;

@@ -33,6 +33,51 @@ void release(DevMem& b) {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+static cudaEvent_t prof_event(Ctx& c) {
+  if (!c.prof.pool.empty()) {
+    cudaEvent_t e = c.prof.pool.back();
+    c.prof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+int prof_begin(Ctx& c, int cat) {
+  if (!c.prof.on) return -1;
+  Prof::Rec r;
+  r.cat = cat;
+  r.a = prof_event(c);
+  r.b = prof_event(c);
+  r.work = 0;
+  cudaEventRecord(r.a, c.stream);
+  c.prof.recs.push_back(r);
+  return (int)c.prof.recs.size() - 1;
+}
+
+void prof_end(Ctx& c, int rec, int64_t work) {
+  if (rec < 0) return;
+  cudaEventRecord(c.prof.recs[rec].b, c.stream);
+  c.prof.recs[rec].work = work;
+}
+
+void prof_collect(Ctx& c) {
+  if (c.prof.recs.empty()) return;
+  cudaStreamSynchronize(c.stream);
+  for (auto& r : c.prof.recs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      c.prof.ms[r.cat] += ms;
+      c.prof.launches[r.cat] += 1;
+      c.prof.work[r.cat] += r.work;
+    }
+    c.prof.pool.push_back(r.a);
+    c.prof.pool.push_back(r.b);
+  }
+  c.prof.recs.clear();
+}
+
 Status fail(Ctx& c, cmsvd_status s, const std::string& msg) {
   c.err = msg;
   return s;
@@ -107,9 +152,15 @@ Status do_register(Ctx& c, int64_t m, int32_t count, const int32_t* n, const flo
   int64_t* d_meta = (int64_t*)c.ws[WS_META].p;
   CK(cudaMemcpyAsync(d_meta, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, c.stream), "register: meta h2d");
   CK(cudaMemsetAsync(c.ws[WS_BAD].p, 0, 4, c.stream), "register: memset");
-  CK(launch_energy(c, d_meta, d_meta + count, maxlen, (double*)c.ws[WS_PARTIAL].p, (int*)c.ws[WS_BAD].p,
-                   (double*)c.d_E.p),
-     "register: energy kernel");
+  {
+    int pr = prof_begin(c, PC_ENERGY);
+    CK(launch_energy(c, d_meta, d_meta + count, maxlen, (double*)c.ws[WS_PARTIAL].p, (int*)c.ws[WS_BAD].p,
+                     (double*)c.d_E.p),
+       "register: energy kernel");
+    int64_t bytes = 0;
+    for (int32_t i = 0; i < count; ++i) bytes += (int64_t)n[i] * m * 4;
+    prof_end(c, pr, bytes);
+  }
   c.E.resize(count);
   int bad = 0;
   CK(cudaMemcpyAsync(c.E.data(), c.d_E.p, (size_t)count * 8, cudaMemcpyDeviceToHost, c.stream), "register: E d2h");
@@ -194,11 +245,19 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
   CK(ensure(c.ws[WS_A], gd.size() * sizeof(GemmDesc)), "spectra: gd");
   CK(cudaMemcpyAsync(c.ws[WS_A].p, gd.data(), gd.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice, c.stream),
      "spectra: gd h2d");
-  CK(launch_gemm_tn(c, (const GemmDesc*)c.ws[WS_A].p, N, nmax, nmax, true), "spectra: gram");
+  {
+    int pr = prof_begin(c, PC_SPEC_GRAM);
+    CK(launch_gemm_tn(c, (const GemmDesc*)c.ws[WS_A].p, N, nmax, nmax, true), "spectra: gram");
+    prof_end(c, pr);
+  }
   // eigen-decomposition A_i^T A_i = V diag(lambda) V^T (values + vectors)
-  CK(launch_syev_jacobi(c, G, nmax, gstride, d_kcols, N, nmax, (double*)c.ws[WS_V].p, gstride,
-                        (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, nmax, (int*)c.ws[WS_STAT].p),
-     "spectra: jacobi");
+  {
+    int pr = prof_begin(c, PC_SPEC_EIG);
+    CK(launch_syev_jacobi(c, G, nmax, gstride, d_kcols, N, nmax, (double*)c.ws[WS_V].p, gstride,
+                          (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, nmax, (int*)c.ws[WS_STAT].p),
+       "spectra: jacobi");
+    prof_end(c, pr);
+  }
   std::vector<int> stat(N);
   CK(cudaMemcpyAsync(stat.data(), c.ws[WS_STAT].p, (size_t)N * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
   CK(cudaStreamSynchronize(c.stream), "spectra: sync");
@@ -206,6 +265,7 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
     if (stat[i] < 0) return fail(c, CMSVD_E_NOCONV, "block_spectra: Jacobi did not converge for block " +
                                                         std::to_string(i) + " (" + std::to_string(c.kcols[i]) + "x" +
                                                         std::to_string(c.kcols[i]) + " Gram)");
+  const int pr_misc = prof_begin(c, PC_SPEC_MISC);
   k_spec_stats<<<(N + 127) / 128, 128, 0, c.stream>>>(
       N, nmax, r, (const double*)c.ws[WS_EV].p, d_kcols, (const double*)c.d_E.p, (double*)c.d_sig.p,
       (float*)c.d_sig32.p, (int*)c.d_rank.p, d_uoff, (const float*)c.d_U.p, d_boff, d_ncols, arena, d_foff,
@@ -226,6 +286,7 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
     c.launches += 1;
     CK(cudaGetLastError(), "spectra: trunc");
   }
+  prof_end(c, pr_misc);
   // host copies
   c.sig.resize((size_t)N * nmax);
   c.rank.resize(N);
@@ -303,30 +364,50 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       trG = (double*)(base + otG);
       trW = (double*)(base + otW);
       zn2 = (double*)(base + ozn);
+      int pf = prof_begin(c, PC_DESCS);
       k_make_descs<<<(unsigned)((Pc + 255) / 256), 256, 0, c.stream>>>(pr, Pc, d_bd, d_ad, m, full ? 1 : 0, QMAX,
                                                                        WMAX, GMAX, Z, R, W, ZZ, dZ, dR, dW, dZZ, nG,
                                                                        nW, thrW, r);
       c.launches += 1;
       CK(cudaGetLastError(), "pairs: descs");
+      prof_end(c, pf);
+      pf = prof_begin(c, PC_PROJ);
       CK(launch_gemm_tn(c, dZ, (int)Pc, QMAX, WMAX, false), "pairs: Z = Q^T F");
+      prof_end(c, pf);
+      pf = prof_begin(c, PC_RESID);
       CK(launch_gemm_nn_sub(c, dR, (int)Pc, (int)m, WMAX), "pairs: R = F - Q Z");
+      prof_end(c, pf);
+      pf = prof_begin(c, PC_GRAM_W);
       CK(launch_gemm_tn(c, dW, (int)Pc, WMAX, WMAX, true), "pairs: W = R^T R");
+      prof_end(c, pf);
+      pf = prof_begin(c, PC_GRAM_ZZ);
       CK(launch_gemm_tn(c, dZZ, (int)Pc, WMAX, WMAX, true), "pairs: Z^T Z");
+      prof_end(c, pf);
+      pf = prof_begin(c, PC_BUILD_G);
       k_build_G<<<(unsigned)Pc, kThreads, 0, c.stream>>>(pr, d_bd, d_ad, QMAX, WMAX, GMAX, Z, W, ZZ, Gm, zn2);
       c.launches += 1;
       CK(cudaGetLastError(), "pairs: build G");
-      if (kinds & CMSVD_INCREMENTAL)
+      prof_end(c, pf);
+      if (kinds & CMSVD_INCREMENTAL) {
+        pf = prof_begin(c, PC_EIG_G);
         CK(launch_tridiag_topk(c, Gm, GMAX, (int64_t)GMAX * GMAX, nG, (int)Pc, GMAX, nullptr, r, evG, cntG, trG),
            "pairs: eig(G)");
-      if (kinds & CMSVD_RESIDUAL)
+        prof_end(c, pf);
+      }
+      if (kinds & CMSVD_RESIDUAL) {
+        pf = prof_begin(c, PC_EIG_W);
         CK(launch_tridiag_topk(c, W, WMAX, (int64_t)WMAX * WMAX, nW, (int)Pc, WMAX, thrW, r, evW, cntW, trW),
            "pairs: eig(W)");
+        prof_end(c, pf);
+      }
     }
+    int prf = prof_begin(c, PC_FINALIZE);
     k_finalize<<<(unsigned)((Pc + 127) / 128), 128, 0, c.stream>>>(
         pr, Pc, d_bd, d_ad, r, kinds, evG, cntG, trG, evW, cntW, trW, zn2, d_err2 + 3 * p0, d_total + p0,
         d_st ? d_st + p0 * r : nullptr, d_mu ? d_mu + p0 * r : nullptr);
     c.launches += 1;
     CK(cudaGetLastError(), "pairs: finalize");
+    prof_end(c, prf);
   }
   return CMSVD_OK;
 }

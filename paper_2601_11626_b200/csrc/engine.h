@@ -16,6 +16,11 @@ struct Dims {
 };
 
 Status fail(Ctx& c, cmsvd_status s, const std::string& msg);
+
+// profiling helpers: prof_begin returns the index of an open record (or -1)
+int prof_begin(Ctx& c, int cat);
+void prof_end(Ctx& c, int rec, int64_t work = 0);
+void prof_collect(Ctx& c);
 Status cuda_fail(Ctx& c, cudaError_t e, const char* where);
 
 Status do_register(Ctx& c, int64_t m, int32_t count, const int32_t* n, const float* const* blocks, const int64_t* ld,
