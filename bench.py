@@ -222,7 +222,10 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     import paper_2601_11626_b200 as cm
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream: the library enqueues on it and every
+    # CUDA event of the timed region is recorded on it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     col = workload(args.config, rank)
     r = col.r
     ctx = cm.Context(local, stream.cuda_stream)

@@ -316,11 +316,14 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
   const int QMAX = std::max(1, full ? dims.qmax : dims.rrmax);
   const int WMAX = std::max(1, dims.wmax);
   const int GMAX = std::max(1, dims.rrmax + dims.wmax);
+  if (need_mat && (GMAX > kEigMax || WMAX > kEigMax))
+    return fail(c, CMSVD_E_SHAPE, "pair_errors: core size r'+w = " + std::to_string(GMAX) + " exceeds " +
+                                      std::to_string(kEigMax) + " (large-core path not built yet)");
   size_t per_pair = 0;
   if (need_mat) {
     per_pair = align_up((size_t)QMAX * WMAX * 4, 256) + align_up((size_t)m * WMAX * 4, 256) +
                2 * align_up((size_t)WMAX * WMAX * 8, 256) + align_up((size_t)GMAX * GMAX * 8, 256) +
-               4 * sizeof(GemmDesc) + 2 * (size_t)r * 8 + 64;
+               4 * sizeof(GemmDesc) + 2 * (size_t)r * 8 + (size_t)(2 * GMAX + 4) * 8 + 64;
   }
   size_t budget = c.ws_budget;
   int64_t chunk = P;
@@ -343,6 +346,7 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       size_t oevG = carve((size_t)Pc * r * 8), oevW = carve((size_t)Pc * r * 8);
       size_t ocG = carve((size_t)Pc * 4), ocW = carve((size_t)Pc * 4);
       size_t otG = carve((size_t)Pc * 8), otW = carve((size_t)Pc * 8), ozn = carve((size_t)Pc * 8);
+      size_t oscr = carve(tridiag_scratch_bytes((int)Pc, GMAX));
       CK(ensure(c.ws[WS_PAIR], off), "pairs: workspace");
       char* base = (char*)c.ws[WS_PAIR].p;
       float* Z = (float*)(base + oZ);
@@ -364,6 +368,7 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       trG = (double*)(base + otG);
       trW = (double*)(base + otW);
       zn2 = (double*)(base + ozn);
+      double* scr = (double*)(base + oscr);
       int pf = prof_begin(c, PC_DESCS);
       k_make_descs<<<(unsigned)((Pc + 255) / 256), 256, 0, c.stream>>>(pr, Pc, d_bd, d_ad, m, full ? 1 : 0, QMAX,
                                                                        WMAX, GMAX, Z, R, W, ZZ, dZ, dR, dW, dZZ, nG,
@@ -390,13 +395,13 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       prof_end(c, pf);
       if (kinds & CMSVD_INCREMENTAL) {
         pf = prof_begin(c, PC_EIG_G);
-        CK(launch_tridiag_topk(c, Gm, GMAX, (int64_t)GMAX * GMAX, nG, (int)Pc, GMAX, nullptr, r, evG, cntG, trG),
+        CK(launch_tridiag_topk(c, Gm, GMAX, (int64_t)GMAX * GMAX, nG, (int)Pc, GMAX, nullptr, r, evG, cntG, trG, scr),
            "pairs: eig(G)");
         prof_end(c, pf);
       }
       if (kinds & CMSVD_RESIDUAL) {
         pf = prof_begin(c, PC_EIG_W);
-        CK(launch_tridiag_topk(c, W, WMAX, (int64_t)WMAX * WMAX, nW, (int)Pc, WMAX, thrW, r, evW, cntW, trW),
+        CK(launch_tridiag_topk(c, W, WMAX, (int64_t)WMAX * WMAX, nW, (int)Pc, WMAX, thrW, r, evW, cntW, trW, scr),
            "pairs: eig(W)");
         prof_end(c, pf);
       }

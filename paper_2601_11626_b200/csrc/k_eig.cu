@@ -14,6 +14,8 @@
 //                     R'^T R' (Thm 2: sigma(R) for the mu multiset).
 // Both are fp64: the bounds subtract captured energy from total energy, so
 // eigenvalue errors must be small relative to ||G|| * 1e-9.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -173,121 +175,321 @@ cudaError_t launch_syev_jacobi(Ctx& c, const double* G, int64_t ld_in, int64_t s
 // Outputs: ev[p*kw + l] (non-increasing; entries not computed are 0),
 // cnt[p] = number of eigenvalues > thr (capped at kw), trace[p] = sum of the
 // diagonal (fixed order).
+//
+// Tridiagonalisation: thread-per-row, matrix (full storage, column-major)
+// staged in shared memory.  Step k applies the rank-2 update of reflector k
+// and, in the same pass over the trailing matrix, accumulates the matrix-
+// vector product with reflector k+1 (which only needs the already-updated
+// column k+1): every trailing element is read and written once per step and
+// no per-column warp reduction is needed (2 block reductions per step).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2, int n,
-                                           double x, double pivmin) {
-  int cnt = 0;
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  cnt += (q < 0.0);
+// fp64 reciprocal: MUFU.RCP64H approximation + 2 Newton steps (full precision
+// for |q| >= pivmin, far cheaper than the IEEE division subroutine).
+__device__ __forceinline__ double rcp_nr(double q) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  double e = fma(-q, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-q, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double div_fast(double a, double b) { return a * rcp_nr(b); }
+__device__ __forceinline__ float div_fast(float a, float b) { return __fdividef(a, b); }
+
+template <typename T>
+__device__ __forceinline__ void sturm2(const T* __restrict__ d, const T* __restrict__ e2, int n, T x0, T x1,
+                                       T pivmin, int& c0, int& c1) {
+  T q0 = d[0] - x0, q1 = d[0] - x1;
+  if (fabs(q0) < pivmin) q0 = -pivmin;
+  if (fabs(q1) < pivmin) q1 = -pivmin;
+  int a0 = q0 < T(0), a1 = q1 < T(0);
+#pragma unroll 4
   for (int i = 1; i < n; ++i) {
-    q = (d[i] - x) - e2[i - 1] / q;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += (q < 0.0);
+    const T di = d[i], ei = e2[i - 1];
+    q0 = (di - x0) - div_fast(ei, q0);
+    q1 = (di - x1) - div_fast(ei, q1);
+    if (fabs(q0) < pivmin) q0 = -pivmin;
+    if (fabs(q1) < pivmin) q1 = -pivmin;
+    a0 += q0 < T(0);
+    a1 += q1 < T(0);
   }
-  return cnt;
+  c0 = a0;
+  c1 = a1;
 }
 
-__global__ void __launch_bounds__(kThreads) k_tridiag_topk(const double* __restrict__ Gin, int64_t ld_in,
-                                                           int64_t stride_in, const int* __restrict__ ns,
-                                                           const double* __restrict__ thr, int kw,
-                                                           double* __restrict__ ev, int* __restrict__ cnt_out,
-                                                           double* __restrict__ trace_out) {
+// ---------------------------------------------------------------------------
+// Batched Householder tridiagonalisation (values path).
+// Problem p: n = ns[p] (0 <= n <= 256), symmetric matrix at Gin + p*stride_in
+// (ld_in, full storage).  Staged in shared memory (full storage, ld = n):
+// 200 KB at n = 160, one CTA of 8 warps per SM.
+// Step k applies reflector k's rank-2 update to the trailing matrix and, in
+// the same pass, accumulates the product with reflector k+1 (which only needs
+// the already-updated column k+1): warp per column, lanes over rows, a
+// compile-time number of 32-row chunks per step (no predicated-off work
+// except the last chunk), per-warp row partials combined in fixed order.
+// Outputs per problem: d[n], e2[n-1] (squared sub-diagonal), trace, and
+// Gershgorin data gsh[4] = {lo, hi, pivmin, norm}; cnt = min(kw, #eig > thr).
+// ---------------------------------------------------------------------------
+#ifndef CMSVD_TRI_WARPS
+#define CMSVD_TRI_WARPS 8
+#endif
+constexpr int kTriWarps = CMSVD_TRI_WARPS;
+constexpr int kTriThreads = 32 * kTriWarps;
+constexpr int kTriMax = 256;  // 8 row chunks of 32 lanes
+
+__device__ __forceinline__ double block_sum8(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < kTriWarps; ++k) t += red[k];  // fixed order, every thread
+  return t;
+}
+
+// One fused pass over the trailing block B (rows/cols 0..m-1, column-major, ld):
+//   if UPD: B -= v w^T + w v^T   (v, w indexed with offset `off`)
+//   part[wid][i] = sum_{j in this warp's columns} B_new[i][j] * u[j]
+template <int NT, bool UPD>
+__device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, const double* __restrict__ u,
+                                         const double* __restrict__ vv, const double* __restrict__ ww, int off,
+                                         double* __restrict__ part, int n, double* __restrict__ dpart) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double acc[NT], vi[NT], wi[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int i = lane + 32 * t;
+    const bool ok = i < m;
+    acc[t] = 0.0;
+    vi[t] = (UPD && ok) ? vv[off + i] : 0.0;
+    wi[t] = (UPD && ok) ? ww[off + i] : 0.0;
+  }
+  // two columns per iteration (j, j + kTriWarps): all loads of both columns are issued before
+  // any store so that they overlap (the compiler cannot reorder smem loads across stores itself)
+  int j = wid;
+  for (; j + kTriWarps < m; j += 2 * kTriWarps) {
+    const int j1 = j + kTriWarps;
+    const double uj0 = u[j], uj1 = u[j1];
+    double vj0 = 0.0, wj0 = 0.0, vj1 = 0.0, wj1 = 0.0;
+    if (UPD) { vj0 = vv[off + j]; wj0 = ww[off + j]; vj1 = vv[off + j1]; wj1 = ww[off + j1]; }
+    double* __restrict__ col0 = B + j * ld;
+    double* __restrict__ col1 = B + j1 * ld;
+    double x0[NT], x1[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int i = lane + 32 * t;
+      if (t + 1 < NT || i < m) { x0[t] = col0[i]; x1[t] = col1[i]; }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int i = lane + 32 * t;
+      if (t + 1 < NT || i < m) {
+        if (UPD) {
+          x0[t] = fma(-vi[t], wj0, x0[t]); x0[t] = fma(-wi[t], vj0, x0[t]);
+          x1[t] = fma(-vi[t], wj1, x1[t]); x1[t] = fma(-wi[t], vj1, x1[t]);
+          col0[i] = x0[t];
+          col1[i] = x1[t];
+        }
+        acc[t] = fma(x0[t], uj0, acc[t]);
+        acc[t] = fma(x1[t], uj1, acc[t]);
+      }
+    }
+  }
+  if (j < m) {
+    const double uj = u[j];
+    double vj = 0.0, wj = 0.0;
+    if (UPD) { vj = vv[off + j]; wj = ww[off + j]; }
+    double* __restrict__ col = B + j * ld;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int i = lane + 32 * t;
+      if (t + 1 < NT || i < m) {
+        double x = col[i];
+        if (UPD) {
+          x = fma(-vi[t], wj, x);
+          x = fma(-wi[t], vj, x);
+          col[i] = x;
+        }
+        acc[t] = fma(x, uj, acc[t]);
+      }
+    }
+  }
+  double dw = 0.0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int i = lane + 32 * t;
+    if (t + 1 < NT || i < m) {
+      part[wid * n + i] = acc[t];
+      dw = fma(acc[t], u[i], dw);
+    }
+  }
+  dw = warp_sum(dw);
+  if (lane == 0) dpart[wid] = dw;
+}
+
+template <bool UPD>
+__device__ __forceinline__ void tri_pass_dispatch(double* B, int ld, int m, const double* u, const double* vv,
+                                                  const double* ww, int off, double* part, int n, double* dpart) {
+  switch ((m + 31) >> 5) {
+    case 0: break;
+    case 1: tri_pass<1, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 2: tri_pass<2, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 3: tri_pass<3, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 4: tri_pass<4, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 5: tri_pass<5, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 6: tri_pass<6, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 7: tri_pass<7, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    default: tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+  }
+}
+
+__global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __restrict__ Gin, int64_t ld_in,
+                                                            int64_t stride_in, const int* __restrict__ ns,
+                                                            const double* __restrict__ thr, int kw, int nstride,
+                                                            double* __restrict__ dout, double* __restrict__ e2out,
+                                                            double* __restrict__ gsh, int* __restrict__ cnt_out,
+                                                            double* __restrict__ trace_out) {
   extern __shared__ double sm[];
   const int p = blockIdx.x;
   const int n = ns[p];
-  const int ld = n | 1;
-  double* A = sm;                         // n x ld
-  double* v = A + (int64_t)n * ld;        // n
-  double* pw = v + n;                     // n
-  double* d = pw + n;                     // n
-  double* e2 = d + n;                     // n
-  double* lo = e2 + n;                    // kw
-  double* hi = lo + kw;                   // kw
-  int* cnts = reinterpret_cast<int*>(hi + kw);  // blockDim.x
-  __shared__ double red[kThreads / 32];
-  __shared__ double s_tau, s_K;
-  __shared__ int s_k, s_done;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ld = n;
+  double* __restrict__ A = sm;                          // n x n, column-major
+  double* vA = A + n * ld;                              // reflector buffers (ping-pong)
+  double* vB = vA + n;
+  double* __restrict__ w = vB + n;
+  double* __restrict__ pp = w + n;                      // tau * A v of the current reflector
+  double* __restrict__ e2 = pp + n;
+  double* __restrict__ part = e2 + n;                   // kTriWarps x n row-partials
+  double* __restrict__ d = part;                        // aliases part at the end
+  __shared__ double red[2][kTriWarps];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double* Gp = Gin + (int64_t)p * stride_in;
+  double* dO = dout + (int64_t)p * nstride;
+  double* eO = e2out + (int64_t)p * nstride;
   if (n <= 0) {
-    if (threadIdx.x == 0) { cnt_out[p] = 0; trace_out[p] = 0.0; }
-    for (int l = threadIdx.x; l < kw; l += blockDim.x) ev[(int64_t)p * kw + l] = 0.0;
+    if (tid == 0) { cnt_out[p] = 0; trace_out[p] = 0.0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; }
     return;
   }
-  for (int j = wid; j < n; j += nw)
-    for (int i = lane; i < n; i += 32) A[(int64_t)j * ld + i] = Gp[(int64_t)j * ld_in + i];
+  for (int j = wid; j < n; j += kTriWarps) {
+    const double* src = Gp + (int64_t)j * ld_in;
+    double* dst = A + j * ld;
+    for (int i = lane; i < n; i += 32) dst[i] = src[i];
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {  // fixed-order trace (deterministic)
+  if (tid == 0) {
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s += A[(int64_t)i * ld + i];
+    for (int i = 0; i < n; ++i) s += A[i * ld + i];
     trace_out[p] = s;
   }
-  // ---- tridiagonalisation ----
-  for (int k = 0; k + 2 < n; ++k) {
-    const int s = n - 1 - k;
-    const double* x = A + (int64_t)k * ld + (k + 1);   // column k, rows k+1..n-1
-    if (wid == 0) {
-      double t = 0.0;
-      for (int i = 1 + lane; i < s; i += 32) t += x[i] * x[i];
-      t = warp_sum(t);
-      double alpha = x[0];
-      if (lane == 0) {
-        if (t == 0.0) {
-          s_tau = 0.0;
-          e2[k] = alpha * alpha;
-        } else {
-          double xn = sqrt(alpha * alpha + t);
-          double beta = alpha >= 0.0 ? -xn : xn;
-          s_tau = (beta - alpha) / beta;
-          s_K = 1.0 / (alpha - beta);   // temporary: scale for v
-          e2[k] = beta * beta;
+  // Per step (3 barriers): [all warps] fused update + product pass, each warp
+  // also reduces its partial dot p.v2 -> | [all threads, redundantly] K from the
+  // 8 partial dots; per row p, w and the update of column k+1; per-warp partial
+  // norms of the next column -> | [all threads, redundantly] next reflector
+  // scalars from the 8 partial norms; per row v2 -> next pass.  No block-wide
+  // serial reduction chain.
+  __shared__ double s_dot[kTriWarps], s_nrm[kTriWarps];
+  auto rsqrt_nr = [](double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = 0.5 * x * y;
+    double r = fma(-h, y, 0.5);
+    y = fma(y, r, y);
+    h = 0.5 * x * y;
+    r = fma(-h, y, 0.5);
+    return fma(y, r, y);
+  };
+  // next reflector from column kk (rows kk+1..), given the partial norms of rows kk+2.. in s_nrm
+  auto reflector = [&](int kk, double* vec) -> double {
+    const int s = n - 1 - kk;
+    const double* x = A + kk * ld + (kk + 1);
+    double sig2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kTriWarps; ++q) sig2 += s_nrm[q];
+    const double alpha = x[0];
+    double tau, scale, ee;
+    if (sig2 == 0.0) {
+      tau = 0.0; scale = 0.0; ee = alpha * alpha;
+    } else {
+      const double x2 = fma(alpha, alpha, sig2);
+      const double xn = x2 * rsqrt_nr(x2);
+      const double beta = alpha >= 0.0 ? -xn : xn;
+      tau = (beta - alpha) * rcp_nr(beta);
+      scale = rcp_nr(alpha - beta);
+      ee = beta * beta;
+    }
+    if (tid == 0) e2[kk] = ee;
+    for (int i = tid; i < s; i += kTriThreads) vec[i] = (i == 0) ? 1.0 : x[i] * scale;
+    return tau;
+  };
+  auto partial_norm = [&](const double* x, int s) {  // sum_{i>=1} x[i]^2 over this thread's rows, warp-reduced
+    double prt = 0.0;
+    for (int i = 1 + tid; i < s; i += kTriThreads) prt = fma(x[i], x[i], prt);
+    prt = warp_sum(prt);
+    if (lane == 0) s_nrm[wid] = prt;
+  };
+  if (n >= 3) {
+    double* v = vA;
+    double* v2 = vB;
+    partial_norm(A + 1, n - 1);
+    __syncthreads();
+    double tau = reflector(0, v);
+    __syncthreads();
+    tri_pass_dispatch<false>(A + 1 * ld + 1, ld, n - 1, v, nullptr, nullptr, 0, part, n, s_dot);
+    __syncthreads();
+    for (int k = 0; k + 2 < n; ++k) {
+      const int s = n - 1 - k;  // trailing size of step k (rows/cols k+1..n-1)
+      double dsum = 0.0;
+#pragma unroll
+      for (int q = 0; q < kTriWarps; ++q) dsum += s_dot[q];
+      const double Kc = 0.5 * tau * tau * dsum;  // (tau/2) p.v with p = tau * sum(part)
+      double p0 = 0.0;
+#pragma unroll
+      for (int q = 0; q < kTriWarps; ++q) p0 += part[q * n];
+      p0 *= tau;
+      const double w0 = p0 - Kc;  // v[0] = 1
+      double* c0 = A + (k + 1) * ld + (k + 1);
+      double prt = 0.0;
+      for (int i = tid; i < s; i += kTriThreads) {
+        double pi = 0.0;
+#pragma unroll
+        for (int q = 0; q < kTriWarps; ++q) pi += part[q * n + i];
+        pi *= tau;
+        const double wi = pi - Kc * v[i];
+        w[i] = wi;
+        double ci = c0[i];
+        if (tau != 0.0) {
+          ci = fma(-v[i], w0, ci - wi);
+          c0[i] = ci;
         }
+        if (i >= 2) prt = fma(ci, ci, prt);
       }
-      __syncwarp();
+      prt = warp_sum(prt);
+      if (lane == 0) s_nrm[wid] = prt;
+      __syncthreads();
+      const double tau2 = reflector(k + 1, v2);
+      __syncthreads();
+      // fused: update trailing (local 1..s-1) and partial products with v2
+      if (tau != 0.0) tri_pass_dispatch<true>(c0 + ld + 1, ld, s - 1, v2, v, w, 1, part, n, s_dot);
+      else tri_pass_dispatch<false>(c0 + ld + 1, ld, s - 1, v2, v, w, 1, part, n, s_dot);
+      __syncthreads();
+      double* tmp = v; v = v2; v2 = tmp;
+      tau = tau2;
     }
-    __syncthreads();
-    const double tau = s_tau;
-    if (tau == 0.0) continue;
-    const double sc = s_K;
-    for (int i = threadIdx.x; i < s; i += blockDim.x) v[i] = (i == 0) ? 1.0 : x[i] * sc;
-    __syncthreads();
-    // p = tau * A_trail v
-    double* At = A + (int64_t)(k + 1) * ld + (k + 1);
-    for (int j = wid; j < s; j += nw) {
-      const double* col = At + (int64_t)j * ld;
-      double t = 0.0;
-      for (int i = lane; i < s; i += 32) t = fma(col[i], v[i], t);
-      t = warp_sum(t);
-      if (lane == 0) pw[j] = tau * t;
-    }
-    __syncthreads();
-    if (wid == 0) {
-      double t = 0.0;
-      for (int i = lane; i < s; i += 32) t = fma(pw[i], v[i], t);
-      t = warp_sum(t);
-      if (lane == 0) s_K = 0.5 * tau * t;
-      __syncwarp();
-    }
-    __syncthreads();
-    const double Kc = s_K;
-    for (int i = threadIdx.x; i < s; i += blockDim.x) pw[i] -= Kc * v[i];
-    __syncthreads();
-    for (int j = wid; j < s; j += nw) {
-      double* col = At + (int64_t)j * ld;
-      const double vj = v[j], wj = pw[j];
-      for (int i = lane; i < s; i += 32) col[i] -= v[i] * wj + pw[i] * vj;
-    }
-    __syncthreads();
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = A[(int64_t)i * ld + i];
-  if (threadIdx.x == 0 && n >= 2) {
-    double t = A[(int64_t)(n - 2) * ld + (n - 1)];
+  if (tid == 0 && n >= 2 && n < 3) {
+    const double t = A[(n - 2) * ld + (n - 1)];
     e2[n - 2] = t * t;
   }
   __syncthreads();
-  // ---- Gershgorin bounds, pivmin, count above threshold ----
-  if (threadIdx.x == 0) {
+  for (int i = tid; i < n; i += kTriThreads) {
+    const double di = A[i * ld + i];
+    d[i] = di;
+    dO[i] = di;
+    if (i + 1 < n) eO[i] = e2[i];
+  }
+  __syncthreads();
+  if (tid == 0) {
     double glo = 1e300, ghi = -1e300, emax = 0.0;
     for (int i = 0; i < n; ++i) {
       double r = 0.0;
@@ -297,86 +499,111 @@ __global__ void __launch_bounds__(kThreads) k_tridiag_topk(const double* __restr
       ghi = fmax(ghi, d[i] + r);
       if (i + 1 < n) emax = fmax(emax, e2[i]);
     }
-    double nrm = fmax(fabs(glo), fabs(ghi));
-    double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
+    const double nrm = fmax(fmax(fabs(glo), fabs(ghi)), 1e-300);
+    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax) * 4.0;
     glo -= 2.2e-16 * nrm * n + pivmin;
     ghi += 2.2e-16 * nrm * n + pivmin;
-    red[0] = glo; red[1] = ghi; red[2] = pivmin; red[3] = nrm;
+    gsh[4 * p] = glo; gsh[4 * p + 1] = ghi; gsh[4 * p + 2] = pivmin; gsh[4 * p + 3] = nrm;
     int above = n;
     if (thr) {
-      double t = thr[p];
-      if (t > glo) above = n - sturm_count(d, e2, n, t, pivmin);
+      const double t = thr[p];
       if (t >= ghi) above = 0;
-    }
-    s_k = min(kw, above);
-  }
-  __syncthreads();
-  const double glo = red[0], ghi = red[1], pivmin = red[2], nrm = red[3];
-  const int k = s_k;
-  for (int l = threadIdx.x; l < kw; l += blockDim.x) {
-    lo[l] = glo; hi[l] = ghi;
-    if (l >= k) ev[(int64_t)p * kw + l] = 0.0;
-  }
-  if (threadIdx.x == 0) cnt_out[p] = k;
-  __syncthreads();
-  if (k == 0) return;
-  // ---- multisection: T threads per eigenvalue, eigenvalues in batches ----
-  const double tol_abs = 4.0 * 2.220446049250313e-16 * nrm;
-  for (int base = 0; base < k; base += blockDim.x) {
-    const int kk = min((int)blockDim.x, k - base);
-    const int T = blockDim.x / kk;
-    const int l = base + threadIdx.x / T, sidx = threadIdx.x % T;
-    const bool active = (threadIdx.x / T) < kk;
-    for (int it = 0; it < 200; ++it) {
-      if (threadIdx.x == 0) s_done = 1;
-      __syncthreads();
-      int c = -1;
-      if (active) {
-        double a = lo[l], b = hi[l];
-        if (b - a > tol_abs + 4.0 * 2.220446049250313e-16 * fmax(fabs(a), fabs(b))) {
-          double x = a + (b - a) * (double)(sidx + 1) / (double)(T + 1);
-          c = sturm_count(d, e2, n, x, pivmin);
-          s_done = 0;
-        }
+      else if (t > glo) {
+        int c0, c1;
+        sturm2<double>(d, e2, n, t, t, pivmin, c0, c1);
+        above = n - c0;
       }
-      cnts[threadIdx.x] = c;
-      __syncthreads();
-      if (s_done) break;
-      if (active && sidx == 0 && c >= 0) {
-        // target ascending index a = n-1-l: N(x) <= a  <=>  x <= lambda_a
-        const int target = n - 1 - l;
-        const double a = lo[l], b = hi[l];
-        double na = a, nb = b;
-        const int t0 = threadIdx.x;
-        for (int s2 = 0; s2 < T; ++s2) {
-          double xs = a + (b - a) * (double)(s2 + 1) / (double)(T + 1);
-          if (cnts[t0 + s2] <= target) na = xs;
-          else { nb = xs; break; }
-        }
-        lo[l] = na; hi[l] = nb;
-      }
-      __syncthreads();
     }
+    cnt_out[p] = min(kw, above);
   }
-  __syncthreads();
-  for (int q = threadIdx.x; q < k; q += blockDim.x) ev[(int64_t)p * kw + q] = 0.5 * (lo[q] + hi[q]);
+}
+
+// ---------------------------------------------------------------------------
+// Plain bisection, one thread per wanted eigenvalue (high occupancy; the
+// tridiagonals are read through L1).  fp32 coarse phase on the normalised
+// matrix to ~4e-7 ||T||, widened by 1e-5 ||T||, then fp64 to 1e-13 ||T||.
+// ev[p*kw + l] = l-th largest eigenvalue for l < cnt[p], else 0.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, const int* __restrict__ ns,
+                                                const double* __restrict__ dd, const double* __restrict__ ee2,
+                                                const double* __restrict__ gsh, const int* __restrict__ cnt,
+                                                double* __restrict__ ev) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int64_t)P * kw) return;
+  const int p = (int)(g / kw), l = (int)(g % kw);
+  double* out = ev + (int64_t)p * kw + l;
+  if (l >= cnt[p]) { *out = 0.0; return; }
+  const int n = ns[p];
+  const double* d = dd + (int64_t)p * nstride;
+  const double* e2 = ee2 + (int64_t)p * nstride;
+  const double glo = gsh[4 * p], ghi = gsh[4 * p + 1], pivmin = gsh[4 * p + 2], nrm = gsh[4 * p + 3];
+  const int target = n - 1 - l;
+  double lo = glo, hi = ghi;
+  // fp32 phase
+  {
+    const float inv = (float)(1.0 / nrm);
+    float a = (float)(lo / nrm), b = (float)(hi / nrm);
+    for (int it = 0; it < 40 && (b - a) > 4e-7f; ++it) {
+      const float x = 0.5f * (a + b);
+      float q = (float)(__ldg(d) * inv) - x;
+      if (fabsf(q) < 1e-30f) q = -1e-30f;
+      int c = q < 0.f;
+      for (int i = 1; i < n; ++i) {
+        const float di = (float)__ldg(d + i) * inv;
+        const float ei = (float)(__ldg(e2 + i - 1)) * inv * inv;
+        q = (di - x) - __fdividef(ei, q);
+        if (fabsf(q) < 1e-30f) q = -1e-30f;
+        c += q < 0.f;
+      }
+      if (c <= target) a = x; else b = x;
+    }
+    lo = fmax(glo, (double)a * nrm - 1e-5 * nrm);
+    hi = fmin(ghi, (double)b * nrm + 1e-5 * nrm);
+  }
+  const double tol = 1e-13 * nrm;
+  for (int it = 0; it < 80 && (hi - lo) > tol + 4.4e-16 * fmax(fabs(lo), fabs(hi)); ++it) {
+    const double x = 0.5 * (lo + hi);
+    double q = __ldg(d) - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    int c = q < 0.0;
+    for (int i = 1; i < n; ++i) {
+      q = (__ldg(d + i) - x) - __ldg(e2 + i - 1) * rcp_nr(q);
+      if (fabs(q) < pivmin) q = -pivmin;
+      c += q < 0.0;
+    }
+    if (c <= target) lo = x; else hi = x;
+  }
+  *out = 0.5 * (lo + hi);
 }
 
 size_t tridiag_smem(int nmax, int kw) {
-  int ld = nmax | 1;
-  return (size_t)nmax * ld * 8 + (size_t)4 * nmax * 8 + (size_t)2 * kw * 8 + kThreads * 4 + 64;
+  (void)kw;
+  return (size_t)nmax * nmax * 8 + (size_t)(5 + kTriWarps) * nmax * 8 + 64;
 }
 
 cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
                                 int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
-                                double* trace) {
+                                double* trace, double* scratch) {
   if (nprob <= 0) return cudaSuccess;
-  size_t smem = tridiag_smem(nmax, kw);
-  cudaError_t e = cudaFuncSetAttribute(k_tridiag_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (nmax > kTriMax) return cudaErrorInvalidValue;
+  const size_t smem = tridiag_smem(nmax, kw);
+  cudaError_t e = cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_tridiag_topk<<<nprob, kThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, d_thr, kw, ev, cnt, trace);
+  const int nstride = nmax;
+  double* dd = scratch;
+  double* ee = dd + (size_t)nprob * nstride;
+  double* gsh = ee + (size_t)nprob * nstride;
+  k_tridiag<<<nprob, kTriThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, d_thr, kw, nstride, dd, ee, gsh, cnt,
+                                                  trace);
+  c.launches += 1;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t total = (int64_t)nprob * kw;
+  k_bisect<<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
   c.launches += 1;
   return cudaGetLastError();
 }
+
+size_t tridiag_scratch_bytes(int nprob, int nmax) { return ((size_t)nprob * (2 * nmax + 4)) * 8; }
 
 }  // namespace cmsvd

@@ -21,7 +21,8 @@ cudaError_t launch_syev_jacobi(Ctx& c, const double* G, int64_t ld_in, int64_t s
 size_t tridiag_smem(int nmax, int kw);
 cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
                                 int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
-                                double* trace);
+                                double* trace, double* scratch);
+size_t tridiag_scratch_bytes(int nprob, int nmax);
 
 // pair pipeline kernels (k_pair.cu)
 __global__ void k_make_descs(const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int64_t m,
