@@ -234,7 +234,7 @@ struct Driver {
     const int n = (o.algorithm == CMSVD_ALG_APPROX) ? rr + w : w;
     const int nn = std::max(n, 1);
     CK(ensure(c.cws[CW_G], (size_t)nn * nn * 8 * 3), "cluster: G");
-    CK(ensure(c.cws[CW_V], (size_t)nn * nn * 8), "cluster: V");
+    CK(ensure(c.cws[CW_V], (size_t)nn * nn * 8 * 2), "cluster: V");
     CK(ensure(c.cws[CW_EV], (size_t)nn * 8 + (size_t)nn * 8), "cluster: ev");
     CK(ensure(c.cws[CW_PERM], (size_t)nn * 4 + 64), "cluster: perm");
     CK(ensure(c.cws[CW_NS], 64), "cluster: ns");
@@ -293,8 +293,8 @@ struct Driver {
       CK(launch_gemm_tn(c, d_hd, 2, w, w, true), "cluster: commit grams");
       CK(launch_build_G1(c, rr, w, st.spec, Z, qz, ZZ, WW, G), "cluster: commit G");
     }
-    CK(launch_syev_jacobi(c, G, n, (int64_t)n * n, d_ns, 1, n, (double*)c.cws[CW_V].p, (int64_t)n * n, ev, perm, n,
-                          stat),
+    CK(launch_syev(c, G, n, (int64_t)n * n, d_ns, 1, n, (double*)c.cws[CW_V].p, (int64_t)n * n,
+                   (double*)c.cws[CW_V].p + (size_t)nn * nn, ev, perm, n, stat),
        "cluster: commit eig");
     CK(cudaMemcpyAsync(lam.data(), ev, (size_t)n * 8, cudaMemcpyDeviceToHost, c.stream), "cluster: commit d2h");
     CK(cudaMemcpyAsync(&status, stat, 4, cudaMemcpyDeviceToHost, c.stream), "cluster: commit d2h");

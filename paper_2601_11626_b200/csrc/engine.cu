@@ -183,8 +183,8 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
   const int N = c.count;
   for (int i = 0; i < N; ++i) {
     if (c.n[i] > m) return fail(c, CMSVD_E_SHAPE, "block_spectra: wide blocks (n_i > m) are not supported");
-    if (c.n[i] > kJacobiMax)
-      return fail(c, CMSVD_E_SHAPE, "block_spectra: n_i > " + std::to_string(kJacobiMax) + " not supported yet");
+    if (c.n[i] > kEigMax)
+      return fail(c, CMSVD_E_SHAPE, "block_spectra: n_i > " + std::to_string(kEigMax) + " not supported yet");
   }
   const int nmax = c.nmax;
   c.kcols.assign(c.n.begin(), c.n.end());
@@ -253,16 +253,17 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
   // eigen-decomposition A_i^T A_i = V diag(lambda) V^T (values + vectors)
   {
     int pr = prof_begin(c, PC_SPEC_EIG);
-    CK(launch_syev_jacobi(c, G, nmax, gstride, d_kcols, N, nmax, (double*)c.ws[WS_V].p, gstride,
-                          (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, nmax, (int*)c.ws[WS_STAT].p),
-       "spectra: jacobi");
+    CK(ensure(c.ws[WS_B], (size_t)N * gstride * 8), "spectra: VH");
+    CK(launch_syev(c, G, nmax, gstride, d_kcols, N, nmax, (double*)c.ws[WS_V].p, gstride, (double*)c.ws[WS_B].p,
+                   (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, nmax, (int*)c.ws[WS_STAT].p),
+       "spectra: eig");
     prof_end(c, pr);
   }
   std::vector<int> stat(N);
   CK(cudaMemcpyAsync(stat.data(), c.ws[WS_STAT].p, (size_t)N * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
   CK(cudaStreamSynchronize(c.stream), "spectra: sync");
   for (int i = 0; i < N; ++i)
-    if (stat[i] < 0) return fail(c, CMSVD_E_NOCONV, "block_spectra: Jacobi did not converge for block " +
+    if (stat[i] < 0) return fail(c, CMSVD_E_NOCONV, "block_spectra: QL did not converge for block " +
                                                         std::to_string(i) + " (" + std::to_string(c.kcols[i]) + "x" +
                                                         std::to_string(c.kcols[i]) + " Gram)");
   const int pr_misc = prof_begin(c, PC_SPEC_MISC);

@@ -7,8 +7,7 @@ namespace cmsvd {
 
 typedef cmsvd_status Status;
 
-constexpr int kJacobiMax = 160;  // largest block width handled by the smem Jacobi (S2)
-constexpr int kEigMax = 164;     // largest Gram handled by the shared-memory tridiagonalisation (n^2+13n <= 29048)
+constexpr int kEigMax = 160;     // largest Gram handled by the shared-memory eigensolvers (fits 227 KB)
 
 struct Dims {
   int qmax = 0;   // projection-basis columns (full range)

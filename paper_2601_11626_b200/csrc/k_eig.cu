@@ -21,168 +21,6 @@
 
 namespace cmsvd {
 
-// ---------------------------------------------------------------------------
-// Two-sided cyclic Jacobi with vectors.
-// G: n x n fp64 (ld_in) per problem; V: n x n fp64 workspace per problem (ld n);
-// outputs: evals[p*n + l] sorted non-increasing, perm[p*n + l] = column of V
-// holding the l-th eigenvector.  status[p] = sweeps used, or -1 on no
-// convergence.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_syev_jacobi(const double* __restrict__ Gin, int64_t ld_in,
-                                                          int64_t stride_in, const int* __restrict__ ns,
-                                                          double* __restrict__ Vws, int64_t stride_v,
-                                                          double* __restrict__ evals, int* __restrict__ perm,
-                                                          int64_t stride_out, int* __restrict__ status,
-                                                          int max_sweeps) {
-  extern __shared__ double sm[];
-  const int p = blockIdx.x;
-  const int n = ns[p];
-  const int ld = n | 1;
-  double* G = sm;                         // n x ld
-  const int ne = n + (n & 1);             // even player count (dummy = n)
-  double* rc = G + (int64_t)n * ld;       // cs per pair
-  double* rs = rc + ne / 2;               // sn per pair
-  double* ra = rs + ne / 2;               // new a
-  double* rb = ra + ne / 2;               // new b
-  int* rp = reinterpret_cast<int*>(rb + ne / 2);
-  int* rq = rp + ne / 2;
-  __shared__ int rotated;
-  __shared__ double scale_s;
-  double* V = Vws + (int64_t)p * stride_v;
-  const double* Gp = Gin + (int64_t)p * stride_in;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    int i = e % n, j = e / n;
-    G[(int64_t)j * ld + i] = Gp[(int64_t)j * ld_in + i];
-    V[(int64_t)j * n + i] = (i == j) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < n; ++i) s = fmax(s, fabs(G[(int64_t)i * ld + i]));
-    scale_s = s;
-  }
-  __syncthreads();
-  const double floor_abs = 64.0 * 2.220446049250313e-16 * scale_s;
-  int sweep = 0;
-  bool converged = (n <= 1);
-  for (; sweep < max_sweeps && !converged; ++sweep) {
-    if (threadIdx.x == 0) rotated = 0;
-    __syncthreads();
-    for (int t = 0; t < ne - 1; ++t) {
-      // pairs of this round (circle method)
-      for (int k = threadIdx.x; k < ne / 2; k += blockDim.x) {
-        int a, b;
-        if (k == 0) { a = 0; b = (t % (ne - 1)) + 1; }
-        else { a = ((k + t) % (ne - 1)) + 1; b = ((ne - 1 - k + t) % (ne - 1)) + 1; }
-        if (a > b) { int x = a; a = b; b = x; }
-        double cs = 1.0, sn = 0.0, na = 0.0, nb = 0.0;
-        int pa = -1, pb = -1;
-        if (b < n) {
-          double ga = G[(int64_t)a * ld + a], gb = G[(int64_t)b * ld + b], gc = G[(int64_t)b * ld + a];
-          double thr = fmax(1e-14 * sqrt(fabs(ga * gb)), floor_abs);
-          if (fabs(gc) > thr) {
-            double zeta = (gb - ga) / (2.0 * gc);
-            double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            cs = 1.0 / sqrt(1.0 + tt * tt);
-            sn = cs * tt;
-            na = ga - tt * gc;
-            nb = gb + tt * gc;
-            pa = a; pb = b;
-            rotated = 1;
-          }
-        }
-        rc[k] = cs; rs[k] = sn; ra[k] = na; rb[k] = nb; rp[k] = pa; rq[k] = pb;
-      }
-      __syncthreads();
-      // rows: G[a][j], G[b][j]
-      const int np = ne / 2;
-      for (int e = threadIdx.x; e < np * n; e += blockDim.x) {
-        int k = e / n, j = e % n;
-        int a = rp[k];
-        if (a < 0) continue;
-        int b = rq[k];
-        double cs = rc[k], sn = rs[k];
-        double ga = G[(int64_t)j * ld + a], gb = G[(int64_t)j * ld + b];
-        G[(int64_t)j * ld + a] = cs * ga - sn * gb;
-        G[(int64_t)j * ld + b] = sn * ga + cs * gb;
-      }
-      __syncthreads();
-      // columns: G[i][a], G[i][b] and V[:, a], V[:, b]
-      for (int e = threadIdx.x; e < np * n; e += blockDim.x) {
-        int k = e / n, i = e % n;
-        int a = rp[k];
-        if (a < 0) continue;
-        int b = rq[k];
-        double cs = rc[k], sn = rs[k];
-        double ga = G[(int64_t)a * ld + i], gb = G[(int64_t)b * ld + i];
-        G[(int64_t)a * ld + i] = cs * ga - sn * gb;
-        G[(int64_t)b * ld + i] = sn * ga + cs * gb;
-        double va = V[(int64_t)a * n + i], vb = V[(int64_t)b * n + i];
-        V[(int64_t)a * n + i] = cs * va - sn * vb;
-        V[(int64_t)b * n + i] = sn * va + cs * vb;
-      }
-      __syncthreads();
-      for (int k = threadIdx.x; k < np; k += blockDim.x) {
-        int a = rp[k];
-        if (a < 0) continue;
-        int b = rq[k];
-        G[(int64_t)a * ld + a] = ra[k];
-        G[(int64_t)b * ld + b] = rb[k];
-        G[(int64_t)b * ld + a] = 0.0;
-        G[(int64_t)a * ld + b] = 0.0;
-      }
-      __syncthreads();
-    }
-    converged = (rotated == 0);
-    __syncthreads();
-  }
-  // sort eigenvalues non-increasing (ties: smaller index first)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double li = G[(int64_t)i * ld + i];
-    int rank = 0;
-    for (int j = 0; j < n; ++j) {
-      double lj = G[(int64_t)j * ld + j];
-      rank += (lj > li) || (lj == li && j < i);
-    }
-    evals[(int64_t)p * stride_out + rank] = li;
-    perm[(int64_t)p * stride_out + rank] = i;
-  }
-  if (threadIdx.x == 0) status[p] = converged ? sweep : -1;
-}
-
-size_t syev_jacobi_smem(int nmax) {
-  int ld = nmax | 1;
-  int ne = nmax + (nmax & 1);
-  return (size_t)nmax * ld * 8 + (size_t)(ne / 2) * (4 * 8 + 2 * 4) + 64;
-}
-
-cudaError_t launch_syev_jacobi(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns, int nprob,
-                               int nmax, double* Vws, int64_t stride_v, double* evals, int* perm, int64_t stride_out,
-                               int* status) {
-  size_t smem = syev_jacobi_smem(nmax);
-  cudaError_t e = cudaFuncSetAttribute(k_syev_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_syev_jacobi<<<nprob, kThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, Vws, stride_v, evals, perm,
-                                                      stride_out, status, 60);
-  c.launches += 1;
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// Householder tridiagonalisation + Sturm multisection, values only.
-// Problem p: n = ns[p] (0 allowed), matrix at Gin + p*stride_in (ld_in),
-// wants the kw largest eigenvalues that are > thr[p] (thr may be NULL: all).
-// Outputs: ev[p*kw + l] (non-increasing; entries not computed are 0),
-// cnt[p] = number of eigenvalues > thr (capped at kw), trace[p] = sum of the
-// diagonal (fixed order).
-//
-// Tridiagonalisation: thread-per-row, matrix (full storage, column-major)
-// staged in shared memory.  Step k applies the rank-2 update of reflector k
-// and, in the same pass over the trailing matrix, accumulates the matrix-
-// vector product with reflector k+1 (which only needs the already-updated
-// column k+1): every trailing element is read and written once per step and
-// no per-column warp reduction is needed (2 block reductions per step).
-// ---------------------------------------------------------------------------
 // fp64 reciprocal: MUFU.RCP64H approximation + 2 Newton steps (full precision
 // for |q| >= pivmin, far cheaper than the IEEE division subroutine).
 __device__ __forceinline__ double rcp_nr(double q) {
@@ -344,51 +182,23 @@ __device__ __forceinline__ void tri_pass_dispatch(double* B, int ld, int m, cons
   }
 }
 
-__global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __restrict__ Gin, int64_t ld_in,
-                                                            int64_t stride_in, const int* __restrict__ ns,
-                                                            const double* __restrict__ thr, int kw, int nstride,
-                                                            double* __restrict__ dout, double* __restrict__ e2out,
-                                                            double* __restrict__ gsh, int* __restrict__ cnt_out,
-                                                            double* __restrict__ trace_out) {
-  extern __shared__ double sm[];
-  const int p = blockIdx.x;
-  const int n = ns[p];
-  const int ld = n;
-  double* __restrict__ A = sm;                          // n x n, column-major
-  double* vA = A + n * ld;                              // reflector buffers (ping-pong)
-  double* vB = vA + n;
-  double* __restrict__ w = vB + n;
-  double* __restrict__ pp = w + n;                      // tau * A v of the current reflector
-  double* __restrict__ e2 = pp + n;
-  double* __restrict__ part = e2 + n;                   // kTriWarps x n row-partials
-  double* __restrict__ d = part;                        // aliases part at the end
-  __shared__ double red[2][kTriWarps];
+// Householder reduction of the n x n symmetric matrix A (shared memory, full
+// storage, ld) to tridiagonal form; e2[k] = squared sub-diagonal.  With SAVE,
+// reflector k (v_k, 1 at local 0, rows k+1..n-1) is written to column k of VH
+// (n x n, global), tau_k to tauH[k] and the signed sub-diagonal beta_k to esg[k].
+template <bool SAVE>
+__device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld, double* vA, double* vB,
+                                           double* __restrict__ w, double* __restrict__ part,
+                                           double* __restrict__ e2, double* __restrict__ esg,
+                                           double* __restrict__ VH, double* __restrict__ tauH) {
+  __shared__ double s_dot[kTriWarps], s_nrm[kTriWarps];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const double* Gp = Gin + (int64_t)p * stride_in;
-  double* dO = dout + (int64_t)p * nstride;
-  double* eO = e2out + (int64_t)p * nstride;
-  if (n <= 0) {
-    if (tid == 0) { cnt_out[p] = 0; trace_out[p] = 0.0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; }
-    return;
-  }
-  for (int j = wid; j < n; j += kTriWarps) {
-    const double* src = Gp + (int64_t)j * ld_in;
-    double* dst = A + j * ld;
-    for (int i = lane; i < n; i += 32) dst[i] = src[i];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-    for (int i = 0; i < n; ++i) s += A[i * ld + i];
-    trace_out[p] = s;
-  }
   // Per step (3 barriers): [all warps] fused update + product pass, each warp
   // also reduces its partial dot p.v2 -> | [all threads, redundantly] K from the
   // 8 partial dots; per row p, w and the update of column k+1; per-warp partial
   // norms of the next column -> | [all threads, redundantly] next reflector
   // scalars from the 8 partial norms; per row v2 -> next pass.  No block-wide
   // serial reduction chain.
-  __shared__ double s_dot[kTriWarps], s_nrm[kTriWarps];
   auto rsqrt_nr = [](double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -418,8 +228,15 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __rest
       scale = rcp_nr(alpha - beta);
       ee = beta * beta;
     }
-    if (tid == 0) e2[kk] = ee;
-    for (int i = tid; i < s; i += kTriThreads) vec[i] = (i == 0) ? 1.0 : x[i] * scale;
+    if (tid == 0) {
+      e2[kk] = ee;
+      if (SAVE) { esg[kk] = (sig2 == 0.0) ? alpha : -copysign(1.0, alpha) * sqrt(ee); tauH[kk] = tau; }
+    }
+    for (int i = tid; i < s; i += kTriThreads) {
+      const double vi = (i == 0) ? 1.0 : x[i] * scale;
+      vec[i] = vi;
+      if (SAVE) VH[(int64_t)kk * n + kk + 1 + i] = vi;
+    }
     return tau;
   };
   auto partial_norm = [&](const double* x, int s) {  // sum_{i>=1} x[i]^2 over this thread's rows, warp-reduced
@@ -477,6 +294,47 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __rest
       tau = tau2;
     }
   }
+}
+
+__global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __restrict__ Gin, int64_t ld_in,
+                                                            int64_t stride_in, const int* __restrict__ ns,
+                                                            const double* __restrict__ thr, int kw, int nstride,
+                                                            double* __restrict__ dout, double* __restrict__ e2out,
+                                                            double* __restrict__ gsh, int* __restrict__ cnt_out,
+                                                            double* __restrict__ trace_out) {
+  extern __shared__ double sm[];
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  const int ld = n;
+  double* __restrict__ A = sm;                          // n x n, column-major
+  double* vA = A + n * ld;                              // reflector buffers (ping-pong)
+  double* vB = vA + n;
+  double* __restrict__ w = vB + n;
+  double* __restrict__ pp = w + n;                      // tau * A v of the current reflector
+  double* __restrict__ e2 = pp + n;
+  double* __restrict__ part = e2 + n;                   // kTriWarps x n row-partials
+  double* __restrict__ d = part;                        // aliases part at the end
+  __shared__ double red[2][kTriWarps];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double* Gp = Gin + (int64_t)p * stride_in;
+  double* dO = dout + (int64_t)p * nstride;
+  double* eO = e2out + (int64_t)p * nstride;
+  if (n <= 0) {
+    if (tid == 0) { cnt_out[p] = 0; trace_out[p] = 0.0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; }
+    return;
+  }
+  for (int j = wid; j < n; j += kTriWarps) {
+    const double* src = Gp + (int64_t)j * ld_in;
+    double* dst = A + j * ld;
+    for (int i = lane; i < n; i += 32) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += A[i * ld + i];
+    trace_out[p] = s;
+  }
+  tri_reduce<false>(A, n, ld, vA, vB, w, part, e2, nullptr, nullptr, nullptr);
   if (tid == 0 && n >= 2 && n < 3) {
     const double t = A[(n - 2) * ld + (n - 1)];
     e2[n - 2] = t * t;
@@ -574,6 +432,192 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
     if (c <= target) lo = x; else hi = x;
   }
   *out = 0.5 * (lo + hi);
+}
+
+// ---------------------------------------------------------------------------
+// Symmetric eigen-decomposition with vectors (block spectra S2, cluster-state
+// commits S10): the tridiagonal reduction above with the reflectors saved,
+// implicit QL with Wilkinson-type shift on the tridiagonal (rotations
+// generated by one thread, applied to the rows of Z by all threads in
+// parallel), back-transformation Z <- H_0 ... H_{n-3} Z.  One CTA per problem,
+// fp64.  Outputs: evals[p*stride_out + l] non-increasing; the eigenvector of
+// evals[l] is column perm[p*stride_out + l] of V_p (n x n, ld n, at
+// Vws + p*stride_v); status[p] = QL iterations, or -1 on no convergence.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __restrict__ Gin, int64_t ld_in,
+                                                            int64_t stride_in, const int* __restrict__ ns,
+                                                            double* __restrict__ Vws, int64_t stride_v,
+                                                            double* __restrict__ VHws, double* __restrict__ evals,
+                                                            int* __restrict__ perm, int64_t stride_out,
+                                                            int* __restrict__ status, int max_iter) {
+  extern __shared__ double sm[];
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int ldz = n | 1;
+  double* __restrict__ A = sm;                         // n x n (ld n), later Z (n x ldz)
+  const int64_t asz = (int64_t)n * ldz;
+  double* vA = A + asz;
+  double* vB = vA + n;
+  double* __restrict__ w = vB + n;
+  double* __restrict__ part = w + n;                   // kTriWarps x n
+  double* __restrict__ e2 = part + (int64_t)kTriWarps * n;
+  double* __restrict__ dd = e2 + n;
+  double* __restrict__ ee = dd + n;
+  double* __restrict__ rc = ee + n;                    // rotation cosines of a sweep
+  double* __restrict__ rs = rc + n;                    // rotation sines
+  double* __restrict__ tauH = rs + n;
+  __shared__ int s_l, s_m, s_iters, s_fail;
+  double* VH = VHws + (int64_t)p * stride_v;
+  double* V = Vws + (int64_t)p * stride_v;
+  if (n <= 0) { if (tid == 0) status[p] = 0; return; }
+  for (int j = wid; j < n; j += kTriWarps) {
+    const double* src = Gin + (int64_t)p * stride_in + (int64_t)j * ld_in;
+    for (int i = lane; i < n; i += 32) A[j * n + i] = src[i];
+  }
+  __syncthreads();
+  tri_reduce<true>(A, n, n, vA, vB, w, part, e2, ee, VH, tauH);
+  __syncthreads();
+  for (int i = tid; i < n; i += kTriThreads) dd[i] = A[i * n + i];
+  if (tid == 0) {
+    if (n == 2) ee[0] = A[0 * n + 1];
+    ee[n - 1] = 0.0;
+  }
+  __syncthreads();
+  // Z = I (overwrites A, which is dead), ld = ldz
+  for (int e = tid; e < n * ldz; e += kTriThreads) A[e] = 0.0;
+  __syncthreads();
+  for (int i = tid; i < n; i += kTriThreads) A[(int64_t)i * ldz + i] = 1.0;
+  __shared__ double s_anorm;
+  if (tid == 0) {
+    s_iters = 0; s_fail = 0;
+    double an = 0.0;
+    for (int i = 0; i < n; ++i) an = fmax(an, fabs(dd[i]) + fabs(ee[i]) + (i > 0 ? fabs(ee[i - 1]) : 0.0));
+    s_anorm = an;
+  }
+  __syncthreads();
+  // ---- implicit QL (tql2) ----
+  // deflate when |e_m| <= eps (|d_m| + |d_m+1|) or |e_m| <= 8 eps ||T|| (absolute accuracy ~ eps ||T||,
+  // the same as the reduction's backward error; needed when both neighbours are ~0)
+  const double defl_abs = 8.0 * 2.220446049250313e-16 * s_anorm;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0;
+    while (true) {
+      if (tid == 0) {
+        int m = l;
+        for (; m < n - 1; ++m) {
+          const double dsum = fabs(dd[m]) + fabs(dd[m + 1]);
+          if (fabs(ee[m]) <= 2.220446049250313e-16 * dsum || fabs(ee[m]) <= defl_abs) break;
+        }
+        s_m = m;
+        if (m != l) {
+          if (iter >= max_iter) { s_fail = 1; s_m = l; }
+          else {
+            double g = (dd[l + 1] - dd[l]) / (2.0 * ee[l]);
+            double r = hypot(g, 1.0);
+            g = dd[m] - dd[l] + ee[l] / (g + copysign(r, g));
+            double sn = 1.0, cs = 1.0, pp = 0.0;
+            int i = m - 1;
+            bool underflow = false;
+            for (; i >= l; --i) {
+              double f = sn * ee[i];
+              const double b = cs * ee[i];
+              r = hypot(f, g);
+              ee[i + 1] = r;
+              if (r == 0.0) {
+                dd[i + 1] -= pp;
+                ee[m] = 0.0;
+                underflow = true;
+                break;
+              }
+              sn = f / r;
+              cs = g / r;
+              g = dd[i + 1] - pp;
+              r = (dd[i] - g) * sn + 2.0 * cs * b;
+              pp = sn * r;
+              dd[i + 1] = g + pp;
+              g = cs * r - b;
+              rc[i] = cs;
+              rs[i] = sn;
+            }
+            // rotations actually generated: indices i_stop+1 .. m-1 (i_stop = i)
+            s_l = underflow ? i + 1 : l;   // lowest rotation index applied
+            if (!underflow) {
+              dd[l] -= pp;
+              ee[l] = g;
+              ee[m] = 0.0;
+            }
+            s_iters += 1;
+          }
+        }
+      }
+      __syncthreads();
+      const int m = s_m;
+      if (m == l || s_fail) break;
+      const int lo_i = s_l;
+      // apply rotations i = m-1 .. lo_i to columns (i, i+1) of Z: each thread owns rows
+      for (int row = tid; row < n; row += kTriThreads) {
+        double* z = A + row;
+        for (int i = m - 1; i >= lo_i; --i) {
+          const double f = z[(int64_t)(i + 1) * ldz];
+          const double zi = z[(int64_t)i * ldz];
+          z[(int64_t)(i + 1) * ldz] = rs[i] * zi + rc[i] * f;
+          z[(int64_t)i * ldz] = rc[i] * zi - rs[i] * f;
+        }
+      }
+      __syncthreads();
+      ++iter;
+    }
+    if (s_fail) break;
+  }
+  __syncthreads();
+  // ---- back-transformation Z <- H_0 H_1 ... H_{n-3} Z (thread per column) ----
+  for (int k = n - 3; k >= 0; --k) {
+    const double tk = tauH[k];
+    if (tk != 0.0) {
+      const double* vk = VH + (int64_t)k * n + k + 1;  // length n-1-k, vk[0] = 1
+      for (int c = tid; c < n; c += kTriThreads) {
+        double* zc = A + (int64_t)c * ldz + k + 1;
+        double dot = 0.0;
+        for (int i = 0; i < n - 1 - k; ++i) dot = fma(vk[i], zc[i], dot);
+        dot *= tk;
+        for (int i = 0; i < n - 1 - k; ++i) zc[i] = fma(-dot, vk[i], zc[i]);
+      }
+    }
+    __syncthreads();
+  }
+  // ---- sort (non-increasing, ties by index) and write ----
+  for (int i = tid; i < n; i += kTriThreads) {
+    const double li = dd[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double lj = dd[j];
+      rank += (lj > li) || (lj == li && j < i);
+    }
+    evals[(int64_t)p * stride_out + rank] = li;
+    perm[(int64_t)p * stride_out + rank] = i;
+  }
+  for (int j = wid; j < n; j += kTriWarps)
+    for (int i = lane; i < n; i += 32) V[(int64_t)j * n + i] = A[(int64_t)j * ldz + i];
+  if (tid == 0) status[p] = s_fail ? -1 : s_iters;
+}
+
+size_t syev_smem(int nmax) {
+  return (size_t)nmax * (nmax | 1) * 8 + (size_t)(9 + kTriWarps) * nmax * 8 + 64;
+}
+
+cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns, int nprob,
+                        int nmax, double* Vws, int64_t stride_v, double* VHws, double* evals, int* perm,
+                        int64_t stride_out, int* status) {
+  if (nprob <= 0) return cudaSuccess;
+  if (nmax > kTriMax) return cudaErrorInvalidValue;
+  const size_t smem = syev_smem(nmax);
+  cudaError_t e = cudaFuncSetAttribute(k_syev_ql, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_syev_ql<<<nprob, kTriThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, Vws, stride_v, VHws, evals, perm,
+                                                     stride_out, status, 60);
+  c.launches += 1;
+  return cudaGetLastError();
 }
 
 size_t tridiag_smem(int nmax, int kw) {

@@ -14,10 +14,11 @@ cudaError_t launch_gemm_tn(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM,
 cudaError_t launch_gemm_nn_sub(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN);
 
 // eigensolvers
-size_t syev_jacobi_smem(int nmax);
-cudaError_t launch_syev_jacobi(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns, int nprob,
-                               int nmax, double* Vws, int64_t stride_v, double* evals, int* perm, int64_t stride_out,
-                               int* status);
+size_t syev_smem(int nmax);
+// eigen-decomposition with vectors; VHws: scratch of nprob x stride_v doubles (Householder vectors)
+cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns, int nprob,
+                        int nmax, double* Vws, int64_t stride_v, double* VHws, double* evals, int* perm,
+                        int64_t stride_out, int* status);
 size_t tridiag_smem(int nmax, int kw);
 cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
                                 int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
