@@ -306,9 +306,15 @@ def main():
         kernels[name] = e
     dom = max((k for k in kernels), key=lambda k: kernels[k]["ms_total"])
     d = kernels[dom]
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")   # dram bytes per launch from ncu --set full
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(args.config, {}).get(dom)
     if dom in flops:
         roof = {"bound": "alu", "kernel": dom, "achieved": d["tflops"], "peak": peaks[dom], "unit": "TFLOP/s",
-                "frac": d["frac_of_peak"], "traffic": None,
+                "frac": d["frac_of_peak"], "traffic": traffic,
+                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
+                                "(profiles/ncu_*_summary.txt)",
                 "peak_source": "own DFMA/FFMA microbenchmark (tools/peaks.cu, profiles/peaks_r01.txt); "
                                "MEASURED_PEAKS.json has no FP64/FP32-SIMT peak",
                 "algorithmic": "Householder tridiagonalisation 4/3 n^3 flops per (r'+w)^2 Gram"
