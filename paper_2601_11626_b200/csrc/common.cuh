@@ -65,11 +65,11 @@ struct DevMem {
 // Per-kernel-category CUDA-event timing (cmsvd_profile_enable/read).
 enum ProfCat {
   PC_ENERGY = 0, PC_SPEC_GRAM, PC_SPEC_EIG, PC_SPEC_MISC, PC_DESCS, PC_PROJ, PC_RESID, PC_GRAM_W, PC_GRAM_ZZ,
-  PC_BUILD_G, PC_EIG_G, PC_EIG_W, PC_FINALIZE, PC_CLUSTER, PC_COUNT
+  PC_BUILD_G, PC_EIG_G, PC_EIG_W, PC_FINALIZE, PC_CLUSTER, PC_PAIR_TC, PC_COUNT
 };
 static const char* const kProfNames[PC_COUNT] = {
   "energy", "spectra_gram", "spectra_eig", "spectra_misc", "pair_descs", "proj_Z", "resid_R", "gram_W",
-  "gram_ZZ", "build_G", "eig_G", "eig_W", "finalize", "cluster_misc"};
+  "gram_ZZ", "build_G", "eig_G", "eig_W", "finalize", "cluster_misc", "pair_tc"};
 
 struct Prof {
   bool on = false;
@@ -117,6 +117,8 @@ struct Ctx {
   DevMem ws[16];
   DevMem cws[16];  // cluster-driver state and scratch
   size_t ws_budget = (size_t)8 << 30;  // bytes of pair workspace per chunk
+  bool use_tc = true;                  // tcgen05 contraction kernel (CMSVD_NO_TC=1 selects the SIMT path)
+  bool tc_ok = true;                   // every block numerically full column rank (set by block_spectra)
 };
 
 // grow-only device buffer

@@ -297,7 +297,11 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
     CK(cudaMemcpyAsync(sigma, c.d_sig32.p, (size_t)N * r * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
   CK(cudaStreamSynchronize(c.stream), "spectra: sync");
   c.rr.resize(N);
-  for (int i = 0; i < N; ++i) c.rr[i] = std::min(r, c.rank[i]);
+  c.tc_ok = true;
+  for (int i = 0; i < N; ++i) {
+    c.rr[i] = std::min(r, c.rank[i]);
+    if (c.rank[i] < c.kcols[i]) c.tc_ok = false;
+  }
   if (energy) std::memcpy(energy, c.E.data(), (size_t)N * 8);
   if (rank_out) std::memcpy(rank_out, c.rank.data(), (size_t)N * 4);
   c.spectra_r = r;
@@ -315,6 +319,10 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
   const bool need_mat = (kinds & (CMSVD_RESIDUAL | CMSVD_INCREMENTAL)) != 0;
   const bool full = (kinds & CMSVD_RESIDUAL) != 0;
   const int QMAX = std::max(1, full ? dims.qmax : dims.rrmax);
+  // tcgen05 path (fp32 accumulation) unless the collection has numerically rank-deficient blocks: an
+  // fp32-accumulated Gram resolves exactly-zero singular values only to ~sqrt(u32)*sigma_1, the
+  // fp64-accumulated SIMT path to ~1e-8*sigma_1 ("precision dispatch")
+  const bool use_tc = c.use_tc && c.tc_ok && (full ? dims.qmax : dims.rrmax) <= 128 && dims.wmax <= 128;
   const int WMAX = std::max(1, dims.wmax);
   const int GMAX = std::max(1, dims.rrmax + dims.wmax);
   if (need_mat && (GMAX > kEigMax || WMAX > kEigMax))
@@ -322,7 +330,7 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
                                       std::to_string(kEigMax) + " (large-core path not built yet)");
   size_t per_pair = 0;
   if (need_mat) {
-    per_pair = align_up((size_t)QMAX * WMAX * 4, 256) + align_up((size_t)m * WMAX * 4, 256) +
+    per_pair = align_up((size_t)QMAX * WMAX * 4, 256) + (use_tc ? 0 : align_up((size_t)m * WMAX * 4, 256)) +
                2 * align_up((size_t)WMAX * WMAX * 8, 256) + align_up((size_t)GMAX * GMAX * 8, 256) +
                4 * sizeof(GemmDesc) + 2 * (size_t)r * 8 + (size_t)(2 * GMAX + 4) * 8 + 64;
   }
@@ -339,7 +347,7 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       // carve the workspace
       size_t off = 0;
       auto carve = [&](size_t bytes) { size_t o = off; off += align_up(bytes, 256); return o; };
-      size_t oZ = carve((size_t)Pc * QMAX * WMAX * 4), oR = carve((size_t)Pc * m * WMAX * 4);
+      size_t oZ = carve((size_t)Pc * QMAX * WMAX * 4), oR = carve(use_tc ? 256 : (size_t)Pc * m * WMAX * 4);
       size_t oW = carve((size_t)Pc * WMAX * WMAX * 8), oZZ = carve((size_t)Pc * WMAX * WMAX * 8);
       size_t oG = carve((size_t)Pc * GMAX * GMAX * 8);
       size_t oD = carve((size_t)Pc * 4 * sizeof(GemmDesc));
@@ -377,15 +385,22 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       c.launches += 1;
       CK(cudaGetLastError(), "pairs: descs");
       prof_end(c, pf);
-      pf = prof_begin(c, PC_PROJ);
-      CK(launch_gemm_tn(c, dZ, (int)Pc, QMAX, WMAX, false), "pairs: Z = Q^T F");
-      prof_end(c, pf);
-      pf = prof_begin(c, PC_RESID);
-      CK(launch_gemm_nn_sub(c, dR, (int)Pc, (int)m, WMAX), "pairs: R = F - Q Z");
-      prof_end(c, pf);
-      pf = prof_begin(c, PC_GRAM_W);
-      CK(launch_gemm_tn(c, dW, (int)Pc, WMAX, WMAX, true), "pairs: W = R^T R");
-      prof_end(c, pf);
+      if (use_tc) {
+        // fused tcgen05 3xTF32: Z = Q^T F, R' = F - Q Z (on chip), W' = R'^T R'
+        pf = prof_begin(c, PC_PAIR_TC);
+        CK(launch_pair_tc(c, pr, Pc, d_bd, d_ad, m, full ? 1 : 0, QMAX, WMAX, Z, W), "pairs: tcgen05 Z/R/W");
+        prof_end(c, pf);
+      } else {
+        pf = prof_begin(c, PC_PROJ);
+        CK(launch_gemm_tn(c, dZ, (int)Pc, QMAX, WMAX, false), "pairs: Z = Q^T F");
+        prof_end(c, pf);
+        pf = prof_begin(c, PC_RESID);
+        CK(launch_gemm_nn_sub(c, dR, (int)Pc, (int)m, WMAX), "pairs: R = F - Q Z");
+        prof_end(c, pf);
+        pf = prof_begin(c, PC_GRAM_W);
+        CK(launch_gemm_tn(c, dW, (int)Pc, WMAX, WMAX, true), "pairs: W = R^T R");
+        prof_end(c, pf);
+      }
       pf = prof_begin(c, PC_GRAM_ZZ);
       CK(launch_gemm_tn(c, dZZ, (int)Pc, WMAX, WMAX, true), "pairs: Z^T Z");
       prof_end(c, pf);

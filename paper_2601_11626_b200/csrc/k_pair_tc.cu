@@ -1,0 +1,403 @@
+// k_pair_tc.cu -- fused per-candidate tensor-core contractions (S4, S5, S6
+// Gram) on sm_100a: for the pair (base basis Q: m x q, appended F: m x w)
+//   phase 1  Z  = Q^T F                      (K = m)       -> TMEM, then global (fp32)
+//   phase 2  R' = F - Q Z   per 128-row tile (K = q)       -> TMEM -> registers (never HBM)
+//            W' += R'^T R'  per tile         (K = 128)     -> TMEM, then global (fp64)
+// i.e. Lemma 1's Y = Q_t^T A, R = A - Q_t Y and the Gram B^T B = R^T R of
+// its R-factor, and Thm 2's residual.
+// All products are 3xTF32 on tcgen05 (hi*hi + hi*lo + lo*hi, fp32
+// accumulation in TMEM, summed per 128-long K block in fp32 registers, see
+// below; the cancellation-prone product Q Z uses a 3-way split and six
+// products): fp32-equivalent accuracy, which the parity
+// tolerances need (1xTF32 measured 1.3e-2 relative error).
+//
+// One CTA (4 warps) per pair; thread 0 issues the MMAs, all threads stage the
+// operands (fp32 -> tf32 hi/lo split happens during the global -> smem copy,
+// so the split operands never exist in HBM).  Operands are K-major in the
+// no-swizzle canonical layout with padded strides LBO = 144 B, SBO = 1152 B
+// (byte(r,k) = (k/4)*144 + (r/8)*1152 + (r%8)*16 + (k%4)*4), which makes every
+// staging store pattern bank-conflict free.  Two smem stages; tcgen05.commit
+// on per-stage mbarriers releases a stage.
+// Limits of this kernel: q <= 128, w <= 128 (larger shapes use the SIMT path).
+#include "common.cuh"
+#include "kernels.cuh"
+#include "tc_common.cuh"
+
+namespace cmsvd {
+namespace {
+
+constexpr int kTcThreads = 128;
+constexpr int KT = 32;                  // k elements per stage
+constexpr uint32_t LBO = 144, SBO = 1152;
+constexpr uint32_t kTile = 128 * 144;   // bytes of a 128-row x 32-k operand tile (one of hi/lo)
+constexpr uint32_t kStage = 6 * kTile;  // A hi/mid/lo, B hi/mid/lo (phase 1 and W' use hi/lo only)
+constexpr uint32_t kSmemTc = 2 * kStage + 1024;
+
+__device__ __forceinline__ uint32_t poff(int r, int k) {
+  return (uint32_t)((k >> 2) * LBO + (r >> 3) * SBO + (r & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ void st_split4_3(uint8_t* hi, uint8_t* mi, uint8_t* lo, uint32_t off, float4 v) {
+  float4 h, m, l;
+  tc::split3_tf32(v.x, h.x, m.x, l.x);
+  tc::split3_tf32(v.y, h.y, m.y, l.y);
+  tc::split3_tf32(v.z, h.z, m.z, l.z);
+  tc::split3_tf32(v.w, h.w, m.w, l.w);
+  *reinterpret_cast<float4*>(hi + off) = h;
+  *reinterpret_cast<float4*>(mi + off) = m;
+  *reinterpret_cast<float4*>(lo + off) = l;
+}
+
+__device__ __forceinline__ void st_split4(uint8_t* hi, uint8_t* lo, uint32_t off, float4 v) {
+  float4 h, l;
+  tc::split_tf32(v.x, h.x, l.x);
+  tc::split_tf32(v.y, h.y, l.y);
+  tc::split_tf32(v.z, h.z, l.z);
+  tc::split_tf32(v.w, h.w, l.w);
+  *reinterpret_cast<float4*>(hi + off) = h;
+  *reinterpret_cast<float4*>(lo + off) = l;
+}
+
+// Stage a (rows x 32) tile whose source is contiguous along k:
+// element (r, k) = src[r*ld + k0 + k]  for r < nrows, k0 + k < kmax; else 0.
+// Lanes: 8 k-chunks x 4 rows per warp -> coalesced 128 B per row in global,
+// conflict-free 16 B stores in shared memory.
+template <bool NC>
+__device__ __forceinline__ float ldf(const float* p) { return NC ? __ldg(p) : __ldcg(p); }
+template <bool NC>
+__device__ __forceinline__ float4 ldf4(const float* p) {
+  return NC ? __ldg(reinterpret_cast<const float4*>(p)) : __ldcg(reinterpret_cast<const float4*>(p));
+}
+
+// NC = true: read-only path (inputs); false: L2 path (data written earlier in this kernel)
+template <bool NC>
+__device__ __forceinline__ void stage_kcontig(uint8_t* hi, uint8_t* lo, int rows, const float* __restrict__ src,
+                                              int64_t ld, int nrows, int64_t k0, int64_t kmax,
+                                              uint8_t* mi = nullptr) {
+  const int tid = threadIdx.x;
+  const int c = tid & 7;
+  const bool vec = ((ld & 3) == 0) && ((k0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+  const int64_t k = k0 + 4 * c;
+  constexpr int kIt = 128 / (kTcThreads / 8);   // up to 8 row groups per thread
+  float4 v[kIt];
+  // issue every global load of this thread before any shared store (memory-level parallelism)
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int r = (tid >> 3) + i * (kTcThreads / 8);
+    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < rows && r < nrows) {
+      const float* p = src + (int64_t)r * ld + k;
+      if (vec && k + 3 < kmax) {
+        v[i] = ldf4<NC>(p);
+      } else {
+        if (k + 0 < kmax) v[i].x = ldf<NC>(p + 0);
+        if (k + 1 < kmax) v[i].y = ldf<NC>(p + 1);
+        if (k + 2 < kmax) v[i].z = ldf<NC>(p + 2);
+        if (k + 3 < kmax) v[i].w = ldf<NC>(p + 3);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int r = (tid >> 3) + i * (kTcThreads / 8);
+    if (r < rows) {
+      if (mi) st_split4_3(hi, mi, lo, poff(r, 4 * c), v[i]);
+      else st_split4(hi, lo, poff(r, 4 * c), v[i]);
+    }
+  }
+}
+
+// Stage a (128 x 32) tile whose source is contiguous along rows:
+// element (r, k) = src[(k0 + k)*ld + r0 + r] for r0 + r < rmax, k0 + k < kmax; else 0.
+// Lanes over rows (coalesced per column), 4 columns gathered per 16 B store.
+__device__ __forceinline__ void stage_rcontig(uint8_t* hi, uint8_t* mi, uint8_t* lo, const float* __restrict__ src,
+                                              int64_t ld, int64_t r0, int64_t rmax, int k0, int kmax) {
+  const int r = threadIdx.x;  // 128 threads = 128 rows
+  const bool rok = (r0 + r) < rmax;
+  float4 v[KT / 4];
+#pragma unroll
+  for (int kq = 0; kq < KT / 4; ++kq) {
+    v[kq] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int k = k0 + 4 * kq;
+    if (rok) {
+      const float* p = src + (int64_t)k * ld + r0 + r;
+      if (k + 0 < kmax) v[kq].x = __ldg(p);
+      if (k + 1 < kmax) v[kq].y = __ldg(p + ld);
+      if (k + 2 < kmax) v[kq].z = __ldg(p + 2 * ld);
+      if (k + 3 < kmax) v[kq].w = __ldg(p + 3 * ld);
+    }
+  }
+#pragma unroll
+  for (int kq = 0; kq < KT / 4; ++kq) st_split4_3(hi, mi, lo, poff(r, 4 * kq), v[kq]);
+}
+
+// 6-product (3-way split) MMA sequence for one 32-k stage: hh, hm, mh, hl, mm, lh
+__device__ __forceinline__ void issue_6x(uint32_t d_tmem, uint32_t ah, uint32_t am, uint32_t al, uint32_t bh,
+                                         uint32_t bm, uint32_t bl, uint32_t idesc, bool first) {
+#pragma unroll
+  for (int s = 0; s < KT / 8; ++s) {
+    const uint32_t o = 2 * s * LBO;
+    const uint64_t dah = tc::make_desc(ah + o, LBO, SBO), dam = tc::make_desc(am + o, LBO, SBO),
+                   dal = tc::make_desc(al + o, LBO, SBO);
+    const uint64_t dbh = tc::make_desc(bh + o, LBO, SBO), dbm = tc::make_desc(bm + o, LBO, SBO),
+                   dbl = tc::make_desc(bl + o, LBO, SBO);
+    tc::mma_tf32(d_tmem, dah, dbh, idesc, (first && s == 0) ? 0u : 1u);
+    tc::mma_tf32(d_tmem, dah, dbm, idesc, 1u);
+    tc::mma_tf32(d_tmem, dam, dbh, idesc, 1u);
+    tc::mma_tf32(d_tmem, dah, dbl, idesc, 1u);
+    tc::mma_tf32(d_tmem, dam, dbm, idesc, 1u);
+    tc::mma_tf32(d_tmem, dal, dbh, idesc, 1u);
+  }
+}
+
+__device__ __forceinline__ void issue_3x(uint32_t d_tmem, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
+                                         uint32_t idesc, bool first) {
+#pragma unroll
+  for (int s = 0; s < KT / 8; ++s) {
+    const uint32_t o = 2 * s * LBO;
+    const uint64_t dah = tc::make_desc(ah + o, LBO, SBO), dal = tc::make_desc(al + o, LBO, SBO);
+    const uint64_t dbh = tc::make_desc(bh + o, LBO, SBO), dbl = tc::make_desc(bl + o, LBO, SBO);
+    tc::mma_tf32(d_tmem, dah, dbh, idesc, (first && s == 0) ? 0u : 1u);
+    tc::mma_tf32(d_tmem, dah, dbl, idesc, 1u);
+    tc::mma_tf32(d_tmem, dal, dbh, idesc, 1u);
+  }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restrict__ pairs,
+                                                           const BaseDesc* __restrict__ bd,
+                                                           const AppDesc* __restrict__ ad, int64_t m,
+                                                           int use_full_basis, int QMAX, int WMAX,
+                                                           float* __restrict__ Zws, double* __restrict__ Wws) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar_stage[2];
+  __shared__ uint64_t bar_done;
+  __shared__ uint64_t bar_slot[2];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int64_t p = blockIdx.x;
+  const int2 pr = pairs[p];
+  const BaseDesc b = bd[pr.x];
+  const AppDesc a = ad[pr.y];
+  const int q = use_full_basis ? b.q : b.rr;
+  const int w = a.w;
+  const int wp = ((w + 31) / 32) * 32;   // MMA N (multiple of 32 for the 32-column TMEM drains)
+  float* Zg = Zws + p * (int64_t)QMAX * WMAX;
+  double* Wg = Wws + p * (int64_t)WMAX * WMAX;
+  const float* Q = b.basis;
+  const float* F = a.F;
+
+  if (wid == 0) tc::tmem_alloc(&tmem_base, 512);
+  if (tid == 0) {
+    tc::mbar_init(&bar_stage[0], 1);
+    tc::mbar_init(&bar_stage[1], 1);
+    tc::mbar_init(&bar_done, 1);
+    tc::mbar_init(&bar_slot[0], 1);
+    tc::mbar_init(&bar_slot[1], 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  // TMEM columns: phase 1 Z block accumulators (two slots) at [0,128) and [128,256), running sum at
+  // [256,384); phase 2 R' tile accumulator at [0,128), W' tile contribution at [128,256), sum at [256,384).
+  const uint32_t t_z0 = tmem, t_r = tmem, t_w = tmem + 128, t_sum = tmem + 256;
+  const uint32_t lane_off = (uint32_t)(32 * wid) << 16;
+  uint32_t ph_stage[2] = {0, 0}, ph_done = 0, ph_slot[2] = {0, 0};
+  int used[2] = {0, 0};  // MMAs outstanding on a stage
+  auto stage_ptr = [&](int s, int which) { return sm + s * kStage + which * kTile; };
+  auto acquire = [&](int s) {
+    if (used[s]) { tc::mbar_wait(&bar_stage[s], ph_stage[s]); ph_stage[s] ^= 1; used[s] = 0; }
+  };
+  // The tensor core accumulates fp32 with truncation: the bias grows linearly with the number of
+  // accumulations (measured 1.3e-5 relative at K = 2048).  Accumulation chains in TMEM are therefore
+  // limited to one 128-long K block; blocks are summed in fp32 registers with round-to-nearest.
+  // running sum (fp32, round-to-nearest adds) kept in TMEM columns [256, 256+wp)
+  bool sum_empty = true;
+  auto drain_add = [&](uint32_t tcol) {
+    for (int c = 0; c < wp; c += 32) {
+      float v[32], acc[32];
+      tc::tmem_ld32(tcol + lane_off + c, v);
+      if (!sum_empty) tc::tmem_ld32(t_sum + lane_off + c, acc);
+      tc::wait_ld();
+      if (!sum_empty) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += acc[j];
+      }
+      tc::tmem_st32(t_sum + lane_off + c, v);
+    }
+    tc::wait_st();
+    sum_empty = false;
+  };
+  // write the running sum (rows 32*wid + lane, columns < ncol) to global through a callback
+  auto drain_sum = [&](auto&& store) {
+    for (int c = 0; c < wp; c += 32) {
+      float v[32];
+      if (sum_empty) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+      } else {
+        tc::tmem_ld32(t_sum + lane_off + c, v);
+        tc::wait_ld();
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) store(c + j, v[j]);
+    }
+  };
+  const uint32_t idesc_z = tc::make_idesc_tf32(128, wp);
+  constexpr int kBlk = 128 / KT;  // stages per K block
+
+  // ---------------- phase 1: Z = Q^T F (K = m) ----------------
+  if (w > 0) {
+    int it = 0;
+    const int nst = (int)((m + KT - 1) / KT);
+    for (; it < nst; ++it) {
+      const int64_t k0 = (int64_t)it * KT;
+      const int s = it & 1;
+      const int blk = it / kBlk, slot = blk & 1;
+      acquire(s);
+      stage_kcontig<true>(stage_ptr(s, 0), stage_ptr(s, 1), 128, Q, m, q, k0, m);
+      stage_kcontig<true>(stage_ptr(s, 2), stage_ptr(s, 3), wp, F, m, w, k0, m);
+      tc::fence_proxy_async();
+      tc::fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after();
+        issue_3x(t_z0 + 128 * slot, tc::smem_u32(stage_ptr(s, 0)), tc::smem_u32(stage_ptr(s, 1)),
+                 tc::smem_u32(stage_ptr(s, 2)), tc::smem_u32(stage_ptr(s, 3)), idesc_z, (it % kBlk) == 0);
+        tc::mma_commit(&bar_stage[s]);
+        if ((it % kBlk) == kBlk - 1 || it == nst - 1) tc::mma_commit(&bar_slot[slot]);
+      }
+      used[s] = 1;
+      // once block blk is issued, drain block blk-1 (its slot is reused by block blk+1)
+      if (((it % kBlk) == kBlk - 1 || it == nst - 1) && blk >= 1) {
+        const int ps = (blk - 1) & 1;
+        tc::mbar_wait(&bar_slot[ps], ph_slot[ps]);
+        ph_slot[ps] ^= 1;
+        tc::fence_after();
+        drain_add(t_z0 + 128 * ps);
+        tc::fence_before();
+      }
+    }
+    {  // last block
+      const int lb = (nst - 1) / kBlk, ls = lb & 1;
+      tc::mbar_wait(&bar_slot[ls], ph_slot[ls]);
+      ph_slot[ls] ^= 1;
+      tc::fence_after();
+      drain_add(t_z0 + 128 * ls);
+    }
+    for (int s = 0; s < 2; ++s) acquire(s);
+    const int ar = 32 * wid + lane;
+    drain_sum([&](int j, float x) {
+      if (ar < q && j < w) Zg[(int64_t)j * QMAX + ar] = x;
+    });
+  }
+  __threadfence_block();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  sum_empty = true;
+
+  // ---------------- phase 2: per 128-row tile, R' = F - Q Z, W' += R'^T R' ----------------
+  const uint32_t idesc_r = tc::make_idesc_tf32(128, wp);
+  const uint32_t idesc_w = tc::make_idesc_tf32(128, wp);
+  int it = 0;
+  for (int64_t m0 = 0; m0 < m && w > 0; m0 += 128) {
+    // R accumulator over a-chunks of 32
+    bool r_first = true;
+    for (int a0 = 0; a0 < q; a0 += KT, ++it) {
+      const int s = it & 1;
+      acquire(s);
+      // R' = F - Q Z is a cancellation (||R'|| << ||F||): its product uses the 3-way split
+      stage_rcontig(stage_ptr(s, 0), stage_ptr(s, 4), stage_ptr(s, 1), Q, m, m0, m, a0, q);
+      stage_kcontig<false>(stage_ptr(s, 2), stage_ptr(s, 3), wp, Zg, QMAX, w, a0, q, stage_ptr(s, 5));
+      tc::fence_proxy_async();
+      tc::fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after();
+        issue_6x(t_r, tc::smem_u32(stage_ptr(s, 0)), tc::smem_u32(stage_ptr(s, 4)), tc::smem_u32(stage_ptr(s, 1)),
+                 tc::smem_u32(stage_ptr(s, 2)), tc::smem_u32(stage_ptr(s, 5)), tc::smem_u32(stage_ptr(s, 3)),
+                 idesc_r, r_first);
+        tc::mma_commit(&bar_stage[s]);
+      }
+      used[s] = 1;
+      r_first = false;
+    }
+    if (tid == 0) tc::mma_commit(&bar_done);
+    tc::mbar_wait(&bar_done, ph_done);
+    ph_done ^= 1;
+    for (int s = 0; s < 2; ++s) acquire(s);
+    tc::fence_after();
+    // epilogue: rows r = 32*wid + lane of this tile -> R' into warp wid's chunk buffer
+    // chunk buffer (hi, lo) of warp wid: operand with rows = b (128), k = r_local (32)
+    uint8_t* chi = sm + (uint32_t)wid * 2 * kTile;
+    uint8_t* clo = chi + kTile;
+    const int64_t grow = m0 + 32 * wid + lane;
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      float v[32];
+      if (c0 < wp) {
+        if (q > 0) {
+          tc::tmem_ld32(t_r + lane_off + c0, v);
+          tc::wait_ld();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int bcol = c0 + j;
+        float rv = 0.f;
+        if (c0 < wp && bcol < w && grow < m) rv = __ldg(F + (int64_t)bcol * m + grow) - v[j];
+        float h, l;
+        tc::split_tf32(rv, h, l);
+        const uint32_t o = poff(bcol, lane);
+        *reinterpret_cast<float*>(chi + o) = h;
+        *reinterpret_cast<float*>(clo + o) = l;
+      }
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      for (int cw = 0; cw < 4; ++cw) {
+        const uint32_t h = tc::smem_u32(sm + cw * 2 * kTile), l = h + kTile;
+        issue_3x(t_w, h, l, h, l, idesc_w, cw == 0);
+      }
+      tc::mma_commit(&bar_done);
+    }
+    tc::mbar_wait(&bar_done, ph_done);
+    ph_done ^= 1;
+    tc::fence_after();
+    drain_add(t_w);          // this tile's W' contribution -> fp32 registers (round-to-nearest)
+    tc::fence_before();
+  }
+  // ---------------- W' (rows b = 32*wid + lane) from the running sum ----------------
+  if (w > 0) {
+    const int br = 32 * wid + lane;
+    drain_sum([&](int j, float x) {
+      if (br < w && j < w) Wg[(int64_t)j * WMAX + br] = (double)x;
+    });
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (wid == 0) tc::tmem_dealloc(tmem, 512);
+}
+
+cudaError_t launch_pair_tc(Ctx& c, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int64_t m,
+                           int use_full_basis, int QMAX, int WMAX, float* Zws, double* Wws) {
+  if (P <= 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_pair_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTc);
+  if (e != cudaSuccess) return e;
+  k_pair_tc<<<(unsigned)P, kTcThreads, kSmemTc, c.stream>>>(pairs, bd, ad, m, use_full_basis, QMAX, WMAX, Zws,
+                                                             Wws);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace cmsvd

@@ -43,6 +43,8 @@ __global__ void k_spec_stats(int count, int nmax, int r, const double* evals, co
 __global__ void k_leftvec(int64_t m, const float* arena, const int64_t* boff, const int* kcols, const double* V,
                           int64_t strideV, const int* perm, int nmax, const double* sig, const int* rank, float* U,
                           const int64_t* uoff);
+cudaError_t launch_pair_tc(Ctx& c, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int64_t m,
+                           int use_full_basis, int QMAX, int WMAX, float* Zws, double* Wws);
 cudaError_t launch_build_G1(Ctx& c, int rr, int w, const double* spec, const float* Z, int ldz, const double* ZZ,
                             const double* WW, double* G);
 __global__ void k_trunc_operand(int64_t m, const BaseDesc* bd, const AppDesc* ad_trunc, float* Fbase);
