@@ -11,7 +11,7 @@ marshals numpy arrays and holds the host-side greedy drivers
 (``oracle.cluster``).  It shares no code with the CUDA path.
 
 Every function cites the PAPER.md passage it follows; ambiguous passages use
-the SURVEY.md §8(c) readings (A1..A21), restated in DESIGN.md.
+the SURVEY.md §8(c) readings (A1..A21) and DESIGN.md's A22, restated in DESIGN.md.
 
 Parity unpinned: the TRUNC operand (A6) and the exact cluster
 compositions of greedy runs on synthetic data are bound only by invariants
@@ -31,6 +31,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 TAU = 1e-5          # numerical-rank rule (A5): keep sigma_l > TAU * sigma_1
+BIG_N = 512         # blocks with more columns take reading A22 (range = R^m, spectra from the m x m Gram)
 WEYL, RESIDUAL, INCREMENTAL = 1, 2, 4
 RAW, TRUNC = 0, 1
 
@@ -150,12 +151,37 @@ def block_spectra(blocks, tau: float = TAU) -> Spectra:
     n = np.array([a.shape[1] for a in A], dtype=np.int32)
     N = len(A)
     E = np.array([float(np.sum(a * a)) for a in A])   # fp64 sum of squares (exact products)
+    big = [int(k) > BIG_N for k in n]
+    if any(big) and not all(big):
+        raise ValueError("collections mixing blocks wider than BIG_N columns with narrower ones (A22)")
+    if all(big):
+        return _block_spectra_big(A, m, n, E)
     sig = [np.zeros(min(m, int(k))) for k in n]
     U = [np.zeros((m, min(m, int(k))), order="F") for k in n]
     st = lib().or_block_svds(m, N, _ip(n), _ptrs(A), _ptrs(sig), _ptrs(U))
     if st:
         raise RuntimeError(f"oracle block SVD failed (status {st})")
     rank = np.array([int(np.sum(s > tau * s[0])) if s[0] > 0 else 0 for s in sig], dtype=np.int32)
+    return Spectra(m, n, A, E, sig, U, rank)
+
+
+def _block_spectra_big(A, m, n, E) -> Spectra:
+    """Reading A22 for blocks wider than BIG_N columns (configs 3
+    and 4, square weight-like blocks; n_i >= m required): the spectra follow
+    A15's exact route, the m x m fp64 Gram A A^T = U diag(sigma^2) U^T
+    (library symmetric eigensolver as one step; squaring costs relative
+    accuracy (sigma_1/sigma_l)^2 * 1e-16 only), and the block's range is taken
+    as all of R^m: rank_i = min(m, n_i) and the paper-literal residual
+    R = (I - Q Q^T) F is identically 0 (oracle.c, pair_residual)."""
+    sig, U = [], []
+    for a in A:
+        if a.shape[1] < m:
+            raise ValueError("A22 blocks must have n_i >= m")
+        lam, V = np.linalg.eigh(a @ a.T)
+        lam, V = lam[::-1], V[:, ::-1]
+        sig.append(np.sqrt(np.maximum(lam, 0.0)))
+        U.append(np.asfortranarray(V))
+    rank = np.array([min(m, int(k)) for k in n], dtype=np.int32)
     return Spectra(m, n, A, E, sig, U, rank)
 
 

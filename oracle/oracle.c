@@ -326,7 +326,9 @@ static int pair_residual(const or_collection* c, int32_t i, const double* F, int
   double* R = (double*)malloc(sizeof(double) * m * w);
   memcpy(R, F, sizeof(double) * m * w);
   double* Z = (double*)malloc(sizeof(double) * (q > 0 ? q : 1) * w);
-  for (int pass = 0; pass < 2; ++pass) {
+  /* q >= m: Q spans R^m (A22 blocks), Q Q^T = I and R = 0 exactly */
+  if (q >= m) memset(R, 0, sizeof(double) * m * w);
+  for (int pass = 0; pass < 2 && q < m; ++pass) {
     for (int64_t b = 0; b < w; ++b)
       for (int64_t a = 0; a < q; ++a) {
         double t = 0.0;
@@ -340,7 +342,7 @@ static int pair_residual(const or_collection* c, int32_t i, const double* F, int
         R[k + b * m] -= t;
       }
   }
-  int64_t kr = m < w ? m : w;
+  int64_t kr = q >= m ? 0 : (m < w ? m : w);
   double* sr = (double*)malloc(sizeof(double) * (kr > 0 ? kr : 1));
   int st = OR_OK;
   if (kr > 0) st = or_svd(m, w, R, m, sr, NULL, 0, NULL, 0);

@@ -1,3 +1,4 @@
+#include <algorithm>
 // abi.cu -- the extern "C" boundary of libcmsvd (declared in include/cmsvd.h).
 // Every entry point converts C++/CUDA failures into a cmsvd_status plus a
 // per-context message; no exception crosses the ABI.
@@ -74,6 +75,7 @@ cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
   cudaDeviceGetAttribute(&h->c.sm_count, cudaDevAttrMultiProcessorCount, device);
   if (const char* env = getenv("CMSVD_WS_BYTES")) h->c.ws_budget = (size_t)atoll(env);
   if (const char* env = getenv("CMSVD_NO_TC")) h->c.use_tc = !(env[0] == '1');
+  if (const char* env = getenv("CMSVD_SUBSPACE_ITERS")) h->c.subspace_iters = std::max(0, atoi(env));
   *out = h;
   return CMSVD_OK;
 }

@@ -357,6 +357,9 @@ Status do_cluster(Ctx& c, const cmsvd_cluster_opts* o, int32_t* assign, int32_t*
     return fail(c, CMSVD_E_ARG, "cluster: bad algorithm/sort/operand");
   if (c.count <= 0 || c.spectra_r <= 0) return fail(c, CMSVD_E_STATE, "cluster: call block_spectra first");
   if (o->r != c.spectra_r) return fail(c, CMSVD_E_STATE, "cluster: r differs from the block_spectra r");
+  if (c.big && o->algorithm == CMSVD_ALG_RESIDUAL)
+    return fail(c, CMSVD_E_SHAPE, "cluster: Alg. 2 needs an explicit range basis; blocks wider than 512 columns "
+                                  "keep only U_r (A22)");
   const int N = c.count;
   const double eps2 = o->eps * o->eps;
   std::vector<int> rem(N);

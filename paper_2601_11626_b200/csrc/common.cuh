@@ -28,7 +28,8 @@ struct BaseDesc {
   int q;                // columns of the projection basis used by this evaluation
   int rr;               // size of the tracked top-r part (incremental)
   int ns;               // length of spec
-  int pad;
+  int full;             // 1: the base's range is all of R^m (A22, blocks wider than kEigMax): the
+                        //    paper-literal residual (I - QQ^T)F is identically 0
   double E;             // energy ||.||_F^2 of the base
   double tail_inc;      // E - sum_{l<rr} spec_l^2, computed as a sum of the dropped part (>= 0)
   double rest_res;      // E - sum_{all l} spec_l^2 (energy not represented in spec, >= 0)
@@ -119,6 +120,8 @@ struct Ctx {
   size_t ws_budget = (size_t)8 << 30;  // bytes of pair workspace per chunk
   bool use_tc = true;                  // tcgen05 contraction kernel (CMSVD_NO_TC=1 selects the SIMT path)
   bool tc_ok = true;                   // every block numerically full column rank (set by block_spectra)
+  bool big = false;                    // collection of blocks wider than kEigMax (A22 spectra, full-range bases)
+  int subspace_iters = 12;             // power iterations of the big-block spectra (CMSVD_SUBSPACE_ITERS)
 };
 
 // grow-only device buffer

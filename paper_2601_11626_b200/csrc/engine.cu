@@ -176,16 +176,188 @@ Status do_register(Ctx& c, int64_t m, int32_t count, const int32_t* n, const flo
 // ---------------------------------------------------------------------------
 // S2: block spectra (tall-thin / square blocks with n_i <= min(m, 160))
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// S2 for blocks wider than kEigMax columns (configs 3, 4: square weight-like
+// blocks).  Reading A22: the per-block Gram is too large for the
+// batched eigensolver, so the top-s singular triplets (s = min(m, 2r, 512))
+// come from randomized subspace iteration with fp64 accumulation and CholQR2
+// orthonormalisation, followed by a Rayleigh-Ritz step:
+//   Y = A Omega; repeat q: Z = orth(A^T orth(Y)), Y = A Z;  Q = orth(Y)
+//   Bt = A^T Q;  H = Bt^T Bt = W diag(lambda) W^T;  sigma = sqrt(lambda), U_r = Q W_r
+// The block's range is taken as R^m (n_i >= m required), so the paper-literal
+// residual R = (I - QQ^T)F vanishes and rank_i = min(m, n_i).
+// ---------------------------------------------------------------------------
+Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int32_t* rank_out) {
+  const int64_t m = c.m;
+  const int N = c.count;
+  for (int i = 0; i < N; ++i)
+    if (c.n[i] < m)
+      return fail(c, CMSVD_E_SHAPE, "block_spectra: blocks wider than " + std::to_string(kEigMax) +
+                                        " columns must have n_i >= m (A22)");
+  const int s = (int)std::min<int64_t>(std::min<int64_t>(m, 2 * (int64_t)r), kEigMax);
+  if (r > s && r < m)
+    return fail(c, CMSVD_E_SHAPE, "block_spectra: r > " + std::to_string(kEigMax) + " on blocks wider than " +
+                                      std::to_string(kEigMax) + " columns");
+  const int kc = (int)std::min<int64_t>(r, m);
+  const int nmax = c.nmax;
+  c.big = true;
+  c.kcols.assign(N, kc);
+  c.uoff.resize(N + 1);
+  c.foff.resize(N + 1);
+  int64_t uo = 0;
+  for (int i = 0; i < N; ++i) {
+    c.uoff[i] = uo;
+    uo += align_up((size_t)kc * m, kArenaAlign);
+  }
+  c.uoff[N] = uo;
+  for (int i = 0; i <= N; ++i) c.foff[i] = c.uoff[i];
+  CK(ensure(c.d_U, (size_t)uo * 4), "spectra: U");
+  CK(ensure(c.d_Ftrunc, (size_t)uo * 4), "spectra: Ftrunc");
+  CK(ensure(c.d_sig, (size_t)N * nmax * 8), "spectra: sig");
+  CK(ensure(c.d_sig32, (size_t)N * r * 4), "spectra: sig32");
+  CK(ensure(c.d_rank, (size_t)N * 4), "spectra: rank");
+  CK(ensure(c.d_bdesc, (size_t)(N + 1) * sizeof(BaseDesc)), "spectra: bdesc");
+  CK(ensure(c.d_adesc_raw, (size_t)(N + 1) * sizeof(AppDesc)), "spectra: adesc");
+  CK(ensure(c.d_adesc_trunc, (size_t)(N + 1) * sizeof(AppDesc)), "spectra: adesc");
+  CK(ensure(c.d_meta32, (size_t)N * 4), "spectra: meta");
+  CK(cudaMemcpyAsync(c.d_meta32.p, c.n.data(), (size_t)N * 4, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
+  const int* d_ncols = (const int*)c.d_meta32.p;
+  // group blocks by width (Omega is shared inside a group), batch under the workspace budget
+  std::vector<int> order(N);
+  for (int i = 0; i < N; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return c.n[a] < c.n[b]; });
+  const int pr_all = prof_begin(c, PC_SPEC_EIG);
+  for (int g0 = 0; g0 < N;) {
+    const int n = c.n[order[g0]];
+    int g1 = g0;
+    while (g1 < N && c.n[order[g1]] == n) ++g1;
+    const size_t per = 8 * ((size_t)m * s + (size_t)n * s + (size_t)std::max<int64_t>(m, n) * s + 5 * (size_t)s * s +
+                            2 * (size_t)s) + 64;
+    const int nbmax = (int)std::max<size_t>(1, std::min<size_t>((size_t)(g1 - g0), c.ws_budget / per));
+    CK(ensure(c.ws[WS_C], (size_t)n * s * 8), "spectra: Omega");
+    double* Om = (double*)c.ws[WS_C].p;
+    CK(launch_randn(c, Om, (int64_t)n * s, 0x243F6A8885A308D3ull ^ (uint64_t)n), "spectra: Omega");
+    for (int b0 = g0; b0 < g1; b0 += nbmax) {
+      const int nb = std::min(nbmax, g1 - b0);
+      CK(ensure(c.ws[WS_A], (size_t)nb * m * s * 8), "spectra: Y");
+      CK(ensure(c.ws[WS_PAIR], (size_t)nb * n * s * 8), "spectra: Z");
+      CK(ensure(c.ws[WS_OUT], (size_t)nb * std::max<int64_t>(m, n) * s * 8), "spectra: tmp");
+      CK(ensure(c.ws[WS_G], (size_t)nb * s * s * 8 * 2), "spectra: H");
+      CK(ensure(c.ws[WS_V], (size_t)nb * s * s * 8), "spectra: V");
+      CK(ensure(c.ws[WS_B], (size_t)nb * s * s * 8), "spectra: VH");
+      CK(ensure(c.ws[WS_EV], (size_t)nb * s * 8), "spectra: ev");
+      CK(ensure(c.ws[WS_PERM], (size_t)nb * s * 4), "spectra: perm");
+      CK(ensure(c.ws[WS_STAT], (size_t)nb * 4 * 2 + 64), "spectra: stat");
+      double* Y = (double*)c.ws[WS_A].p;
+      double* Z = (double*)c.ws[WS_PAIR].p;
+      double* Tmp = (double*)c.ws[WS_OUT].p;
+      double* H = (double*)c.ws[WS_G].p;
+      double* T = H + (size_t)nb * s * s;
+      int* st = (int*)c.ws[WS_STAT].p;
+      // pointer tables: A (arena), U, Ftrunc, ids, ns
+      std::vector<const float*> hA(nb), hU(nb), hF(nb);
+      std::vector<int> hid(nb), hns(nb, s);
+      for (int t = 0; t < nb; ++t) {
+        const int i = order[b0 + t];
+        hid[t] = i;
+        hA[t] = (const float*)c.arena.p + c.boff[i];
+        hU[t] = (const float*)c.d_U.p + c.uoff[i];
+        hF[t] = (const float*)c.d_Ftrunc.p + c.foff[i];
+      }
+      CK(ensure(c.ws[WS_META], (size_t)nb * 8 * 3 + (size_t)nb * 8 + 64), "spectra: ptrs");
+      char* mb = (char*)c.ws[WS_META].p;
+      const float** dA = (const float**)mb;
+      const float** dU = dA + nb;
+      const float** dF = dU + nb;
+      int* dids = (int*)(dF + nb);
+      int* dns = dids + nb;
+      CK(cudaMemcpyAsync(dA, hA.data(), (size_t)nb * 8, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
+      CK(cudaMemcpyAsync(dU, hU.data(), (size_t)nb * 8, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
+      CK(cudaMemcpyAsync(dF, hF.data(), (size_t)nb * 8, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
+      CK(cudaMemcpyAsync(dids, hid.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
+      CK(cudaMemcpyAsync(dns, hns.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
+      const int64_t ms = m * s, ns_ = (int64_t)n * s;
+      // Y = A Omega, orth
+      CK((gemm_mixed<float, false>(c, nb, (int)m, s, n, nullptr, m, 0, Om, n, 0, Y, m, ms, 1.0, dA)), "spectra: AO");
+      CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st), "spectra: cholqr");
+      for (int it = 0; it < c.subspace_iters; ++it) {
+        CK((gemm_mixed<float, true>(c, nb, n, s, (int)m, nullptr, m, 0, Y, m, ms, Z, n, ns_, 1.0, dA)),
+           "spectra: AtY");
+        CK(cholqr(c, nb, n, s, Z, Tmp, H, T, st), "spectra: cholqr");
+        CK((gemm_mixed<float, false>(c, nb, (int)m, s, n, nullptr, m, 0, Z, n, ns_, Y, m, ms, 1.0, dA)),
+           "spectra: AZ");
+        CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st), "spectra: cholqr");
+      }
+      // Rayleigh-Ritz: Bt = A^T Q, H = Bt^T Bt
+      CK((gemm_mixed<float, true>(c, nb, n, s, (int)m, nullptr, m, 0, Y, m, ms, Z, n, ns_, 1.0, dA)), "spectra: Bt");
+      CK((gemm_mixed<double, true>(c, nb, s, s, n, Z, n, ns_, Z, n, ns_, H, s, (int64_t)s * s)), "spectra: H");
+      CK(launch_syev(c, H, s, (int64_t)s * s, dns, nb, s, (double*)c.ws[WS_V].p, (int64_t)s * s,
+                     (double*)c.ws[WS_B].p, (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, s, st + nb),
+         "spectra: eig(H)");
+      {
+        dim3 g((unsigned)((m + 255) / 256), kc, nb);
+        k_big_leftvec<<<g, 256, 0, c.stream>>>(m, s, kc, Y, (const double*)c.ws[WS_V].p, (const int*)c.ws[WS_PERM].p,
+                                               (float* const*)dU);
+        c.launches += 1;
+        CK(cudaGetLastError(), "spectra: U_r");
+      }
+      k_big_stats<<<(nb + 127) / 128, 128, 0, c.stream>>>(
+          nb, dids, s, r, m, nmax, (const double*)c.ws[WS_EV].p, (const double*)c.d_E.p, d_ncols, (double*)c.d_sig.p,
+          (float*)c.d_sig32.p, (int*)c.d_rank.p, (const float* const*)dU, (const float* const*)dA,
+          (const float* const*)dF, (BaseDesc*)c.d_bdesc.p, (AppDesc*)c.d_adesc_raw.p, (AppDesc*)c.d_adesc_trunc.p);
+      c.launches += 1;
+      CK(cudaGetLastError(), "spectra: stats");
+      std::vector<int> stat(nb);
+      CK(cudaMemcpyAsync(stat.data(), st + nb, (size_t)nb * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
+      CK(cudaStreamSynchronize(c.stream), "spectra: sync");
+      for (int t = 0; t < nb; ++t)
+        if (stat[t] < 0)
+          return fail(c, CMSVD_E_NOCONV, "block_spectra: QL did not converge on the Rayleigh-Ritz matrix of block " +
+                                             std::to_string(hid[t]) + " (" + std::to_string(s) + "x" +
+                                             std::to_string(s) + ")");
+    }
+    g0 = g1;
+  }
+  prof_end(c, pr_all);
+  {
+    dim3 g2((unsigned)((m + kThreads - 1) / kThreads), kc, N);
+    k_trunc_operand<<<g2, kThreads, 0, c.stream>>>(m, (const BaseDesc*)c.d_bdesc.p, (const AppDesc*)c.d_adesc_trunc.p,
+                                                   (float*)c.d_Ftrunc.p);
+    c.launches += 1;
+    CK(cudaGetLastError(), "spectra: trunc");
+  }
+  c.sig.resize((size_t)N * nmax);
+  c.rank.resize(N);
+  CK(cudaMemcpyAsync(c.sig.data(), c.d_sig.p, (size_t)N * nmax * 8, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
+  CK(cudaMemcpyAsync(c.rank.data(), c.d_rank.p, (size_t)N * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
+  if (sigma)
+    CK(cudaMemcpyAsync(sigma, c.d_sig32.p, (size_t)N * r * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
+  CK(cudaStreamSynchronize(c.stream), "spectra: sync");
+  c.rr.resize(N);
+  c.tc_ok = true;
+  for (int i = 0; i < N; ++i) c.rr[i] = std::min(kc, c.rank[i]);
+  if (energy) std::memcpy(energy, c.E.data(), (size_t)N * 8);
+  if (rank_out) std::memcpy(rank_out, c.rank.data(), (size_t)N * 4);
+  c.spectra_r = r;
+  return CMSVD_OK;
+}
+
 Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t* rank_out) {
   if (c.count <= 0) return fail(c, CMSVD_E_STATE, "block_spectra: no collection registered");
   if (r < 1) return fail(c, CMSVD_E_ARG, "block_spectra: r must be >= 1");
   const int64_t m = c.m;
   const int N = c.count;
-  for (int i = 0; i < N; ++i) {
-    if (c.n[i] > m) return fail(c, CMSVD_E_SHAPE, "block_spectra: wide blocks (n_i > m) are not supported");
-    if (c.n[i] > kEigMax)
-      return fail(c, CMSVD_E_SHAPE, "block_spectra: n_i > " + std::to_string(kEigMax) + " not supported yet");
+  int nbig = 0;
+  for (int i = 0; i < N; ++i) nbig += c.n[i] > kEigMax;
+  if (nbig > 0) {
+    if (nbig < N)
+      return fail(c, CMSVD_E_SHAPE, "block_spectra: collections mixing blocks wider than " +
+                                        std::to_string(kEigMax) + " columns with narrower ones are not supported");
+    return do_block_spectra_big(c, r, energy, sigma, rank_out);
   }
+  c.big = false;
+  for (int i = 0; i < N; ++i)
+    if (c.n[i] > m) return fail(c, CMSVD_E_SHAPE, "block_spectra: wide blocks (m < n_i <= 512) are not supported");
   const int nmax = c.nmax;
   c.kcols.assign(c.n.begin(), c.n.end());
   c.uoff.resize(N + 1);
@@ -415,7 +587,7 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
            "pairs: eig(G)");
         prof_end(c, pf);
       }
-      if (kinds & CMSVD_RESIDUAL) {
+      if ((kinds & CMSVD_RESIDUAL) && !c.big) {  // A22 bases: R = (I - QQ^T)F = 0, sigma(W') unused
         pf = prof_begin(c, PC_EIG_W);
         CK(launch_tridiag_topk(c, W, WMAX, (int64_t)WMAX * WMAX, nW, (int)Pc, WMAX, thrW, r, evW, cntW, trW, scr),
            "pairs: eig(W)");
@@ -436,7 +608,7 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
 Dims block_dims(const Ctx& c, int operand) {
   Dims d;
   for (int i = 0; i < c.count; ++i) {
-    d.qmax = std::max(d.qmax, c.rank[i]);
+    d.qmax = std::max(d.qmax, c.big ? c.rr[i] : c.rank[i]);  // A22: full-range bases keep only U_r
     d.rrmax = std::max(d.rrmax, c.rr[i]);
     d.wmax = std::max(d.wmax, operand == CMSVD_OPERAND_TRUNC ? c.rr[i] : c.n[i]);
   }

@@ -7,7 +7,7 @@ namespace cmsvd {
 
 typedef cmsvd_status Status;
 
-constexpr int kEigMax = 160;     // largest Gram handled by the shared-memory eigensolvers (fits 227 KB)
+constexpr int kEigMax = 512;     // largest Gram handled by the eigensolvers (> 160: in place in global memory)
 
 struct Dims {
   int qmax = 0;   // projection-basis columns (full range)
@@ -25,6 +25,7 @@ Status cuda_fail(Ctx& c, cudaError_t e, const char* where);
 
 Status do_register(Ctx& c, int64_t m, int32_t count, const int32_t* n, const float* const* blocks, const int64_t* ld,
                    int where);
+Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int32_t* rank_out);
 Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t* rank_out);
 Status do_pair_errors(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, uint32_t kinds, int operand, int where,
                       double* err2, double* total, float* sigma_tilde, float* mu);

@@ -1,0 +1,291 @@
+// k_big.cu -- block spectra (S2) for blocks too wide for the per-block Gram
+// eigensolver (n_i > 512 or square weight-like blocks, configs 3 and 4):
+// randomized subspace iteration with fp64 accumulation,
+//   Y = A Omega;  repeat q: Z = orth(A^T orth(Y)); Y = A Z;  Q = orth(Y)
+//   Bt = A^T Q (n x s);  H = Bt^T Bt (s x s);  H = W diag(lambda) W^T
+//   sigma_l = sqrt(lambda_l), U_r = Q W_r     (l <= r)
+// (the top-r singular triplets of A; exact to the convergence of range(Q),
+// (sigma_{s+1}/sigma_r)^{2q+1}).  Orthonormalisation: CholQR2 (fp64 Gram,
+// Cholesky, triangular inverse, product), run twice.
+// Kernels: batched mixed-precision SIMT GEMM (fp32 or fp64 A, fp64 B, fp64
+// accumulate), batched Cholesky + upper-triangular inverse (one CTA per
+// problem, global memory), Gaussian test matrices (counter-based hash).
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cmsvd {
+
+// ---------------------------------------------------------------------------
+// C = op(A) * B (+ C if accumulate), fp64 accumulation.
+//   TA = false: A is M x K column-major (lda), element (i,k) at A[k*lda + i]
+//   TA = true : A is K x M column-major (lda), element (i,k) at A[i*lda + k]
+//   B: K x N column-major (ldb), C: M x N column-major (ldc).
+// Batched over blockIdx.z with strides sA, sB, sC.  64x64 tiles, BK = 16.
+// ---------------------------------------------------------------------------
+template <typename TAe, bool TA>
+__global__ void __launch_bounds__(256) k_gemm_mixed(int M, int N, int K, const TAe* __restrict__ A,
+                                                    const TAe* const* __restrict__ Ap, int64_t lda, int64_t sA,
+                                                    const double* __restrict__ B, int64_t ldb, int64_t sB,
+                                                    double* __restrict__ C, int64_t ldc, int64_t sC, double alpha) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ double As[BK][BM + 1];
+  __shared__ double Bs[BK][BN + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
+  const TAe* Ab = Ap ? Ap[blockIdx.z] : A + (int64_t)blockIdx.z * sA;
+  const double* Bb = B + (int64_t)blockIdx.z * sB;
+  double* Cb = C + (int64_t)blockIdx.z * sC;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int e = tid + 256 * s;
+      double va = 0.0;
+      if (TA) {  // element (i, k) at A[i*lda + k]: coalesce along k
+        const int k = e & 15, i = e >> 4;
+        if (i0 + i < M && k0 + k < K) va = (double)Ab[(int64_t)(i0 + i) * lda + k0 + k];
+        As[k][i] = va;
+      } else {   // element (i, k) at A[k*lda + i]: coalesce along i
+        const int i = e & 63, k = e >> 6;
+        if (i0 + i < M && k0 + k < K) va = (double)Ab[(int64_t)(k0 + k) * lda + i0 + i];
+        As[k][i] = va;
+      }
+      const int kb = e & 15, j = e >> 4;  // B element (k, j) at B[j*ldb + k]: coalesce along k
+      double vb = 0.0;
+      if (j0 + j < N && k0 + kb < K) vb = Bb[(int64_t)(j0 + j) * ldb + k0 + kb];
+      Bs[kb][j] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[k][tx + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[k][ty + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + tx + 16 * a, j = j0 + ty + 16 * b;
+      if (i < M && j < N) Cb[(int64_t)j * ldc + i] = alpha * acc[a][b];
+    }
+}
+
+template <typename TAe, bool TA>
+cudaError_t gemm_mixed(Ctx& c, int batch, int M, int N, int K, const TAe* A, int64_t lda, int64_t sA,
+                       const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
+                       double alpha, const TAe* const* Ap) {
+  if (batch <= 0 || M <= 0 || N <= 0) return cudaSuccess;
+  dim3 g((M + 63) / 64, (N + 63) / 64, batch);
+  k_gemm_mixed<TAe, TA><<<g, 256, 0, c.stream>>>(M, N, K, A, Ap, lda, sA, B, ldb, sB, C, ldc, sC, alpha);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// H (s x s, SPD, column-major ld s) -> Cholesky H = R^T R in place (R upper,
+// in the upper triangle of H) and T = R^{-1} (upper, zero below) into Ts.
+// A relative diagonal shift 1e-13 * max(diag) keeps numerically semidefinite
+// Grams factorable (CholQR2: the second pass re-orthonormalises).
+// One CTA per problem (256 threads), matrices in global memory (L2-resident).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_chol_inv(double* __restrict__ Hs, double* __restrict__ Ts, int s,
+                                                  int64_t stride, int* __restrict__ status) {
+  double* H = Hs + (int64_t)blockIdx.x * stride;
+  double* T = Ts + (int64_t)blockIdx.x * stride;
+  const int tid = threadIdx.x;
+  __shared__ double s_piv, s_shift;
+  __shared__ double red[8];
+  __shared__ int s_bad;
+  double mx = 0.0;
+  for (int i = tid; i < s; i += blockDim.x) mx = fmax(mx, fabs(H[(int64_t)i * s + i]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m2 = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m2 = fmax(m2, red[k]);
+    s_shift = 1e-13 * m2;
+    s_bad = 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < s; i += blockDim.x) H[(int64_t)i * s + i] += s_shift;
+  __syncthreads();
+  for (int k = 0; k < s; ++k) {
+    if (tid == 0) {
+      double d = H[(int64_t)k * s + k];
+      if (!(d > 0.0)) { s_bad = 1; d = fmax(s_shift, 1e-300); }
+      s_piv = sqrt(d);
+      H[(int64_t)k * s + k] = s_piv;
+    }
+    __syncthreads();
+    const double inv = 1.0 / s_piv;
+    for (int j = k + 1 + tid; j < s; j += blockDim.x) H[(int64_t)j * s + k] *= inv;  // R(k, j)
+    __syncthreads();
+    const int rem = s - k - 1;
+    // H(i, j) -= R(k, i) R(k, j) for k < i <= j: one thread per column j, loop over i
+    for (int j = k + 1 + tid; j < s; j += blockDim.x) {
+      const double rkj = H[(int64_t)j * s + k];
+      double* colj = H + (int64_t)j * s;
+      for (int i = k + 1; i <= j; ++i) colj[i] = fma(-H[(int64_t)i * s + k], rkj, colj[i]);
+    }
+    (void)rem;
+    __syncthreads();
+  }
+  // T = R^{-1}: column j by one thread, back substitution
+  for (int j = tid; j < s; j += blockDim.x) {
+    double* tj = T + (int64_t)j * s;
+    for (int i = j + 1; i < s; ++i) tj[i] = 0.0;
+    tj[j] = 1.0 / H[(int64_t)j * s + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double acc = 0.0;
+      for (int k = i + 1; k <= j; ++k) acc = fma(H[(int64_t)k * s + i], tj[k], acc);
+      tj[i] = -acc / H[(int64_t)i * s + i];
+    }
+  }
+  if (tid == 0) status[blockIdx.x] = s_bad;
+}
+
+// Gaussian N(0,1) test matrix from a counter-based hash (splitmix64 + Box-Muller); deterministic.
+__global__ void k_randn(double* __restrict__ X, int64_t n, uint64_t seed) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  auto mix = [](uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  const uint64_t a = mix(seed * 0x100000001B3ull + 2 * (uint64_t)i), b = mix(seed * 0x100000001B3ull + 2 * (uint64_t)i + 1);
+  const double u1 = ((double)(a >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+  const double u2 = ((double)(b >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+  X[i] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+}
+
+cudaError_t launch_randn(Ctx& c, double* X, int64_t n, uint64_t seed) {
+  k_randn<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(X, n, seed);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+// CholQR on a batch: Y (rows x s per problem, ld rows) -> Y T with Y^T Y = R^T R, T = R^{-1}.
+// Workspace: H, T (s x s each per problem), Ytmp (rows x s per problem).
+cudaError_t cholqr(Ctx& c, int batch, int64_t rows, int s, double* Y, double* Ytmp, double* H, double* T,
+                   int* status) {
+  cudaError_t e;
+  for (int pass = 0; pass < 2; ++pass) {
+    e = gemm_mixed<double, true>(c, batch, s, s, (int)rows, Y, rows, rows * s, Y, rows, rows * s, H, s,
+                                 (int64_t)s * s);
+    if (e != cudaSuccess) return e;
+    k_chol_inv<<<batch, 256, 0, c.stream>>>(H, T, s, (int64_t)s * s, status);
+    c.launches += 1;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = gemm_mixed<double, false>(c, batch, (int)rows, s, s, Y, rows, rows * s, T, s, (int64_t)s * s, Ytmp, rows,
+                                  rows * s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(Y, Ytmp, sizeof(double) * (size_t)batch * rows * s, cudaMemcpyDeviceToDevice, c.stream);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// U[:, l] = Y W[:, perm[l]] (fp32 out) for l < kc: the top-kc left singular
+// vectors from the Rayleigh-Ritz step (Y = orthonormal range basis, m x s).
+__global__ void __launch_bounds__(256) k_big_leftvec(int64_t m, int s, int kc, const double* __restrict__ Y,
+                                                     const double* __restrict__ V, const int* __restrict__ perm,
+                                                     float* const* __restrict__ Uout) {
+  const int b = blockIdx.z, l = blockIdx.y;
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= m || l >= kc) return;
+  const double* y = Y + (int64_t)b * m * s;
+  const double* v = V + (int64_t)b * s * s + (int64_t)perm[(int64_t)b * s + l] * s;
+  double acc = 0.0;
+  for (int k = 0; k < s; ++k) acc = fma(y[(int64_t)k * m + row], v[k], acc);
+  Uout[b][(int64_t)l * m + row] = (float)acc;
+}
+
+// Spectrum statistics + descriptors for "big" blocks (A22): only the top
+// ns = min(r, s) singular values are kept; the base's range is R^m (q = rr
+// stored columns, full = 1: the paper-literal residual R = (I - QQ^T)F is 0).
+__global__ void k_big_stats(int nb, const int* __restrict__ ids, int s, int r, int64_t m, int nmax_sig,
+                            const double* __restrict__ ev, const double* __restrict__ E, const int* __restrict__ ncols,
+                            double* __restrict__ sig, float* __restrict__ sig32, int* __restrict__ rank,
+                            const float* const* __restrict__ Uptr, const float* const* __restrict__ Aptr,
+                            const float* const* __restrict__ Fptr, BaseDesc* __restrict__ bd,
+                            AppDesc* __restrict__ ad_raw, AppDesc* __restrict__ ad_trunc) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const int i = ids[b];
+  const double* e = ev + (int64_t)b * s;
+  double* sg = sig + (int64_t)i * nmax_sig;
+  const int n = ncols[i];
+  const int rk = (int)(m < n ? m : n);
+  const int ns = r < s ? r : s;
+  const int rr = ns < rk ? ns : rk;
+  double top = 0.0, topr = 0.0;
+  for (int l = 0; l < nmax_sig; ++l) sg[l] = 0.0;
+  for (int l = 0; l < ns; ++l) {
+    const double lam = fmax(e[l], 0.0);
+    sg[l] = sqrt(lam);
+    if (l < rr) top += lam;
+    if (l < r) topr += lam;
+  }
+  for (int l = 0; l < r; ++l) sig32[(int64_t)i * r + l] = (l < ns) ? (float)sg[l] : 0.f;
+  rank[i] = rk;
+  const double Ei = E[i];
+  BaseDesc d;
+  d.basis = Uptr[b];
+  d.spec = sg;
+  d.q = rr;
+  d.rr = rr;
+  d.ns = rr;
+  d.full = 1;
+  d.E = Ei;
+  d.tail_inc = fmax(Ei - top, 0.0);
+  d.rest_res = d.tail_inc;
+  d.tailw = fmax(Ei - topr, 0.0);
+  bd[i] = d;
+  AppDesc a;
+  a.F = Aptr[b];
+  a.w = n;
+  a.pad = 0;
+  a.E = Ei;
+  a.extra = 0.0;
+  a.tailw = d.tailw;
+  ad_raw[i] = a;
+  a.F = Fptr[b];
+  a.w = rr;
+  a.extra = d.tail_inc;
+  ad_trunc[i] = a;
+}
+
+// Explicit instantiations used by the engine
+template cudaError_t gemm_mixed<float, false>(Ctx&, int, int, int, int, const float*, int64_t, int64_t,
+                                              const double*, int64_t, int64_t, double*, int64_t, int64_t, double,
+                                              const float* const*);
+template cudaError_t gemm_mixed<float, true>(Ctx&, int, int, int, int, const float*, int64_t, int64_t,
+                                             const double*, int64_t, int64_t, double*, int64_t, int64_t, double,
+                                              const float* const*);
+template cudaError_t gemm_mixed<double, false>(Ctx&, int, int, int, int, const double*, int64_t, int64_t,
+                                               const double*, int64_t, int64_t, double*, int64_t, int64_t, double,
+                                               const double* const*);
+template cudaError_t gemm_mixed<double, true>(Ctx&, int, int, int, int, const double*, int64_t, int64_t,
+                                              const double*, int64_t, int64_t, double*, int64_t, int64_t, double,
+                                              const double* const*);
+
+}  // namespace cmsvd

@@ -73,7 +73,8 @@ __device__ __forceinline__ void sturm2(const T* __restrict__ d, const T* __restr
 #endif
 constexpr int kTriWarps = CMSVD_TRI_WARPS;
 constexpr int kTriThreads = 32 * kTriWarps;
-constexpr int kTriMax = 256;  // 8 row chunks of 32 lanes
+constexpr int kTriMax = 512;      // up to 16 row chunks of 32 lanes (n > 160: matrix in global memory)
+constexpr int kEigSmemMax = 160;  // largest n staged entirely in shared memory
 
 __device__ __forceinline__ double block_sum8(double v, double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -117,12 +118,12 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int i = lane + 32 * t;
-      if (t + 1 < NT || i < m) { x0[t] = col0[i]; x1[t] = col1[i]; }
+      if (32 * (t + 1) <= m || i < m) { x0[t] = col0[i]; x1[t] = col1[i]; }
     }
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int i = lane + 32 * t;
-      if (t + 1 < NT || i < m) {
+      if (32 * (t + 1) <= m || i < m) {
         if (UPD) {
           x0[t] = fma(-vi[t], wj0, x0[t]); x0[t] = fma(-wi[t], vj0, x0[t]);
           x1[t] = fma(-vi[t], wj1, x1[t]); x1[t] = fma(-wi[t], vj1, x1[t]);
@@ -142,7 +143,7 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int i = lane + 32 * t;
-      if (t + 1 < NT || i < m) {
+      if (32 * (t + 1) <= m || i < m) {
         double x = col[i];
         if (UPD) {
           x = fma(-vi[t], wj, x);
@@ -157,7 +158,7 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     const int i = lane + 32 * t;
-    if (t + 1 < NT || i < m) {
+    if (32 * (t + 1) <= m || i < m) {
       part[wid * n + i] = acc[t];
       dw = fma(acc[t], u[i], dw);
     }
@@ -178,7 +179,10 @@ __device__ __forceinline__ void tri_pass_dispatch(double* B, int ld, int m, cons
     case 5: tri_pass<5, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
     case 6: tri_pass<6, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
     case 7: tri_pass<7, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    default: tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 8: tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 9: case 10: tri_pass<10, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 11: case 12: tri_pass<12, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    default: tri_pass<16, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
   }
 }
 
@@ -296,6 +300,9 @@ __device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld
   }
 }
 
+// GL = true: the matrix is reduced in place in global memory (L2-resident; n up to 512), only the
+// vectors and partial sums live in shared memory.
+template <bool GL>
 __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __restrict__ Gin, int64_t ld_in,
                                                             int64_t stride_in, const int* __restrict__ ns,
                                                             const double* __restrict__ thr, int kw, int nstride,
@@ -305,9 +312,9 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __rest
   extern __shared__ double sm[];
   const int p = blockIdx.x;
   const int n = ns[p];
-  const int ld = n;
-  double* __restrict__ A = sm;                          // n x n, column-major
-  double* vA = A + n * ld;                              // reflector buffers (ping-pong)
+  const int ld = GL ? (int)ld_in : n;
+  double* __restrict__ A = GL ? const_cast<double*>(Gin) + (int64_t)p * stride_in : sm;  // column-major
+  double* vA = GL ? sm : A + n * ld;                    // reflector buffers (ping-pong)
   double* vB = vA + n;
   double* __restrict__ w = vB + n;
   double* __restrict__ pp = w + n;                      // tau * A v of the current reflector
@@ -323,25 +330,27 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __rest
     if (tid == 0) { cnt_out[p] = 0; trace_out[p] = 0.0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; }
     return;
   }
-  for (int j = wid; j < n; j += kTriWarps) {
-    const double* src = Gp + (int64_t)j * ld_in;
-    double* dst = A + j * ld;
-    for (int i = lane; i < n; i += 32) dst[i] = src[i];
+  if (!GL) {
+    for (int j = wid; j < n; j += kTriWarps) {
+      const double* src = Gp + (int64_t)j * ld_in;
+      double* dst = A + j * ld;
+      for (int i = lane; i < n; i += 32) dst[i] = src[i];
+    }
   }
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s += A[i * ld + i];
+    for (int i = 0; i < n; ++i) s += A[(int64_t)i * ld + i];
     trace_out[p] = s;
   }
   tri_reduce<false>(A, n, ld, vA, vB, w, part, e2, nullptr, nullptr, nullptr);
   if (tid == 0 && n >= 2 && n < 3) {
-    const double t = A[(n - 2) * ld + (n - 1)];
+    const double t = A[(int64_t)(n - 2) * ld + (n - 1)];
     e2[n - 2] = t * t;
   }
   __syncthreads();
   for (int i = tid; i < n; i += kTriThreads) {
-    const double di = A[i * ld + i];
+    const double di = A[(int64_t)i * ld + i];
     d[i] = di;
     dO[i] = di;
     if (i + 1 < n) eO[i] = e2[i];
@@ -444,6 +453,7 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
 // evals[l] is column perm[p*stride_out + l] of V_p (n x n, ld n, at
 // Vws + p*stride_v); status[p] = QL iterations, or -1 on no convergence.
 // ---------------------------------------------------------------------------
+template <bool GL>
 __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __restrict__ Gin, int64_t ld_in,
                                                             int64_t stride_in, const int* __restrict__ ns,
                                                             double* __restrict__ Vws, int64_t stride_v,
@@ -454,10 +464,10 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
   const int p = blockIdx.x;
   const int n = ns[p];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int ldz = n | 1;
-  double* __restrict__ A = sm;                         // n x n (ld n), later Z (n x ldz)
-  const int64_t asz = (int64_t)n * ldz;
-  double* vA = A + asz;
+  const int ldz = GL ? (int)ld_in : (n | 1);
+  double* __restrict__ A = GL ? const_cast<double*>(Gin) + (int64_t)p * stride_in : sm;  // later Z (n x ldz)
+  const int64_t asz = GL ? 0 : (int64_t)n * ldz;
+  double* vA = (GL ? sm : A) + asz;
   double* vB = vA + n;
   double* __restrict__ w = vB + n;
   double* __restrict__ part = w + n;                   // kTriWarps x n
@@ -471,21 +481,24 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
   double* VH = VHws + (int64_t)p * stride_v;
   double* V = Vws + (int64_t)p * stride_v;
   if (n <= 0) { if (tid == 0) status[p] = 0; return; }
-  for (int j = wid; j < n; j += kTriWarps) {
-    const double* src = Gin + (int64_t)p * stride_in + (int64_t)j * ld_in;
-    for (int i = lane; i < n; i += 32) A[j * n + i] = src[i];
+  const int lda = GL ? (int)ld_in : n;
+  if (!GL) {
+    for (int j = wid; j < n; j += kTriWarps) {
+      const double* src = Gin + (int64_t)p * stride_in + (int64_t)j * ld_in;
+      for (int i = lane; i < n; i += 32) A[j * n + i] = src[i];
+    }
   }
   __syncthreads();
-  tri_reduce<true>(A, n, n, vA, vB, w, part, e2, ee, VH, tauH);
+  tri_reduce<true>(A, n, lda, vA, vB, w, part, e2, ee, VH, tauH);
   __syncthreads();
-  for (int i = tid; i < n; i += kTriThreads) dd[i] = A[i * n + i];
+  for (int i = tid; i < n; i += kTriThreads) dd[i] = A[(int64_t)i * lda + i];
   if (tid == 0) {
-    if (n == 2) ee[0] = A[0 * n + 1];
+    if (n == 2) ee[0] = A[0 * lda + 1];
     ee[n - 1] = 0.0;
   }
   __syncthreads();
   // Z = I (overwrites A, which is dead), ld = ldz
-  for (int e = tid; e < n * ldz; e += kTriThreads) A[e] = 0.0;
+  for (int64_t e = tid; e < (int64_t)n * ldz; e += kTriThreads) A[e] = 0.0;
   __syncthreads();
   for (int i = tid; i < n; i += kTriThreads) A[(int64_t)i * ldz + i] = 1.0;
   __shared__ double s_anorm;
@@ -603,7 +616,8 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
 }
 
 size_t syev_smem(int nmax) {
-  return (size_t)nmax * (nmax | 1) * 8 + (size_t)(9 + kTriWarps) * nmax * 8 + 64;
+  const size_t vec = (size_t)(9 + kTriWarps) * nmax * 8 + 64;
+  return nmax > kEigSmemMax ? vec : (size_t)nmax * (nmax | 1) * 8 + vec;
 }
 
 cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns, int nprob,
@@ -612,17 +626,35 @@ cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_i
   if (nprob <= 0) return cudaSuccess;
   if (nmax > kTriMax) return cudaErrorInvalidValue;
   const size_t smem = syev_smem(nmax);
-  cudaError_t e = cudaFuncSetAttribute(k_syev_ql, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (nmax <= kEigSmemMax) {
+    cudaError_t e = cudaFuncSetAttribute(k_syev_ql<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_syev_ql<false><<<nprob, kTriThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, Vws, stride_v, VHws, evals,
+                                                             perm, stride_out, status, 60);
+    c.launches += 1;
+    return cudaGetLastError();
+  }
+  // in place in global memory (G is destroyed); batches sized to stay L2-resident
+  cudaError_t e = cudaFuncSetAttribute(k_syev_ql<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_syev_ql<<<nprob, kTriThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, Vws, stride_v, VHws, evals, perm,
-                                                     stride_out, status, 60);
-  c.launches += 1;
-  return cudaGetLastError();
+  const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(nprob, (int64_t)(96 << 20) / ((int64_t)nmax * nmax * 8)));
+  for (int p0 = 0; p0 < nprob; p0 += batch) {
+    const int nb = std::min(batch, nprob - p0);
+    k_syev_ql<true><<<nb, kTriThreads, smem, c.stream>>>(G + (int64_t)p0 * stride_in, ld_in, stride_in, d_ns + p0,
+                                                         Vws + (int64_t)p0 * stride_v, stride_v,
+                                                         VHws + (int64_t)p0 * stride_v, evals + (int64_t)p0 * stride_out,
+                                                         perm + (int64_t)p0 * stride_out, stride_out, status + p0, 60);
+    c.launches += 1;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 size_t tridiag_smem(int nmax, int kw) {
   (void)kw;
-  return (size_t)nmax * nmax * 8 + (size_t)(5 + kTriWarps) * nmax * 8 + 64;
+  const size_t vec = (size_t)(5 + kTriWarps) * nmax * 8 + 64;
+  return nmax > kEigSmemMax ? vec : (size_t)nmax * nmax * 8 + vec;
 }
 
 cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
@@ -631,15 +663,32 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   if (nprob <= 0) return cudaSuccess;
   if (nmax > kTriMax) return cudaErrorInvalidValue;
   const size_t smem = tridiag_smem(nmax, kw);
-  cudaError_t e = cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   const int nstride = nmax;
   double* dd = scratch;
   double* ee = dd + (size_t)nprob * nstride;
   double* gsh = ee + (size_t)nprob * nstride;
-  k_tridiag<<<nprob, kTriThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, d_thr, kw, nstride, dd, ee, gsh, cnt,
-                                                  trace);
-  c.launches += 1;
+  cudaError_t e;
+  if (nmax <= kEigSmemMax) {
+    e = cudaFuncSetAttribute(k_tridiag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_tridiag<false><<<nprob, kTriThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, d_thr, kw, nstride, dd, ee,
+                                                             gsh, cnt, trace);
+    c.launches += 1;
+  } else {
+    // in place in global memory (G is destroyed); batches sized to stay L2-resident
+    e = cudaFuncSetAttribute(k_tridiag<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(nprob, (int64_t)(96 << 20) / ((int64_t)nmax * nmax * 8)));
+    for (int p0 = 0; p0 < nprob; p0 += batch) {
+      const int nb = std::min(batch, nprob - p0);
+      k_tridiag<true><<<nb, kTriThreads, smem, c.stream>>>(
+          G + (int64_t)p0 * stride_in, ld_in, stride_in, d_ns + p0, d_thr ? d_thr + p0 : nullptr, kw, nstride,
+          dd + (int64_t)p0 * nstride, ee + (int64_t)p0 * nstride, gsh + 4 * (int64_t)p0, cnt + p0, trace + p0);
+      c.launches += 1;
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t total = (int64_t)nprob * kw;

@@ -93,6 +93,8 @@ __global__ void __launch_bounds__(kThreads) k_build_G(const int2* __restrict__ p
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < w; ++i) s += ZZ[(int64_t)i * WMAX + i];
+    if (b.full)  // A22: ||F||^2 = ||U_r^T F||^2 + ||(I - U_r U_r^T) F||^2 (whole operand is "residual-free")
+      for (int i = 0; i < w; ++i) s += W[(int64_t)i * WMAX + i];
     zn2[p] = s;
   }
 }
@@ -129,8 +131,8 @@ __global__ void k_finalize(const int2* __restrict__ pairs, int64_t P, const Base
     for (int l = 0; l < r; ++l) sigma_tilde[p * r + l] = nanf("");
   }
   if (kinds & CMSVD_RESIDUAL) {
-    const double* ev = evW + p * r;
-    int c = cntW[p];
+    const double* ev = b.full ? nullptr : evW + p * r;
+    int c = b.full ? 0 : cntW[p];
     int ib = 0, iw = 0;
     double sel_w = 0.0;
     for (int l = 0; l < r; ++l) {
@@ -144,7 +146,8 @@ __global__ void k_finalize(const int2* __restrict__ pairs, int64_t P, const Base
     }
     double unsel = 0.0;
     for (int l = ib; l < b.ns; ++l) unsel += b.spec[l] * b.spec[l];
-    er = b.rest_res + unsel + fmax(trW[p] - sel_w, 0.0) + zn2[p] + a.extra;
+    // A22 (full-range base): R = 0, mu = top-r sigma(A_i), err^2 = E_i - sum_sel sigma^2 + ||F||^2 + extra
+    er = b.rest_res + unsel + (b.full ? 0.0 : fmax(trW[p] - sel_w, 0.0)) + zn2[p] + a.extra;
   } else if (mu) {
     for (int l = 0; l < r; ++l) mu[p * r + l] = nanf("");
   }
@@ -220,7 +223,7 @@ __global__ void k_spec_stats(int count, int nmax, int r, const double* __restric
   b.q = rk;
   b.rr = rr;
   b.ns = k;
-  b.pad = 0;
+  b.full = 0;
   b.E = Ei;
   b.tail_inc = tail_inc;
   b.rest_res = fmax(Ei - all, 0.0);

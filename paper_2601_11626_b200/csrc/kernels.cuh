@@ -47,6 +47,20 @@ cudaError_t launch_pair_tc(Ctx& c, const int2* pairs, int64_t P, const BaseDesc*
                            int use_full_basis, int QMAX, int WMAX, float* Zws, double* Wws);
 cudaError_t launch_build_G1(Ctx& c, int rr, int w, const double* spec, const float* Z, int ldz, const double* ZZ,
                             const double* WW, double* G);
+// k_big.cu: large-block spectra helpers
+template <typename TAe, bool TA>
+cudaError_t gemm_mixed(Ctx& c, int batch, int M, int N, int K, const TAe* A, int64_t lda, int64_t sA,
+                       const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
+                       double alpha = 1.0, const TAe* const* Ap = nullptr);
+__global__ void k_big_leftvec(int64_t m, int s, int kc, const double* Y, const double* V, const int* perm,
+                              float* const* Uout);
+__global__ void k_big_stats(int nb, const int* ids, int s, int r, int64_t m, int nmax_sig, const double* ev,
+                            const double* E, const int* ncols, double* sig, float* sig32, int* rank,
+                            const float* const* Uptr, const float* const* Aptr, const float* const* Fptr,
+                            BaseDesc* bd, AppDesc* ad_raw, AppDesc* ad_trunc);
+cudaError_t launch_randn(Ctx& c, double* X, int64_t n, uint64_t seed);
+cudaError_t cholqr(Ctx& c, int batch, int64_t rows, int s, double* Y, double* Ytmp, double* H, double* T,
+                   int* status);
 __global__ void k_trunc_operand(int64_t m, const BaseDesc* bd, const AppDesc* ad_trunc, float* Fbase);
 
 }  // namespace cmsvd

@@ -1,0 +1,124 @@
+"""GPU parity on collections of blocks wider than 512 columns (configs 3 and 4,
+square weight-like blocks), reading A22: spectra by subspace
+iteration on the GPU vs the oracle's exact m x m Gram eigendecomposition; the
+base range is R^m so the paper-literal residual vanishes.  Reduced sizes keep
+the oracle within seconds; the full-size config-4 case checks sampled pairs."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import cluster as oc
+import synth
+from tolerances import assert_err2, assert_sigma
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def cm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_11626_b200 as cm
+    cm.load()
+    return cm
+
+
+def norm_order(E):
+    return np.array(sorted(range(len(E)), key=lambda i: (-E[i], i)))
+
+
+def compare(out, ref, kinds, what):
+    for k, name in enumerate(["weyl", "residual", "incremental"]):
+        if kinds & (1 << k):
+            assert_err2(out["err2"][:, k], ref.err2[:, k], ref.total, f"{what} {name}")
+    assert np.allclose(out["total"], ref.total, rtol=1e-12)
+    if kinds & 4:
+        assert_sigma(out["sigma_tilde"], ref.sigma_tilde, ref.sigma_tilde[:, 0], f"{what} sigma~")
+    if kinds & 2:
+        assert_sigma(out["mu"], ref.mu, ref.mu[:, 0], f"{what} mu")
+
+
+def run_pairs(cm, col, r, pairs=None):
+    sp = oracle.block_spectra(col.blocks)
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        E, sig, rank = ctx.block_spectra(r)
+        if pairs is None:
+            pairs = synth.all_pairs_by_norm_order(norm_order(sp.E))
+        out = ctx.pair_errors(pairs, kinds=7, operand=cm.TRUNC)
+    return sp, E, sig, rank, pairs, out
+
+
+@pytest.fixture(scope="module")
+def c3(cm):
+    col = synth.config3(N=6)
+    return (col,) + run_pairs(cm, col, col.r)
+
+
+def test_c3_spectra(c3):
+    col, sp, E, sig, rank, *_ = c3
+    assert np.allclose(E, sp.E, rtol=1e-12)
+    ref = np.stack([s[:col.r] for s in sp.sig])
+    assert_sigma(sig, ref, ref[:, 0], "config3 block sigma")
+    assert np.all(rank == col.m)          # A22: rank = min(m, n)
+
+
+def test_c3_all_pairs_trunc(c3):
+    col, sp, E, sig, rank, pairs, out = c3
+    ref = oracle.pair_errors(sp, pairs, col.r, 7, oracle.TRUNC)
+    compare(out, ref, 7, "config3")
+    # A22: residual = E_i + E_j - sum_{l<=r} sigma_l(A_i)^2 exactly (R = 0)
+    tops = np.array([np.sum(s[:col.r] ** 2) for s in sp.sig])
+    res = sp.E[pairs[:, 0]] + sp.E[pairs[:, 1]] - tops[pairs[:, 0]]
+    assert np.allclose(ref.err2[:, 1], res, rtol=1e-12)
+    # soundness ordering of the estimates (P6): incremental <= residual, all >= 0
+    assert np.all(out["err2"][:, 2] <= out["err2"][:, 1] * (1 + 1e-6))
+
+
+def test_c4_reduced(cm):
+    col = synth.config4(N=4, m=1024, rank=64)
+    r = 64
+    sp, E, sig, rank, pairs, out = run_pairs(cm, col, r)
+    ref = np.stack([s[:r] for s in sp.sig])
+    assert_sigma(sig, ref, ref[:, 0], "config4-reduced block sigma")
+    orc = oracle.pair_errors(sp, pairs, r, 7, oracle.TRUNC)
+    compare(out, orc, 7, "config4-reduced")
+
+
+def test_c3_cluster_replay(cm):
+    """Alg. 3 (incremental) greedy growth on a reduced config 3 at eps = 0.3,
+    residual sort, TRUNC operand: decision replay in the oracle (A12)."""
+    from test_gpu_cluster import replay
+    col = synth.config3(N=8)
+    sp = oracle.block_spectra(col.blocks)
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        ctx.block_spectra(col.r)
+        g = ctx.cluster(cm.ALG_APPROX, 0.3, sort=cm.SORT_RESIDUAL, operand=cm.TRUNC)
+    replay(sp, g, oc.APPROX, col.r, 0.3, oc.SORT_RESIDUAL, operand=oracle.TRUNC)
+    assert sum(len(c) for c in g["clusters"]) == col.N
+
+
+def test_big_edge_cases(cm):
+    col = synth.config3(N=3, m=640)
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        ctx.block_spectra(32)
+        with pytest.raises(cm.CmsvdError):          # RAW operand: core 32 + 640 > 512
+            ctx.pair_errors(np.array([[0, 1]]), kinds=7, operand=cm.RAW)
+        out = ctx.pair_errors(np.array([[0, 1]]), kinds=1, operand=cm.RAW)   # Weyl needs no core
+        assert np.isfinite(out["err2"][0, 0])
+        with pytest.raises(cm.CmsvdError):          # Alg. 2 state needs an explicit range basis
+            ctx.cluster(cm.ALG_RESIDUAL, 0.3, operand=cm.TRUNC)
+    # mixing wide and narrow blocks is rejected
+    with cm.Context(0) as ctx:
+        ctx.register([np.asfortranarray(np.ones((640, 640), np.float32)), np.asfortranarray(np.ones((640, 8), np.float32))])
+        with pytest.raises(cm.CmsvdError):
+            ctx.block_spectra(8)
+    # tall blocks with more than 512 columns are rejected
+    with cm.Context(0) as ctx:
+        ctx.register([np.asfortranarray(np.random.default_rng(0).standard_normal((700, 600)).astype(np.float32))] * 2)
+        with pytest.raises(cm.CmsvdError):
+            ctx.block_spectra(8)
