@@ -386,6 +386,353 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __rest
 }
 
 // ---------------------------------------------------------------------------
+// Register-resident Householder tridiagonalisation (values path), n <= 32*S.
+// The lower triangle of the matrix lives in the register file of one CTA of
+// 16 warps: thread (lane, warp) holds A(i, j) for rows i = lane + 32 s and
+// columns j = warp + 16 c, for the chunks (s, c) that meet the lower triangle
+// (16 c <= 32 s + 31; 30 doubles per thread at n = 160).  The 32 x 32
+// diagonal blocks (c = 2s, 2s+1) are stored in full, so every stored element
+// contributes a_ij v_j to p_i and only the strictly-lower chunks (c < 2s) add
+// the mirrored a_ij v_i to p_j: no per-element masks.  Per reflector k:
+//   [B2] row partials of A v_k (shared memory), mirrored column partials
+//        (lane butterfly) and v^T A v partials are in -> per row
+//        p = tau A v, w = p - (tau/2)(p.v) v (zero for rows <= k)
+//   the warp owning column k+1 waits (named barrier) for those rows only,
+//        forms the updated column k+1 in temporaries and builds reflector
+//        k+1 while the other warps head to
+//   [B3] -> one fused pass over the registers: rank-2 update with (v_k, w_k)
+//        and the products with v_{k+1} (-> B2).
+// Passes are specialised at compile time on the first live column chunk
+// k/16 (finished chunks cost nothing).  No matrix traffic through shared
+// memory; same outputs as k_tridiag.
+// ---------------------------------------------------------------------------
+#ifdef CMSVD_RR_PROF
+__device__ unsigned long long g_rr_prof[8];
+#define RR_T(slot, cond) do { if ((cond) && blockIdx.x == 0) { unsigned long long _t = clock64(); if (lane == 0) atomicAdd(&g_rr_prof[slot], _t - t_last); } t_last = clock64(); } while (0)
+#else
+#define RR_T(slot, cond) do { } while (0)
+#endif
+constexpr int kRRWarps = 16;
+constexpr int kRRThreads = 32 * kRRWarps;
+
+__host__ __device__ constexpr bool rr_present(int s, int c) { return 16 * c <= 32 * s + 31; }
+__host__ __device__ constexpr bool rr_lower(int s, int c) { return 16 * c + 15 < 32 * s; }  // strictly below
+__host__ __device__ constexpr int rr_pow2(int x) { return x <= 1 ? 1 : x <= 2 ? 2 : x <= 4 ? 4 : x <= 8 ? 8 : 16; }
+
+// One pass over the live chunks (column chunks c >= KC, row chunks s >= KC/2):
+// UPD: a -= v w^T + w v^T;  MV: row partials of a u -> part[wid], mirrored
+// column partials -> cs (butterfly over lanes), u^T a u partial -> red[wid].
+template <int S, int C, int KC, bool UPD, bool MV>
+__device__ __forceinline__ void rr_pass(double (&a)[S][C], const int lane, const int wid,
+                                        const double* __restrict__ v, const double* __restrict__ w,
+                                        const double* __restrict__ u, double* __restrict__ part,
+                                        double* __restrict__ cs, double* __restrict__ red) {
+  constexpr int NR = 32 * S;
+  constexpr int CL = 2 * (S - 1);
+  constexpr int C2 = rr_pow2(CL);
+  constexpr int S0 = KC / 2;
+  double vi[S], wi[S], ui[S], pr[S], pc[C2];
+#pragma unroll
+  for (int s = S0; s < S; ++s) {
+    const int i = lane + 32 * s;
+    if (UPD) { vi[s] = v[i]; wi[s] = w[i]; }
+    if (MV) { ui[s] = u[i]; pr[s] = 0.0; }
+  }
+#pragma unroll
+  for (int c = 0; c < C2; ++c) pc[c] = 0.0;
+  double dd = 0.0;
+#pragma unroll
+  for (int c = KC; c < C; ++c) {
+    const int j = wid + 16 * c;
+    double vj = 0.0, wj = 0.0, uj = 0.0;
+    if (UPD) { vj = v[j]; wj = w[j]; }
+    if (MV) uj = u[j];
+#pragma unroll
+    for (int s = S0; s < S; ++s)
+      if (rr_present(s, c)) {
+        double x = a[s][c];
+        if (UPD) {
+          x = fma(-vi[s], wj, fma(-wi[s], vj, x));
+          a[s][c] = x;
+        }
+        if (MV) {
+          pr[s] = fma(x, uj, pr[s]);
+          if (rr_lower(s, c)) pc[c] = fma(x, ui[s], pc[c]);
+        }
+      }
+    if (MV && c < CL) dd = fma(uj, pc[c], dd);
+  }
+  if (!MV) return;
+#pragma unroll
+  for (int s = S0; s < S; ++s) dd = fma(ui[s], pr[s], dd);
+  if (CL > 0) {  // recursive-halving butterfly: lane ends with the sum of chunk lane >> (5 - log2 C2)
+    int cnt = C2;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      if (cnt > 1) {
+        const int half = cnt >> 1;
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int q = 0; q < C2 / 2; ++q)
+          if (q < half) {
+            const double send = hi ? pc[q] : pc[q + half];
+            const double keep = hi ? pc[q + half] : pc[q];
+            pc[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        cnt = half;
+      } else {
+        pc[0] += __shfl_xor_sync(0xffffffffu, pc[0], o);
+      }
+    }
+    constexpr int sh = (C2 == 1) ? 5 : (C2 == 2) ? 4 : (C2 == 4) ? 3 : (C2 == 8) ? 2 : 1;
+    const int c = lane >> sh;
+    if ((lane & ((1 << sh) - 1)) == 0 && c < CL) cs[wid + 16 * c] = pc[0];
+  }
+#pragma unroll
+  for (int s = S0; s < S; ++s) part[wid * NR + lane + 32 * s] = pr[s];
+  dd = warp_sum(dd);
+  if (lane == 0) red[wid] = dd;
+}
+
+template <int S, int C, bool UPD, bool MV>
+__device__ __forceinline__ void rr_pass_kc(int kc, double (&a)[S][C], const int lane, const int wid,
+                                           const double* v, const double* w, const double* u, double* part,
+                                           double* cs, double* red) {
+#define RR_CASE(K)                                                                     \
+  case K:                                                                              \
+    if (K < C) rr_pass<S, C, (K < C ? K : 0), UPD, MV>(a, lane, wid, v, w, u, part, cs, red); \
+    break;
+  switch (kc) {
+    RR_CASE(0) RR_CASE(1) RR_CASE(2) RR_CASE(3) RR_CASE(4) RR_CASE(5) RR_CASE(6) RR_CASE(7)
+    RR_CASE(8) RR_CASE(9) RR_CASE(10) RR_CASE(11) RR_CASE(12) RR_CASE(13) RR_CASE(14) RR_CASE(15)
+    default: break;
+  }
+#undef RR_CASE
+}
+
+template <int S, int C>
+__device__ __forceinline__ void rr_column(int ck, const double (&a)[S][C], double* x) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) x[s] = 0.0;
+#define RR_COL(K)                                                      \
+  case K:                                                              \
+    _Pragma("unroll") for (int s = 0; s < S; ++s) if (K < C && rr_present(s, K)) x[s] = a[s][K < C ? K : 0]; \
+    break;
+  switch (ck) {
+    RR_COL(0) RR_COL(1) RR_COL(2) RR_COL(3) RR_COL(4) RR_COL(5) RR_COL(6) RR_COL(7)
+    RR_COL(8) RR_COL(9) RR_COL(10) RR_COL(11) RR_COL(12) RR_COL(13) RR_COL(14) RR_COL(15)
+    default: break;
+  }
+#undef RR_COL
+}
+
+template <int S, int C>
+__global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __restrict__ Gin, int64_t ld_in,
+                                                              int64_t stride_in, const int* __restrict__ ns,
+                                                              const double* __restrict__ thr, int kw, int nstride,
+                                                              double* __restrict__ dout, double* __restrict__ e2out,
+                                                              double* __restrict__ gsh, int* __restrict__ cnt_out,
+                                                              double* __restrict__ trace_out) {
+  constexpr int NR = 32 * S;
+  constexpr int CL = 2 * (S - 1);
+  static_assert(C == 2 * S && C <= 16, "column chunks");
+  __shared__ double vb[2][NR], wb[NR], part[kRRWarps * NR], cs[NR], ds[NR], e2s[NR];
+  __shared__ double red[kRRWarps], s_tau[2];
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double* Gp = Gin + (int64_t)p * stride_in;
+  double* dO = dout + (int64_t)p * nstride;
+  double* eO = e2out + (int64_t)p * nstride;
+  if (n <= 0) {
+    if (tid == 0) { cnt_out[p] = 0; trace_out[p] = 0.0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; }
+    return;
+  }
+  double a[S][C];
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (rr_present(s, c)) {
+        const int i = lane + 32 * s, j = wid + 16 * c;
+        a[s][c] = (i < n && j < n) ? Gp[(int64_t)j * ld_in + i] : 0.0;
+      }
+  if (wid == 0) {
+    double t = 0.0;
+    for (int i = lane; i < n; i += 32) t += Gp[(int64_t)i * ld_in + i];
+    t = warp_sum(t);
+    if (lane == 0) trace_out[p] = t;
+  }
+  auto rsqrt_nr = [](double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = 0.5 * x * y;
+    double r = fma(-h, y, 0.5);
+    y = fma(y, r, y);
+    h = 0.5 * x * y;
+    r = fma(-h, y, 0.5);
+    return fma(y, r, y);
+  };
+  // reflector from the (updated) column kk held as x[s] = A(lane + 32 s, kk) by its owner warp:
+  // e2[kk], d[kk], tau -> s_tau[kk & 1], v -> vb[kk & 1]
+  auto reflector = [&](int kk, const double* x) {
+    double sg = 0.0, al = 0.0, dk = 0.0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int i = lane + 32 * s;
+      if (i > kk + 1 && i < n) sg = fma(x[s], x[s], sg);
+      if (i == kk + 1) al = x[s];
+      if (i == kk) dk = x[s];
+    }
+    sg = warp_sum(sg);
+    al = __shfl_sync(0xffffffffu, al, (kk + 1) & 31);
+    dk = __shfl_sync(0xffffffffu, dk, kk & 31);
+    double tau, scale, ee;
+    if (sg == 0.0) {
+      tau = 0.0; scale = 0.0; ee = al * al;
+    } else {
+      const double x2 = fma(al, al, sg);
+      const double xn = x2 * rsqrt_nr(x2);
+      const double beta = al >= 0.0 ? -xn : xn;
+      tau = (beta - al) * rcp_nr(beta);
+      scale = rcp_nr(al - beta);
+      ee = beta * beta;
+    }
+    if (lane == 0) { e2s[kk] = ee; ds[kk] = dk; s_tau[kk & 1] = tau; }
+    double* vv = vb[kk & 1];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int i = lane + 32 * s;
+      vv[i] = (i == kk + 1) ? 1.0 : ((i > kk + 1 && i < n) ? x[s] * scale : 0.0);
+    }
+  };
+  // columns without strictly-lower parts (the last two chunks) never get a mirrored sum
+  for (int j = 16 * CL + tid; j < NR; j += kRRThreads) cs[j] = 0.0;
+#ifdef CMSVD_RR_PROF
+  unsigned long long t_last = clock64();
+#endif
+  if (n >= 3) {
+    if (wid == 0) {
+      double x[S];
+      rr_column<S, C>(0, a, x);
+      reflector(0, x);
+    }
+    __syncthreads();
+    if (s_tau[0] != 0.0) rr_pass<S, C, 0, false, true>(a, lane, wid, nullptr, nullptr, vb[0], part, cs, red);
+    for (int k = 0; k + 2 < n; ++k) {
+      const double* v = vb[k & 1];
+      const double tau = s_tau[k & 1];
+      RR_T(0, wid == 1);
+      __syncthreads();  // B2: part, cs, red of A v_k
+      RR_T(1, wid == 1);
+      if (tid < NR) {
+        double vta = 0.0;
+#pragma unroll
+        for (int q = 0; q < kRRWarps; q += 4) vta += (red[q] + red[q + 1]) + (red[q + 2] + red[q + 3]);
+        const double Kc = 0.5 * tau * tau * vta;
+        double pt = cs[tid];
+#pragma unroll
+        for (int q = 0; q < kRRWarps; q += 4)
+          pt += (part[q * NR + tid] + part[(q + 1) * NR + tid]) + (part[(q + 2) * NR + tid] + part[(q + 3) * NR + tid]);
+        wb[tid] = (tid > k && tid < n && tau != 0.0) ? fma(tau, pt, -Kc * v[tid]) : 0.0;
+      }
+      const int k1 = k + 1;
+      const bool more = k1 + 2 < n;  // reflector k+1 exists
+      const int owner = k1 & 15;
+      if (more) {
+        const int nb = 32 * (S + (owner >= S ? 1 : 0));
+        if (wid == owner) {
+          RR_T(2, true);
+          asm volatile("bar.sync 1, %0;" ::"r"(nb) : "memory");  // the w rows (warps 0..S-1) only
+          RR_T(3, true);
+          double x[S];
+          rr_column<S, C>(k1 >> 4, a, x);
+          if (tau != 0.0) {  // updated column k+1, same arithmetic as the fused pass below
+            const double wk1 = wb[k1], vk1 = v[k1];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              const int i = lane + 32 * s;
+              x[s] = fma(-v[i], wk1, fma(-wb[i], vk1, x[s]));
+            }
+          }
+          RR_T(4, true);
+          reflector(k1, x);
+          RR_T(5, true);
+        } else if (wid < S) {
+          asm volatile("bar.arrive 1, %0;" ::"r"(nb) : "memory");
+        }
+      }
+      RR_T(6, wid == 1);
+      __syncthreads();  // B3: w_k, v_{k+1}
+      RR_T(7, wid == 1);
+      const bool mv = more && s_tau[k1 & 1] != 0.0;
+      const double* u = vb[k1 & 1];
+      if (tau != 0.0 && mv) rr_pass_kc<S, C, true, true>(k >> 4, a, lane, wid, v, wb, u, part, cs, red);
+      else if (tau != 0.0) rr_pass<S, C, 0, true, false>(a, lane, wid, v, wb, nullptr, part, cs, red);
+      else if (mv) rr_pass<S, C, 0, false, true>(a, lane, wid, nullptr, nullptr, u, part, cs, red);
+    }
+  }
+  __syncthreads();
+  // trailing 2x2 (or n <= 2): d[n-2], d[n-1], e2[n-2]
+  {
+    const int lo = n >= 2 ? n - 2 : 0;
+    for (int jj = lo; jj < n; ++jj) {
+      if (wid == (jj & 15)) {
+        double x[S];
+        rr_column<S, C>(jj >> 4, a, x);
+        double dj = 0.0, ej = 0.0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const int i = lane + 32 * s;
+          if (i == jj) dj = x[s];
+          if (i == jj + 1) ej = x[s];
+        }
+        dj = __shfl_sync(0xffffffffu, dj, jj & 31);
+        ej = __shfl_sync(0xffffffffu, ej, (jj + 1) & 31);
+        if (lane == 0) {
+          ds[jj] = dj;
+          if (jj + 1 < n) e2s[jj] = ej * ej;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kRRThreads) {
+    dO[i] = ds[i];
+    if (i + 1 < n) eO[i] = e2s[i];
+  }
+  if (tid == 0) {
+    const double* d = ds;
+    const double* e2 = e2s;
+    double glo = 1e300, ghi = -1e300, emax = 0.0;
+    for (int i = 0; i < n; ++i) {
+      double r = 0.0;
+      if (i > 0) r += sqrt(e2[i - 1]);
+      if (i + 1 < n) r += sqrt(e2[i]);
+      glo = fmin(glo, d[i] - r);
+      ghi = fmax(ghi, d[i] + r);
+      if (i + 1 < n) emax = fmax(emax, e2[i]);
+    }
+    const double nrm = fmax(fmax(fabs(glo), fabs(ghi)), 1e-300);
+    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax) * 4.0;
+    glo -= 2.2e-16 * nrm * n + pivmin;
+    ghi += 2.2e-16 * nrm * n + pivmin;
+    gsh[4 * p] = glo; gsh[4 * p + 1] = ghi; gsh[4 * p + 2] = pivmin; gsh[4 * p + 3] = nrm;
+    int above = n;
+    if (thr) {
+      const double t = thr[p];
+      if (t >= ghi) above = 0;
+      else if (t > glo) {
+        int c0, c1;
+        sturm2<double>(d, e2, n, t, t, pivmin, c0, c1);
+        above = n - c0;
+      }
+    }
+    cnt_out[p] = min(kw, above);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Plain bisection, one thread per wanted eigenvalue (high occupancy; the
 // tridiagonals are read through L1).  fp32 coarse phase on the normalised
 // matrix to ~4e-7 ||T||, widened by 1e-5 ||T||, then fp64 to 1e-13 ||T||.
@@ -668,7 +1015,19 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   double* ee = dd + (size_t)nprob * nstride;
   double* gsh = ee + (size_t)nprob * nstride;
   cudaError_t e;
-  if (nmax <= kEigSmemMax) {
+  const bool use_rr = c.eig_rr && nmax <= 160;
+  if (use_rr) {
+#define RR_LAUNCH(S_, C_)                                                                                          \
+  k_tridiag_rr<S_, C_><<<nprob, kRRThreads, 0, c.stream>>>(G, ld_in, stride_in, d_ns, d_thr, kw, nstride, dd, ee, \
+                                                          gsh, cnt, trace)
+    if (nmax <= 32) RR_LAUNCH(1, 2);
+    else if (nmax <= 64) RR_LAUNCH(2, 4);
+    else if (nmax <= 96) RR_LAUNCH(3, 6);
+    else if (nmax <= 128) RR_LAUNCH(4, 8);
+    else RR_LAUNCH(5, 10);
+#undef RR_LAUNCH
+    c.launches += 1;
+  } else if (nmax <= kEigSmemMax) {
     e = cudaFuncSetAttribute(k_tridiag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_tridiag<false><<<nprob, kTriThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, d_thr, kw, nstride, dd, ee,

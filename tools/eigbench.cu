@@ -27,15 +27,39 @@ int main(int argc, char** argv) {
   cudaMalloc(&ev, 8 * (size_t)P * kw); cudaMalloc(&tr, 8 * P); cudaMalloc(&cnt, 4 * P);
   Ctx c; c.stream = 0;
   double* scr; cudaMalloc(&scr, tridiag_scratch_bytes(P, n));
+  std::vector<double> evs[2];
+  std::vector<double> trs[2];
+  for (int variant = 0; variant < 2; ++variant) {
+  c.eig_rr = variant == 1;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
     launch_tridiag_topk(c, dG, n, (int64_t)n * n, dn, P, n, nullptr, kw, ev, cnt, tr, scr);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
-    printf("n=%d P=%d kw=%d: %.3f ms  (%.2f us/problem/SM)  err=%s\n", n, P, kw, ms, ms * 1e3 * 148 / P,
-           cudaGetErrorString(cudaGetLastError()));
+    printf("%s n=%d P=%d kw=%d: %.3f ms  (%.2f us/problem/SM)  err=%s\n", variant ? "rr  " : "smem", n, P, kw, ms,
+           ms * 1e3 * 148 / P, cudaGetErrorString(cudaGetLastError()));
   }
+  evs[variant].resize((size_t)P * kw);
+  trs[variant].resize(P);
+  cudaMemcpy(evs[variant].data(), ev, 8 * (size_t)P * kw, cudaMemcpyDeviceToHost);
+  cudaMemcpy(trs[variant].data(), tr, 8 * (size_t)P, cudaMemcpyDeviceToHost);
+  }
+#ifdef CMSVD_RR_PROF
+  unsigned long long hp[8];
+  cudaMemcpyFromSymbol(hp, g_rr_prof, sizeof(hp));
+  const char* nm[8] = {"w1 fused+bfly", "w1 B2 wait", "owner pre", "owner nbar wait", "owner col upd", "owner reflector", "w1 phase2", "w1 B3 wait"};
+  for (int q = 0; q < 8; ++q) printf("  %-18s %10.1f cycles/step\n", nm[q], hp[q] / 6.0 / (n - 2));
+#endif
+  double md = 0, mx = 0;
+  for (size_t q = 0; q < evs[0].size(); ++q) { md = fmax(md, fabs(evs[0][q] - evs[1][q])); mx = fmax(mx, fabs(evs[0][q])); }
+  double sd = 0;
+  for (int q = 0; q < P; ++q) {
+    double s0 = trs[0][q], s1 = trs[1][q];
+    for (int l = 0; l < kw; ++l) { s0 -= evs[0][(size_t)q * kw + l]; s1 -= evs[1][(size_t)q * kw + l]; }
+    sd = fmax(sd, fabs(s0 - s1) / fmax(fabs(s0), 1e-300));
+  }
+  printf("max |ev_smem - ev_rr| = %.3e (max ev %.3e); max rel diff of trace - top = %.3e\n", md, mx, sd);
   std::vector<double> hev(kw);
   cudaMemcpy(hev.data(), ev, 8 * kw, cudaMemcpyDeviceToHost);
   printf("top eig: %.6e %.6e ... %.6e\n", hev[0], hev[1], hev[kw - 1]);
