@@ -69,6 +69,13 @@ DFMA_TFLOPS = 33.96
 FFMA_TFLOPS = 72.54
 
 
+def tf32_fp32eq_tflops() -> float:
+    """fp32-equivalent 3xTF32 tensor peak: MEASURED_PEAKS.json dense bf16 burst x the nominal TF32/BF16
+    ratio (1.125/2.25 PF dense) / 3 MMAs per useful product; fallback 2250/2/3."""
+    bf16 = load_peaks().get("bf16_tflops", 2250.0)
+    return bf16 * 0.5 / 3.0
+
+
 def workload(name: str, rank: int):
     if name == "config2":
         col = synth.config2(seed=1 + 1000 * rank)
@@ -290,9 +297,10 @@ def main():
         "gram_ZZ": float(np.sum(q)) * w * (w + 1),
         "proj_Z": float(np.sum(2.0 * col.m * q * w)),
         "resid_R": float(np.sum(2.0 * col.m * q * w)),
+        "pair_tc": float(np.sum(4.0 * col.m * q * w) + P * col.m * w * (w + 1)),   # Z, R', W' useful flops
     }
     peaks = {"eig_G": DFMA_TFLOPS, "eig_W": DFMA_TFLOPS, "gram_W": DFMA_TFLOPS, "gram_ZZ": DFMA_TFLOPS,
-             "proj_Z": FFMA_TFLOPS, "resid_R": FFMA_TFLOPS}
+             "proj_Z": FFMA_TFLOPS, "resid_R": FFMA_TFLOPS, "pair_tc": tf32_fp32eq_tflops()}
     kernels = {}
     for name, (ms, cnt) in prof.items():
         if cnt == 0:
@@ -311,12 +319,15 @@ def main():
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get(args.config, {}).get(dom)
     if dom in flops:
-        roof = {"bound": "alu", "kernel": dom, "achieved": d["tflops"], "peak": peaks[dom], "unit": "TFLOP/s",
+        roof = {"bound": "tensor" if dom == "pair_tc" else "alu", "kernel": dom, "achieved": d["tflops"],
+                "peak": peaks[dom], "unit": "TFLOP/s",
                 "frac": d["frac_of_peak"], "traffic": traffic,
                 "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
                                 "(profiles/ncu_*_summary.txt)",
-                "peak_source": "own DFMA/FFMA microbenchmark (tools/peaks.cu, profiles/peaks_r01.txt); "
-                               "MEASURED_PEAKS.json has no FP64/FP32-SIMT peak",
+                "peak_source": ("MEASURED_PEAKS.json bf16 burst x 0.5 (nominal TF32/BF16) / 3 (3xTF32 MMAs per "
+                                "useful fp32 product)") if dom == "pair_tc" else
+                               ("own DFMA/FFMA microbenchmark (tools/peaks.cu, profiles/peaks_r01.txt); "
+                                "MEASURED_PEAKS.json has no FP64/FP32-SIMT peak"),
                 "algorithmic": "Householder tridiagonalisation 4/3 n^3 flops per (r'+w)^2 Gram"
                 if dom.startswith("eig") else "2 m q w (GEMM) / m w (w+1) (SYRK) flops per pair"}
     else:
