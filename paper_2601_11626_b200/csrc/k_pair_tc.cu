@@ -11,7 +11,7 @@
 // products): fp32-equivalent accuracy, which the parity
 // tolerances need (1xTF32 measured 1.3e-2 relative error).
 //
-// One CTA (4 warps) per pair; thread 0 issues the MMAs, all threads stage the
+// One CTA (8 warps) per pair; thread 0 issues the MMAs, all threads stage the
 // operands (fp32 -> tf32 hi/lo split happens during the global -> smem copy,
 // so the split operands never exist in HBM).  Operands are K-major in the
 // no-swizzle canonical layout with padded strides LBO = 144 B, SBO = 1152 B
@@ -26,7 +26,7 @@
 namespace cmsvd {
 namespace {
 
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;   // 8 warps: 2 per SM sub-partition (latency hiding for the staging)
 constexpr int KT = 32;                  // k elements per stage
 constexpr uint32_t LBO = 144, SBO = 1152;
 constexpr uint32_t kTile = 128 * 144;   // bytes of a 128-row x 32-k operand tile (one of hi/lo)
@@ -112,23 +112,26 @@ __device__ __forceinline__ void stage_kcontig(uint8_t* hi, uint8_t* lo, int rows
 // Lanes over rows (coalesced per column), 4 columns gathered per 16 B store.
 __device__ __forceinline__ void stage_rcontig(uint8_t* hi, uint8_t* mi, uint8_t* lo, const float* __restrict__ src,
                                               int64_t ld, int64_t r0, int64_t rmax, int k0, int kmax) {
-  const int r = threadIdx.x;  // 128 threads = 128 rows
+  const int r = threadIdx.x & 127;          // 128 rows; the two thread halves take alternate k quads
+  const int h = threadIdx.x >> 7;
   const bool rok = (r0 + r) < rmax;
-  float4 v[KT / 4];
+  constexpr int NQ = KT / 4 / (kTcThreads / 128);
+  float4 v[NQ];
 #pragma unroll
-  for (int kq = 0; kq < KT / 4; ++kq) {
-    v[kq] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int t = 0; t < NQ; ++t) {
+    const int kq = h + t * (kTcThreads / 128);
+    v[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int k = k0 + 4 * kq;
     if (rok) {
       const float* p = src + (int64_t)k * ld + r0 + r;
-      if (k + 0 < kmax) v[kq].x = __ldg(p);
-      if (k + 1 < kmax) v[kq].y = __ldg(p + ld);
-      if (k + 2 < kmax) v[kq].z = __ldg(p + 2 * ld);
-      if (k + 3 < kmax) v[kq].w = __ldg(p + 3 * ld);
+      if (k + 0 < kmax) v[t].x = __ldg(p);
+      if (k + 1 < kmax) v[t].y = __ldg(p + ld);
+      if (k + 2 < kmax) v[t].z = __ldg(p + 2 * ld);
+      if (k + 3 < kmax) v[t].w = __ldg(p + 3 * ld);
     }
   }
 #pragma unroll
-  for (int kq = 0; kq < KT / 4; ++kq) st_split4_3(hi, mi, lo, poff(r, 4 * kq), v[kq]);
+  for (int t = 0; t < NQ; ++t) st_split4_3(hi, mi, lo, poff(r, 4 * (h + t * (kTcThreads / 128))), v[t]);
 }
 
 // 6-product (3-way split) MMA sequence for one 32-k stage: hh, hm, mh, hl, mm, lh
@@ -177,6 +180,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   __shared__ uint64_t bar_slot[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int wq = wid & 3;     // TMEM lane quarter of this warp (tcgen05.ld 32x32b: lanes 32*(warp%4)..)
+  const int half = wid >> 2;  // column half [64*half, 64*half+64) handled by this warp in the drains
   const int64_t p = blockIdx.x;
   const int2 pr = pairs[p];
   const BaseDesc b = bd[pr.x];
@@ -205,7 +210,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   // TMEM columns: phase 1 Z block accumulators (two slots) at [0,128) and [128,256), running sum at
   // [256,384); phase 2 R' tile accumulator at [0,128), W' tile contribution at [128,256), sum at [256,384).
   const uint32_t t_z0 = tmem, t_r = tmem, t_w = tmem + 128, t_sum = tmem + 256;
-  const uint32_t lane_off = (uint32_t)(32 * wid) << 16;
+  const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+  const int c_lo = 64 * half, c_hi = min(wp, 64 * half + 64);
   uint32_t ph_stage[2] = {0, 0}, ph_done = 0, ph_slot[2] = {0, 0};
   int used[2] = {0, 0};  // MMAs outstanding on a stage
   auto stage_ptr = [&](int s, int which) { return sm + s * kStage + which * kTile; };
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   // running sum (fp32, round-to-nearest adds) kept in TMEM columns [256, 256+wp)
   bool sum_empty = true;
   auto drain_add = [&](uint32_t tcol) {
-    for (int c = 0; c < wp; c += 32) {
+    for (int c = c_lo; c < c_hi; c += 32) {
       float v[32], acc[32];
       tc::tmem_ld32(tcol + lane_off + c, v);
       if (!sum_empty) tc::tmem_ld32(t_sum + lane_off + c, acc);
@@ -232,9 +238,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
     tc::wait_st();
     sum_empty = false;
   };
-  // write the running sum (rows 32*wid + lane, columns < ncol) to global through a callback
+  // write the running sum (rows 32*wq + lane, this warp's column half) to global through a callback
   auto drain_sum = [&](auto&& store) {
-    for (int c = 0; c < wp; c += 32) {
+    for (int c = c_lo; c < c_hi; c += 32) {
       float v[32];
       if (sum_empty) {
 #pragma unroll
@@ -290,7 +296,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
       drain_add(t_z0 + 128 * ls);
     }
     for (int s = 0; s < 2; ++s) acquire(s);
-    const int ar = 32 * wid + lane;
+    const int ar = 32 * wq + lane;
     drain_sum([&](int j, float x) {
       if (ar < q && j < w) Zg[(int64_t)j * QMAX + ar] = x;
     });
@@ -332,12 +338,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
     ph_done ^= 1;
     for (int s = 0; s < 2; ++s) acquire(s);
     tc::fence_after();
-    // epilogue: rows r = 32*wid + lane of this tile -> R' into warp wid's chunk buffer
-    // chunk buffer (hi, lo) of warp wid: operand with rows = b (128), k = r_local (32)
-    uint8_t* chi = sm + (uint32_t)wid * 2 * kTile;
+    // epilogue: rows r = 32*wq + lane of this tile -> R' into chunk buffer wq (columns of this warp's half)
+    // chunk buffer (hi, lo) wq: operand with rows = b (128), k = r_local (32)
+    uint8_t* chi = sm + (uint32_t)wq * 2 * kTile;
     uint8_t* clo = chi + kTile;
-    const int64_t grow = m0 + 32 * wid + lane;
-    for (int c0 = 0; c0 < 128; c0 += 32) {
+    const int64_t grow = m0 + 32 * wq + lane;
+    for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
       float v[32];
       if (c0 < wp) {
         if (q > 0) {
@@ -377,9 +383,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
     drain_add(t_w);          // this tile's W' contribution -> fp32 registers (round-to-nearest)
     tc::fence_before();
   }
-  // ---------------- W' (rows b = 32*wid + lane) from the running sum ----------------
+  // ---------------- W' (rows b = 32*wq + lane) from the running sum ----------------
   if (w > 0) {
-    const int br = 32 * wid + lane;
+    const int br = 32 * wq + lane;
     drain_sum([&](int j, float x) {
       if (br < w && j < w) Wg[(int64_t)j * WMAX + br] = (double)x;
     });
