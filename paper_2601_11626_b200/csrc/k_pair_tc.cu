@@ -26,7 +26,7 @@
 namespace cmsvd {
 namespace {
 
-constexpr int kTcThreads = 256;   // 8 warps: 2 per SM sub-partition (latency hiding for the staging)
+constexpr int kTcThreads = 512;   // 16 warps: 4 per SM sub-partition (latency hiding for the staging)
 constexpr int KT = 32;                  // k elements per stage
 constexpr uint32_t LBO = 144, SBO = 1152;
 constexpr uint32_t kTile = 128 * 144;   // bytes of a 128-row x 32-k operand tile (one of hi/lo)
@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int wq = wid & 3;     // TMEM lane quarter of this warp (tcgen05.ld 32x32b: lanes 32*(warp%4)..)
-  const int half = wid >> 2;  // column half [64*half, 64*half+64) handled by this warp in the drains
+  constexpr int kGroups = kTcThreads / 128;       // warps sharing a TMEM lane quarter
+  constexpr int kColW = 128 / kGroups;            // columns per warp in the drains / epilogue
+  const int half = wid >> 2;  // column group [kColW*half, kColW*half+kColW) handled by this warp in the drains
   const int64_t p = blockIdx.x;
   const int2 pr = pairs[p];
   const BaseDesc b = bd[pr.x];
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   // [256,384); phase 2 R' tile accumulator at [0,128), W' tile contribution at [128,256), sum at [256,384).
   const uint32_t t_z0 = tmem, t_r = tmem, t_w = tmem + 128, t_sum = tmem + 256;
   const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
-  const int c_lo = 64 * half, c_hi = min(wp, 64 * half + 64);
+  const int c_lo = kColW * half, c_hi = min(wp, kColW * half + kColW);
   uint32_t ph_stage[2] = {0, 0}, ph_done = 0, ph_slot[2] = {0, 0};
   int used[2] = {0, 0};  // MMAs outstanding on a stage
   auto stage_ptr = [&](int s, int which) { return sm + s * kStage + which * kTile; };
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
     uint8_t* chi = sm + (uint32_t)wq * 2 * kTile;
     uint8_t* clo = chi + kTile;
     const int64_t grow = m0 + 32 * wq + lane;
-    for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
+    for (int c0 = kColW * half; c0 < kColW * half + kColW; c0 += 32) {
       float v[32];
       if (c0 < wp) {
         if (q > 0) {
