@@ -882,16 +882,34 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
             for (; i >= l; --i) {
               double f = sn * ee[i];
               const double b = cs * ee[i];
-              r = hypot(f, g);
-              ee[i + 1] = r;
-              if (r == 0.0) {
-                dd[i + 1] -= pp;
-                ee[m] = 0.0;
-                underflow = true;
-                break;
+              // r = hypot(f, g), sn = f / r, cs = g / r: one MUFU.RSQ64H + Newton steps instead of the
+              // IEEE hypot and two divisions on this sequential chain; scaled fallback near under/overflow
+              const double x2 = fma(f, f, g * g);
+              if (x2 > 1e-280 && x2 < 1e280) {
+                double y;
+                asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x2));
+                double hh = 0.5 * x2 * y;
+                double rr = fma(-hh, y, 0.5);
+                y = fma(y, rr, y);
+                hh = 0.5 * x2 * y;
+                rr = fma(-hh, y, 0.5);
+                y = fma(y, rr, y);
+                r = x2 * y;
+                ee[i + 1] = r;
+                sn = f * y;
+                cs = g * y;
+              } else {
+                r = hypot(f, g);
+                ee[i + 1] = r;
+                if (r == 0.0) {
+                  dd[i + 1] -= pp;
+                  ee[m] = 0.0;
+                  underflow = true;
+                  break;
+                }
+                sn = f / r;
+                cs = g / r;
               }
-              sn = f / r;
-              cs = g / r;
               g = dd[i + 1] - pp;
               r = (dd[i] - g) * sn + 2.0 * cs * b;
               pp = sn * r;
