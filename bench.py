@@ -89,6 +89,17 @@ def workload(name: str, rank: int):
     return col
 
 
+def max_over_ranks(dist, x: float, dev=None) -> float:
+    """Max of a host scalar over all ranks (timings: the job is as slow as its slowest rank)."""
+    if not dist:
+        return x
+    import torch
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws <= 1:
@@ -278,10 +289,7 @@ def main():
     torch.cuda.synchronize()
     times = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(times)
-    if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(dist, total_ms, dev)
     units = P * args.steps * ws
     value = units / (total_ms / 1e3)
 
@@ -362,10 +370,7 @@ def main():
             ctx2.block_spectra(r)
             res_h = ctx2.pair_errors(pairs_h)
         t_e2e = time.perf_counter() - t0
-        if dist:
-            t = torch.tensor([t_e2e], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = float(t.item())
+        t_e2e = max_over_ranks(dist, t_e2e, dev)
         h2d = col.blocks.nbytes + pairs_h.nbytes
         d2h = res_h["err2"].nbytes + res_h["total"].nbytes + res_h["sigma_tilde"].nbytes + res_h["mu"].nbytes + \
             col.N * (8 + 4 * r + 4)

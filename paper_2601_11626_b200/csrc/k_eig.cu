@@ -863,12 +863,22 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
   for (int l = 0; l < n; ++l) {
     int iter = 0;
     while (true) {
-      if (tid == 0) {
-        int m = l;
-        for (; m < n - 1; ++m) {
-          const double dsum = fabs(dd[m]) + fabs(dd[m + 1]);
-          if (fabs(ee[m]) <= 2.220446049250313e-16 * dsum || fabs(ee[m]) <= defl_abs) break;
+      // deflation search by warp 0 (32 candidates per ballot), the sweep by its lane 0
+      int mq = n - 1;
+      if (wid == 0) {
+        for (int base = l; base < n - 1; base += 32) {
+          const int mm = base + lane;
+          bool neg = false;
+          if (mm < n - 1) {
+            const double dsum = fabs(dd[mm]) + fabs(dd[mm + 1]);
+            neg = fabs(ee[mm]) <= 2.220446049250313e-16 * dsum || fabs(ee[mm]) <= defl_abs;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, neg);
+          if (bal) { mq = base + __ffs(bal) - 1; break; }
         }
+      }
+      if (tid == 0) {
+        const int m = mq;
         s_m = m;
         if (m != l) {
           if (iter >= max_iter) { s_fail = 1; s_m = l; }
@@ -879,9 +889,14 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
             double sn = 1.0, cs = 1.0, pp = 0.0;
             int i = m - 1;
             bool underflow = false;
+            // every d/e value read below is an original one (the sweep writes ee[i+1], dd[i+1] behind the
+            // read front), so the next iteration's operands are prefetched into registers
+            double e_i = ee[i], d_i1 = dd[i + 1], d_i = dd[i];
             for (; i >= l; --i) {
-              double f = sn * ee[i];
-              const double b = cs * ee[i];
+              const double e_n = (i > l) ? ee[i - 1] : 0.0;
+              const double d_n = (i > l) ? dd[i - 1] : 0.0;
+              double f = sn * e_i;
+              const double b = cs * e_i;
               // r = hypot(f, g), sn = f / r, cs = g / r: one MUFU.RSQ64H + Newton steps instead of the
               // IEEE hypot and two divisions on this sequential chain; scaled fallback near under/overflow
               const double x2 = fma(f, f, g * g);
@@ -902,7 +917,7 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
                 r = hypot(f, g);
                 ee[i + 1] = r;
                 if (r == 0.0) {
-                  dd[i + 1] -= pp;
+                  dd[i + 1] = d_i1 - pp;
                   ee[m] = 0.0;
                   underflow = true;
                   break;
@@ -910,13 +925,16 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
                 sn = f / r;
                 cs = g / r;
               }
-              g = dd[i + 1] - pp;
-              r = (dd[i] - g) * sn + 2.0 * cs * b;
+              g = d_i1 - pp;
+              r = (d_i - g) * sn + 2.0 * cs * b;
               pp = sn * r;
               dd[i + 1] = g + pp;
               g = cs * r - b;
               rc[i] = cs;
               rs[i] = sn;
+              e_i = e_n;
+              d_i1 = d_i;
+              d_i = d_n;
             }
             // rotations actually generated: indices i_stop+1 .. m-1 (i_stop = i)
             s_l = underflow ? i + 1 : l;   // lowest rotation index applied
@@ -936,12 +954,17 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
       // apply rotations i = m-1 .. lo_i to columns (i, i+1) of Z: each thread owns rows
       for (int row = tid; row < n; row += kTriThreads) {
         double* z = A + row;
+        // the rotated column i is carried in a register to the next rotation; loads run one ahead
+        double f = z[(int64_t)m * ldz];
+        double zi = z[(int64_t)(m - 1) * ldz];
         for (int i = m - 1; i >= lo_i; --i) {
-          const double f = z[(int64_t)(i + 1) * ldz];
-          const double zi = z[(int64_t)i * ldz];
-          z[(int64_t)(i + 1) * ldz] = rs[i] * zi + rc[i] * f;
-          z[(int64_t)i * ldz] = rc[i] * zi - rs[i] * f;
+          const double zn = (i > lo_i) ? z[(int64_t)(i - 1) * ldz] : 0.0;
+          const double c_ = rc[i], s_ = rs[i];
+          z[(int64_t)(i + 1) * ldz] = s_ * zi + c_ * f;
+          f = c_ * zi - s_ * f;
+          zi = zn;
         }
+        z[(int64_t)lo_i * ldz] = f;
       }
       __syncthreads();
       ++iter;

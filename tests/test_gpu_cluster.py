@@ -155,3 +155,17 @@ def test_random_collections_replay(cm, seed):
                 if len(c) > 1 and alg == oc.RESIDUAL_ALG:
                     ex = oracle.exact_groups(sp, [c], 4)[0]
                     assert np.sqrt(ex / tot) <= 0.1 + 1e-6
+
+
+@pytest.mark.parametrize("alg", [oc.RESIDUAL_ALG, oc.APPROX])
+@pytest.mark.parametrize("knn", [2, 4])
+def test_knn_window_matches_oracle(cm, alg, knn):
+    """kNN window (skip-and-continue over the knn best-ranked candidates, A10) on config 1 and a
+    reduced config 5 (tall-thin 2048 x 64, 32 hidden groups): identical partitions and
+    evaluation counts (keys and merges are well separated on these inputs)."""
+    for col, eps in [(synth.config1(), 0.05), (synth.config5(N=48, r=16), 0.1)]:
+        sp = oracle.block_spectra(col.blocks)
+        g = run_gpu(cm, col.blocks, col.r, alg, eps, oc.SORT_RESIDUAL, knn=knn)
+        o = oc.cluster(sp, alg, col.r, eps, oc.SORT_RESIDUAL, knn=knn)
+        assert g["clusters"] == o.clusters, (col.name, knn)
+        assert g["n_evals"] == o.n_evals
