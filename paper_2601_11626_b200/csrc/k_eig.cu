@@ -426,7 +426,8 @@ template <int S, int C, int KC, bool UPD, bool MV>
 __device__ __forceinline__ void rr_pass(double (&a)[S][C], const int lane, const int wid,
                                         const double* __restrict__ v, const double* __restrict__ w,
                                         const double* __restrict__ u, double* __restrict__ part,
-                                        double* __restrict__ cs, double* __restrict__ red) {
+                                        double* __restrict__ cs, double* __restrict__ red, const int pub_j,
+                                        double* __restrict__ colbuf) {
   constexpr int NR = 32 * S;
   constexpr int CL = 2 * (S - 1);
   constexpr int C2 = rr_pow2(CL);
@@ -460,6 +461,11 @@ __device__ __forceinline__ void rr_pass(double (&a)[S][C], const int lane, const
           if (rr_lower(s, c)) pc[c] = fma(x, ui[s], pc[c]);
         }
       }
+    if (j == pub_j) {  // this warp owns the column the next reflector is built from: publish it
+#pragma unroll
+      for (int s = S0; s < S; ++s)
+        if (rr_present(s, c)) colbuf[lane + 32 * s] = a[s][c];
+    }
     if (MV && c < CL) dd = fma(uj, pc[c], dd);
   }
   if (!MV) return;
@@ -497,10 +503,10 @@ __device__ __forceinline__ void rr_pass(double (&a)[S][C], const int lane, const
 template <int S, int C, bool UPD, bool MV>
 __device__ __forceinline__ void rr_pass_kc(int kc, double (&a)[S][C], const int lane, const int wid,
                                            const double* v, const double* w, const double* u, double* part,
-                                           double* cs, double* red) {
-#define RR_CASE(K)                                                                     \
-  case K:                                                                              \
-    if (K < C) rr_pass<S, C, (K < C ? K : 0), UPD, MV>(a, lane, wid, v, w, u, part, cs, red); \
+                                           double* cs, double* red, int pub_j, double* colbuf) {
+#define RR_CASE(K)                                                                                           \
+  case K:                                                                                                    \
+    if (K < C) rr_pass<S, C, (K < C ? K : 0), UPD, MV>(a, lane, wid, v, w, u, part, cs, red, pub_j, colbuf); \
     break;
   switch (kc) {
     RR_CASE(0) RR_CASE(1) RR_CASE(2) RR_CASE(3) RR_CASE(4) RR_CASE(5) RR_CASE(6) RR_CASE(7)
@@ -508,6 +514,18 @@ __device__ __forceinline__ void rr_pass_kc(int kc, double (&a)[S][C], const int 
     default: break;
   }
 #undef RR_CASE
+}
+
+// fixed-order pairwise sum of 16 values x[q * stride]
+__device__ __forceinline__ double tree16(const double* x, int stride) {
+  double t[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) t[q] = x[q * stride] + x[(q + 8) * stride];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) t[q] += t[q + 4];
+  t[0] += t[2];
+  t[1] += t[3];
+  return t[0] + t[1];
 }
 
 template <int S, int C>
@@ -536,8 +554,8 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
   constexpr int NR = 32 * S;
   constexpr int CL = 2 * (S - 1);
   static_assert(C == 2 * S && C <= 16, "column chunks");
-  __shared__ double vb[2][NR], wb[NR], part[kRRWarps * NR], cs[NR], ds[NR], e2s[NR];
-  __shared__ double red[kRRWarps], s_tau[2];
+  __shared__ double vb[2][NR], wb[NR], part[kRRWarps * NR], cs[NR], ds[NR], e2s[NR], colbuf[NR];
+  __shared__ double red[kRRWarps], red2[S], s_tau[2], s_alpha, s_dk;
   const int p = blockIdx.x;
   const int n = ns[p];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -618,48 +636,54 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
       reflector(0, x);
     }
     __syncthreads();
-    if (s_tau[0] != 0.0) rr_pass<S, C, 0, false, true>(a, lane, wid, nullptr, nullptr, vb[0], part, cs, red);
+    // products with v_0; publish column 1 (reflector 1 is formed in the row phase of step 0)
+    if (s_tau[0] != 0.0) rr_pass<S, C, 0, false, true>(a, lane, wid, nullptr, nullptr, vb[0], part, cs, red, 1, colbuf);
+    else rr_pass<S, C, 0, false, false>(a, lane, wid, nullptr, nullptr, nullptr, part, cs, red, 1, colbuf);
     for (int k = 0; k + 2 < n; ++k) {
       const double* v = vb[k & 1];
       const double tau = s_tau[k & 1];
-      RR_T(0, wid == 1);
-      __syncthreads();  // B2: part, cs, red of A v_k
-      RR_T(1, wid == 1);
-      if (tid < NR) {
-        double vta = 0.0;
-#pragma unroll
-        for (int q = 0; q < kRRWarps; q += 4) vta += (red[q] + red[q + 1]) + (red[q + 2] + red[q + 3]);
-        const double Kc = 0.5 * tau * tau * vta;
-        double pt = cs[tid];
-#pragma unroll
-        for (int q = 0; q < kRRWarps; q += 4)
-          pt += (part[q * NR + tid] + part[(q + 1) * NR + tid]) + (part[(q + 2) * NR + tid] + part[(q + 3) * NR + tid]);
-        wb[tid] = (tid > k && tid < n && tau != 0.0) ? fma(tau, pt, -Kc * v[tid]) : 0.0;
-      }
       const int k1 = k + 1;
       const bool more = k1 + 2 < n;  // reflector k+1 exists
-      const int owner = k1 & 15;
-      if (more) {
-        const int nb = 32 * (S + (owner >= S ? 1 : 0));
-        if (wid == owner) {
-          RR_T(2, true);
-          asm volatile("bar.sync 1, %0;" ::"r"(nb) : "memory");  // the w rows (warps 0..S-1) only
-          RR_T(3, true);
-          double x[S];
-          rr_column<S, C>(k1 >> 4, a, x);
-          if (tau != 0.0) {  // updated column k+1, same arithmetic as the fused pass below
-            const double wk1 = wb[k1], vk1 = v[k1];
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-              const int i = lane + 32 * s;
-              x[s] = fma(-v[i], wk1, fma(-wb[i], vk1, x[s]));
-            }
+      RR_T(0, wid == 1);
+      __syncthreads();  // B2: part, cs, red of A v_k; colbuf = column k+1 (before step k's update)
+      RR_T(1, wid == 1);
+      // Row phase (warps 0..S-1, thread t = row t): w_t, and -- instead of a single owner warp -- the
+      // updated column k+1 (same fma order as the register update), its norm and reflector k+1.
+      if (tid < NR) {
+        const double Kc = 0.5 * tau * tau * tree16(red, 1);
+        const double pt = cs[tid] + tree16(&part[tid], NR);
+        const double wt = (tid > k && tid < n && tau != 0.0) ? fma(tau, pt, -Kc * v[tid]) : 0.0;
+        wb[tid] = wt;
+        if (more) {
+          double y = colbuf[tid];
+          if (tau != 0.0) {
+            const double pk1 = cs[k1] + tree16(&part[k1], NR);
+            const double wk1 = fma(tau, pk1, -Kc * v[k1]);
+            y = fma(-v[tid], wk1, fma(-wt, v[k1], y));
           }
-          RR_T(4, true);
-          reflector(k1, x);
-          RR_T(5, true);
-        } else if (wid < S) {
-          asm volatile("bar.arrive 1, %0;" ::"r"(nb) : "memory");
+          double sq = (tid > k1 + 1 && tid < n) ? y * y : 0.0;
+          sq = warp_sum(sq);
+          if (lane == 0) red2[wid] = sq;
+          if (tid == k1 + 1) s_alpha = y;
+          if (tid == k1) s_dk = y;
+          asm volatile("bar.sync 1, %0;" ::"r"(NR) : "memory");  // row warps only
+          double sg = 0.0;
+#pragma unroll
+          for (int q = 0; q < S; ++q) sg += red2[q];
+          const double al = s_alpha;
+          double tau1, scale, ee;
+          if (sg == 0.0) {
+            tau1 = 0.0; scale = 0.0; ee = al * al;
+          } else {
+            const double x2 = fma(al, al, sg);
+            const double xn = x2 * rsqrt_nr(x2);
+            const double beta = al >= 0.0 ? -xn : xn;
+            tau1 = (beta - al) * rcp_nr(beta);
+            scale = rcp_nr(al - beta);
+            ee = beta * beta;
+          }
+          if (tid == 0) { e2s[k1] = ee; ds[k1] = s_dk; s_tau[k1 & 1] = tau1; }
+          vb[k1 & 1][tid] = (tid == k1 + 1) ? 1.0 : ((tid > k1 + 1 && tid < n) ? y * scale : 0.0);
         }
       }
       RR_T(6, wid == 1);
@@ -667,9 +691,11 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
       RR_T(7, wid == 1);
       const bool mv = more && s_tau[k1 & 1] != 0.0;
       const double* u = vb[k1 & 1];
-      if (tau != 0.0 && mv) rr_pass_kc<S, C, true, true>(k >> 4, a, lane, wid, v, wb, u, part, cs, red);
-      else if (tau != 0.0) rr_pass<S, C, 0, true, false>(a, lane, wid, v, wb, nullptr, part, cs, red);
-      else if (mv) rr_pass<S, C, 0, false, true>(a, lane, wid, nullptr, nullptr, u, part, cs, red);
+      const int pub = (k + 3 < n) ? k + 2 : -1;  // column of reflector k+2
+      if (tau != 0.0 && mv) rr_pass_kc<S, C, true, true>(k >> 4, a, lane, wid, v, wb, u, part, cs, red, pub, colbuf);
+      else if (tau != 0.0) rr_pass<S, C, 0, true, false>(a, lane, wid, v, wb, nullptr, part, cs, red, pub, colbuf);
+      else if (mv) rr_pass<S, C, 0, false, true>(a, lane, wid, nullptr, nullptr, u, part, cs, red, pub, colbuf);
+      else rr_pass<S, C, 0, false, false>(a, lane, wid, nullptr, nullptr, nullptr, part, cs, red, pub, colbuf);
     }
   }
   __syncthreads();
