@@ -1051,7 +1051,7 @@ cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_i
   // in place in global memory (G is destroyed); batches sized to stay L2-resident
   cudaError_t e = cudaFuncSetAttribute(k_syev_ql<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(nprob, (int64_t)(96 << 20) / ((int64_t)nmax * nmax * 8)));
+  const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(nprob, (int64_t)c.gl_batch_mb * (1 << 20) / ((int64_t)nmax * nmax * 8)));
   for (int p0 = 0; p0 < nprob; p0 += batch) {
     const int nb = std::min(batch, nprob - p0);
     k_syev_ql<true><<<nb, kTriThreads, smem, c.stream>>>(G + (int64_t)p0 * stride_in, ld_in, stride_in, d_ns + p0,
@@ -1104,7 +1104,7 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
     // in place in global memory (G is destroyed); batches sized to stay L2-resident
     e = cudaFuncSetAttribute(k_tridiag<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(nprob, (int64_t)(96 << 20) / ((int64_t)nmax * nmax * 8)));
+    const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(nprob, (int64_t)c.gl_batch_mb * (1 << 20) / ((int64_t)nmax * nmax * 8)));
     for (int p0 = 0; p0 < nprob; p0 += batch) {
       const int nb = std::min(batch, nprob - p0);
       k_tridiag<true><<<nb, kTriThreads, smem, c.stream>>>(

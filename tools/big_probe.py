@@ -27,6 +27,15 @@ with cm.Context(0, torch.cuda.current_stream().cuda_stream) as ctx:
         t = time.time()
         E, sig, rank = ctx.block_spectra(col.r)
         print(f"spectra {time.time() - t:.3f}s", flush=True)
+    ctx.profile(True)
+    ctx.register(blocks)
+    ctx.block_spectra(col.r)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    ems = prof["energy"][0]
+    nbytes = col.blocks.nbytes
+    print(f"S1 energy kernel: {ems:.3f} ms for {nbytes / 1e9:.2f} GB = {nbytes / (ems * 1e-3) / 1e9:.0f} GB/s; "
+          f"S2 profile {prof}", flush=True)
     for i in [0, col.N - 1]:
         a = col.blocks[i].T.astype(np.float64)
         lam = np.linalg.eigvalsh(a @ a.T)[::-1][:col.r]

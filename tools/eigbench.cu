@@ -26,6 +26,7 @@ int main(int argc, char** argv) {
   double *ev, *tr; int* cnt;
   cudaMalloc(&ev, 8 * (size_t)P * kw); cudaMalloc(&tr, 8 * P); cudaMalloc(&cnt, 4 * P);
   Ctx c; c.stream = 0;
+  if (getenv("GLMB")) c.gl_batch_mb = atoi(getenv("GLMB"));
   double* scr; cudaMalloc(&scr, tridiag_scratch_bytes(P, n));
   std::vector<double> evs[2];
   std::vector<double> trs[2];
