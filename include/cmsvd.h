@@ -118,9 +118,14 @@ cmsvd_status cmsvd_register(cmsvd_ctx ctx, int64_t m, int32_t count, const int32
  *   energy[count]   fp64 ||A_i||_F^2
  *   sigma[count*r]  fp32 sigma_1..r(A_i), non-increasing, zero-padded past min(m, n_i)
  *   rank_out[count] numerical rank under tau.
+ * Blocks with n_i <= 512 columns (n_i <= m) take the exact fp64 Gram
+ * eigendecomposition.  Blocks wider than 512 columns (square/wide weight-like
+ * blocks, n_i >= m) follow reading A22: top min(m, 2r, 512)
+ * triplets by subspace iteration, range taken as R^m, rank_out = min(m, n_i).
  * Errors: CMSVD_E_STATE (no collection), CMSVD_E_ARG (r < 1), CMSVD_E_SHAPE
- * (a block shape this build does not support: n_i > 256 with n_i <= m, or
- * n_i > m), CMSVD_E_NOCONV, CMSVD_E_CUDA, CMSVD_E_NOMEM. */
+ * (unsupported shapes: m < n_i <= 512; 512 < n_i < m; a collection mixing
+ * blocks wider than 512 columns with narrower ones; r > 512 on wide blocks),
+ * CMSVD_E_NOCONV, CMSVD_E_CUDA, CMSVD_E_NOMEM. */
 cmsvd_status cmsvd_block_spectra(cmsvd_ctx ctx, int32_t r, double* energy, float* sigma, int32_t* rank_out);
 
 /* Evaluate P >= 0 candidate merges M = [A_base, F_app] (S3-S9).
@@ -144,6 +149,23 @@ cmsvd_status cmsvd_block_spectra(cmsvd_ctx ctx, int32_t r, double* energy, float
 cmsvd_status cmsvd_pair_errors(cmsvd_ctx ctx, const int32_t* pairs, int64_t P, int32_t r, uint32_t kinds,
                                int operand, int where, double* err2, double* total, float* sigma_tilde,
                                float* mu);
+
+/* Tighter certified variants BEYOND THE PAPER, for the
+ * same candidate pairs / operand / where conventions as cmsvd_pair_errors:
+ *   err2x[2p + 0] residual bound with the tracked top-r basis U_r of the base
+ *                 instead of its full numerical range (reading A4: the
+ *                 projector U_r U_r^T + W, W inside range(I - U_r U_r^T),
+ *                 carries Thm 2's partial-sum argument);
+ *                 mu = top-r of sigma(A_base) U sigma((I - U_r U_r^T) F_app);
+ *   err2x[2p + 1] per-index Weyl bound E_i + E_j - sum_{l<=r} max(sigma_l(A_i),
+ *                 sigma_l(F_j))^2 (reading A8, from sigma_l(M) >= sigma_l(A_k),
+ *                 PAPER.md:1530-1533);
+ *   total[p]      E_base + E_app.
+ * Both are >= the exact error and <= the paper's residual / Weyl values
+ * (chain exact <= incremental <= residual(U_r) <= residual(full) <= Weyl).
+ * Errors as cmsvd_pair_errors. */
+cmsvd_status cmsvd_pair_errors_tight(cmsvd_ctx ctx, const int32_t* pairs, int64_t P, int32_t r, int operand,
+                                     int where, double* err2x, double* total);
 
 /* Greedy clustering (Appendix E). */
 enum { CMSVD_ALG_MAX_NORM = 0, CMSVD_ALG_RESIDUAL = 1, CMSVD_ALG_APPROX = 2 };

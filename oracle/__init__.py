@@ -62,6 +62,9 @@ def lib():
         L.or_pair_errors.restype = ctypes.c_int
         L.or_pair_errors.argtypes = [i64, ctypes.c_int32, ip, pp, dp, pp, pp, ip, ip, i64,
                                      ctypes.c_int32, ctypes.c_uint32, ctypes.c_int, dp, dp, dp, dp]
+        L.or_pair_errors_tight.restype = ctypes.c_int
+        L.or_pair_errors_tight.argtypes = [i64, ctypes.c_int32, ip, pp, dp, pp, pp, ip, ip, i64,
+                                           ctypes.c_int32, ctypes.c_int, dp, dp]
         L.or_block_svds.restype = ctypes.c_int
         L.or_block_svds.argtypes = [i64, ctypes.c_int32, ip, pp, pp, pp]
         L.or_exact_groups.restype = ctypes.c_int
@@ -212,6 +215,22 @@ def pair_errors(spec: Spectra, pairs, r: int, kinds: int = 7, operand: int = RAW
     if status:
         raise RuntimeError(f"oracle pair evaluation failed (status {status})")
     return PairResult(err2, total, st_, mu)
+
+
+def pair_errors_tight(spec: Spectra, pairs, r: int, operand: int = RAW):
+    """Beyond the paper: (P, 2) [residual bound with the tracked
+    basis U_r (A4), per-index Weyl bound (A8)] and the totals.  See oracle.c
+    or_pair_errors_tight."""
+    pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+    P = pairs.shape[0]
+    err2x = np.zeros((P, 2))
+    total = np.zeros(P)
+    st = lib().or_pair_errors_tight(spec.m, len(spec.A), _ip(spec.n), _ptrs(spec.A), _dp(spec.E),
+                                    _ptrs(spec.sig), _ptrs(spec.U), _ip(spec.rank), _ip(pairs), P, r,
+                                    operand, _dp(err2x), _dp(total))
+    if st:
+        raise RuntimeError(f"oracle tight pair evaluation failed (status {st})")
+    return err2x, total
 
 
 def exact_groups(spec: Spectra, groups, r: int) -> np.ndarray:

@@ -318,10 +318,19 @@ static double pair_weyl(const or_collection* c, int32_t i, int32_t j, int32_t r)
  * mu = top-r of the multiset sigma(A_i) U sigma(R) (proof Step 5,
  * PAPER.md:1694-1706), err^2 = E_i + E_j - sum_{l<=r} mu_l^2.  Only the
  * partial-sum form of Thm 2 is used (A1). */
+static int pair_residual_q(const or_collection* c, int32_t i, const double* F, int64_t w,
+                           double Ej, int32_t r, int64_t q, double* err2, double* mu_out);
 static int pair_residual(const or_collection* c, int32_t i, const double* F, int64_t w,
                          double Ej, int32_t r, double* err2, double* mu_out) {
+  return pair_residual_q(c, i, F, w, Ej, r, c->rank[i], err2, mu_out);
+}
+
+/* Thm 2 residual with the first q left singular vectors of the base as the
+ * projection basis: q = rank (paper-literal, A4) or q = min(r, rank) (the
+ * tracked-basis variant beyond the paper, N3). */
+static int pair_residual_q(const or_collection* c, int32_t i, const double* F, int64_t w,
+                           double Ej, int32_t r, int64_t q, double* err2, double* mu_out) {
   int64_t m = c->m;
-  int64_t q = c->rank[i];
   const double* Q = c->U[i];
   double* R = (double*)malloc(sizeof(double) * m * w);
   memcpy(R, F, sizeof(double) * m * w);
@@ -428,6 +437,45 @@ int or_pair_errors(int64_t m, int32_t count, const int32_t* n, const double* con
       err2[3 * p + 2] = clamp_err2(e, tot);
       if (st) status = st;
     }
+    free(F);
+  }
+  return status;
+}
+
+/* Beyond the paper: err2x[2p] = residual bound with the tracked
+ * basis U_r (q = min(r, rank_i), reading A4), err2x[2p+1] = per-index Weyl
+ * bound E_i + E_j - sum_{l<=r} max(sigma_l(A_i), sigma_l(F_j))^2 (reading A8,
+ * from sigma_l(M) >= sigma_l(A_k)), both clamped. */
+int or_pair_errors_tight(int64_t m, int32_t count, const int32_t* n, const double* const* A,
+                         const double* E, const double* const* sig, const double* const* U,
+                         const int32_t* rank, const int32_t* pairs, int64_t P, int32_t r,
+                         int operand, double* err2x, double* total) {
+  or_collection c = {m, count, n, A, E, sig, U, rank};
+  int status = OR_OK;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t p = 0; p < P; ++p) {
+    int32_t i = pairs[2 * p], j = pairs[2 * p + 1];
+    int64_t w = 0;
+    double* F = make_operand(&c, j, r, operand, &w);
+    double Ej = E[j];
+    double tot = E[i] + Ej;
+    total[p] = tot;
+    int64_t q = rank[i] < r ? rank[i] : r;
+    double e;
+    int st = pair_residual_q(&c, i, F, w, Ej, r, q, &e, NULL);
+    err2x[2 * p] = clamp_err2(e, tot);
+    if (st) status = st;
+    /* per-index Weyl on the two blocks' spectra (as Eq. 5's implementation, pair_weyl, for either operand) */
+    int64_t ki = m < n[i] ? m : n[i];
+    int64_t kj = m < n[j] ? m : n[j];
+    double top = 0.0;
+    for (int32_t l = 0; l < r; ++l) {
+      double si = l < ki ? sig[i][l] : 0.0;
+      double sj = l < kj ? sig[j][l] : 0.0;
+      double mx = si > sj ? si : sj;
+      top += mx * mx;
+    }
+    err2x[2 * p + 1] = clamp_err2(E[i] + Ej - top, tot);
     free(F);
   }
   return status;

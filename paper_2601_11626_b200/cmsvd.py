@@ -25,7 +25,7 @@ ALG_MAX_NORM, ALG_RESIDUAL, ALG_APPROX = 0, 1, 2
 SORT_FROBENIUS, SORT_RESIDUAL = 0, 1
 
 EXPORTS = ["cmsvd_status_string", "cmsvd_last_error", "cmsvd_version", "cmsvd_create", "cmsvd_destroy",
-           "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_cluster", "cmsvd_launch_count",
+           "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_pair_errors_tight", "cmsvd_cluster", "cmsvd_launch_count",
            "cmsvd_profile_enable", "cmsvd_profile_read"]
 
 
@@ -69,6 +69,8 @@ def load(path: str = LIB_PATH):
     L.cmsvd_pair_errors.restype = ctypes.c_int
     L.cmsvd_pair_errors.argtypes = [vp, vp, i64, i32, u32, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]
     L.cmsvd_cluster.restype = ctypes.c_int
+    L.cmsvd_pair_errors_tight.argtypes = [vp, vp, i64, i32, ctypes.c_int, ctypes.c_int, vp, vp]
+    L.cmsvd_pair_errors_tight.restype = ctypes.c_int
     L.cmsvd_cluster.argtypes = [vp, ctypes.POINTER(ClusterOpts), vp, vp, vp, vp, vp, vp]
     L.cmsvd_launch_count.restype = i64
     L.cmsvd_launch_count.argtypes = [vp]
@@ -226,6 +228,19 @@ class Context:
         self._check(self._L.cmsvd_pair_errors(self._h, _ptr(pairs), P, r, kinds, operand, HOST, _ptr(err2),
                                               _ptr(total), _ptr(st), _ptr(mu)))
         return {"err2": err2, "total": total, "sigma_tilde": st, "mu": mu}
+
+    # -- cmsvd_pair_errors_tight (N3, beyond the paper) -------------------
+    def pair_errors_tight(self, pairs, r: int | None = None, operand: int = RAW):
+        """Residual bound with the U_r basis and per-index Weyl bound (host path):
+        returns {"err2x": (P, 2) f64 [residual_Ur, weyl_index], "total": (P,) f64}."""
+        r = self.r if r is None else r
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        P = pairs.shape[0]
+        err2x = np.zeros((P, 2))
+        total = np.zeros(P)
+        self._check(self._L.cmsvd_pair_errors_tight(self._h, _ptr(pairs), P, r, operand, HOST, _ptr(err2x),
+                                                    _ptr(total)))
+        return {"err2x": err2x, "total": total}
 
     # -- cmsvd_cluster ---------------------------------------------------
     def cluster(self, algorithm: int, eps: float, r: int | None = None, sort: int = SORT_FROBENIUS,

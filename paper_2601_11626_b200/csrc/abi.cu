@@ -134,6 +134,18 @@ cmsvd_status cmsvd_pair_errors(cmsvd_ctx ctx, const int32_t* pairs, int64_t P, i
   }
 }
 
+cmsvd_status cmsvd_pair_errors_tight(cmsvd_ctx ctx, const int32_t* pairs, int64_t P, int32_t r, int operand,
+                                     int where, double* err2x, double* total) {
+  GUARD_CTX(ctx);
+  try {
+    return do_pair_errors_tight(c, pairs, P, r, operand, where, err2x, total);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "pair_errors_tight: host allocation failed");
+  } catch (...) {
+    return fail(c, CMSVD_E_ARG, "pair_errors_tight: unexpected exception");
+  }
+}
+
 cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_t* assign, int32_t* order,
                            int32_t* n_clusters, double* cluster_err2, double* cluster_total, int64_t* n_evals) {
   GUARD_CTX(ctx);

@@ -40,10 +40,11 @@ struct BaseDesc {
 struct AppDesc {
   const float* F;       // m x w column-major (ld = m)
   int w;
-  int pad;
+  int ns;               // length of spec
   double E;             // full energy of the appended block
   double extra;         // E - ||F||_F^2 for TRUNC (the dropped tail), 0 for RAW
   double tailw;         // E - sum_{l<r} sigma_l^2 of the appended block (Weyl)
+  const double* spec;   // sigma of the appended block, non-increasing (per-index Weyl, N3)
 };
 
 // One batched-GEMM problem for the SIMT kernels.

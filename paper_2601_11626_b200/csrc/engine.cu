@@ -485,11 +485,13 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
 // ---------------------------------------------------------------------------
 Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kinds, const BaseDesc* d_bd,
                      const AppDesc* d_ad, const Dims& dims, double* d_err2, double* d_total, float* d_st,
-                     float* d_mu) {
+                     float* d_mu, bool tight) {
   if (P <= 0) return CMSVD_OK;
   const int64_t m = c.m;
+  // tight (N3): residual with the U_r basis + per-index Weyl; d_err2 is then P x 2
+  if (tight) kinds = CMSVD_RESIDUAL;
   const bool need_mat = (kinds & (CMSVD_RESIDUAL | CMSVD_INCREMENTAL)) != 0;
-  const bool full = (kinds & CMSVD_RESIDUAL) != 0;
+  const bool full = (kinds & CMSVD_RESIDUAL) != 0 && !tight;
   const int QMAX = std::max(1, full ? dims.qmax : dims.rrmax);
   // tcgen05 path (fp32 accumulation) unless the collection has numerically rank-deficient blocks: an
   // fp32-accumulated Gram resolves exactly-zero singular values only to ~sqrt(u32)*sigma_1, the
@@ -497,7 +499,7 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
   const bool use_tc = c.use_tc && c.tc_ok && (full ? dims.qmax : dims.rrmax) <= 128 && dims.wmax <= 128;
   const int WMAX = std::max(1, dims.wmax);
   const int GMAX = std::max(1, dims.rrmax + dims.wmax);
-  if (need_mat && (GMAX > kEigMax || WMAX > kEigMax))
+  if (need_mat && ((!tight && GMAX > kEigMax) || WMAX > kEigMax))
     return fail(c, CMSVD_E_SHAPE, "pair_errors: core size r'+w = " + std::to_string(GMAX) + " exceeds " +
                                       std::to_string(kEigMax) + " (large-core path not built yet)");
   size_t per_pair = 0;
@@ -559,6 +561,7 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       prof_end(c, pf);
       if (use_tc) {
         // fused tcgen05 3xTF32: Z = Q^T F, R' = F - Q Z (on chip), W' = R'^T R'
+        // (tight: Q = U_r, the same projection as the incremental estimator)
         pf = prof_begin(c, PC_PAIR_TC);
         CK(launch_pair_tc(c, pr, Pc, d_bd, d_ad, m, full ? 1 : 0, QMAX, WMAX, Z, W), "pairs: tcgen05 Z/R/W");
         prof_end(c, pf);
@@ -573,21 +576,29 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
         CK(launch_gemm_tn(c, dW, (int)Pc, WMAX, WMAX, true), "pairs: W = R^T R");
         prof_end(c, pf);
       }
-      pf = prof_begin(c, PC_GRAM_ZZ);
-      CK(launch_gemm_tn(c, dZZ, (int)Pc, WMAX, WMAX, true), "pairs: Z^T Z");
-      prof_end(c, pf);
-      pf = prof_begin(c, PC_BUILD_G);
-      k_build_G<<<(unsigned)Pc, kThreads, 0, c.stream>>>(pr, d_bd, d_ad, QMAX, WMAX, GMAX, Z, W, ZZ, Gm, zn2);
-      c.launches += 1;
-      CK(cudaGetLastError(), "pairs: build G");
-      prof_end(c, pf);
+      if (tight) {
+        pf = prof_begin(c, PC_BUILD_G);
+        k_znorm<<<(unsigned)Pc, kThreads, 0, c.stream>>>(pr, d_bd, d_ad, Z, QMAX, WMAX, zn2);
+        c.launches += 1;
+        CK(cudaGetLastError(), "pairs: ||U_r^T F||");
+        prof_end(c, pf);
+      } else {
+        pf = prof_begin(c, PC_GRAM_ZZ);
+        CK(launch_gemm_tn(c, dZZ, (int)Pc, WMAX, WMAX, true), "pairs: Z^T Z");
+        prof_end(c, pf);
+        pf = prof_begin(c, PC_BUILD_G);
+        k_build_G<<<(unsigned)Pc, kThreads, 0, c.stream>>>(pr, d_bd, d_ad, QMAX, WMAX, GMAX, Z, W, ZZ, Gm, zn2);
+        c.launches += 1;
+        CK(cudaGetLastError(), "pairs: build G");
+        prof_end(c, pf);
+      }
       if (kinds & CMSVD_INCREMENTAL) {
         pf = prof_begin(c, PC_EIG_G);
         CK(launch_tridiag_topk(c, Gm, GMAX, (int64_t)GMAX * GMAX, nG, (int)Pc, GMAX, nullptr, r, evG, cntG, trG, scr),
            "pairs: eig(G)");
         prof_end(c, pf);
       }
-      if ((kinds & CMSVD_RESIDUAL) && !c.big) {  // A22 bases: R = (I - QQ^T)F = 0, sigma(W') unused
+      if ((kinds & CMSVD_RESIDUAL) && (!c.big || tight)) {  // A22 bases: R = (I - QQ^T)F = 0, sigma(W') unused
         pf = prof_begin(c, PC_EIG_W);
         CK(launch_tridiag_topk(c, W, WMAX, (int64_t)WMAX * WMAX, nW, (int)Pc, WMAX, thrW, r, evW, cntW, trW, scr),
            "pairs: eig(W)");
@@ -595,6 +606,14 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       }
     }
     int prf = prof_begin(c, PC_FINALIZE);
+    if (tight) {
+      k_finalize_tight<<<(unsigned)((Pc + 127) / 128), 128, 0, c.stream>>>(pr, Pc, d_bd, d_ad, r, evW, cntW, trW,
+                                                                         zn2, d_err2 + 2 * p0, d_total + p0);
+      c.launches += 1;
+      CK(cudaGetLastError(), "pairs: finalize (tight)");
+      prof_end(c, prf);
+      continue;
+    }
     k_finalize<<<(unsigned)((Pc + 127) / 128), 128, 0, c.stream>>>(
         pr, Pc, d_bd, d_ad, r, kinds, evG, cntG, trG, evW, cntW, trW, zn2, d_err2 + 3 * p0, d_total + p0,
         d_st ? d_st + p0 * r : nullptr, d_mu ? d_mu + p0 * r : nullptr);
@@ -663,6 +682,51 @@ Status do_pair_errors(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, uint32
   if (bad) return fail(c, CMSVD_E_SHAPE, "pair_errors: a device pair index is out of range");
   return pair_eval_dev(c, (const int2*)pairs, P, r, kinds, (const BaseDesc*)c.d_bdesc.p, d_ad, dims, err2, total,
                        sigma_tilde, mu);
+}
+
+// N3 (beyond the paper): residual bound with the tracked basis U_r and the per-index Weyl bound for the
+// candidate pairs; err2x[2p + {0,1}], total[p].  Same validation and host/device conventions as
+// do_pair_errors.
+Status do_pair_errors_tight(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, int operand, int where,
+                            double* err2x, double* total) {
+  if (P < 0) return fail(c, CMSVD_E_ARG, "pair_errors_tight: P < 0");
+  if (P == 0) return CMSVD_OK;
+  if (!pairs || !err2x || !total) return fail(c, CMSVD_E_ARG, "pair_errors_tight: pairs, err2x and total are required");
+  if (c.count <= 0 || c.spectra_r <= 0) return fail(c, CMSVD_E_STATE, "pair_errors_tight: call block_spectra first");
+  if (r != c.spectra_r) return fail(c, CMSVD_E_STATE, "pair_errors_tight: r differs from the block_spectra r");
+  if (operand != CMSVD_OPERAND_RAW && operand != CMSVD_OPERAND_TRUNC)
+    return fail(c, CMSVD_E_ARG, "pair_errors_tight: bad operand");
+  if (where != CMSVD_HOST && where != CMSVD_DEVICE) return fail(c, CMSVD_E_ARG, "pair_errors_tight: bad `where`");
+  const AppDesc* d_ad = (const AppDesc*)(operand == CMSVD_OPERAND_TRUNC ? c.d_adesc_trunc.p : c.d_adesc_raw.p);
+  const Dims dims = block_dims(c, operand);
+  if (where == CMSVD_HOST) {
+    for (int64_t p = 0; p < 2 * P; ++p)
+      if (pairs[p] < 0 || pairs[p] >= c.count)
+        return fail(c, CMSVD_E_SHAPE, "pair_errors_tight: pair index out of range at entry " + std::to_string(p));
+    size_t off = 0;
+    size_t oP = off; off += align_up((size_t)P * 8, 256);
+    size_t oE = off; off += align_up((size_t)P * 16, 256);
+    size_t oT = off; off += align_up((size_t)P * 8, 256);
+    CK(ensure(c.ws[WS_OUT], off), "pair_errors_tight: io buffers");
+    char* b = (char*)c.ws[WS_OUT].p;
+    CK(cudaMemcpyAsync(b + oP, pairs, (size_t)P * 8, cudaMemcpyHostToDevice, c.stream), "pair_errors_tight: h2d");
+    Status s = pair_eval_dev(c, (const int2*)(b + oP), P, r, CMSVD_RESIDUAL, (const BaseDesc*)c.d_bdesc.p, d_ad, dims,
+                             (double*)(b + oE), (double*)(b + oT), nullptr, nullptr, true);
+    if (s != CMSVD_OK) return s;
+    CK(cudaMemcpyAsync(err2x, b + oE, (size_t)P * 16, cudaMemcpyDeviceToHost, c.stream), "pair_errors_tight: d2h");
+    CK(cudaMemcpyAsync(total, b + oT, (size_t)P * 8, cudaMemcpyDeviceToHost, c.stream), "pair_errors_tight: d2h");
+    CK(cudaStreamSynchronize(c.stream), "pair_errors_tight: sync");
+    return CMSVD_OK;
+  }
+  CK(ensure(c.ws[WS_BAD], 16), "pair_errors_tight: flag");
+  CK(cudaMemsetAsync(c.ws[WS_BAD].p, 0, 4, c.stream), "pair_errors_tight: memset");
+  CK(launch_check_pairs(c, (const int2*)pairs, P, c.count, (int*)c.ws[WS_BAD].p), "pair_errors_tight: check");
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, c.ws[WS_BAD].p, 4, cudaMemcpyDeviceToHost, c.stream), "pair_errors_tight: flag d2h");
+  CK(cudaStreamSynchronize(c.stream), "pair_errors_tight: sync");
+  if (bad) return fail(c, CMSVD_E_SHAPE, "pair_errors_tight: a device pair index is out of range");
+  return pair_eval_dev(c, (const int2*)pairs, P, r, CMSVD_RESIDUAL, (const BaseDesc*)c.d_bdesc.p, d_ad, dims, err2x,
+                       total, nullptr, nullptr, true);
 }
 
 }  // namespace cmsvd

@@ -30,7 +30,10 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
 Status do_pair_errors(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, uint32_t kinds, int operand, int where,
                       double* err2, double* total, float* sigma_tilde, float* mu);
 Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kinds, const BaseDesc* d_bd,
-                     const AppDesc* d_ad, const Dims& dims, double* d_err2, double* d_total, float* d_st, float* d_mu);
+                     const AppDesc* d_ad, const Dims& dims, double* d_err2, double* d_total, float* d_st, float* d_mu,
+                     bool tight = false);
+Status do_pair_errors_tight(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, int operand, int where,
+                            double* err2x, double* total);
 Dims block_dims(const Ctx& c, int operand);
 cudaError_t launch_check_pairs(Ctx& c, const int2* d_pairs, int64_t P, int count, int* d_bad);
 Status do_cluster(Ctx& c, const cmsvd_cluster_opts* o, int32_t* assign, int32_t* order, int32_t* n_clusters,

@@ -263,7 +263,8 @@ __global__ void k_big_stats(int nb, const int* __restrict__ ids, int s, int r, i
   AppDesc a;
   a.F = Aptr[b];
   a.w = n;
-  a.pad = 0;
+  a.ns = ns;
+  a.spec = sg;
   a.E = Ei;
   a.extra = 0.0;
   a.tailw = d.tailw;

@@ -157,6 +157,71 @@ __global__ void k_finalize(const int2* __restrict__ pairs, int64_t P, const Base
   err2[3 * p + 2] = clampv(ei);
 }
 
+// Tighter certified variants beyond the paper, one thread per pair:
+//   err2x[2p]   = residual bound with the tracked basis U_r (A4): mu = top-r of sigma(A_i) U sigma(R_r),
+//                 R_r = (I - U_r U_r^T) F, summed as the dropped part like k_finalize;
+//   err2x[2p+1] = per-index Weyl bound E_i + E_j - sum_{l<r} max(sigma_l(A_i), sigma_l(A_j))^2 (A8; the
+//                 inequality sigma_l(M) >= sigma_l(A_k) of the proof line PAPER.md:1530-1533).
+// zn2[p] = ||U_r^T F||_F^2; evW/cntW/trW = eigenvalues of R_r^T R_r above sigma_r(A_i)^2.
+__global__ void k_finalize_tight(const int2* __restrict__ pairs, int64_t P, const BaseDesc* __restrict__ bd,
+                                 const AppDesc* __restrict__ ad, int r, const double* __restrict__ evW,
+                                 const int* __restrict__ cntW, const double* __restrict__ trW,
+                                 const double* __restrict__ zn2, double* __restrict__ err2x,
+                                 double* __restrict__ total) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const int2 pr = pairs[p];
+  const BaseDesc b = bd[pr.x];
+  const AppDesc a = ad[pr.y];
+  const double tot = b.E + a.E;
+  total[p] = tot;
+  // residual with U_r
+  const double* ev = evW + p * r;
+  const int c = cntW[p];
+  int ib = 0, iw = 0;
+  double sel_w = 0.0;
+  for (int l = 0; l < r; ++l) {
+    const double sb = (ib < b.ns) ? b.spec[ib] : -1.0;
+    const double sw = (iw < c) ? sqrt(fmax(ev[iw], 0.0)) : -1.0;
+    if (sb < 0.0 && sw < 0.0) break;
+    if (sb >= sw) ++ib;
+    else { sel_w += fmax(ev[iw], 0.0); ++iw; }
+  }
+  double unsel = 0.0;
+  for (int l = ib; l < b.ns; ++l) unsel += b.spec[l] * b.spec[l];
+  const double er = b.rest_res + unsel + fmax(trW[p] - sel_w, 0.0) + zn2[p] + a.extra;
+  // per-index Weyl: sum of the dropped part, E_i + E_j - sum_{l<r} max^2 =
+  //   (E_i - sum_{l<r} s_il^2) + (E_j - sum_{l<r} s_jl^2) + sum_{l<r} min(s_il, s_jl)^2
+  double mn = 0.0;
+  for (int l = 0; l < r; ++l) {
+    const double si = (l < b.ns) ? b.spec[l] : 0.0, sj = (l < a.ns) ? a.spec[l] : 0.0;
+    const double lo = fmin(si, sj);
+    mn += lo * lo;
+  }
+  const double ew = b.tailw + a.tailw + mn;
+  auto clampv = [&](double v) { return fmin(fmax(v, 0.0), tot); };
+  err2x[2 * p + 0] = clampv(er);
+  err2x[2 * p + 1] = clampv(ew);
+}
+
+// ||Z||_F^2 per pair (rows < QMAX of a q x w fp32 block, ld QMAX), fp64 accumulation; one CTA per pair.
+__global__ void __launch_bounds__(kThreads) k_znorm(const int2* __restrict__ pairs, const BaseDesc* __restrict__ bd,
+                                                    const AppDesc* __restrict__ ad, const float* __restrict__ Zws,
+                                                    int QMAX, int WMAX, double* __restrict__ zn2) {
+  __shared__ double red[kThreads / 32];
+  const int64_t p = blockIdx.x;
+  const int2 pr = pairs[p];
+  const int q = bd[pr.x].rr, w = ad[pr.y].w;
+  const float* Z = Zws + p * (int64_t)QMAX * WMAX;
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < q * w; e += blockDim.x) {
+    const double z = Z[(int64_t)(e / q) * QMAX + (e % q)];
+    acc = fma(z, z, acc);
+  }
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) zn2[p] = s;
+}
+
 // Single-problem G builder for cluster commits (same layout as k_build_G).
 __global__ void k_build_G1(int rr, int w, const double* __restrict__ spec, const float* __restrict__ Z, int ldz,
                            const double* __restrict__ ZZ, const double* __restrict__ WW, double* __restrict__ G) {
@@ -232,7 +297,8 @@ __global__ void k_spec_stats(int count, int nmax, int r, const double* __restric
   AppDesc a;
   a.F = arena + boff[i];
   a.w = ncols[i];
-  a.pad = 0;
+  a.ns = k;
+  a.spec = s;
   a.E = Ei;
   a.extra = 0.0;
   a.tailw = tailw;

@@ -32,6 +32,11 @@ __global__ void k_make_descs(const int2* pairs, int64_t P, const BaseDesc* bd, c
                              double* thrW, int r);
 __global__ void k_build_G(const int2* pairs, const BaseDesc* bd, const AppDesc* ad, int QMAX, int WMAX, int GMAX,
                           const float* Zws, const double* Wws, const double* ZZws, double* Gws, double* zn2);
+__global__ void k_finalize_tight(const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int r,
+                                 const double* evW, const int* cntW, const double* trW, const double* zn2,
+                                 double* err2x, double* total);
+__global__ void k_znorm(const int2* pairs, const BaseDesc* bd, const AppDesc* ad, const float* Zws, int QMAX,
+                        int WMAX, double* zn2);
 __global__ void k_finalize(const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int r, unsigned kinds,
                            const double* evG, const int* cntG, const double* trG, const double* evW, const int* cntW,
                            const double* trW, const double* zn2, double* err2, double* total, float* sigma_tilde,

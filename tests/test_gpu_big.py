@@ -122,3 +122,18 @@ def test_big_edge_cases(cm):
         ctx.register([np.asfortranarray(np.random.default_rng(0).standard_normal((700, 600)).astype(np.float32))] * 2)
         with pytest.raises(cm.CmsvdError):
             ctx.block_spectra(8)
+
+
+def test_c3_tight_variants(cm):
+    """N3 variants on A22 bases (square blocks): the U_r residual is a real projection here
+    (the full-range residual vanishes), per-index Weyl from the top-r spectra."""
+    col = synth.config3(N=4)
+    sp = oracle.block_spectra(col.blocks)
+    pairs = synth.all_pairs_by_norm_order(norm_order(sp.E))
+    ref, tot = oracle.pair_errors_tight(sp, pairs, col.r, oracle.TRUNC)
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        ctx.block_spectra(col.r)
+        out = ctx.pair_errors_tight(pairs, operand=cm.TRUNC)
+    assert_err2(out["err2x"][:, 0], ref[:, 0], tot, "config3 residual(U_r)")
+    assert_err2(out["err2x"][:, 1], ref[:, 1], tot, "config3 per-index Weyl")

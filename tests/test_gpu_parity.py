@@ -264,3 +264,31 @@ def test_c5_knn_sample(cm, r):
         ex = oracle.exact_groups(sp, [list(p) for p in pairs[:24]], r)
         assert_err2(out["err2"][:24, 2], ex, out["total"][:24], "config5 exactness")
     ctx.close()
+
+
+# ------------------------------------------------- N3 (beyond the paper) --
+def test_tight_variants_c1_all_pairs(c1, cm):
+    """cmsvd_pair_errors_tight (residual with U_r, per-index Weyl) vs the oracle, all config-1 pairs,
+    RAW and TRUNC, plus the ordering against the paper's estimators."""
+    col, sp, ctx, *_ = c1
+    pairs = synth.all_pairs_by_norm_order(norm_order(sp.E))
+    for operand in (cm.RAW, cm.TRUNC):
+        ref, tot = oracle.pair_errors_tight(sp, pairs, col.r, operand)
+        out = ctx.pair_errors_tight(pairs, operand=operand)
+        assert np.allclose(out["total"], tot, rtol=1e-12)
+        assert_err2(out["err2x"][:, 0], ref[:, 0], tot, "residual(U_r)")
+        assert_err2(out["err2x"][:, 1], ref[:, 1], tot, "per-index Weyl")
+        std = ctx.pair_errors(pairs, operand=operand)
+        assert np.all(out["err2x"][:, 0] <= std["err2"][:, 1] * (1 + 2e-3) + 1e-7 * tot)
+        assert np.all(out["err2x"][:, 1] <= std["err2"][:, 0] * (1 + 1e-9) + 1e-9 * tot)
+        assert np.all(std["err2"][:, 2] <= out["err2x"][:, 0] * (1 + 2e-3) + 1e-7 * tot)
+
+
+def test_tight_variants_c2_sampled(c2):
+    col, sp, ctx, E, *_ = c2
+    pairs = synth.all_pairs_by_norm_order(norm_order(sp.E))
+    sel = pairs[np.random.default_rng(7).choice(pairs.shape[0], 64, replace=False)]
+    ref, tot = oracle.pair_errors_tight(sp, sel, col.r)
+    out = ctx.pair_errors_tight(sel)
+    assert_err2(out["err2x"][:, 0], ref[:, 0], tot, "config2 residual(U_r)")
+    assert_err2(out["err2x"][:, 1], ref[:, 1], tot, "config2 per-index Weyl")

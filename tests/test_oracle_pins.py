@@ -328,3 +328,64 @@ def test_zero_and_low_rank_blocks_vs_brute_force(r):
         st = np.linalg.svd(np.concatenate([UA[:, :rr] * sA[:rr], Y], 1), compute_uv=False)[:r]
         st = np.pad(st, (0, r - st.size))
         assert np.allclose(res.sigma_tilde[0], st, atol=1e-12 * max(1, st[0]))
+
+
+# ---------------------------------------------------------------------------
+# N3 (beyond the paper): residual bound with the tracked basis U_r (A4) and the
+# per-index Weyl bound (A8), oracle.pair_errors_tight
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("seed", range(20))
+def test_tight_variants_chain_and_definitions(seed):
+    """Chain exact <= inc <= residual(U_r) <= residual(full) <= Weyl and
+    exact <= per-index Weyl <= Weyl (Eq. 5); both variants against direct numpy
+    evaluations of their definitions (LAPACK SVDs, independent of oracle.c)."""
+    R = rng(700 + seed)
+    m = int(R.integers(6, 20))
+    n1, n2 = int(R.integers(1, 7)), int(R.integers(1, 7))
+    if seed % 2:
+        U = np.linalg.qr(R.standard_normal((m, 3)))[0]
+        A = U @ R.standard_normal((3, n1)) + 0.05 * R.standard_normal((m, n1))
+        B = U @ R.standard_normal((3, n2)) + 0.05 * R.standard_normal((m, n2))
+    else:
+        A = R.standard_normal((m, n1)); B = R.standard_normal((m, n2))
+    r = int(R.integers(1, min(m, n1 + n2) + 1))
+    sA = np.linalg.svd(A, compute_uv=False); sB = np.linalg.svd(B, compute_uv=False)
+    if np.sum(sB[:r] ** 2) > np.sum(sA[:r] ** 2):
+        A, B = B, A
+        sA, sB = sB, sA
+    sp = oracle.block_spectra([A, B])
+    std = oracle.pair_errors(sp, [[0, 1]], r, 7)
+    x, tot = oracle.pair_errors_tight(sp, [[0, 1]], r)
+    res_ur, w_idx = x[0]
+    w, res, inc = std.err2[0]
+    ex = exact([A, B], r)
+    tol = 1e-10 * tot[0]
+    assert ex <= inc + tol and inc <= res_ur + tol and res_ur <= res + tol and res <= w + tol
+    assert ex <= w_idx + tol and w_idx <= w + tol
+    E = np.sum(A * A) + np.sum(B * B)
+    # per-index Weyl by definition
+    k = r
+    sa = np.pad(sA, (0, max(0, k - sA.size)))[:k]; sb = np.pad(sB, (0, max(0, k - sB.size)))[:k]
+    assert abs(w_idx - max(0.0, E - np.sum(np.maximum(sa, sb) ** 2))) < 1e-10 * E
+    # residual with U_r by definition: Q = first min(r, rank) left singular vectors of A
+    Ua, sa_full, _ = np.linalg.svd(A, full_matrices=False)
+    rank = int(np.sum(sa_full > 1e-5 * sa_full[0]))
+    Q = Ua[:, :min(r, rank)]
+    Rr = B - Q @ (Q.T @ B)
+    mu = np.sort(np.concatenate([sa_full, np.linalg.svd(Rr, compute_uv=False)]))[::-1][:r]
+    assert abs(res_ur - max(0.0, E - np.sum(mu ** 2))) < 1e-9 * E
+
+
+def test_tight_variants_closed_form_AA():
+    """[A, A]: residual(U_r) = per-index Weyl = E_A + tail_r(A) (R = (I - U_r U_r^T)A
+    has sigma_{>r}(A), so the top-r of mu are sigma_{<=r}(A))."""
+    R = rng(41)
+    A = R.standard_normal((18, 7)) @ np.diag([5, 4, 3, 2, 1, 0.5, 0.2])
+    s = np.linalg.svd(A, compute_uv=False)
+    EA = np.sum(A * A)
+    for r in (1, 3, 6):
+        sp = oracle.block_spectra([A])
+        x, tot = oracle.pair_errors_tight(sp, [[0, 0]], r)
+        t = np.sum(s[r:] ** 2)
+        assert abs(x[0, 0] - (EA + t)) < 1e-10 * EA
+        assert abs(x[0, 1] - (EA + t)) < 1e-10 * EA
