@@ -167,6 +167,24 @@ cmsvd_status cmsvd_pair_errors(cmsvd_ctx ctx, const int32_t* pairs, int64_t P, i
 cmsvd_status cmsvd_pair_errors_tight(cmsvd_ctx ctx, const int32_t* pairs, int64_t P, int32_t r, int operand,
                                      int where, double* err2x, double* total);
 
+/* Cluster verification and compression accounting (
+ * PAPER.md:142-173, 579-597).  For the partition assign[count] (cluster ids
+ * 0..n_clusters-1, every cluster non-empty; host arrays) and target rank r >= 1:
+ *   exact_err2[c] = sum_{j>r} sigma_j^2(M_c) of the explicit concatenation M_c
+ *                   of cluster c's blocks in ascending block order (Thm EYM,
+ *                   the error of the rank-r truncated SVD
+ *                   M_c ~ U_c S_c V_c^T and of the reconstruction Ũ_c V_c,i^T);
+ *                   fp64 Gram (min(m, N_c) square) + eigenvalues;
+ *   total[c]      = ||M_c||_F^2   (eps_rel = sqrt(exact_err2 / total));
+ *   mem[c]        = min(m N_c, r_c (m + N_c)) stored parameters, r_c =
+ *                   min(r, m, N_c) (reading A23: a cluster
+ *                   is stored raw when that is smaller, cf. Table 2's 1.000*).
+ * The compression ratio is sum_i m n_i / sum_c mem[c].
+ * Errors: CMSVD_E_STATE (no collection), CMSVD_E_ARG (bad assign / r),
+ * CMSVD_E_SHAPE (min(m, N_c) > 512), CMSVD_E_NOCONV, CMSVD_E_CUDA, CMSVD_E_NOMEM. */
+cmsvd_status cmsvd_cluster_verify(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters,
+                                  double* exact_err2, double* total, int64_t* mem);
+
 /* Greedy clustering (Appendix E). */
 enum { CMSVD_ALG_MAX_NORM = 0, CMSVD_ALG_RESIDUAL = 1, CMSVD_ALG_APPROX = 2 };
 enum { CMSVD_SORT_FROBENIUS = 0, CMSVD_SORT_RESIDUAL = 1 };

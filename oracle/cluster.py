@@ -226,3 +226,19 @@ def cluster(spec: Spectra, algorithm: int, r: int, eps: float, sort: int = SORT_
     if algorithm == MAX_NORM:
         return cluster_max_norm(spec, r, eps)
     return cluster_tracked(spec, algorithm, r, eps, sort, knn, operand)
+
+
+def compression(m: int, ncols, clusters, r: int):
+    """Compression accounting of a partition (PAPER.md:158-162 mem_c = r_c (m + N_c);
+    PAPER.md:590-597 ratio = parameters before / after).  Reading A23: a
+    cluster is stored raw when that is smaller, mem_c = min(m N_c, r_c (m + N_c)) with
+    r_c = min(r, m, N_c) -- consistent with Table 2's 1.000* for failed (all-singleton)
+    clusterings.  Returns (mem per cluster, ratio)."""
+    ncols = np.asarray(ncols, dtype=np.int64)
+    mem = []
+    for members in clusters:
+        Nc = int(np.sum(ncols[list(members)]))
+        rc = min(r, m, Nc)
+        mem.append(min(m * Nc, rc * (m + Nc)))
+    mem = np.array(mem, dtype=np.int64)
+    return mem, float(m * np.sum(ncols)) / float(np.sum(mem))

@@ -25,8 +25,9 @@ ALG_MAX_NORM, ALG_RESIDUAL, ALG_APPROX = 0, 1, 2
 SORT_FROBENIUS, SORT_RESIDUAL = 0, 1
 
 EXPORTS = ["cmsvd_status_string", "cmsvd_last_error", "cmsvd_version", "cmsvd_create", "cmsvd_destroy",
-           "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_pair_errors_tight", "cmsvd_cluster", "cmsvd_launch_count",
-           "cmsvd_profile_enable", "cmsvd_profile_read"]
+           "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_pair_errors_tight",
+           "cmsvd_cluster", "cmsvd_cluster_verify", "cmsvd_launch_count", "cmsvd_profile_enable",
+           "cmsvd_profile_read"]
 
 
 class CmsvdError(RuntimeError):
@@ -72,6 +73,8 @@ def load(path: str = LIB_PATH):
     L.cmsvd_pair_errors_tight.argtypes = [vp, vp, i64, i32, ctypes.c_int, ctypes.c_int, vp, vp]
     L.cmsvd_pair_errors_tight.restype = ctypes.c_int
     L.cmsvd_cluster.argtypes = [vp, ctypes.POINTER(ClusterOpts), vp, vp, vp, vp, vp, vp]
+    L.cmsvd_cluster_verify.restype = ctypes.c_int
+    L.cmsvd_cluster_verify.argtypes = [vp, i32, vp, i32, vp, vp, vp]
     L.cmsvd_launch_count.restype = i64
     L.cmsvd_launch_count.argtypes = [vp]
     L.cmsvd_profile_enable.restype = ctypes.c_int
@@ -194,6 +197,7 @@ class Context:
         del keep
         self.count = N
         self.m = int(m)
+        self._ncols = np.asarray(ns, np.int64)
         return self
 
     # -- cmsvd_block_spectra ---------------------------------------------
@@ -241,6 +245,21 @@ class Context:
         self._check(self._L.cmsvd_pair_errors_tight(self._h, _ptr(pairs), P, r, operand, HOST, _ptr(err2x),
                                                     _ptr(total)))
         return {"err2x": err2x, "total": total}
+
+    # -- cmsvd_cluster_verify (N1) -----------------------------------------
+    def cluster_verify(self, assign, r: int | None = None):
+        """Exact per-cluster rank-r errors of the explicit concatenations and the
+        compression accounting: {"exact_err2", "total", "rel", "mem", "ratio"}."""
+        r = self.r if r is None else r
+        assign = np.ascontiguousarray(assign, dtype=np.int32)
+        nc = int(assign.max()) + 1 if assign.size else 0
+        e2 = np.zeros(nc)
+        tot = np.zeros(nc)
+        mem = np.zeros(nc, np.int64)
+        self._check(self._L.cmsvd_cluster_verify(self._h, int(r), _ptr(assign), nc, _ptr(e2), _ptr(tot), _ptr(mem)))
+        raw = float(self.m) * float(np.sum(self._ncols)) if hasattr(self, "_ncols") else float("nan")
+        return {"exact_err2": e2, "total": tot, "rel": np.sqrt(e2 / np.maximum(tot, 1e-300)), "mem": mem,
+                "ratio": raw / float(np.sum(mem)) if nc else float("nan")}
 
     # -- cmsvd_cluster ---------------------------------------------------
     def cluster(self, algorithm: int, eps: float, r: int | None = None, sort: int = SORT_FROBENIUS,

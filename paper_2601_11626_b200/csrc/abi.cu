@@ -146,6 +146,18 @@ cmsvd_status cmsvd_pair_errors_tight(cmsvd_ctx ctx, const int32_t* pairs, int64_
   }
 }
 
+cmsvd_status cmsvd_cluster_verify(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters,
+                                  double* exact_err2, double* total, int64_t* mem) {
+  GUARD_CTX(ctx);
+  try {
+    return do_cluster_verify(c, r, assign, n_clusters, exact_err2, total, mem);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "cluster_verify: host allocation failed");
+  } catch (...) {
+    return fail(c, CMSVD_E_ARG, "cluster_verify: unexpected exception");
+  }
+}
+
 cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_t* assign, int32_t* order,
                            int32_t* n_clusters, double* cluster_err2, double* cluster_total, int64_t* n_evals) {
   GUARD_CTX(ctx);

@@ -95,7 +95,6 @@ Status cuda_fail(Ctx& c, cudaError_t e, const char* where) {
   } while (0)
 
 // Workspace slots
-enum { WS_PARTIAL = 0, WS_BAD, WS_META, WS_G, WS_V, WS_EV, WS_PERM, WS_STAT, WS_PAIR, WS_OUT, WS_A, WS_B, WS_C };
 
 // ---------------------------------------------------------------------------
 // S1: register

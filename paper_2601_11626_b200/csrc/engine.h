@@ -7,7 +7,10 @@ namespace cmsvd {
 
 typedef cmsvd_status Status;
 
-constexpr int kEigMax = 512;     // largest Gram handled by the eigensolvers (> 160: in place in global memory)
+constexpr int kEigMax = 512;
+
+// context workspace slots (Ctx::ws)
+enum { WS_PARTIAL = 0, WS_BAD, WS_META, WS_G, WS_V, WS_EV, WS_PERM, WS_STAT, WS_PAIR, WS_OUT, WS_A, WS_B, WS_C };     // largest Gram handled by the eigensolvers (> 160: in place in global memory)
 
 struct Dims {
   int qmax = 0;   // projection-basis columns (full range)
@@ -36,6 +39,8 @@ Status do_pair_errors_tight(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, 
                             double* err2x, double* total);
 Dims block_dims(const Ctx& c, int operand);
 cudaError_t launch_check_pairs(Ctx& c, const int2* d_pairs, int64_t P, int count, int* d_bad);
+Status do_cluster_verify(Ctx& c, int32_t r, const int32_t* assign, int32_t n_clusters, double* exact_err2,
+                         double* total, int64_t* mem);
 Status do_cluster(Ctx& c, const cmsvd_cluster_opts* o, int32_t* assign, int32_t* order, int32_t* n_clusters,
                   double* cluster_err2, double* cluster_total, int64_t* n_evals);
 

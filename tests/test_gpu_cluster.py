@@ -169,3 +169,55 @@ def test_knn_window_matches_oracle(cm, alg, knn):
         o = oc.cluster(sp, alg, col.r, eps, oc.SORT_RESIDUAL, knn=knn)
         assert g["clusters"] == o.clusters, (col.name, knn)
         assert g["n_evals"] == o.n_evals
+
+
+def _clusters_of(assign):
+    nc = int(np.max(assign)) + 1
+    return [sorted(np.flatnonzero(assign == c).tolist()) for c in range(nc)]
+
+
+@pytest.mark.parametrize("alg", [oc.MAX_NORM, oc.RESIDUAL_ALG, oc.APPROX])
+def test_cluster_verify_c1(cm, alg):
+    """N1: exact per-cluster errors of the explicit concatenations (both Gram orientations: singletons
+    N_c = 32 < m = 64, merged clusters N_c > m) vs the oracle's brute-force SVD; compression accounting
+    identical to the oracle's (reading A23); certified algorithms stay within eps (P12)."""
+    from tolerances import assert_err2
+    col = synth.config1()
+    sp = oracle.block_spectra(col.blocks)
+    eps = 0.05
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        ctx.block_spectra(col.r)
+        g = ctx.cluster(alg, eps, sort=cm.SORT_RESIDUAL if alg else cm.SORT_FROBENIUS)
+        assign = np.asarray(g["assign"], np.int32)
+        v = ctx.cluster_verify(assign)
+    groups = _clusters_of(assign)
+    ex = oracle.exact_groups(sp, groups, col.r)
+    tot = np.array([sum(sp.E[i] for i in gr) for gr in groups])
+    assert np.allclose(v["total"], tot, rtol=1e-12)
+    assert_err2(v["exact_err2"], ex, tot, "cluster exact error")
+    mem, ratio = oc.compression(col.m, sp.n, groups, col.r)
+    assert np.array_equal(v["mem"], mem) and abs(v["ratio"] - ratio) < 1e-12 * ratio
+    if alg in (oc.MAX_NORM, oc.RESIDUAL_ALG):      # certified clusterings (P12)
+        assert np.all(v["rel"] <= eps * (1 + 1e-3))
+
+
+def test_cluster_verify_c2_row_gram(cm):
+    """Config 2, Alg. 3 residual sort at eps = 0.05: 8 clusters of 16 blocks, N_c = 2048 > m = 512 (row
+    Gram, 512 x 512 eigen-solve); two clusters checked against the oracle's explicit SVD, all within eps."""
+    from tolerances import assert_err2
+    col = synth.config2()
+    sp = oracle.block_spectra(col.blocks)
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        ctx.block_spectra(col.r)
+        g = ctx.cluster(cm.ALG_APPROX, 0.05, sort=cm.SORT_RESIDUAL)
+        assign = np.asarray(g["assign"], np.int32)
+        v = ctx.cluster_verify(assign)
+    groups = _clusters_of(assign)
+    assert len(groups) == 8
+    ex = oracle.exact_groups(sp, groups[:2], col.r)
+    assert_err2(v["exact_err2"][:2], ex, v["total"][:2], "config2 cluster exact error")
+    assert np.all(v["rel"] <= 0.05)
+    mem, ratio = oc.compression(col.m, sp.n, groups, col.r)
+    assert np.array_equal(v["mem"], mem)

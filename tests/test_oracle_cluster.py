@@ -94,3 +94,18 @@ def test_config1_regimes():
         assert len({int(col.groups[b]) for b in c}) == 1
     for c in res.clusters:
         assert exact_rel(sp, c, col.r) <= 0.05
+
+
+def test_compression_closed_forms():
+    """P14: PDEBench (Table 1: 5000 blocks of 3072 x 67, r = 67) in one cluster gives Table 2's
+    45.4341; all-singleton clusterings of BigEarthNet (1440 x 20, r = 20) give
+    exactly 1.0 (Table 2's 1.000*, reading A23)."""
+    from oracle.cluster import compression
+    mem, ratio = compression(3072, np.full(5000, 67), [list(range(5000))], 67)
+    assert abs(ratio - 45.43411) < 5e-5
+    assert mem[0] == 67 * (3072 + 5000 * 67)
+    mem, ratio = compression(1440, np.full(10, 20), [[i] for i in range(10)], 20)
+    assert ratio == 1.0 and np.all(mem == 1440 * 20)
+    # a compressible pair next to raw singletons
+    mem, ratio = compression(12800, np.full(4, 20), [[0, 1], [2], [3]], 20)
+    assert list(mem) == [20 * (12800 + 40), 12800 * 20, 12800 * 20]
