@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
                                                            int use_full_basis, int QMAX, int WMAX,
                                                            float* __restrict__ Zws, double* __restrict__ Wws) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned, derived by pointer arithmetic so that the compiler keeps the shared address space
+  uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar_stage[2];
   __shared__ uint64_t bar_done;
   __shared__ uint64_t bar_slot[2];

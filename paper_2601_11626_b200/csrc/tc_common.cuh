@@ -141,23 +141,25 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
 }
 __device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// fp32 -> tf32 (round to nearest, ties away) and the 3xTF32 split x = hi + lo
+// fp32 -> tf32 (round to nearest, ties away from zero), two integer ops: add half a tf32 ulp to the
+// magnitude bits and clear the 13 dropped mantissa bits.  Finite inputs only (the collection is checked
+// for NaN/Inf at registration; products and residuals of finite data stay far from FLT_MAX).
 __device__ __forceinline__ float to_tf32(float x) {
-  uint32_t y;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
-  return __uint_as_float(y);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
+// 3xTF32 split x = hi + lo: hi = RN_tf32(x), lo = x - hi exact in fp32 (|lo| <= half a tf32 ulp of x);
+// the tensor core reads lo's leading 11 bits, so the pair represents x to ~2^-23 relative.
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = to_tf32(x);
-  lo = to_tf32(x - hi);
+  lo = x - hi;
 }
-// 3-way split x = hi + mid + lo (representation error ~2^-33 |x|); with the six
-// products hh, hm, mh, hl, mm, lh the product error is at the fp32 accumulation level
+// 3-way split x = hi + mid + lo (exact: 11 + 11 + <= 2 significant bits); with the six products
+// hh, hm, mh, hl, mm, lh the product error is at the fp32 accumulation level
 __device__ __forceinline__ void split3_tf32(float x, float& hi, float& mid, float& lo) {
   hi = to_tf32(x);
   const float r = x - hi;
   mid = to_tf32(r);
-  lo = to_tf32(r - mid);
+  lo = r - mid;
 }
 
 }  // namespace tc
