@@ -5,11 +5,13 @@
 //            W' += R'^T R'  per tile         (K = 128)     -> TMEM, then global (fp64)
 // i.e. Lemma 1's Y = Q_t^T A, R = A - Q_t Y and the Gram B^T B = R^T R of
 // its R-factor, and Thm 2's residual.
-// All products are 3xTF32 on tcgen05 (hi*hi + hi*lo + lo*hi, fp32
-// accumulation in TMEM, summed per 128-long K block in fp32 registers, see
-// below; the cancellation-prone product Q Z uses a 3-way split and six
-// products): fp32-equivalent accuracy, which the parity
-// tolerances need (1xTF32 measured 1.3e-2 relative error).
+// All products are 3xTF32 on tcgen05 (hi*hi + hi*lo + lo*hi with round-to-
+// nearest splits, fp32 accumulation in TMEM, summed per 128-long K block with
+// round-to-nearest adds, see below): fp32-equivalent accuracy, which the
+// parity tolerances need (1xTF32 measured 1.3e-2 relative error).
+// The cancellation R' = F - Q Z keeps an absolute error ~2^-22 ||Q|| ||Z|| per
+// element, far below the tolerance floors (a 3-way split with six products is
+// available with -DCMSVD_SPLIT3R=1).
 //
 // One CTA (8 warps) per pair; thread 0 issues the MMAs, all threads stage the
 // operands (fp32 -> tf32 hi/lo split happens during the global -> smem copy,
@@ -32,6 +34,12 @@ constexpr uint32_t LBO = 144, SBO = 1152;
 constexpr uint32_t kTile = 128 * 144;   // bytes of a 128-row x 32-k operand tile (one of hi/lo)
 constexpr uint32_t kStage = 6 * kTile;  // A hi/mid/lo, B hi/mid/lo (phase 1 and W' use hi/lo only)
 constexpr uint32_t kSmemTc = 2 * kStage + 1024;
+// R' = F - Q Z is a cancellation; with round-to-nearest splits the plain 3xTF32 products keep its error at
+// ~2^-22 ||Q|| ||Z|| per element (set true for the 3-way split and six products)
+#ifndef CMSVD_SPLIT3R
+#define CMSVD_SPLIT3R 0
+#endif
+constexpr bool kSplit3R = CMSVD_SPLIT3R != 0;
 
 __device__ __forceinline__ uint32_t poff(int r, int k) {
   return (uint32_t)((k >> 2) * LBO + (r >> 3) * SBO + (r & 7) * 16 + (k & 3) * 4);
@@ -131,7 +139,11 @@ __device__ __forceinline__ void stage_rcontig(uint8_t* hi, uint8_t* mi, uint8_t*
     }
   }
 #pragma unroll
-  for (int t = 0; t < NQ; ++t) st_split4_3(hi, mi, lo, poff(r, 4 * (h + t * (kTcThreads / 128))), v[t]);
+  for (int t = 0; t < NQ; ++t) {
+    const uint32_t o = poff(r, 4 * (h + t * (kTcThreads / 128)));
+    if (mi) st_split4_3(hi, mi, lo, o, v[t]);
+    else st_split4(hi, lo, o, v[t]);
+  }
 }
 
 // 6-product (3-way split) MMA sequence for one 32-k stage: hh, hm, mh, hl, mm, lh
@@ -321,16 +333,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
       const int s = it & 1;
       acquire(s);
       // R' = F - Q Z is a cancellation (||R'|| << ||F||): its product uses the 3-way split
-      stage_rcontig(stage_ptr(s, 0), stage_ptr(s, 4), stage_ptr(s, 1), Q, m, m0, m, a0, q);
-      stage_kcontig<false>(stage_ptr(s, 2), stage_ptr(s, 3), wp, Zg, QMAX, w, a0, q, stage_ptr(s, 5));
+      stage_rcontig(stage_ptr(s, 0), kSplit3R ? stage_ptr(s, 4) : nullptr, stage_ptr(s, 1), Q, m, m0, m, a0, q);
+      stage_kcontig<false>(stage_ptr(s, 2), stage_ptr(s, 3), wp, Zg, QMAX, w, a0, q,
+                           kSplit3R ? stage_ptr(s, 5) : nullptr);
       tc::fence_proxy_async();
       tc::fence_before();
       __syncthreads();
       if (tid == 0) {
         tc::fence_after();
-        issue_6x(t_r, tc::smem_u32(stage_ptr(s, 0)), tc::smem_u32(stage_ptr(s, 4)), tc::smem_u32(stage_ptr(s, 1)),
-                 tc::smem_u32(stage_ptr(s, 2)), tc::smem_u32(stage_ptr(s, 5)), tc::smem_u32(stage_ptr(s, 3)),
-                 idesc_r, r_first);
+        if (kSplit3R)
+          issue_6x(t_r, tc::smem_u32(stage_ptr(s, 0)), tc::smem_u32(stage_ptr(s, 4)), tc::smem_u32(stage_ptr(s, 1)),
+                   tc::smem_u32(stage_ptr(s, 2)), tc::smem_u32(stage_ptr(s, 5)), tc::smem_u32(stage_ptr(s, 3)),
+                   idesc_r, r_first);
+        else
+          issue_3x(t_r, tc::smem_u32(stage_ptr(s, 0)), tc::smem_u32(stage_ptr(s, 1)), tc::smem_u32(stage_ptr(s, 2)),
+                   tc::smem_u32(stage_ptr(s, 3)), idesc_r, r_first);
         tc::mma_commit(&bar_stage[s]);
       }
       used[s] = 1;
