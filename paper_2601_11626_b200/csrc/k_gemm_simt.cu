@@ -22,8 +22,9 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const GemmDesc* __restrict__ de
   const int i0 = tm * BM, j0 = tn * BN;
   if (i0 >= d.M || j0 >= d.N) return;
   if (d.sym && tm < tn) return;
-  __shared__ float As[BK][PADM];
-  __shared__ float Bs[BK][PADN];
+  // operands staged in the accumulation type (fp32 data converted once, not per use)
+  __shared__ AccT As[BK][PADM];
+  __shared__ AccT Bs[BK][PADN];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   AccT acc[4][4];
 #pragma unroll
@@ -40,17 +41,17 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const GemmDesc* __restrict__ de
         if (i0 + i < d.M) va = d.A[(int64_t)(i0 + i) * d.lda + k0 + k];
         if (j0 + i < d.N) vb = d.B[(int64_t)(j0 + i) * d.ldb + k0 + k];
       }
-      As[k][i] = va;
-      Bs[k][i] = vb;
+      As[k][i] = (AccT)va;
+      Bs[k][i] = (AccT)vb;
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
       AccT av[4], bv[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = (AccT)As[k][tx + 16 * a];
+      for (int a = 0; a < 4; ++a) av[a] = As[k][tx + 16 * a];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = (AccT)Bs[k][ty + 16 * b];
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[k][ty + 16 * b];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
