@@ -28,6 +28,12 @@
 namespace cmsvd {
 namespace {
 
+#ifdef CMSVD_TC_PROF
+__device__ unsigned long long g_tc_prof[8];
+#define TC_T(slot) do { if (blockIdx.x < 148 && threadIdx.x == 0) { unsigned long long _t = clock64(); atomicAdd(&g_tc_prof[slot], _t - t_last); t_last = _t; } } while (0)
+#else
+#define TC_T(slot) do { } while (0)
+#endif
 constexpr int kTcThreads = 512;   // 16 warps: 4 per SM sub-partition (latency hiding for the staging)
 constexpr int KT = 32;                  // k elements per stage
 constexpr uint32_t LBO = 144, SBO = 1152;
@@ -115,18 +121,57 @@ __device__ __forceinline__ void stage_kcontig(uint8_t* hi, uint8_t* lo, int rows
   }
 }
 
-// Stage a (128 x 32) tile whose source is contiguous along rows:
-// element (r, k) = src[(k0 + k)*ld + r0 + r] for r0 + r < rmax, k0 + k < kmax; else 0.
-// Lanes over rows (coalesced per column), 4 columns gathered per 16 B store.
-__device__ __forceinline__ void stage_rcontig(uint8_t* hi, uint8_t* mi, uint8_t* lo, const float* __restrict__ src,
-                                              int64_t ld, int64_t r0, int64_t rmax, int k0, int kmax) {
-  const int r = threadIdx.x & 127;          // 128 rows; the two thread halves take alternate k quads
+// Split-phase staging (software pipelining): the global loads of stage i+1 are issued into registers
+// before stage i's barrier and MMAs, and converted/stored one iteration later.
+constexpr int kItK = 128 / (kTcThreads / 8);          // k-contiguous tile: row groups per thread
+constexpr int kItR = KT / 4 / (kTcThreads / 128);      // row-contiguous tile: k quads per thread
+
+template <bool NC>
+__device__ __forceinline__ void load_kcontig(float4 (&v)[kItK], int rows, const float* __restrict__ src, int64_t ld,
+                                             int nrows, int64_t k0, int64_t kmax) {
+  const int tid = threadIdx.x;
+  const int c = tid & 7;
+  const bool vec = ((ld & 3) == 0) && ((k0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+  const int64_t k = k0 + 4 * c;
+#pragma unroll
+  for (int i = 0; i < kItK; ++i) {
+    const int r = (tid >> 3) + i * (kTcThreads / 8);
+    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < rows && r < nrows) {
+      const float* p = src + (int64_t)r * ld + k;
+      if (vec && k + 3 < kmax) {
+        v[i] = ldf4<NC>(p);
+      } else {
+        if (k + 0 < kmax) v[i].x = ldf<NC>(p + 0);
+        if (k + 1 < kmax) v[i].y = ldf<NC>(p + 1);
+        if (k + 2 < kmax) v[i].z = ldf<NC>(p + 2);
+        if (k + 3 < kmax) v[i].w = ldf<NC>(p + 3);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void store_kcontig(const float4 (&v)[kItK], uint8_t* hi, uint8_t* lo, int rows,
+                                              uint8_t* mi) {
+  const int tid = threadIdx.x;
+  const int c = tid & 7;
+#pragma unroll
+  for (int i = 0; i < kItK; ++i) {
+    const int r = (tid >> 3) + i * (kTcThreads / 8);
+    if (r < rows) {
+      if (mi) st_split4_3(hi, mi, lo, poff(r, 4 * c), v[i]);
+      else st_split4(hi, lo, poff(r, 4 * c), v[i]);
+    }
+  }
+}
+
+__device__ __forceinline__ void load_rcontig(float4 (&v)[kItR], const float* __restrict__ src, int64_t ld, int64_t r0,
+                                             int64_t rmax, int k0, int kmax) {
+  const int r = threadIdx.x & 127;
   const int h = threadIdx.x >> 7;
   const bool rok = (r0 + r) < rmax;
-  constexpr int NQ = KT / 4 / (kTcThreads / 128);
-  float4 v[NQ];
 #pragma unroll
-  for (int t = 0; t < NQ; ++t) {
+  for (int t = 0; t < kItR; ++t) {
     const int kq = h + t * (kTcThreads / 128);
     v[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int k = k0 + 4 * kq;
@@ -138,8 +183,13 @@ __device__ __forceinline__ void stage_rcontig(uint8_t* hi, uint8_t* mi, uint8_t*
       if (k + 3 < kmax) v[t].w = __ldg(p + 3 * ld);
     }
   }
+}
+
+__device__ __forceinline__ void store_rcontig(const float4 (&v)[kItR], uint8_t* hi, uint8_t* mi, uint8_t* lo) {
+  const int r = threadIdx.x & 127;
+  const int h = threadIdx.x >> 7;
 #pragma unroll
-  for (int t = 0; t < NQ; ++t) {
+  for (int t = 0; t < kItR; ++t) {
     const uint32_t o = poff(r, 4 * (h + t * (kTcThreads / 128)));
     if (mi) st_split4_3(hi, mi, lo, o, v[t]);
     else st_split4(hi, lo, o, v[t]);
@@ -271,17 +321,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   const uint32_t idesc_z = tc::make_idesc_tf32(128, wp);
   constexpr int kBlk = 128 / KT;  // stages per K block
 
+#ifdef CMSVD_TC_PROF
+  unsigned long long t_last = clock64();
+#endif
   // ---------------- phase 1: Z = Q^T F (K = m) ----------------
   if (w > 0) {
     int it = 0;
     const int nst = (int)((m + KT - 1) / KT);
+    float4 qa[kItK], fb[kItK];
+    load_kcontig<true>(qa, 128, Q, m, q, 0, m);
+    load_kcontig<true>(fb, wp, F, m, w, 0, m);
     for (; it < nst; ++it) {
-      const int64_t k0 = (int64_t)it * KT;
       const int s = it & 1;
       const int blk = it / kBlk, slot = blk & 1;
       acquire(s);
-      stage_kcontig<true>(stage_ptr(s, 0), stage_ptr(s, 1), 128, Q, m, q, k0, m);
-      stage_kcontig<true>(stage_ptr(s, 2), stage_ptr(s, 3), wp, F, m, w, k0, m);
+      store_kcontig(qa, stage_ptr(s, 0), stage_ptr(s, 1), 128, nullptr);
+      store_kcontig(fb, stage_ptr(s, 2), stage_ptr(s, 3), wp, nullptr);
+      if (it + 1 < nst) {  // next stage's loads fly during this stage's barrier and MMAs
+        const int64_t k1 = (int64_t)(it + 1) * KT;
+        load_kcontig<true>(qa, 128, Q, m, q, k1, m);
+        load_kcontig<true>(fb, wp, F, m, w, k1, m);
+      }
       tc::fence_proxy_async();
       tc::fence_before();
       __syncthreads();
@@ -322,20 +382,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   tc::fence_after();
   sum_empty = true;
 
+  TC_T(0);  // phase 1 incl. Z drain
   // ---------------- phase 2: per 128-row tile, R' = F - Q Z, W' += R'^T R' ----------------
   const uint32_t idesc_r = tc::make_idesc_tf32(128, wp);
   const uint32_t idesc_w = tc::make_idesc_tf32(128, wp);
   int it = 0;
+  float4 qv[kItR], zv[kItK];
+  if (w > 0 && m > 0) {
+    load_rcontig(qv, Q, m, 0, m, 0, q);
+    load_kcontig<false>(zv, wp, Zg, QMAX, w, 0, q);
+  }
   for (int64_t m0 = 0; m0 < m && w > 0; m0 += 128) {
     // R accumulator over a-chunks of 32
     bool r_first = true;
     for (int a0 = 0; a0 < q; a0 += KT, ++it) {
       const int s = it & 1;
       acquire(s);
-      // R' = F - Q Z is a cancellation (||R'|| << ||F||): its product uses the 3-way split
-      stage_rcontig(stage_ptr(s, 0), kSplit3R ? stage_ptr(s, 4) : nullptr, stage_ptr(s, 1), Q, m, m0, m, a0, q);
-      stage_kcontig<false>(stage_ptr(s, 2), stage_ptr(s, 3), wp, Zg, QMAX, w, a0, q,
-                           kSplit3R ? stage_ptr(s, 5) : nullptr);
+      store_rcontig(qv, stage_ptr(s, 0), kSplit3R ? stage_ptr(s, 4) : nullptr, stage_ptr(s, 1));
+      store_kcontig(zv, stage_ptr(s, 2), stage_ptr(s, 3), wp, kSplit3R ? stage_ptr(s, 5) : nullptr);
+      {  // next stage (possibly the first of the next tile): its loads also cover the epilogue
+        int64_t nm0 = m0;
+        int na0 = a0 + KT;
+        if (na0 >= q) { na0 = 0; nm0 = m0 + 128; }
+        if (nm0 < m) {
+          load_rcontig(qv, Q, m, nm0, m, na0, q);
+          load_kcontig<false>(zv, wp, Zg, QMAX, w, na0, q);
+        }
+      }
       tc::fence_proxy_async();
       tc::fence_before();
       __syncthreads();
@@ -353,11 +426,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
       used[s] = 1;
       r_first = false;
     }
+    TC_T(1);  // staging + R' MMA issue
     if (tid == 0) tc::mma_commit(&bar_done);
     tc::mbar_wait(&bar_done, ph_done);
     ph_done ^= 1;
     for (int s = 0; s < 2; ++s) acquire(s);
     tc::fence_after();
+    TC_T(2);  // wait for R' MMAs
     // epilogue: rows r = 32*wq + lane of this tile -> R' into chunk buffer wq (columns of this warp's half)
     // chunk buffer (hi, lo) wq: operand with rows = b (128), k = r_local (32)
     uint8_t* chi = sm + (uint32_t)wq * 2 * kTile;
@@ -386,6 +461,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
         *reinterpret_cast<float*>(clo + o) = l;
       }
     }
+    TC_T(3);  // epilogue (TMEM -> F - QZ -> split -> smem)
     tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
@@ -400,8 +476,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
     tc::mbar_wait(&bar_done, ph_done);
     ph_done ^= 1;
     tc::fence_after();
+    TC_T(4);  // W' MMAs
     drain_add(t_w);          // this tile's W' contribution -> fp32 registers (round-to-nearest)
     tc::fence_before();
+    TC_T(5);  // drain
   }
   // ---------------- W' (rows b = 32*wq + lane) from the running sum ----------------
   if (w > 0) {
