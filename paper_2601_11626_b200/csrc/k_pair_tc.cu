@@ -277,11 +277,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   const uint32_t t_z0 = tmem, t_r = tmem, t_w = tmem + 128, t_sum = tmem + 256;
   const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
   const int c_lo = kColW * half, c_hi = min(wp, kColW * half + kColW);
-  uint32_t ph_stage[2] = {0, 0}, ph_done = 0, ph_slot[2] = {0, 0};
-  int used[2] = {0, 0};  // MMAs outstanding on a stage
+  // per-stage / per-slot mbarrier phases and "MMAs outstanding" flags as bit masks (bit s), so that the
+  // runtime stage index never forces them into local memory
+  uint32_t ph_stage = 0, ph_done = 0, ph_slot = 0, used = 0;
   auto stage_ptr = [&](int s, int which) { return sm + s * kStage + which * kTile; };
   auto acquire = [&](int s) {
-    if (used[s]) { tc::mbar_wait(&bar_stage[s], ph_stage[s]); ph_stage[s] ^= 1; used[s] = 0; }
+    if ((used >> s) & 1u) {
+      tc::mbar_wait(&bar_stage[s], (ph_stage >> s) & 1u);
+      ph_stage ^= 1u << s;
+      used &= ~(1u << s);
+    }
   };
   // The tensor core accumulates fp32 with truncation: the bias grows linearly with the number of
   // accumulations (measured 1.3e-5 relative at K = 2048).  Accumulation chains in TMEM are therefore
@@ -352,12 +357,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
         tc::mma_commit(&bar_stage[s]);
         if ((it % kBlk) == kBlk - 1 || it == nst - 1) tc::mma_commit(&bar_slot[slot]);
       }
-      used[s] = 1;
+      used |= 1u << s;
       // once block blk is issued, drain block blk-1 (its slot is reused by block blk+1)
       if (((it % kBlk) == kBlk - 1 || it == nst - 1) && blk >= 1) {
         const int ps = (blk - 1) & 1;
-        tc::mbar_wait(&bar_slot[ps], ph_slot[ps]);
-        ph_slot[ps] ^= 1;
+        tc::mbar_wait(&bar_slot[ps], (ph_slot >> ps) & 1u);
+        ph_slot ^= 1u << ps;
         tc::fence_after();
         drain_add(t_z0 + 128 * ps);
         tc::fence_before();
@@ -365,8 +370,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
     }
     {  // last block
       const int lb = (nst - 1) / kBlk, ls = lb & 1;
-      tc::mbar_wait(&bar_slot[ls], ph_slot[ls]);
-      ph_slot[ls] ^= 1;
+      tc::mbar_wait(&bar_slot[ls], (ph_slot >> ls) & 1u);
+      ph_slot ^= 1u << ls;
       tc::fence_after();
       drain_add(t_z0 + 128 * ls);
     }
@@ -423,11 +428,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
                    tc::smem_u32(stage_ptr(s, 3)), idesc_r, r_first);
         tc::mma_commit(&bar_stage[s]);
       }
-      used[s] = 1;
+      used |= 1u << s;
       r_first = false;
     }
     TC_T(1);  // staging + R' MMA issue
     if (tid == 0) tc::mma_commit(&bar_done);
+    // the epilogue's F values (rows 32*wq + lane of this tile, this warp's 32 columns), loaded while
+    // the tensor core finishes R'
+    const int64_t grow_e = m0 + 32 * wq + lane;
+    const int c0_e = kColW * half;
+    float fpre[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int bcol = c0_e + j;
+      fpre[j] = (c0_e < wp && bcol < w && grow_e < m) ? __ldg(F + (int64_t)bcol * m + grow_e) : 0.f;
+    }
     tc::mbar_wait(&bar_done, ph_done);
     ph_done ^= 1;
     for (int s = 0; s < 2; ++s) acquire(s);
@@ -453,7 +468,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
       for (int j = 0; j < 32; ++j) {
         const int bcol = c0 + j;
         float rv = 0.f;
-        if (c0 < wp && bcol < w && grow < m) rv = __ldg(F + (int64_t)bcol * m + grow) - v[j];
+        if (c0 < wp && bcol < w && grow < m) rv = fpre[j] - v[j];
         float h, l;
         tc::split_tf32(rv, h, l);
         const uint32_t o = poff(bcol, lane);
