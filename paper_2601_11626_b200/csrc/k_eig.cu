@@ -422,8 +422,36 @@ __host__ __device__ constexpr int rr_pow2(int x) { return x <= 1 ? 1 : x <= 2 ? 
 // One pass over the live chunks (column chunks c >= KC, row chunks s >= KC/2):
 // UPD: a -= v w^T + w v^T;  MV: row partials of a u -> part[wid], mirrored
 // column partials -> cs (butterfly over lanes), u^T a u partial -> red[wid].
-template <int S, int C, int KC, bool UPD, bool MV>
-__device__ __forceinline__ void rr_pass(double (&a)[S][C], const int lane, const int wid,
+// Matrix storage policies of the register-resident kernels: the chunks of one problem live either in
+// the thread's registers (RegAcc) or, for a second problem sharing the CTA, in shared memory with the
+// same ownership (SmemAcc: present chunk q of thread t at A[q * kRRThreads + t], conflict-free).
+template <int S, int C>
+struct RegAcc {
+  double (&a)[S][C];
+  __device__ __forceinline__ double ld(int s, int c) const { return a[s][c]; }
+  __device__ __forceinline__ void st(int s, int c, double x) const { a[s][c] = x; }
+};
+template <int S, int C>
+__host__ __device__ constexpr int rr_qidx(int s, int c) {  // ordinal of present chunk (s, c), row-major
+  int q = 0;
+  for (int s2 = 0; s2 < S; ++s2)
+    for (int c2 = 0; c2 < C; ++c2) {
+      if (s2 == s && c2 == c) return q;
+      if (16 * c2 <= 32 * s2 + 31) ++q;
+    }
+  return q;
+}
+template <int S, int C>
+__host__ __device__ constexpr int rr_nchunks() { return rr_qidx<S, C>(S, 0); }
+template <int S, int C>
+struct SmemAcc {
+  double* A;   // this thread's column: A + tid
+  __device__ __forceinline__ double ld(int s, int c) const { return A[rr_qidx<S, C>(s, c) * kRRThreads]; }
+  __device__ __forceinline__ void st(int s, int c, double x) const { A[rr_qidx<S, C>(s, c) * kRRThreads] = x; }
+};
+
+template <int S, int C, int KC, bool UPD, bool MV, class ACC>
+__device__ __forceinline__ void rr_pass(ACC a, const int lane, const int wid,
                                         const double* __restrict__ v, const double* __restrict__ w,
                                         const double* __restrict__ u, double* __restrict__ part,
                                         double* __restrict__ cs, double* __restrict__ red, const int pub_j,
@@ -451,10 +479,10 @@ __device__ __forceinline__ void rr_pass(double (&a)[S][C], const int lane, const
 #pragma unroll
     for (int s = S0; s < S; ++s)
       if (rr_present(s, c)) {
-        double x = a[s][c];
+        double x = a.ld(s, c);
         if (UPD) {
           x = fma(-vi[s], wj, fma(-wi[s], vj, x));
-          a[s][c] = x;
+          a.st(s, c, x);
         }
         if (MV) {
           pr[s] = fma(x, uj, pr[s]);
@@ -464,7 +492,7 @@ __device__ __forceinline__ void rr_pass(double (&a)[S][C], const int lane, const
     if (j == pub_j) {  // this warp owns the column the next reflector is built from: publish it
 #pragma unroll
       for (int s = S0; s < S; ++s)
-        if (rr_present(s, c)) colbuf[lane + 32 * s] = a[s][c];
+        if (rr_present(s, c)) colbuf[lane + 32 * s] = a.ld(s, c);
     }
     if (MV && c < CL) dd = fma(uj, pc[c], dd);
   }
@@ -500,13 +528,13 @@ __device__ __forceinline__ void rr_pass(double (&a)[S][C], const int lane, const
   if (lane == 0) red[wid] = dd;
 }
 
-template <int S, int C, bool UPD, bool MV>
-__device__ __forceinline__ void rr_pass_kc(int kc, double (&a)[S][C], const int lane, const int wid,
+template <int S, int C, bool UPD, bool MV, class ACC>
+__device__ __forceinline__ void rr_pass_kc(int kc, ACC a, const int lane, const int wid,
                                            const double* v, const double* w, const double* u, double* part,
                                            double* cs, double* red, int pub_j, double* colbuf) {
 #define RR_CASE(K)                                                                                           \
   case K:                                                                                                    \
-    if (K < C) rr_pass<S, C, (K < C ? K : 0), UPD, MV>(a, lane, wid, v, w, u, part, cs, red, pub_j, colbuf); \
+    if (K < C) rr_pass<S, C, (K < C ? K : 0), UPD, MV, ACC>(a, lane, wid, v, w, u, part, cs, red, pub_j, colbuf); \
     break;
   switch (kc) {
     RR_CASE(0) RR_CASE(1) RR_CASE(2) RR_CASE(3) RR_CASE(4) RR_CASE(5) RR_CASE(6) RR_CASE(7)
@@ -528,13 +556,13 @@ __device__ __forceinline__ double tree16(const double* x, int stride) {
   return t[0] + t[1];
 }
 
-template <int S, int C>
-__device__ __forceinline__ void rr_column(int ck, const double (&a)[S][C], double* x) {
+template <int S, int C, class ACC>
+__device__ __forceinline__ void rr_column(int ck, ACC a, double* x) {
 #pragma unroll
   for (int s = 0; s < S; ++s) x[s] = 0.0;
 #define RR_COL(K)                                                      \
   case K:                                                              \
-    _Pragma("unroll") for (int s = 0; s < S; ++s) if (K < C && rr_present(s, K)) x[s] = a[s][K < C ? K : 0]; \
+    _Pragma("unroll") for (int s = 0; s < S; ++s) if (K < C && rr_present(s, K)) x[s] = a.ld(s, K < C ? K : 0); \
     break;
   switch (ck) {
     RR_COL(0) RR_COL(1) RR_COL(2) RR_COL(3) RR_COL(4) RR_COL(5) RR_COL(6) RR_COL(7)
@@ -566,14 +594,15 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
     if (tid == 0) { cnt_out[p] = 0; trace_out[p] = 0.0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; }
     return;
   }
-  double a[S][C];
+  double a_[S][C];
+  const RegAcc<S, C> a{a_};
 #pragma unroll
   for (int s = 0; s < S; ++s)
 #pragma unroll
     for (int c = 0; c < C; ++c)
       if (rr_present(s, c)) {
         const int i = lane + 32 * s, j = wid + 16 * c;
-        a[s][c] = (i < n && j < n) ? Gp[(int64_t)j * ld_in + i] : 0.0;
+        a_[s][c] = (i < n && j < n) ? Gp[(int64_t)j * ld_in + i] : 0.0;
       }
   if (wid == 0) {
     double t = 0.0;
@@ -632,13 +661,13 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
   if (n >= 3) {
     if (wid == 0) {
       double x[S];
-      rr_column<S, C>(0, a, x);
+      rr_column<S, C, RegAcc<S, C>>(0, a, x);
       reflector(0, x);
     }
     __syncthreads();
     // products with v_0; publish column 1 (reflector 1 is formed in the row phase of step 0)
-    if (s_tau[0] != 0.0) rr_pass<S, C, 0, false, true>(a, lane, wid, nullptr, nullptr, vb[0], part, cs, red, 1, colbuf);
-    else rr_pass<S, C, 0, false, false>(a, lane, wid, nullptr, nullptr, nullptr, part, cs, red, 1, colbuf);
+    if (s_tau[0] != 0.0) rr_pass<S, C, 0, false, true, RegAcc<S, C>>(a, lane, wid, nullptr, nullptr, vb[0], part, cs, red, 1, colbuf);
+    else rr_pass<S, C, 0, false, false, RegAcc<S, C>>(a, lane, wid, nullptr, nullptr, nullptr, part, cs, red, 1, colbuf);
     for (int k = 0; k + 2 < n; ++k) {
       const double* v = vb[k & 1];
       const double tau = s_tau[k & 1];
@@ -692,10 +721,10 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
       const bool mv = more && s_tau[k1 & 1] != 0.0;
       const double* u = vb[k1 & 1];
       const int pub = (k + 3 < n) ? k + 2 : -1;  // column of reflector k+2
-      if (tau != 0.0 && mv) rr_pass_kc<S, C, true, true>(k >> 4, a, lane, wid, v, wb, u, part, cs, red, pub, colbuf);
-      else if (tau != 0.0) rr_pass<S, C, 0, true, false>(a, lane, wid, v, wb, nullptr, part, cs, red, pub, colbuf);
-      else if (mv) rr_pass<S, C, 0, false, true>(a, lane, wid, nullptr, nullptr, u, part, cs, red, pub, colbuf);
-      else rr_pass<S, C, 0, false, false>(a, lane, wid, nullptr, nullptr, nullptr, part, cs, red, pub, colbuf);
+      if (tau != 0.0 && mv) rr_pass_kc<S, C, true, true, RegAcc<S, C>>(k >> 4, a, lane, wid, v, wb, u, part, cs, red, pub, colbuf);
+      else if (tau != 0.0) rr_pass<S, C, 0, true, false, RegAcc<S, C>>(a, lane, wid, v, wb, nullptr, part, cs, red, pub, colbuf);
+      else if (mv) rr_pass<S, C, 0, false, true, RegAcc<S, C>>(a, lane, wid, nullptr, nullptr, u, part, cs, red, pub, colbuf);
+      else rr_pass<S, C, 0, false, false, RegAcc<S, C>>(a, lane, wid, nullptr, nullptr, nullptr, part, cs, red, pub, colbuf);
     }
   }
   __syncthreads();
@@ -705,7 +734,7 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
     for (int jj = lo; jj < n; ++jj) {
       if (wid == (jj & 15)) {
         double x[S];
-        rr_column<S, C>(jj >> 4, a, x);
+        rr_column<S, C, RegAcc<S, C>>(jj >> 4, a, x);
         double dj = 0.0, ej = 0.0;
 #pragma unroll
         for (int s = 0; s < S; ++s) {
