@@ -787,6 +787,339 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
   }
 }
 
+template <int S>
+struct RRProb {
+  double vb[2][32 * S], wb[32 * S], part[kRRWarps * 32 * S], cs[32 * S], ds[32 * S], e2s[32 * S],
+      colbuf[32 * S];
+  double red[kRRWarps], red2[S], s_tau[2], s_alpha, s_dk;
+  unsigned long long bar2, bar3;
+};
+
+__device__ __forceinline__ void rr_mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void rr_mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+__device__ __forceinline__ void rr_mbar_wait(unsigned long long* b, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "RRW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra RRW_%=;\n\t"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ double rr_rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x * y;
+  double r = fma(-h, y, 0.5);
+  y = fma(y, r, y);
+  h = 0.5 * x * y;
+  r = fma(-h, y, 0.5);
+  return fma(y, r, y);
+}
+
+// reflector kk from the column held as x[s] = A(lane + 32 s, kk) by one warp (prologue, kk = 0)
+template <int S>
+__device__ __forceinline__ void rr_reflector_warp(RRProb<S>& P, int kk, const double* x, int n, int lane) {
+  double sg = 0.0, al = 0.0, dk = 0.0;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int i = lane + 32 * s;
+    if (i > kk + 1 && i < n) sg = fma(x[s], x[s], sg);
+    if (i == kk + 1) al = x[s];
+    if (i == kk) dk = x[s];
+  }
+  sg = warp_sum(sg);
+  al = __shfl_sync(0xffffffffu, al, (kk + 1) & 31);
+  dk = __shfl_sync(0xffffffffu, dk, kk & 31);
+  double tau, scale, ee;
+  if (sg == 0.0) {
+    tau = 0.0; scale = 0.0; ee = al * al;
+  } else {
+    const double x2 = fma(al, al, sg);
+    const double xn = x2 * rr_rsqrt_nr(x2);
+    const double beta = al >= 0.0 ? -xn : xn;
+    tau = (beta - al) * rcp_nr(beta);
+    scale = rcp_nr(al - beta);
+    ee = beta * beta;
+  }
+  if (lane == 0) { P.e2s[kk] = ee; P.ds[kk] = dk; P.s_tau[kk & 1] = tau; }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int i = lane + 32 * s;
+    P.vb[kk & 1][i] = (i == kk + 1) ? 1.0 : ((i > kk + 1 && i < n) ? x[s] * scale : 0.0);
+  }
+}
+
+// row phase of step k on the row threads t = 0..32S-1 (warps wr = 0..S-1 of the group); bar_id = the
+// group's named barrier for the norm
+template <int S>
+__device__ __forceinline__ void rr_row_phase(RRProb<S>& P, int k, int n, int t, int wr, int lane, int bar_id) {
+  constexpr int NR = 32 * S;
+  const double* v = P.vb[k & 1];
+  const double tau = P.s_tau[k & 1];
+  const int k1 = k + 1;
+  const bool more = k1 + 2 < n;
+  const double Kc = 0.5 * tau * tau * tree16(P.red, 1);
+  const double pt = P.cs[t] + tree16(&P.part[t], NR);
+  const double wt = (t > k && t < n && tau != 0.0) ? fma(tau, pt, -Kc * v[t]) : 0.0;
+  P.wb[t] = wt;
+  if (more) {
+    double y = P.colbuf[t];
+    if (tau != 0.0) {
+      const double pk1 = P.cs[k1] + tree16(&P.part[k1], NR);
+      const double wk1 = fma(tau, pk1, -Kc * v[k1]);
+      y = fma(-v[t], wk1, fma(-wt, v[k1], y));
+    }
+    double sq = (t > k1 + 1 && t < n) ? y * y : 0.0;
+    sq = warp_sum(sq);
+    if (lane == 0) P.red2[wr] = sq;
+    if (t == k1 + 1) P.s_alpha = y;
+    if (t == k1) P.s_dk = y;
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(NR) : "memory");
+    double sg = 0.0;
+#pragma unroll
+    for (int q = 0; q < S; ++q) sg += P.red2[q];
+    const double al = P.s_alpha;
+    double tau1, scale, ee;
+    if (sg == 0.0) {
+      tau1 = 0.0; scale = 0.0; ee = al * al;
+    } else {
+      const double x2 = fma(al, al, sg);
+      const double xn = x2 * rr_rsqrt_nr(x2);
+      const double beta = al >= 0.0 ? -xn : xn;
+      tau1 = (beta - al) * rcp_nr(beta);
+      scale = rcp_nr(al - beta);
+      ee = beta * beta;
+    }
+    if (t == 0) { P.e2s[k1] = ee; P.ds[k1] = P.s_dk; P.s_tau[k1 & 1] = tau1; }
+    P.vb[k1 & 1][t] = (t == k1 + 1) ? 1.0 : ((t > k1 + 1 && t < n) ? y * scale : 0.0);
+  }
+}
+
+// fused pass of step k (k = -1: prologue products with v_0 only), then arrive on B2
+template <int S, int C, class ACC>
+__device__ __forceinline__ void rr_fused_step(RRProb<S>& P, ACC a, int k, int n, int lane, int wid) {
+  const int k1 = k + 1;
+  if (k < 0) {
+    if (P.s_tau[0] != 0.0) rr_pass<S, C, 0, false, true, ACC>(a, lane, wid, nullptr, nullptr, P.vb[0], P.part, P.cs, P.red, 1, P.colbuf);
+    else rr_pass<S, C, 0, false, false, ACC>(a, lane, wid, nullptr, nullptr, nullptr, P.part, P.cs, P.red, 1, P.colbuf);
+  } else {
+    const double* v = P.vb[k & 1];
+    const double tau = P.s_tau[k & 1];
+    const bool more = k1 + 2 < n;
+    const bool mv = more && P.s_tau[k1 & 1] != 0.0;
+    const double* u = P.vb[k1 & 1];
+    const int pub = (k + 3 < n) ? k + 2 : -1;
+    if (tau != 0.0 && mv) rr_pass_kc<S, C, true, true, ACC>(k >> 4, a, lane, wid, v, P.wb, u, P.part, P.cs, P.red, pub, P.colbuf);
+    else if (tau != 0.0) rr_pass<S, C, 0, true, false, ACC>(a, lane, wid, v, P.wb, nullptr, P.part, P.cs, P.red, pub, P.colbuf);
+    else if (mv) rr_pass<S, C, 0, false, true, ACC>(a, lane, wid, nullptr, nullptr, u, P.part, P.cs, P.red, pub, P.colbuf);
+    else rr_pass<S, C, 0, false, false, ACC>(a, lane, wid, nullptr, nullptr, nullptr, P.part, P.cs, P.red, pub, P.colbuf);
+  }
+  rr_mbar_arrive(&P.bar2);
+}
+
+// d, e^2 of the trailing 2x2 (or n <= 2) from the matrix chunks
+template <int S, int C, class ACC>
+__device__ __forceinline__ void rr_tail(RRProb<S>& P, ACC a, int n, int lane, int wid) {
+  const int lo = n >= 2 ? n - 2 : 0;
+  for (int jj = lo; jj < n; ++jj) {
+    if (wid == (jj & 15)) {
+      double x[S];
+      rr_column<S, C, ACC>(jj >> 4, a, x);
+      double dj = 0.0, ej = 0.0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        if (i == jj) dj = x[s];
+        if (i == jj + 1) ej = x[s];
+      }
+      dj = __shfl_sync(0xffffffffu, dj, jj & 31);
+      ej = __shfl_sync(0xffffffffu, ej, (jj + 1) & 31);
+      if (lane == 0) {
+        P.ds[jj] = dj;
+        if (jj + 1 < n) P.e2s[jj] = ej * ej;
+      }
+    }
+  }
+}
+
+// outputs of one problem (threads of one half of the CTA: h = 0..255)
+template <int S>
+__device__ __forceinline__ void rr_outputs(RRProb<S>& P, int n, int p, int h, int hstride, const double* thr, int kw,
+                                           int nstride, double* dout, double* e2out, double* gsh, int* cnt_out) {
+  double* dO = dout + (int64_t)p * nstride;
+  double* eO = e2out + (int64_t)p * nstride;
+  for (int i = h; i < n; i += hstride) {
+    dO[i] = P.ds[i];
+    if (i + 1 < n) eO[i] = P.e2s[i];
+  }
+  if (h == 0) {
+    const double* d = P.ds;
+    const double* e2 = P.e2s;
+    double glo = 1e300, ghi = -1e300, emax = 0.0;
+    for (int i = 0; i < n; ++i) {
+      double r = 0.0;
+      if (i > 0) r += sqrt(e2[i - 1]);
+      if (i + 1 < n) r += sqrt(e2[i]);
+      glo = fmin(glo, d[i] - r);
+      ghi = fmax(ghi, d[i] + r);
+      if (i + 1 < n) emax = fmax(emax, e2[i]);
+    }
+    if (n <= 0) { glo = 0.0; ghi = 0.0; }
+    const double nrm = fmax(fmax(fabs(glo), fabs(ghi)), 1e-300);
+    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax) * 4.0;
+    glo -= 2.2e-16 * nrm * n + pivmin;
+    ghi += 2.2e-16 * nrm * n + pivmin;
+    gsh[4 * p] = glo; gsh[4 * p + 1] = ghi; gsh[4 * p + 2] = pivmin; gsh[4 * p + 3] = nrm;
+    int above = n;
+    if (thr && n > 0) {
+      const double t = thr[p];
+      if (t >= ghi) above = 0;
+      else if (t > glo) {
+        int c0, c1;
+        sturm2<double>(d, e2, n, t, t, pivmin, c0, c1);
+        above = n - c0;
+      }
+    }
+    cnt_out[p] = n > 0 ? min(kw, above) : 0;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Two problems per CTA with dedicated row warps (k_tridiag_duo, n <= 128).
+// Both problems' lower-triangle chunks live in shared memory (SmemAcc, 2 x 80 KB
+// at n = 128) with the ownership of k_tridiag_rr; 16 element warps run the
+// fused passes of both problems, S dedicated row warps (thread t = row t) run
+// the row phases.  A row phase only waits for its own problem's partial
+// products (mbarrier B2) and the element warps only for its results (mbarrier
+// B3), so the latency-bound row phase of one problem overlaps the fused pass
+// of the other:  element warps  F0(k) F1(k) F0(k+1) ...;  row warps  R0(k+1)
+// R1(k+1) ...  (R_p(k+1) needs F_p(k); F_p(k+1) needs R_p(k+1)).
+// ---------------------------------------------------------------------------
+constexpr int kDuoThreads = kRRThreads + 32 * 4;  // 16 element warps + up to 4 row warps (n <= 128)
+
+template <int S, int C>
+__global__ void __launch_bounds__(kDuoThreads, 1) k_tridiag_duo(const double* __restrict__ Gin, int64_t ld_in,
+                                                                int64_t stride_in, const int* __restrict__ ns,
+                                                                int nprob, const double* __restrict__ thr, int kw,
+                                                                int nstride, double* __restrict__ dout,
+                                                                double* __restrict__ e2out, double* __restrict__ gsh,
+                                                                int* __restrict__ cnt_out,
+                                                                double* __restrict__ trace_out) {
+  constexpr int NR = 32 * S;
+  constexpr int CL = 2 * (S - 1);
+  constexpr int NQ = rr_nchunks<S, C>();
+  static_assert(C == 2 * S && S <= 4, "duo kernel: n <= 128");
+  extern __shared__ __align__(16) unsigned char duo_smem[];
+  RRProb<S>* PP = reinterpret_cast<RRProb<S>*>(duo_smem);
+  double* A0 = reinterpret_cast<double*>(duo_smem + 2 * sizeof(RRProb<S>));
+  double* A1 = A0 + (size_t)NQ * kRRThreads;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool elem = tid < kRRThreads;
+  const int pa = 2 * blockIdx.x, pb = pa + 1;
+  const int n0 = ns[pa], n1 = (pb < nprob) ? ns[pb] : 0;
+  RRProb<S>& P0 = PP[0];
+  RRProb<S>& P1 = PP[1];
+  const SmemAcc<S, C> a0{A0 + (elem ? tid : 0)};
+  const SmemAcc<S, C> a1{A1 + (elem ? tid : 0)};
+  if (elem) {
+    const double* G0 = Gin + (int64_t)pa * stride_in;
+    const double* G1 = Gin + (int64_t)pb * stride_in;
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (rr_present(s, c)) {
+          const int i = lane + 32 * s, j = wid + 16 * c;
+          a0.st(s, c, (i < n0 && j < n0) ? G0[(int64_t)j * ld_in + i] : 0.0);
+          a1.st(s, c, (i < n1 && j < n1) ? G1[(int64_t)j * ld_in + i] : 0.0);
+        }
+    if (wid == 0 || wid == 8) {
+      const double* G = wid == 0 ? G0 : G1;
+      const int n = wid == 0 ? n0 : n1;
+      double t = 0.0;
+      for (int i = lane; i < n; i += 32) t += G[(int64_t)i * ld_in + i];
+      t = warp_sum(t);
+      if (lane == 0) {
+        if (wid == 0) trace_out[pa] = t;
+        else if (pb < nprob) trace_out[pb] = t;
+      }
+    }
+  }
+  for (int j = 16 * CL + tid; j < NR; j += kDuoThreads) { P0.cs[j] = 0.0; P1.cs[j] = 0.0; }
+  if (tid == 0) {
+    rr_mbar_init(&P0.bar2, kRRThreads);
+    rr_mbar_init(&P0.bar3, NR);
+    rr_mbar_init(&P1.bar2, kRRThreads);
+    rr_mbar_init(&P1.bar3, NR);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (wid == 0) {  // reflector 0 of each problem, by the owner warp of column 0
+    double x[S];
+    if (n0 >= 3) {
+      rr_column<S, C, SmemAcc<S, C>>(0, a0, x);
+      rr_reflector_warp<S>(P0, 0, x, n0, lane);
+    }
+    if (n1 >= 3) {
+      rr_column<S, C, SmemAcc<S, C>>(0, a1, x);
+      rr_reflector_warp<S>(P1, 0, x, n1, lane);
+    }
+  }
+  __syncthreads();
+  const int nsteps = max(n0, n1) - 2;
+  if (elem) {
+    if (n0 >= 3) rr_fused_step<S, C, SmemAcc<S, C>>(P0, a0, -1, n0, lane, wid);
+    if (n1 >= 3) rr_fused_step<S, C, SmemAcc<S, C>>(P1, a1, -1, n1, lane, wid);
+    for (int k = 0; k < nsteps; ++k) {
+      if (k + 2 < n0) {
+        rr_mbar_wait(&P0.bar3, k & 1);
+        rr_fused_step<S, C, SmemAcc<S, C>>(P0, a0, k, n0, lane, wid);
+      }
+      if (k + 2 < n1) {
+        rr_mbar_wait(&P1.bar3, k & 1);
+        rr_fused_step<S, C, SmemAcc<S, C>>(P1, a1, k, n1, lane, wid);
+      }
+    }
+  } else if (tid - kRRThreads < NR) {
+    const int t = tid - kRRThreads, wr = wid - kRRWarps;
+    for (int k = 0; k < nsteps; ++k) {
+      if (k + 2 < n0) {
+        rr_mbar_wait(&P0.bar2, k & 1);
+        rr_row_phase<S>(P0, k, n0, t, wr, lane, 1);
+        rr_mbar_arrive(&P0.bar3);
+      }
+      if (k + 2 < n1) {
+        rr_mbar_wait(&P1.bar2, k & 1);
+        rr_row_phase<S>(P1, k, n1, t, wr, lane, 2);
+        rr_mbar_arrive(&P1.bar3);
+      }
+    }
+  }
+  __syncthreads();
+  if (elem) {
+    rr_tail<S, C, SmemAcc<S, C>>(P0, a0, n0, lane, wid);
+    rr_tail<S, C, SmemAcc<S, C>>(P1, a1, n1, lane, wid);
+  }
+  __syncthreads();
+  if (tid < kDuoThreads / 2) rr_outputs<S>(P0, n0, pa, tid, kDuoThreads / 2, thr, kw, nstride, dout, e2out, gsh, cnt_out);
+  else if (pb < nprob) rr_outputs<S>(P1, n1, pb, tid - kDuoThreads / 2, kDuoThreads / 2, thr, kw, nstride, dout, e2out, gsh, cnt_out);
+}
+
+template <int S, int C>
+size_t duo_smem_bytes() {
+  return 2 * sizeof(RRProb<S>) + 2 * (size_t)rr_nchunks<S, C>() * kRRThreads * sizeof(double);
+}
+
 // ---------------------------------------------------------------------------
 // Plain bisection, one thread per wanted eigenvalue (high occupancy; the
 // tridiagonals are read through L1).  fp32 coarse phase on the normalised
@@ -1112,7 +1445,22 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   double* gsh = ee + (size_t)nprob * nstride;
   cudaError_t e;
   const bool use_rr = c.eig_rr && nmax <= 160;
-  if (use_rr) {
+  if (use_rr && c.eig_duo && nmax <= 128) {
+#define DUO_LAUNCH(S_, C_)                                                                                          \
+  do {                                                                                                              \
+    const size_t sm2 = duo_smem_bytes<S_, C_>();                                                                    \
+    e = cudaFuncSetAttribute(k_tridiag_duo<S_, C_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);         \
+    if (e != cudaSuccess) return e;                                                                                 \
+    k_tridiag_duo<S_, C_><<<(nprob + 1) / 2, kDuoThreads, sm2, c.stream>>>(G, ld_in, stride_in, d_ns, nprob, d_thr, \
+                                                                          kw, nstride, dd, ee, gsh, cnt, trace);    \
+  } while (0)
+    if (nmax <= 32) DUO_LAUNCH(1, 2);
+    else if (nmax <= 64) DUO_LAUNCH(2, 4);
+    else if (nmax <= 96) DUO_LAUNCH(3, 6);
+    else DUO_LAUNCH(4, 8);
+#undef DUO_LAUNCH
+    c.launches += 1;
+  } else if (use_rr) {
 #define RR_LAUNCH(S_, C_)                                                                                          \
   k_tridiag_rr<S_, C_><<<nprob, kRRThreads, 0, c.stream>>>(G, ld_in, stride_in, d_ns, d_thr, kw, nstride, dd, ee, \
                                                           gsh, cnt, trace)

@@ -28,17 +28,19 @@ int main(int argc, char** argv) {
   Ctx c; c.stream = 0;
   if (getenv("GLMB")) c.gl_batch_mb = atoi(getenv("GLMB"));
   double* scr; cudaMalloc(&scr, tridiag_scratch_bytes(P, n));
-  std::vector<double> evs[2];
-  std::vector<double> trs[2];
-  for (int variant = 0; variant < 2; ++variant) {
-  c.eig_rr = variant == 1;
+  std::vector<double> evs[3];
+  std::vector<double> trs[3];
+  const char* vname[3] = {"smem", "rr  ", "duo "};
+  for (int variant = 0; variant < 3; ++variant) {
+  c.eig_rr = variant >= 1;
+  c.eig_duo = variant == 2;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
     launch_tridiag_topk(c, dG, n, (int64_t)n * n, dn, P, n, nullptr, kw, ev, cnt, tr, scr);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
-    printf("%s n=%d P=%d kw=%d: %.3f ms  (%.2f us/problem/SM)  err=%s\n", variant ? "rr  " : "smem", n, P, kw, ms,
+    printf("%s n=%d P=%d kw=%d: %.3f ms  (%.2f us/problem/SM)  err=%s\n", vname[variant], n, P, kw, ms,
            ms * 1e3 * 148 / P, cudaGetErrorString(cudaGetLastError()));
   }
   evs[variant].resize((size_t)P * kw);
@@ -52,8 +54,9 @@ int main(int argc, char** argv) {
   const char* nm[8] = {"w1 fused+bfly", "w1 B2 wait", "owner pre", "owner nbar wait", "owner col upd", "owner reflector", "w1 phase2", "w1 B3 wait"};
   for (int q = 0; q < 8; ++q) printf("  %-18s %10.1f cycles/step\n", nm[q], hp[q] / 6.0 / (n - 2));
 #endif
-  double md = 0, mx = 0;
-  for (size_t q = 0; q < evs[0].size(); ++q) { md = fmax(md, fabs(evs[0][q] - evs[1][q])); mx = fmax(mx, fabs(evs[0][q])); }
+  double md = 0, mx = 0, md2 = 0;
+  for (size_t q = 0; q < evs[0].size(); ++q) { md = fmax(md, fabs(evs[0][q] - evs[1][q])); md2 = fmax(md2, fabs(evs[1][q] - evs[2][q])); mx = fmax(mx, fabs(evs[0][q])); }
+  printf("max |ev_rr - ev_duo| = %.3e\n", md2);
   double sd = 0;
   for (int q = 0; q < P; ++q) {
     double s0 = trs[0][q], s1 = trs[1][q];
