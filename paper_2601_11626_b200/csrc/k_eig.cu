@@ -1005,7 +1005,14 @@ __device__ __forceinline__ void rr_outputs(RRProb<S>& P, int n, int p, int h, in
 // of the other:  element warps  F0(k) F1(k) F0(k+1) ...;  row warps  R0(k+1)
 // R1(k+1) ...  (R_p(k+1) needs F_p(k); F_p(k+1) needs R_p(k+1)).
 // ---------------------------------------------------------------------------
-constexpr int kDuoThreads = kRRThreads + 32 * 4;  // 16 element warps + up to 4 row warps (n <= 128)
+#ifndef CMSVD_DUO_GROUPS
+#define CMSVD_DUO_GROUPS 1   // row-warp groups: 1 = shared by both problems, 2 = one per problem (measured: no gain at n = 128)
+#endif
+constexpr int kDuoGroups = CMSVD_DUO_GROUPS;
+constexpr int kDuoThreads = kRRThreads + 32 * 4 * kDuoGroups;  // 16 element warps + 4 row warps per group
+#ifndef CMSVD_DUO_REG0
+#define CMSVD_DUO_REG0 1   // problem 0 of the pair in registers (problem 1 in shared memory)
+#endif
 
 template <int S, int C>
 __global__ void __launch_bounds__(kDuoThreads, 1) k_tridiag_duo(const double* __restrict__ Gin, int64_t ld_in,
@@ -1029,7 +1036,14 @@ __global__ void __launch_bounds__(kDuoThreads, 1) k_tridiag_duo(const double* __
   const int n0 = ns[pa], n1 = (pb < nprob) ? ns[pb] : 0;
   RRProb<S>& P0 = PP[0];
   RRProb<S>& P1 = PP[1];
+#if CMSVD_DUO_REG0
+  double a0_[S][C];
+  const RegAcc<S, C> a0{a0_};
+  using Acc0 = RegAcc<S, C>;
+#else
   const SmemAcc<S, C> a0{A0 + (elem ? tid : 0)};
+  using Acc0 = SmemAcc<S, C>;
+#endif
   const SmemAcc<S, C> a1{A1 + (elem ? tid : 0)};
   if (elem) {
     const double* G0 = Gin + (int64_t)pa * stride_in;
@@ -1067,7 +1081,7 @@ __global__ void __launch_bounds__(kDuoThreads, 1) k_tridiag_duo(const double* __
   if (wid == 0) {  // reflector 0 of each problem, by the owner warp of column 0
     double x[S];
     if (n0 >= 3) {
-      rr_column<S, C, SmemAcc<S, C>>(0, a0, x);
+      rr_column<S, C, Acc0>(0, a0, x);
       rr_reflector_warp<S>(P0, 0, x, n0, lane);
     }
     if (n1 >= 3) {
@@ -1078,36 +1092,61 @@ __global__ void __launch_bounds__(kDuoThreads, 1) k_tridiag_duo(const double* __
   __syncthreads();
   const int nsteps = max(n0, n1) - 2;
   if (elem) {
-    if (n0 >= 3) rr_fused_step<S, C, SmemAcc<S, C>>(P0, a0, -1, n0, lane, wid);
+    if (n0 >= 3) rr_fused_step<S, C, Acc0>(P0, a0, -1, n0, lane, wid);
     if (n1 >= 3) rr_fused_step<S, C, SmemAcc<S, C>>(P1, a1, -1, n1, lane, wid);
+#ifdef CMSVD_RR_PROF
+    unsigned long long t_last = clock64();
+#endif
     for (int k = 0; k < nsteps; ++k) {
       if (k + 2 < n0) {
         rr_mbar_wait(&P0.bar3, k & 1);
-        rr_fused_step<S, C, SmemAcc<S, C>>(P0, a0, k, n0, lane, wid);
+        RR_T(0, wid == 1);
+        rr_fused_step<S, C, Acc0>(P0, a0, k, n0, lane, wid);
+        RR_T(1, wid == 1);
       }
       if (k + 2 < n1) {
         rr_mbar_wait(&P1.bar3, k & 1);
+        RR_T(2, wid == 1);
         rr_fused_step<S, C, SmemAcc<S, C>>(P1, a1, k, n1, lane, wid);
+        RR_T(3, wid == 1);
       }
     }
+  } else if (kDuoGroups == 2) {
+    // one row-warp group per problem: the two row phases run concurrently
+    const int g = (tid - kRRThreads) / 128, t = (tid - kRRThreads) % 128, wr = t >> 5;
+    RRProb<S>& P = g == 0 ? P0 : P1;
+    const int n = g == 0 ? n0 : n1;
+    if (t < NR)
+      for (int k = 0; k + 2 < n; ++k) {
+        rr_mbar_wait(&P.bar2, k & 1);
+        rr_row_phase<S>(P, k, n, t, wr, lane, 1 + g);
+        rr_mbar_arrive(&P.bar3);
+      }
   } else if (tid - kRRThreads < NR) {
     const int t = tid - kRRThreads, wr = wid - kRRWarps;
+#ifdef CMSVD_RR_PROF
+    unsigned long long t_last = clock64();
+#endif
     for (int k = 0; k < nsteps; ++k) {
       if (k + 2 < n0) {
         rr_mbar_wait(&P0.bar2, k & 1);
+        RR_T(4, wr == 0);
         rr_row_phase<S>(P0, k, n0, t, wr, lane, 1);
         rr_mbar_arrive(&P0.bar3);
+        RR_T(5, wr == 0);
       }
       if (k + 2 < n1) {
         rr_mbar_wait(&P1.bar2, k & 1);
+        RR_T(6, wr == 0);
         rr_row_phase<S>(P1, k, n1, t, wr, lane, 2);
         rr_mbar_arrive(&P1.bar3);
+        RR_T(7, wr == 0);
       }
     }
   }
   __syncthreads();
   if (elem) {
-    rr_tail<S, C, SmemAcc<S, C>>(P0, a0, n0, lane, wid);
+    rr_tail<S, C, Acc0>(P0, a0, n0, lane, wid);
     rr_tail<S, C, SmemAcc<S, C>>(P1, a1, n1, lane, wid);
   }
   __syncthreads();

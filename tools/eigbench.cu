@@ -51,8 +51,8 @@ int main(int argc, char** argv) {
 #ifdef CMSVD_RR_PROF
   unsigned long long hp[8];
   cudaMemcpyFromSymbol(hp, g_rr_prof, sizeof(hp));
-  const char* nm[8] = {"w1 fused+bfly", "w1 B2 wait", "owner pre", "owner nbar wait", "owner col upd", "owner reflector", "w1 phase2", "w1 B3 wait"};
-  for (int q = 0; q < 8; ++q) printf("  %-18s %10.1f cycles/step\n", nm[q], hp[q] / 6.0 / (n - 2));
+  const char* nm[8] = {"elem wait B3_0", "elem F0", "elem wait B3_1", "elem F1", "row wait B2_0", "row R0", "row wait B2_1", "row R1"};
+  for (int q = 0; q < 8; ++q) printf("  %-18s %10.1f cycles/step\n", nm[q], hp[q] / 3.0 / (n - 2));
 #endif
   double md = 0, mx = 0, md2 = 0;
   for (size_t q = 0; q < evs[0].size(); ++q) { md = fmax(md, fabs(evs[0][q] - evs[1][q])); md2 = fmax(md2, fabs(evs[1][q] - evs[2][q])); mx = fmax(mx, fabs(evs[0][q])); }
