@@ -137,3 +137,29 @@ def test_c3_tight_variants(cm):
         out = ctx.pair_errors_tight(pairs, operand=cm.TRUNC)
     assert_err2(out["err2x"][:, 0], ref[:, 0], tot, "config3 residual(U_r)")
     assert_err2(out["err2x"][:, 1], ref[:, 1], tot, "config3 per-index Weyl")
+
+
+def _subset_spectra(col, ids):
+    """Oracle spectra of a subset of blocks (the oracle's per-block results do not depend on the rest)."""
+    return oracle.block_spectra(np.ascontiguousarray(col.blocks[ids]))
+
+
+@pytest.mark.parametrize("name", ["config3", "config4"])
+def test_full_size_sampled_pairs(cm, name):
+    """BASELINE.json's full-size configs 3 (256 x 1024^2, r = 128) and 4 (64 x 4096^2, r = 256) in the
+    bench launch configuration (all blocks registered, all-pairs chunking), sampled pairs checked
+    against the oracle evaluated on just the blocks they touch."""
+    col = synth.make_config(name)
+    ids = [0, 1, 2, col.N - 1] if name == "config3" else [0, 5, col.N - 1]
+    sp = _subset_spectra(col, ids)
+    sub_pairs = np.array([[a, b] for a in range(len(ids)) for b in range(len(ids)) if a != b], np.int32)
+    ref = oracle.pair_errors(sp, sub_pairs, col.r, 7, oracle.TRUNC)
+    full_pairs = np.array([[ids[a], ids[b]] for a, b in sub_pairs], np.int32)
+    with cm.Context(0) as ctx:
+        ctx.register(torch.from_numpy(col.blocks).cuda())
+        E, sig, rank = ctx.block_spectra(col.r)
+        out = ctx.pair_errors(full_pairs, kinds=7, operand=cm.TRUNC)
+    refs = np.stack([s[:col.r] for s in sp.sig])
+    assert_sigma(sig[ids], refs, refs[:, 0], f"{name} block sigma")
+    assert np.allclose(E[ids], sp.E, rtol=1e-12)
+    compare(out, ref, 7, f"{name} full size")
