@@ -249,9 +249,11 @@ def test_c2_regimes(c2):
 
 
 # --------------------------------------------------------------- config 5 --
-@pytest.mark.parametrize("r", [16, 64])
-def test_c5_knn_sample(cm, r):
-    col = synth.config5(N=512, r=r)
+@pytest.mark.parametrize("N,r", [(512, 16), (512, 64), (2048, 64)])
+def test_c5_knn_sample(cm, N, r):
+    """Config 5 scaling sweep sizes (N in {512, 2048}, r in {16, 64}): sampled pairs of the full
+    registered collection against the oracle."""
+    col = synth.config5(N=N, r=r)
     sp = oracle.block_spectra(col.blocks)
     ctx, E, sig, rank = gpu_ctx(cm, col.blocks, r)
     R = np.random.default_rng(5)
