@@ -1263,7 +1263,14 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
     }
   }
   __syncthreads();
+#ifdef CMSVD_SYEV_PROF
+  unsigned long long t0 = clock64();
+#endif
   tri_reduce<true>(A, n, lda, vA, vB, w, part, e2, ee, VH, tauH);
+#ifdef CMSVD_SYEV_PROF
+  __syncthreads();
+  unsigned long long t1 = clock64();
+#endif
   __syncthreads();
   for (int i = tid; i < n; i += kTriThreads) dd[i] = A[(int64_t)i * lda + i];
   if (tid == 0) {
@@ -1399,6 +1406,9 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
     if (s_fail) break;
   }
   __syncthreads();
+#ifdef CMSVD_SYEV_PROF
+  unsigned long long t2 = clock64();
+#endif
   // ---- back-transformation Z <- H_0 H_1 ... H_{n-3} Z (thread per column) ----
   for (int k = n - 3; k >= 0; --k) {
     const double tk = tauH[k];
@@ -1414,6 +1424,10 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
     }
     __syncthreads();
   }
+#ifdef CMSVD_SYEV_PROF
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    printf("syev n=%d: tridiag %llu  QL %llu  backtransform %llu cycles (iters %d)\n", n, t1 - t0, t2 - t1, clock64() - t2, s_iters);
+#endif
   // ---- sort (non-increasing, ties by index) and write ----
   for (int i = tid; i < n; i += kTriThreads) {
     const double li = dd[i];
