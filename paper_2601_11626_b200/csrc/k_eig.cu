@@ -321,7 +321,6 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __rest
   double* __restrict__ e2 = pp + n;
   double* __restrict__ part = e2 + n;                   // kTriWarps x n row-partials
   double* __restrict__ d = part;                        // aliases part at the end
-  __shared__ double red[2][kTriWarps];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double* Gp = Gin + (int64_t)p * stride_in;
   double* dO = dout + (int64_t)p * nstride;
@@ -496,7 +495,7 @@ __device__ __forceinline__ void rr_pass(ACC a, const int lane, const int wid,
     }
     if (MV && c < CL) dd = fma(uj, pc[c], dd);
   }
-  if (!MV) return;
+  if constexpr (MV) {
 #pragma unroll
   for (int s = S0; s < S; ++s) dd = fma(ui[s], pr[s], dd);
   if (CL > 0) {  // recursive-halving butterfly: lane ends with the sum of chunk lane >> (5 - log2 C2)
@@ -526,6 +525,7 @@ __device__ __forceinline__ void rr_pass(ACC a, const int lane, const int wid,
   for (int s = S0; s < S; ++s) part[wid * NR + lane + 32 * s] = pr[s];
   dd = warp_sum(dd);
   if (lane == 0) red[wid] = dd;
+  }
 }
 
 template <int S, int C, bool UPD, bool MV, class ACC>

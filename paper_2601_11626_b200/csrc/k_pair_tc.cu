@@ -83,44 +83,6 @@ __device__ __forceinline__ float4 ldf4(const float* p) {
   return NC ? __ldg(reinterpret_cast<const float4*>(p)) : __ldcg(reinterpret_cast<const float4*>(p));
 }
 
-// NC = true: read-only path (inputs); false: L2 path (data written earlier in this kernel)
-template <bool NC>
-__device__ __forceinline__ void stage_kcontig(uint8_t* hi, uint8_t* lo, int rows, const float* __restrict__ src,
-                                              int64_t ld, int nrows, int64_t k0, int64_t kmax,
-                                              uint8_t* mi = nullptr) {
-  const int tid = threadIdx.x;
-  const int c = tid & 7;
-  const bool vec = ((ld & 3) == 0) && ((k0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-  const int64_t k = k0 + 4 * c;
-  constexpr int kIt = 128 / (kTcThreads / 8);   // up to 8 row groups per thread
-  float4 v[kIt];
-  // issue every global load of this thread before any shared store (memory-level parallelism)
-#pragma unroll
-  for (int i = 0; i < kIt; ++i) {
-    const int r = (tid >> 3) + i * (kTcThreads / 8);
-    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < rows && r < nrows) {
-      const float* p = src + (int64_t)r * ld + k;
-      if (vec && k + 3 < kmax) {
-        v[i] = ldf4<NC>(p);
-      } else {
-        if (k + 0 < kmax) v[i].x = ldf<NC>(p + 0);
-        if (k + 1 < kmax) v[i].y = ldf<NC>(p + 1);
-        if (k + 2 < kmax) v[i].z = ldf<NC>(p + 2);
-        if (k + 3 < kmax) v[i].w = ldf<NC>(p + 3);
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < kIt; ++i) {
-    const int r = (tid >> 3) + i * (kTcThreads / 8);
-    if (r < rows) {
-      if (mi) st_split4_3(hi, mi, lo, poff(r, 4 * c), v[i]);
-      else st_split4(hi, lo, poff(r, 4 * c), v[i]);
-    }
-  }
-}
-
 // Split-phase staging (software pipelining): the global loads of stage i+1 are issued into registers
 // before stage i's barrier and MMAs, and converted/stored one iteration later.
 constexpr int kItK = 128 / (kTcThreads / 8);          // k-contiguous tile: row groups per thread
