@@ -185,6 +185,22 @@ cmsvd_status cmsvd_pair_errors_tight(cmsvd_ctx ctx, const int32_t* pairs, int64_
 cmsvd_status cmsvd_cluster_verify(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters,
                                   double* exact_err2, double* total, int64_t* mem);
 
+/* Predicted errors of given block sequences -- the estimates of the paper's estimator
+ * conservativeness diagnostic (slack Delta = predicted - exact; SURVEY.md
+ * §8(f) N2).  Sequence s is ids[offs[s] .. offs[s+1]) (host arrays, non-empty, block ids
+ * < count), the blocks in append order.  For each sequence:
+ *   err2[3s + 0] Weyl bound, Eq. 5 over its K blocks;
+ *   err2[3s + 1] residual bound: Alg. 2's state after appending blocks 2..K to block 1
+ *                (Thm 2 / Cor 1);
+ *   err2[3s + 2] incremental estimate: Alg. 3's state after the same appends (Lemma 1,
+ *                Cor 3, Cor 2);
+ *   total[s]     sum of the members' energies.
+ * A single block gives its own truncation error for every kind; kinds not requested give
+ * NaN.  The exact error of the concatenation comes from cmsvd_cluster_verify.
+ * Errors as cmsvd_cluster (CMSVD_E_SHAPE for the residual kind on blocks wider than 512). */
+cmsvd_status cmsvd_sequence_errors(cmsvd_ctx ctx, const int32_t* offs, const int32_t* ids, int32_t nseq, int32_t r,
+                                   uint32_t kinds, int operand, double* err2, double* total);
+
 /* Greedy clustering (Appendix E). */
 enum { CMSVD_ALG_MAX_NORM = 0, CMSVD_ALG_RESIDUAL = 1, CMSVD_ALG_APPROX = 2 };
 enum { CMSVD_SORT_FROBENIUS = 0, CMSVD_SORT_RESIDUAL = 1 };

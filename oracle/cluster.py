@@ -134,7 +134,11 @@ class _ResidualState:
         R, s, Ur, mu = data
         if s.size and s[0] > 0:
             keep = s > TAU * s[0]
-            self.Q = np.concatenate([self.Q, Ur[:, keep]], axis=1)
+            # the range basis grows to at most m columns ("Q grows to <= m
+            # columns"): once Q spans R^m the residual is rounding noise and adds no direction
+            room = self.Q.shape[0] - self.Q.shape[1]
+            idx = np.flatnonzero(keep)[:max(room, 0)]
+            self.Q = np.concatenate([self.Q, Ur[:, idx]], axis=1)
         self.mu = mu
         self.E += Ej
 
@@ -242,3 +246,32 @@ def compression(m: int, ncols, clusters, r: int):
         mem.append(min(m * Nc, rc * (m + Nc)))
     mem = np.array(mem, dtype=np.int64)
     return mem, float(m * np.sum(ncols)) / float(np.sum(mem))
+
+
+def sequence_errors(spec: Spectra, seqs, r: int, kinds: int = 7, operand: int = RAW):
+    """Predicted rank-r errors of given block sequences (clusters in append order) --
+    the slack diagnostic's estimates: for each sequence
+    (A_1, ..., A_K): Weyl = Eq. 5 over the K blocks; residual =
+    Alg. 2's state after appending A_2..A_K to A_1 (Thm 2 / Cor 1); incremental =
+    Alg. 3's state after the same appends (Lemma 1 + Cor 3 + Cor 2).  A single block
+    gives its own truncation error for every kind.  Returns (err2 (S, 3), total (S,))."""
+    S = len(seqs)
+    err2 = np.full((S, 3), np.nan)
+    total = np.zeros(S)
+    for s, seq in enumerate(seqs):
+        seq = [int(b) for b in seq]
+        tot = float(sum(spec.E[b] for b in seq))
+        total[s] = tot
+        if kinds & 1:
+            top = max(float(np.sum(spec.sig[b][:r] ** 2)) for b in seq)
+            err2[s, 0] = min(max(tot - top, 0.0), tot)
+        for bit, col, State in ((2, 1, _ResidualState), (4, 2, _IncrementalState)):
+            if not kinds & bit:
+                continue
+            st = State(spec, seq[0], r)
+            e2 = st.err2()
+            for b in seq[1:]:
+                e2, _, data = st.tentative(_operand(spec, b, r, operand), float(spec.E[b]))
+                st.commit(float(spec.E[b]), data)
+            err2[s, col] = min(max(e2, 0.0), tot)
+    return err2, total

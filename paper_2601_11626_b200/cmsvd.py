@@ -26,7 +26,8 @@ SORT_FROBENIUS, SORT_RESIDUAL = 0, 1
 
 EXPORTS = ["cmsvd_status_string", "cmsvd_last_error", "cmsvd_version", "cmsvd_create", "cmsvd_destroy",
            "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_pair_errors_tight",
-           "cmsvd_cluster", "cmsvd_cluster_verify", "cmsvd_launch_count", "cmsvd_profile_enable",
+           "cmsvd_cluster", "cmsvd_cluster_verify", "cmsvd_sequence_errors", "cmsvd_launch_count",
+           "cmsvd_profile_enable",
            "cmsvd_profile_read"]
 
 
@@ -73,6 +74,8 @@ def load(path: str = LIB_PATH):
     L.cmsvd_pair_errors_tight.argtypes = [vp, vp, i64, i32, ctypes.c_int, ctypes.c_int, vp, vp]
     L.cmsvd_pair_errors_tight.restype = ctypes.c_int
     L.cmsvd_cluster.argtypes = [vp, ctypes.POINTER(ClusterOpts), vp, vp, vp, vp, vp, vp]
+    L.cmsvd_sequence_errors.restype = ctypes.c_int
+    L.cmsvd_sequence_errors.argtypes = [vp, vp, vp, i32, i32, u32, ctypes.c_int, vp, vp]
     L.cmsvd_cluster_verify.restype = ctypes.c_int
     L.cmsvd_cluster_verify.argtypes = [vp, i32, vp, i32, vp, vp, vp]
     L.cmsvd_launch_count.restype = i64
@@ -245,6 +248,21 @@ class Context:
         self._check(self._L.cmsvd_pair_errors_tight(self._h, _ptr(pairs), P, r, operand, HOST, _ptr(err2x),
                                                     _ptr(total)))
         return {"err2x": err2x, "total": total}
+
+    # -- cmsvd_sequence_errors (N2) ----------------------------------------
+    def sequence_errors(self, seqs, r: int | None = None, kinds: int = ALL, operand: int = RAW):
+        """Predicted errors of block sequences (lists of block ids in append order):
+        {"err2": (S, 3) [weyl, residual, incremental], "total": (S,)}."""
+        r = self.r if r is None else r
+        offs = np.zeros(len(seqs) + 1, np.int32)
+        offs[1:] = np.cumsum([len(q) for q in seqs])
+        ids = np.ascontiguousarray(np.concatenate([np.asarray(q, np.int32) for q in seqs]) if seqs else
+                                   np.zeros(0, np.int32), dtype=np.int32)
+        e2 = np.zeros((len(seqs), 3))
+        tot = np.zeros(len(seqs))
+        self._check(self._L.cmsvd_sequence_errors(self._h, _ptr(offs), _ptr(ids), len(seqs), int(r), kinds, operand,
+                                                  _ptr(e2), _ptr(tot)))
+        return {"err2": e2, "total": tot}
 
     # -- cmsvd_cluster_verify (N1) -----------------------------------------
     def cluster_verify(self, assign, r: int | None = None):

@@ -159,6 +159,18 @@ cmsvd_status cmsvd_cluster_verify(cmsvd_ctx ctx, int32_t r, const int32_t* assig
   }
 }
 
+cmsvd_status cmsvd_sequence_errors(cmsvd_ctx ctx, const int32_t* offs, const int32_t* ids, int32_t nseq, int32_t r,
+                                   uint32_t kinds, int operand, double* err2, double* total) {
+  GUARD_CTX(ctx);
+  try {
+    return do_sequence_errors(c, offs, ids, nseq, r, kinds, operand, err2, total);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "sequence_errors: host allocation failed");
+  } catch (...) {
+    return fail(c, CMSVD_E_ARG, "sequence_errors: unexpected exception");
+  }
+}
+
 cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_t* assign, int32_t* order,
                            int32_t* n_clusters, double* cluster_err2, double* cluster_total, int64_t* n_evals) {
   GUARD_CTX(ctx);

@@ -348,6 +348,74 @@ struct Driver {
 
 }  // namespace
 
+// Predicted errors of given block sequences (clusters in append order), the estimates of the
+// slack diagnostic: Weyl = Eq. 5 over the K blocks; residual /
+// incremental = the Alg. 2 / Alg. 3 state after appending blocks 2..K to block 1 in order, each append
+// one tentative evaluation + commit on the GPU (the drivers' own machinery).  A single block gives its
+// own truncation error for every kind.
+Status do_sequence_errors(Ctx& c, const int32_t* offs, const int32_t* ids, int32_t nseq, int32_t r, uint32_t kinds,
+                          int operand, double* err2, double* total) {
+  if (nseq < 0 || !offs || (nseq > 0 && (!ids || !err2 || !total)))
+    return fail(c, CMSVD_E_ARG, "sequence_errors: bad arguments");
+  if (c.count <= 0 || c.spectra_r <= 0) return fail(c, CMSVD_E_STATE, "sequence_errors: call block_spectra first");
+  if (r != c.spectra_r) return fail(c, CMSVD_E_STATE, "sequence_errors: r differs from the block_spectra r");
+  if ((kinds & ~7u) != 0 || kinds == 0) return fail(c, CMSVD_E_ARG, "sequence_errors: bad kinds mask");
+  if (operand != CMSVD_OPERAND_RAW && operand != CMSVD_OPERAND_TRUNC)
+    return fail(c, CMSVD_E_ARG, "sequence_errors: bad operand");
+  if (c.big && (kinds & CMSVD_RESIDUAL))
+    return fail(c, CMSVD_E_SHAPE, "sequence_errors: the residual state needs an explicit range basis (A22)");
+  for (int32_t s = 0; s < nseq; ++s) {
+    if (offs[s + 1] <= offs[s]) return fail(c, CMSVD_E_ARG, "sequence_errors: empty sequence " + std::to_string(s));
+    for (int32_t t = offs[s]; t < offs[s + 1]; ++t)
+      if (ids[t] < 0 || ids[t] >= c.count)
+        return fail(c, CMSVD_E_SHAPE, "sequence_errors: block id out of range in sequence " + std::to_string(s));
+  }
+  const int nmax = c.nmax;
+  auto top_r = [&](int b) {
+    const double* sg = &c.sig[(size_t)b * nmax];
+    double t = 0.0;
+    for (int l = 0; l < std::min(r, c.kcols[b]); ++l) t += sg[l] * sg[l];
+    return t;
+  };
+  for (int32_t s = 0; s < nseq; ++s) {
+    const int32_t* seq = ids + offs[s];
+    const int K = offs[s + 1] - offs[s];
+    double tot = 0.0, top = 0.0;
+    for (int t = 0; t < K; ++t) { tot += c.E[seq[t]]; top = std::max(top, top_r(seq[t])); }
+    total[s] = tot;
+    auto clampv = [&](double v) { return std::min(std::max(v, 0.0), tot); };
+    err2[3 * s + 0] = (kinds & CMSVD_WEYL) ? clampv(tot - top) : std::nan("");
+    for (int kk = 1; kk <= 2; ++kk) {
+      const unsigned bit = kk == 1 ? CMSVD_RESIDUAL : CMSVD_INCREMENTAL;
+      if (!(kinds & bit)) { err2[3 * s + kk] = std::nan(""); continue; }
+      if (K == 1) { err2[3 * s + kk] = clampv(c.E[seq[0]] - top_r(seq[0])); continue; }
+      cmsvd_cluster_opts o{};
+      o.algorithm = kk == 1 ? CMSVD_ALG_RESIDUAL : CMSVD_ALG_APPROX;
+      o.sort = CMSVD_SORT_FROBENIUS;
+      o.knn = 1;
+      o.operand = operand;
+      o.r = r;
+      o.eps = 0.5;
+      Driver d(c, o);
+      Status st = d.setup();
+      if (st != CMSVD_OK) return st;
+      st = d.init_state(seq[0]);
+      if (st != CMSVD_OK) return st;
+      double e = 0.0;
+      for (int t = 1; t < K; ++t) {
+        std::vector<double> e2v, totv;
+        st = d.evaluate(std::vector<int>{seq[t]}, e2v, totv);
+        if (st != CMSVD_OK) return st;
+        e = e2v[0];
+        st = d.commit(seq[t], e);
+        if (st != CMSVD_OK) return st;
+      }
+      err2[3 * s + kk] = clampv(e);
+    }
+  }
+  return CMSVD_OK;
+}
+
 Status do_cluster(Ctx& c, const cmsvd_cluster_opts* o, int32_t* assign, int32_t* order, int32_t* n_clusters,
                   double* cluster_err2, double* cluster_total, int64_t* n_evals) {
   if (!o) return fail(c, CMSVD_E_ARG, "cluster: opts is NULL");

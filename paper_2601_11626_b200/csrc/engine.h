@@ -41,6 +41,8 @@ Dims block_dims(const Ctx& c, int operand);
 cudaError_t launch_check_pairs(Ctx& c, const int2* d_pairs, int64_t P, int count, int* d_bad);
 Status do_cluster_verify(Ctx& c, int32_t r, const int32_t* assign, int32_t n_clusters, double* exact_err2,
                          double* total, int64_t* mem);
+Status do_sequence_errors(Ctx& c, const int32_t* offs, const int32_t* ids, int32_t nseq, int32_t r, uint32_t kinds,
+                          int operand, double* err2, double* total);
 Status do_cluster(Ctx& c, const cmsvd_cluster_opts* o, int32_t* assign, int32_t* order, int32_t* n_clusters,
                   double* cluster_err2, double* cluster_total, int64_t* n_evals);
 

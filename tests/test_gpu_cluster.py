@@ -221,3 +221,29 @@ def test_cluster_verify_c2_row_gram(cm):
     assert np.all(v["rel"] <= 0.05)
     mem, ratio = oc.compression(col.m, sp.n, groups, col.r)
     assert np.array_equal(v["mem"], mem)
+
+
+@pytest.mark.parametrize("name", ["config1", "config2"])
+def test_sequence_errors_vs_oracle(cm, name):
+    """N2: Weyl / residual / incremental estimates of random block sequences (K = 1..6, the slack
+    diagnostic's inputs) against the oracle's state machines; every estimate >= the exact error of
+    the explicit concatenation (GPU cluster_verify)."""
+    from tolerances import assert_err2
+    col = synth.make_config(name)
+    sp = oracle.block_spectra(col.blocks)
+    R = np.random.default_rng(11)
+    seqs = [list(map(int, R.choice(col.N, size=int(R.integers(1, 7)), replace=False))) for _ in range(10)]
+    ref, tot = oc.sequence_errors(sp, seqs, col.r)
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        ctx.block_spectra(col.r)
+        out = ctx.sequence_errors(seqs)
+        ex = []
+        for q in seqs:     # exact error of each sequence's concatenation: one cluster of its members
+            assign = np.ones(col.N, np.int32)
+            assign[q] = 0
+            ex.append(ctx.cluster_verify(assign)["exact_err2"][0])
+    assert np.allclose(out["total"], tot, rtol=1e-12)
+    for k, nm in enumerate(["weyl", "residual", "incremental"]):
+        assert_err2(out["err2"][:, k], ref[:, k], tot, f"{name} sequence {nm}")
+        assert np.all(out["err2"][:, k] >= np.asarray(ex) * (1 - 2e-3) - 1e-7 * tot)

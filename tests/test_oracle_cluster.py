@@ -109,3 +109,24 @@ def test_compression_closed_forms():
     # a compressible pair next to raw singletons
     mem, ratio = compression(12800, np.full(4, 20), [[0, 1], [2], [3]], 20)
     assert list(mem) == [20 * (12800 + 40), 12800 * 20, 12800 * 20]
+
+
+def test_sequence_errors_pins():
+    """N2 estimates of block sequences: a 2-block sequence equals the pair estimators (same
+    definitions), every estimate of a K-block sequence is >= the exact error of the explicit
+    concatenation (Thm 1, Cor 1, F3), and a single block gives its own tail for every kind."""
+    col = synth.config1()
+    sp = oracle.block_spectra(col.blocks)
+    r = col.r
+    R = np.random.default_rng(3)
+    e2, tot = oc.sequence_errors(sp, [[3, 7]], r)
+    pe = oracle.pair_errors(sp, [[3, 7]], r, 7)
+    assert np.allclose(e2[0], pe.err2[0], rtol=1e-12, atol=1e-12 * tot[0])
+    seqs = [list(R.choice(col.N, size=int(R.integers(1, 7)), replace=False)) for _ in range(12)]
+    e2, tot = oc.sequence_errors(sp, seqs, r)
+    ex = oracle.exact_groups(sp, seqs, r)
+    for s, seq in enumerate(seqs):
+        assert np.all(e2[s] >= ex[s] - 1e-9 * tot[s]), (seq, e2[s], ex[s])
+        if len(seq) == 1:
+            tail = float(np.sum(sp.sig[seq[0]][r:] ** 2))
+            assert np.allclose(e2[s], tail, rtol=1e-9, atol=1e-9 * tot[s])
