@@ -185,6 +185,19 @@ cmsvd_status cmsvd_pair_errors_tight(cmsvd_ctx ctx, const int32_t* pairs, int64_
 cmsvd_status cmsvd_cluster_verify(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters,
                                   double* exact_err2, double* total, int64_t* mem);
 
+/* The compressed representation of a partition: for each
+ * cluster c (ids 0..n_clusters-1 of assign[count], host arrays) the rank-r_c truncated SVD of the
+ * concatenation M_c of its blocks in ascending block order, r_c = min(r, m, N_c), stored as
+ *   Ũ_c = U_c S_c  (m x r_c, fp32, column-major) at Ut + sum_{c'<c} m r_c', and
+ *   V_c            (N_c x r_c, fp32, column-major; rows follow the member blocks' columns)
+ *                  at V + sum_{c'<c} N_c' r_c',
+ * so that block i of cluster c is reconstructed as Ũ_c V_{c,i}^T; rc[c] = r_c.
+ * Directions with sigma <= 1e-5 sigma_1 are returned as zero columns.  The caller allocates
+ * Ut (sum_c m r_c floats), V (sum_c N_c r_c floats) and rc (n_clusters); host memory.
+ * Errors: as cmsvd_cluster_verify. */
+cmsvd_status cmsvd_cluster_factors(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters, float* Ut,
+                                   float* V, int32_t* rc);
+
 /* Predicted errors of given block sequences -- the estimates of the paper's estimator
  * conservativeness diagnostic (slack Delta = predicted - exact; SURVEY.md
  * §8(f) N2).  Sequence s is ids[offs[s] .. offs[s+1]) (host arrays, non-empty, block ids

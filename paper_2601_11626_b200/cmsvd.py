@@ -26,7 +26,8 @@ SORT_FROBENIUS, SORT_RESIDUAL = 0, 1
 
 EXPORTS = ["cmsvd_status_string", "cmsvd_last_error", "cmsvd_version", "cmsvd_create", "cmsvd_destroy",
            "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_pair_errors_tight",
-           "cmsvd_cluster", "cmsvd_cluster_verify", "cmsvd_sequence_errors", "cmsvd_launch_count",
+           "cmsvd_cluster", "cmsvd_cluster_verify", "cmsvd_cluster_factors", "cmsvd_sequence_errors",
+           "cmsvd_launch_count",
            "cmsvd_profile_enable",
            "cmsvd_profile_read"]
 
@@ -76,6 +77,8 @@ def load(path: str = LIB_PATH):
     L.cmsvd_cluster.argtypes = [vp, ctypes.POINTER(ClusterOpts), vp, vp, vp, vp, vp, vp]
     L.cmsvd_sequence_errors.restype = ctypes.c_int
     L.cmsvd_sequence_errors.argtypes = [vp, vp, vp, i32, i32, u32, ctypes.c_int, vp, vp]
+    L.cmsvd_cluster_factors.restype = ctypes.c_int
+    L.cmsvd_cluster_factors.argtypes = [vp, i32, vp, i32, vp, vp, vp]
     L.cmsvd_cluster_verify.restype = ctypes.c_int
     L.cmsvd_cluster_verify.argtypes = [vp, i32, vp, i32, vp, vp, vp]
     L.cmsvd_launch_count.restype = i64
@@ -263,6 +266,29 @@ class Context:
         self._check(self._L.cmsvd_sequence_errors(self._h, _ptr(offs), _ptr(ids), len(seqs), int(r), kinds, operand,
                                                   _ptr(e2), _ptr(tot)))
         return {"err2": e2, "total": tot}
+
+    # -- cmsvd_cluster_factors (N1 codec) ----------------------------------
+    def cluster_factors(self, assign, r: int | None = None):
+        """Per-cluster factors of the rank-r truncated SVD of each concatenation: a list of
+        (members, Ut (m x r_c), V (N_c x r_c)); block i is reconstructed as Ut @ V_i.T."""
+        r = self.r if r is None else r
+        assign = np.ascontiguousarray(assign, dtype=np.int32)
+        nc = int(assign.max()) + 1 if assign.size else 0
+        members = [np.flatnonzero(assign == c) for c in range(nc)]
+        ncols = [int(np.sum(self._ncols[mb])) for mb in members]
+        rcs = [min(r, self.m, n) for n in ncols]
+        Ut = np.zeros(sum(self.m * k for k in rcs), np.float32)
+        V = np.zeros(sum(n * k for n, k in zip(ncols, rcs)), np.float32)
+        rc = np.zeros(nc, np.int32)
+        self._check(self._L.cmsvd_cluster_factors(self._h, int(r), _ptr(assign), nc, _ptr(Ut), _ptr(V), _ptr(rc)))
+        out, uo, vo = [], 0, 0
+        for c in range(nc):
+            k = int(rc[c])
+            out.append((members[c], Ut[uo:uo + self.m * k].reshape(k, self.m).T,
+                        V[vo:vo + ncols[c] * k].reshape(k, ncols[c]).T))
+            uo += self.m * k
+            vo += ncols[c] * k
+        return out
 
     # -- cmsvd_cluster_verify (N1) -----------------------------------------
     def cluster_verify(self, assign, r: int | None = None):

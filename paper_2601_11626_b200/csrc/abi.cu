@@ -171,6 +171,18 @@ cmsvd_status cmsvd_sequence_errors(cmsvd_ctx ctx, const int32_t* offs, const int
   }
 }
 
+cmsvd_status cmsvd_cluster_factors(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters, float* Ut,
+                                   float* V, int32_t* rc) {
+  GUARD_CTX(ctx);
+  try {
+    return do_cluster_factors(c, r, assign, n_clusters, Ut, V, rc);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "cluster_factors: host allocation failed");
+  } catch (...) {
+    return fail(c, CMSVD_E_ARG, "cluster_factors: unexpected exception");
+  }
+}
+
 cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_t* assign, int32_t* order,
                            int32_t* n_clusters, double* cluster_err2, double* cluster_total, int64_t* n_evals) {
   GUARD_CTX(ctx);

@@ -39,6 +39,8 @@ Status do_pair_errors_tight(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, 
                             double* err2x, double* total);
 Dims block_dims(const Ctx& c, int operand);
 cudaError_t launch_check_pairs(Ctx& c, const int2* d_pairs, int64_t P, int count, int* d_bad);
+Status do_cluster_factors(Ctx& c, int32_t r, const int32_t* assign, int32_t n_clusters, float* Ut, float* V,
+                          int32_t* rc_out);
 Status do_cluster_verify(Ctx& c, int32_t r, const int32_t* assign, int32_t n_clusters, double* exact_err2,
                          double* total, int64_t* mem);
 Status do_sequence_errors(Ctx& c, const int32_t* offs, const int32_t* ids, int32_t nseq, int32_t r, uint32_t kinds,

@@ -200,4 +200,124 @@ Status do_cluster_verify(Ctx& c, int32_t r, const int32_t* assign, int32_t n_clu
   return CMSVD_OK;
 }
 
+// Factors of each cluster's rank-r truncated SVD M_c ~ U_c S_c V_c^T: Ũ_c = U_c S_c
+// (m x r_c) and V_c (N_c x r_c), from the Gram eigenvectors.  Column Gram (N_c <= m): V = eigenvectors,
+// Ũ = M V.  Row Gram (m < N_c): U = eigenvectors, Ũ = U S, V = M^T U S^-1.  fp64 accumulation.
+// One thread per output element; the eigenvector of the l-th largest eigenvalue is column perm[l] of Ev.
+__global__ void k_cluster_factors(int64_t m, int ncol, int dim, int rc, bool rows, const float* __restrict__ X,
+                                  const double* __restrict__ Ev, const int* __restrict__ perm,
+                                  const double* __restrict__ lam, float* __restrict__ Ut, float* __restrict__ V) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nU = m * rc, nV = (int64_t)ncol * rc;
+  if (e >= nU + nV) return;
+  const double s1 = sqrt(fmax(lam[0], 0.0));
+  if (e < nU) {                                  // Ũ[i, l]
+    const int l = (int)(e / m);
+    const int64_t i = e % m;
+    const double sl = sqrt(fmax(lam[l], 0.0));
+    const double* ev = Ev + (int64_t)perm[l] * dim;
+    double acc = 0.0;
+    if (rows) acc = ev[i] * sl;                  // U S
+    else
+      for (int k = 0; k < ncol; ++k) acc = fma((double)X[(int64_t)k * m + i], ev[k], acc);   // M V
+    Ut[(int64_t)l * m + i] = (sl > 1e-5 * s1) ? (float)acc : 0.f;
+  } else {                                       // V[k, l]
+    const int64_t f = e - nU;
+    const int l = (int)(f / ncol);
+    const int k = (int)(f % ncol);
+    const double sl = sqrt(fmax(lam[l], 0.0));
+    const double* ev = Ev + (int64_t)perm[l] * dim;
+    double acc = 0.0;
+    if (rows) {
+      for (int64_t i = 0; i < m; ++i) acc = fma((double)X[(int64_t)k * m + i], ev[i], acc);   // (M^T U)[k, l]
+      acc = (sl > 1e-5 * s1) ? acc / sl : 0.0;
+    } else {
+      acc = (sl > 1e-5 * s1) ? ev[k] : 0.0;
+    }
+    V[(int64_t)l * ncol + k] = (float)acc;
+  }
+}
+
+Status do_cluster_factors(Ctx& c, int32_t r, const int32_t* assign, int32_t n_clusters, float* Ut, float* Vout,
+                          int32_t* rc_out) {
+  if (c.count <= 0) return fail(c, CMSVD_E_STATE, "cluster_factors: no collection registered");
+  if (r < 1 || n_clusters < 0 || !assign) return fail(c, CMSVD_E_ARG, "cluster_factors: need r >= 1, assign");
+  if (n_clusters == 0) return CMSVD_OK;
+  if (!Ut || !Vout || !rc_out) return fail(c, CMSVD_E_ARG, "cluster_factors: outputs are required");
+  const int N = c.count;
+  const int64_t m = c.m;
+  std::vector<std::vector<int>> members(n_clusters);
+  for (int i = 0; i < N; ++i) {
+    if (assign[i] < 0 || assign[i] >= n_clusters)
+      return fail(c, CMSVD_E_ARG, "cluster_factors: assign[" + std::to_string(i) + "] out of range");
+    members[assign[i]].push_back(i);
+  }
+  size_t uo = 0, vo = 0;
+  for (int g = 0; g < n_clusters; ++g) {
+    if (members[g].empty()) return fail(c, CMSVD_E_ARG, "cluster_factors: empty cluster " + std::to_string(g));
+    int64_t nc = 0;
+    for (int i : members[g]) nc += c.n[i];
+    const int64_t dim = std::min<int64_t>(m, nc);
+    if (dim > kEigMax)
+      return fail(c, CMSVD_E_SHAPE, "cluster_factors: min(m, N_c) > " + std::to_string(kEigMax));
+    const int rc = (int)std::min<int64_t>(r, dim);
+    // one cluster at a time: gather, Gram, eigenvectors, factors
+    CKV(ensure(c.ws[WS_A], (size_t)m * nc * 4), "cluster_factors: concatenation");
+    CKV(ensure(c.ws[WS_G], (size_t)dim * dim * 8), "cluster_factors: Gram");
+    CKV(ensure(c.ws[WS_V], (size_t)dim * dim * 8 * 2), "cluster_factors: vectors");
+    CKV(ensure(c.ws[WS_EV], (size_t)dim * 8 + 64), "cluster_factors: eigenvalues");
+    CKV(ensure(c.ws[WS_PERM], (size_t)dim * 4 + 64), "cluster_factors: perm");
+    CKV(ensure(c.ws[WS_STAT], 64), "cluster_factors: status");
+    CKV(ensure(c.ws[WS_META], 64), "cluster_factors: meta");
+    CKV(ensure(c.ws[WS_OUT], (size_t)(m + nc) * rc * 4 + 64), "cluster_factors: out");
+    float* X = (float*)c.ws[WS_A].p;
+    int64_t col = 0;
+    for (int i : members[g]) {
+      CKV(cudaMemcpyAsync(X + col * m, (const float*)c.arena.p + c.boff[i], (size_t)m * c.n[i] * 4,
+                          cudaMemcpyDeviceToDevice, c.stream),
+          "cluster_factors: gather");
+      col += c.n[i];
+    }
+    const bool rows = nc > m;
+    const float* hx[1] = {X};
+    double* hg[1] = {(double*)c.ws[WS_G].p};
+    const int hn[1] = {(int)nc};
+    const int hd[1] = {(int)dim};
+    char* mb = (char*)c.ws[WS_META].p;
+    CKV(cudaMemcpyAsync(mb, hx, 8, cudaMemcpyHostToDevice, c.stream), "cluster_factors: h2d");
+    CKV(cudaMemcpyAsync(mb + 8, hg, 8, cudaMemcpyHostToDevice, c.stream), "cluster_factors: h2d");
+    CKV(cudaMemcpyAsync(mb + 16, hn, 4, cudaMemcpyHostToDevice, c.stream), "cluster_factors: h2d");
+    CKV(cudaMemcpyAsync(mb + 20, hd, 4, cudaMemcpyHostToDevice, c.stream), "cluster_factors: h2d");
+    const unsigned tiles = (unsigned)((dim + 63) / 64);
+    if (rows) k_gram<true><<<dim3(tiles, tiles, 1), 256, 0, c.stream>>>((const float* const*)mb, (const int*)(mb + 16), m,
+                                                                   (double* const*)(mb + 8), dim);
+    else k_gram<false><<<dim3(tiles, tiles, 1), 256, 0, c.stream>>>((const float* const*)mb, (const int*)(mb + 16), m,
+                                                                (double* const*)(mb + 8), dim);
+    c.launches += 1;
+    CKV(cudaGetLastError(), "cluster_factors: Gram");
+    double* Ev = (double*)c.ws[WS_V].p;
+    CKV(launch_syev(c, (const double*)c.ws[WS_G].p, dim, dim * dim, (const int*)(mb + 20), 1, (int)dim, Ev, dim * dim,
+                    Ev + dim * dim, (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, dim, (int*)c.ws[WS_STAT].p),
+        "cluster_factors: eigenvectors");
+    float* dU = (float*)c.ws[WS_OUT].p;
+    float* dVo = dU + (size_t)m * rc;
+    const int64_t tot = (m + nc) * rc;
+    k_cluster_factors<<<(unsigned)((tot + 255) / 256), 256, 0, c.stream>>>(
+        m, (int)nc, (int)dim, rc, rows, X, Ev, (const int*)c.ws[WS_PERM].p, (const double*)c.ws[WS_EV].p, dU, dVo);
+    c.launches += 1;
+    CKV(cudaGetLastError(), "cluster_factors: factors");
+    int st = 0;
+    CKV(cudaMemcpyAsync(&st, c.ws[WS_STAT].p, 4, cudaMemcpyDeviceToHost, c.stream), "cluster_factors: d2h");
+    CKV(cudaMemcpyAsync(Ut + uo, dU, (size_t)m * rc * 4, cudaMemcpyDeviceToHost, c.stream), "cluster_factors: d2h");
+    CKV(cudaMemcpyAsync(Vout + vo, dVo, (size_t)nc * rc * 4, cudaMemcpyDeviceToHost, c.stream), "cluster_factors: d2h");
+    CKV(cudaStreamSynchronize(c.stream), "cluster_factors: sync");
+    if (st < 0) return fail(c, CMSVD_E_NOCONV, "cluster_factors: eigensolver did not converge for cluster " +
+                                                   std::to_string(g));
+    rc_out[g] = rc;
+    uo += (size_t)m * rc;
+    vo += (size_t)nc * rc;
+  }
+  return CMSVD_OK;
+}
+
 }  // namespace cmsvd

@@ -247,3 +247,33 @@ def test_sequence_errors_vs_oracle(cm, name):
     for k, nm in enumerate(["weyl", "residual", "incremental"]):
         assert_err2(out["err2"][:, k], ref[:, k], tot, f"{name} sequence {nm}")
         assert np.all(out["err2"][:, k] >= np.asarray(ex) * (1 - 2e-3) - 1e-7 * tot)
+
+
+@pytest.mark.parametrize("name", ["config1", "config2"])
+def test_cluster_factors_reconstruction(cm, name):
+    """N1 codec: per-cluster factors Ũ_c = U_c S_c and V_c of the rank-r truncated SVD of the
+    concatenation; reconstructing every block as Ũ_c V_{c,i}^T gives the exact
+    rank-r error of the cluster (Thm EYM) -- checked against cmsvd_cluster_verify and, for config 1,
+    the oracle's explicit SVD; V_c has orthonormal columns (both Gram orientations are exercised)."""
+    col = synth.make_config(name)
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        ctx.block_spectra(col.r)
+        g = ctx.cluster(cm.ALG_APPROX, 0.05, sort=cm.SORT_RESIDUAL)
+        assign = np.asarray(g["assign"], np.int32)
+        fac = ctx.cluster_factors(assign)
+        v = ctx.cluster_verify(assign)
+    for c, (members, Ut, V) in enumerate(fac):
+        X = np.concatenate([col.blocks[i].T.astype(np.float64) for i in members], axis=1)
+        Xh = Ut.astype(np.float64) @ V.astype(np.float64).T
+        err2 = float(np.sum((X - Xh) ** 2))
+        tot = float(np.sum(X * X))
+        assert abs(err2 - v["exact_err2"][c]) <= 2e-3 * v["exact_err2"][c] + 1e-6 * tot, (c, err2, v["exact_err2"][c])
+        G = V.astype(np.float64).T @ V.astype(np.float64)
+        live = np.linalg.norm(Ut, axis=0) > 0
+        assert np.allclose(G[np.ix_(live, live)], np.eye(int(live.sum())), atol=1e-5)
+    if name == "config1":
+        sp = oracle.block_spectra(col.blocks)
+        ex = oracle.exact_groups(sp, [list(mb) for mb, _, _ in fac], col.r)
+        from tolerances import assert_err2
+        assert_err2(v["exact_err2"], ex, v["total"], "config1 cluster exact")
