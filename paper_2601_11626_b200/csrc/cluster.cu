@@ -233,7 +233,11 @@ struct Driver {
     CK(ensure(c.cws[CW_R], (size_t)m * std::max(w, 1) * 4 * 2), "cluster: R");
     const int n = (o.algorithm == CMSVD_ALG_APPROX) ? rr + w : w;
     const int nn = std::max(n, 1);
-    CK(ensure(c.cws[CW_G], (size_t)nn * nn * 8 * 3), "cluster: G");
+    // Alg. 3 keeps only the top-r eigenpairs of G: tridiagonal reduction + bisection + inverse iteration
+    // (k_eig.cu launch_syev_topk) instead of the full QL with vectors
+    const int kw = std::min(o.r, n);
+    const bool topk = o.algorithm == CMSVD_ALG_APPROX && c.commit_topk && n <= 160 && kw >= 1 && kw <= 64;
+    CK(ensure(c.cws[CW_G], (size_t)nn * nn * 8 * 3 + (topk ? syev_topk_scratch_bytes(n, kw) : 0)), "cluster: G");
     CK(ensure(c.cws[CW_V], (size_t)nn * nn * 8 * 2), "cluster: V");
     CK(ensure(c.cws[CW_EV], (size_t)nn * 8 + (size_t)nn * 8), "cluster: ev");
     CK(ensure(c.cws[CW_PERM], (size_t)nn * 4 + 64), "cluster: perm");
@@ -293,11 +297,21 @@ struct Driver {
       CK(launch_gemm_tn(c, d_hd, 2, w, w, true), "cluster: commit grams");
       CK(launch_build_G1(c, rr, w, st.spec, Z, qz, ZZ, WW, G), "cluster: commit G");
     }
-    CK(launch_syev(c, G, n, (int64_t)n * n, d_ns, 1, n, (double*)c.cws[CW_V].p, (int64_t)n * n,
-                   (double*)c.cws[CW_V].p + (size_t)nn * nn, ev, perm, n, stat),
-       "cluster: commit eig");
-    CK(cudaMemcpyAsync(lam.data(), ev, (size_t)n * 8, cudaMemcpyDeviceToHost, c.stream), "cluster: commit d2h");
-    CK(cudaMemcpyAsync(&status, stat, 4, cudaMemcpyDeviceToHost, c.stream), "cluster: commit d2h");
+    if (topk) {
+      std::vector<int> id(kw);
+      for (int l = 0; l < kw; ++l) id[l] = l;
+      CK(cudaMemcpyAsync(perm, id.data(), (size_t)kw * 4, cudaMemcpyHostToDevice, c.stream), "cluster: commit");
+      CK(launch_syev_topk(c, G, n, d_ns, kw, (double*)c.cws[CW_V].p, ev, G + (size_t)nn * nn * 3),
+         "cluster: commit eig");
+      std::fill(lam.begin(), lam.end(), 0.0);
+      CK(cudaMemcpyAsync(lam.data(), ev, (size_t)kw * 8, cudaMemcpyDeviceToHost, c.stream), "cluster: commit d2h");
+    } else {
+      CK(launch_syev(c, G, n, (int64_t)n * n, d_ns, 1, n, (double*)c.cws[CW_V].p, (int64_t)n * n,
+                     (double*)c.cws[CW_V].p + (size_t)nn * nn, ev, perm, n, stat),
+         "cluster: commit eig");
+      CK(cudaMemcpyAsync(lam.data(), ev, (size_t)n * 8, cudaMemcpyDeviceToHost, c.stream), "cluster: commit d2h");
+      CK(cudaMemcpyAsync(&status, stat, 4, cudaMemcpyDeviceToHost, c.stream), "cluster: commit d2h");
+    }
     CK(cudaStreamSynchronize(c.stream), "cluster: commit sync");
     if (status < 0) return fail(c, CMSVD_E_NOCONV, "cluster: commit eigensolver did not converge");
     const double l0 = lam.empty() ? 0.0 : std::max(lam[0], 0.0);

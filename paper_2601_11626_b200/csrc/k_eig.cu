@@ -578,7 +578,10 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
                                                               const double* __restrict__ thr, int kw, int nstride,
                                                               double* __restrict__ dout, double* __restrict__ e2out,
                                                               double* __restrict__ gsh, int* __restrict__ cnt_out,
-                                                              double* __restrict__ trace_out) {
+                                                              double* __restrict__ trace_out,
+                                                              double* __restrict__ save = nullptr) {
+  // save (optional, one problem per launch): [v_k as column k of an n x n array][tau_k][signed e_k],
+  // so that Q^T G Q = tridiag(d, e) with Q = H_0 ... H_{n-3}, H_k = I - tau_k v_k v_k^T
   constexpr int NR = 32 * S;
   constexpr int CL = 2 * (S - 1);
   static_assert(C == 2 * S && C <= 16, "column chunks");
@@ -634,23 +637,25 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
     sg = warp_sum(sg);
     al = __shfl_sync(0xffffffffu, al, (kk + 1) & 31);
     dk = __shfl_sync(0xffffffffu, dk, kk & 31);
-    double tau, scale, ee;
+    double tau, scale, ee, es;
     if (sg == 0.0) {
-      tau = 0.0; scale = 0.0; ee = al * al;
+      tau = 0.0; scale = 0.0; ee = al * al; es = al;
     } else {
       const double x2 = fma(al, al, sg);
       const double xn = x2 * rsqrt_nr(x2);
       const double beta = al >= 0.0 ? -xn : xn;
       tau = (beta - al) * rcp_nr(beta);
       scale = rcp_nr(al - beta);
-      ee = beta * beta;
+      ee = beta * beta; es = beta;
     }
     if (lane == 0) { e2s[kk] = ee; ds[kk] = dk; s_tau[kk & 1] = tau; }
+    if (save && lane == 0) { save[(int64_t)n * n + kk] = tau; save[(int64_t)n * n + n + kk] = es; }
     double* vv = vb[kk & 1];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int i = lane + 32 * s;
       vv[i] = (i == kk + 1) ? 1.0 : ((i > kk + 1 && i < n) ? x[s] * scale : 0.0);
+      if (save && i < n) save[(int64_t)kk * n + i] = vv[i];
     }
   };
   // columns without strictly-lower parts (the last two chunks) never get a mirrored sum
@@ -700,19 +705,24 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
 #pragma unroll
           for (int q = 0; q < S; ++q) sg += red2[q];
           const double al = s_alpha;
-          double tau1, scale, ee;
+          double tau1, scale, ee, es;
           if (sg == 0.0) {
-            tau1 = 0.0; scale = 0.0; ee = al * al;
+            tau1 = 0.0; scale = 0.0; ee = al * al; es = al;
           } else {
             const double x2 = fma(al, al, sg);
             const double xn = x2 * rsqrt_nr(x2);
             const double beta = al >= 0.0 ? -xn : xn;
             tau1 = (beta - al) * rcp_nr(beta);
             scale = rcp_nr(al - beta);
-            ee = beta * beta;
+            ee = beta * beta; es = beta;
           }
           if (tid == 0) { e2s[k1] = ee; ds[k1] = s_dk; s_tau[k1 & 1] = tau1; }
-          vb[k1 & 1][tid] = (tid == k1 + 1) ? 1.0 : ((tid > k1 + 1 && tid < n) ? y * scale : 0.0);
+          const double vt = (tid == k1 + 1) ? 1.0 : ((tid > k1 + 1 && tid < n) ? y * scale : 0.0);
+          vb[k1 & 1][tid] = vt;
+          if (save) {
+            if (tid < n) save[(int64_t)k1 * n + tid] = vt;
+            if (tid == 0) { save[(int64_t)n * n + k1] = tau1; save[(int64_t)n * n + n + k1] = es; }
+          }
         }
       }
       RR_T(6, wid == 1);
@@ -747,6 +757,7 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
         if (lane == 0) {
           ds[jj] = dj;
           if (jj + 1 < n) e2s[jj] = ej * ej;
+          if (save && jj + 1 < n) save[(int64_t)n * n + n + jj] = ej;
         }
       }
     }
@@ -1217,6 +1228,50 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
   *out = 0.5 * (lo + hi);
 }
 
+// Multisection for small batches (latency-bound: e.g. one greedy evaluation or
+// commit): one warp per wanted eigenvalue, the 32 lanes evaluate Sturm counts
+// at 32 interior points of the bracket, so each fp64 step narrows it 33x.
+// Same stopping rule and output as k_bisect.
+constexpr int64_t kMultisectMax = 1024;  // wanted eigenvalues in a launch below which multisection wins
+__global__ void __launch_bounds__(128) k_multisect(int P, int kw, int nstride, const int* __restrict__ ns,
+                                                   const double* __restrict__ dd, const double* __restrict__ ee2,
+                                                   const double* __restrict__ gsh, const int* __restrict__ cnt,
+                                                   double* __restrict__ ev) {
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= (int64_t)P * kw) return;
+  const int p = (int)(g / kw), l = (int)(g % kw);
+  double* out = ev + (int64_t)p * kw + l;
+  if (l >= cnt[p]) { if (lane == 0) *out = 0.0; return; }
+  const int n = ns[p];
+  const double* d = dd + (int64_t)p * nstride;
+  const double* e2 = ee2 + (int64_t)p * nstride;
+  const double pivmin = gsh[4 * p + 2], nrm = gsh[4 * p + 3];
+  double lo = gsh[4 * p], hi = gsh[4 * p + 1];
+  const int target = n - 1 - l;
+  const double tol = 1e-13 * nrm;
+  for (int it = 0; it < 40 && (hi - lo) > tol + 4.4e-16 * fmax(fabs(lo), fabs(hi)); ++it) {
+    const double h = (hi - lo) * (1.0 / 33.0);
+    const double x = fma((double)(lane + 1), h, lo);
+    double q = __ldg(d) - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    int c = q < 0.0;
+#pragma unroll 4
+    for (int i = 1; i < n; ++i) {
+      q = (__ldg(d + i) - x) - __ldg(e2 + i - 1) * rcp_nr(q);
+      if (fabs(q) < pivmin) q = -pivmin;
+      c += q < 0.0;
+    }
+    const unsigned below = __ballot_sync(0xffffffffu, c <= target);  // a prefix of the lanes
+    const int k = __popc(below);
+    const double xl = __shfl_sync(0xffffffffu, x, (k + 31) & 31);
+    const double xh = __shfl_sync(0xffffffffu, x, k & 31);
+    if (k > 0) lo = xl;
+    if (k < 32) hi = xh;
+  }
+  if (lane == 0) *out = 0.5 * (lo + hi);
+}
+
 // ---------------------------------------------------------------------------
 // Symmetric eigen-decomposition with vectors (block spectra S2, cluster-state
 // commits S10): the tridiagonal reduction above with the reflectors saved,
@@ -1548,11 +1603,247 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t total = (int64_t)nprob * kw;
-  k_bisect<<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
+  if (total <= kMultisectMax)
+    k_multisect<<<(unsigned)((total + 3) / 4), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
+  else
+    k_bisect<<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
   c.launches += 1;
   return cudaGetLastError();
 }
 
 size_t tridiag_scratch_bytes(int nprob, int nmax) { return ((size_t)nprob * (2 * nmax + 4)) * 8; }
+
+// ---------------------------------------------------------------------------
+// Top-k eigenpairs of one symmetric n x n matrix (n <= 160), for the Alg. 3
+// cluster-state commit ("incremental" update; only the top
+// r eigenvectors of G are kept).  Replaces the full QL with vectors:
+//   k_tridiag_rr (reflectors saved) -> k_bisect (top-k eigenvalues, 1e-13 ||T||)
+//   -> k_tri_invit (inverse iteration on the tridiagonal, one warp per cluster
+//      of close eigenvalues, Gram-Schmidt inside a cluster every iteration)
+//   -> k_tri_backtrans (Z <- H_0 ... H_{n-3} Z, one warp per vector).
+// ---------------------------------------------------------------------------
+constexpr int kInvWarps = 16;
+constexpr int kInvMaxK = 64;
+constexpr int kInvIters = 3;  // 2 for an isolated eigenvalue
+constexpr double kInvClusterTol = 1e-7;
+
+__device__ __forceinline__ double inv_hash(unsigned j, unsigned i) {
+  unsigned h = j * 0x9E3779B9u ^ (i + 0x7F4A7C15u) * 0x85EBCA6Bu;
+  h ^= h >> 16; h *= 0x7FEB352Du; h ^= h >> 15; h *= 0x846CA68Bu; h ^= h >> 16;
+  return (double)(h >> 8) * (2.0 / 16777216.0) - 1.0;
+}
+
+// d[n], e[n-1] signed off-diagonal; ev[kw] non-increasing; Z (n x kw, ld n) unit eigenvectors of the
+// tridiagonal.  Per-warp LU factors and iterate live in shared memory (dynamic, kInvWarps * 6 * n doubles).
+__global__ void __launch_bounds__(kInvWarps * 32) k_tri_invit(int n, int kw, const double* __restrict__ d,
+                                                              const double* __restrict__ e,
+                                                              const double* __restrict__ ev,
+                                                              const double* __restrict__ gsh, double* __restrict__ Z) {
+  extern __shared__ double inv_smem[];
+  __shared__ int cl[kInvMaxK + 1];
+  __shared__ int ncl;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double nrm = gsh[3];
+  double* ds_ = inv_smem + (size_t)kInvWarps * 6 * n;  // the tridiagonal, staged once
+  double* es_ = ds_ + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    ds_[i] = d[i];
+    es_[i] = i + 1 < n ? e[i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    // clusters: consecutive eigenvalues closer than kInvClusterTol ||T|| (LAPACK dstein uses 1e-3; the
+    // commit stores the basis in fp32, and vectors of eigenvalues further apart than 1e-7 ||T|| come out
+    // orthogonal to ~1e-13 / 1e-7 per iteration without Gram-Schmidt)
+    int c = 0;
+    cl[0] = 0;
+    for (int j = 1; j < kw; ++j)
+      if (ev[j - 1] - ev[j] > kInvClusterTol * nrm) cl[++c] = j;
+    cl[++c] = kw;
+    ncl = c;
+  }
+  __syncthreads();
+  double* u0 = inv_smem + (size_t)wid * 6 * n;  // 1 / pivot
+  double* u1 = u0 + n;
+  double* u2 = u1 + n;
+  double* ml = u2 + n;
+  double* pv = ml + n;
+  double* x = pv + n;
+  const double tiny = 2.2204460492503131e-16 * nrm;
+#ifdef CMSVD_INV_PROF
+  const long long t_start = clock64();
+#endif
+  for (int c = blockIdx.x * kInvWarps + wid; c < ncl; c += gridDim.x * kInvWarps) {
+    const int iters = cl[c + 1] - cl[c] > 1 ? kInvIters : kInvIters - 1;
+    double xjm = 0.0;
+    for (int j = cl[c]; j < cl[c + 1]; ++j) {
+      double xj = ev[j];
+      const double pertol = 10.0 * 2.2204460492503131e-16 * fmax(fabs(xj), nrm * 1e-3);
+      if (j > cl[c] && xjm - xj < pertol) xj = xjm - pertol;
+      xjm = xj;
+      if (lane == 0) {
+        // T - xj I = P L U, partial pivoting (rows k, k+1); U has up to two super-diagonals
+        double w0 = ds_[0] - xj, w1 = es_[0];
+#pragma unroll 4
+        for (int k = 0; k + 1 < n; ++k) {
+          const double ck = es_[k], ak1 = ds_[k + 1] - xj, bk1 = es_[k + 1];
+          if (fabs(w0) >= fabs(ck)) {
+            if (fabs(w0) < tiny) w0 = w0 >= 0.0 ? tiny : -tiny;
+            const double r = rcp_nr(w0);
+            const double mlt = ck * r;
+            u0[k] = r; u1[k] = w1; u2[k] = 0.0; ml[k] = mlt; pv[k] = 0.0;
+            w0 = fma(-mlt, w1, ak1);
+            w1 = bk1;
+          } else {
+            const double r = rcp_nr(ck);
+            const double mlt = w0 * r;
+            u0[k] = r; u1[k] = ak1; u2[k] = bk1; ml[k] = mlt; pv[k] = 1.0;
+            w0 = fma(-mlt, ak1, w1);
+            w1 = -mlt * bk1;
+          }
+        }
+        if (fabs(w0) < tiny) w0 = w0 >= 0.0 ? tiny : -tiny;
+        u0[n - 1] = rcp_nr(w0);
+      }
+      for (int i = lane; i < n; i += 32) x[i] = inv_hash((unsigned)j, (unsigned)i);
+      __syncwarp();
+      for (int it = 0; it < iters; ++it) {
+        if (lane == 0) {
+          // forward: P, L
+          double cur = x[0];
+#pragma unroll 4
+          for (int k = 0; k + 1 < n; ++k) {
+            double nx = x[k + 1];
+            if (pv[k] != 0.0) { const double t = cur; cur = nx; nx = t; }
+            x[k] = cur;
+            cur = fma(-ml[k], cur, nx);
+          }
+          // back substitution with U
+          double x1 = cur * u0[n - 1], x2 = 0.0;
+          x[n - 1] = x1;
+#pragma unroll 4
+          for (int k = n - 2; k >= 0; --k) {
+            const double xk = fma(-u2[k], x2, fma(-u1[k], x1, x[k])) * u0[k];
+            x[k] = xk;
+            x2 = x1; x1 = xk;
+          }
+        }
+        __syncwarp();
+        // Gram-Schmidt against the cluster's earlier vectors, then normalise
+        for (int q = cl[c]; q < j; ++q) {
+          const double* zq = Z + (size_t)q * n;
+          double t = 0.0;
+          for (int i = lane; i < n; i += 32) t = fma(x[i], zq[i], t);
+          t = warp_sum(t);
+          for (int i = lane; i < n; i += 32) x[i] = fma(-t, zq[i], x[i]);
+        }
+        double ss = 0.0, mx = 0.0;
+        for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(x[i]));
+        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const double sc = mx > 0.0 ? 1.0 / mx : 1.0;
+        for (int i = lane; i < n; i += 32) { x[i] *= sc; ss = fma(x[i], x[i], ss); }
+        ss = warp_sum(ss);
+        const double inv = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+        for (int i = lane; i < n; i += 32) x[i] *= inv;
+        __syncwarp();
+      }
+      double* zj = Z + (size_t)j * n;
+      for (int i = lane; i < n; i += 32) zj[i] = x[i];
+#ifdef CMSVD_INV_PROF
+      if (lane == 0) printf("invit: cluster %d/%d (size %d) vec %d: %lld cycles since start\n", c, ncl,
+                            cl[c + 1] - cl[c], j, (long long)(clock64() - t_start));
+#endif
+      __threadfence_block();
+      __syncwarp();
+    }
+  }
+}
+
+// Z (n x kw, ld n) <- H_0 H_1 ... H_{n-3} Z; VH column k = v_k, tau[k].  n <= 160.  Reflectors are
+// staged into shared memory 32 at a time (dynamic: 32 * n doubles); one warp per column of Z.
+__global__ void __launch_bounds__(kInvWarps * 32) k_tri_backtrans(int n, int kw, const double* __restrict__ VH,
+                                                                  const double* __restrict__ tau,
+                                                                  double* __restrict__ Z) {
+  extern __shared__ double bt_smem[];
+  __shared__ double st[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ncol = (kw + kInvWarps - 1) / kInvWarps;  // columns per warp (kw <= 64: at most 4)
+  double z[4][5];
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int j = wid + kInvWarps * cc, i = lane + 32 * s;
+      z[cc][s] = (cc < ncol && j < kw && i < n) ? Z[(size_t)j * n + i] : 0.0;
+    }
+  for (int k1 = n - 3; k1 >= 0; k1 -= 32) {
+    const int k0 = max(k1 - 31, 0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < (k1 - k0 + 1) * n; t += blockDim.x) bt_smem[t] = VH[(size_t)k0 * n + t];
+    if (threadIdx.x <= k1 - k0) st[threadIdx.x] = tau[k0 + threadIdx.x];
+    __syncthreads();
+    for (int k = k1; k >= k0; --k) {
+      const double tk = st[k - k0];
+      if (tk == 0.0) continue;
+      const double* v = bt_smem + (size_t)(k - k0) * n;
+      double vr[5];
+#pragma unroll
+      for (int s = 0; s < 5; ++s) {
+        const int i = lane + 32 * s;
+        vr[s] = (i > k && i < n) ? v[i] : 0.0;
+      }
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        if (cc < ncol) {
+          double t = 0.0;
+#pragma unroll
+          for (int s = 0; s < 5; ++s) t = fma(vr[s], z[cc][s], t);
+          t = warp_sum(t) * tk;
+#pragma unroll
+          for (int s = 0; s < 5; ++s) z[cc][s] = fma(-t, vr[s], z[cc][s]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int j = wid + kInvWarps * cc, i = lane + 32 * s;
+      if (cc < ncol && j < kw && i < n) Z[(size_t)j * n + i] = z[cc][s];
+    }
+}
+
+size_t syev_topk_scratch_bytes(int n, int kw) {
+  (void)kw;
+  return ((size_t)n * n + 2 * n + 2 * n + 4 + 8) * 8 + 64;
+}
+
+cudaError_t launch_syev_topk(Ctx& c, const double* G, int n, const int* d_n, int kw, double* Z, double* evals,
+                             double* scratch) {
+  if (n < 1 || n > 160 || kw < 1 || kw > kInvMaxK || kw > n) return cudaErrorInvalidValue;
+  double* save = scratch;
+  double* dd = save + (size_t)n * n + 2 * n;
+  double* ee = dd + n;
+  double* gsh = ee + n;
+  double* trace = gsh + 4;
+  int* cnt = (int*)(trace + 1);
+#define RRS_LAUNCH(S_, C_)                                                                                           \
+  k_tridiag_rr<S_, C_><<<1, kRRThreads, 0, c.stream>>>(G, n, (int64_t)n * n, d_n, nullptr, kw, n, dd, ee, gsh, cnt, \
+                                                      trace, save)
+  if (n <= 32) RRS_LAUNCH(1, 2);
+  else if (n <= 64) RRS_LAUNCH(2, 4);
+  else if (n <= 96) RRS_LAUNCH(3, 6);
+  else if (n <= 128) RRS_LAUNCH(4, 8);
+  else RRS_LAUNCH(5, 10);
+#undef RRS_LAUNCH
+  k_multisect<<<(unsigned)((kw + 3) / 4), 128, 0, c.stream>>>(1, kw, n, d_n, dd, ee, gsh, cnt, evals);
+  const int sm_inv = (kInvWarps * 6 + 2) * n * 8, sm_bt = 32 * n * 8;
+  cudaError_t e = cudaFuncSetAttribute(k_tri_invit, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_inv);
+  if (e != cudaSuccess) return e;
+  k_tri_invit<<<(kw + kInvWarps - 1) / kInvWarps, kInvWarps * 32, sm_inv, c.stream>>>(n, kw, dd, save + (size_t)n * n + n, evals, gsh, Z);
+  k_tri_backtrans<<<1, kInvWarps * 32, sm_bt, c.stream>>>(n, kw, save, save + (size_t)n * n, Z);
+  c.launches += 4;
+  return cudaGetLastError();
+}
 
 }  // namespace cmsvd

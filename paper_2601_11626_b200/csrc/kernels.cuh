@@ -24,6 +24,11 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
                                 int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
                                 double* trace, double* scratch);
 size_t tridiag_scratch_bytes(int nprob, int nmax);
+// top-kw eigenpairs of one n x n symmetric matrix (n <= 160, kw <= 64): Z (n x kw, ld n), evals[kw]
+// non-increasing; G is read only.  d_n: device int holding n.
+size_t syev_topk_scratch_bytes(int n, int kw);
+cudaError_t launch_syev_topk(Ctx& c, const double* G, int n, const int* d_n, int kw, double* Z, double* evals,
+                             double* scratch);
 
 // pair pipeline kernels (k_pair.cu)
 __global__ void k_make_descs(const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int64_t m,
