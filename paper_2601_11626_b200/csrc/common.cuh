@@ -123,6 +123,7 @@ struct Ctx {
   bool tc_ok = true;                   // every block numerically full column rank (set by block_spectra)
   int gl_batch_mb = 1024;              // in-place global-memory eigen batches (n > 160), MB of matrices per launch
   bool eig_rr = true;
+  bool zz_syrk = true;               // w <= 128: Z^T Z by k_syrk_zz instead of k_gemm_tn (CMSVD_ZZ_SYRK=0: off)
   bool eig_duo = true;                 // n <= 128: two problems per CTA with dedicated row warps (CMSVD_EIG_DUO=0: off)
   bool commit_topk = true;             // Alg. 3 commits: top-r eigenpairs by inverse iteration (CMSVD_COMMIT_TOPK=0: QL)
   bool eig_rr2 = true;                 // two problems per CTA in the register-resident kernel (CMSVD_EIG_RR2=0: one)                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)

@@ -583,7 +583,10 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
         prof_end(c, pf);
       } else {
         pf = prof_begin(c, PC_GRAM_ZZ);
-        CK(launch_gemm_tn(c, dZZ, (int)Pc, WMAX, WMAX, true), "pairs: Z^T Z");
+        if (c.zz_syrk && WMAX <= 128)
+          CK(launch_syrk_zz(c, pr, Pc, d_bd, d_ad, full ? 1 : 0, QMAX, WMAX, Z, ZZ), "pairs: Z^T Z");
+        else
+          CK(launch_gemm_tn(c, dZZ, (int)Pc, WMAX, WMAX, true), "pairs: Z^T Z");
         prof_end(c, pf);
         pf = prof_begin(c, PC_BUILD_G);
         k_build_G<<<(unsigned)Pc, kThreads, 0, c.stream>>>(pr, d_bd, d_ad, QMAX, WMAX, GMAX, Z, W, ZZ, Gm, zn2);

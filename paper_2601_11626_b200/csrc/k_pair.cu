@@ -99,6 +99,117 @@ __global__ void __launch_bounds__(kThreads) k_build_G(const int2* __restrict__ p
   }
 }
 
+// Z^T Z (fp64 accumulation) for w <= 128, replacing k_gemm_tn<double> on Z: one CTA per pair; the 136
+// lower-triangular 8x8 tiles of the 128 x 128 product are owned by threads 0..135.  Rows of Z arrive 32
+// at a time by cp.async into a double-buffered fp32 staging area (no registers held across the
+// products), are widened once into the fp64 operand rows, and each thread accumulates its tile; the
+// tile and its mirror are stored (store-only epilogue).  The accumulation is the sequential fma over k of
+// k_gemm_tn (fp32 products are exact in fp64): bitwise the same ZZ.
+constexpr int kZZThreads = 160;
+constexpr int kZZBK = 32;
+constexpr int kZZLD = 162;  // doubles per operand row (tile t at 10 t: 8 + 2 pad; +2 spreads the widening stores)
+constexpr size_t kZZSmem = (size_t)kZZBK * kZZLD * 8 + 2 * (size_t)kZZBK * 128 * 4;
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+
+__global__ void __launch_bounds__(kZZThreads, 2) k_syrk_zz(const int2* __restrict__ pairs,
+                                                           const BaseDesc* __restrict__ bd,
+                                                           const AppDesc* __restrict__ ad, int use_full_basis,
+                                                           int QMAX, int WMAX, const float* __restrict__ Zws,
+                                                           double* __restrict__ ZZws) {
+  extern __shared__ __align__(16) unsigned char zz_smem[];
+  double* Zs = reinterpret_cast<double*>(zz_smem);
+  float* Zst = reinterpret_cast<float*>(zz_smem + (size_t)kZZBK * kZZLD * 8);   // [2][128 cols][32 rows]
+  const int64_t p = blockIdx.x;
+  const int2 pr = pairs[p];
+  const BaseDesc b = bd[pr.x];
+  const int w = ad[pr.y].w;
+  const int q = use_full_basis ? b.q : b.rr;
+  const float* Z = Zws + p * (int64_t)QMAX * WMAX;
+  double* ZZ = ZZws + p * (int64_t)WMAX * WMAX;
+  const int tid = threadIdx.x;
+  int ti = 0, tj = tid;
+  while (tj > ti) { ++ti; tj -= ti; }                        // tid = ti (ti + 1) / 2 + tj, tj <= ti
+  const bool active = tid < 136 && 8 * tj < w;
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  auto fetch = [&](int l0, float* dst) {
+    for (int e = tid; e < kZZBK * 128; e += kZZThreads) {
+      const int l = e & (kZZBK - 1), j = e >> 5;
+      const bool v = l0 + l < q && j < w;
+      cp_async4(dst + e, v ? Z + (int64_t)j * QMAX + l0 + l : Z, v);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int nch = (q + kZZBK - 1) / kZZBK;
+  if (nch > 0) fetch(0, Zst);
+  for (int c = 0; c < nch; ++c) {
+    const int l0 = c * kZZBK;
+    if (c + 1 < nch) {
+      fetch(l0 + kZZBK, Zst + ((c + 1) & 1) * kZZBK * 128);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();  // chunk c staged by every thread; the previous products are done with Zs
+    const float* src = Zst + (c & 1) * kZZBK * 128;
+    for (int e = tid; e < kZZBK * 128; e += kZZThreads) {
+      const int l = e & (kZZBK - 1), j = e >> 5;
+      Zs[l * kZZLD + j + 2 * (j >> 3)] = (double)src[e];
+    }
+    __syncthreads();
+    if (active) {
+      const int lmax = min(kZZBK, q - l0);
+      for (int l = 0; l < lmax; ++l) {
+        const double* row = Zs + l * kZZLD;
+        double a[8], bb[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2 x = *reinterpret_cast<const double2*>(row + 10 * ti + 2 * u);
+          const double2 y = *reinterpret_cast<const double2*>(row + 10 * tj + 2 * u);
+          a[2 * u] = x.x; a[2 * u + 1] = x.y;
+          bb[2 * u] = y.x; bb[2 * u + 1] = y.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+      }
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int gj = 8 * tj + j;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int gi = 8 * ti + i;
+        if (gi < w && gj < w) {
+          ZZ[(int64_t)gj * WMAX + gi] = acc[i][j];
+          if (ti != tj) ZZ[(int64_t)gi * WMAX + gj] = acc[i][j];
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_syrk_zz(Ctx& c, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad,
+                           int use_full_basis, int QMAX, int WMAX, const float* Zws, double* ZZws) {
+  if (P <= 0) return cudaSuccess;
+  if (WMAX > 128) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k_syrk_zz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZZSmem);
+  if (e != cudaSuccess) return e;
+  k_syrk_zz<<<(unsigned)P, kZZThreads, kZZSmem, c.stream>>>(pairs, bd, ad, use_full_basis, QMAX, WMAX, Zws, ZZws);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 // Final per-pair combination (S3, S7, S8, S9): one thread per pair.
 __global__ void k_finalize(const int2* __restrict__ pairs, int64_t P, const BaseDesc* __restrict__ bd,
                            const AppDesc* __restrict__ ad, int r, unsigned kinds, const double* __restrict__ evG,
