@@ -446,8 +446,10 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
   c.launches += 1;
   CK(cudaGetLastError(), "spectra: stats");
   {
-    dim3 g((unsigned)((m + kThreads - 1) / kThreads), nmax, N);
-    k_leftvec<<<g, kThreads, 0, c.stream>>>(m, arena, d_boff, d_kcols, (const double*)c.ws[WS_V].p, gstride,
+    dim3 g((unsigned)((m + kThreads - 1) / kThreads), (unsigned)((nmax + 7) / 8), N);
+    const size_t lv_smem = (size_t)8 * nmax * sizeof(double);
+    CK(cudaFuncSetAttribute(k_leftvec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv_smem), "spectra: leftvec");
+    k_leftvec<<<g, kThreads, lv_smem, c.stream>>>(m, arena, d_boff, d_kcols, (const double*)c.ws[WS_V].p, gstride,
                                             (const int*)c.ws[WS_PERM].p, nmax, (const double*)c.d_sig.p,
                                             (const int*)c.d_rank.p, (float*)c.d_U.p, d_uoff);
     c.launches += 1;

@@ -1173,7 +1173,7 @@ size_t duo_smem_bytes() {
 // ---------------------------------------------------------------------------
 // Plain bisection, one thread per wanted eigenvalue (high occupancy; the
 // tridiagonals are read through L1).  fp32 coarse phase on the normalised
-// matrix to ~4e-7 ||T||, widened by 1e-5 ||T||, then fp64 to 1e-13 ||T||.
+// matrix to ~4e-7 ||T||, widened by 1e-5 ||T||, then fp64 to max(1e-13 ||T||, 1e-11 lambda).
 // ev[p*kw + l] = l-th largest eigenvalue for l < cnt[p], else 0.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, const int* __restrict__ ns,
@@ -1212,8 +1212,11 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
     lo = fmax(glo, (double)a * nrm - 1e-5 * nrm);
     hi = fmin(ghi, (double)b * nrm + 1e-5 * nrm);
   }
+  // stop at 1e-13 ||T|| absolute (the floor that resolves sigma = sqrt(lambda) near zero, A13) or
+  // 1e-11 relative, whichever is looser: a large eigenvalue needs no more for sigma~ (1e-4) or for the
+  // captured-energy sums (error <= 1e-11 E against the 1e-7 E floor)
   const double tol = 1e-13 * nrm;
-  for (int it = 0; it < 80 && (hi - lo) > tol + 4.4e-16 * fmax(fabs(lo), fabs(hi)); ++it) {
+  for (int it = 0; it < 80 && (hi - lo) > fmax(tol, 1e-11 * fmax(fabs(lo), fabs(hi))) + 4.4e-16 * fmax(fabs(lo), fabs(hi)); ++it) {
     const double x = 0.5 * (lo + hi);
     double q = __ldg(d) - x;
     if (fabs(q) < pivmin) q = -pivmin;

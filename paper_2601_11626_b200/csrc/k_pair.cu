@@ -420,26 +420,48 @@ __global__ void k_spec_stats(int count, int nmax, int r, const double* __restric
   ad_trunc[i] = a;
 }
 
-// U[:, l] = A V[:, perm[l]] / sigma_l for l < rank (else 0); fp64 accumulation.
+// U[:, l] = A V[:, perm[l]] / sigma_l for l < rank (else 0); fp64 accumulation, sequential over the
+// columns of A.  A thread computes kLvCols columns l of one row (A read once per kLvCols products), the
+// CTA's V columns are staged in shared memory.  Grid: (ceil(m / kThreads), ceil(nmax / kLvCols), count).
+constexpr int kLvCols = 8;
 __global__ void __launch_bounds__(kThreads) k_leftvec(int64_t m, const float* __restrict__ arena,
                                                       const int64_t* __restrict__ boff, const int* __restrict__ kcols,
                                                       const double* __restrict__ V, int64_t strideV,
                                                       const int* __restrict__ perm, int nmax,
                                                       const double* __restrict__ sig, const int* __restrict__ rank,
                                                       float* __restrict__ U, const int64_t* __restrict__ uoff) {
+  extern __shared__ double lv_smem[];                     // kLvCols x k
   const int blk = blockIdx.z;
-  const int l = blockIdx.y;
+  const int l0 = blockIdx.y * kLvCols;
   const int k = kcols[blk];
-  if (l >= k) return;
+  if (l0 >= k) return;
+  const int rk = rank[blk];
+  const int nl = min(kLvCols, k - l0);
+  for (int e = threadIdx.x; e < kLvCols * k; e += blockDim.x) {
+    const int t = e / k, c = e % k;
+    lv_smem[e] = (t < nl && l0 + t < rk)
+                     ? V[(int64_t)blk * strideV + (int64_t)perm[(int64_t)blk * nmax + l0 + t] * k + c]
+                     : 0.0;
+  }
+  __syncthreads();
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= m) return;
-  float* u = U + uoff[blk] + (int64_t)l * m;
-  if (l >= rank[blk]) { u[row] = 0.f; return; }
-  const double* v = V + (int64_t)blk * strideV + (int64_t)perm[(int64_t)blk * nmax + l] * k;
   const float* A = arena + boff[blk];
-  double acc = 0.0;
-  for (int c = 0; c < k; ++c) acc = fma((double)A[(int64_t)c * m + row], v[c], acc);
-  u[row] = (float)(acc / sig[(int64_t)blk * nmax + l]);
+  double acc[kLvCols];
+#pragma unroll
+  for (int t = 0; t < kLvCols; ++t) acc[t] = 0.0;
+#pragma unroll 4
+  for (int c = 0; c < k; ++c) {
+    const double a = (double)A[(int64_t)c * m + row];
+#pragma unroll
+    for (int t = 0; t < kLvCols; ++t) acc[t] = fma(a, lv_smem[t * k + c], acc[t]);
+  }
+  float* Ub = U + uoff[blk];
+#pragma unroll
+  for (int t = 0; t < kLvCols; ++t) {
+    const int l = l0 + t;
+    if (t < nl) Ub[(int64_t)l * m + row] = (l < rk) ? (float)(acc[t] / sig[(int64_t)blk * nmax + l]) : 0.f;
+  }
 }
 
 // TRUNC operand F_i = U_i[:, :rr] diag(sigma_i[:rr]) (fp32).
