@@ -294,3 +294,30 @@ def test_tight_variants_c2_sampled(c2):
     out = ctx.pair_errors_tight(sel)
     assert_err2(out["err2x"][:, 0], ref[:, 0], tot, "config2 residual(U_r)")
     assert_err2(out["err2x"][:, 1], ref[:, 1], tot, "config2 per-index Weyl")
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_syrk_zz_bitwise_equals_gemm_path(cm, seed, monkeypatch):
+    """k_syrk_zz (default Z^T Z kernel, w <= 128) and the generic fp64-accumulated SIMT GEMM
+    (CMSVD_ZZ_SYRK=0) accumulate in the same order: every output must be bitwise equal.  Ragged
+    widths and ranks exercise the partial tiles and the q-chunk tail (q not a multiple of 32)."""
+    rng = np.random.default_rng(100 + seed)
+    m = 96
+    blocks = []
+    for i in range(10):
+        n = int(rng.integers(5, 41))
+        k = int(rng.integers(2, n + 1))
+        a = rng.standard_normal((m, k)) @ rng.standard_normal((k, n)) + 1e-3 * rng.standard_normal((m, n))
+        blocks.append(np.asfortranarray(a.astype(np.float32)))
+    r = 7
+    pairs = np.array([(i, j) for i in range(10) for j in range(10) if i != j], np.int32)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("CMSVD_ZZ_SYRK", flag)
+        ctx = cm.Context(0, torch.cuda.current_stream().cuda_stream)
+        ctx.register(blocks)
+        ctx.block_spectra(r)
+        outs.append(ctx.pair_errors(pairs))
+        ctx.close()
+    for key in ("err2", "total", "sigma_tilde", "mu"):
+        assert np.array_equal(outs[0][key], outs[1][key], equal_nan=True), key

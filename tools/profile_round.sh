@@ -13,7 +13,7 @@ BENCH="python bench.py --steps 1 --warmup 3 --no-e2e --no-greedy --no-cpu-baseli
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_$tag.csv $BENCH \
   > $out/ncu_launch_$tag.log 2>&1
 echo "launch list rc=$?"
-for k in k_tridiag_rr k_pair_tc k_syev_ql; do
+for k in k_tridiag_rr k_tridiag_duo k_pair_tc k_syev_ql k_syrk_zz; do
   ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $out/ncu_${k}_$tag $BENCH \
     > $out/ncu_${k}_$tag.log 2>&1
   echo "$k rc=$?"
