@@ -122,11 +122,11 @@ struct Ctx {
   bool use_tc = true;                  // tcgen05 contraction kernel (CMSVD_NO_TC=1 selects the SIMT path)
   bool tc_ok = true;                   // every block numerically full column rank (set by block_spectra)
   int gl_batch_mb = 1024;              // in-place global-memory eigen batches (n > 160), MB of matrices per launch
-  bool eig_rr = true;
-  bool zz_syrk = true;               // w <= 128: Z^T Z by k_syrk_zz instead of k_gemm_tn (CMSVD_ZZ_SYRK=0: off)
+  bool eig_rr = true;                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)
+  bool zz_syrk = true;                 // w <= 128: Z^T Z by k_syrk_zz instead of k_gemm_tn (CMSVD_ZZ_SYRK=0: off)
+  bool tc_big = true;                  // q or w > 128: tcgen05 GEMM tiles instead of SIMT (CMSVD_TC_BIG=0: off)
   bool eig_duo = true;                 // n <= 128: two problems per CTA with dedicated row warps (CMSVD_EIG_DUO=0: off)
   bool commit_topk = true;             // Alg. 3 commits: top-r eigenpairs by inverse iteration (CMSVD_COMMIT_TOPK=0: QL)
-  bool eig_rr2 = true;                 // two problems per CTA in the register-resident kernel (CMSVD_EIG_RR2=0: one)                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)
   bool big = false;                    // collection of blocks wider than kEigMax (A22 spectra, full-range bases)
   int subspace_iters = 12;             // power iterations of the big-block spectra (CMSVD_SUBSPACE_ITERS)
 };

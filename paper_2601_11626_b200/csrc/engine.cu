@@ -498,6 +498,7 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
   // fp32-accumulated Gram resolves exactly-zero singular values only to ~sqrt(u32)*sigma_1, the
   // fp64-accumulated SIMT path to ~1e-8*sigma_1 ("precision dispatch")
   const bool use_tc = c.use_tc && c.tc_ok && (full ? dims.qmax : dims.rrmax) <= 128 && dims.wmax <= 128;
+  const bool use_tc_big = !use_tc && c.use_tc && c.tc_ok && c.tc_big;  // same precision class, tiled
   const int WMAX = std::max(1, dims.wmax);
   const int GMAX = std::max(1, dims.rrmax + dims.wmax);
   if (need_mat && ((!tight && GMAX > kEigMax) || WMAX > kEigMax))
@@ -565,6 +566,18 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
         // (tight: Q = U_r, the same projection as the incremental estimator)
         pf = prof_begin(c, PC_PAIR_TC);
         CK(launch_pair_tc(c, pr, Pc, d_bd, d_ad, m, full ? 1 : 0, QMAX, WMAX, Z, W), "pairs: tcgen05 Z/R/W");
+        prof_end(c, pf);
+      } else if (use_tc_big) {
+        // operands wider than one 128-column tile: the same 3xTF32 contractions as tcgen05 GEMM tiles,
+        // R' materialised (m x w per pair)
+        pf = prof_begin(c, PC_PROJ);
+        CK(launch_gemm_tc(c, dZ, (int)Pc, QMAX, WMAX, false, false), "pairs: Z = Q^T F (tc)");
+        prof_end(c, pf);
+        pf = prof_begin(c, PC_RESID);
+        CK(launch_gemm_tc(c, dR, (int)Pc, (int)m, WMAX, true, false), "pairs: R = F - Q Z (tc)");
+        prof_end(c, pf);
+        pf = prof_begin(c, PC_GRAM_W);
+        CK(launch_gemm_tc(c, dW, (int)Pc, WMAX, WMAX, false, true), "pairs: W = R^T R (tc)");
         prof_end(c, pf);
       } else {
         pf = prof_begin(c, PC_PROJ);

@@ -470,6 +470,199 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   if (wid == 0) tc::tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// Batched 3xTF32 GEMM tiles for operands wider than one 128-column tile (q or w > 128, e.g. config 4's
+// 256-column bases and TRUNC operands), with the staging, MMA issue and per-128-K-block round-to-nearest
+// summation of k_pair_tc's phase 1:
+//   kTN    C (M x N) = A^T B       A: K x M, B: K x N column-major   (Z = Q^T F, W' = R'^T R')
+//   kNNSub C (M x N) = C0 - A B    A: M x K, B: K x N column-major   (R' = F - Q Z)
+// One CTA (16 warps) per 128 x 128 output tile: grid (tiles_m * tiles_n, batch); sym = 1 computes the
+// lower tiles only and mirrors them.  OUT64 stores C as fp64 (W' for the fp64 Gram assembly).
+// ---------------------------------------------------------------------------
+enum { kTN = 0, kNNSub = 1 };
+template <int MODE, bool OUT64>
+__global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __restrict__ descs, int tiles_n) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar_stage[2];
+  __shared__ uint64_t bar_slot[2];
+  __shared__ uint32_t tmem_base;
+  const GemmDesc d = descs[blockIdx.y];
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  const int i0 = 128 * tm, j0 = 128 * tn;
+  if (i0 >= d.M || j0 >= d.N) return;
+  if (d.sym && tm < tn) return;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int wq = wid & 3;
+  constexpr int kGroups = kTcThreads / 128;
+  constexpr int kColW = 128 / kGroups;
+  const int half = wid >> 2;
+  const int mr = min(128, d.M - i0), nc = min(128, d.N - j0);
+  const int wp = ((nc + 31) / 32) * 32;
+  const int K = d.K;
+  if (wid == 0) tc::tmem_alloc(&tmem_base, 512);
+  if (tid == 0) {
+    tc::mbar_init(&bar_stage[0], 1);
+    tc::mbar_init(&bar_stage[1], 1);
+    tc::mbar_init(&bar_slot[0], 1);
+    tc::mbar_init(&bar_slot[1], 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t t_acc = tmem, t_sum = tmem + 256;   // two block slots [0,128), [128,256); running sum
+  const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+  const int c_lo = kColW * half, c_hi = min(wp, kColW * half + kColW);
+  uint32_t ph_stage = 0, ph_slot = 0, used = 0;
+  auto stage_ptr = [&](int s, int which) { return sm + s * kStage + which * kTile; };
+  auto acquire = [&](int s) {
+    if ((used >> s) & 1u) {
+      tc::mbar_wait(&bar_stage[s], (ph_stage >> s) & 1u);
+      ph_stage ^= 1u << s;
+      used &= ~(1u << s);
+    }
+  };
+  bool sum_empty = true;
+  auto drain_add = [&](uint32_t tcol) {
+    for (int c = c_lo; c < c_hi; c += 32) {
+      float v[32], acc[32];
+      tc::tmem_ld32(tcol + lane_off + c, v);
+      if (!sum_empty) tc::tmem_ld32(t_sum + lane_off + c, acc);
+      tc::wait_ld();
+      if (!sum_empty) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += acc[j];
+      }
+      tc::tmem_st32(t_sum + lane_off + c, v);
+    }
+    tc::wait_st();
+    sum_empty = false;
+  };
+  const uint32_t idesc = tc::make_idesc_tf32(128, wp);
+  constexpr int kBlk = 128 / KT;
+  const int nst = (K + KT - 1) / KT;
+  float4 av[kItK], ar[kItR], bv[kItK];
+  auto load_a = [&](int64_t k0) {
+    if (MODE == kTN) load_kcontig<true>(av, 128, d.A + (int64_t)i0 * d.lda, d.lda, mr, k0, K);
+    else load_rcontig(ar, d.A, d.lda, i0, d.M, (int)k0, K);
+  };
+  if (nst > 0) {
+    load_a(0);
+    load_kcontig<true>(bv, wp, d.B + (int64_t)j0 * d.ldb, d.ldb, nc, 0, K);
+  }
+  for (int it = 0; it < nst; ++it) {
+    const int s = it & 1;
+    const int blk = it / kBlk, slot = blk & 1;
+    acquire(s);
+    if (MODE == kTN) store_kcontig(av, stage_ptr(s, 0), stage_ptr(s, 1), 128, nullptr);
+    else store_rcontig(ar, stage_ptr(s, 0), nullptr, stage_ptr(s, 1));
+    store_kcontig(bv, stage_ptr(s, 2), stage_ptr(s, 3), wp, nullptr);
+    if (it + 1 < nst) {
+      const int64_t k1 = (int64_t)(it + 1) * KT;
+      load_a(k1);
+      load_kcontig<true>(bv, wp, d.B + (int64_t)j0 * d.ldb, d.ldb, nc, k1, K);
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      issue_3x(t_acc + 128 * slot, tc::smem_u32(stage_ptr(s, 0)), tc::smem_u32(stage_ptr(s, 1)),
+               tc::smem_u32(stage_ptr(s, 2)), tc::smem_u32(stage_ptr(s, 3)), idesc, (it % kBlk) == 0);
+      tc::mma_commit(&bar_stage[s]);
+      if ((it % kBlk) == kBlk - 1 || it == nst - 1) tc::mma_commit(&bar_slot[slot]);
+    }
+    used |= 1u << s;
+    if (((it % kBlk) == kBlk - 1 || it == nst - 1) && blk >= 1) {
+      const int ps = (blk - 1) & 1;
+      tc::mbar_wait(&bar_slot[ps], (ph_slot >> ps) & 1u);
+      ph_slot ^= 1u << ps;
+      tc::fence_after();
+      drain_add(t_acc + 128 * ps);
+      tc::fence_before();
+    }
+  }
+  // epilogue: row r = 32 wq + lane of the tile, this warp's columns [c_lo, c_hi) (one 32-column chunk);
+  // the minuend C0 is loaded while the tensor core finishes the last block
+  const int r = 32 * wq + lane;
+  float c0v[32];
+  if (MODE == kNNSub) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int jj = c_lo + j;
+      c0v[j] = (d.C0 && r < mr && jj < c_hi && jj < nc) ? __ldg(d.C0 + (int64_t)(j0 + jj) * d.ldc0 + i0 + r) : 0.f;
+    }
+  }
+  if (nst > 0) {  // last block
+    const int lb = (nst - 1) / kBlk, ls = lb & 1;
+    tc::mbar_wait(&bar_slot[ls], (ph_slot >> ls) & 1u);
+    ph_slot ^= 1u << ls;
+    tc::fence_after();
+    drain_add(t_acc + 128 * ls);
+  }
+  for (int s = 0; s < 2; ++s) acquire(s);
+  static_assert(kColW == 32, "one 32-column chunk per warp in the epilogue");
+  for (int c = c_lo; c < c_hi; c += 32) {
+    float v[32];
+    if (sum_empty) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    } else {
+      tc::tmem_ld32(t_sum + lane_off + c, v);
+      tc::wait_ld();
+    }
+    if (r < mr) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int jj = c + j;
+        if (jj < nc) {
+          const int64_t gi = i0 + r, gj = j0 + jj;
+          float x = v[j];
+          if (MODE == kNNSub) x = c0v[j] - x;
+          if (OUT64) {
+            double* C = reinterpret_cast<double*>(d.C);
+            C[gj * d.ldc + gi] = (double)x;
+            if (d.sym && tm != tn) C[gi * d.ldc + gj] = (double)x;
+          } else {
+            float* C = reinterpret_cast<float*>(d.C);
+            C[gj * d.ldc + gi] = x;
+            if (d.sym && tm != tn) C[gi * d.ldc + gj] = x;
+          }
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (wid == 0) tc::tmem_dealloc(tmem, 512);
+}
+
+cudaError_t launch_gemm_tc(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN, bool nnsub, bool out64) {
+  if (nprob <= 0) return cudaSuccess;
+  const int tm = (maxM + 127) / 128, tn = (maxN + 127) / 128;
+  dim3 g(tm * tn, nprob);
+#define GTC(MODE_, O64_)                                                                                       \
+  do {                                                                                                         \
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<MODE_, O64_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         (int)kSmemTc);                                                        \
+    if (e != cudaSuccess) return e;                                                                            \
+    k_gemm_tc<MODE_, O64_><<<g, kTcThreads, kSmemTc, c.stream>>>(d_descs, tn);                                  \
+  } while (0)
+  if (nnsub) {
+    if (out64) return cudaErrorInvalidValue;
+    GTC(kNNSub, false);
+  } else if (out64) {
+    GTC(kTN, true);
+  } else {
+    GTC(kTN, false);
+  }
+#undef GTC
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pair_tc(Ctx& c, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int64_t m,
                            int use_full_basis, int QMAX, int WMAX, float* Zws, double* Wws) {
   if (P <= 0) return cudaSuccess;

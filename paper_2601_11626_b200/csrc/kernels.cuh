@@ -55,6 +55,8 @@ __global__ void k_leftvec(int64_t m, const float* arena, const int64_t* boff, co
                           const int64_t* uoff);
 cudaError_t launch_pair_tc(Ctx& c, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int64_t m,
                            int use_full_basis, int QMAX, int WMAX, float* Zws, double* Wws);
+// batched 3xTF32 tcgen05 GEMM tiles (C = A^T B, or C = C0 - A B with nnsub); out64: fp64 C
+cudaError_t launch_gemm_tc(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN, bool nnsub, bool out64);
 cudaError_t launch_syrk_zz(Ctx& c, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad,
                            int use_full_basis, int QMAX, int WMAX, const float* Zws, double* ZZws);
 cudaError_t launch_build_G1(Ctx& c, int rr, int w, const double* spec, const float* Z, int ldz, const double* ZZ,

@@ -163,3 +163,16 @@ def test_full_size_sampled_pairs(cm, name):
     assert_sigma(sig[ids], refs, refs[:, 0], f"{name} block sigma")
     assert np.allclose(E[ids], sp.E, rtol=1e-12)
     compare(out, ref, 7, f"{name} full size")
+
+
+@pytest.mark.parametrize("tc_big", ["1", "0"])
+def test_c4_reduced_wide_operands(cm, tc_big, monkeypatch):
+    """r = 192 > 128: bases and TRUNC operands wider than one 128-column tile take the tcgen05 GEMM-tile
+    path (k_gemm_tc: Z = Q^T F, R' = F - Q Z, W' = R'^T R' as 3xTF32 tiles; CMSVD_TC_BIG=0: SIMT).
+    Both against the oracle."""
+    monkeypatch.setenv("CMSVD_TC_BIG", tc_big)
+    col = synth.config4(N=4, m=1024, rank=64)
+    r = 192
+    sp, E, sig, rank, pairs, out = run_pairs(cm, col, r)
+    orc = oracle.pair_errors(sp, pairs, r, 7, oracle.TRUNC)
+    compare(out, orc, 7, f"config4-reduced r=192 tc_big={tc_big}")
