@@ -480,8 +480,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
 // lower tiles only and mirrors them.  OUT64 stores C as fp64 (W' for the fp64 Gram assembly).
 // ---------------------------------------------------------------------------
 enum { kTN = 0, kNNSub = 1 };
-template <int MODE, bool OUT64>
+// NT = output tile width (128, or 256 for the plain A^T B: the A tile is then staged once per 256 output
+// columns, which brings the shared-memory traffic per MMA below the tensor core's operand rate; TMEM then
+// holds one 256-column block slot + the running sum, so a block's drain is not overlapped with the next
+// block's MMAs).
+template <int MODE, bool OUT64, int NT>
 __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __restrict__ descs, int tiles_n) {
+  static_assert(NT == 128 || (NT == 256 && MODE == kTN), "256-wide tiles: A^T B only");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar_stage[2];
@@ -489,15 +494,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
   __shared__ uint32_t tmem_base;
   const GemmDesc d = descs[blockIdx.y];
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
-  const int i0 = 128 * tm, j0 = 128 * tn;
+  const int i0 = 128 * tm, j0 = NT * tn;
   if (i0 >= d.M || j0 >= d.N) return;
-  if (d.sym && tm < tn) return;
+  if (d.sym && NT == 128 && tm < tn) return;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int wq = wid & 3;
   constexpr int kGroups = kTcThreads / 128;
-  constexpr int kColW = 128 / kGroups;
+  constexpr int kColW = NT / kGroups;
+  constexpr int kSlots = NT == 128 ? 2 : 1;
   const int half = wid >> 2;
-  const int mr = min(128, d.M - i0), nc = min(128, d.N - j0);
+  const int mr = min(128, d.M - i0), nc = min(NT, d.N - j0);
   const int wp = ((nc + 31) / 32) * 32;
   const int K = d.K;
   if (wid == 0) tc::tmem_alloc(&tmem_base, 512);
@@ -512,7 +518,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
-  const uint32_t t_acc = tmem, t_sum = tmem + 256;   // two block slots [0,128), [128,256); running sum
+  const uint32_t t_acc = tmem, t_sum = tmem + 256;   // block slots at [0, 256), running sum at [256, 256 + NT)
   const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
   const int c_lo = kColW * half, c_hi = min(wp, kColW * half + kColW);
   uint32_t ph_stage = 0, ph_slot = 0, used = 0;
@@ -525,17 +531,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
     }
   };
   bool sum_empty = true;
-  auto drain_add = [&](uint32_t tcol) {
-    for (int c = c_lo; c < c_hi; c += 32) {
-      float v[32], acc[32];
-      tc::tmem_ld32(tcol + lane_off + c, v);
-      if (!sum_empty) tc::tmem_ld32(t_sum + lane_off + c, acc);
+  auto drain_add = [&](uint32_t tcol) {  // 16-column chunks: the prefetched operands stay in registers
+    for (int c = c_lo; c < c_hi; c += 16) {
+      float v[16], acc[16];
+      tc::tmem_ld16(tcol + lane_off + c, v);
+      if (!sum_empty) tc::tmem_ld16(t_sum + lane_off + c, acc);
       tc::wait_ld();
       if (!sum_empty) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += acc[j];
+        for (int j = 0; j < 16; ++j) v[j] += acc[j];
       }
-      tc::tmem_st32(t_sum + lane_off + c, v);
+      tc::tmem_st16(t_sum + lane_off + c, v);
     }
     tc::wait_st();
     sum_empty = false;
@@ -543,26 +549,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
   const uint32_t idesc = tc::make_idesc_tf32(128, wp);
   constexpr int kBlk = 128 / KT;
   const int nst = (K + KT - 1) / KT;
-  float4 av[kItK], ar[kItR], bv[kItK];
+  // B operand: NT rows (hi at stage tile 2 [.. 2 + NT/128), lo after it)
+  constexpr int kBT = NT / 128;
+  float4 av[kItK], ar[kItR], bv[kBT][kItK];
   auto load_a = [&](int64_t k0) {
     if (MODE == kTN) load_kcontig<true>(av, 128, d.A + (int64_t)i0 * d.lda, d.lda, mr, k0, K);
     else load_rcontig(ar, d.A, d.lda, i0, d.M, (int)k0, K);
   };
+  auto load_b = [&](int64_t k0) {
+#pragma unroll
+    for (int h = 0; h < kBT; ++h)
+      load_kcontig<true>(bv[h], 128, d.B + (int64_t)(j0 + 128 * h) * d.ldb, d.ldb, nc - 128 * h, k0, K);
+  };
+  auto wait_block = [&](int pb) {  // MMAs of K block pb complete; fold it into the running sum
+    const int ps = pb & 1;
+    tc::mbar_wait(&bar_slot[ps], (ph_slot >> ps) & 1u);
+    ph_slot ^= 1u << ps;
+    tc::fence_after();
+    drain_add(t_acc + 128 * (ps % kSlots));
+  };
   if (nst > 0) {
     load_a(0);
-    load_kcontig<true>(bv, wp, d.B + (int64_t)j0 * d.ldb, d.ldb, nc, 0, K);
+    load_b(0);
   }
   for (int it = 0; it < nst; ++it) {
     const int s = it & 1;
-    const int blk = it / kBlk, slot = blk & 1;
+    const int blk = it / kBlk, slot = blk % kSlots;
     acquire(s);
     if (MODE == kTN) store_kcontig(av, stage_ptr(s, 0), stage_ptr(s, 1), 128, nullptr);
     else store_rcontig(ar, stage_ptr(s, 0), nullptr, stage_ptr(s, 1));
-    store_kcontig(bv, stage_ptr(s, 2), stage_ptr(s, 3), wp, nullptr);
+#pragma unroll
+    for (int h = 0; h < kBT; ++h)
+      store_kcontig(bv[h], stage_ptr(s, 2) + h * kTile, stage_ptr(s, 2 + kBT) + h * kTile, 128, nullptr);
     if (it + 1 < nst) {
       const int64_t k1 = (int64_t)(it + 1) * KT;
       load_a(k1);
-      load_kcontig<true>(bv, wp, d.B + (int64_t)j0 * d.ldb, d.ldb, nc, k1, K);
+      load_b(k1);
+    }
+    // one slot (NT = 256): the previous block must be drained before this block's first MMA
+    if (kSlots == 1 && (it % kBlk) == 0 && blk >= 1) {
+      wait_block(blk - 1);
+      tc::fence_before();
     }
     tc::fence_proxy_async();
     tc::fence_before();
@@ -570,40 +597,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
     if (tid == 0) {
       tc::fence_after();
       issue_3x(t_acc + 128 * slot, tc::smem_u32(stage_ptr(s, 0)), tc::smem_u32(stage_ptr(s, 1)),
-               tc::smem_u32(stage_ptr(s, 2)), tc::smem_u32(stage_ptr(s, 3)), idesc, (it % kBlk) == 0);
+               tc::smem_u32(stage_ptr(s, 2)), tc::smem_u32(stage_ptr(s, 2 + kBT)), idesc, (it % kBlk) == 0);
       tc::mma_commit(&bar_stage[s]);
-      if ((it % kBlk) == kBlk - 1 || it == nst - 1) tc::mma_commit(&bar_slot[slot]);
+      if ((it % kBlk) == kBlk - 1 || it == nst - 1) tc::mma_commit(&bar_slot[blk & 1]);
     }
     used |= 1u << s;
-    if (((it % kBlk) == kBlk - 1 || it == nst - 1) && blk >= 1) {
-      const int ps = (blk - 1) & 1;
-      tc::mbar_wait(&bar_slot[ps], (ph_slot >> ps) & 1u);
-      ph_slot ^= 1u << ps;
-      tc::fence_after();
-      drain_add(t_acc + 128 * ps);
+    // two slots: once block blk is issued, drain block blk-1 (its slot is reused by block blk+1)
+    if (kSlots == 2 && ((it % kBlk) == kBlk - 1 || it == nst - 1) && blk >= 1) {
+      wait_block(blk - 1);
       tc::fence_before();
     }
   }
-  // epilogue: row r = 32 wq + lane of the tile, this warp's columns [c_lo, c_hi) (one 32-column chunk);
-  // the minuend C0 is loaded while the tensor core finishes the last block
+  // epilogue: row r = 32 wq + lane of the tile, this warp's columns [c_lo, c_hi);
+  // the minuend C0 (one 32-column chunk) is loaded while the tensor core finishes the last block
   const int r = 32 * wq + lane;
   float c0v[32];
   if (MODE == kNNSub) {
+    static_assert(MODE != kNNSub || kColW == 32, "one 32-column chunk per warp");
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int jj = c_lo + j;
       c0v[j] = (d.C0 && r < mr && jj < c_hi && jj < nc) ? __ldg(d.C0 + (int64_t)(j0 + jj) * d.ldc0 + i0 + r) : 0.f;
     }
   }
-  if (nst > 0) {  // last block
-    const int lb = (nst - 1) / kBlk, ls = lb & 1;
-    tc::mbar_wait(&bar_slot[ls], (ph_slot >> ls) & 1u);
-    ph_slot ^= 1u << ls;
-    tc::fence_after();
-    drain_add(t_acc + 128 * ls);
-  }
+  if (nst > 0) wait_block((nst - 1) / kBlk);  // last block
   for (int s = 0; s < 2; ++s) acquire(s);
-  static_assert(kColW == 32, "one 32-column chunk per warp in the epilogue");
   for (int c = c_lo; c < c_hi; c += 32) {
     float v[32];
     if (sum_empty) {
@@ -621,14 +639,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
           const int64_t gi = i0 + r, gj = j0 + jj;
           float x = v[j];
           if (MODE == kNNSub) x = c0v[j] - x;
+          const bool mirror = d.sym && NT == 128 && tm != tn;
           if (OUT64) {
             double* C = reinterpret_cast<double*>(d.C);
             C[gj * d.ldc + gi] = (double)x;
-            if (d.sym && tm != tn) C[gi * d.ldc + gj] = (double)x;
+            if (mirror) C[gi * d.ldc + gj] = (double)x;
           } else {
             float* C = reinterpret_cast<float*>(d.C);
             C[gj * d.ldc + gi] = x;
-            if (d.sym && tm != tn) C[gi * d.ldc + gj] = x;
+            if (mirror) C[gi * d.ldc + gj] = x;
           }
         }
       }
@@ -641,22 +660,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
 
 cudaError_t launch_gemm_tc(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN, bool nnsub, bool out64) {
   if (nprob <= 0) return cudaSuccess;
-  const int tm = (maxM + 127) / 128, tn = (maxN + 127) / 128;
+  // 256-wide tiles for the plain fp32 A^T B when the operand is wider than one tile (Z = Q^T F)
+  const bool wide = !nnsub && !out64 && maxN > 128 && c.tc_wide;
+  const int ntile = wide ? 256 : 128;
+  const int tm = (maxM + 127) / 128, tn = (maxN + ntile - 1) / ntile;
   dim3 g(tm * tn, nprob);
-#define GTC(MODE_, O64_)                                                                                       \
-  do {                                                                                                         \
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<MODE_, O64_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         (int)kSmemTc);                                                        \
-    if (e != cudaSuccess) return e;                                                                            \
-    k_gemm_tc<MODE_, O64_><<<g, kTcThreads, kSmemTc, c.stream>>>(d_descs, tn);                                  \
+#define GTC(MODE_, O64_, NT_)                                                                                      \
+  do {                                                                                                             \
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<MODE_, O64_, NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         (int)kSmemTc);                                                            \
+    if (e != cudaSuccess) return e;                                                                                \
+    k_gemm_tc<MODE_, O64_, NT_><<<g, kTcThreads, kSmemTc, c.stream>>>(d_descs, tn);                               \
   } while (0)
   if (nnsub) {
     if (out64) return cudaErrorInvalidValue;
-    GTC(kNNSub, false);
+    GTC(kNNSub, false, 128);
   } else if (out64) {
-    GTC(kTN, true);
+    GTC(kTN, true, 128);
+  } else if (wide) {
+    GTC(kTN, false, 256);
   } else {
-    GTC(kTN, false);
+    GTC(kTN, false, 128);
   }
 #undef GTC
   c.launches += 1;
