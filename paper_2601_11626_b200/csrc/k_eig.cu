@@ -87,15 +87,19 @@ __device__ __forceinline__ double block_sum8(double v, double* red) {
   return t;
 }
 
-// One fused pass over the trailing block B (rows/cols 0..m-1, column-major, ld):
+// One fused pass over the LOWER triangle of the trailing block B (rows/cols 0..m-1, column-major, ld;
+// the strictly upper part is never read or written):
 //   if UPD: B -= v w^T + w v^T   (v, w indexed with offset `off`)
-//   part[wid][i] = sum_{j in this warp's columns} B_new[i][j] * u[j]
+//   part[wid][i] = sum_{j in this warp's columns, j <= i} B_new[i][j] u[j]      (row partials)
+//   cpart[j]     = sum_{i > j} B_new[i][j] u[i]                                  (mirrored, one warp per column)
+// so that (B_new u)_i = sum_wid part[wid][i] + cpart[i]; dpart[wid] = this warp's share of u^T B_new u.
 template <int NT, bool UPD>
 __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, const double* __restrict__ u,
                                          const double* __restrict__ vv, const double* __restrict__ ww, int off,
-                                         double* __restrict__ part, int n, double* __restrict__ dpart) {
+                                         double* __restrict__ part, int n, double* __restrict__ dpart,
+                                         double* __restrict__ cpart) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double acc[NT], vi[NT], wi[NT];
+  double acc[NT], vi[NT], wi[NT], ui[NT];
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     const int i = lane + 32 * t;
@@ -103,9 +107,11 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
     acc[t] = 0.0;
     vi[t] = (UPD && ok) ? vv[off + i] : 0.0;
     wi[t] = (UPD && ok) ? ww[off + i] : 0.0;
+    ui[t] = ok ? u[i] : 0.0;
   }
+  double cdot = 0.0;  // sum over this warp's columns of cpart[j] u[j]
   // two columns per iteration (j, j + kTriWarps): all loads of both columns are issued before
-  // any store so that they overlap (the compiler cannot reorder smem loads across stores itself)
+  // any store so that they overlap (the compiler cannot reorder loads across stores itself)
   int j = wid;
   for (; j + kTriWarps < m; j += 2 * kTriWarps) {
     const int j1 = j + kTriWarps;
@@ -118,32 +124,47 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int i = lane + 32 * t;
-      if (32 * (t + 1) <= m || i < m) { x0[t] = col0[i]; x1[t] = col1[i]; }
+      x0[t] = 0.0; x1[t] = 0.0;
+      if (i < m && i >= j) x0[t] = col0[i];
+      if (i < m && i >= j1) x1[t] = col1[i];
     }
+    double c0 = 0.0, c1 = 0.0;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int i = lane + 32 * t;
-      if (32 * (t + 1) <= m || i < m) {
+      if (i < m && i >= j) {
         if (UPD) {
           x0[t] = fma(-vi[t], wj0, x0[t]); x0[t] = fma(-wi[t], vj0, x0[t]);
-          x1[t] = fma(-vi[t], wj1, x1[t]); x1[t] = fma(-wi[t], vj1, x1[t]);
           col0[i] = x0[t];
-          col1[i] = x1[t];
         }
         acc[t] = fma(x0[t], uj0, acc[t]);
+        if (i > j) c0 = fma(x0[t], ui[t], c0);
+      }
+      if (i < m && i >= j1) {
+        if (UPD) {
+          x1[t] = fma(-vi[t], wj1, x1[t]); x1[t] = fma(-wi[t], vj1, x1[t]);
+          col1[i] = x1[t];
+        }
         acc[t] = fma(x1[t], uj1, acc[t]);
+        if (i > j1) c1 = fma(x1[t], ui[t], c1);
       }
     }
+    c0 = warp_sum(c0);
+    c1 = warp_sum(c1);
+    if (lane == 0) { cpart[j] = c0; cpart[j1] = c1; }
+    cdot = fma(c0, uj0, cdot);
+    cdot = fma(c1, uj1, cdot);
   }
   if (j < m) {
     const double uj = u[j];
     double vj = 0.0, wj = 0.0;
     if (UPD) { vj = vv[off + j]; wj = ww[off + j]; }
     double* __restrict__ col = B + j * ld;
+    double c0 = 0.0;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int i = lane + 32 * t;
-      if (32 * (t + 1) <= m || i < m) {
+      if (i < m && i >= j) {
         double x = col[i];
         if (UPD) {
           x = fma(-vi[t], wj, x);
@@ -151,38 +172,43 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
           col[i] = x;
         }
         acc[t] = fma(x, uj, acc[t]);
+        if (i > j) c0 = fma(x, ui[t], c0);
       }
     }
+    c0 = warp_sum(c0);
+    if (lane == 0) cpart[j] = c0;
+    cdot = fma(c0, uj, cdot);
   }
   double dw = 0.0;
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     const int i = lane + 32 * t;
-    if (32 * (t + 1) <= m || i < m) {
+    if (i < m) {
       part[wid * n + i] = acc[t];
-      dw = fma(acc[t], u[i], dw);
+      dw = fma(acc[t], ui[t], dw);
     }
   }
   dw = warp_sum(dw);
-  if (lane == 0) dpart[wid] = dw;
+  if (lane == 0) dpart[wid] = dw + cdot;
 }
 
 template <bool UPD>
 __device__ __forceinline__ void tri_pass_dispatch(double* B, int ld, int m, const double* u, const double* vv,
-                                                  const double* ww, int off, double* part, int n, double* dpart) {
+                                                  const double* ww, int off, double* part, int n, double* dpart,
+                                                  double* cpart) {
   switch ((m + 31) >> 5) {
     case 0: break;
-    case 1: tri_pass<1, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    case 2: tri_pass<2, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    case 3: tri_pass<3, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    case 4: tri_pass<4, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    case 5: tri_pass<5, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    case 6: tri_pass<6, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    case 7: tri_pass<7, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    case 8: tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    case 9: case 10: tri_pass<10, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    case 11: case 12: tri_pass<12, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
-    default: tri_pass<16, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart); break;
+    case 1: tri_pass<1, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 2: tri_pass<2, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 3: tri_pass<3, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 4: tri_pass<4, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 5: tri_pass<5, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 6: tri_pass<6, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 7: tri_pass<7, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 8: tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 9: case 10: tri_pass<10, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 11: case 12: tri_pass<12, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    default: tri_pass<16, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
   }
 }
 
@@ -196,6 +222,7 @@ __device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld
                                            double* __restrict__ e2, double* __restrict__ esg,
                                            double* __restrict__ VH, double* __restrict__ tauH) {
   __shared__ double s_dot[kTriWarps], s_nrm[kTriWarps];
+  __shared__ double cpart[kTriMax];  // mirrored column partials of the lower-triangle passes
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // Per step (3 barriers): [all warps] fused update + product pass, each warp
   // also reduces its partial dot p.v2 -> | [all threads, redundantly] K from the
@@ -256,7 +283,7 @@ __device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld
     __syncthreads();
     double tau = reflector(0, v);
     __syncthreads();
-    tri_pass_dispatch<false>(A + 1 * ld + 1, ld, n - 1, v, nullptr, nullptr, 0, part, n, s_dot);
+    tri_pass_dispatch<false>(A + 1 * ld + 1, ld, n - 1, v, nullptr, nullptr, 0, part, n, s_dot, cpart);
     __syncthreads();
     for (int k = 0; k + 2 < n; ++k) {
       const int s = n - 1 - k;  // trailing size of step k (rows/cols k+1..n-1)
@@ -264,7 +291,7 @@ __device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld
 #pragma unroll
       for (int q = 0; q < kTriWarps; ++q) dsum += s_dot[q];
       const double Kc = 0.5 * tau * tau * dsum;  // (tau/2) p.v with p = tau * sum(part)
-      double p0 = 0.0;
+      double p0 = cpart[0];
 #pragma unroll
       for (int q = 0; q < kTriWarps; ++q) p0 += part[q * n];
       p0 *= tau;
@@ -272,7 +299,7 @@ __device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld
       double* c0 = A + (k + 1) * ld + (k + 1);
       double prt = 0.0;
       for (int i = tid; i < s; i += kTriThreads) {
-        double pi = 0.0;
+        double pi = cpart[i];
 #pragma unroll
         for (int q = 0; q < kTriWarps; ++q) pi += part[q * n + i];
         pi *= tau;
@@ -291,8 +318,8 @@ __device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld
       const double tau2 = reflector(k + 1, v2);
       __syncthreads();
       // fused: update trailing (local 1..s-1) and partial products with v2
-      if (tau != 0.0) tri_pass_dispatch<true>(c0 + ld + 1, ld, s - 1, v2, v, w, 1, part, n, s_dot);
-      else tri_pass_dispatch<false>(c0 + ld + 1, ld, s - 1, v2, v, w, 1, part, n, s_dot);
+      if (tau != 0.0) tri_pass_dispatch<true>(c0 + ld + 1, ld, s - 1, v2, v, w, 1, part, n, s_dot, cpart);
+      else tri_pass_dispatch<false>(c0 + ld + 1, ld, s - 1, v2, v, w, 1, part, n, s_dot, cpart);
       __syncthreads();
       double* tmp = v; v = v2; v2 = tmp;
       tau = tau2;
