@@ -88,32 +88,37 @@ __device__ __forceinline__ double block_sum8(double v, double* red) {
 }
 
 // One fused pass over the LOWER triangle of the trailing block B (rows/cols 0..m-1, column-major, ld;
-// the strictly upper part is never read or written):
+// the strictly upper part is never read or written), for the row segment [r0, r0 + 32 NT):
 //   if UPD: B -= v w^T + w v^T   (v, w indexed with offset `off`)
 //   part[wid][i] = sum_{j in this warp's columns, j <= i} B_new[i][j] u[j]      (row partials)
 //   cpart[j]     = sum_{i > j} B_new[i][j] u[i]                                  (mirrored, one warp per column)
 // so that (B_new u)_i = sum_wid part[wid][i] + cpart[i]; dpart[wid] = this warp's share of u^T B_new u.
+// Segments after the first accumulate into cpart / dpart (same warp, fixed order).
 template <int NT, bool UPD>
 __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, const double* __restrict__ u,
                                          const double* __restrict__ vv, const double* __restrict__ ww, int off,
                                          double* __restrict__ part, int n, double* __restrict__ dpart,
-                                         double* __restrict__ cpart) {
+                                         double* __restrict__ cpart, int r0, bool first) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double acc[NT], vi[NT], wi[NT], ui[NT];
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
-    const int i = lane + 32 * t;
+    const int i = r0 + lane + 32 * t;
     const bool ok = i < m;
     acc[t] = 0.0;
     vi[t] = (UPD && ok) ? vv[off + i] : 0.0;
     wi[t] = (UPD && ok) ? ww[off + i] : 0.0;
     ui[t] = ok ? u[i] : 0.0;
   }
-  double cdot = 0.0;  // sum over this warp's columns of cpart[j] u[j]
+  const int jend = min(m, r0 + 32 * NT);  // columns with rows in this segment
+  double cdot = 0.0;  // sum over this warp's columns of (this segment's) cpart[j] u[j]
+  auto put = [&](int j, double c) {
+    if (lane == 0) cpart[j] = first ? c : cpart[j] + c;
+  };
   // two columns per iteration (j, j + kTriWarps): all loads of both columns are issued before
   // any store so that they overlap (the compiler cannot reorder loads across stores itself)
   int j = wid;
-  for (; j + kTriWarps < m; j += 2 * kTriWarps) {
+  for (; j + kTriWarps < jend; j += 2 * kTriWarps) {
     const int j1 = j + kTriWarps;
     const double uj0 = u[j], uj1 = u[j1];
     double vj0 = 0.0, wj0 = 0.0, vj1 = 0.0, wj1 = 0.0;
@@ -123,7 +128,7 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
     double x0[NT], x1[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-      const int i = lane + 32 * t;
+      const int i = r0 + lane + 32 * t;
       x0[t] = 0.0; x1[t] = 0.0;
       if (i < m && i >= j) x0[t] = col0[i];
       if (i < m && i >= j1) x1[t] = col1[i];
@@ -131,7 +136,7 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
     double c0 = 0.0, c1 = 0.0;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-      const int i = lane + 32 * t;
+      const int i = r0 + lane + 32 * t;
       if (i < m && i >= j) {
         if (UPD) {
           x0[t] = fma(-vi[t], wj0, x0[t]); x0[t] = fma(-wi[t], vj0, x0[t]);
@@ -151,11 +156,12 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
     }
     c0 = warp_sum(c0);
     c1 = warp_sum(c1);
-    if (lane == 0) { cpart[j] = c0; cpart[j1] = c1; }
+    put(j, c0);
+    put(j1, c1);
     cdot = fma(c0, uj0, cdot);
     cdot = fma(c1, uj1, cdot);
   }
-  if (j < m) {
+  if (j < jend) {
     const double uj = u[j];
     double vj = 0.0, wj = 0.0;
     if (UPD) { vj = vv[off + j]; wj = ww[off + j]; }
@@ -163,7 +169,7 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
     double c0 = 0.0;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-      const int i = lane + 32 * t;
+      const int i = r0 + lane + 32 * t;
       if (i < m && i >= j) {
         double x = col[i];
         if (UPD) {
@@ -176,20 +182,24 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
       }
     }
     c0 = warp_sum(c0);
-    if (lane == 0) cpart[j] = c0;
+    put(j, c0);
     cdot = fma(c0, uj, cdot);
   }
+  // columns of this warp beyond the segment have no rows here: first segment still defines cpart
+  if (first)
+    for (int jj = (j < jend) ? j + kTriWarps : j; jj < m; jj += kTriWarps)
+      if (jj >= jend && lane == 0) cpart[jj] = 0.0;
   double dw = 0.0;
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
-    const int i = lane + 32 * t;
+    const int i = r0 + lane + 32 * t;
     if (i < m) {
       part[wid * n + i] = acc[t];
       dw = fma(acc[t], ui[t], dw);
     }
   }
   dw = warp_sum(dw);
-  if (lane == 0) dpart[wid] = dw + cdot;
+  if (lane == 0) dpart[wid] = first ? dw + cdot : dpart[wid] + dw + cdot;
 }
 
 template <bool UPD>
@@ -198,17 +208,18 @@ __device__ __forceinline__ void tri_pass_dispatch(double* B, int ld, int m, cons
                                                   double* cpart) {
   switch ((m + 31) >> 5) {
     case 0: break;
-    case 1: tri_pass<1, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    case 2: tri_pass<2, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    case 3: tri_pass<3, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    case 4: tri_pass<4, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    case 5: tri_pass<5, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    case 6: tri_pass<6, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    case 7: tri_pass<7, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    case 8: tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    case 9: case 10: tri_pass<10, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    case 11: case 12: tri_pass<12, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
-    default: tri_pass<16, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart); break;
+    case 1: tri_pass<1, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
+    case 2: tri_pass<2, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
+    case 3: tri_pass<3, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
+    case 4: tri_pass<4, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
+    case 5: tri_pass<5, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
+    case 6: tri_pass<6, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
+    case 7: tri_pass<7, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
+    case 8: tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
+    default:  // row segments of 256 (register budget of two CTAs per SM)
+      for (int r0 = 0; r0 < m; r0 += 256)
+        tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, r0, r0 == 0);
+      break;
   }
 }
 
@@ -330,7 +341,7 @@ __device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld
 // GL = true: the matrix is reduced in place in global memory (L2-resident; n up to 512), only the
 // vectors and partial sums live in shared memory.
 template <bool GL>
-__global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(const double* __restrict__ Gin, int64_t ld_in,
+__global__ void __launch_bounds__(kTriThreads, GL ? 2 : 1) k_tridiag(const double* __restrict__ Gin, int64_t ld_in,
                                                             int64_t stride_in, const int* __restrict__ ns,
                                                             const double* __restrict__ thr, int kw, int nstride,
                                                             double* __restrict__ dout, double* __restrict__ e2out,
