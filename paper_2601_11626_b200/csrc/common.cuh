@@ -125,6 +125,7 @@ struct Ctx {
   bool eig_rr = true;                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)
   bool zz_syrk = true;                 // w <= 128: Z^T Z by k_syrk_zz instead of k_gemm_tn (CMSVD_ZZ_SYRK=0: off)
   bool tc_big = true;                  // q or w > 128: tcgen05 GEMM tiles instead of SIMT (CMSVD_TC_BIG=0: off)
+  bool big_tc = true;                  // A22 subspace-iteration products on tcgen05 tiles (CMSVD_BIG_TC=0: SIMT fp64)
   bool tc_wide = true;                 // ... with 256-column tiles for Z = Q^T F (CMSVD_TC_WIDE=0: 128)
   bool eig_duo = true;                 // n <= 128: two problems per CTA with dedicated row warps (CMSVD_EIG_DUO=0: off)
   bool commit_topk = true;             // Alg. 3 commits: top-r eigenpairs by inverse iteration (CMSVD_COMMIT_TOPK=0: QL)

@@ -276,6 +276,47 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
       CK(cudaMemcpyAsync(dids, hid.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
       CK(cudaMemcpyAsync(dns, hns.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
       const int64_t ms = m * s, ns_ = (int64_t)n * s;
+      if (c.big_tc && c.use_tc) {
+        // the products with A on tcgen05 (3xTF32 tiles, fp64 outputs for the fp64 CholQR2); the
+        // orthonormal bases enter them rounded to fp32 (a 6e-8 relative perturbation of the basis,
+        // which the next power iteration and CholQR absorb; the Rayleigh-Ritz values move by O(u32))
+        CK(ensure(c.ws[WS_D], (size_t)nb * (m + n) * s * 4 + (size_t)n * s * 4), "spectra: fp32 bases");
+        CK(ensure(c.ws[WS_E], (size_t)3 * nb * sizeof(GemmDesc)), "spectra: descs");
+        float* Y32 = (float*)c.ws[WS_D].p;
+        float* Z32 = Y32 + (size_t)nb * m * s;
+        float* Om32 = Z32 + (size_t)nb * n * s;
+        GemmDesc* dAO = (GemmDesc*)c.ws[WS_E].p;
+        GemmDesc* dAtY = dAO + nb;
+        GemmDesc* dAZ = dAtY + nb;
+        std::vector<GemmDesc> hd(3 * (size_t)nb);
+        for (int t = 0; t < nb; ++t) {
+          GemmDesc g{};
+          g.A = hA[t]; g.lda = m; g.C0 = nullptr; g.ldc0 = 0; g.sym = 0;
+          g.B = Om32; g.ldb = n; g.C = Y + (size_t)t * ms; g.ldc = m; g.M = (int)m; g.N = s; g.K = n;   // Y = A Om
+          hd[t] = g;
+          g.B = Y32 + (size_t)t * ms; g.ldb = m; g.C = Z + (size_t)t * ns_; g.ldc = n; g.M = n; g.K = (int)m;  // Z = A^T Y
+          hd[nb + t] = g;
+          g.B = Z32 + (size_t)t * ns_; g.ldb = n; g.C = Y + (size_t)t * ms; g.ldc = m; g.M = (int)m; g.K = n;  // Y = A Z
+          hd[2 * nb + t] = g;
+        }
+        CK(cudaMemcpyAsync(dAO, hd.data(), hd.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice, c.stream),
+           "spectra: h2d");
+        // orthonormalisation once per power step A A^T (the intermediate Z = A^T Y is used as is: the
+        // step's condition number (sigma_1 / sigma_s)^2 stays far inside CholQR's fp64 range), one
+        // CholQR pass inside the loop, CholQR2 for the final basis of the Rayleigh-Ritz step
+        CK(launch_to_f32(c, Om, Om32, (int64_t)n * s), "spectra: Omega32");
+        CK(launch_gemm_tc_nn64(c, dAO, nb, (int)m, s), "spectra: AO (tc)");
+        CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st, 1), "spectra: cholqr");
+        for (int it = 0; it < c.subspace_iters; ++it) {
+          CK(launch_to_f32(c, Y, Y32, (int64_t)nb * ms), "spectra: Y32");
+          CK(launch_gemm_tc(c, dAtY, nb, n, s, false, true), "spectra: AtY (tc)");
+          CK(launch_to_f32(c, Z, Z32, (int64_t)nb * ns_), "spectra: Z32");
+          CK(launch_gemm_tc_nn64(c, dAZ, nb, (int)m, s), "spectra: AZ (tc)");
+          CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st, it + 1 == c.subspace_iters ? 2 : 1), "spectra: cholqr");
+        }
+        CK(launch_to_f32(c, Y, Y32, (int64_t)nb * ms), "spectra: Y32");
+        CK(launch_gemm_tc(c, dAtY, nb, n, s, false, true), "spectra: Bt (tc)");
+      } else {
       // Y = A Omega, orth
       CK((gemm_mixed<float, false>(c, nb, (int)m, s, n, nullptr, m, 0, Om, n, 0, Y, m, ms, 1.0, dA)), "spectra: AO");
       CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st), "spectra: cholqr");
@@ -289,6 +330,7 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
       }
       // Rayleigh-Ritz: Bt = A^T Q, H = Bt^T Bt
       CK((gemm_mixed<float, true>(c, nb, n, s, (int)m, nullptr, m, 0, Y, m, ms, Z, n, ns_, 1.0, dA)), "spectra: Bt");
+      }
       CK((gemm_mixed<double, true>(c, nb, s, s, n, Z, n, ns_, Z, n, ns_, H, s, (int64_t)s * s)), "spectra: H");
       CK(launch_syev(c, H, s, (int64_t)s * s, dns, nb, s, (double*)c.ws[WS_V].p, (int64_t)s * s,
                      (double*)c.ws[WS_B].p, (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, s, st + nb),

@@ -7,10 +7,10 @@ namespace cmsvd {
 
 typedef cmsvd_status Status;
 
-constexpr int kEigMax = 512;
+constexpr int kEigMax = 512;  // largest Gram handled by the eigensolvers (> 160: in place in global memory)
 
 // context workspace slots (Ctx::ws)
-enum { WS_PARTIAL = 0, WS_BAD, WS_META, WS_G, WS_V, WS_EV, WS_PERM, WS_STAT, WS_PAIR, WS_OUT, WS_A, WS_B, WS_C };     // largest Gram handled by the eigensolvers (> 160: in place in global memory)
+enum { WS_PARTIAL = 0, WS_BAD, WS_META, WS_G, WS_V, WS_EV, WS_PERM, WS_STAT, WS_PAIR, WS_OUT, WS_A, WS_B, WS_C, WS_D, WS_E };
 
 struct Dims {
   int qmax = 0;   // projection-basis columns (full range)

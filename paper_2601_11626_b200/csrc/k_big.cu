@@ -12,6 +12,8 @@
 // problem, global memory), Gaussian test matrices (counter-based hash).
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -103,28 +105,34 @@ cudaError_t gemm_mixed(Ctx& c, int batch, int M, int N, int K, const TAe* A, int
 // Grams factorable (CholQR2: the second pass re-orthonormalises).
 // One CTA per problem (256 threads), matrices in global memory (L2-resident).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_chol_inv(double* __restrict__ Hs, double* __restrict__ Ts, int s,
-                                                  int64_t stride, int* __restrict__ status) {
+constexpr int kCholThreads = 1024;
+__global__ void __launch_bounds__(kCholThreads) k_chol_inv(double* __restrict__ Hs, double* __restrict__ Ts, int s,
+                                                          int64_t stride, int* __restrict__ status) {
+  // s <= 512: row k of R (Cholesky) / column j of R (inverse) staged in shared memory; every pass over
+  // the matrices is coalesced (lanes over consecutive rows of a column)
+  __shared__ double rk[512];
+  __shared__ double s_piv, s_shift;
+  __shared__ double red[kCholThreads / 32];
+  __shared__ int s_bad;
   double* H = Hs + (int64_t)blockIdx.x * stride;
   double* T = Ts + (int64_t)blockIdx.x * stride;
-  const int tid = threadIdx.x;
-  __shared__ double s_piv, s_shift;
-  __shared__ double red[8];
-  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int nw = kCholThreads / 32;
   double mx = 0.0;
-  for (int i = tid; i < s; i += blockDim.x) mx = fmax(mx, fabs(H[(int64_t)i * s + i]));
+  for (int i = tid; i < s; i += kCholThreads) mx = fmax(mx, fabs(H[(int64_t)i * s + i]));
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  if (lane == 0) red[wid] = mx;
   __syncthreads();
   if (tid == 0) {
     double m2 = 0.0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m2 = fmax(m2, red[k]);
+    for (int k = 0; k < nw; ++k) m2 = fmax(m2, red[k]);
     s_shift = 1e-13 * m2;
     s_bad = 0;
   }
   __syncthreads();
-  for (int i = tid; i < s; i += blockDim.x) H[(int64_t)i * s + i] += s_shift;
+  for (int i = tid; i < s; i += kCholThreads) H[(int64_t)i * s + i] += s_shift;
   __syncthreads();
+  // right-looking Cholesky H = R^T R, R upper (H(k, j) for k <= j)
   for (int k = 0; k < s; ++k) {
     if (tid == 0) {
       double d = H[(int64_t)k * s + k];
@@ -134,28 +142,35 @@ __global__ void __launch_bounds__(256) k_chol_inv(double* __restrict__ Hs, doubl
     }
     __syncthreads();
     const double inv = 1.0 / s_piv;
-    for (int j = k + 1 + tid; j < s; j += blockDim.x) H[(int64_t)j * s + k] *= inv;  // R(k, j)
-    __syncthreads();
-    const int rem = s - k - 1;
-    // H(i, j) -= R(k, i) R(k, j) for k < i <= j: one thread per column j, loop over i
-    for (int j = k + 1 + tid; j < s; j += blockDim.x) {
-      const double rkj = H[(int64_t)j * s + k];
-      double* colj = H + (int64_t)j * s;
-      for (int i = k + 1; i <= j; ++i) colj[i] = fma(-H[(int64_t)i * s + k], rkj, colj[i]);
+    for (int j = k + 1 + tid; j < s; j += kCholThreads) {
+      const double v = H[(int64_t)j * s + k] * inv;  // R(k, j)
+      H[(int64_t)j * s + k] = v;
+      rk[j] = v;
     }
-    (void)rem;
+    __syncthreads();
+    // H(i, j) -= R(k, i) R(k, j) for k < i <= j: warp per column j, lanes over rows i
+    for (int j = k + 1 + wid; j < s; j += nw) {
+      const double rkj = rk[j];
+      double* colj = H + (int64_t)j * s;
+      for (int i = k + 1 + lane; i <= j; i += 32) colj[i] = fma(-rk[i], rkj, colj[i]);
+    }
     __syncthreads();
   }
-  // T = R^{-1}: column j by one thread, back substitution
-  for (int j = tid; j < s; j += blockDim.x) {
-    double* tj = T + (int64_t)j * s;
-    for (int i = j + 1; i < s; ++i) tj[i] = 0.0;
-    tj[j] = 1.0 / H[(int64_t)j * s + j];
-    for (int i = j - 1; i >= 0; --i) {
+  // T = R^{-1} (upper), column by column: T(j, j) = 1 / R(j, j), T(0:j, j) = -T(j, j) T(0:j, 0:j) R(0:j, j)
+  for (int e = tid; e < s * s; e += kCholThreads) T[e] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < s; ++j) {
+    for (int k = tid; k <= j; k += kCholThreads) rk[k] = H[(int64_t)j * s + k];  // R(0:j, j)
+    __syncthreads();
+    const double tjj = 1.0 / rk[j];
+    for (int r = tid; r < j; r += kCholThreads) {  // T(r, k) = 0 for k < r: lanes read rows r of column k
       double acc = 0.0;
-      for (int k = i + 1; k <= j; ++k) acc = fma(H[(int64_t)k * s + i], tj[k], acc);
-      tj[i] = -acc / H[(int64_t)i * s + i];
+#pragma unroll 8
+      for (int k = 0; k < j; ++k) acc = fma(T[(int64_t)k * s + r], rk[k], acc);
+      T[(int64_t)j * s + r] = -tjj * acc;
     }
+    if (tid == 0) T[(int64_t)j * s + j] = tjj;
+    __syncthreads();
   }
   if (tid == 0) status[blockIdx.x] = s_bad;
 }
@@ -182,16 +197,29 @@ cudaError_t launch_randn(Ctx& c, double* X, int64_t n, uint64_t seed) {
   return cudaGetLastError();
 }
 
+__global__ void k_to_f32(const double* __restrict__ X, float* __restrict__ Y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    Y[i] = (float)X[i];
+}
+
+cudaError_t launch_to_f32(Ctx& c, const double* X, float* Y, int64_t n) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c.sm_count * 16);
+  k_to_f32<<<blocks, 256, 0, c.stream>>>(X, Y, n);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 // CholQR on a batch: Y (rows x s per problem, ld rows) -> Y T with Y^T Y = R^T R, T = R^{-1}.
 // Workspace: H, T (s x s each per problem), Ytmp (rows x s per problem).
 cudaError_t cholqr(Ctx& c, int batch, int64_t rows, int s, double* Y, double* Ytmp, double* H, double* T,
-                   int* status) {
+                   int* status, int passes) {
   cudaError_t e;
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int pass = 0; pass < passes; ++pass) {
     e = gemm_mixed<double, true>(c, batch, s, s, (int)rows, Y, rows, rows * s, Y, rows, rows * s, H, s,
                                  (int64_t)s * s);
     if (e != cudaSuccess) return e;
-    k_chol_inv<<<batch, 256, 0, c.stream>>>(H, T, s, (int64_t)s * s, status);
+    k_chol_inv<<<batch, kCholThreads, 0, c.stream>>>(H, T, s, (int64_t)s * s, status);
     c.launches += 1;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -1482,19 +1482,46 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
       if (m == l || s_fail) break;
       const int lo_i = s_l;
       // apply rotations i = m-1 .. lo_i to columns (i, i+1) of Z: each thread owns rows
-      for (int row = tid; row < n; row += kTriThreads) {
-        double* z = A + row;
-        // the rotated column i is carried in a register to the next rotation; loads run one ahead
-        double f = z[(int64_t)m * ldz];
-        double zi = z[(int64_t)(m - 1) * ldz];
-        for (int i = m - 1; i >= lo_i; --i) {
-          const double zn = (i > lo_i) ? z[(int64_t)(i - 1) * ldz] : 0.0;
-          const double c_ = rc[i], s_ = rs[i];
-          z[(int64_t)(i + 1) * ldz] = s_ * zi + c_ * f;
-          f = c_ * zi - s_ * f;
-          zi = zn;
+      if (GL) {
+        for (int row = tid; row < n; row += kTriThreads) {
+          double* z = A + row;
+          // the rotated column i is carried in a register to the next rotation; the original values of
+          // the next 8 columns are loaded ahead in one batch (every load precedes the stores that follow
+          // it), which hides the global-memory latency of the in-place (n > 160) variant
+          double f = z[(int64_t)m * ldz];
+          int i = m - 1;
+          while (i >= lo_i) {
+            const int cnt = min(8, i - lo_i + 1);
+            double zc[8];
+  #pragma unroll
+            for (int t = 0; t < 8; ++t) zc[t] = (t < cnt) ? z[(int64_t)(i - t) * ldz] : 0.0;
+  #pragma unroll
+            for (int t = 0; t < 8; ++t)
+              if (t < cnt) {
+                const int ii = i - t;
+                const double c_ = rc[ii], s_ = rs[ii];
+                z[(int64_t)(ii + 1) * ldz] = s_ * zc[t] + c_ * f;
+                f = c_ * zc[t] - s_ * f;
+              }
+            i -= cnt;
+          }
+          z[(int64_t)lo_i * ldz] = f;
         }
-        z[(int64_t)lo_i * ldz] = f;
+      } else {
+        for (int row = tid; row < n; row += kTriThreads) {
+          double* z = A + row;
+          // the rotated column i is carried in a register to the next rotation; loads run one ahead
+          double f = z[(int64_t)m * ldz];
+          double zi = z[(int64_t)(m - 1) * ldz];
+          for (int i = m - 1; i >= lo_i; --i) {
+            const double zn = (i > lo_i) ? z[(int64_t)(i - 1) * ldz] : 0.0;
+            const double c_ = rc[i], s_ = rs[i];
+            z[(int64_t)(i + 1) * ldz] = s_ * zi + c_ * f;
+            f = c_ * zi - s_ * f;
+            zi = zn;
+          }
+          z[(int64_t)lo_i * ldz] = f;
+        }
       }
       __syncthreads();
       ++iter;
@@ -1505,17 +1532,28 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
 #ifdef CMSVD_SYEV_PROF
   unsigned long long t2 = clock64();
 #endif
-  // ---- back-transformation Z <- H_0 H_1 ... H_{n-3} Z (thread per column) ----
+  // ---- back-transformation Z <- H_0 H_1 ... H_{n-3} Z ----
+  // shared memory: thread per column; global memory (GL): warp per column, lanes over rows (coalesced)
   for (int k = n - 3; k >= 0; --k) {
     const double tk = tauH[k];
     if (tk != 0.0) {
       const double* vk = VH + (int64_t)k * n + k + 1;  // length n-1-k, vk[0] = 1
-      for (int c = tid; c < n; c += kTriThreads) {
-        double* zc = A + (int64_t)c * ldz + k + 1;
-        double dot = 0.0;
-        for (int i = 0; i < n - 1 - k; ++i) dot = fma(vk[i], zc[i], dot);
-        dot *= tk;
-        for (int i = 0; i < n - 1 - k; ++i) zc[i] = fma(-dot, vk[i], zc[i]);
+      if (GL) {
+        for (int c = wid; c < n; c += kTriWarps) {
+          double* zc = A + (int64_t)c * ldz + k + 1;
+          double dot = 0.0;
+          for (int i = lane; i < n - 1 - k; i += 32) dot = fma(vk[i], zc[i], dot);
+          dot = warp_sum(dot) * tk;
+          for (int i = lane; i < n - 1 - k; i += 32) zc[i] = fma(-dot, vk[i], zc[i]);
+        }
+      } else {
+        for (int c = tid; c < n; c += kTriThreads) {
+          double* zc = A + (int64_t)c * ldz + k + 1;
+          double dot = 0.0;
+          for (int i = 0; i < n - 1 - k; ++i) dot = fma(vk[i], zc[i], dot);
+          dot *= tk;
+          for (int i = 0; i < n - 1 - k; ++i) zc[i] = fma(-dot, vk[i], zc[i]);
+        }
       }
     }
     __syncthreads();

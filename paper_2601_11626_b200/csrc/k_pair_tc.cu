@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
 // One CTA (16 warps) per 128 x 128 output tile: grid (tiles_m * tiles_n, batch); sym = 1 computes the
 // lower tiles only and mirrors them.  OUT64 stores C as fp64 (W' for the fp64 Gram assembly).
 // ---------------------------------------------------------------------------
-enum { kTN = 0, kNNSub = 1 };
+enum { kTN = 0, kNNSub = 1, kNN = 2 };  // kNN: C = A B (A: M x K, B: K x N column-major)
 // NT = output tile width (128, or 256 for the plain A^T B: the A tile is then staged once per 256 output
 // columns, which brings the shared-memory traffic per MMA below the tensor core's operand rate; TMEM then
 // holds one 256-column block slot + the running sum, so a block's drain is not overlapped with the next
@@ -487,6 +487,7 @@ enum { kTN = 0, kNNSub = 1 };
 template <int MODE, bool OUT64, int NT>
 __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __restrict__ descs, int tiles_n) {
   static_assert(NT == 128 || (NT == 256 && MODE == kTN), "256-wide tiles: A^T B only");
+  static_assert(MODE != kNNSub || !OUT64, "C0 - A B: fp32 output");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar_stage[2];
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
   float4 av[kItK], ar[kItR], bv[kBT][kItK];
   auto load_a = [&](int64_t k0) {
     if (MODE == kTN) load_kcontig<true>(av, 128, d.A + (int64_t)i0 * d.lda, d.lda, mr, k0, K);
-    else load_rcontig(ar, d.A, d.lda, i0, d.M, (int)k0, K);
+    else load_rcontig(ar, d.A, d.lda, i0, d.M, (int)k0, K);  // kNNSub, kNN
   };
   auto load_b = [&](int64_t k0) {
 #pragma unroll
@@ -577,7 +578,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
     const int blk = it / kBlk, slot = blk % kSlots;
     acquire(s);
     if (MODE == kTN) store_kcontig(av, stage_ptr(s, 0), stage_ptr(s, 1), 128, nullptr);
-    else store_rcontig(ar, stage_ptr(s, 0), nullptr, stage_ptr(s, 1));
+    else store_rcontig(ar, stage_ptr(s, 0), nullptr, stage_ptr(s, 1));  // kNNSub, kNN
 #pragma unroll
     for (int h = 0; h < kBT; ++h)
       store_kcontig(bv[h], stage_ptr(s, 2) + h * kTile, stage_ptr(s, 2 + kBT) + h * kTile, 128, nullptr);
@@ -656,6 +657,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const GemmDesc* __res
   tc::fence_before();
   __syncthreads();
   if (wid == 0) tc::tmem_dealloc(tmem, 512);
+}
+
+cudaError_t launch_gemm_tc_nn64(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN) {
+  if (nprob <= 0) return cudaSuccess;
+  const int tm = (maxM + 127) / 128, tn = (maxN + 127) / 128;
+  dim3 g(tm * tn, nprob);
+  cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<kNN, true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemTc);
+  if (e != cudaSuccess) return e;
+  k_gemm_tc<kNN, true, 128><<<g, kTcThreads, kSmemTc, c.stream>>>(d_descs, tn);
+  c.launches += 1;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_gemm_tc(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN, bool nnsub, bool out64) {

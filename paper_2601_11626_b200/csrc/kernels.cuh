@@ -57,6 +57,10 @@ cudaError_t launch_pair_tc(Ctx& c, const int2* pairs, int64_t P, const BaseDesc*
                            int use_full_basis, int QMAX, int WMAX, float* Zws, double* Wws);
 // batched 3xTF32 tcgen05 GEMM tiles (C = A^T B, or C = C0 - A B with nnsub); out64: fp64 C
 cudaError_t launch_gemm_tc(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN, bool nnsub, bool out64);
+// C (fp64) = A B, A: M x K, B: K x N column-major fp32 (3xTF32 tiles)
+cudaError_t launch_gemm_tc_nn64(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN);
+// Y[i] = (float) X[i] for n doubles
+cudaError_t launch_to_f32(Ctx& c, const double* X, float* Y, int64_t n);
 cudaError_t launch_syrk_zz(Ctx& c, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad,
                            int use_full_basis, int QMAX, int WMAX, const float* Zws, double* ZZws);
 cudaError_t launch_build_G1(Ctx& c, int rr, int w, const double* spec, const float* Z, int ldz, const double* ZZ,
@@ -74,7 +78,7 @@ __global__ void k_big_stats(int nb, const int* ids, int s, int r, int64_t m, int
                             BaseDesc* bd, AppDesc* ad_raw, AppDesc* ad_trunc);
 cudaError_t launch_randn(Ctx& c, double* X, int64_t n, uint64_t seed);
 cudaError_t cholqr(Ctx& c, int batch, int64_t rows, int s, double* Y, double* Ytmp, double* H, double* T,
-                   int* status);
+                   int* status, int passes = 2);
 __global__ void k_trunc_operand(int64_t m, const BaseDesc* bd, const AppDesc* ad_trunc, float* Fbase);
 
 }  // namespace cmsvd
