@@ -84,9 +84,18 @@ def workload(name: str, rank: int):
     elif name.startswith("config5"):
         r = 64 if name.endswith("r64") else 16
         col = synth.config5(seed=4 + 1000 * rank, N=512, r=r)
+    elif name == "config3":
+        col = synth.config3(seed=2 + 1000 * rank)
+    elif name == "config4":
+        col = synth.config4(seed=3 + 1000 * rank)
     else:
         raise SystemExit(f"unknown config {name}")
     return col
+
+
+def is_big(name: str) -> bool:
+    """configs 3/4: square weight-like blocks, TRUNC operand (A6), A22 spectra."""
+    return name in ("config3", "config4")
 
 
 def max_over_ranks(dist, x: float, dev=None) -> float:
@@ -173,21 +182,37 @@ def tridiag_flops(n):
     return 4.0 / 3.0 * n ** 3
 
 
-def cpu_baseline(col, pairs, r, sample, timeout_s=40.0):
+def cpu_baseline(col, pairs, r, sample, timeout_s=40.0, big=False):
     import oracle
-    t0 = time.perf_counter()
-    sp = oracle.block_spectra(col.blocks)
-    t_spec = time.perf_counter() - t0
     P = pairs.shape[0]
-    S = min(sample, P)
-    t0 = time.perf_counter()
-    oracle.pair_errors(sp, pairs[:S], r, 7, oracle.RAW)
-    t_pairs = time.perf_counter() - t0
+    if big:
+        # configs 3/4: the oracle's exact m x m Gram eigendecompositions cost seconds per block, so the
+        # sample is the pairs among the first three norm-ordered blocks, their spectra scaled to all N
+        ids = list(dict.fromkeys(int(b) for pr in pairs[:3] for b in pr))[:3]
+        sub = np.array([[a, b] for a in range(len(ids)) for b in range(len(ids)) if a != b], np.int32)
+        t0 = time.perf_counter()
+        sp = oracle.block_spectra(np.ascontiguousarray(col.blocks[ids]))
+        t_spec = (time.perf_counter() - t0) * col.N / len(ids)
+        S = sub.shape[0]
+        t0 = time.perf_counter()
+        oracle.pair_errors(sp, sub, r, 7, oracle.TRUNC)
+        t_pairs = time.perf_counter() - t0
+        what = (f"the {S} ordered pairs among blocks {ids} (TRUNC operand, all 3 estimators, float64 oracle); "
+                f"block spectra measured on those {len(ids)} blocks, scaled to all {col.N} ({t_spec:.1f} s) "
+                f"and prorated by {S}/{P}")
+    else:
+        t0 = time.perf_counter()
+        sp = oracle.block_spectra(col.blocks)
+        t_spec = time.perf_counter() - t0
+        S = min(sample, P)
+        t0 = time.perf_counter()
+        oracle.pair_errors(sp, pairs[:S], r, 7, oracle.RAW)
+        t_pairs = time.perf_counter() - t0
+        what = (f"first {S} of the {P} norm-ordered pairs, all 3 estimators, float64 oracle "
+                f"(OpenMP over pairs); its block spectra ({t_spec:.2f} s for all {col.N} blocks) "
+                f"prorated by {S}/{P}")
     rate = S / (t_pairs + t_spec * S / P)
-    return {"value": rate, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"first {S} of the {P} norm-ordered pairs, all 3 estimators, float64 oracle "
-                      f"(OpenMP over pairs); its block spectra ({t_spec:.2f} s for all {col.N} blocks) "
-                      f"prorated by {S}/{P}",
+    return {"value": rate, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle", "sample": what,
             "seconds": t_pairs + t_spec * S / P}
 
 
@@ -196,6 +221,9 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle
+    if is_big(args.config):
+        raise SystemExit("--impl reference times configs 1, 2 and 5 (configs 3/4: see cpu_baseline of the "
+                         "cmsvd arm, whose oracle sample covers a block subset)")
     col = workload(args.config, 0)
     sp = oracle.block_spectra(col.blocks)
     order = np.array(sorted(range(col.N), key=lambda i: (-sp.E[i], i)))
@@ -260,10 +288,13 @@ def main():
            "mu": torch.empty((P, r), dtype=torch.float32, device=dev)}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    big = is_big(args.config)
+    operand = cm.TRUNC if big else cm.RAW
+
     def step():
         ctx.register(blocks_d)
         ctx.block_spectra(r)
-        ctx.pair_errors(pairs_d, out=out)
+        ctx.pair_errors(pairs_d, out=out, operand=operand)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -294,46 +325,56 @@ def main():
     value = units / (total_ms / 1e3)
 
     # ---- roofline of the dominant kernel category (live CUDA events) ----
-    q = blk_rank[pairs[:, 0]].astype(np.float64)          # full-range basis columns of each base
-    rr = np.minimum(r, blk_rank)[pairs[:, 0]].astype(np.float64)
-    w = float(col.n)
+    rr_b = np.minimum(r, blk_rank).astype(np.float64)
+    # projection basis of each base: the full numerical range (configs 1, 2, 5) or U_r (A22 blocks);
+    # appended operand width: the raw block (RAW) or its rank-r factor (TRUNC)
+    q = (rr_b if big else blk_rank.astype(np.float64))[pairs[:, 0]]
+    w = rr_b[pairs[:, 1]] if big else np.full(P, float(col.n))
+    rr = rr_b[pairs[:, 0]]
     nG = rr + w
     flops = {                                                # algorithmic flops per launch (all P pairs)
         "eig_G": float(np.sum(tridiag_flops(nG))),
-        "eig_W": float(P * tridiag_flops(w)),
-        "gram_W": float(P) * col.m * w * (w + 1),
-        "gram_ZZ": float(np.sum(q)) * w * (w + 1),
+        "eig_W": float(np.sum(tridiag_flops(w))),
+        "gram_W": float(np.sum(col.m * w * (w + 1))),
+        "gram_ZZ": float(np.sum(q * w * (w + 1))),
         "proj_Z": float(np.sum(2.0 * col.m * q * w)),
         "resid_R": float(np.sum(2.0 * col.m * q * w)),
-        "pair_tc": float(np.sum(4.0 * col.m * q * w) + P * col.m * w * (w + 1)),   # Z, R', W' useful flops
+        "pair_tc": float(np.sum(4.0 * col.m * q * w + col.m * w * (w + 1))),   # Z, R', W' useful flops
     }
-    peaks = {"eig_G": DFMA_TFLOPS, "eig_W": DFMA_TFLOPS, "gram_W": DFMA_TFLOPS, "gram_ZZ": DFMA_TFLOPS,
-             "proj_Z": FFMA_TFLOPS, "resid_R": FFMA_TFLOPS, "pair_tc": tf32_fp32eq_tflops()}
+    # operands wider than 128 columns run Z, R', W' as tcgen05 GEMM tiles (k_gemm_tc), else SIMT
+    tiles = float(np.max(q)) > 128 or float(np.max(w)) > 128
+    tc_peak = tf32_fp32eq_tflops()
+    peaks = {"eig_G": DFMA_TFLOPS, "eig_W": DFMA_TFLOPS, "gram_W": tc_peak if tiles else DFMA_TFLOPS,
+             "gram_ZZ": DFMA_TFLOPS, "proj_Z": tc_peak if tiles else FFMA_TFLOPS,
+             "resid_R": tc_peak if tiles else FFMA_TFLOPS, "pair_tc": tc_peak}
     kernels = {}
     for name, (ms, cnt) in prof.items():
         if cnt == 0:
             continue
         e = {"ms_total": ms, "launches": cnt, "share": ms / max(total_ms, 1e-9)}
         if name in flops:
-            per_launch = flops[name]
-            avg = ms / cnt
-            e["tflops"] = per_launch / (avg * 1e-3) / 1e12
+            # flops[name] covers all P pairs of one step; a step may launch a category several times
+            # (pair-workspace chunks), so the rate is per step, not per launch group
+            e["tflops"] = flops[name] * args.steps / (ms * 1e-3) / 1e12
             e["frac_of_peak"] = e["tflops"] / peaks[name]
         kernels[name] = e
-    dom = max((k for k in kernels), key=lambda k: kernels[k]["ms_total"])
+    # dominant category with an algorithmic flop model (configs 3/4: the one-time A22 block spectra of the
+    # step can take longer; they are reported as "dominant_category")
+    dom_all = max((k for k in kernels), key=lambda k: kernels[k]["ms_total"])
+    dom = max((k for k in kernels if k in flops), key=lambda k: kernels[k]["ms_total"], default=dom_all)
     d = kernels[dom]
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")   # dram bytes per launch from ncu --set full
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get(args.config, {}).get(dom)
     if dom in flops:
-        roof = {"bound": "tensor" if dom == "pair_tc" else "alu", "kernel": dom, "achieved": d["tflops"],
+        roof = {"bound": "tensor" if peaks[dom] == tc_peak else "alu", "kernel": dom, "achieved": d["tflops"],
                 "peak": peaks[dom], "unit": "TFLOP/s",
                 "frac": d["frac_of_peak"], "traffic": traffic,
                 "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
                                 "(profiles/ncu_*_summary.txt)",
                 "peak_source": ("MEASURED_PEAKS.json bf16 burst x 0.5 (nominal TF32/BF16) / 3 (3xTF32 MMAs per "
-                                "useful fp32 product)") if dom == "pair_tc" else
+                                "useful fp32 product)") if peaks[dom] == tc_peak else
                                ("own DFMA/FFMA microbenchmark (tools/peaks.cu, profiles/peaks_r01.txt); "
                                 "MEASURED_PEAKS.json has no FP64/FP32-SIMT peak"),
                 "algorithmic": "Householder tridiagonalisation 4/3 n^3 flops per (r'+w)^2 Gram"
@@ -346,11 +387,11 @@ def main():
               "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
               "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
               "config": {"workload": args.config, "N": col.N, "m": col.m, "n": col.n, "r": r, "pairs": P,
-                         "kinds": "weyl+residual+incremental", "operand": "RAW",
+                         "kinds": "weyl+residual+incremental", "operand": "TRUNC" if big else "RAW",
                          "step": "register(S1)+block_spectra(S2)+pair_errors(S3-S9), device-resident input",
                          "l2": "flushed (256 MiB write) before every step, outside the step events",
                          "parallelism": f"replicas x{ws} (independent collections, no collective)"},
-              "gpu_launches": launches, "roofline": roof, "kernels": kernels,
+              "gpu_launches": launches, "roofline": roof, "kernels": kernels, "dominant_category": dom_all,
               "step_ms": times}
     with_clk = clk.summary()
     result["clocks"] = with_clk
@@ -362,13 +403,13 @@ def main():
         ctx2 = cm.Context(local, stream.cuda_stream)
         ctx2.register(pinned)
         ctx2.block_spectra(r)
-        ctx2.pair_errors(pairs_h)
+        ctx2.pair_errors(pairs_h, operand=operand)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             ctx2.register(pinned)
             ctx2.block_spectra(r)
-            res_h = ctx2.pair_errors(pairs_h)
+            res_h = ctx2.pair_errors(pairs_h, operand=operand)
         t_e2e = time.perf_counter() - t0
         t_e2e = max_over_ranks(dist, t_e2e, dev)
         h2d = col.blocks.nbytes + pairs_h.nbytes
@@ -381,7 +422,7 @@ def main():
         ctx2.close()
 
     # ---- greedy drivers (S10), reported beside the metric ----
-    if not args.no_greedy and rank == 0:
+    if not args.no_greedy and rank == 0 and not big:
         g = {}
         for alg, srt, name in [(cm.ALG_APPROX, cm.SORT_RESIDUAL, "approx_residual"),
                                (cm.ALG_RESIDUAL, cm.SORT_FROBENIUS, "residual_frobenius"),
@@ -394,7 +435,7 @@ def main():
         result["greedy"] = g
 
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(col, pairs, r, args.cpu_sample)
+        result["cpu_baseline"] = cpu_baseline(col, pairs, r, args.cpu_sample, big=big)
     ctx.close()
     if rank == 0:
         print(json.dumps(result))
