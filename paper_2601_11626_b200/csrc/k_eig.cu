@@ -93,8 +93,11 @@ __device__ __forceinline__ double block_sum8(double v, double* red) {
 //   part[wid][i] = sum_{j in this warp's columns, j <= i} B_new[i][j] u[j]      (row partials)
 //   cpart[j]     = sum_{i > j} B_new[i][j] u[i]                                  (mirrored, one warp per column)
 // so that (B_new u)_i = sum_wid part[wid][i] + cpart[i]; dpart[wid] = this warp's share of u^T B_new u.
-// Segments after the first accumulate into cpart / dpart (same warp, fixed order).
-template <int NT, bool UPD>
+// Segments after the first accumulate into cpart / dpart (same warp, fixed order).  NC columns of a
+// warp are processed per iteration: all their loads are issued before any store so that they overlap
+// (the compiler cannot reorder loads across stores itself); NC = 4 keeps more global loads in flight
+// for the in-place (n > 160) reduction.
+template <int NT, bool UPD, int NC = 2>
 __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, const double* __restrict__ u,
                                          const double* __restrict__ vv, const double* __restrict__ ww, int off,
                                          double* __restrict__ part, int n, double* __restrict__ dpart,
@@ -115,53 +118,49 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
   auto put = [&](int j, double c) {
     if (lane == 0) cpart[j] = first ? c : cpart[j] + c;
   };
-  // two columns per iteration (j, j + kTriWarps): all loads of both columns are issued before
-  // any store so that they overlap (the compiler cannot reorder loads across stores itself)
   int j = wid;
-  for (; j + kTriWarps < jend; j += 2 * kTriWarps) {
-    const int j1 = j + kTriWarps;
-    const double uj0 = u[j], uj1 = u[j1];
-    double vj0 = 0.0, wj0 = 0.0, vj1 = 0.0, wj1 = 0.0;
-    if (UPD) { vj0 = vv[off + j]; wj0 = ww[off + j]; vj1 = vv[off + j1]; wj1 = ww[off + j1]; }
-    double* __restrict__ col0 = B + j * ld;
-    double* __restrict__ col1 = B + j1 * ld;
-    double x0[NT], x1[NT];
+  for (; j + (NC - 1) * kTriWarps < jend; j += NC * kTriWarps) {
+    double uj[NC], vj[NC], wj[NC], x[NC][NT], c[NC];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int i = r0 + lane + 32 * t;
-      x0[t] = 0.0; x1[t] = 0.0;
-      if (i < m && i >= j) x0[t] = col0[i];
-      if (i < m && i >= j1) x1[t] = col1[i];
-    }
-    double c0 = 0.0, c1 = 0.0;
+    for (int q = 0; q < NC; ++q) {
+      const int jq = j + q * kTriWarps;
+      uj[q] = u[jq];
+      vj[q] = UPD ? vv[off + jq] : 0.0;
+      wj[q] = UPD ? ww[off + jq] : 0.0;
+      const double* __restrict__ col = B + jq * ld;
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int i = r0 + lane + 32 * t;
-      if (i < m && i >= j) {
-        if (UPD) {
-          x0[t] = fma(-vi[t], wj0, x0[t]); x0[t] = fma(-wi[t], vj0, x0[t]);
-          col0[i] = x0[t];
-        }
-        acc[t] = fma(x0[t], uj0, acc[t]);
-        if (i > j) c0 = fma(x0[t], ui[t], c0);
-      }
-      if (i < m && i >= j1) {
-        if (UPD) {
-          x1[t] = fma(-vi[t], wj1, x1[t]); x1[t] = fma(-wi[t], vj1, x1[t]);
-          col1[i] = x1[t];
-        }
-        acc[t] = fma(x1[t], uj1, acc[t]);
-        if (i > j1) c1 = fma(x1[t], ui[t], c1);
+      for (int t = 0; t < NT; ++t) {
+        const int i = r0 + lane + 32 * t;
+        x[q][t] = (i < m && i >= jq) ? col[i] : 0.0;
       }
     }
-    c0 = warp_sum(c0);
-    c1 = warp_sum(c1);
-    put(j, c0);
-    put(j1, c1);
-    cdot = fma(c0, uj0, cdot);
-    cdot = fma(c1, uj1, cdot);
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int jq = j + q * kTriWarps;
+      double* __restrict__ col = B + jq * ld;
+      c[q] = 0.0;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int i = r0 + lane + 32 * t;
+        if (i < m && i >= jq) {
+          if (UPD) {
+            x[q][t] = fma(-vi[t], wj[q], x[q][t]);
+            x[q][t] = fma(-wi[t], vj[q], x[q][t]);
+            col[i] = x[q][t];
+          }
+          acc[t] = fma(x[q][t], uj[q], acc[t]);
+          if (i > jq) c[q] = fma(x[q][t], ui[t], c[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      c[q] = warp_sum(c[q]);
+      put(j + q * kTriWarps, c[q]);
+      cdot = fma(c[q], uj[q], cdot);
+    }
   }
-  if (j < jend) {
+  for (; j < jend; j += kTriWarps) {
     const double uj = u[j];
     double vj = 0.0, wj = 0.0;
     if (UPD) { vj = vv[off + j]; wj = ww[off + j]; }
@@ -171,24 +170,24 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
     for (int t = 0; t < NT; ++t) {
       const int i = r0 + lane + 32 * t;
       if (i < m && i >= j) {
-        double x = col[i];
+        double xx = col[i];
         if (UPD) {
-          x = fma(-vi[t], wj, x);
-          x = fma(-wi[t], vj, x);
-          col[i] = x;
+          xx = fma(-vi[t], wj, xx);
+          xx = fma(-wi[t], vj, xx);
+          col[i] = xx;
         }
-        acc[t] = fma(x, uj, acc[t]);
-        if (i > j) c0 = fma(x, ui[t], c0);
+        acc[t] = fma(xx, uj, acc[t]);
+        if (i > j) c0 = fma(xx, ui[t], c0);
       }
     }
     c0 = warp_sum(c0);
     put(j, c0);
     cdot = fma(c0, uj, cdot);
   }
-  // columns of this warp beyond the segment have no rows here: first segment still defines cpart
+  // columns of this warp beyond the segment have no rows here: the first segment still defines cpart
   if (first)
-    for (int jj = (j < jend) ? j + kTriWarps : j; jj < m; jj += kTriWarps)
-      if (jj >= jend && lane == 0) cpart[jj] = 0.0;
+    for (int jj = j; jj < m; jj += kTriWarps)
+      if (lane == 0) cpart[jj] = 0.0;
   double dw = 0.0;
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
@@ -213,12 +212,9 @@ __device__ __forceinline__ void tri_pass_dispatch(double* B, int ld, int m, cons
     case 3: tri_pass<3, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
     case 4: tri_pass<4, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
     case 5: tri_pass<5, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
-    case 6: tri_pass<6, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
-    case 7: tri_pass<7, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
-    case 8: tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
-    default:  // row segments of 256 (register budget of two CTAs per SM)
-      for (int r0 = 0; r0 < m; r0 += 256)
-        tri_pass<8, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, r0, r0 == 0);
+    default:  // n > 160 (in place in global memory): row segments of 128, four columns in flight per warp
+      for (int r0 = 0; r0 < m; r0 += 128)
+        tri_pass<4, UPD, 4>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, r0, r0 == 0);
       break;
   }
 }
