@@ -201,6 +201,12 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
   if (lane == 0) dpart[wid] = first ? dw + cdot : dpart[wid] + dw + cdot;
 }
 
+#ifndef CMSVD_GL_NT
+#define CMSVD_GL_NT 4
+#endif
+#ifndef CMSVD_GL_NC
+#define CMSVD_GL_NC 4
+#endif
 template <bool UPD>
 __device__ __forceinline__ void tri_pass_dispatch(double* B, int ld, int m, const double* u, const double* vv,
                                                   const double* ww, int off, double* part, int n, double* dpart,
@@ -212,9 +218,9 @@ __device__ __forceinline__ void tri_pass_dispatch(double* B, int ld, int m, cons
     case 3: tri_pass<3, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
     case 4: tri_pass<4, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
     case 5: tri_pass<5, UPD>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, 0, true); break;
-    default:  // n > 160 (in place in global memory): row segments of 128, four columns in flight per warp
-      for (int r0 = 0; r0 < m; r0 += 128)
-        tri_pass<4, UPD, 4>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, r0, r0 == 0);
+    default:  // n > 160 (in place in global memory): row segments of 32 GL_NT rows, GL_NC columns in flight per warp
+      for (int r0 = 0; r0 < m; r0 += 32 * CMSVD_GL_NT)
+        tri_pass<CMSVD_GL_NT, UPD, CMSVD_GL_NC>(B, ld, m, u, vv, ww, off, part, n, dpart, cpart, r0, r0 == 0);
       break;
   }
 }
