@@ -74,7 +74,7 @@ __global__ void k_commit_res(int64_t m, const float* __restrict__ R, int w, cons
 namespace {
 
 enum { CW_BASIS0 = 0, CW_BASIS1, CW_SPEC, CW_KEYS, CW_PAIRS, CW_OUT, CW_Z, CW_R, CW_G, CW_V, CW_EV, CW_PERM,
-       CW_STAT, CW_DESC, CW_NS };
+       CW_STAT, CW_DESC, CW_NS, CW_SAVE };
 
 size_t au(size_t x) { return (x + 255) / 256 * 256; }
 
@@ -91,6 +91,8 @@ struct Driver {
   int cur = 0;                // which basis buffer is live
   std::vector<double> spec;   // host copy of the state spectrum
   int cap = 0;                // basis capacity (columns)
+  EigKeep keep;               // reflectors of the last evaluation's Grams (Alg. 3 commits reuse them)
+  std::vector<int> last_win;
 
   Driver(Ctx& cc, const cmsvd_cluster_opts& oo) : c(cc), o(oo), N(cc.count), m(cc.m) {}
 
@@ -207,8 +209,18 @@ struct Driver {
     const unsigned kinds = o.algorithm == CMSVD_ALG_RESIDUAL ? CMSVD_RESIDUAL : CMSVD_INCREMENTAL;
     double* d_e = (double*)c.cws[CW_OUT].p;
     double* d_t = (double*)((char*)c.cws[CW_OUT].p + au((size_t)N * 24));
+    // Alg. 3: keep the Grams' tridiagonal reductions, so that the commit of the accepted candidate only
+    // computes its top-r eigenvectors (inverse iteration + back-transformation) instead of rebuilding G
+    keep = EigKeep{};
+    last_win = win;
+    if (o.algorithm == CMSVD_ALG_APPROX && c.commit_topk) {
+      const int64_t gm = std::max(1, st.rr + wmax);
+      keep.save_stride = gm * gm + 2 * gm;
+      CK(ensure(c.cws[CW_SAVE], (size_t)P * keep.save_stride * 8), "cluster: save");
+      keep.save = (double*)c.cws[CW_SAVE].p;
+    }
     Status s = pair_eval_dev(c, d_pr, P, o.r, kinds, (const BaseDesc*)c.d_bdesc.p, d_ad, d, d_e, d_t, nullptr,
-                             nullptr);
+                             nullptr, false, &keep);
     if (s != CMSVD_OK) return s;
     std::vector<double> e3(3 * P);
     tot.resize(P);
@@ -218,6 +230,31 @@ struct Driver {
     err2.resize(P);
     for (int t = 0; t < P; ++t) err2[t] = e3[3 * t + (kinds == CMSVD_RESIDUAL ? 1 : 2)];
     return CMSVD_OK;
+  }
+
+  // Alg. 3 state update from the top eigenpairs of G (lam on the host, ev on the device, vectors in CW_V)
+  Status finish_inc(int j, double e2, const AppDesc& a, int n, const std::vector<double>& lam, const int* perm,
+                    const double* ev) {
+    (void)j;
+    const int rr = st.rr, w = a.w;
+    const double s0 = lam.empty() ? 0.0 : std::sqrt(std::max(lam[0], 0.0));
+    int kp = 0;
+    for (int l = 0; l < std::min(o.r, n); ++l)
+      if (s0 > 0.0 && std::sqrt(std::max(lam[l], 0.0)) > kTau * s0) ++kp;
+    if (kp > 0) {
+      dim3 g((unsigned)((m + 255) / 256), kp);
+      k_commit_inc<<<g, 256, 0, c.stream>>>(m, basis(cur), st.spec, rr, a.F, w, (const double*)c.cws[CW_V].p, perm,
+                                            ev, basis(1 - cur));
+      c.launches += 1;
+      CK(cudaGetLastError(), "cluster: commit inc");
+    }
+    cur = 1 - cur;
+    spec.resize(kp);
+    for (int l = 0; l < kp; ++l) spec[l] = std::sqrt(std::max(lam[l], 0.0));
+    st.q = kp; st.rr = kp; st.ns = kp;
+    st.E += a.E;
+    st.tail_inc = e2;
+    return upload_state();
   }
 
   // commit candidate j (its accepted certificate value e2)
@@ -237,6 +274,26 @@ struct Driver {
     // (k_eig.cu launch_syev_topk) instead of the full QL with vectors
     const int kw = std::min(o.r, n);
     const bool topk = o.algorithm == CMSVD_ALG_APPROX && c.commit_topk && n <= 160 && kw >= 1 && kw <= 64;
+    // the accepted candidate's G was reduced by the last evaluation (same state, same operand)
+    const int t_win = (int)(std::find(last_win.begin(), last_win.end(), j) - last_win.begin());
+    const bool reuse = topk && keep.kept && t_win < (int)last_win.size();
+    if (reuse) {
+      CK(ensure(c.cws[CW_V], (size_t)nn * nn * 8 * 2), "cluster: V");
+      CK(ensure(c.cws[CW_PERM], (size_t)nn * 4 + 64), "cluster: perm");
+      int* perm = (int*)c.cws[CW_PERM].p;
+      std::vector<int> id(kw);
+      for (int l = 0; l < kw; ++l) id[l] = l;
+      CK(cudaMemcpyAsync(perm, id.data(), (size_t)kw * 4, cudaMemcpyHostToDevice, c.stream), "cluster: commit");
+      const double* ev_t = keep.evG + (size_t)t_win * o.r;
+      CK(launch_topk_vectors(c, n, kw, keep.dd + (size_t)t_win * keep.nstride,
+                             keep.save + (size_t)t_win * keep.save_stride, ev_t, keep.gsh + 4 * (size_t)t_win,
+                             (double*)c.cws[CW_V].p),
+         "cluster: commit vectors");
+      std::vector<double> lam(kw);
+      CK(cudaMemcpyAsync(lam.data(), ev_t, (size_t)kw * 8, cudaMemcpyDeviceToHost, c.stream), "cluster: commit d2h");
+      CK(cudaStreamSynchronize(c.stream), "cluster: commit sync");
+      return finish_inc(j, e2, a, n, lam, perm, ev_t);
+    }
     CK(ensure(c.cws[CW_G], (size_t)nn * nn * 8 * 3 + (topk ? syev_topk_scratch_bytes(n, kw) : 0)), "cluster: G");
     CK(ensure(c.cws[CW_V], (size_t)nn * nn * 8 * 2), "cluster: V");
     CK(ensure(c.cws[CW_EV], (size_t)nn * 8 + (size_t)nn * 8), "cluster: ev");
@@ -317,22 +374,7 @@ struct Driver {
     const double l0 = lam.empty() ? 0.0 : std::max(lam[0], 0.0);
     const double s0 = std::sqrt(l0);
     if (o.algorithm == CMSVD_ALG_APPROX) {
-      int keep = 0;
-      for (int l = 0; l < std::min(o.r, n); ++l)
-        if (s0 > 0.0 && std::sqrt(std::max(lam[l], 0.0)) > kTau * s0) ++keep;
-      if (keep > 0) {
-        dim3 g((unsigned)((m + 255) / 256), keep);
-        k_commit_inc<<<g, 256, 0, c.stream>>>(m, basis(cur), st.spec, rr, a.F, w, (const double*)c.cws[CW_V].p, perm,
-                                              ev, basis(1 - cur));
-        c.launches += 1;
-        CK(cudaGetLastError(), "cluster: commit inc");
-      }
-      cur = 1 - cur;
-      spec.resize(keep);
-      for (int l = 0; l < keep; ++l) spec[l] = std::sqrt(std::max(lam[l], 0.0));
-      st.q = keep; st.rr = keep; st.ns = keep;
-      st.E += a.E;
-      st.tail_inc = e2;
+      return finish_inc(j, e2, a, n, lam, perm, ev);
     } else {
       int keep = 0;
       for (int l = 0; l < n; ++l)

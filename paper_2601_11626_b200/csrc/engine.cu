@@ -528,7 +528,8 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
 // ---------------------------------------------------------------------------
 Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kinds, const BaseDesc* d_bd,
                      const AppDesc* d_ad, const Dims& dims, double* d_err2, double* d_total, float* d_st,
-                     float* d_mu, bool tight) {
+                     float* d_mu, bool tight, EigKeep* keep) {
+  if (keep) keep->kept = false;
   if (P <= 0) return CMSVD_OK;
   const int64_t m = c.m;
   // tight (N3): residual with the U_r basis + per-index Weyl; d_err2 is then P x 2
@@ -652,10 +653,20 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
         prof_end(c, pf);
       }
       if (kinds & CMSVD_INCREMENTAL) {
+        const bool save = keep && keep->save && Pc == P && tridiag_can_save(c, GMAX) &&
+                          keep->save_stride >= (int64_t)GMAX * GMAX + 2 * GMAX;
         pf = prof_begin(c, PC_EIG_G);
-        CK(launch_tridiag_topk(c, Gm, GMAX, (int64_t)GMAX * GMAX, nG, (int)Pc, GMAX, nullptr, r, evG, cntG, trG, scr),
+        CK(launch_tridiag_topk(c, Gm, GMAX, (int64_t)GMAX * GMAX, nG, (int)Pc, GMAX, nullptr, r, evG, cntG, trG, scr,
+                               save ? keep->save : nullptr, save ? keep->save_stride : 0),
            "pairs: eig(G)");
         prof_end(c, pf);
+        if (save) {  // launch_tridiag_topk's scratch: dd (Pc x GMAX), e2 (Pc x GMAX), gsh (4 per pair)
+          keep->kept = true;
+          keep->dd = scr;
+          keep->gsh = scr + 2 * (size_t)Pc * GMAX;
+          keep->evG = evG;
+          keep->nstride = GMAX;
+        }
       }
       if ((kinds & CMSVD_RESIDUAL) && (!c.big || tight)) {  // A22 bases: R = (I - QQ^T)F = 0, sigma(W') unused
         pf = prof_begin(c, PC_EIG_W);

@@ -32,9 +32,22 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
 Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t* rank_out);
 Status do_pair_errors(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, uint32_t kinds, int operand, int where,
                       double* err2, double* total, float* sigma_tilde, float* mu);
+// Reflectors of the incremental Grams kept by an evaluation (the greedy driver commits the accepted
+// candidate from them instead of reducing G again).  In: save (P x save_stride doubles) or nullptr.
+// Out: kept, and device pointers to the diagonals (ld nstride), Gershgorin data (4 per pair) and top-r
+// eigenvalues (r per pair) of the evaluated Grams.
+struct EigKeep {
+  double* save = nullptr;
+  int64_t save_stride = 0;
+  bool kept = false;
+  const double* dd = nullptr;
+  const double* gsh = nullptr;
+  const double* evG = nullptr;
+  int nstride = 0;
+};
 Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kinds, const BaseDesc* d_bd,
                      const AppDesc* d_ad, const Dims& dims, double* d_err2, double* d_total, float* d_st, float* d_mu,
-                     bool tight = false);
+                     bool tight = false, EigKeep* keep = nullptr);
 Status do_pair_errors_tight(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, int operand, int where,
                             double* err2x, double* total);
 Dims block_dims(const Ctx& c, int operand);

@@ -619,9 +619,11 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
                                                               double* __restrict__ dout, double* __restrict__ e2out,
                                                               double* __restrict__ gsh, int* __restrict__ cnt_out,
                                                               double* __restrict__ trace_out,
-                                                              double* __restrict__ save = nullptr) {
-  // save (optional, one problem per launch): [v_k as column k of an n x n array][tau_k][signed e_k],
-  // so that Q^T G Q = tridiag(d, e) with Q = H_0 ... H_{n-3}, H_k = I - tau_k v_k v_k^T
+                                                              double* __restrict__ save_base = nullptr,
+                                                              int64_t save_stride = 0) {
+  // save (optional; problem p at save_base + p * save_stride): [v_k as column k of an n x n array][tau_k]
+  // [signed e_k], so that Q^T G Q = tridiag(d, e) with Q = H_0 ... H_{n-3}, H_k = I - tau_k v_k v_k^T
+  double* const save = save_base ? save_base + (int64_t)blockIdx.x * save_stride : nullptr;
   constexpr int NR = 32 * S;
   constexpr int CL = 2 * (S - 1);
   static_assert(C == 2 * S && C <= 16, "column chunks");
@@ -1622,9 +1624,12 @@ size_t tridiag_smem(int nmax, int kw) {
   return nmax > kEigSmemMax ? vec : (size_t)nmax * nmax * 8 + vec;
 }
 
+bool tridiag_can_save(const Ctx& c, int nmax) { return c.eig_rr && nmax <= 160 && (nmax > 128 || !c.eig_duo); }
+
 cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
                                 int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
-                                double* trace, double* scratch) {
+                                double* trace, double* scratch, double* save, int64_t save_stride) {
+  if (save && !tridiag_can_save(c, nmax)) return cudaErrorInvalidValue;
   if (nprob <= 0) return cudaSuccess;
   if (nmax > kTriMax) return cudaErrorInvalidValue;
   const size_t smem = tridiag_smem(nmax, kw);
@@ -1652,7 +1657,7 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   } else if (use_rr) {
 #define RR_LAUNCH(S_, C_)                                                                                          \
   k_tridiag_rr<S_, C_><<<nprob, kRRThreads, 0, c.stream>>>(G, ld_in, stride_in, d_ns, d_thr, kw, nstride, dd, ee, \
-                                                          gsh, cnt, trace)
+                                                          gsh, cnt, trace, save, save_stride)
     if (nmax <= 32) RR_LAUNCH(1, 2);
     else if (nmax <= 64) RR_LAUNCH(2, 4);
     else if (nmax <= 96) RR_LAUNCH(3, 6);
@@ -1892,6 +1897,19 @@ __global__ void __launch_bounds__(kInvWarps * 32) k_tri_backtrans(int n, int kw,
       const int j = wid + kInvWarps * cc, i = lane + 32 * s;
       if (cc < ncol && j < kw && i < n) Z[(size_t)j * n + i] = z[cc][s];
     }
+}
+
+cudaError_t launch_topk_vectors(Ctx& c, int n, int kw, const double* d, const double* save, const double* ev,
+                                const double* gsh, double* Z) {
+  if (n < 1 || n > 160 || kw < 1 || kw > kInvMaxK || kw > n) return cudaErrorInvalidValue;
+  const int sm_inv = (kInvWarps * 6 + 2) * n * 8, sm_bt = 32 * n * 8;
+  cudaError_t e = cudaFuncSetAttribute(k_tri_invit, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_inv);
+  if (e != cudaSuccess) return e;
+  k_tri_invit<<<(kw + kInvWarps - 1) / kInvWarps, kInvWarps * 32, sm_inv, c.stream>>>(n, kw, d, save + (size_t)n * n + n,
+                                                                                     ev, gsh, Z);
+  k_tri_backtrans<<<1, kInvWarps * 32, sm_bt, c.stream>>>(n, kw, save, save + (size_t)n * n, Z);
+  c.launches += 2;
+  return cudaGetLastError();
 }
 
 size_t syev_topk_scratch_bytes(int n, int kw) {

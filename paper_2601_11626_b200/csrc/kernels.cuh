@@ -22,7 +22,13 @@ cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_i
 size_t tridiag_smem(int nmax, int kw);
 cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
                                 int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
-                                double* trace, double* scratch);
+                                double* trace, double* scratch, double* save = nullptr, int64_t save_stride = 0);
+// whether launch_tridiag_topk can save the reflectors (register-resident kernel) at this size
+bool tridiag_can_save(const Ctx& c, int nmax);
+// top-kw eigenvectors (n x kw, ld n) of the matrix whose tridiagonal reduction is saved at `save` (layout of
+// k_tridiag_rr), d = its diagonal, ev = its top-kw eigenvalues, gsh its Gershgorin data
+cudaError_t launch_topk_vectors(Ctx& c, int n, int kw, const double* d, const double* save, const double* ev,
+                                const double* gsh, double* Z);
 size_t tridiag_scratch_bytes(int nprob, int nmax);
 // top-kw eigenpairs of one n x n symmetric matrix (n <= 160, kw <= 64): Z (n x kw, ld n), evals[kw]
 // non-increasing; G is read only.  d_n: device int holding n.
