@@ -1218,18 +1218,54 @@ size_t duo_smem_bytes() {
 // matrix to ~4e-7 ||T||, widened by 1e-5 ||T||, then fp64 to max(1e-13 ||T||, 1e-11 lambda).
 // ev[p*kw + l] = l-th largest eigenvalue for l < cnt[p], else 0.
 // ---------------------------------------------------------------------------
+// STAGE: the block's problems (at most kBisStage) are staged in shared memory, with the normalised fp32
+// copies of the fp32 phase computed once (same fp32 operations as the per-step conversion of the
+// unstaged variant, so the results are identical).
+constexpr int kBisStage = 6;
+template <bool STAGE>
 __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, const int* __restrict__ ns,
                                                 const double* __restrict__ dd, const double* __restrict__ ee2,
                                                 const double* __restrict__ gsh, const int* __restrict__ cnt,
                                                 double* __restrict__ ev) {
+  extern __shared__ double bis_sm[];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+  const int p0 = (int)(g0 / kw);
+  if (STAGE) {  // problems p0 .. p0 + np - 1 of this block
+    const int64_t glast = min((int64_t)P * kw, g0 + blockDim.x) - 1;
+    const int np = glast >= g0 ? (int)(glast / kw) - p0 + 1 : 0;
+    double* d64 = bis_sm;
+    double* e64 = d64 + (size_t)kBisStage * nstride;
+    float* d32 = reinterpret_cast<float*>(e64 + (size_t)kBisStage * nstride);
+    float* e32 = d32 + (size_t)kBisStage * nstride;
+    for (int q = 0; q < np; ++q) {
+      const int pq = p0 + q;
+      const int n = ns[pq];
+      const float inv = (float)(1.0 / gsh[4 * pq + 3]);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double di = dd[(int64_t)pq * nstride + i];
+        d64[q * nstride + i] = di;
+        d32[q * nstride + i] = (float)di * inv;
+        if (i + 1 < n) {
+          const double ei = ee2[(int64_t)pq * nstride + i];
+          e64[q * nstride + i] = ei;
+          e32[q * nstride + i] = (float)ei * inv * inv;
+        }
+      }
+    }
+    __syncthreads();
+  }
   if (g >= (int64_t)P * kw) return;
   const int p = (int)(g / kw), l = (int)(g % kw);
   double* out = ev + (int64_t)p * kw + l;
   if (l >= cnt[p]) { *out = 0.0; return; }
   const int n = ns[p];
-  const double* d = dd + (int64_t)p * nstride;
-  const double* e2 = ee2 + (int64_t)p * nstride;
+  const double* d = STAGE ? bis_sm + (size_t)(p - p0) * nstride : dd + (int64_t)p * nstride;
+  const double* e2 = STAGE ? bis_sm + (size_t)(kBisStage + p - p0) * nstride : ee2 + (int64_t)p * nstride;
+  const float* d32 = STAGE ? reinterpret_cast<const float*>(bis_sm + (size_t)2 * kBisStage * nstride) +
+                                 (size_t)(p - p0) * nstride
+                           : nullptr;
+  const float* e32 = STAGE ? d32 + (size_t)kBisStage * nstride : nullptr;
   const double glo = gsh[4 * p], ghi = gsh[4 * p + 1], pivmin = gsh[4 * p + 2], nrm = gsh[4 * p + 3];
   const int target = n - 1 - l;
   double lo = glo, hi = ghi;
@@ -1239,12 +1275,12 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
     float a = (float)(lo / nrm), b = (float)(hi / nrm);
     for (int it = 0; it < 40 && (b - a) > 4e-7f; ++it) {
       const float x = 0.5f * (a + b);
-      float q = (float)(__ldg(d) * inv) - x;
+      float q = (float)(d[0] * inv) - x;
       if (fabsf(q) < 1e-30f) q = -1e-30f;
       int c = q < 0.f;
       for (int i = 1; i < n; ++i) {
-        const float di = (float)__ldg(d + i) * inv;
-        const float ei = (float)(__ldg(e2 + i - 1)) * inv * inv;
+        const float di = STAGE ? d32[i] : (float)__ldg(d + i) * inv;
+        const float ei = STAGE ? e32[i - 1] : (float)(__ldg(e2 + i - 1)) * inv * inv;
         q = (di - x) - __fdividef(ei, q);
         if (fabsf(q) < 1e-30f) q = -1e-30f;
         c += q < 0.f;
@@ -1260,11 +1296,11 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
   const double tol = 1e-13 * nrm;
   for (int it = 0; it < 80 && (hi - lo) > fmax(tol, 1e-11 * fmax(fabs(lo), fabs(hi))) + 4.4e-16 * fmax(fabs(lo), fabs(hi)); ++it) {
     const double x = 0.5 * (lo + hi);
-    double q = __ldg(d) - x;
+    double q = d[0] - x;
     if (fabs(q) < pivmin) q = -pivmin;
     int c = q < 0.0;
     for (int i = 1; i < n; ++i) {
-      q = (__ldg(d + i) - x) - __ldg(e2 + i - 1) * rcp_nr(q);
+      q = (d[i] - x) - e2[i - 1] * rcp_nr(q);
       if (fabs(q) < pivmin) q = -pivmin;
       c += q < 0.0;
     }
@@ -1692,7 +1728,19 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   if (total <= kMultisectMax)
     k_multisect<<<(unsigned)((total + 3) / 4), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
   else
-    k_bisect<<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
+  {
+    // stage the block's tridiagonals when a block spans at most kBisStage problems
+    const size_t sm = (size_t)kBisStage * nstride * (2 * sizeof(double) + 2 * sizeof(float));
+    if (128 / kw + 2 <= kBisStage && sm <= 96 * 1024) {
+      e = cudaFuncSetAttribute(k_bisect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      k_bisect<true><<<(unsigned)((total + 127) / 128), 128, sm, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh,
+                                                                             cnt, ev);
+    } else {
+      k_bisect<false><<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh,
+                                                                              cnt, ev);
+    }
+  }
   c.launches += 1;
   return cudaGetLastError();
 }
