@@ -23,13 +23,21 @@ namespace cmsvd {
 
 // fp64 reciprocal: MUFU.RCP64H approximation + 2 Newton steps (full precision
 // for |q| >= pivmin, far cheaper than the IEEE division subroutine).
+// (the approximation is good to ~1e-6; one cubic step y (1 + e + e^2), e = 1 - q y, reaches 1 ulp with
+// three dependent operations instead of the four of two Newton steps -- measured: tools/rcp_prec.cu)
 __device__ __forceinline__ double rcp_nr(double q) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
-  double e = fma(-q, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-q, y, 1.0);
-  return fma(y, e, y);
+  const double e = fma(-q, y, 1.0);
+  return fma(y * e, 1.0 + e, y);
+}
+// 1/sqrt(x): MUFU approximation (~1e-6) + one cubic step y (1 + e/2 + 3e^2/8), e = 1 - x y^2: full double
+// precision in four dependent operations instead of six (tools/rsqrt_prec.cu)
+__device__ __forceinline__ double rsqrt_cubic(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-(x * y), y, 1.0);
+  return fma(y * e, fma(e, 0.375, 0.5), y);
 }
 __device__ __forceinline__ double div_fast(double a, double b) { return a * rcp_nr(b); }
 __device__ __forceinline__ float div_fast(float a, float b) { return __fdividef(a, b); }
@@ -243,16 +251,7 @@ __device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld
   // norms of the next column -> | [all threads, redundantly] next reflector
   // scalars from the 8 partial norms; per row v2 -> next pass.  No block-wide
   // serial reduction chain.
-  auto rsqrt_nr = [](double x) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double h = 0.5 * x * y;
-    double r = fma(-h, y, 0.5);
-    y = fma(y, r, y);
-    h = 0.5 * x * y;
-    r = fma(-h, y, 0.5);
-    return fma(y, r, y);
-  };
+  auto rsqrt_nr = [](double x) { return rsqrt_cubic(x); };
   // next reflector from column kk (rows kk+1..), given the partial norms of rows kk+2.. in s_nrm
   auto reflector = [&](int kk, double* vec) -> double {
     const int s = n - 1 - kk;
@@ -655,16 +654,7 @@ __global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __re
     t = warp_sum(t);
     if (lane == 0) trace_out[p] = t;
   }
-  auto rsqrt_nr = [](double x) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double h = 0.5 * x * y;
-    double r = fma(-h, y, 0.5);
-    y = fma(y, r, y);
-    h = 0.5 * x * y;
-    r = fma(-h, y, 0.5);
-    return fma(y, r, y);
-  };
+  auto rsqrt_nr = [](double x) { return rsqrt_cubic(x); };
   // reflector from the (updated) column kk held as x[s] = A(lane + 32 s, kk) by its owner warp:
   // e2[kk], d[kk], tau -> s_tau[kk & 1], v -> vb[kk & 1]
   auto reflector = [&](int kk, const double* x) {
@@ -867,16 +857,7 @@ __device__ __forceinline__ void rr_mbar_wait(unsigned long long* b, unsigned par
       : "memory");
 }
 
-__device__ __forceinline__ double rr_rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double h = 0.5 * x * y;
-  double r = fma(-h, y, 0.5);
-  y = fma(y, r, y);
-  h = 0.5 * x * y;
-  r = fma(-h, y, 0.5);
-  return fma(y, r, y);
-}
+__device__ __forceinline__ double rr_rsqrt_nr(double x) { return rsqrt_cubic(x); }
 
 // reflector kk from the column held as x[s] = A(lane + 32 s, kk) by one warp (prologue, kk = 0)
 template <int S>
@@ -1471,14 +1452,7 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
               // IEEE hypot and two divisions on this sequential chain; scaled fallback near under/overflow
               const double x2 = fma(f, f, g * g);
               if (x2 > 1e-280 && x2 < 1e280) {
-                double y;
-                asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x2));
-                double hh = 0.5 * x2 * y;
-                double rr = fma(-hh, y, 0.5);
-                y = fma(y, rr, y);
-                hh = 0.5 * x2 * y;
-                rr = fma(-hh, y, 0.5);
-                y = fma(y, rr, y);
+                const double y = rsqrt_cubic(x2);
                 r = x2 * y;
                 ee[i + 1] = r;
                 sn = f * y;
