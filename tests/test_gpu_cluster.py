@@ -277,3 +277,21 @@ def test_cluster_factors_reconstruction(cm, name):
         ex = oracle.exact_groups(sp, [list(mb) for mb, _, _ in fac], col.r)
         from tolerances import assert_err2
         assert_err2(v["exact_err2"], ex, v["total"], "config1 cluster exact")
+
+
+@pytest.mark.parametrize("knn", [1, 4])
+def test_c2_commit_reuse_matches_full_commit(cm, knn, monkeypatch):
+    """Alg. 3 commits from the evaluation's saved reflectors (default) vs the full QL commit
+    (CMSVD_COMMIT_TOPK=0) on config 2 (n = r + w = 160, register-resident kernel; knn = 4 exercises the
+    per-pair save stride of the evaluation window): the same clusters, certificates within 1e-6."""
+    col = synth.config2()
+    res = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("CMSVD_COMMIT_TOPK", flag)
+        with cm.Context(0, torch.cuda.current_stream().cuda_stream) as ctx:
+            ctx.register(torch.from_numpy(col.blocks).cuda())
+            ctx.block_spectra(col.r)
+            res.append(ctx.cluster(cm.ALG_APPROX, 0.05, sort=cm.SORT_RESIDUAL, knn=knn))
+    a, b = res
+    assert np.array_equal(np.asarray(a["assign"]), np.asarray(b["assign"]))
+    assert np.allclose(a["err2"], b["err2"], rtol=1e-6, atol=1e-9 * float(np.max(b["total"])))
