@@ -113,6 +113,35 @@ __device__ __forceinline__ void load_kcontig(float4 (&v)[kItK], int rows, const 
   }
 }
 
+// Two-source variant: rows r < nA come from srcA (row r), rows r >= nA from srcB (row r - nA) -- the operand
+// of two grouped pairs with the same base (their appended blocks side by side).
+template <bool NC>
+__device__ __forceinline__ void load_kcontig2(float4 (&v)[kItK], int rows, const float* __restrict__ srcA, int nA,
+                                              const float* __restrict__ srcB, int64_t ld, int nrows, int64_t k0,
+                                              int64_t kmax) {
+  const int tid = threadIdx.x;
+  const int c = tid & 7;
+  const bool vec = ((ld & 3) == 0) && ((k0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(srcA) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(srcB) & 15) == 0);
+  const int64_t k = k0 + 4 * c;
+#pragma unroll
+  for (int i = 0; i < kItK; ++i) {
+    const int r = (tid >> 3) + i * (kTcThreads / 8);
+    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < rows && r < nrows) {
+      const float* p = (r < nA ? srcA + (int64_t)r * ld : srcB + (int64_t)(r - nA) * ld) + k;
+      if (vec && k + 3 < kmax) {
+        v[i] = ldf4<NC>(p);
+      } else {
+        if (k + 0 < kmax) v[i].x = ldf<NC>(p + 0);
+        if (k + 1 < kmax) v[i].y = ldf<NC>(p + 1);
+        if (k + 2 < kmax) v[i].z = ldf<NC>(p + 2);
+        if (k + 3 < kmax) v[i].w = ldf<NC>(p + 3);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void store_kcontig(const float4 (&v)[kItK], uint8_t* hi, uint8_t* lo, int rows,
                                               uint8_t* mi) {
   const int tid = threadIdx.x;
@@ -192,11 +221,13 @@ __device__ __forceinline__ void issue_3x(uint32_t d_tmem, uint32_t ah, uint32_t 
 
 }  // namespace
 
+template <bool GROUP>
 __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restrict__ pairs,
                                                            const BaseDesc* __restrict__ bd,
                                                            const AppDesc* __restrict__ ad, int64_t m,
                                                            int use_full_basis, int QMAX, int WMAX,
-                                                           float* __restrict__ Zws, double* __restrict__ Wws) {
+                                                           float* __restrict__ Zws, double* __restrict__ Wws,
+                                                           int64_t P) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned, derived by pointer arithmetic so that the compiler keeps the shared address space
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -210,16 +241,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   constexpr int kColW = 128 / kGroups;            // columns per warp in the drains / epilogue
   const int half = wid >> 2;  // column group [kColW*half, kColW*half+kColW) handled by this warp in the drains
   const int64_t p = blockIdx.x;
+  // Pairs 2g and 2g+1 with the same base and appended widths <= 64 are one CTA's work (their operands side
+  // by side: one 128-wide MMA instead of two half-empty ones); the odd CTA of such a group exits.
+  auto grouped_at = [&](int64_t x) {
+    if (!GROUP || x < 0 || (x & 1) || x + 1 >= P) return false;
+    const int2 p0 = pairs[x], p1 = pairs[x + 1];
+    return p0.x == p1.x && ad[p0.y].w <= 64 && ad[p1.y].w <= 64;
+  };
+  if (grouped_at(p - 1)) return;
+  const bool grouped = grouped_at(p);
   const int2 pr = pairs[p];
   const BaseDesc b = bd[pr.x];
   const AppDesc a = ad[pr.y];
+  const AppDesc a2 = grouped ? ad[pairs[p + 1].y] : a;
   const int q = use_full_basis ? b.q : b.rr;
-  const int w = a.w;
+  const int w1 = a.w;                     // columns of the first pair (all columns when not grouped)
+  const int w = grouped ? w1 + a2.w : w1;
   const int wp = ((w + 31) / 32) * 32;   // MMA N (multiple of 32 for the 32-column TMEM drains)
   float* Zg = Zws + p * (int64_t)QMAX * WMAX;
   double* Wg = Wws + p * (int64_t)WMAX * WMAX;
+  float* Zg2 = grouped ? Zg + (int64_t)QMAX * WMAX : Zg;
+  double* Wg2 = grouped ? Wg + (int64_t)WMAX * WMAX : Wg;
   const float* Q = b.basis;
   const float* F = a.F;
+  const float* F2 = grouped ? a2.F : a.F;
 
   if (wid == 0) tc::tmem_alloc(&tmem_base, 512);
   if (tid == 0) {
@@ -297,7 +342,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
     const int nst = (int)((m + KT - 1) / KT);
     float4 qa[kItK], fb[kItK];
     load_kcontig<true>(qa, 128, Q, m, q, 0, m);
-    load_kcontig<true>(fb, wp, F, m, w, 0, m);
+    if constexpr (GROUP) load_kcontig2<true>(fb, wp, F, w1, F2, m, w, 0, m);
+    else load_kcontig<true>(fb, wp, F, m, w, 0, m);
     for (; it < nst; ++it) {
       const int s = it & 1;
       const int blk = it / kBlk, slot = blk & 1;
@@ -307,7 +353,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
       if (it + 1 < nst) {  // next stage's loads fly during this stage's barrier and MMAs
         const int64_t k1 = (int64_t)(it + 1) * KT;
         load_kcontig<true>(qa, 128, Q, m, q, k1, m);
-        load_kcontig<true>(fb, wp, F, m, w, k1, m);
+        if constexpr (GROUP) load_kcontig2<true>(fb, wp, F, w1, F2, m, w, k1, m);
+        else load_kcontig<true>(fb, wp, F, m, w, k1, m);
       }
       tc::fence_proxy_async();
       tc::fence_before();
@@ -340,7 +387,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
     for (int s = 0; s < 2; ++s) acquire(s);
     const int ar = 32 * wq + lane;
     drain_sum([&](int j, float x) {
-      if (ar < q && j < w) Zg[(int64_t)j * QMAX + ar] = x;
+      if (ar < q && j < w) {
+        if (!GROUP || j < w1) Zg[(int64_t)j * QMAX + ar] = x;
+        else Zg2[(int64_t)(j - w1) * QMAX + ar] = x;
+      }
     });
   }
   __threadfence_block();
@@ -357,7 +407,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   float4 qv[kItR], zv[kItK];
   if (w > 0 && m > 0) {
     load_rcontig(qv, Q, m, 0, m, 0, q);
-    load_kcontig<false>(zv, wp, Zg, QMAX, w, 0, q);
+    if constexpr (GROUP) load_kcontig2<false>(zv, wp, Zg, w1, Zg2, QMAX, w, 0, q);
+    else load_kcontig<false>(zv, wp, Zg, QMAX, w, 0, q);
   }
   for (int64_t m0 = 0; m0 < m && w > 0; m0 += 128) {
     // R accumulator over a-chunks of 32
@@ -373,7 +424,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
         if (na0 >= q) { na0 = 0; nm0 = m0 + 128; }
         if (nm0 < m) {
           load_rcontig(qv, Q, m, nm0, m, na0, q);
-          load_kcontig<false>(zv, wp, Zg, QMAX, w, na0, q);
+          if constexpr (GROUP) load_kcontig2<false>(zv, wp, Zg, w1, Zg2, QMAX, w, na0, q);
+          else load_kcontig<false>(zv, wp, Zg, QMAX, w, na0, q);
         }
       }
       tc::fence_proxy_async();
@@ -403,7 +455,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int bcol = c0_e + j;
-      fpre[j] = (c0_e < wp && bcol < w && grow_e < m) ? __ldg(F + (int64_t)bcol * m + grow_e) : 0.f;
+      if constexpr (GROUP)
+        fpre[j] = (c0_e < wp && bcol < w && grow_e < m)
+                      ? __ldg((bcol < w1 ? F + (int64_t)bcol * m : F2 + (int64_t)(bcol - w1) * m) + grow_e)
+                      : 0.f;
+      else
+        fpre[j] = (c0_e < wp && bcol < w && grow_e < m) ? __ldg(F + (int64_t)bcol * m + grow_e) : 0.f;
     }
     tc::mbar_wait(&bar_done, ph_done);
     ph_done ^= 1;
@@ -462,7 +519,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pair_tc(const int2* __restric
   if (w > 0) {
     const int br = 32 * wq + lane;
     drain_sum([&](int j, float x) {
-      if (br < w && j < w) Wg[(int64_t)j * WMAX + br] = (double)x;
+      if constexpr (GROUP) {
+        if (br < w1 && j < w1) Wg[(int64_t)j * WMAX + br] = (double)x;          // first pair's block
+        else if (br >= w1 && j >= w1 && br < w && j < w)                         // second pair's block
+          Wg2[(int64_t)(j - w1) * WMAX + (br - w1)] = (double)x;
+      } else {
+        if (br < w && j < w) Wg[(int64_t)j * WMAX + br] = (double)x;
+      }
     });
   }
   tc::fence_before();
@@ -703,10 +766,19 @@ cudaError_t launch_gemm_tc(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM,
 cudaError_t launch_pair_tc(Ctx& c, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int64_t m,
                            int use_full_basis, int QMAX, int WMAX, float* Zws, double* Wws) {
   if (P <= 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_pair_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTc);
+  cudaError_t e = cudaFuncSetAttribute(k_pair_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTc);
   if (e != cudaSuccess) return e;
-  k_pair_tc<<<(unsigned)P, kTcThreads, kSmemTc, c.stream>>>(pairs, bd, ad, m, use_full_basis, QMAX, WMAX, Zws,
-                                                             Wws);
+  // grouping of same-base pairs (operands <= 64 columns) only where it can happen: the general kernel keeps
+  // its register budget
+  if (WMAX <= 64) {
+    e = cudaFuncSetAttribute(k_pair_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTc);
+    if (e != cudaSuccess) return e;
+    k_pair_tc<true><<<(unsigned)P, kTcThreads, kSmemTc, c.stream>>>(pairs, bd, ad, m, use_full_basis, QMAX, WMAX,
+                                                                     Zws, Wws, P);
+  } else {
+    k_pair_tc<false><<<(unsigned)P, kTcThreads, kSmemTc, c.stream>>>(pairs, bd, ad, m, use_full_basis, QMAX, WMAX,
+                                                                      Zws, Wws, P);
+  }
   c.launches += 1;
   return cudaGetLastError();
 }
