@@ -212,6 +212,9 @@ __device__ __forceinline__ void tri_pass(double* __restrict__ B, int ld, int m, 
 #ifndef CMSVD_GL_NT
 #define CMSVD_GL_NT 4
 #endif
+#ifndef CMSVD_GL_CTAS
+#define CMSVD_GL_CTAS 2
+#endif
 #ifndef CMSVD_GL_NC
 #define CMSVD_GL_NC 4
 #endif
@@ -342,7 +345,7 @@ __device__ __forceinline__ void tri_reduce(double* __restrict__ A, int n, int ld
 // GL = true: the matrix is reduced in place in global memory (L2-resident; n up to 512), only the
 // vectors and partial sums live in shared memory.
 template <bool GL>
-__global__ void __launch_bounds__(kTriThreads, GL ? 2 : 1) k_tridiag(const double* __restrict__ Gin, int64_t ld_in,
+__global__ void __launch_bounds__(kTriThreads, GL ? CMSVD_GL_CTAS : 1) k_tridiag(const double* __restrict__ Gin, int64_t ld_in,
                                                             int64_t stride_in, const int* __restrict__ ns,
                                                             const double* __restrict__ thr, int kw, int nstride,
                                                             double* __restrict__ dout, double* __restrict__ e2out,
