@@ -1052,7 +1052,7 @@ constexpr int kDuoThreads = kRRThreads + 32 * 4 * kDuoGroups;  // 16 element war
 #endif
 
 template <int S, int C>
-__global__ void __launch_bounds__(kDuoThreads, 1) k_tridiag_duo(const double* __restrict__ Gin, int64_t ld_in,
+__global__ void __launch_bounds__(kDuoThreads, (S <= 2 ? 2 : 1)) k_tridiag_duo(const double* __restrict__ Gin, int64_t ld_in,
                                                                 int64_t stride_in, const int* __restrict__ ns,
                                                                 int nprob, const double* __restrict__ thr, int kw,
                                                                 int nstride, double* __restrict__ dout,
