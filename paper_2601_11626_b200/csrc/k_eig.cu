@@ -615,7 +615,7 @@ __device__ __forceinline__ void rr_column(int ck, ACC a, double* x) {
 }
 
 template <int S, int C>
-__global__ void __launch_bounds__(kRRThreads, 1) k_tridiag_rr(const double* __restrict__ Gin, int64_t ld_in,
+__global__ void __launch_bounds__(kRRThreads, (S <= 3 ? 2 : 1)) k_tridiag_rr(const double* __restrict__ Gin, int64_t ld_in,
                                                               int64_t stride_in, const int* __restrict__ ns,
                                                               const double* __restrict__ thr, int kw, int nstride,
                                                               double* __restrict__ dout, double* __restrict__ e2out,
@@ -1637,7 +1637,10 @@ size_t tridiag_smem(int nmax, int kw) {
   return nmax > kEigSmemMax ? vec : (size_t)nmax * nmax * 8 + vec;
 }
 
-bool tridiag_can_save(const Ctx& c, int nmax) { return c.eig_rr && nmax <= 160 && (nmax > 128 || !c.eig_duo); }
+// the two-problem kernel for n <= 128, except 64 < n <= 96 where two one-problem CTAs per SM of the
+// register-resident kernel are 4% faster (measured, tools/eigbench.cu)
+static bool uses_duo(const Ctx& c, int nmax) { return c.eig_rr && c.eig_duo && nmax <= 128 && !(nmax > 64 && nmax <= 96); }
+bool tridiag_can_save(const Ctx& c, int nmax) { return c.eig_rr && nmax <= 160 && !uses_duo(c, nmax); }
 
 cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
                                 int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
@@ -1652,7 +1655,7 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   double* gsh = ee + (size_t)nprob * nstride;
   cudaError_t e;
   const bool use_rr = c.eig_rr && nmax <= 160;
-  if (use_rr && c.eig_duo && nmax <= 128) {
+  if (uses_duo(c, nmax)) {
 #define DUO_LAUNCH(S_, C_)                                                                                          \
   do {                                                                                                              \
     const size_t sm2 = duo_smem_bytes<S_, C_>();                                                                    \
