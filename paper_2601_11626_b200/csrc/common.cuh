@@ -128,6 +128,7 @@ struct Ctx {
   bool big_tc = true;                  // A22 subspace-iteration products on tcgen05 tiles (CMSVD_BIG_TC=0: SIMT fp64)
   bool tc_wide = true;                 // ... with 256-column tiles for Z = Q^T F (CMSVD_TC_WIDE=0: 128)
   bool eig_duo = true;                 // n <= 128: two problems per CTA with dedicated row warps (CMSVD_EIG_DUO=0: off)
+  bool eig_duo160 = true;              // ... and for 128 < n <= 160 (CMSVD_EIG_DUO160=0: off)
   bool commit_topk = true;             // Alg. 3 commits: top-r eigenpairs by inverse iteration (CMSVD_COMMIT_TOPK=0: QL)
   bool big = false;                    // collection of blocks wider than kEigMax (A22 spectra, full-range bases)
   int subspace_iters = 12;             // power iterations of the big-block spectra (CMSVD_SUBSPACE_ITERS)

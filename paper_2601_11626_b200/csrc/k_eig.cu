@@ -491,6 +491,22 @@ struct SmemAcc {
   __device__ __forceinline__ void st(int s, int c, double x) const { A[rr_qidx<S, C>(s, c) * kRRThreads] = x; }
 };
 
+// Split storage (two-problem kernel at n = 160): the last NQR present chunks (the longest-lived, row-major
+// ordinals >= NQ - NQR) in registers, the others in shared memory like SmemAcc.
+template <int S, int C, int NQR>
+struct HybAcc {
+  static constexpr int NQS = rr_nchunks<S, C>() - NQR;
+  double (&a)[S][C];
+  double* A;   // this thread's column of the shared-memory part: A + tid
+  __device__ __forceinline__ double ld(int s, int c) const {
+    return rr_qidx<S, C>(s, c) >= NQS ? a[s][c] : A[rr_qidx<S, C>(s, c) * kRRThreads];
+  }
+  __device__ __forceinline__ void st(int s, int c, double x) const {
+    if (rr_qidx<S, C>(s, c) >= NQS) a[s][c] = x;
+    else A[rr_qidx<S, C>(s, c) * kRRThreads] = x;
+  }
+};
+
 template <int S, int C, int KC, bool UPD, bool MV, class ACC>
 __device__ __forceinline__ void rr_pass(ACC a, const int lane, const int wid,
                                         const double* __restrict__ v, const double* __restrict__ w,
@@ -895,35 +911,53 @@ __device__ __forceinline__ void rr_reflector_warp(RRProb<S>& P, int kk, const do
   }
 }
 
-// row phase of step k on the row threads t = 0..32S-1 (warps wr = 0..S-1 of the group); bar_id = the
-// group's named barrier for the norm
-template <int S>
-__device__ __forceinline__ void rr_row_phase(RRProb<S>& P, int k, int n, int t, int wr, int lane, int bar_id) {
+// row phase of step k on the row threads t0 = 0..32RW-1 (warps wr = 0..RW-1 of the group; thread t0 owns
+// rows t0 + 32 RW j); bar_id = the group's named barrier for the norm.  RW = S: one row per thread.
+template <int S, int RW = S>
+__device__ __forceinline__ void rr_row_phase(RRProb<S>& P, int k, int n, int t0, int wr, int lane, int bar_id) {
   constexpr int NR = 32 * S;
+  constexpr int RT = 32 * RW;
+  constexpr int NRT = (NR + RT - 1) / RT;
   const double* v = P.vb[k & 1];
   const double tau = P.s_tau[k & 1];
   const int k1 = k + 1;
   const bool more = k1 + 2 < n;
   const double Kc = 0.5 * tau * tau * tree16(P.red, 1);
-  const double pt = P.cs[t] + tree16(&P.part[t], NR);
-  const double wt = (t > k && t < n && tau != 0.0) ? fma(tau, pt, -Kc * v[t]) : 0.0;
-  P.wb[t] = wt;
-  if (more) {
-    double y = P.colbuf[t];
-    if (tau != 0.0) {
-      const double pk1 = P.cs[k1] + tree16(&P.part[k1], NR);
-      const double wk1 = fma(tau, pk1, -Kc * v[k1]);
-      y = fma(-v[t], wk1, fma(-wt, v[k1], y));
+  double wk1 = 0.0;
+  if (more && tau != 0.0) {
+    const double pk1 = P.cs[k1] + tree16(&P.part[k1], NR);
+    wk1 = fma(tau, pk1, -Kc * v[k1]);
+  }
+  double y[NRT];
+  double sq = 0.0;
+#pragma unroll
+  for (int j = 0; j < NRT; ++j) {
+    const int t = t0 + RT * j;
+    y[j] = 0.0;
+    if (NR % RT == 0 || t < NR) {
+      const double pt = P.cs[t] + tree16(&P.part[t], NR);
+      const double wt = (t > k && t < n && tau != 0.0) ? fma(tau, pt, -Kc * v[t]) : 0.0;
+      P.wb[t] = wt;
+      if (more) {
+        double yy = P.colbuf[t];
+        if (tau != 0.0) yy = fma(-v[t], wk1, fma(-wt, v[k1], yy));
+        y[j] = yy;
+        if (t > k1 + 1 && t < n) {
+          if (j == 0) sq = yy * yy;
+          else sq = fma(yy, yy, sq);
+        }
+        if (t == k1 + 1) P.s_alpha = yy;
+        if (t == k1) P.s_dk = yy;
+      }
     }
-    double sq = (t > k1 + 1 && t < n) ? y * y : 0.0;
+  }
+  if (more) {
     sq = warp_sum(sq);
     if (lane == 0) P.red2[wr] = sq;
-    if (t == k1 + 1) P.s_alpha = y;
-    if (t == k1) P.s_dk = y;
-    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(NR) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(RT) : "memory");
     double sg = 0.0;
 #pragma unroll
-    for (int q = 0; q < S; ++q) sg += P.red2[q];
+    for (int q = 0; q < RW; ++q) sg += P.red2[q];
     const double al = P.s_alpha;
     double tau1, scale, ee;
     if (sg == 0.0) {
@@ -936,8 +970,13 @@ __device__ __forceinline__ void rr_row_phase(RRProb<S>& P, int k, int n, int t, 
       scale = rcp_nr(al - beta);
       ee = beta * beta;
     }
-    if (t == 0) { P.e2s[k1] = ee; P.ds[k1] = P.s_dk; P.s_tau[k1 & 1] = tau1; }
-    P.vb[k1 & 1][t] = (t == k1 + 1) ? 1.0 : ((t > k1 + 1 && t < n) ? y * scale : 0.0);
+    if (t0 == 0) { P.e2s[k1] = ee; P.ds[k1] = P.s_dk; P.s_tau[k1 & 1] = tau1; }
+#pragma unroll
+    for (int j = 0; j < NRT; ++j) {
+      const int t = t0 + RT * j;
+      if (NR % RT == 0 || t < NR)
+        P.vb[k1 & 1][t] = (t == k1 + 1) ? 1.0 : ((t > k1 + 1 && t < n) ? y[j] * scale : 0.0);
+    }
   }
 }
 
@@ -1032,11 +1071,12 @@ __device__ __forceinline__ void rr_outputs(RRProb<S>& P, int n, int p, int h, in
 
 
 // ---------------------------------------------------------------------------
-// Two problems per CTA with dedicated row warps (k_tridiag_duo, n <= 128).
-// Both problems' lower-triangle chunks live in shared memory (SmemAcc, 2 x 80 KB
-// at n = 128) with the ownership of k_tridiag_rr; 16 element warps run the
-// fused passes of both problems, S dedicated row warps (thread t = row t) run
-// the row phases.  A row phase only waits for its own problem's partial
+// Two problems per CTA with dedicated row warps (k_tridiag_duo, n <= 160).
+// Problem 0's lower-triangle chunks live in registers (n <= 128; at n = 160 only
+// the last NQR chunks, the rest in shared memory: HybAcc), problem 1's in shared
+// memory (SmemAcc), with the ownership of k_tridiag_rr; 16 element warps run the
+// fused passes of both problems, RW dedicated row warps (thread t owns rows
+// t + 32 RW j; RW = S for n <= 128: row t) run the row phases.  A row phase only waits for its own problem's partial
 // products (mbarrier B2) and the element warps only for its results (mbarrier
 // B3), so the latency-bound row phase of one problem overlaps the fused pass
 // of the other:  element warps  F0(k) F1(k) F0(k+1) ...;  row warps  R0(k+1)
@@ -1047,12 +1087,16 @@ __device__ __forceinline__ void rr_outputs(RRProb<S>& P, int n, int p, int h, in
 #endif
 constexpr int kDuoGroups = CMSVD_DUO_GROUPS;
 constexpr int kDuoThreads = kRRThreads + 32 * 4 * kDuoGroups;  // 16 element warps + 4 row warps per group
-#ifndef CMSVD_DUO_REG0
-#define CMSVD_DUO_REG0 1   // problem 0 of the pair in registers (problem 1 in shared memory)
+#ifndef CMSVD_DUO160_RW
+#define CMSVD_DUO160_RW 3     // n = 160: row warps (measured: 2-4 within 2%)
 #endif
+#ifndef CMSVD_DUO160_NQR
+#define CMSVD_DUO160_NQR 18   // n = 160: problem-0 chunks in registers (of 30; >= 18 for shared memory)
+#endif
+__host__ __device__ constexpr int duo_threads(int S, int RW) { return S <= 4 ? kDuoThreads : kRRThreads + 32 * RW; }
 
-template <int S, int C>
-__global__ void __launch_bounds__(kDuoThreads, (S <= 2 ? 2 : 1)) k_tridiag_duo(const double* __restrict__ Gin, int64_t ld_in,
+template <int S, int C, int RW = S, int NQR = rr_nchunks<S, C>()>
+__global__ void __launch_bounds__(duo_threads(S, RW), (S <= 2 ? 2 : 1)) k_tridiag_duo(const double* __restrict__ Gin, int64_t ld_in,
                                                                 int64_t stride_in, const int* __restrict__ ns,
                                                                 int nprob, const double* __restrict__ thr, int kw,
                                                                 int nstride, double* __restrict__ dout,
@@ -1062,25 +1106,22 @@ __global__ void __launch_bounds__(kDuoThreads, (S <= 2 ? 2 : 1)) k_tridiag_duo(c
   constexpr int NR = 32 * S;
   constexpr int CL = 2 * (S - 1);
   constexpr int NQ = rr_nchunks<S, C>();
-  static_assert(C == 2 * S && S <= 4, "duo kernel: n <= 128");
+  constexpr int NT = duo_threads(S, RW);
+  constexpr int NQS = NQ - NQR;  // problem-0 chunks in shared memory
+  static_assert(C == 2 * S && S <= 5 && RW <= S && 32 * RW <= NT - kRRThreads, "duo kernel: n <= 160");
   extern __shared__ __align__(16) unsigned char duo_smem[];
   RRProb<S>* PP = reinterpret_cast<RRProb<S>*>(duo_smem);
   double* A0 = reinterpret_cast<double*>(duo_smem + 2 * sizeof(RRProb<S>));
-  double* A1 = A0 + (size_t)NQ * kRRThreads;
+  double* A1 = A0 + (size_t)NQS * kRRThreads;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool elem = tid < kRRThreads;
   const int pa = 2 * blockIdx.x, pb = pa + 1;
   const int n0 = ns[pa], n1 = (pb < nprob) ? ns[pb] : 0;
   RRProb<S>& P0 = PP[0];
   RRProb<S>& P1 = PP[1];
-#if CMSVD_DUO_REG0
   double a0_[S][C];
-  const RegAcc<S, C> a0{a0_};
-  using Acc0 = RegAcc<S, C>;
-#else
-  const SmemAcc<S, C> a0{A0 + (elem ? tid : 0)};
-  using Acc0 = SmemAcc<S, C>;
-#endif
+  using Acc0 = HybAcc<S, C, NQR>;
+  const Acc0 a0{a0_, A0 + (elem ? tid : 0)};
   const SmemAcc<S, C> a1{A1 + (elem ? tid : 0)};
   if (elem) {
     const double* G0 = Gin + (int64_t)pa * stride_in;
@@ -1106,12 +1147,12 @@ __global__ void __launch_bounds__(kDuoThreads, (S <= 2 ? 2 : 1)) k_tridiag_duo(c
       }
     }
   }
-  for (int j = 16 * CL + tid; j < NR; j += kDuoThreads) { P0.cs[j] = 0.0; P1.cs[j] = 0.0; }
+  for (int j = 16 * CL + tid; j < NR; j += NT) { P0.cs[j] = 0.0; P1.cs[j] = 0.0; }
   if (tid == 0) {
     rr_mbar_init(&P0.bar2, kRRThreads);
-    rr_mbar_init(&P0.bar3, NR);
+    rr_mbar_init(&P0.bar3, 32 * RW);
     rr_mbar_init(&P1.bar2, kRRThreads);
-    rr_mbar_init(&P1.bar3, NR);
+    rr_mbar_init(&P1.bar3, 32 * RW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1159,7 +1200,7 @@ __global__ void __launch_bounds__(kDuoThreads, (S <= 2 ? 2 : 1)) k_tridiag_duo(c
         rr_row_phase<S>(P, k, n, t, wr, lane, 1 + g);
         rr_mbar_arrive(&P.bar3);
       }
-  } else if (tid - kRRThreads < NR) {
+  } else if (tid - kRRThreads < 32 * RW) {
     const int t = tid - kRRThreads, wr = wid - kRRWarps;
 #ifdef CMSVD_RR_PROF
     unsigned long long t_last = clock64();
@@ -1168,14 +1209,14 @@ __global__ void __launch_bounds__(kDuoThreads, (S <= 2 ? 2 : 1)) k_tridiag_duo(c
       if (k + 2 < n0) {
         rr_mbar_wait(&P0.bar2, k & 1);
         RR_T(4, wr == 0);
-        rr_row_phase<S>(P0, k, n0, t, wr, lane, 1);
+        rr_row_phase<S, RW>(P0, k, n0, t, wr, lane, 1);
         rr_mbar_arrive(&P0.bar3);
         RR_T(5, wr == 0);
       }
       if (k + 2 < n1) {
         rr_mbar_wait(&P1.bar2, k & 1);
         RR_T(6, wr == 0);
-        rr_row_phase<S>(P1, k, n1, t, wr, lane, 2);
+        rr_row_phase<S, RW>(P1, k, n1, t, wr, lane, 2);
         rr_mbar_arrive(&P1.bar3);
         RR_T(7, wr == 0);
       }
@@ -1187,13 +1228,13 @@ __global__ void __launch_bounds__(kDuoThreads, (S <= 2 ? 2 : 1)) k_tridiag_duo(c
     rr_tail<S, C, SmemAcc<S, C>>(P1, a1, n1, lane, wid);
   }
   __syncthreads();
-  if (tid < kDuoThreads / 2) rr_outputs<S>(P0, n0, pa, tid, kDuoThreads / 2, thr, kw, nstride, dout, e2out, gsh, cnt_out);
-  else if (pb < nprob) rr_outputs<S>(P1, n1, pb, tid - kDuoThreads / 2, kDuoThreads / 2, thr, kw, nstride, dout, e2out, gsh, cnt_out);
+  if (tid < NT / 2) rr_outputs<S>(P0, n0, pa, tid, NT / 2, thr, kw, nstride, dout, e2out, gsh, cnt_out);
+  else if (pb < nprob) rr_outputs<S>(P1, n1, pb, tid - NT / 2, NT / 2, thr, kw, nstride, dout, e2out, gsh, cnt_out);
 }
 
-template <int S, int C>
+template <int S, int C, int NQR = rr_nchunks<S, C>()>
 size_t duo_smem_bytes() {
-  return 2 * sizeof(RRProb<S>) + 2 * (size_t)rr_nchunks<S, C>() * kRRThreads * sizeof(double);
+  return 2 * sizeof(RRProb<S>) + (size_t)(2 * rr_nchunks<S, C>() - NQR) * kRRThreads * sizeof(double);
 }
 
 // ---------------------------------------------------------------------------
@@ -1639,8 +1680,12 @@ size_t tridiag_smem(int nmax, int kw) {
 
 // the two-problem kernel for n <= 128, except 64 < n <= 96 where two one-problem CTAs per SM of the
 // register-resident kernel are 4% faster (measured, tools/eigbench.cu)
-static bool uses_duo(const Ctx& c, int nmax) { return c.eig_rr && c.eig_duo && nmax <= 128 && !(nmax > 64 && nmax <= 96); }
-bool tridiag_can_save(const Ctx& c, int nmax) { return c.eig_rr && nmax <= 160 && !uses_duo(c, nmax); }
+// (128 < n <= 160: problem 0 split between registers and shared memory, CMSVD_EIG_DUO160; the saving
+// variant, for the greedy commits, stays on the one-problem kernel)
+static bool uses_duo(const Ctx& c, int nmax) {
+  return c.eig_rr && c.eig_duo && nmax <= 160 && !(nmax > 64 && nmax <= 96) && (nmax <= 128 || c.eig_duo160);
+}
+bool tridiag_can_save(const Ctx& c, int nmax) { return c.eig_rr && nmax <= 160 && !(nmax <= 128 && uses_duo(c, nmax)); }
 
 cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
                                 int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
@@ -1655,19 +1700,21 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   double* gsh = ee + (size_t)nprob * nstride;
   cudaError_t e;
   const bool use_rr = c.eig_rr && nmax <= 160;
-  if (uses_duo(c, nmax)) {
-#define DUO_LAUNCH(S_, C_)                                                                                          \
+  if (!save && uses_duo(c, nmax)) {
+#define DUO_LAUNCH(S_, C_, RW_, NQR_)                                                                               \
   do {                                                                                                              \
-    const size_t sm2 = duo_smem_bytes<S_, C_>();                                                                    \
-    e = cudaFuncSetAttribute(k_tridiag_duo<S_, C_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);         \
+    const size_t sm2 = duo_smem_bytes<S_, C_, NQR_>();                                                              \
+    e = cudaFuncSetAttribute(k_tridiag_duo<S_, C_, RW_, NQR_>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                             (int)sm2);                                                                             \
     if (e != cudaSuccess) return e;                                                                                 \
-    k_tridiag_duo<S_, C_><<<(nprob + 1) / 2, kDuoThreads, sm2, c.stream>>>(G, ld_in, stride_in, d_ns, nprob, d_thr, \
-                                                                          kw, nstride, dd, ee, gsh, cnt, trace);    \
+    k_tridiag_duo<S_, C_, RW_, NQR_><<<(nprob + 1) / 2, duo_threads(S_, RW_), sm2, c.stream>>>(                     \
+        G, ld_in, stride_in, d_ns, nprob, d_thr, kw, nstride, dd, ee, gsh, cnt, trace);                             \
   } while (0)
-    if (nmax <= 32) DUO_LAUNCH(1, 2);
-    else if (nmax <= 64) DUO_LAUNCH(2, 4);
-    else if (nmax <= 96) DUO_LAUNCH(3, 6);
-    else DUO_LAUNCH(4, 8);
+    if (nmax <= 32) DUO_LAUNCH(1, 2, 1, 2);
+    else if (nmax <= 64) DUO_LAUNCH(2, 4, 2, 6);
+    else if (nmax <= 96) DUO_LAUNCH(3, 6, 3, 12);
+    else if (nmax <= 128) DUO_LAUNCH(4, 8, 4, 20);
+    else DUO_LAUNCH(5, 10, CMSVD_DUO160_RW, CMSVD_DUO160_NQR);
 #undef DUO_LAUNCH
     c.launches += 1;
   } else if (use_rr) {

@@ -321,3 +321,32 @@ def test_syrk_zz_bitwise_equals_gemm_path(cm, seed, monkeypatch):
         ctx.close()
     for key in ("err2", "total", "sigma_tilde", "mu"):
         assert np.array_equal(outs[0][key], outs[1][key], equal_nan=True), key
+
+
+def test_duo160_ragged_vs_oracle_and_one_problem_kernel(cm, monkeypatch):
+    """Incremental Grams of 128 < n <= 160 on the two-problem eigen kernel (k_tridiag_duo<5>, problem 0
+    split between registers and shared memory) vs the oracle, ragged n = r' + w in 129..160 and an odd
+    problem count (the last CTA carries one problem); the one-problem kernel (CMSVD_EIG_DUO160=0) must
+    agree with it to the same tolerance."""
+    rng = np.random.default_rng(160)
+    m = 256
+    widths = [97, 100, 111, 119, 124, 127, 128]
+    blocks = []
+    for n in widths:
+        k = int(rng.integers(40, n + 1))
+        a = (rng.standard_normal((m, k)) * np.geomspace(1.0, 1e-2, k)) @ rng.standard_normal((k, n))
+        blocks.append(np.asfortranarray((a + 1e-3 * rng.standard_normal((m, n))).astype(np.float32)))
+    r = 32
+    pairs = np.array([(i, j) for i in range(7) for j in range(7) if i != j], np.int32)[:41]
+    sp = oracle.block_spectra(blocks)
+    ref = oracle.pair_errors(sp, pairs, r)
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("CMSVD_EIG_DUO160", flag)
+        ctx = cm.Context(0, torch.cuda.current_stream().cuda_stream)
+        ctx.register(blocks)
+        ctx.block_spectra(r)
+        outs.append(ctx.pair_errors(pairs))
+        ctx.close()
+        compare_pairs(outs[-1], ref, what=f"duo160={flag}")
+    assert_err2(outs[0]["err2"][:, 2], outs[1]["err2"][:, 2], ref.total, "duo160 vs one-problem kernel")

@@ -34,6 +34,7 @@ int main(int argc, char** argv) {
   for (int variant = 0; variant < 3; ++variant) {
   c.eig_rr = variant >= 1;
   c.eig_duo = variant == 2;
+  c.eig_duo160 = variant == 2;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
