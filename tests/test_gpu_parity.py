@@ -325,19 +325,20 @@ def test_syrk_zz_bitwise_equals_gemm_path(cm, seed, monkeypatch):
 
 def test_duo160_ragged_vs_oracle_and_one_problem_kernel(cm, monkeypatch):
     """Incremental Grams of 128 < n <= 160 on the two-problem eigen kernel (k_tridiag_duo<5>, problem 0
-    split between registers and shared memory) vs the oracle, ragged n = r' + w in 129..160 and an odd
-    problem count (the last CTA carries one problem); the one-problem kernel (CMSVD_EIG_DUO160=0) must
+    split between registers and shared memory) vs the oracle, ragged n = r' + w in 129..160 mixed with
+    n = 2..4 and n = 33..34 in one launch, and an odd problem count (the last CTA carries one problem); the one-problem kernel (CMSVD_EIG_DUO160=0) must
     agree with it to the same tolerance."""
     rng = np.random.default_rng(160)
     m = 256
-    widths = [97, 100, 111, 119, 124, 127, 128]
+    widths = [97, 100, 111, 119, 124, 127, 128, 1, 2]   # + tiny blocks: Grams of n = 2..4 in the same launch
     blocks = []
     for n in widths:
-        k = int(rng.integers(40, n + 1))
-        a = (rng.standard_normal((m, k)) * np.geomspace(1.0, 1e-2, k)) @ rng.standard_normal((k, n))
+        k = int(rng.integers(40, n + 1)) if n > 40 else n
+        a = (rng.standard_normal((m, k)) * np.geomspace(1.0, 1e-2 if n > 40 else 0.5, k)) @ rng.standard_normal((k, n))
         blocks.append(np.asfortranarray((a + 1e-3 * rng.standard_normal((m, n))).astype(np.float32)))
     r = 32
-    pairs = np.array([(i, j) for i in range(7) for j in range(7) if i != j], np.int32)[:41]
+    nb = len(widths)
+    pairs = np.array([(i, j) for i in range(nb) for j in range(nb) if i != j], np.int32)[1:]  # 71
     sp = oracle.block_spectra(blocks)
     ref = oracle.pair_errors(sp, pairs, r)
     outs = []
