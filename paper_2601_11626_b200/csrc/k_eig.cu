@@ -42,6 +42,24 @@ __device__ __forceinline__ double rsqrt_cubic(double x) {
 __device__ __forceinline__ double div_fast(double a, double b) { return a * rcp_nr(b); }
 __device__ __forceinline__ float div_fast(float a, float b) { return __fdividef(a, b); }
 
+// Sturm-count pivot clamp and sign test in the integer domain (the IEEE bit order of |q| is its
+// magnitude order; after the clamp |q| >= pivmin > 0, so the sign bit is q < 0): the same results as
+// fabs(q) < pivmin ? -pivmin : q and q < 0.0, off the fp64 pipe that bounds the bisection.
+__device__ __forceinline__ double sturm_clamp(double q, unsigned long long pivbits, double negpiv) {
+  unsigned hi = (unsigned)__double2hiint(q), lo = (unsigned)__double2loint(q);
+  asm("lop3.b32 %0, %0, 0x7FFFFFFF, 0, 0xc0;" : "+r"(hi));  // |q| bits (kept off the fp64 pipe)
+  return (((unsigned long long)hi << 32) | lo) < pivbits ? negpiv : q;
+}
+// Reciprocal for the Sturm recurrences: the MUFU seed y, e = 1 - q y, 1/q = y (1 + e + e^2) in three
+// dependent fp64 operations (the e^3 term is below the rounding of the result)
+__device__ __forceinline__ double rcp_sturm(double q) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  const double e = fma(-q, y, 1.0);
+  return fma(y, fma(e, e, e), y);
+}
+__device__ __forceinline__ int sturm_neg(double q) { return (int)((unsigned)__double2hiint(q) >> 31); }
+
 template <typename T>
 __device__ __forceinline__ void sturm2(const T* __restrict__ d, const T* __restrict__ e2, int n, T x0, T x1,
                                        T pivmin, int& c0, int& c1) {
@@ -1319,15 +1337,14 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
   // 1e-11 relative, whichever is looser: a large eigenvalue needs no more for sigma~ (1e-4) or for the
   // captured-energy sums (error <= 1e-11 E against the 1e-7 E floor)
   const double tol = 1e-13 * nrm;
+  const unsigned long long pivbits = (unsigned long long)__double_as_longlong(pivmin);
   for (int it = 0; it < 80 && (hi - lo) > fmax(tol, 1e-11 * fmax(fabs(lo), fabs(hi))) + 4.4e-16 * fmax(fabs(lo), fabs(hi)); ++it) {
     const double x = 0.5 * (lo + hi);
-    double q = d[0] - x;
-    if (fabs(q) < pivmin) q = -pivmin;
-    int c = q < 0.0;
+    double q = sturm_clamp(d[0] - x, pivbits, -pivmin);
+    int c = sturm_neg(q);
     for (int i = 1; i < n; ++i) {
-      q = (d[i] - x) - e2[i - 1] * rcp_nr(q);
-      if (fabs(q) < pivmin) q = -pivmin;
-      c += q < 0.0;
+      q = sturm_clamp((d[i] - x) - e2[i - 1] * rcp_sturm(q), pivbits, -pivmin);
+      c += sturm_neg(q);
     }
     if (c <= target) lo = x; else hi = x;
   }
@@ -1359,14 +1376,13 @@ __global__ void __launch_bounds__(128) k_multisect(int P, int kw, int nstride, c
   for (int it = 0; it < 40 && (hi - lo) > tol + 4.4e-16 * fmax(fabs(lo), fabs(hi)); ++it) {
     const double h = (hi - lo) * (1.0 / 33.0);
     const double x = fma((double)(lane + 1), h, lo);
-    double q = __ldg(d) - x;
-    if (fabs(q) < pivmin) q = -pivmin;
-    int c = q < 0.0;
+    const unsigned long long pivbits = (unsigned long long)__double_as_longlong(pivmin);
+    double q = sturm_clamp(__ldg(d) - x, pivbits, -pivmin);
+    int c = sturm_neg(q);
 #pragma unroll 4
     for (int i = 1; i < n; ++i) {
-      q = (__ldg(d + i) - x) - __ldg(e2 + i - 1) * rcp_nr(q);
-      if (fabs(q) < pivmin) q = -pivmin;
-      c += q < 0.0;
+      q = sturm_clamp((__ldg(d + i) - x) - __ldg(e2 + i - 1) * rcp_sturm(q), pivbits, -pivmin);
+      c += sturm_neg(q);
     }
     const unsigned below = __ballot_sync(0xffffffffu, c <= target);  // a prefix of the lanes
     const int k = __popc(below);
