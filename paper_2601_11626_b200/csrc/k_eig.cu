@@ -44,10 +44,10 @@ __device__ __forceinline__ float div_fast(float a, float b) { return __fdividef(
 
 // Sturm-count pivot clamp and sign test in the integer domain (the IEEE bit order of |q| is its
 // magnitude order; after the clamp |q| >= pivmin > 0, so the sign bit is q < 0): the same results as
-// fabs(q) < pivmin ? -pivmin : q and q < 0.0, off the fp64 pipe that bounds the bisection.
+// fabs(q) < pivmin ? -pivmin : q and q < 0.0, off the fp64 pipe.
 __device__ __forceinline__ double sturm_clamp(double q, unsigned long long pivbits, double negpiv) {
   unsigned hi = (unsigned)__double2hiint(q), lo = (unsigned)__double2loint(q);
-  asm("lop3.b32 %0, %0, 0x7FFFFFFF, 0, 0xc0;" : "+r"(hi));  // |q| bits (kept off the fp64 pipe)
+  asm("lop3.b32 %0, %0, 0x7FFFFFFF, 0, 0xc0;" : "+r"(hi));  // |q| bits (a plain & becomes an fp64 abs)
   return (((unsigned long long)hi << 32) | lo) < pivbits ? negpiv : q;
 }
 // Reciprocal for the Sturm recurrences: the MUFU seed y, e = 1 - q y, 1/q = y (1 + e + e^2) in three
@@ -1277,23 +1277,21 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
   if (STAGE) {  // problems p0 .. p0 + np - 1 of this block
     const int64_t glast = min((int64_t)P * kw, g0 + blockDim.x) - 1;
     const int np = glast >= g0 ? (int)(glast / kw) - p0 + 1 : 0;
-    double* d64 = bis_sm;
-    double* e64 = d64 + (size_t)kBisStage * nstride;
-    float* d32 = reinterpret_cast<float*>(e64 + (size_t)kBisStage * nstride);
-    float* e32 = d32 + (size_t)kBisStage * nstride;
+    // problem q: (d_i, e2_{i-1}) pairs at bis_sm + 2 q nstride, their normalised fp32 copies after all
+    // kBisStage fp64 problems (one vector load per Sturm step)
+    double* de64 = bis_sm;
+    float* de32 = reinterpret_cast<float*>(bis_sm + (size_t)2 * kBisStage * nstride);
     for (int q = 0; q < np; ++q) {
       const int pq = p0 + q;
       const int n = ns[pq];
       const float inv = (float)(1.0 / gsh[4 * pq + 3]);
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double di = dd[(int64_t)pq * nstride + i];
-        d64[q * nstride + i] = di;
-        d32[q * nstride + i] = (float)di * inv;
-        if (i + 1 < n) {
-          const double ei = ee2[(int64_t)pq * nstride + i];
-          e64[q * nstride + i] = ei;
-          e32[q * nstride + i] = (float)ei * inv * inv;
-        }
+        const double ei = i > 0 ? ee2[(int64_t)pq * nstride + i - 1] : 0.0;
+        de64[(size_t)q * 2 * nstride + 2 * i] = di;
+        de64[(size_t)q * 2 * nstride + 2 * i + 1] = ei;
+        de32[(size_t)q * 2 * nstride + 2 * i] = (float)di * inv;
+        de32[(size_t)q * 2 * nstride + 2 * i + 1] = (float)ei * inv * inv;
       }
     }
     __syncthreads();
@@ -1303,12 +1301,14 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
   double* out = ev + (int64_t)p * kw + l;
   if (l >= cnt[p]) { *out = 0.0; return; }
   const int n = ns[p];
-  const double* d = STAGE ? bis_sm + (size_t)(p - p0) * nstride : dd + (int64_t)p * nstride;
-  const double* e2 = STAGE ? bis_sm + (size_t)(kBisStage + p - p0) * nstride : ee2 + (int64_t)p * nstride;
-  const float* d32 = STAGE ? reinterpret_cast<const float*>(bis_sm + (size_t)2 * kBisStage * nstride) +
-                                 (size_t)(p - p0) * nstride
-                           : nullptr;
-  const float* e32 = STAGE ? d32 + (size_t)kBisStage * nstride : nullptr;
+  const double* d = dd + (int64_t)p * nstride;
+  const double* e2 = ee2 + (int64_t)p * nstride;
+  const double2* de64 = reinterpret_cast<const double2*>(bis_sm + (size_t)2 * (p - p0) * nstride);
+  const float2* de32 = reinterpret_cast<const float2*>(
+      reinterpret_cast<const float*>(bis_sm + (size_t)2 * kBisStage * nstride) + (size_t)2 * (p - p0) * nstride);
+  // (d_i, e2_{i-1}), i >= 1
+  auto ld64 = [&](int i) -> double2 { return STAGE ? de64[i] : make_double2(__ldg(d + i), __ldg(e2 + i - 1)); };
+  const double d0 = STAGE ? de64[0].x : d[0];
   const double glo = gsh[4 * p], ghi = gsh[4 * p + 1], pivmin = gsh[4 * p + 2], nrm = gsh[4 * p + 3];
   const int target = n - 1 - l;
   double lo = glo, hi = ghi;
@@ -1318,13 +1318,12 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
     float a = (float)(lo / nrm), b = (float)(hi / nrm);
     for (int it = 0; it < 40 && (b - a) > 4e-7f; ++it) {
       const float x = 0.5f * (a + b);
-      float q = (float)(d[0] * inv) - x;
+      float q = (float)(d0 * inv) - x;
       if (fabsf(q) < 1e-30f) q = -1e-30f;
       int c = q < 0.f;
       for (int i = 1; i < n; ++i) {
-        const float di = STAGE ? d32[i] : (float)__ldg(d + i) * inv;
-        const float ei = STAGE ? e32[i - 1] : (float)(__ldg(e2 + i - 1)) * inv * inv;
-        q = (di - x) - __fdividef(ei, q);
+        const float2 de = STAGE ? de32[i] : make_float2((float)__ldg(d + i) * inv, (float)(__ldg(e2 + i - 1)) * inv * inv);
+        q = (de.x - x) - __fdividef(de.y, q);
         if (fabsf(q) < 1e-30f) q = -1e-30f;
         c += q < 0.f;
       }
@@ -1340,10 +1339,12 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
   const unsigned long long pivbits = (unsigned long long)__double_as_longlong(pivmin);
   for (int it = 0; it < 80 && (hi - lo) > fmax(tol, 1e-11 * fmax(fabs(lo), fabs(hi))) + 4.4e-16 * fmax(fabs(lo), fabs(hi)); ++it) {
     const double x = 0.5 * (lo + hi);
-    double q = sturm_clamp(d[0] - x, pivbits, -pivmin);
+    double q = sturm_clamp(d0 - x, pivbits, -pivmin);
     int c = sturm_neg(q);
+#pragma unroll 4
     for (int i = 1; i < n; ++i) {
-      q = sturm_clamp((d[i] - x) - e2[i - 1] * rcp_sturm(q), pivbits, -pivmin);
+      const double2 de = ld64(i);
+      q = sturm_clamp((de.x - x) - de.y * rcp_sturm(q), pivbits, -pivmin);
       c += sturm_neg(q);
     }
     if (c <= target) lo = x; else hi = x;
