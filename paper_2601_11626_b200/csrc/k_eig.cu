@@ -1108,12 +1108,18 @@ constexpr int kDuoThreads = kRRThreads + 32 * 4 * kDuoGroups;  // 16 element war
 #ifndef CMSVD_DUO160_RW
 #define CMSVD_DUO160_RW 3     // n = 160: row warps (measured: 2-4 within 2%)
 #endif
+#ifndef CMSVD_DUO128_NQR
+#define CMSVD_DUO128_NQR 20   // n <= 128: problem-0 chunks in registers (of 20)
+#endif
+#ifndef CMSVD_DUO128_NQR1
+#define CMSVD_DUO128_NQR1 6   // n <= 128: problem-1 chunks in registers (of 20; measured 0/2/4/6/8/10: 6 best, -2%)
+#endif
 #ifndef CMSVD_DUO160_NQR
 #define CMSVD_DUO160_NQR 18   // n = 160: problem-0 chunks in registers (of 30; >= 18 for shared memory)
 #endif
 __host__ __device__ constexpr int duo_threads(int S, int RW) { return S <= 4 ? kDuoThreads : kRRThreads + 32 * RW; }
 
-template <int S, int C, int RW = S, int NQR = rr_nchunks<S, C>()>
+template <int S, int C, int RW = S, int NQR = rr_nchunks<S, C>(), int NQR1 = 0>
 __global__ void __launch_bounds__(duo_threads(S, RW), (S <= 2 ? 2 : 1)) k_tridiag_duo(const double* __restrict__ Gin, int64_t ld_in,
                                                                 int64_t stride_in, const int* __restrict__ ns,
                                                                 int nprob, const double* __restrict__ thr, int kw,
@@ -1130,7 +1136,7 @@ __global__ void __launch_bounds__(duo_threads(S, RW), (S <= 2 ? 2 : 1)) k_tridia
   extern __shared__ __align__(16) unsigned char duo_smem[];
   RRProb<S>* PP = reinterpret_cast<RRProb<S>*>(duo_smem);
   double* A0 = reinterpret_cast<double*>(duo_smem + 2 * sizeof(RRProb<S>));
-  double* A1 = A0 + (size_t)NQS * kRRThreads;
+  double* A1 = A0 + (size_t)NQS * kRRThreads;  // problem 1: its first NQ - NQR1 chunks (the rest in registers)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool elem = tid < kRRThreads;
   const int pa = 2 * blockIdx.x, pb = pa + 1;
@@ -1140,7 +1146,9 @@ __global__ void __launch_bounds__(duo_threads(S, RW), (S <= 2 ? 2 : 1)) k_tridia
   double a0_[S][C];
   using Acc0 = HybAcc<S, C, NQR>;
   const Acc0 a0{a0_, A0 + (elem ? tid : 0)};
-  const SmemAcc<S, C> a1{A1 + (elem ? tid : 0)};
+  double a1_[S][C];
+  using Acc1 = HybAcc<S, C, NQR1>;
+  const Acc1 a1{a1_, A1 + (elem ? tid : 0)};
   if (elem) {
     const double* G0 = Gin + (int64_t)pa * stride_in;
     const double* G1 = Gin + (int64_t)pb * stride_in;
@@ -1181,7 +1189,7 @@ __global__ void __launch_bounds__(duo_threads(S, RW), (S <= 2 ? 2 : 1)) k_tridia
       rr_reflector_warp<S>(P0, 0, x, n0, lane);
     }
     if (n1 >= 3) {
-      rr_column<S, C, SmemAcc<S, C>>(0, a1, x);
+      rr_column<S, C, Acc1>(0, a1, x);
       rr_reflector_warp<S>(P1, 0, x, n1, lane);
     }
   }
@@ -1189,7 +1197,7 @@ __global__ void __launch_bounds__(duo_threads(S, RW), (S <= 2 ? 2 : 1)) k_tridia
   const int nsteps = max(n0, n1) - 2;
   if (elem) {
     if (n0 >= 3) rr_fused_step<S, C, Acc0>(P0, a0, -1, n0, lane, wid);
-    if (n1 >= 3) rr_fused_step<S, C, SmemAcc<S, C>>(P1, a1, -1, n1, lane, wid);
+    if (n1 >= 3) rr_fused_step<S, C, Acc1>(P1, a1, -1, n1, lane, wid);
 #ifdef CMSVD_RR_PROF
     unsigned long long t_last = clock64();
 #endif
@@ -1203,7 +1211,7 @@ __global__ void __launch_bounds__(duo_threads(S, RW), (S <= 2 ? 2 : 1)) k_tridia
       if (k + 2 < n1) {
         rr_mbar_wait(&P1.bar3, k & 1);
         RR_T(2, wid == 1);
-        rr_fused_step<S, C, SmemAcc<S, C>>(P1, a1, k, n1, lane, wid);
+        rr_fused_step<S, C, Acc1>(P1, a1, k, n1, lane, wid);
         RR_T(3, wid == 1);
       }
     }
@@ -1243,16 +1251,16 @@ __global__ void __launch_bounds__(duo_threads(S, RW), (S <= 2 ? 2 : 1)) k_tridia
   __syncthreads();
   if (elem) {
     rr_tail<S, C, Acc0>(P0, a0, n0, lane, wid);
-    rr_tail<S, C, SmemAcc<S, C>>(P1, a1, n1, lane, wid);
+    rr_tail<S, C, Acc1>(P1, a1, n1, lane, wid);
   }
   __syncthreads();
   if (tid < NT / 2) rr_outputs<S>(P0, n0, pa, tid, NT / 2, thr, kw, nstride, dout, e2out, gsh, cnt_out);
   else if (pb < nprob) rr_outputs<S>(P1, n1, pb, tid - NT / 2, NT / 2, thr, kw, nstride, dout, e2out, gsh, cnt_out);
 }
 
-template <int S, int C, int NQR = rr_nchunks<S, C>()>
+template <int S, int C, int NQR = rr_nchunks<S, C>(), int NQR1 = 0>
 size_t duo_smem_bytes() {
-  return 2 * sizeof(RRProb<S>) + (size_t)(2 * rr_nchunks<S, C>() - NQR) * kRRThreads * sizeof(double);
+  return 2 * sizeof(RRProb<S>) + (size_t)(2 * rr_nchunks<S, C>() - NQR - NQR1) * kRRThreads * sizeof(double);
 }
 
 // ---------------------------------------------------------------------------
@@ -1718,20 +1726,20 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   cudaError_t e;
   const bool use_rr = c.eig_rr && nmax <= 160;
   if (!save && uses_duo(c, nmax)) {
-#define DUO_LAUNCH(S_, C_, RW_, NQR_)                                                                               \
+#define DUO_LAUNCH(S_, C_, RW_, NQR_, NQR1_)                                                                        \
   do {                                                                                                              \
-    const size_t sm2 = duo_smem_bytes<S_, C_, NQR_>();                                                              \
-    e = cudaFuncSetAttribute(k_tridiag_duo<S_, C_, RW_, NQR_>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+    const size_t sm2 = duo_smem_bytes<S_, C_, NQR_, NQR1_>();                                                       \
+    e = cudaFuncSetAttribute(k_tridiag_duo<S_, C_, RW_, NQR_, NQR1_>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                              (int)sm2);                                                                             \
     if (e != cudaSuccess) return e;                                                                                 \
-    k_tridiag_duo<S_, C_, RW_, NQR_><<<(nprob + 1) / 2, duo_threads(S_, RW_), sm2, c.stream>>>(                     \
+    k_tridiag_duo<S_, C_, RW_, NQR_, NQR1_><<<(nprob + 1) / 2, duo_threads(S_, RW_), sm2, c.stream>>>(              \
         G, ld_in, stride_in, d_ns, nprob, d_thr, kw, nstride, dd, ee, gsh, cnt, trace);                             \
   } while (0)
-    if (nmax <= 32) DUO_LAUNCH(1, 2, 1, 2);
-    else if (nmax <= 64) DUO_LAUNCH(2, 4, 2, 6);
-    else if (nmax <= 96) DUO_LAUNCH(3, 6, 3, 12);
-    else if (nmax <= 128) DUO_LAUNCH(4, 8, 4, 20);
-    else DUO_LAUNCH(5, 10, CMSVD_DUO160_RW, CMSVD_DUO160_NQR);
+    if (nmax <= 32) DUO_LAUNCH(1, 2, 1, 2, 0);
+    else if (nmax <= 64) DUO_LAUNCH(2, 4, 2, 6, 0);
+    else if (nmax <= 96) DUO_LAUNCH(3, 6, 3, 12, 0);
+    else if (nmax <= 128) DUO_LAUNCH(4, 8, 4, CMSVD_DUO128_NQR, CMSVD_DUO128_NQR1);
+    else DUO_LAUNCH(5, 10, CMSVD_DUO160_RW, CMSVD_DUO160_NQR, 0);
 #undef DUO_LAUNCH
     c.launches += 1;
   } else if (use_rr) {
