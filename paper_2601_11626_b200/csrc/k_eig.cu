@@ -1108,6 +1108,9 @@ constexpr int kDuoThreads = kRRThreads + 32 * 4 * kDuoGroups;  // 16 element war
 #ifndef CMSVD_DUO160_RW
 #define CMSVD_DUO160_RW 3     // n = 160: row warps (measured: 2-4 within 2%)
 #endif
+#ifndef CMSVD_DUO160_NQR1
+#define CMSVD_DUO160_NQR1 0   // n = 160: problem-1 chunks in registers (of 30; measured (NQR, NQR1) = (16, 4) / (14, 6): within 1%)
+#endif
 #ifndef CMSVD_DUO128_NQR
 #define CMSVD_DUO128_NQR 20   // n <= 128: problem-0 chunks in registers (of 20)
 #endif
@@ -1739,7 +1742,7 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
     else if (nmax <= 64) DUO_LAUNCH(2, 4, 2, 6, 0);
     else if (nmax <= 96) DUO_LAUNCH(3, 6, 3, 12, 0);
     else if (nmax <= 128) DUO_LAUNCH(4, 8, 4, CMSVD_DUO128_NQR, CMSVD_DUO128_NQR1);
-    else DUO_LAUNCH(5, 10, CMSVD_DUO160_RW, CMSVD_DUO160_NQR, 0);
+    else DUO_LAUNCH(5, 10, CMSVD_DUO160_RW, CMSVD_DUO160_NQR, CMSVD_DUO160_NQR1);
 #undef DUO_LAUNCH
     c.launches += 1;
   } else if (use_rr) {
