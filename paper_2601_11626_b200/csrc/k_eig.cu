@@ -1520,31 +1520,34 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
               const double d_n = (i > l) ? dd[i - 1] : 0.0;
               double f = sn * e_i;
               const double b = cs * e_i;
-              // r = hypot(f, g), sn = f / r, cs = g / r: one MUFU.RSQ64H + Newton steps instead of the
+              // r = hypot(f, g), sn = f / r, cs = g / r: one MUFU.RSQ64H + a cubic step instead of the
               // IEEE hypot and two divisions on this sequential chain; scaled fallback near under/overflow
               const double x2 = fma(f, f, g * g);
+              const double gq = d_i1 - pp;
               if (x2 > 1e-280 && x2 < 1e280) {
+                // (d_i - gq) sn + 2 cs b = y ((d_i - gq) f + 2 g b): the bracket is formed while the
+                // reciprocal square root is in flight, so one multiply follows it on the chain
+                const double T = fma(d_i - gq, f, 2.0 * g * b);
                 const double y = rsqrt_cubic(x2);
-                r = x2 * y;
-                ee[i + 1] = r;
+                ee[i + 1] = x2 * y;
                 sn = f * y;
                 cs = g * y;
+                r = T * y;
               } else {
                 r = hypot(f, g);
                 ee[i + 1] = r;
                 if (r == 0.0) {
-                  dd[i + 1] = d_i1 - pp;
+                  dd[i + 1] = gq;
                   ee[m] = 0.0;
                   underflow = true;
                   break;
                 }
                 sn = f / r;
                 cs = g / r;
+                r = (d_i - gq) * sn + 2.0 * cs * b;
               }
-              g = d_i1 - pp;
-              r = (d_i - g) * sn + 2.0 * cs * b;
               pp = sn * r;
-              dd[i + 1] = g + pp;
+              dd[i + 1] = gq + pp;
               g = cs * r - b;
               rc[i] = cs;
               rs[i] = sn;
