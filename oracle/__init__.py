@@ -13,9 +13,11 @@ marshals numpy arrays and holds the host-side greedy drivers
 Every function cites the PAPER.md passage it follows; ambiguous passages use
 the SURVEY.md §8(c) readings (A1..A21) and DESIGN.md's A22, restated in DESIGN.md.
 
-Parity unpinned: the TRUNC operand (A6) and the exact cluster
-compositions of greedy runs on synthetic data are bound only by invariants
-(P6/P17) and brute force at reduced size.
+Pins: tests/test_oracle_pins.py, tests/test_oracle_big_pins.py and
+tests/test_oracle_cluster.py (closed forms, LAPACK cross-checks, brute force,
+invariants).  Parity unpinned: the exact cluster compositions
+of greedy runs on synthetic data are bound only by the certified-error
+property (P12) and decision replay.
 """
 from __future__ import annotations
 
@@ -70,6 +72,10 @@ def lib():
         L.or_exact_groups.restype = ctypes.c_int
         L.or_exact_groups.argtypes = [i64, ip, pp, ip, ip, ctypes.c_int32, ctypes.c_int32, dp]
         L.or_num_threads.restype = ctypes.c_int
+        L.or_sym_eig_topk.restype = ctypes.c_int
+        L.or_sym_eig_topk.argtypes = [i64, dp, i64, i64, dp, dp, i64]
+        L.or_block_spectra_big.restype = ctypes.c_int
+        L.or_block_spectra_big.argtypes = [i64, i64, ctypes.c_void_p, i64, dp, dp]
         _lib = L
     return _lib
 
@@ -140,12 +146,28 @@ class Spectra:
     rank: np.ndarray     # int32 numerical rank (sigma_l > TAU sigma_1)
 
 
-def block_spectra(blocks, tau: float = TAU) -> Spectra:
+def sym_eig_topk(G: np.ndarray, k: int):
+    """All eigenvalues (non-increasing) and the top-k eigenvectors of a
+    symmetric matrix: textbook Householder tridiagonalisation, bisection on
+    Sturm counts, inverse iteration + back-transformation (oracle.c,
+    or_sym_eig_topk; reading A15)."""
+    G = np.array(G, dtype=np.float64, order="F", copy=True)
+    m = G.shape[0]
+    lam = np.zeros(m)
+    V = np.zeros((m, max(k, 1)), order="F")
+    st = lib().or_sym_eig_topk(m, _dp(G), m, int(k), _dp(lam), _dp(V), m)
+    if st:
+        raise RuntimeError(f"oracle symmetric eigensolver failed (status {st})")
+    return lam, V[:, :k]
+
+
+def block_spectra(blocks, tau: float = TAU, nvec: int | None = None) -> Spectra:
     """Per-block thin SVD in float64 (the Weyl bound needs the blocks' leading
     singular values; the residual bound the range basis,
     PAPER.md:362-363; Alg. 3 starts from the anchor's top-r SVD,
     PAPER.md:1999).  ``blocks`` is the (N, n, m) float32 array of synth or a
-    list of m×n_i arrays."""
+    list of m×n_i arrays.  ``nvec``: left singular vectors kept per block
+    wider than BIG_N (A22; default min(m, 256)); narrower blocks keep all."""
     if isinstance(blocks, np.ndarray) and blocks.ndim == 3:
         A = [np.asfortranarray(blocks[i].T, dtype=np.float64) for i in range(blocks.shape[0])]
     else:
@@ -158,7 +180,7 @@ def block_spectra(blocks, tau: float = TAU) -> Spectra:
     if any(big) and not all(big):
         raise ValueError("collections mixing blocks wider than BIG_N columns with narrower ones (A22)")
     if all(big):
-        return _block_spectra_big(A, m, n, E)
+        return _block_spectra_big(blocks, A, m, n, E, min(m, 256) if nvec is None else int(nvec))
     sig = [np.zeros(min(m, int(k))) for k in n]
     U = [np.zeros((m, min(m, int(k))), order="F") for k in n]
     st = lib().or_block_svds(m, N, _ip(n), _ptrs(A), _ptrs(sig), _ptrs(U))
@@ -168,22 +190,29 @@ def block_spectra(blocks, tau: float = TAU) -> Spectra:
     return Spectra(m, n, A, E, sig, U, rank)
 
 
-def _block_spectra_big(A, m, n, E) -> Spectra:
+def _block_spectra_big(blocks, A, m, n, E, nvec) -> Spectra:
     """Reading A22 for blocks wider than BIG_N columns (configs 3
     and 4, square weight-like blocks; n_i >= m required): the spectra follow
-    A15's exact route, the m x m fp64 Gram A A^T = U diag(sigma^2) U^T
-    (library symmetric eigensolver as one step; squaring costs relative
-    accuracy (sigma_1/sigma_l)^2 * 1e-16 only), and the block's range is taken
-    as all of R^m: rank_i = min(m, n_i) and the paper-literal residual
-    R = (I - Q Q^T) F is identically 0 (oracle.c, pair_residual)."""
+    A15's exact route in oracle.c (or_block_spectra_big): the m x m fp64 Gram
+    A A^T, own Householder tridiagonalisation, bisection for every eigenvalue,
+    inverse iteration for the top ``nvec`` eigenvectors (squaring costs
+    relative accuracy (sigma_1/sigma_l)^2 * 1e-16 only).  The block's range is
+    taken as all of R^m: rank_i = min(m, n_i) and the paper-literal residual
+    R = (I - Q Q^T) F is identically 0 (oracle.c, pair_residual).  U keeps
+    the top ``nvec`` left singular vectors (pair evaluations need r <= nvec)."""
     sig, U = [], []
-    for a in A:
+    for i, a in enumerate(A):
         if a.shape[1] < m:
             raise ValueError("A22 blocks must have n_i >= m")
-        lam, V = np.linalg.eigh(a @ a.T)
-        lam, V = lam[::-1], V[:, ::-1]
-        sig.append(np.sqrt(np.maximum(lam, 0.0)))
-        U.append(np.asfortranarray(V))
+        a32 = np.asfortranarray(blocks[i].T if isinstance(blocks, np.ndarray) and blocks.ndim == 3 else a,
+                                dtype=np.float32)
+        s = np.zeros(m)
+        u = np.zeros((m, max(nvec, 1)), order="F")
+        st = lib().or_block_spectra_big(m, a32.shape[1], a32.ctypes.data, nvec, _dp(s), _dp(u))
+        if st:
+            raise RuntimeError(f"oracle big-block spectra failed (status {st})")
+        sig.append(s)
+        U.append(u[:, :nvec])
     rank = np.array([min(m, int(k)) for k in n], dtype=np.int32)
     return Spectra(m, n, A, E, sig, U, rank)
 
@@ -199,11 +228,19 @@ class PairResult:
     mu: np.ndarray            # (P, r)
 
 
+def _check_vectors(spec: Spectra, r: int):
+    """The pair estimators read U_{i, 1..min(r, rank_i)}: blocks wider than BIG_N keep only nvec vectors."""
+    for u, rk in zip(spec.U, spec.rank):
+        if min(r, int(rk)) > u.shape[1]:
+            raise ValueError(f"r = {r} needs more left singular vectors than block_spectra(nvec={u.shape[1]}) kept")
+
+
 def pair_errors(spec: Spectra, pairs, r: int, kinds: int = 7, operand: int = RAW) -> PairResult:
     """Weyl (Eq. 5), residual (Eq. 6) and incremental (Cor. 2) estimates of
     E_r^2([A_i, F_j]) for ordered pairs (base i, appended j).  See oracle.c
     for the per-estimator definitions and citations."""
     pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+    _check_vectors(spec, r)
     P = pairs.shape[0]
     err2 = np.zeros((P, 3))
     total = np.zeros(P)
@@ -222,6 +259,7 @@ def pair_errors_tight(spec: Spectra, pairs, r: int, operand: int = RAW):
     basis U_r (A4), per-index Weyl bound (A8)] and the totals.  See oracle.c
     or_pair_errors_tight."""
     pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+    _check_vectors(spec, r)
     P = pairs.shape[0]
     err2x = np.zeros((P, 2))
     total = np.zeros(P)

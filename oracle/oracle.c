@@ -19,9 +19,13 @@
  *   or_pair_*       : brute-force SVD of the explicit concatenation (exact
  *                     error), Example D.1, Proposition 1 (corrected, A2),
  *                     [A, A] closed forms, untruncated exactness (Cor. 2),
- *                     soundness chain exact <= inc <= res <= weyl (F3, F4).
- * Parity unpinned: nothing in this file (the TRUNC operand path is pinned
- * only by invariants P6/P17).
+ *                     soundness chain exact <= inc <= res <= weyl (F3, F4),
+ *                     the hand-computed TRUNC merge (A6, n > r).
+ *   or_sym_eig_topk : 1-D Laplacian closed form under a Haar similarity,
+ *                     repeated eigenvalues, diagonal (tests/test_oracle_big_pins.py).
+ *   or_block_spectra_big : block built from a known SVD (sigma, U_r), energy
+ *                     split P1, LAPACK cross-check, A22 pair closed forms.
+ *   or_exact_groups : LAPACK on random groups, union-spectrum closed form.
  */
 #include <math.h>
 #include <stdint.h>
@@ -502,6 +506,234 @@ int or_block_svds(int64_t m, int32_t count, const int32_t* n, const double* cons
     if (st) status = st;
   }
   return status;
+}
+
+/* ------------------------------------------------------------------ */
+/* Spectra of blocks wider than 512 columns (configs 3 and 4, reading A15 */
+/* / A22): the exact route of A15, written as the textbook algorithms.    */
+/*   1. Gram G = A A^T (m x m, fp64 sums of exact fp32 products);          */
+/*   2. Householder tridiagonalisation Q^T G Q = T (Golub & Van Loan,       */
+/*      "Householder tridiagonalization": p = beta G22 v,                   */
+/*      w = p - (beta p^T v / 2) v, G22 <- G22 - v w^T - w v^T), reflectors  */
+/*      kept;                                                              */
+/*   3. every eigenvalue of T by bisection on Sturm counts (the number of   */
+/*      negative pivots of T - x I);                                        */
+/*   4. the top-k eigenvectors by inverse iteration on T - lambda I         */
+/*      (Gaussian elimination with partial pivoting, 3 iterations) with     */
+/*      full Gram-Schmidt re-orthogonalisation against the vectors already */
+/*      found, then back-transformed by the reflectors (u = Q y).           */
+/* sigma_l = sqrt(max(lambda_l, 0)): A A^T = U diag(sigma^2) U^T, so the    */
+/* left singular vectors of A are the eigenvectors of G (Thm EYM's SVD,     */
+/* PAPER.md:1211-1238).  Squaring costs (sigma_1/sigma_l)^2 * 1e-16         */
+/* relative accuracy only (A15).  OpenMP over rows / columns inside each    */
+/* loop (the loop bodies are the textbook ones).                            */
+/* ------------------------------------------------------------------ */
+
+/* number of eigenvalues of the symmetric tridiagonal (d, e) below x */
+static int64_t sturm_count(int64_t n, const double* d, const double* e, double x, double pivmin) {
+  int64_t cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  if (q < 0.0) ++cnt;
+  for (int64_t i = 1; i < n; ++i) {
+    q = (d[i] - x) - e[i - 1] * e[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+
+/* Solve (T - x I) y = b in place (b -> y) by Gaussian elimination with
+   partial pivoting on the tridiagonal (the eliminated matrix has two
+   superdiagonals); zero pivots are replaced by pivmin. */
+static void tri_solve_shifted(int64_t n, const double* d, const double* e, double x, double pivmin,
+                              double* b, double* w /* 3n scratch */) {
+  double* u0 = w;           /* diagonal of U */
+  double* u1 = w + n;       /* first superdiagonal */
+  double* u2 = w + 2 * n;   /* second superdiagonal (fill-in from row swaps) */
+  /* working rows: row i = (a_i, b_i, c_i) at columns (i, i+1, i+2) */
+  double a = d[0] - x, bb = n > 1 ? e[0] : 0.0, c = 0.0;
+  for (int64_t i = 0; i < n - 1; ++i) {
+    /* next row: (e_i, d_{i+1} - x, e_{i+1}) at columns (i, i+1, i+2) */
+    double na = e[i], nb = d[i + 1] - x, nc = (i + 2 < n) ? e[i + 1] : 0.0;
+    if (fabs(na) > fabs(a)) {       /* swap rows */
+      double ta = a, tb = bb, tc = c;
+      a = na; bb = nb; c = nc;
+      na = ta; nb = tb; nc = tc;
+      double tmp = b[i]; b[i] = b[i + 1]; b[i + 1] = tmp;
+    }
+    if (fabs(a) < pivmin) a = (a < 0.0 ? -pivmin : pivmin);
+    double l = na / a;
+    u0[i] = a; u1[i] = bb; u2[i] = c;
+    b[i + 1] -= l * b[i];
+    /* the remaining row after elimination starts at column i+1 */
+    a = nb - l * bb;
+    bb = nc - l * c;
+    c = 0.0;
+  }
+  if (fabs(a) < pivmin) a = (a < 0.0 ? -pivmin : pivmin);
+  u0[n - 1] = a; u1[n - 1] = 0.0; u2[n - 1] = 0.0;
+  /* back substitution */
+  for (int64_t i = n - 1; i >= 0; --i) {
+    double t = b[i];
+    if (i + 1 < n) t -= u1[i] * b[i + 1];
+    if (i + 2 < n) t -= u2[i] * b[i + 2];
+    b[i] = t / u0[i];
+  }
+}
+
+/* Symmetric eigen-decomposition of the m x m matrix G (column-major, full
+   storage; destroyed).  lam[m] = all eigenvalues, non-increasing;
+   V (m x k, ldv) = eigenvectors of the top k (k <= m). */
+int or_sym_eig_topk(int64_t m, double* G, int64_t ldg, int64_t k, double* lam, double* V, int64_t ldv) {
+  if (m <= 0 || k < 0 || k > m) return OR_EARG;
+  double* d = (double*)malloc(sizeof(double) * m);
+  double* e = (double*)calloc((size_t)(m > 1 ? m : 1), sizeof(double));
+  double* beta = (double*)calloc((size_t)(m > 1 ? m : 1), sizeof(double));
+  double* p = (double*)malloc(sizeof(double) * m);
+  /* 2. tridiagonalisation; reflector j (j = 0..m-3) acts on rows j+1..m-1 and
+     is stored in G(j+1:m, j) with v[j+1] = 1 implicit */
+  for (int64_t j = 0; j + 2 < m; ++j) {
+    double* x = G + j * ldg;           /* column j, rows j+1..m-1 */
+    const int64_t n2 = m - j - 1;
+    double sig2 = 0.0;
+    for (int64_t i = j + 2; i < m; ++i) sig2 += x[i] * x[i];
+    double alpha = x[j + 1];
+    if (sig2 == 0.0) {                  /* already tridiagonal in this column */
+      beta[j] = 0.0;
+      d[j] = G[j + j * ldg];
+      e[j] = alpha;
+      continue;
+    }
+    double mu = sqrt(alpha * alpha + sig2);
+    double v0 = alpha <= 0.0 ? alpha - mu : -sig2 / (alpha + mu);   /* GVL Alg. 5.1.1 */
+    double b = 2.0 * v0 * v0 / (sig2 + v0 * v0);
+    for (int64_t i = j + 2; i < m; ++i) x[i] /= v0;
+    x[j + 1] = 1.0;
+    beta[j] = b;
+    d[j] = G[j + j * ldg];
+    e[j] = mu;                          /* (I - b v v^T) x = mu e_1 */
+    const double* v = x + j + 1;        /* length n2 */
+    /* p = b * G22 v  (G22 = G(j+1:m, j+1:m), symmetric: row i = column i) */
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n2; ++i) {
+      const double* gi = G + (j + 1 + i) * ldg + j + 1;
+      double t = 0.0;
+      for (int64_t l = 0; l < n2; ++l) t += gi[l] * v[l];
+      p[i] = b * t;
+    }
+    double pv = 0.0;
+    for (int64_t i = 0; i < n2; ++i) pv += p[i] * v[i];
+    const double half = 0.5 * b * pv;
+    for (int64_t i = 0; i < n2; ++i) p[i] -= half * v[i];          /* p := w */
+    /* G22 <- G22 - v w^T - w v^T */
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < n2; ++c) {
+      double* gc = G + (j + 1 + c) * ldg + j + 1;
+      const double vc = v[c], wc = p[c];
+      for (int64_t i = 0; i < n2; ++i) gc[i] -= v[i] * wc + p[i] * vc;
+    }
+  }
+  if (m >= 2) {
+    d[m - 2] = G[(m - 2) + (m - 2) * ldg];
+    e[m - 2] = G[(m - 1) + (m - 2) * ldg];
+  }
+  d[m - 1] = G[(m - 1) + (m - 1) * ldg];
+  /* 3. bisection for every eigenvalue inside the Gershgorin interval */
+  double lo = d[0], hi = d[0], tnorm = 0.0;
+  for (int64_t i = 0; i < m; ++i) {
+    double rad = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0);
+    if (d[i] - rad < lo) lo = d[i] - rad;
+    if (d[i] + rad > hi) hi = d[i] + rad;
+    if (fabs(d[i]) + rad > tnorm) tnorm = fabs(d[i]) + rad;
+  }
+  const double pivmin = 1e-300 + 2.2250738585072014e-308 * (tnorm > 1.0 ? tnorm : 1.0);
+  const double eps = 2.220446049250313e-16;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t l = 0; l < m; ++l) {
+    /* lam[l] = the (l+1)-th largest = the eigenvalue with m-1-l eigenvalues below it */
+    const int64_t below = m - 1 - l;
+    double a = lo - eps * tnorm, bnd = hi + eps * tnorm;
+    /* to 2 ulps relative, or 1e-3 ulp of ||T|| absolute (the Gram route's own accuracy is ~ulp ||T||) */
+    for (int it = 0;
+         it < 200 && bnd - a > 2.0 * eps * (fabs(a) > fabs(bnd) ? fabs(a) : fabs(bnd)) + 1e-3 * eps * tnorm + pivmin;
+         ++it) {
+      double mid = 0.5 * (a + bnd);
+      if (sturm_count(m, d, e, mid, pivmin) > below) bnd = mid;
+      else a = mid;
+    }
+    lam[l] = 0.5 * (a + bnd);
+  }
+  /* 4. inverse iteration for the top k eigenvectors of T, re-orthogonalised */
+  double* Y = (double*)calloc((size_t)(m * (k > 0 ? k : 1)), sizeof(double));
+  double* scratch = (double*)malloc(sizeof(double) * 4 * m);
+  for (int64_t l = 0; l < k; ++l) {
+    double* y = Y + l * m;
+    for (int64_t i = 0; i < m; ++i) y[i] = 1.0 + 0.5 * sin((double)(i + 1) * (double)(l + 7) * 0.7317);
+    /* shift perturbed by a few ulps of ||T|| so that T - x I stays solvable */
+    const double x = lam[l] + 4.0 * eps * tnorm;
+    for (int it = 0; it < 3; ++it) {
+      tri_solve_shifted(m, d, e, x, eps * tnorm, y, scratch);
+      for (int64_t q = 0; q < l; ++q) {                 /* Gram-Schmidt against earlier vectors */
+        const double* yq = Y + q * m;
+        double t = 0.0;
+        for (int64_t i = 0; i < m; ++i) t += yq[i] * y[i];
+        for (int64_t i = 0; i < m; ++i) y[i] -= t * yq[i];
+      }
+      double nrm = 0.0;
+      for (int64_t i = 0; i < m; ++i) nrm += y[i] * y[i];
+      nrm = sqrt(nrm);
+      for (int64_t i = 0; i < m; ++i) y[i] /= nrm;
+    }
+  }
+  /* back-transformation u = H_0 H_1 ... H_{m-3} y, applied from the last reflector */
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t l = 0; l < k; ++l) {
+    double* y = Y + l * m;
+    for (int64_t j = m - 3; j >= 0; --j) {
+      if (beta[j] == 0.0) continue;
+      const double* v = G + j * ldg + j + 1;   /* v[0] = 1 stored */
+      double t = 0.0;
+      for (int64_t i = 0; i < m - j - 1; ++i) t += v[i] * y[j + 1 + i];
+      t *= beta[j];
+      for (int64_t i = 0; i < m - j - 1; ++i) y[j + 1 + i] -= t * v[i];
+    }
+    for (int64_t i = 0; i < m; ++i) V[i + l * ldv] = y[i];
+  }
+  free(d); free(e); free(beta); free(p); free(Y); free(scratch);
+  return OR_OK;
+}
+
+/* Spectra of one block A (m x n, fp32 column-major, n >= m) by the Gram
+   route above: sig[m] = sqrt(max(lambda, 0)) non-increasing, U (m x k) the
+   left singular vectors of the top k. */
+int or_block_spectra_big(int64_t m, int64_t n, const float* A, int64_t k, double* sig, double* U) {
+  double* G = (double*)malloc(sizeof(double) * m * m);
+  if (!G) return OR_EARG;
+  /* 1. G = A A^T: G_ij = sum_c A_ic A_jc (A column-major: row i is strided), via A^T rows */
+  double* At = (double*)malloc(sizeof(double) * m * n);     /* At[c + i*n] = A[i + c*m] */
+  if (!At) { free(G); return OR_EARG; }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t c = 0; c < n; ++c) At[c + i * n] = (double)A[i + c * m];
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int64_t j = 0; j < m; ++j) {
+    const double* aj = At + j * n;
+    for (int64_t i = j; i < m; ++i) {
+      const double* ai = At + i * n;
+      double t = 0.0;
+      for (int64_t c = 0; c < n; ++c) t += ai[c] * aj[c];
+      G[i + j * m] = t;
+      G[j + i * m] = t;
+    }
+  }
+  free(At);
+  double* lam = (double*)malloc(sizeof(double) * m);
+  int st = or_sym_eig_topk(m, G, m, k, lam, U, m);
+  for (int64_t l = 0; l < m; ++l) sig[l] = sqrt(lam[l] > 0.0 ? lam[l] : 0.0);
+  free(lam);
+  free(G);
+  return st;
 }
 
 /* Batched explicit-concatenation exact errors for tiny inputs:
