@@ -98,6 +98,23 @@ def _status_name(s: int) -> str:
         return f"status {s}"
 
 
+def _check_tensor(t, name, dtype, shape, device=None):
+    """Device-path argument check (a torch tensor's raw pointer goes to the C ABI): dtype, contiguity,
+    exact shape and device, so that a mismatched tensor raises instead of being misread or overrun."""
+    if t is None:
+        raise CmsvdError(E_ARG, f"{name} is required")
+    if not hasattr(t, "data_ptr"):
+        raise CmsvdError(E_ARG, f"{name}: expected a torch tensor")
+    if str(t.dtype) != dtype:
+        raise CmsvdError(E_ARG, f"{name}: dtype {t.dtype}, expected {dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise CmsvdError(E_SHAPE, f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if not t.is_contiguous():
+        raise CmsvdError(E_ARG, f"{name}: not contiguous")
+    if device is not None and (not t.is_cuda or t.device.index != device):
+        raise CmsvdError(E_ARG, f"{name}: on {t.device}, expected cuda:{device}")
+
+
 def _ptr(a):
     if a is None:
         return None
@@ -117,6 +134,7 @@ class Context:
             raise CmsvdError(s, "cmsvd_create failed (is a CUDA device visible?)")
         self._h = h
         self._L = L
+        self.device = device
         self.count = 0
         self.r = 0
 
@@ -165,6 +183,7 @@ class Context:
         holding the transposed (n_i, m) layout)."""
         if hasattr(blocks, "dim") and blocks.dim() == 3:          # torch tensor (N, n, m)
             N, n, m = blocks.shape
+            _check_tensor(blocks, "blocks", "torch.float32", (N, n, m), self.device if blocks.is_cuda else None)
             dev = blocks.is_cuda
             base = blocks.data_ptr()
             stride = n * m * 4
@@ -186,6 +205,7 @@ class Context:
                 if hasattr(b, "data_ptr"):
                     dev = b.is_cuda
                     nn, mm = b.shape
+                    _check_tensor(b, "blocks[i]", "torch.float32", (nn, mm), self.device if dev else None)
                     ptrs.append(b.data_ptr())
                 else:
                     f = np.asfortranarray(b, dtype=np.float32)
@@ -225,6 +245,12 @@ class Context:
         r = self.r if r is None else r
         if hasattr(pairs, "data_ptr") and pairs.is_cuda:
             P = pairs.shape[0]
+            _check_tensor(pairs, "pairs", "torch.int32", (P, 2), self.device)
+            _check_tensor(out.get("err2"), "out['err2']", "torch.float64", (P, 3), self.device)
+            _check_tensor(out.get("total"), "out['total']", "torch.float64", (P,), self.device)
+            for k in ("sigma_tilde", "mu"):
+                if out.get(k) is not None:
+                    _check_tensor(out[k], f"out['{k}']", "torch.float32", (P, r), self.device)
             self._check(self._L.cmsvd_pair_errors(self._h, _ptr(pairs), P, r, kinds, operand, DEVICE,
                                                   _ptr(out["err2"]), _ptr(out["total"]),
                                                   _ptr(out.get("sigma_tilde")), _ptr(out.get("mu"))))

@@ -194,10 +194,10 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
       return fail(c, CMSVD_E_SHAPE, "block_spectra: blocks wider than " + std::to_string(kEigMax) +
                                         " columns must have n_i >= m (A22)");
   const int s = (int)std::min<int64_t>(std::min<int64_t>(m, 2 * (int64_t)r), kEigMax);
-  if (r > s && r < m)
+  const int kc = (int)std::min<int64_t>(r, m);
+  if (kc > s)  // the subspace holds s columns: more than s = min(m, 2r, 512) top vectors cannot be returned
     return fail(c, CMSVD_E_SHAPE, "block_spectra: r > " + std::to_string(kEigMax) + " on blocks wider than " +
                                       std::to_string(kEigMax) + " columns");
-  const int kc = (int)std::min<int64_t>(r, m);
   const int nmax = c.nmax;
   c.big = true;
   c.kcols.assign(N, kc);
@@ -534,7 +534,9 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
   const int64_t m = c.m;
   // tight (N3): residual with the U_r basis + per-index Weyl; d_err2 is then P x 2
   if (tight) kinds = CMSVD_RESIDUAL;
-  const bool need_mat = (kinds & (CMSVD_RESIDUAL | CMSVD_INCREMENTAL)) != 0;
+  // A22 bases (c.big): the paper-literal residual needs no projection (R = (I - QQ^T)F = 0), so Weyl- and
+  // residual-only evaluations run on the spectra alone
+  const bool need_mat = (kinds & CMSVD_INCREMENTAL) != 0 || tight || ((kinds & CMSVD_RESIDUAL) != 0 && !c.big);
   const bool full = (kinds & CMSVD_RESIDUAL) != 0 && !tight;
   const int QMAX = std::max(1, full ? dims.qmax : dims.rrmax);
   // tcgen05 path (fp32 accumulation) unless the collection has numerically rank-deficient blocks: an

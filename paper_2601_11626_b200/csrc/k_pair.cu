@@ -258,7 +258,9 @@ __global__ void k_finalize(const int2* __restrict__ pairs, int64_t P, const Base
     double unsel = 0.0;
     for (int l = ib; l < b.ns; ++l) unsel += b.spec[l] * b.spec[l];
     // A22 (full-range base): R = 0, mu = top-r sigma(A_i), err^2 = E_i - sum_sel sigma^2 + ||F||^2 + extra
-    er = b.rest_res + unsel + (b.full ? 0.0 : fmax(trW[p] - sel_w, 0.0)) + zn2[p] + a.extra;
+    // zn2 == nullptr: no projection was computed (A22 base, residual without the incremental estimator);
+    // then ||F||^2 = E_app - extra by the appended block's spectrum
+    er = b.rest_res + unsel + (b.full ? 0.0 : fmax(trW[p] - sel_w, 0.0)) + (zn2 ? zn2[p] : a.E - a.extra) + a.extra;
   } else if (mu) {
     for (int l = 0; l < r; ++l) mu[p * r + l] = nanf("");
   }

@@ -29,7 +29,7 @@ def _worker(rank, ws, port, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws))
     import bench
-    r, w, local, d = bench.dist_init(None)
+    r, w, local, d = bench.dist_init()
     assert (r, w) == (rank, ws) and d is not None and d.get_backend() == "gloo"
     mx = bench.max_over_ranks(d, float(10 * rank + 1))
     col = bench.workload("config1", rank)
