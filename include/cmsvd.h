@@ -243,6 +243,19 @@ typedef struct {
 cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_t* assign, int32_t* order,
                            int32_t* n_clusters, double* cluster_err2, double* cluster_total, int64_t* n_evals);
 
+/* Diagnostic: the batched fp64 symmetric eigensolver that yields sigma~^2 from the core Grams (Lemma 1 /
+ * Cor. 3), on caller matrices, for parity tests.
+ *   count >= 1 problems; problem p is n[p] x n[p] (0 <= n[p] <= nmax <= 512) at G + p * nmax * nmax,
+ *   column-major with leading dimension nmax, symmetric (only the lower triangle is read), host memory;
+ *   ev[p * kw + l] = the l-th largest eigenvalue (l < min(kw, n[p])), non-increasing; entries l >= n[p]
+ *   are unspecified; trace[p] = sum of the diagonal (may be NULL).  1 <= kw <= nmax.  The dispatch by
+ *   size is the pair path's (n <= 160 register/shared-memory kernels, 160 < n <= 512 the two-stage band
+ *   reduction; CMSVD_EIG_SBR=0 selects the one-stage in-place kernel).
+ * Errors: CMSVD_E_ARG (NULL pointers, kw out of range), CMSVD_E_SHAPE (n[p] < 0, n[p] > nmax or
+ * nmax > 512), CMSVD_E_CUDA, CMSVD_E_NOMEM. */
+cmsvd_status cmsvd_sym_eigvals(cmsvd_ctx ctx, int32_t count, int32_t nmax, const int32_t* n, const double* G,
+                               int32_t kw, double* ev, double* trace);
+
 /* Number of kernel launches this context has issued since creation (for the
  * bench's gpu_launches accounting). */
 int64_t cmsvd_launch_count(cmsvd_ctx ctx);

@@ -27,7 +27,7 @@ SORT_FROBENIUS, SORT_RESIDUAL = 0, 1
 EXPORTS = ["cmsvd_status_string", "cmsvd_last_error", "cmsvd_version", "cmsvd_create", "cmsvd_destroy",
            "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_pair_errors_tight",
            "cmsvd_cluster", "cmsvd_cluster_verify", "cmsvd_cluster_factors", "cmsvd_sequence_errors",
-           "cmsvd_launch_count",
+           "cmsvd_launch_count", "cmsvd_sym_eigvals",
            "cmsvd_profile_enable",
            "cmsvd_profile_read"]
 
@@ -81,6 +81,8 @@ def load(path: str = LIB_PATH):
     L.cmsvd_cluster_factors.argtypes = [vp, i32, vp, i32, vp, vp, vp]
     L.cmsvd_cluster_verify.restype = ctypes.c_int
     L.cmsvd_cluster_verify.argtypes = [vp, i32, vp, i32, vp, vp, vp]
+    L.cmsvd_sym_eigvals.restype = ctypes.c_int
+    L.cmsvd_sym_eigvals.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp]
     L.cmsvd_launch_count.restype = i64
     L.cmsvd_launch_count.argtypes = [vp]
     L.cmsvd_profile_enable.restype = ctypes.c_int
@@ -175,6 +177,21 @@ class Context:
         cnt = np.zeros(mx, np.int64)
         k = self._L.cmsvd_profile_read(self._h, mx, names, _ptr(ms), _ptr(cnt))
         return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(k)}
+
+    # -- cmsvd_sym_eigvals (diagnostic) ------------------------------------
+    def sym_eigvals(self, mats, kw: int):
+        """Top-kw eigenvalues of symmetric matrices (list of n_p x n_p float64 arrays, n_p <= 512) through
+        the pair path's batched eigensolver: returns (ev (count, kw) non-increasing, trace (count,))."""
+        ns = np.array([m.shape[0] for m in mats], np.int32)
+        nmax = int(max(1, ns.max()))
+        G = np.zeros((len(mats), nmax, nmax))
+        for p, m in enumerate(mats):
+            G[p, :m.shape[0], :m.shape[0]] = np.asarray(m, np.float64).T    # column-major
+        ev = np.zeros((len(mats), kw))
+        tr = np.zeros(len(mats))
+        self._check(self._L.cmsvd_sym_eigvals(self._h, len(mats), nmax, _ptr(ns), _ptr(G), int(kw), _ptr(ev),
+                                              _ptr(tr)))
+        return ev, tr
 
     # -- cmsvd_register --------------------------------------------------
     def register(self, blocks, where: int | None = None):

@@ -83,6 +83,8 @@ cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
   if (const char* env = getenv("CMSVD_EIG_DUO")) h->c.eig_duo = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_DUO160")) h->c.eig_duo160 = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_COMMIT_TOPK")) h->c.commit_topk = !(env[0] == '0');
+  if (const char* env = getenv("CMSVD_CHASE_FLAGS")) h->c.chase_flags = (env[0] == '1');
+  if (const char* env = getenv("CMSVD_EIG_SBR")) h->c.eig_sbr = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_RR")) h->c.eig_rr = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_SUBSPACE_ITERS")) h->c.subspace_iters = std::max(0, atoi(env));
   *out = h;
@@ -198,6 +200,16 @@ cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_
     return fail(c, CMSVD_E_NOMEM, "cluster: host allocation failed");
   } catch (...) {
     return fail(c, CMSVD_E_ARG, "cluster: unexpected exception");
+  }
+}
+
+cmsvd_status cmsvd_sym_eigvals(cmsvd_ctx ctx, int32_t count, int32_t nmax, const int32_t* n, const double* G,
+                               int32_t kw, double* ev, double* trace) {
+  GUARD_CTX(ctx);
+  try {
+    return do_sym_eigvals(c, count, nmax, n, G, kw, ev, trace);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "sym_eigvals: host allocation failed");
   }
 }
 

@@ -67,11 +67,13 @@ struct DevMem {
 // Per-kernel-category CUDA-event timing (cmsvd_profile_enable/read).
 enum ProfCat {
   PC_ENERGY = 0, PC_SPEC_GRAM, PC_SPEC_EIG, PC_SPEC_MISC, PC_DESCS, PC_PROJ, PC_RESID, PC_GRAM_W, PC_GRAM_ZZ,
-  PC_BUILD_G, PC_EIG_G, PC_EIG_W, PC_FINALIZE, PC_CLUSTER, PC_PAIR_TC, PC_COUNT
+  PC_BUILD_G, PC_EIG_G, PC_EIG_W, PC_FINALIZE, PC_CLUSTER, PC_PAIR_TC, PC_SBR_PANEL, PC_SBR_SYMM, PC_SBR_SYR2K,
+  PC_SBR_CHASE, PC_BISECT, PC_COUNT
 };
 static const char* const kProfNames[PC_COUNT] = {
   "energy", "spectra_gram", "spectra_eig", "spectra_misc", "pair_descs", "proj_Z", "resid_R", "gram_W",
-  "gram_ZZ", "build_G", "eig_G", "eig_W", "finalize", "cluster_misc", "pair_tc"};
+  "gram_ZZ", "build_G", "eig_G", "eig_W", "finalize", "cluster_misc", "pair_tc", "sbr_panel", "sbr_symm",
+  "sbr_syr2k", "sbr_chase", "bisect"};
 
 struct Prof {
   bool on = false;
@@ -122,6 +124,8 @@ struct Ctx {
   bool use_tc = true;                  // tcgen05 contraction kernel (CMSVD_NO_TC=1 selects the SIMT path)
   bool tc_ok = true;                   // every block numerically full column rank (set by block_spectra)
   int gl_batch_mb = 1024;              // in-place global-memory eigen batches (n > 160), MB of matrices per launch
+  bool chase_flags = false;            // band chase: per-sweep progress flags instead of time-step barriers
+  bool eig_sbr = true;                 // n > 160: two-stage (band) reduction instead of the one-stage in-place kernel
   bool eig_rr = true;                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)
   bool zz_syrk = true;                 // w <= 128: Z^T Z by k_syrk_zz instead of k_gemm_tn (CMSVD_ZZ_SYRK=0: off)
   bool tc_big = true;                  // q or w > 128: tcgen05 GEMM tiles instead of SIMT (CMSVD_TC_BIG=0: off)

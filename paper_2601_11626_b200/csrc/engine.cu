@@ -801,4 +801,31 @@ Status do_pair_errors_tight(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, 
                        total, nullptr, nullptr, true);
 }
 
+// Diagnostic entry: the pair path's batched eigensolver on caller matrices (include/cmsvd.h).
+Status do_sym_eigvals(Ctx& c, int32_t count, int32_t nmax, const int32_t* n, const double* G, int32_t kw,
+                      double* ev, double* trace) {
+  if (!n || !G || !ev || count < 1) return fail(c, CMSVD_E_ARG, "sym_eigvals: NULL pointer or count < 1");
+  if (nmax < 1 || nmax > kEigMax) return fail(c, CMSVD_E_SHAPE, "sym_eigvals: nmax must be in 1..512");
+  if (kw < 1 || kw > nmax) return fail(c, CMSVD_E_ARG, "sym_eigvals: kw must be in 1..nmax");
+  for (int32_t p = 0; p < count; ++p)
+    if (n[p] < 0 || n[p] > nmax) return fail(c, CMSVD_E_SHAPE, "sym_eigvals: n[p] outside 0..nmax");
+  const size_t mat = (size_t)count * nmax * nmax * 8;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) { size_t o = off; off += align_up(bytes, 256); return o; };
+  const size_t oG = carve(mat), oN = carve((size_t)count * 4), oE = carve((size_t)count * kw * 8),
+               oC = carve((size_t)count * 4), oT = carve((size_t)count * 8),
+               oS = carve(tridiag_scratch_bytes(count, nmax));
+  CK(ensure(c.ws[WS_PAIR], off), "sym_eigvals: workspace");
+  char* b = (char*)c.ws[WS_PAIR].p;
+  CK(cudaMemcpyAsync(b + oG, G, mat, cudaMemcpyHostToDevice, c.stream), "sym_eigvals: h2d");
+  CK(cudaMemcpyAsync(b + oN, n, (size_t)count * 4, cudaMemcpyHostToDevice, c.stream), "sym_eigvals: h2d");
+  CK(launch_tridiag_topk(c, (const double*)(b + oG), nmax, (int64_t)nmax * nmax, (const int*)(b + oN), count, nmax,
+                         nullptr, kw, (double*)(b + oE), (int*)(b + oC), (double*)(b + oT), (double*)(b + oS)),
+     "sym_eigvals: eigensolver");
+  CK(cudaMemcpyAsync(ev, b + oE, (size_t)count * kw * 8, cudaMemcpyDeviceToHost, c.stream), "sym_eigvals: d2h");
+  if (trace) CK(cudaMemcpyAsync(trace, b + oT, (size_t)count * 8, cudaMemcpyDeviceToHost, c.stream), "sym_eigvals: d2h");
+  CK(cudaStreamSynchronize(c.stream), "sym_eigvals: sync");
+  return CMSVD_OK;
+}
+
 }  // namespace cmsvd

@@ -10,7 +10,7 @@ typedef cmsvd_status Status;
 constexpr int kEigMax = 512;  // largest Gram handled by the eigensolvers (> 160: in place in global memory)
 
 // context workspace slots (Ctx::ws)
-enum { WS_PARTIAL = 0, WS_BAD, WS_META, WS_G, WS_V, WS_EV, WS_PERM, WS_STAT, WS_PAIR, WS_OUT, WS_A, WS_B, WS_C, WS_D, WS_E };
+enum { WS_PARTIAL = 0, WS_BAD, WS_META, WS_G, WS_V, WS_EV, WS_PERM, WS_STAT, WS_PAIR, WS_OUT, WS_A, WS_B, WS_C, WS_D, WS_E, WS_SBR };
 
 struct Dims {
   int qmax = 0;   // projection-basis columns (full range)
@@ -58,6 +58,8 @@ Status do_cluster_verify(Ctx& c, int32_t r, const int32_t* assign, int32_t n_clu
                          double* total, int64_t* mem);
 Status do_sequence_errors(Ctx& c, const int32_t* offs, const int32_t* ids, int32_t nseq, int32_t r, uint32_t kinds,
                           int operand, double* err2, double* total);
+Status do_sym_eigvals(Ctx& c, int32_t count, int32_t nmax, const int32_t* n, const double* G, int32_t kw,
+                      double* ev, double* trace);
 Status do_cluster(Ctx& c, const cmsvd_cluster_opts* o, int32_t* assign, int32_t* order, int32_t* n_clusters,
                   double* cluster_err2, double* cluster_total, int64_t* n_evals);
 

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "engine.h"
 
 namespace cmsvd {
 
@@ -1765,6 +1766,13 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
     k_tridiag<false><<<nprob, kTriThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, d_thr, kw, nstride, dd, ee,
                                                              gsh, cnt, trace);
     c.launches += 1;
+  } else if (c.eig_sbr) {
+    // two-stage reduction (k_sbr.cu): dense -> band (BLAS3-shaped panels) -> tridiagonal (bulge chasing)
+    e = ensure(c.ws[WS_SBR], sbr_ws_bytes(nprob));
+    if (e != cudaSuccess) return e;
+    e = launch_tridiag_sbr(c, const_cast<double*>(G), ld_in, stride_in, d_ns, nprob, nmax, d_thr, kw, nstride, dd, ee,
+                           gsh, cnt, trace, (double*)c.ws[WS_SBR].p);
+    if (e != cudaSuccess) return e;
   } else {
     // in place in global memory (G is destroyed); batches sized to stay L2-resident
     e = cudaFuncSetAttribute(k_tridiag<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1783,6 +1791,7 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t total = (int64_t)nprob * kw;
+  const int prb = prof_begin(c, PC_BISECT);
   if (total <= kMultisectMax)
     k_multisect<<<(unsigned)((total + 3) / 4), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
   else
@@ -1800,6 +1809,7 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
     }
   }
   c.launches += 1;
+  prof_end(c, prb);
   return cudaGetLastError();
 }
 

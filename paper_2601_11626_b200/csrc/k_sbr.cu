@@ -1,0 +1,705 @@
+// k_sbr.cu -- two-stage Householder tridiagonalisation of the large core Grams (160 < n <= 512:
+// configs 3 and 4, n = r' + w = 256 / 512), the values path of Cor. 3's eigendecomposition
+// (sigma~^2 = the top-r eigenvalues of the core Gram).
+//
+// The one-stage reduction applies a rank-2 update to the whole trailing matrix per column: at n = 512
+// the 1 MB lower triangle of every problem is streamed from HBM 510 times (358 MB per problem).  Here:
+//   stage 1 (dense -> band of half-bandwidth kSB = 16, "successive band reduction"), per panel t
+//     (columns c0 = 16 t .. c0 + 15, trailing block A22 = rows/cols R0 = c0 + 16 .. n - 1):
+//       k_sbr_panel  : Householder QR of the n_p x 16 panel below the band (n_p = n - R0), one CTA per
+//                      problem in shared memory; V (unit lower trapezoidal), T of the compact WY form
+//                      Q = I - V T V^T (LAPACK's larft recurrence), R written into the band;
+//       k_sbr_symm   : Y = A22 V T (A22 read once per 128-row block as a symmetric row panel), per-block
+//                      partials M_b = V_b^T Y_b;
+//       k_sbr_syr2k  : A22 <- Q^T A22 Q = A22 - V W^T - W V^T with W = Y - 1/2 V (T^T sum_b M_b)
+//                      (lower 64 x 64 tiles; W formed per tile from Y, V and the 16 x 16 partials);
+//     so the trailing matrix is streamed ~2x per 16 columns instead of once per column, in BLAS3-shaped
+//     register-tiled fp64 passes;
+//   stage 2 (band -> tridiagonal by bulge chasing), k_sbr_chase: one CTA per problem, band (lower, with
+//     room for the bulge: 2 kSB + 1 diagonals) in shared memory.  Sweep j annihilates column j below the
+//     subdiagonal with a length-16 Householder H_0 (two-sided on the diagonal block, right-applied to the
+//     block below, which fills it); step s >= 1 annihilates the first column of that fill with H_s
+//     (left-applied to it, two-sided on the next diagonal block, right-applied to the next block).
+//     One warp per sweep; sweep j may run step s once sweep j-1 has finished step s + 2 (the blocks the
+//     two touch are then disjoint), tracked by per-sweep progress counters in shared memory.
+// Outputs: those of k_tridiag (diagonal, squared sub-diagonal, Gershgorin data, count above the
+// threshold, trace) so that the same bisection kernels follow.
+#include <algorithm>
+
+#include "common.cuh"
+#include "engine.h"
+#include "kernels.cuh"
+
+namespace cmsvd {
+
+#ifndef CMSVD_CHASE_SLEEP
+#define CMSVD_CHASE_SLEEP 0
+#endif
+
+constexpr int kSB = 16;                 // band half-width of stage 1
+constexpr int kSBMax = 512;             // largest n
+constexpr int kSBLdb = 2 * kSB + 2;     // band storage: diagonals 0 .. 2 kSB (band + bulge), padded so that a
+                                        // row walk (stride kSBLdb - 1 doubles) is free of bank conflicts
+constexpr int kSymmRows = 128;          // rows of A22 per k_sbr_symm CTA
+constexpr int kSymmJB = 32;             // columns staged per k_sbr_symm step
+constexpr int kSymmThreads = 128;
+constexpr int kSyrTile = 64;            // k_sbr_syr2k tile
+constexpr int kSyrThreads = 256;
+constexpr int kPanelThreads = 256;
+constexpr int kChaseWarps = 12;
+constexpr int kMBlocks = kSBMax / kSymmRows;   // M partials per problem
+
+// workspace per problem (doubles): V (kSBMax x kSB), Y/W (kSBMax x kSB), T (kSB x kSB), M (kMBlocks x kSB x kSB)
+constexpr int64_t kSbrV = (int64_t)kSBMax * kSB;
+constexpr int64_t kSbrPer = 2 * kSbrV + kSB * kSB + (int64_t)kMBlocks * kSB * kSB;
+
+__device__ __forceinline__ double sbr_rcp(double q) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  double e = fma(-q, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-q, y, 1.0);
+  return fma(y, e, y);
+}
+
+// number of stage-1 panels of an n x n problem: panel t exists while at least 2 rows lie below its band
+__host__ __device__ __forceinline__ int sbr_panels(int n) { return n >= kSB + 2 ? (n - kSB - 2) / kSB + 1 : 0; }
+
+// ---------------------------------------------------------------------------
+// Stage 1a: panel QR.  Panel t of problem p: P = A[R0 .. n-1, c0 .. c0+15] (n_p x 16).
+// ---------------------------------------------------------------------------
+constexpr int kPanelLd = kSBMax + 1;   // column stride of the staged panel (odd: conflict-free columns)
+
+__global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict__ G, int64_t ld, int64_t stride,
+                                                              const int* __restrict__ ns, int t,
+                                                              double* __restrict__ ws, double* __restrict__ trace) {
+  extern __shared__ __align__(16) double psm[];
+  double* P = psm;                                   // [kSB][kPanelLd]
+  double* red = P + kSB * kPanelLd;                  // [16][16] partial sums
+  double* scal = red + 256;                          // beta, tau per column; S (16 x 16), T (16 x 16)
+  double* S = scal + 2 * kSB;
+  double* T = S + kSB * kSB;
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  const int tid = threadIdx.x;
+  double* A = G + (int64_t)p * stride;
+  if (t == 0 && tid == 0) {   // trace of the original matrix (invariant, kept for the finalisation)
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += A[(int64_t)i * ld + i];
+    trace[p] = s;
+  }
+  if (t >= sbr_panels(n)) return;
+  const int c0 = t * kSB, R0 = c0 + kSB, np = n - R0;
+  // stage the panel
+  for (int e = tid; e < kSB * np; e += kPanelThreads) {
+    const int c = e / np, i = e - c * np;
+    P[c * kPanelLd + i] = A[(int64_t)(c0 + c) * ld + R0 + i];
+  }
+  __syncthreads();
+  const int g = tid >> 4, cc = tid & 15;   // 16 row groups x 16 columns
+  const int kmax = min(kSB, np);
+  for (int k = 0; k < kmax; ++k) {
+    double* x = P + k * kPanelLd;
+    // squared norm below the diagonal element
+    double part = 0.0;
+    for (int i = k + 1 + tid; i < np; i += kPanelThreads) part = fma(x[i], x[i], part);
+    part = warp_sum(part);
+    if ((tid & 31) == 0) red[tid >> 5] = part;
+    __syncthreads();
+    double sig2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kPanelThreads / 32; ++q) sig2 += red[q];
+    const double alpha = x[k];
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (sig2 > 0.0) {
+      const double xn = sqrt(fma(alpha, alpha, sig2));
+      beta = alpha >= 0.0 ? -xn : xn;
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    __syncthreads();   // red reused below
+    for (int i = k + 1 + tid; i < np; i += kPanelThreads) x[i] *= scale;
+    if (tid == 0) { x[k] = beta; scal[k] = tau; }
+    __syncthreads();
+    // s_c = tau (P[k][c] + sum_{i>k} v_i P[i][c]) for c > k, then P[i][c] -= s_c v_i (v_k = 1)
+    if (tau != 0.0) {
+      double d = 0.0;
+      if (cc > k) {
+        const double* pc = P + cc * kPanelLd;
+        if (g == 0) d = pc[k];
+        for (int i = k + 1 + g; i < np; i += 16) d = fma(x[i], pc[i], d);
+      }
+      red[g * 16 + cc] = d;
+      __syncthreads();
+      if (cc > k) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) s += red[q * 16 + cc];
+        s *= tau;
+        double* pc = P + cc * kPanelLd;
+        if (g == 0) pc[k] -= s;
+        for (int i = k + 1 + g; i < np; i += 16) pc[i] = fma(-s, x[i], pc[i]);
+      }
+      __syncthreads();
+    }
+  }
+  // V^T V (strictly upper part needed): S[j][k] = V[k][j] + sum_{i>k} V[i][j] V[i][k], j < k
+  {
+    const int j = tid >> 4, k = tid & 15;
+    double s = 0.0;
+    if (j < k && k < kmax) {
+      const double* vj = P + j * kPanelLd;
+      const double* vk = P + k * kPanelLd;
+      s = vj[k];
+      for (int i = k + 1; i < np; ++i) s = fma(vj[i], vk[i], s);
+    }
+    S[j * kSB + k] = s;
+  }
+  __syncthreads();
+  // T (upper triangular): T[k][k] = tau_k, T[0:k][k] = -tau_k T[0:k][0:k] S[0:k][k]
+  if (tid < 32) {
+    const int i = tid;
+    for (int k = 0; k < kSB; ++k) {
+      const double tk = k < kmax ? scal[k] : 0.0;
+      double s = 0.0;
+      if (i < k)
+        for (int l = i; l < k; ++l) s = fma(T[i * kSB + l], S[l * kSB + k], s);
+      __syncwarp();
+      if (i < kSB) T[i * kSB + k] = (i < k) ? -tk * s : (i == k ? tk : 0.0);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // outputs: R into the band (rows R0 .. R0 + 15 of the panel columns, upper triangle), V, T
+  double* Vw = ws + (int64_t)p * kSbrPer;
+  double* Tw = Vw + 2 * kSbrV;
+  for (int e = tid; e < kSB * kSB; e += kPanelThreads) {
+    const int c = e >> 4, k = e & 15;   // R[k][c], k <= c
+    if (k <= c && k < np) A[(int64_t)(c0 + c) * ld + R0 + k] = P[c * kPanelLd + k];
+    Tw[e] = T[e];
+  }
+  for (int e = tid; e < kSB * np; e += kPanelThreads) {
+    const int c = e / np, i = e - c * np;
+    const double v = (i < c) ? 0.0 : (i == c ? 1.0 : P[c * kPanelLd + i]);
+    Vw[(int64_t)c * kSBMax + i] = (c < kmax) ? v : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1b: Y = A22 V T for rows [128 b, 128 b + 128) of A22 (n_p x n_p, symmetric, lower stored),
+// M_b = V_b^T Y_b.  Thread t: rows i0 = t % 64 and i0 + 64, columns 8 (t / 64) .. + 7.  The 32-column
+// slices of the symmetric row panel are staged by cp.async into two buffers (the next slice's copies in
+// flight during the current slice's products); slices above the diagonal are read from the lower
+// storage and transposed on the way into shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kSymmLd = kSymmRows + 1;
+constexpr int kSymmBuf = kSymmJB * kSymmLd + kSymmJB * kSB;   // doubles per stage buffer
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+
+__global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __restrict__ G, int64_t ld,
+                                                                int64_t stride, const int* __restrict__ ns, int t,
+                                                                double* __restrict__ ws) {
+  extern __shared__ __align__(16) double ssm[];
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int I0 = blockIdx.y * kSymmRows;
+  if (I0 >= np) return;
+  const int tid = threadIdx.x;
+  const double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;   // A22(i, j) at A[j * ld + i]
+  const double* Vw = ws + (int64_t)p * kSbrPer;
+  double* Yw = const_cast<double*>(Vw) + kSbrV;
+  const int i0 = tid & 63, h = tid >> 6;
+  const int imax = min(kSymmRows, np - I0);
+  // stage the slice starting at column J0 into buffer `buf` (At[j][i] = A22(I0 + i, J0 + j), Vs[j][c])
+  auto stage = [&](int J0, int buf) {
+    double* At = ssm + buf * kSymmBuf;
+    double* Vs = At + kSymmJB * kSymmLd;
+    const int jmax = min(kSymmJB, np - J0);
+    if (J0 + jmax - 1 <= I0) {            // all i >= j: lower storage, contiguous in i
+      for (int e = tid; e < kSymmJB * kSymmRows; e += kSymmThreads) {
+        const int jj = e >> 7, ii = e & 127;
+        const bool ok = jj < jmax && ii < imax;
+        cp_async8(At + jj * kSymmLd + ii, ok ? A + (int64_t)(J0 + jj) * ld + I0 + ii : A, ok);
+      }
+    } else if (I0 + imax - 1 < J0) {      // all i < j: A22(i, j) = A22(j, i) at A[i * ld + j], contiguous in j
+      for (int e = tid; e < kSymmJB * kSymmRows; e += kSymmThreads) {
+        const int ii = e >> 5, jj = e & 31;
+        const bool ok = jj < jmax && ii < imax;
+        cp_async8(At + jj * kSymmLd + ii, ok ? A + (int64_t)(I0 + ii) * ld + J0 + jj : A, ok);
+      }
+    } else {
+      for (int e = tid; e < kSymmJB * kSymmRows; e += kSymmThreads) {
+        const int jj = e >> 7, ii = e & 127;
+        const bool ok = jj < jmax && ii < imax;
+        const int gi = I0 + ii, gj = J0 + jj;
+        const double* src = !ok ? A : (gi >= gj ? A + (int64_t)gj * ld + gi : A + (int64_t)gi * ld + gj);
+        cp_async8(At + jj * kSymmLd + ii, src, ok);
+      }
+    }
+    for (int e = tid; e < kSymmJB * kSB; e += kSymmThreads) {
+      const int jj = e >> 4, c = e & 15;
+      const bool ok = jj < jmax;
+      cp_async8(Vs + e, ok ? Vw + (int64_t)c * kSBMax + J0 + jj : Vw, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[2][8];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
+  const int nsl = (np + kSymmJB - 1) / kSymmJB;
+  stage(0, 0);
+  for (int k = 0; k < nsl; ++k) {
+    if (k + 1 < nsl) {
+      stage((k + 1) * kSymmJB, (k + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* At = ssm + (k & 1) * kSymmBuf;
+    const double* Vs = At + kSymmJB * kSymmLd;
+#pragma unroll 4
+    for (int jj = 0; jj < kSymmJB; ++jj) {
+      const double a0 = At[jj * kSymmLd + i0], a1 = At[jj * kSymmLd + i0 + 64];
+      const double2* vr = reinterpret_cast<const double2*>(Vs + jj * kSB + 8 * h);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 v = vr[q];
+        acc[0][2 * q] = fma(a0, v.x, acc[0][2 * q]);
+        acc[0][2 * q + 1] = fma(a0, v.y, acc[0][2 * q + 1]);
+        acc[1][2 * q] = fma(a1, v.x, acc[1][2 * q]);
+        acc[1][2 * q + 1] = fma(a1, v.y, acc[1][2 * q + 1]);
+      }
+    }
+    __syncthreads();   // this buffer is restaged at step k + 2
+  }
+  // X rows to shared memory (row stride 17: conflict-free column walks), then Y = X T and M_b = V_b^T Y_b
+  constexpr int kX = kSB + 1;
+  double* Xs = ssm;
+  double* Ts = Xs + kSymmRows * kX;
+  double* Ys = Ts + kSB * kSB;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) Xs[(i0 + 64 * a) * kX + 8 * h + c] = acc[a][c];
+  const double* Tw = Vw + 2 * kSbrV;
+  for (int e = tid; e < kSB * kSB; e += kSymmThreads) Ts[e] = Tw[e];
+  __syncthreads();
+  for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
+    const int c = e >> 7, i = e & 127;
+    double y = 0.0;
+    for (int l = 0; l <= c; ++l) y = fma(Xs[i * kX + l], Ts[l * kSB + c], y);
+    Ys[i * kX + c] = (i < imax) ? y : 0.0;
+    if (i < imax) Yw[(int64_t)c * kSBMax + I0 + i] = y;
+  }
+  __syncthreads();
+  double* Mw = const_cast<double*>(Vw) + 2 * kSbrV + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
+  for (int e = tid; e < kSB * kSB; e += kSymmThreads) {
+    const int a = e >> 4, c = e & 15;
+    double s = 0.0;
+    for (int i = 0; i < imax; ++i) s = fma(Vw[(int64_t)a * kSBMax + I0 + i], Ys[i * kX + c], s);
+    Mw[e] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1c: W = Y - V Z in place of Y, Z = 1/2 T^T sum_b M_b (16 x 16), rows [128 b, 128 b + 128).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t, double* __restrict__ ws) {
+  __shared__ double Ms[kSB * kSB], Zs[kSB * kSB];
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int I0 = blockIdx.y * kSymmRows;
+  if (I0 >= np) return;
+  const int tid = threadIdx.x;
+  double* Vw = ws + (int64_t)p * kSbrPer;
+  double* Yw = Vw + kSbrV;
+  const double* Tw = Vw + 2 * kSbrV;
+  const double* Mw = Tw + kSB * kSB;
+  const int nmb = (np + kSymmRows - 1) / kSymmRows;
+  double s = 0.0;
+  for (int b = 0; b < nmb; ++b) s += Mw[b * kSB * kSB + tid];
+  Ms[tid] = s;
+  __syncthreads();
+  {
+    const int a = tid >> 4, c = tid & 15;
+    double z = 0.0;
+    for (int l = 0; l <= a; ++l) z = fma(Tw[l * kSB + a], Ms[l * kSB + c], z);   // (T^T M)[a][c], T upper
+    Zs[tid] = 0.5 * z;
+  }
+  __syncthreads();
+  const int imax = min(kSymmRows, np - I0);
+  for (int e = tid; e < kSymmRows * kSB; e += 256) {
+    const int c = e >> 7, i = e & 127;
+    if (i >= imax) continue;
+    const int64_t gi = I0 + i;
+    double w = Yw[(int64_t)c * kSBMax + gi];
+#pragma unroll
+    for (int l = 0; l < kSB; ++l) w = fma(-Vw[(int64_t)l * kSBMax + gi], Zs[l * kSB + c], w);
+    Yw[(int64_t)c * kSBMax + gi] = w;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1d: A22 <- A22 - V W^T - W V^T on the lower 64 x 64 tiles.
+// Thread t: rows tx = t % 32 (+32), columns 8 (t / 32) .. + 7 of the tile.  The tile's loads are issued
+// first, the V / W rows of the tile are staged while they are in flight.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSyrThreads, 2) k_sbr_syr2k(double* __restrict__ G, int64_t ld, int64_t stride,
+                                                                const int* __restrict__ ns, int t,
+                                                                const double* __restrict__ ws) {
+  __shared__ __align__(16) double VI[kSB * kSyrTile], WI[kSB * kSyrTile], VJ[kSB * kSyrTile], WJ[kSB * kSyrTile];
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int nt = (np + kSyrTile - 1) / kSyrTile;
+  int q = blockIdx.y, ti = 0;
+  while (q > ti) { ++ti; q -= ti; }      // blockIdx.y = ti (ti + 1) / 2 + tj, tj <= ti
+  const int tj = q;
+  if (ti >= nt) return;
+  const int I0 = ti * kSyrTile, J0 = tj * kSyrTile;
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+  double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;
+  const bool diag = ti == tj;
+  double a[2][8];
+#pragma unroll
+  for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int i = tx + 32 * r2, j = 8 * ty + c;
+      const bool ok = I0 + i < np && J0 + j < np && (!diag || i >= j);
+      a[r2][c] = ok ? A[(int64_t)(J0 + j) * ld + I0 + i] : 0.0;
+    }
+  const double* Vw = ws + (int64_t)p * kSbrPer;
+  const double* Ww = Vw + kSbrV;
+  // [l][i] layouts: column l of V / W for the tile rows (coalesced global loads)
+  for (int e = tid; e < kSyrTile * kSB; e += kSyrThreads) {
+    const int l = e >> 6, i = e & 63;
+    const int gi = I0 + i, gj = J0 + i;
+    VI[e] = gi < np ? Vw[(int64_t)l * kSBMax + gi] : 0.0;
+    WI[e] = gi < np ? Ww[(int64_t)l * kSBMax + gi] : 0.0;
+    VJ[e] = gj < np ? Vw[(int64_t)l * kSBMax + gj] : 0.0;
+    WJ[e] = gj < np ? Ww[(int64_t)l * kSBMax + gj] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int l = 0; l < kSB; ++l) {
+    const double vi0 = VI[l * kSyrTile + tx], vi1 = VI[l * kSyrTile + tx + 32];
+    const double wi0 = WI[l * kSyrTile + tx], wi1 = WI[l * kSyrTile + tx + 32];
+    const double2* vj2 = reinterpret_cast<const double2*>(VJ + l * kSyrTile + 8 * ty);
+    const double2* wj2 = reinterpret_cast<const double2*>(WJ + l * kSyrTile + 8 * ty);
+#pragma unroll
+    for (int c2 = 0; c2 < 4; ++c2) {
+      const double2 vj = vj2[c2], wj = wj2[c2];
+      a[0][2 * c2] = fma(-vi0, wj.x, fma(-wi0, vj.x, a[0][2 * c2]));
+      a[1][2 * c2] = fma(-vi1, wj.x, fma(-wi1, vj.x, a[1][2 * c2]));
+      a[0][2 * c2 + 1] = fma(-vi0, wj.y, fma(-wi0, vj.y, a[0][2 * c2 + 1]));
+      a[1][2 * c2 + 1] = fma(-vi1, wj.y, fma(-wi1, vj.y, a[1][2 * c2 + 1]));
+    }
+  }
+#pragma unroll
+  for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int i = tx + 32 * r2, j = 8 * ty + c;
+      const bool ok = I0 + i < np && J0 + j < np && (!diag || i >= j);
+      if (ok) A[(int64_t)(J0 + j) * ld + I0 + i] = a[r2][c];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 2: bulge chasing on the band, one CTA per problem.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double& bat(double* Bd, int i, int j) { return Bd[j * kSBLdb + (i - j)]; }  // i >= j
+
+// task (j, s) of sweep j on the band Bd (n x n), executed by one warp
+__device__ __forceinline__ void chase_task(double* __restrict__ Bd, int n, int j, int s) {
+  const int lane = threadIdx.x & 31;
+  const int r = j + 1 + s * kSB;
+  const int L = min(kSB, n - r);
+  const int cx = (s == 0) ? j : r - kSB;    // column holding the vector to annihilate (rows r .. r + L - 1)
+  const int l16 = lane & 15, hh = lane >> 4;
+  const int r2 = r + L;
+  const int L2 = min(kSB, n - r2);
+  // every load of the task first (the three blocks it updates are disjoint): B (s >= 1, left-apply),
+  // D (two-sided), C (right-apply); lane (l16, hh) holds column / row l16 and the 8 entries 8 hh .. 8 hh + 7
+#ifdef CMSVD_CHASE_PROF
+  long long ck0 = clock64();
+#endif
+  double x = (lane < L) ? bat(Bd, r + lane, cx) : 0.0;
+  double b[8], dd[8], cr[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int l = 8 * hh + q;
+    b[q] = (s > 0 && l < L) ? bat(Bd, r + l, cx + l16) : 0.0;               // B[l][c = l16]
+    dd[q] = (l16 < L && l < L) ? (l16 >= l ? bat(Bd, r + l16, r + l) : bat(Bd, r + l, r + l16)) : 0.0;  // D[a][l]
+    cr[q] = (l16 < L2 && l < L) ? bat(Bd, r2 + l16, r + l) : 0.0;           // C[a][l]
+  }
+  double sq = (lane >= 1 && lane < L) ? x * x : 0.0;
+  sq = warp_sum(sq);
+  const double alpha = __shfl_sync(0xffffffffu, x, 0);
+  double tau = 0.0, beta = alpha, scale = 0.0;
+  if (sq > 0.0) {
+    const double x2 = fma(alpha, alpha, sq);
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x2));
+    const double e = fma(-(x2 * y), y, 1.0);
+    y = fma(y * e, fma(e, 0.375, 0.5), y);
+    const double xn = x2 * y;
+    beta = alpha >= 0.0 ? -xn : xn;
+    tau = (beta - alpha) * sbr_rcp(beta);
+    scale = sbr_rcp(alpha - beta);
+  }
+#ifdef CMSVD_CHASE_PROF
+  long long ck1 = clock64();
+#endif
+  if (tau == 0.0) return;   // H = I (x is already beta e_0): nothing to apply (warp-uniform)
+  // v by lane: vh[q] = v[8 hh + q], va = v[l16]
+  const double vmine = (lane == 0) ? 1.0 : ((lane < L) ? x * scale : 0.0);
+  double vh[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) vh[q] = __shfl_sync(0xffffffffu, vmine, 8 * hh + q);
+  const double va = __shfl_sync(0xffffffffu, vmine, l16);
+  // three independent dot products per lane
+  double db = 0.0, pa = 0.0, qd = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    db = fma(vh[q], b[q], db);
+    pa = fma(dd[q], vh[q], pa);
+    qd = fma(cr[q], vh[q], qd);
+  }
+  db += __shfl_xor_sync(0xffffffffu, db, 16);
+  pa += __shfl_xor_sync(0xffffffffu, pa, 16);
+  qd += __shfl_xor_sync(0xffffffffu, qd, 16);
+  db *= tau;
+  pa *= tau;
+  qd *= tau;
+  // (b) K = tau/2 p.v: lanes 0..15 and 16..31 hold the same p_a, reduce over a (4 levels)
+  double pv = (l16 < L) ? pa * va : 0.0;
+  pv += __shfl_xor_sync(0xffffffffu, pv, 1);
+  pv += __shfl_xor_sync(0xffffffffu, pv, 2);
+  pv += __shfl_xor_sync(0xffffffffu, pv, 4);
+  pv += __shfl_xor_sync(0xffffffffu, pv, 8);
+  const double wa = pa - 0.5 * tau * pv * va;
+  double wh[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) wh[q] = __shfl_sync(0xffffffffu, wa, 8 * hh + q);
+#ifdef CMSVD_CHASE_PROF
+  long long ck2 = clock64();
+#endif
+  // stores (each lane writes only entries it loaded itself, or the lower entries of D it owns)
+  if (s == 0) {
+    if (lane < L) bat(Bd, r + lane, j) = (lane == 0) ? beta : 0.0;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int l = 8 * hh + q;
+      if (l < L) bat(Bd, r + l, cx + l16) = (l16 == 0) ? (l == 0 ? beta : 0.0) : fma(-db, vh[q], b[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int l = 8 * hh + q;
+    if (l16 < L && l <= l16) bat(Bd, r + l16, r + l) = fma(-va, wh[q], fma(-wa, vh[q], dd[q]));
+    if (l16 < L2 && l < L) bat(Bd, r2 + l16, r + l) = fma(-qd, vh[q], cr[q]);
+  }
+#ifdef CMSVD_CHASE_PROF
+  __syncwarp();
+  long long ck3 = clock64();
+  if (blockIdx.x == 0 && lane == 0 && j == 200 && s == 5)
+    printf("task (200,5): householder %lld, applies %lld, stores %lld cycles\n", ck1 - ck0, ck2 - ck1, ck3 - ck2);
+#endif
+}
+
+// FLAGS: per-sweep progress flags (each warp owns whole sweeps and polls its predecessor's counter)
+// instead of one CTA barrier per wavefront time step
+template <bool FLAGS>
+__global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double* __restrict__ G, int64_t ld,
+                                                                    int64_t stride, const int* __restrict__ ns,
+                                                                    const double* __restrict__ thr, int kw,
+                                                                    int nstride, double* __restrict__ dout,
+                                                                    double* __restrict__ e2out,
+                                                                    double* __restrict__ gsh,
+                                                                    int* __restrict__ cnt_out) {
+  extern __shared__ __align__(16) double bsm[];
+  double* Bd = bsm;                                              // [kSBMax][kSBLdb]
+  volatile int* prog = reinterpret_cast<volatile int*>(Bd + kSBMax * kSBLdb);   // steps done per sweep
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double* A = G + (int64_t)p * stride;
+  double* dO = dout + (int64_t)p * nstride;
+  double* eO = e2out + (int64_t)p * nstride;
+  if (n <= 0) {
+    if (tid == 0) { cnt_out[p] = 0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; }
+    return;
+  }
+  for (int e = tid; e < n * kSBLdb; e += blockDim.x) {
+    const int jj = e / kSBLdb, d = e - jj * kSBLdb;
+    Bd[e] = (d <= kSB && jj + d < n) ? A[(int64_t)jj * ld + jj + d] : 0.0;
+  }
+  for (int e = tid; e < n; e += blockDim.x) prog[e] = 0;
+  __syncthreads();
+  if (FLAGS) {
+  // sweeps j = wid, wid + W, ...; step s of sweep j waits until sweep j - 1 has completed step s + 2
+  for (int j = wid; j + 2 < n; j += kChaseWarps) {
+    const int nsteps = (n - 3 - j) / kSB + 1;   // steps with a window of >= 2 rows
+    for (int s = 0; s < nsteps; ++s) {
+      if (j > 0) {
+        const int need = min(s + 3, (n - 3 - (j - 1)) / kSB + 1);
+        if (lane == 0)
+          while (prog[j - 1] < need) {
+#if CMSVD_CHASE_SLEEP
+            __nanosleep(CMSVD_CHASE_SLEEP);
+#endif
+          }
+        __syncwarp();
+        __threadfence_block();
+      }
+      chase_task(Bd, n, j, s);
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) prog[j] = s + 1;
+    }
+  }
+  } else {
+  // time-stepped wavefront: task (j, s) runs at time 3 j + s, so that step s of sweep j follows step s + 2
+  // of sweep j - 1 (their blocks are then disjoint); the tasks of one time step are independent and
+  // spread over the warps, one CTA barrier per time step (no polling)
+  const int tmax = 3 * (n - 3);
+#ifdef CMSVD_CHASE_PROF
+  long long ct0 = clock64();
+#endif
+  for (int tt = 0; tt <= tmax; ++tt) {
+    const int jhi = min(tt / 3, n - 3);
+    for (int idx = wid;; idx += kChaseWarps) {
+      const int j = jhi - idx;
+      const int s = tt - 3 * j;
+      if (j < 0 || s >= (n - 3 - j) / kSB + 1) break;
+      chase_task(Bd, n, j, s);
+    }
+    __syncthreads();
+  }
+#ifdef CMSVD_CHASE_PROF
+  if (blockIdx.x == 0 && tid == 0) printf("chase: %d time steps, %lld cycles (%lld per step)\n", tmax + 1,
+                                          clock64() - ct0, (clock64() - ct0) / (tmax + 1));
+#endif
+  }
+  (void)prog;
+  __syncthreads();
+  // outputs (as k_tridiag): d, e^2, Gershgorin data, threshold count
+  for (int i = tid; i < n; i += blockDim.x) {
+    dO[i] = Bd[i * kSBLdb];
+    if (i + 1 < n) { const double e1 = Bd[i * kSBLdb + 1]; eO[i] = e1 * e1; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double glo = 1e300, ghi = -1e300, emax = 0.0;
+    for (int i = 0; i < n; ++i) {
+      double rr = 0.0;
+      if (i > 0) rr += fabs(Bd[(i - 1) * kSBLdb + 1]);
+      if (i + 1 < n) rr += fabs(Bd[i * kSBLdb + 1]);
+      const double di = Bd[i * kSBLdb];
+      glo = fmin(glo, di - rr);
+      ghi = fmax(ghi, di + rr);
+      if (i + 1 < n) emax = fmax(emax, Bd[i * kSBLdb + 1] * Bd[i * kSBLdb + 1]);
+    }
+    const double nrm = fmax(fmax(fabs(glo), fabs(ghi)), 1e-300);
+    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax) * 4.0;
+    glo -= 2.2e-16 * nrm * n + pivmin;
+    ghi += 2.2e-16 * nrm * n + pivmin;
+    gsh[4 * p] = glo; gsh[4 * p + 1] = ghi; gsh[4 * p + 2] = pivmin; gsh[4 * p + 3] = nrm;
+    int above = n;
+    if (thr) {
+      const double tt = thr[p];
+      if (tt >= ghi) above = 0;
+      else if (tt > glo) {
+        // Sturm count of T - tt I
+        int c0 = 0;
+        double qd = Bd[0] - tt;
+        if (fabs(qd) < pivmin) qd = -pivmin;
+        c0 += qd < 0.0;
+        for (int i = 1; i < n; ++i) {
+          const double e1 = Bd[(i - 1) * kSBLdb + 1];
+          qd = (Bd[i * kSBLdb] - tt) - e1 * e1 / qd;
+          if (fabs(qd) < pivmin) qd = -pivmin;
+          c0 += qd < 0.0;
+        }
+        above = n - c0;
+      }
+    }
+    cnt_out[p] = min(kw, above);
+  }
+}
+
+size_t sbr_ws_bytes(int nprob) { return (size_t)nprob * kSbrPer * sizeof(double); }
+
+// Stage 1 + stage 2 for nprob problems (n = ns[p] <= 512, G destroyed): writes dd, ee (e^2), gsh, cnt,
+// trace like k_tridiag.  ws: sbr_ws_bytes(nprob) bytes.
+cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, const int* d_ns, int nprob, int nmax,
+                               const double* d_thr, int kw, int nstride, double* dd, double* ee, double* gsh,
+                               int* cnt, double* trace, double* ws) {
+  if (nmax > kSBMax) return cudaErrorInvalidValue;
+  const int npan = sbr_panels(nmax);
+  const size_t psmem = ((size_t)kSB * kPanelLd + 256 + 2 * kSB + 2 * kSB * kSB) * sizeof(double);
+  const size_t ssmem = (size_t)2 * kSymmBuf * sizeof(double);
+  const size_t ssmem2 = ((size_t)kSymmRows * (kSB + 1) * 2 + kSB * kSB) * sizeof(double);
+  const size_t symm_smem = std::max(ssmem, ssmem2);
+  cudaError_t e = cudaFuncSetAttribute(k_sbr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_sbr_symm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)symm_smem);
+  if (e != cudaSuccess) return e;
+  // trace (panel 0 kernel) even when there are no panels
+  for (int t = 0; t < std::max(npan, 1); ++t) {
+    const int np0 = nmax - (t + 1) * kSB;   // largest trailing size at this panel
+    int pr = prof_begin(c, PC_SBR_PANEL);
+    k_sbr_panel<<<nprob, kPanelThreads, psmem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace);
+    c.launches += 1;
+    prof_end(c, pr);
+    if (t >= npan) break;
+    const int nrb = (np0 + kSymmRows - 1) / kSymmRows;
+    pr = prof_begin(c, PC_SBR_SYMM);
+    k_sbr_symm<<<dim3(nprob, nrb), kSymmThreads, symm_smem, c.stream>>>(G, ld, stride, d_ns, t, ws);
+    c.launches += 1;
+    prof_end(c, pr);
+    pr = prof_begin(c, PC_SBR_SYR2K);
+    k_sbr_w<<<dim3(nprob, nrb), 256, 0, c.stream>>>(d_ns, t, ws);
+    c.launches += 1;
+    const int nt = (np0 + kSyrTile - 1) / kSyrTile;
+    k_sbr_syr2k<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, 0, c.stream>>>(G, ld, stride, d_ns, t, ws);
+    c.launches += 1;
+    prof_end(c, pr);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const size_t csmem = (size_t)kSBMax * kSBLdb * sizeof(double) + kSBMax * sizeof(int);
+  const int pr = prof_begin(c, PC_SBR_CHASE);
+  if (c.chase_flags) {
+    e = cudaFuncSetAttribute(k_sbr_chase<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
+    if (e != cudaSuccess) return e;
+    k_sbr_chase<true><<<nprob, kChaseWarps * 32, csmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd, ee,
+                                                                    gsh, cnt);
+  } else {
+    e = cudaFuncSetAttribute(k_sbr_chase<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
+    if (e != cudaSuccess) return e;
+    k_sbr_chase<false><<<nprob, kChaseWarps * 32, csmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd, ee,
+                                                                     gsh, cnt);
+  }
+  c.launches += 1;
+  prof_end(c, pr);
+  return cudaGetLastError();
+}
+
+}  // namespace cmsvd
