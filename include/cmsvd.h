@@ -256,6 +256,13 @@ cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_
 cmsvd_status cmsvd_sym_eigvals(cmsvd_ctx ctx, int32_t count, int32_t nmax, const int32_t* n, const double* G,
                                int32_t kw, double* ev, double* trace);
 
+/* Diagnostic: accuracy record of the last cmsvd_block_spectra on blocks wider than 512 columns (reading
+ * A22, subspace iteration): the largest Ritz residual ||A A^T u_l - lambda_l u_l|| / lambda_l over the
+ * returned l < r (guarded: the call iterates further while it exceeds 1e-4 and fails with CMSVD_E_NOCONV
+ * after CMSVD_SUBSPACE_MAX power iterations) and the number of power iterations used.  Both 0 for
+ * collections of narrower blocks (exact eigendecompositions).  Either output may be NULL. */
+cmsvd_status cmsvd_spectra_diagnostics(cmsvd_ctx ctx, double* max_ritz_residual, int32_t* power_iterations);
+
 /* Number of kernel launches this context has issued since creation (for the
  * bench's gpu_launches accounting). */
 int64_t cmsvd_launch_count(cmsvd_ctx ctx);

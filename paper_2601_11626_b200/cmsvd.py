@@ -27,7 +27,7 @@ SORT_FROBENIUS, SORT_RESIDUAL = 0, 1
 EXPORTS = ["cmsvd_status_string", "cmsvd_last_error", "cmsvd_version", "cmsvd_create", "cmsvd_destroy",
            "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_pair_errors_tight",
            "cmsvd_cluster", "cmsvd_cluster_verify", "cmsvd_cluster_factors", "cmsvd_sequence_errors",
-           "cmsvd_launch_count", "cmsvd_sym_eigvals",
+           "cmsvd_launch_count", "cmsvd_sym_eigvals", "cmsvd_spectra_diagnostics",
            "cmsvd_profile_enable",
            "cmsvd_profile_read"]
 
@@ -83,6 +83,8 @@ def load(path: str = LIB_PATH):
     L.cmsvd_cluster_verify.argtypes = [vp, i32, vp, i32, vp, vp, vp]
     L.cmsvd_sym_eigvals.restype = ctypes.c_int
     L.cmsvd_sym_eigvals.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp]
+    L.cmsvd_spectra_diagnostics.restype = ctypes.c_int
+    L.cmsvd_spectra_diagnostics.argtypes = [vp, vp, vp]
     L.cmsvd_launch_count.restype = i64
     L.cmsvd_launch_count.argtypes = [vp]
     L.cmsvd_profile_enable.restype = ctypes.c_int
@@ -177,6 +179,13 @@ class Context:
         cnt = np.zeros(mx, np.int64)
         k = self._L.cmsvd_profile_read(self._h, mx, names, _ptr(ms), _ptr(cnt))
         return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(k)}
+
+    def spectra_diagnostics(self):
+        """(largest Ritz residual, power iterations) of the last big-block (A22) block_spectra."""
+        res = ctypes.c_double()
+        it = ctypes.c_int32()
+        self._check(self._L.cmsvd_spectra_diagnostics(self._h, ctypes.byref(res), ctypes.byref(it)))
+        return res.value, it.value
 
     # -- cmsvd_sym_eigvals (diagnostic) ------------------------------------
     def sym_eigvals(self, mats, kw: int):

@@ -86,6 +86,7 @@ cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
   if (const char* env = getenv("CMSVD_CHASE_FLAGS")) h->c.chase_flags = (env[0] == '1');
   if (const char* env = getenv("CMSVD_EIG_SBR")) h->c.eig_sbr = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_RR")) h->c.eig_rr = !(env[0] == '0');
+  if (const char* env = getenv("CMSVD_SUBSPACE_MAX")) h->c.subspace_max = std::max(0, atoi(env));
   if (const char* env = getenv("CMSVD_SUBSPACE_ITERS")) h->c.subspace_iters = std::max(0, atoi(env));
   *out = h;
   return CMSVD_OK;
@@ -211,6 +212,13 @@ cmsvd_status cmsvd_sym_eigvals(cmsvd_ctx ctx, int32_t count, int32_t nmax, const
   } catch (const std::bad_alloc&) {
     return fail(c, CMSVD_E_NOMEM, "sym_eigvals: host allocation failed");
   }
+}
+
+cmsvd_status cmsvd_spectra_diagnostics(cmsvd_ctx ctx, double* max_ritz_residual, int32_t* power_iterations) {
+  if (!ctx) return CMSVD_E_ARG;
+  if (max_ritz_residual) *max_ritz_residual = ctx->c.big ? ctx->c.spectra_resid : 0.0;
+  if (power_iterations) *power_iterations = ctx->c.big ? ctx->c.spectra_iters : 0;
+  return CMSVD_OK;
 }
 
 int64_t cmsvd_launch_count(cmsvd_ctx ctx) { return ctx ? ctx->c.launches : 0; }

@@ -136,6 +136,9 @@ struct Ctx {
   bool commit_topk = true;             // Alg. 3 commits: top-r eigenpairs by inverse iteration (CMSVD_COMMIT_TOPK=0: QL)
   bool big = false;                    // collection of blocks wider than kEigMax (A22 spectra, full-range bases)
   int subspace_iters = 12;             // power iterations of the big-block spectra (CMSVD_SUBSPACE_ITERS)
+  int subspace_max = 48;               // ... at most, while the Ritz-residual guard fails (CMSVD_SUBSPACE_MAX)
+  double spectra_resid = 0.0;          // largest Ritz residual of the last big-block spectra (diagnostic)
+  int spectra_iters = 0;               // power iterations the last big-block spectra needed
 };
 
 // grow-only device buffer

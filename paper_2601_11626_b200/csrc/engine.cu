@@ -195,6 +195,8 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
                                         " columns must have n_i >= m (A22)");
   const int s = (int)std::min<int64_t>(std::min<int64_t>(m, 2 * (int64_t)r), kEigMax);
   const int kc = (int)std::min<int64_t>(r, m);
+  c.spectra_resid = 0.0;
+  c.spectra_iters = 0;
   if (kc > s)  // the subspace holds s columns: more than s = min(m, 2r, 512) top vectors cannot be returned
     return fail(c, CMSVD_E_SHAPE, "block_spectra: r > " + std::to_string(kEigMax) + " on blocks wider than " +
                                       std::to_string(kEigMax) + " columns");
@@ -246,7 +248,7 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
       CK(ensure(c.ws[WS_B], (size_t)nb * s * s * 8), "spectra: VH");
       CK(ensure(c.ws[WS_EV], (size_t)nb * s * 8), "spectra: ev");
       CK(ensure(c.ws[WS_PERM], (size_t)nb * s * 4), "spectra: perm");
-      CK(ensure(c.ws[WS_STAT], (size_t)nb * 4 * 2 + 64), "spectra: stat");
+      CK(ensure(c.ws[WS_STAT], (size_t)nb * 4 * 2 + (size_t)nb * 8 + 64), "spectra: stat");
       double* Y = (double*)c.ws[WS_A].p;
       double* Z = (double*)c.ws[WS_PAIR].p;
       double* Tmp = (double*)c.ws[WS_OUT].p;
@@ -276,18 +278,21 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
       CK(cudaMemcpyAsync(dids, hid.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
       CK(cudaMemcpyAsync(dns, hns.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
       const int64_t ms = m * s, ns_ = (int64_t)n * s;
-      if (c.big_tc && c.use_tc) {
+      const bool tcp = c.big_tc && c.use_tc;
+      float *Y32 = nullptr, *Z32 = nullptr;
+      GemmDesc *dAtY = nullptr, *dAZ = nullptr;
+      if (tcp) {
         // the products with A on tcgen05 (3xTF32 tiles, fp64 outputs for the fp64 CholQR2); the
         // orthonormal bases enter them rounded to fp32 (a 6e-8 relative perturbation of the basis,
         // which the next power iteration and CholQR absorb; the Rayleigh-Ritz values move by O(u32))
         CK(ensure(c.ws[WS_D], (size_t)nb * (m + n) * s * 4 + (size_t)n * s * 4), "spectra: fp32 bases");
         CK(ensure(c.ws[WS_E], (size_t)3 * nb * sizeof(GemmDesc)), "spectra: descs");
-        float* Y32 = (float*)c.ws[WS_D].p;
-        float* Z32 = Y32 + (size_t)nb * m * s;
+        Y32 = (float*)c.ws[WS_D].p;
+        Z32 = Y32 + (size_t)nb * m * s;
         float* Om32 = Z32 + (size_t)nb * n * s;
         GemmDesc* dAO = (GemmDesc*)c.ws[WS_E].p;
-        GemmDesc* dAtY = dAO + nb;
-        GemmDesc* dAZ = dAtY + nb;
+        dAtY = dAO + nb;
+        dAZ = dAtY + nb;
         std::vector<GemmDesc> hd(3 * (size_t)nb);
         for (int t = 0; t < nb; ++t) {
           GemmDesc g{};
@@ -301,61 +306,120 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
         }
         CK(cudaMemcpyAsync(dAO, hd.data(), hd.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice, c.stream),
            "spectra: h2d");
-        // orthonormalisation once per power step A A^T (the intermediate Z = A^T Y is used as is: the
-        // step's condition number (sigma_1 / sigma_s)^2 stays far inside CholQR's fp64 range), one
-        // CholQR pass inside the loop, CholQR2 for the final basis of the Rayleigh-Ritz step
         CK(launch_to_f32(c, Om, Om32, (int64_t)n * s), "spectra: Omega32");
         CK(launch_gemm_tc_nn64(c, dAO, nb, (int)m, s), "spectra: AO (tc)");
         CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st, 1), "spectra: cholqr");
-        for (int it = 0; it < c.subspace_iters; ++it) {
-          CK(launch_to_f32(c, Y, Y32, (int64_t)nb * ms), "spectra: Y32");
-          CK(launch_gemm_tc(c, dAtY, nb, n, s, false, true), "spectra: AtY (tc)");
-          CK(launch_to_f32(c, Z, Z32, (int64_t)nb * ns_), "spectra: Z32");
-          CK(launch_gemm_tc_nn64(c, dAZ, nb, (int)m, s), "spectra: AZ (tc)");
-          CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st, it + 1 == c.subspace_iters ? 2 : 1), "spectra: cholqr");
-        }
-        CK(launch_to_f32(c, Y, Y32, (int64_t)nb * ms), "spectra: Y32");
-        CK(launch_gemm_tc(c, dAtY, nb, n, s, false, true), "spectra: Bt (tc)");
       } else {
-      // Y = A Omega, orth
-      CK((gemm_mixed<float, false>(c, nb, (int)m, s, n, nullptr, m, 0, Om, n, 0, Y, m, ms, 1.0, dA)), "spectra: AO");
-      CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st), "spectra: cholqr");
-      for (int it = 0; it < c.subspace_iters; ++it) {
-        CK((gemm_mixed<float, true>(c, nb, n, s, (int)m, nullptr, m, 0, Y, m, ms, Z, n, ns_, 1.0, dA)),
-           "spectra: AtY");
-        CK(cholqr(c, nb, n, s, Z, Tmp, H, T, st), "spectra: cholqr");
-        CK((gemm_mixed<float, false>(c, nb, (int)m, s, n, nullptr, m, 0, Z, n, ns_, Y, m, ms, 1.0, dA)),
-           "spectra: AZ");
+        CK((gemm_mixed<float, false>(c, nb, (int)m, s, n, nullptr, m, 0, Om, n, 0, Y, m, ms, 1.0, dA)), "spectra: AO");
         CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st), "spectra: cholqr");
       }
-      // Rayleigh-Ritz: Bt = A^T Q, H = Bt^T Bt
-      CK((gemm_mixed<float, true>(c, nb, n, s, (int)m, nullptr, m, 0, Y, m, ms, Z, n, ns_, 1.0, dA)), "spectra: Bt");
-      }
-      CK((gemm_mixed<double, true>(c, nb, s, s, n, Z, n, ns_, Z, n, ns_, H, s, (int64_t)s * s)), "spectra: H");
-      CK(launch_syev(c, H, s, (int64_t)s * s, dns, nb, s, (double*)c.ws[WS_V].p, (int64_t)s * s,
-                     (double*)c.ws[WS_B].p, (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, s, st + nb),
-         "spectra: eig(H)");
-      {
+      // power steps A A^T (orthonormalised once per step; the intermediate Z = A^T Y is used as is on the
+      // tcgen05 path: the step's condition number (sigma_1 / sigma_s)^2 stays far inside CholQR's fp64
+      // range), CholQR2 for the final basis of each Rayleigh-Ritz step
+      auto power = [&](int iters) -> Status {
+        for (int it = 0; it < iters; ++it) {
+          const int passes = it + 1 == iters ? 2 : 1;
+          if (tcp) {
+            CK(launch_to_f32(c, Y, Y32, (int64_t)nb * ms), "spectra: Y32");
+            CK(launch_gemm_tc(c, dAtY, nb, n, s, false, true), "spectra: AtY (tc)");
+            CK(launch_to_f32(c, Z, Z32, (int64_t)nb * ns_), "spectra: Z32");
+            CK(launch_gemm_tc_nn64(c, dAZ, nb, (int)m, s), "spectra: AZ (tc)");
+          } else {
+            CK((gemm_mixed<float, true>(c, nb, n, s, (int)m, nullptr, m, 0, Y, m, ms, Z, n, ns_, 1.0, dA)),
+               "spectra: AtY");
+            CK(cholqr(c, nb, n, s, Z, Tmp, H, T, st), "spectra: cholqr");
+            CK((gemm_mixed<float, false>(c, nb, (int)m, s, n, nullptr, m, 0, Z, n, ns_, Y, m, ms, 1.0, dA)),
+               "spectra: AZ");
+          }
+          CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st, passes), "spectra: cholqr");
+        }
+        return CMSVD_OK;
+      };
+      // Rayleigh-Ritz: Bt = A^T Q, H = Bt^T Bt = W diag(lambda) W^T, U_r = Q W_r, descriptors
+      auto rayleigh_ritz = [&]() -> Status {
+        if (tcp) {
+          CK(launch_to_f32(c, Y, Y32, (int64_t)nb * ms), "spectra: Y32");
+          CK(launch_gemm_tc(c, dAtY, nb, n, s, false, true), "spectra: Bt (tc)");
+        } else {
+          CK((gemm_mixed<float, true>(c, nb, n, s, (int)m, nullptr, m, 0, Y, m, ms, Z, n, ns_, 1.0, dA)), "spectra: Bt");
+        }
+        CK((gemm_mixed<double, true>(c, nb, s, s, n, Z, n, ns_, Z, n, ns_, H, s, (int64_t)s * s)), "spectra: H");
+        CK(launch_syev(c, H, s, (int64_t)s * s, dns, nb, s, (double*)c.ws[WS_V].p, (int64_t)s * s,
+                       (double*)c.ws[WS_B].p, (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, s, st + nb),
+           "spectra: eig(H)");
         dim3 g((unsigned)((m + 255) / 256), kc, nb);
         k_big_leftvec<<<g, 256, 0, c.stream>>>(m, s, kc, Y, (const double*)c.ws[WS_V].p, (const int*)c.ws[WS_PERM].p,
                                                (float* const*)dU);
         c.launches += 1;
         CK(cudaGetLastError(), "spectra: U_r");
+        k_big_stats<<<(nb + 127) / 128, 128, 0, c.stream>>>(
+            nb, dids, s, r, m, nmax, (const double*)c.ws[WS_EV].p, (const double*)c.d_E.p, d_ncols,
+            (double*)c.d_sig.p, (float*)c.d_sig32.p, (int*)c.d_rank.p, (const float* const*)dU,
+            (const float* const*)dA, (const float* const*)dF, (BaseDesc*)c.d_bdesc.p, (AppDesc*)c.d_adesc_raw.p,
+            (AppDesc*)c.d_adesc_trunc.p);
+        c.launches += 1;
+        CK(cudaGetLastError(), "spectra: stats");
+        return CMSVD_OK;
+      };
+      // a-posteriori accuracy guard: the Ritz residuals rho_l = ||A A^T u_l - lambda_l u_l|| / lambda_l for
+      // l < kc (A A^T u_l = A (Bt w_l), Bt = A^T Q); an eigenvalue of A A^T lies within rho_l lambda_l of
+      // lambda_l, so rho_l <= tol bounds the relative error of sigma_l by tol / 2.  Returns the largest
+      // rho per block in `resid` (host).
+      std::vector<double> resid(nb);
+      auto ritz_check = [&]() -> Status {
+        CK(ensure(c.ws[WS_SBR], (size_t)nb * ((size_t)s * kc + (size_t)n * kc + (size_t)m * kc) * 8 + 64),
+           "spectra: guard");
+        double* Wg = (double*)c.ws[WS_SBR].p;
+        double* BW = Wg + (size_t)nb * s * kc;
+        double* Pm = BW + (size_t)nb * n * kc;
+        CK(launch_ritz_gather(c, nb, s, kc, (const double*)c.ws[WS_V].p, (const int*)c.ws[WS_PERM].p, Wg),
+           "spectra: guard gather");
+        CK((gemm_mixed<double, false>(c, nb, n, kc, s, Z, n, ns_, Wg, s, (int64_t)s * kc, BW, n, (int64_t)n * kc)),
+           "spectra: guard A^T U");
+        CK((gemm_mixed<float, false>(c, nb, (int)m, kc, n, nullptr, m, 0, BW, n, (int64_t)n * kc, Pm, m,
+                                     (int64_t)m * kc, 1.0, dA)),
+           "spectra: guard A A^T U");
+        CK(launch_ritz_resid(c, nb, m, s, kc, Pm, (const double*)c.ws[WS_EV].p, (const float* const*)dU,
+                             (double*)(st + 2 * nb)),
+           "spectra: guard residual");
+        CK(cudaMemcpyAsync(resid.data(), st + 2 * nb, (size_t)nb * 8, cudaMemcpyDeviceToHost, c.stream),
+           "spectra: d2h");
+        return CMSVD_OK;
+      };
+      int done = 0, todo = c.subspace_iters;
+      const int cap = std::max(c.subspace_iters, c.subspace_max);
+      for (;;) {
+        Status sp = power(todo);
+        if (sp != CMSVD_OK) return sp;
+        done += todo;
+        sp = rayleigh_ritz();
+        if (sp != CMSVD_OK) return sp;
+        sp = ritz_check();
+        if (sp != CMSVD_OK) return sp;
+        std::vector<int> stat(nb);
+        CK(cudaMemcpyAsync(stat.data(), st + nb, (size_t)nb * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
+        CK(cudaStreamSynchronize(c.stream), "spectra: sync");
+        for (int t = 0; t < nb; ++t)
+          if (stat[t] < 0)
+            return fail(c, CMSVD_E_NOCONV, "block_spectra: QL did not converge on the Rayleigh-Ritz matrix of block " +
+                                               std::to_string(hid[t]) + " (" + std::to_string(s) + "x" +
+                                               std::to_string(s) + ")");
+        int worst = 0;
+        for (int t = 1; t < nb; ++t)
+          if (!(resid[t] <= resid[worst])) worst = t;
+        c.spectra_iters = std::max(c.spectra_iters, done);
+        if (resid[worst] <= kRitzTol) {
+          c.spectra_resid = std::max(c.spectra_resid, resid[worst]);   // the accepted (final) residuals
+          break;
+        }
+        if (done >= cap) {
+          char buf[160];
+          snprintf(buf, sizeof(buf), " after %d power iterations: Ritz residual %.3g > %.1g (block %d, %dx%d)", done,
+                   resid[worst], kRitzTol, hid[worst], (int)m, n);
+          return fail(c, CMSVD_E_NOCONV, std::string("block_spectra: subspace iteration not converged") + buf);
+        }
+        todo = std::min(cap - done, std::max(4, c.subspace_iters / 2));
       }
-      k_big_stats<<<(nb + 127) / 128, 128, 0, c.stream>>>(
-          nb, dids, s, r, m, nmax, (const double*)c.ws[WS_EV].p, (const double*)c.d_E.p, d_ncols, (double*)c.d_sig.p,
-          (float*)c.d_sig32.p, (int*)c.d_rank.p, (const float* const*)dU, (const float* const*)dA,
-          (const float* const*)dF, (BaseDesc*)c.d_bdesc.p, (AppDesc*)c.d_adesc_raw.p, (AppDesc*)c.d_adesc_trunc.p);
-      c.launches += 1;
-      CK(cudaGetLastError(), "spectra: stats");
-      std::vector<int> stat(nb);
-      CK(cudaMemcpyAsync(stat.data(), st + nb, (size_t)nb * 4, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
-      CK(cudaStreamSynchronize(c.stream), "spectra: sync");
-      for (int t = 0; t < nb; ++t)
-        if (stat[t] < 0)
-          return fail(c, CMSVD_E_NOCONV, "block_spectra: QL did not converge on the Rayleigh-Ritz matrix of block " +
-                                             std::to_string(hid[t]) + " (" + std::to_string(s) + "x" +
-                                             std::to_string(s) + ")");
     }
     g0 = g1;
   }

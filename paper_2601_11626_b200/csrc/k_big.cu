@@ -303,6 +303,56 @@ __global__ void k_big_stats(int nb, const int* __restrict__ ids, int s, int r, i
   ad_trunc[i] = a;
 }
 
+// Ritz-residual guard (engine.cu do_block_spectra_big)
+__global__ void k_ritz_gather(int s, int kc, const double* __restrict__ V, const int* __restrict__ perm,
+                              double* __restrict__ Wg) {
+  const int b = blockIdx.y;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < s * kc; e += gridDim.x * blockDim.x) {
+    const int l = e / s, k = e - l * s;
+    Wg[(int64_t)b * s * kc + e] = V[(int64_t)b * s * s + (int64_t)perm[(int64_t)b * s + l] * s + k];
+  }
+}
+
+cudaError_t launch_ritz_gather(Ctx& c, int nb, int s, int kc, const double* V, const int* perm, double* Wg) {
+  k_ritz_gather<<<dim3(std::max(1, std::min(64, (s * kc + 255) / 256)), nb), 256, 0, c.stream>>>(s, kc, V, perm, Wg);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+// one CTA per block: rho_l = ||P_l - lambda_l U_l|| / lambda_l (columns with lambda_l <= 1e-12 lambda_0, i.e.
+// numerically zero singular values of a rank-deficient square block, are measured against lambda_0)
+__global__ void __launch_bounds__(256) k_ritz_resid(int64_t m, int s, int kc, const double* __restrict__ P,
+                                                    const double* __restrict__ ev, const float* const* __restrict__ U,
+                                                    double* __restrict__ resid) {
+  __shared__ double red[8];
+  const int b = blockIdx.x;
+  const double* e = ev + (int64_t)b * s;
+  const double lam0 = fmax(e[0], 1e-300);
+  double worst = 0.0;
+  for (int l = 0; l < kc; ++l) {
+    const double lam = e[l];
+    const double* p = P + ((int64_t)b * kc + l) * m;
+    const float* u = U[b] + (int64_t)l * m;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const double d = p[i] - lam * (double)u[i];
+      acc = fma(d, d, acc);
+    }
+    const double tot = block_sum(acc, red);
+    const double rho = sqrt(tot) / fmax(lam, 1e-12 * lam0);
+    worst = fmax(worst, rho);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) resid[b] = worst;
+}
+
+cudaError_t launch_ritz_resid(Ctx& c, int nb, int64_t m, int s, int kc, const double* P, const double* ev,
+                              const float* const* U, double* resid) {
+  k_ritz_resid<<<nb, 256, 0, c.stream>>>(m, s, kc, P, ev, U, resid);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 // Explicit instantiations used by the engine
 template cudaError_t gemm_mixed<float, false>(Ctx&, int, int, int, int, const float*, int64_t, int64_t,
                                               const double*, int64_t, int64_t, double*, int64_t, int64_t, double,

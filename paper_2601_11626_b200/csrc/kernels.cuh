@@ -88,6 +88,12 @@ __global__ void k_big_stats(int nb, const int* ids, int s, int r, int64_t m, int
                             const float* const* Uptr, const float* const* Aptr, const float* const* Fptr,
                             BaseDesc* bd, AppDesc* ad_raw, AppDesc* ad_trunc);
 cudaError_t launch_randn(Ctx& c, double* X, int64_t n, uint64_t seed);
+// Ritz-residual guard of the big-block spectra: Wg[b] = V[b][:, perm[b][0..kc)] (s x kc), and
+// resid[b] = max_{l<kc} ||P[b][:, l] - lambda_l U[b][:, l]|| / lambda_l
+constexpr double kRitzTol = 1e-4;
+cudaError_t launch_ritz_gather(Ctx& c, int nb, int s, int kc, const double* V, const int* perm, double* Wg);
+cudaError_t launch_ritz_resid(Ctx& c, int nb, int64_t m, int s, int kc, const double* P, const double* ev,
+                              const float* const* U, double* resid);
 cudaError_t cholqr(Ctx& c, int batch, int64_t rows, int s, double* Y, double* Ytmp, double* H, double* T,
                    int* status, int passes = 2);
 __global__ void k_trunc_operand(int64_t m, const BaseDesc* bd, const AppDesc* ad_trunc, float* Fbase);

@@ -176,3 +176,51 @@ def test_c4_reduced_wide_operands(cm, tc_big, monkeypatch):
     sp, E, sig, rank, pairs, out = run_pairs(cm, col, r)
     orc = oracle.pair_errors(sp, pairs, r, 7, oracle.TRUNC)
     compare(out, orc, 7, f"config4-reduced r=192 tc_big={tc_big}")
+
+
+def _flat_block(R, m, decay):
+    U = np.linalg.qr(R.standard_normal((m, m)))[0]
+    V = np.linalg.qr(R.standard_normal((m, m)))[0]
+    s = np.exp(-decay * np.arange(m))
+    return ((U * s) @ V.T).astype(np.float32)
+
+
+def test_a22_guard_catches_unresolved_spectrum(cm, monkeypatch):
+    """Reading A22's subspace iteration carries an a-posteriori guard: the Ritz residuals
+    ||A A^T u_l - lambda_l u_l|| / lambda_l of the returned l < r must be <= 1e-4 (which bounds the relative
+    error of sigma_l by 5e-5), else more power iterations run, and CMSVD_E_NOCONV after
+    CMSVD_SUBSPACE_MAX.  A spectrum sigma_l = exp(-0.006 l) around r = 32 (s = 64: convergence factor
+    (sigma_65 / sigma_32)^2 = 0.67 per step) cannot be resolved by 2 iterations -> NOCONV, not a silent
+    result; with the defaults (12, up to 48) the guard extends the iteration and the result matches the
+    oracle's exact spectrum."""
+    R = np.random.default_rng(21)
+    m, r = 640, 32
+    blocks = np.stack([_flat_block(R, m, 0.006).T for _ in range(2)])
+    monkeypatch.setenv("CMSVD_SUBSPACE_ITERS", "2")
+    monkeypatch.setenv("CMSVD_SUBSPACE_MAX", "2")
+    with cm.Context(0) as ctx:
+        ctx.register(blocks)
+        with pytest.raises(cm.CmsvdError) as ei:
+            ctx.block_spectra(r)
+        assert ei.value.status == 5   # CMSVD_E_NOCONV
+    monkeypatch.delenv("CMSVD_SUBSPACE_ITERS")
+    monkeypatch.delenv("CMSVD_SUBSPACE_MAX")
+    sp = oracle.block_spectra(blocks, nvec=r)
+    with cm.Context(0) as ctx:
+        ctx.register(blocks)
+        E, sig, rank = ctx.block_spectra(r)
+        resid, iters = ctx.spectra_diagnostics()
+    assert resid <= 1e-4 and iters > 12, (resid, iters)
+    ref = np.stack([s_[:r] for s_ in sp.sig])
+    assert_sigma(sig, ref, ref[:, 0], "flat-spectrum block sigma")
+
+
+@pytest.mark.parametrize("name", ["config3", "config4"])
+def test_a22_guard_quiet_on_bench_configs(cm, name):
+    """On BASELINE.json's configs 3 and 4 the default 12 power iterations already pass the guard."""
+    col = synth.make_config(name, N=4) if name == "config3" else synth.config4(N=4)
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        ctx.block_spectra(col.r)
+        resid, iters = ctx.spectra_diagnostics()
+    assert resid <= 1e-4 and iters == 12, (resid, iters)

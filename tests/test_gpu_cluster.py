@@ -295,3 +295,27 @@ def test_c2_commit_reuse_matches_full_commit(cm, knn, monkeypatch):
     a, b = res
     assert np.array_equal(np.asarray(a["assign"]), np.asarray(b["assign"]))
     assert np.allclose(a["err2"], b["err2"], rtol=1e-6, atol=1e-9 * float(np.max(b["total"])))
+
+
+@pytest.mark.parametrize("alg", [oc.RESIDUAL_ALG, oc.APPROX])
+@pytest.mark.parametrize("sort", [oc.SORT_FROBENIUS, oc.SORT_RESIDUAL])
+@pytest.mark.parametrize("eps", [0.02, 0.05, 0.1])
+def test_c2_full_size_greedy_grid(cm, alg, sort, eps):
+    """BASELINE.json config 2 at full size, every eps it is quoted with, Algs. 2 and 3 x both sort modes:
+    decision replay of the GPU run in the oracle (A12), and Alg. 1 exact."""
+    col = synth.config2()
+    sp = _c2_spectra()
+    g = run_gpu(cm, col.blocks, col.r, alg, eps, sort)
+    replay(sp, g, alg, col.r, eps, sort)
+    assert sum(len(c) for c in g["clusters"]) == col.N
+    g1 = run_gpu(cm, col.blocks, col.r, cm.ALG_MAX_NORM, eps, 0)
+    assert g1["clusters"] == oc.cluster(sp, oc.MAX_NORM, col.r, eps).clusters
+
+
+_C2 = {}
+
+
+def _c2_spectra():
+    if "sp" not in _C2:
+        _C2["sp"] = oracle.block_spectra(synth.config2().blocks)
+    return _C2["sp"]

@@ -1,0 +1,135 @@
+"""Full-size parity against cached float64 oracle results (-m gpu).
+
+The expected values in tests/oracle_cache/*.npz were written by tools/make_oracle_cache.py, which calls
+only oracle/ (the float64 CPU oracle) and synth/ (seeded generators) -- nothing from the CUDA path.  The
+GPU recomputes the same seeded collections here and is compared element by element on EVERY cached pair
+(north_star tolerances, tests/tolerances.py): BASELINE.json's configs 2 (all 8128 pairs), 4 (all 2016
+TRUNC pairs, the bench workload and launch configuration) and 5 (N in {512, 2048} x r in {16, 64}, the
+N*16 seeded candidate pairs), and the greedy drivers' cluster assignments at full size on configs 3, 4
+and 5 (reading A12: identical partitions; the oracle's merges on these inputs lie far from eps).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from tolerances import assert_err2, assert_sigma
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+CACHE = os.path.join(os.path.dirname(__file__), "oracle_cache")
+
+
+def load(name):
+    path = os.path.join(CACHE, name + ".npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing oracle cache {path} (python tools/make_oracle_cache.py)")
+    return np.load(path)
+
+
+@pytest.fixture(scope="module")
+def cm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_11626_b200 as cm
+    cm.load()
+    return cm
+
+
+def gpu_pairs(cm, col, pairs, r, operand):
+    """The bench launch configuration: device-resident collection, pairs and outputs."""
+    dev = torch.device("cuda", 0)
+    P = pairs.shape[0]
+    with cm.Context(0, torch.cuda.current_stream().cuda_stream) as ctx:
+        ctx.register(torch.from_numpy(col.blocks).to(dev))
+        E, sig, rank = ctx.block_spectra(r)
+        out = {"err2": torch.empty((P, 3), dtype=torch.float64, device=dev),
+               "total": torch.empty(P, dtype=torch.float64, device=dev),
+               "sigma_tilde": torch.empty((P, r), dtype=torch.float32, device=dev),
+               "mu": torch.empty((P, r), dtype=torch.float32, device=dev)}
+        ctx.pair_errors(torch.from_numpy(np.ascontiguousarray(pairs, np.int32)).to(dev), out=out, operand=operand)
+        torch.cuda.synchronize()
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+    return E, sig, res
+
+
+def compare(name, ref, E, sig, res, check_mu=True):
+    assert np.allclose(E, ref["E"], rtol=1e-12), f"{name}: energies"
+    assert_sigma(sig, ref["sig"], ref["sig"][:, 0], f"{name}: block sigma_1..r")
+    assert np.allclose(res["total"], ref["total"], rtol=1e-12)
+    for k, kind in enumerate(["weyl", "residual", "incremental"]):
+        assert_err2(res["err2"][:, k], ref["err2"][:, k], ref["total"], f"{name}: {kind}")
+    st = ref["sigma_tilde"].astype(np.float64)
+    assert_sigma(res["sigma_tilde"], st, st[:, 0], f"{name}: sigma~")
+    if check_mu:
+        mu = ref["mu"].astype(np.float64)
+        assert_sigma(res["mu"], mu, mu[:, 0], f"{name}: mu")
+
+
+def test_config2_all_pairs(cm):
+    ref = load("config2_pairs")
+    col = synth.config2()
+    E, sig, res = gpu_pairs(cm, col, ref["pairs"], col.r, cm.RAW)
+    compare("config2 (8128 pairs)", ref, E, sig, res)
+
+
+@pytest.mark.parametrize("N,r", [(512, 16), (512, 64), (2048, 16), (2048, 64)])
+def test_config5_candidate_pairs(cm, N, r):
+    ref = load(f"config5_N{N}_r{r}")
+    col = synth.config5(N=N, r=r)
+    E, sig, res = gpu_pairs(cm, col, ref["pairs"], r, cm.RAW)
+    compare(f"config5 N={N} r={r} ({ref['pairs'].shape[0]} pairs)", ref, E, sig, res)
+
+
+def test_config4_all_pairs(cm):
+    """The headline workload: 64 x 4096^2, r = 256, TRUNC operand, all 2016 pairs, all three estimators
+    (the residual's mu is the base block's top-r spectrum under reading A22)."""
+    ref = load("config4_pairs")
+    col = synth.config4()
+    E, sig, res = gpu_pairs(cm, col, ref["pairs"], col.r, cm.TRUNC)
+    compare("config4 (2016 pairs)", ref, E, sig, res)
+
+
+def _partition(assign):
+    return sorted(sorted(np.flatnonzero(assign == c).tolist()) for c in np.unique(assign))
+
+
+def _check_greedy(cm, col, r, cache, key, alg, sort, eps, knn, operand):
+    with cm.Context(0) as ctx:
+        ctx.register(torch.from_numpy(col.blocks).cuda())
+        ctx.block_spectra(r)
+        g = ctx.cluster(alg, eps, sort=sort, knn=knn, operand=operand)
+    ref_assign = cache[key + "_assign"]
+    assert _partition(np.asarray(g["assign"])) == _partition(ref_assign), key
+    assert np.array_equal(np.asarray(g["assign"]), ref_assign), key            # same creation order
+    assert np.array_equal(np.asarray(g["order"]), cache[key + "_order"]), key  # same append order
+    assert g["n_evals"] == int(cache[key + "_nevals"]), key
+    rel_g = np.sqrt(np.asarray(g["err2"]) / np.asarray(g["total"]))
+    rel_o = np.sqrt(cache[key + "_err2"] / cache[key + "_total"])
+    assert np.allclose(rel_g, rel_o, rtol=1e-3, atol=1e-6), key
+    return g
+
+
+def test_config4_greedy_alg3(cm):
+    """Alg. 3, residual sort, eps = 0.15, TRUNC: 4 clusters of 16 (the 4 layer groups)."""
+    cache = load("greedy_config4")
+    col = synth.config4()
+    g = _check_greedy(cm, col, col.r, cache, "a2_s1_e0.15_k1", cm.ALG_APPROX, cm.SORT_RESIDUAL, 0.15, 1, cm.TRUNC)
+    assert len(g["clusters"]) == 4
+
+
+@pytest.mark.parametrize("key,sort,eps", [("a2_s1_e0.1_k1", 1, 0.1), ("a2_s1_e0.3_k1", 1, 0.3),
+                                          ("a2_s0_e0.3_k1", 0, 0.3)])
+def test_config3_greedy_alg3(cm, key, sort, eps):
+    cache = load("greedy_config3")
+    col = synth.config3()
+    _check_greedy(cm, col, col.r, cache, key, cm.ALG_APPROX, sort, eps, 1, cm.TRUNC)
+
+
+@pytest.mark.parametrize("N,r", [(512, 16), (512, 64), (2048, 16)])
+def test_config5_greedy_knn(cm, N, r):
+    cache = load(f"greedy_config5_N{N}_r{r}")
+    col = synth.config5(N=N, r=r)
+    _check_greedy(cm, col, r, cache, "a2_s1_e0.1_k16", cm.ALG_APPROX, cm.SORT_RESIDUAL, 0.1, 16, cm.RAW)
