@@ -25,10 +25,13 @@
 // Outputs: those of k_tridiag (diagonal, squared sub-diagonal, Gershgorin data, count above the
 // threshold, trace) so that the same bisection kernels follow.
 #include <algorithm>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 #include "engine.h"
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace cmsvd {
 
@@ -420,107 +423,393 @@ __global__ void __launch_bounds__(kSyrThreads, 2) k_sbr_syr2k(double* __restrict
 }
 
 // ---------------------------------------------------------------------------
+// Stage 1d (TMA variant): the 64 x 64 lower tile arrives by one cp.async.bulk.tensor (3-D tensor map over
+// the batch of Grams: rows, columns, problem), is updated in shared memory, and leaves by a bulk tensor
+// store -- no registers are held across the global latency, so more CTAs fit per SM.  Elements outside
+// the problem's n (the box crosses n or the padded leading dimension) are zero-filled on load and land
+// in the unused padding on store; in diagonal tiles only the lower triangle is updated.
+// ---------------------------------------------------------------------------
+using tc::smem_u32;
+using tc::mbar_init;
+using tc::fence_mbar_init;
+using tc::mbar_wait;
+using tc::fence_proxy_async;
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+               ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kSyrThreads) k_sbr_syr2k_tma(const __grid_constant__ CUtensorMap tmap,
+                                                                  const int* __restrict__ ns, int t,
+                                                                  const double* __restrict__ ws) {
+  extern __shared__ __align__(128) double tsm[];
+  double* At = tsm;                                   // [64 cols][64 rows] (TMA box, dense)
+  double* VI = At + kSyrTile * kSyrTile;
+  double* WI = VI + kSB * kSyrTile;
+  double* VJ = WI + kSB * kSyrTile;
+  double* WJ = VJ + kSB * kSyrTile;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(WJ + kSB * kSyrTile);
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int nt = (np + kSyrTile - 1) / kSyrTile;
+  int q = blockIdx.y, ti = 0;
+  while (q > ti) { ++ti; q -= ti; }
+  const int tj = q;
+  if (ti >= nt) return;
+  const int I0 = ti * kSyrTile, J0 = tj * kSyrTile;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"((unsigned)(kSyrTile * kSyrTile * sizeof(double)))
+                 : "memory");
+    tma_load_3d(At, &tmap, R0 + I0, R0 + J0, p, bar);
+  }
+  const double* Vw = ws + (int64_t)p * kSbrPer;
+  const double* Ww = Vw + kSbrV;
+  for (int e = tid; e < kSyrTile * kSB; e += kSyrThreads) {
+    const int l = e >> 6, i = e & 63;
+    const int gi = I0 + i, gj = J0 + i;
+    VI[e] = gi < np ? Vw[(int64_t)l * kSBMax + gi] : 0.0;
+    WI[e] = gi < np ? Ww[(int64_t)l * kSBMax + gi] : 0.0;
+    VJ[e] = gj < np ? Vw[(int64_t)l * kSBMax + gj] : 0.0;
+    WJ[e] = gj < np ? Ww[(int64_t)l * kSBMax + gj] : 0.0;
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  const int tx = tid & 31, ty = tid >> 5;
+  const bool diag = ti == tj;
+  double a[2][8];
+#pragma unroll
+  for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) a[r2][c] = At[(8 * ty + c) * kSyrTile + tx + 32 * r2];
+#pragma unroll 4
+  for (int l = 0; l < kSB; ++l) {
+    const double vi0 = VI[l * kSyrTile + tx], vi1 = VI[l * kSyrTile + tx + 32];
+    const double wi0 = WI[l * kSyrTile + tx], wi1 = WI[l * kSyrTile + tx + 32];
+    const double2* vj2 = reinterpret_cast<const double2*>(VJ + l * kSyrTile + 8 * ty);
+    const double2* wj2 = reinterpret_cast<const double2*>(WJ + l * kSyrTile + 8 * ty);
+#pragma unroll
+    for (int c2 = 0; c2 < 4; ++c2) {
+      const double2 vj = vj2[c2], wj = wj2[c2];
+      a[0][2 * c2] = fma(-vi0, wj.x, fma(-wi0, vj.x, a[0][2 * c2]));
+      a[1][2 * c2] = fma(-vi1, wj.x, fma(-wi1, vj.x, a[1][2 * c2]));
+      a[0][2 * c2 + 1] = fma(-vi0, wj.y, fma(-wi0, vj.y, a[0][2 * c2 + 1]));
+      a[1][2 * c2 + 1] = fma(-vi1, wj.y, fma(-wi1, vj.y, a[1][2 * c2 + 1]));
+    }
+  }
+#pragma unroll
+  for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int i = tx + 32 * r2, j = 8 * ty + c;
+      if (!diag || i >= j) At[j * kSyrTile + i] = a[r2][c];
+    }
+  fence_proxy_async();     // generic-proxy smem writes visible to the bulk copy
+  __syncthreads();
+  if (tid == 0) {
+    tma_store_3d(&tmap, R0 + I0, R0 + J0, p, At);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1b (TMA variant).  Slices below the diagonal block (all i >= j) arrive as one 128 x 32 box of the
+// lower storage (dense [j][i] in shared memory); slices right of it (all i < j, A22(i, j) = G(j, i)) as two
+// 16 x 128 boxes of the transposed region with the 128-byte swizzle, so that reading a row i of the slice
+// (16-byte pairs (j, j+1)) is conflict-free; slices crossing the diagonal are copied element-wise by
+// cp.async.  Two stages in flight; the V slices (32 x 16) follow by cp.async.
+// ---------------------------------------------------------------------------
+constexpr int kSymmA = kSymmJB * kSymmRows;    // doubles per A slice (32 KB)
+constexpr int kSymmStage = kSymmA + kSymmJB * kSB;   // + V slice (4 KB)
+
+__global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_tma(const __grid_constant__ CUtensorMap tlo,
+                                                                    const __grid_constant__ CUtensorMap tup,
+                                                                    const double* __restrict__ G, int64_t ld,
+                                                                    int64_t stride, const int* __restrict__ ns,
+                                                                    int t, double* __restrict__ ws) {
+  extern __shared__ __align__(1024) double ysm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ysm + 2 * kSymmStage);
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int I0 = blockIdx.y * kSymmRows;
+  if (I0 >= np) return;
+  const int tid = threadIdx.x;
+  const double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;   // A22(i, j) at A[j * ld + i]
+  const double* Vw = ws + (int64_t)p * kSbrPer;
+  double* Yw = const_cast<double*>(Vw) + kSbrV;
+  const int i0 = tid & 63, h = tid >> 6;
+  const int imax = min(kSymmRows, np - I0);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto kind = [&](int J0) {
+    const int jmax = min(kSymmJB, np - J0);
+    return (J0 + jmax - 1 <= I0) ? 0 : ((I0 + imax - 1 < J0) ? 1 : 2);
+  };
+  auto issue = [&](int J0, int st) {
+    double* As = ysm + st * kSymmStage;
+    double* Vs = As + kSymmA;
+    const int jmax = min(kSymmJB, np - J0);
+    const int kd = kind(J0);
+    if (kd == 2) {
+      for (int e = tid; e < kSymmJB * kSymmRows; e += kSymmThreads) {
+        const int jj = e >> 7, ii = e & 127;
+        const bool ok = jj < jmax && ii < imax;
+        const int gi = I0 + ii, gj = J0 + jj;
+        const double* src = !ok ? A : (gi >= gj ? A + (int64_t)gj * ld + gi : A + (int64_t)gi * ld + gj);
+        cp_async8(As + jj * kSymmRows + ii, src, ok);
+      }
+    } else if (tid == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[st])),
+                   "r"((unsigned)(kSymmA * sizeof(double)))
+                   : "memory");
+      if (kd == 0) {
+        tma_load_3d(As, &tlo, R0 + I0, R0 + J0, p, &bars[st]);
+      } else {
+        tma_load_3d(As, &tup, R0 + J0, R0 + I0, p, &bars[st]);
+        tma_load_3d(As + kSymmA / 2, &tup, R0 + J0 + 16, R0 + I0, p, &bars[st]);
+      }
+    }
+    for (int e = tid; e < kSymmJB * kSB; e += kSymmThreads) {
+      const int jj = e >> 4, c = e & 15;
+      const bool ok = jj < jmax;
+      cp_async8(Vs + e, ok ? Vw + (int64_t)c * kSBMax + J0 + jj : Vw, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[2][8];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
+  const int nsl = (np + kSymmJB - 1) / kSymmJB;
+  unsigned uses = 0;   // TMA completions consumed per stage (bit st: parity of the next wait)
+  issue(0, 0);
+  for (int k = 0; k < nsl; ++k) {
+    const int st = k & 1;
+    const int J0 = k * kSymmJB;
+    if (k + 1 < nsl) {
+      issue((k + 1) * kSymmJB, (k + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    const int kd = kind(J0);
+    if (kd != 2) {
+      mbar_wait(&bars[st], (uses >> st) & 1u);
+      uses ^= 1u << st;
+    }
+    __syncthreads();
+    const double* As = ysm + st * kSymmStage;
+    const double* Vs = As + kSymmA;
+    const int jmax = min(kSymmJB, np - J0);
+    if (kd != 1) {
+      for (int jj = 0; jj < jmax; ++jj) {
+        const double a0 = As[jj * kSymmRows + i0], a1 = As[jj * kSymmRows + i0 + 64];
+        const double2* vr = reinterpret_cast<const double2*>(Vs + jj * kSB + 8 * h);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 v = vr[q];
+          acc[0][2 * q] = fma(a0, v.x, acc[0][2 * q]);
+          acc[0][2 * q + 1] = fma(a0, v.y, acc[0][2 * q + 1]);
+          acc[1][2 * q] = fma(a1, v.x, acc[1][2 * q]);
+          acc[1][2 * q + 1] = fma(a1, v.y, acc[1][2 * q + 1]);
+        }
+      }
+    } else {
+      // swizzled rows: A22(i, J0 + 2 kp .. + 1) at box (kp >> 3), row i, 16-byte chunk (kp & 7) ^ (i & 7)
+      const int sw = i0 & 7;
+      for (int kp = 0; 2 * kp < jmax; ++kp) {
+        const double* box = As + (kp >> 3) * (kSymmA / 2);
+        const int ch = ((kp & 7) ^ sw) << 1;
+        double2 a0 = *reinterpret_cast<const double2*>(box + i0 * 16 + ch);
+        double2 a1 = *reinterpret_cast<const double2*>(box + (i0 + 64) * 16 + ch);
+        if (2 * kp + 1 >= jmax) { a0.y = 0.0; a1.y = 0.0; }
+        const double2* v0 = reinterpret_cast<const double2*>(Vs + (2 * kp) * kSB + 8 * h);
+        const double2* v1 = reinterpret_cast<const double2*>(Vs + (2 * kp + 1) * kSB + 8 * h);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 x = v0[q], y = v1[q];
+          acc[0][2 * q] = fma(a0.y, y.x, fma(a0.x, x.x, acc[0][2 * q]));
+          acc[0][2 * q + 1] = fma(a0.y, y.y, fma(a0.x, x.y, acc[0][2 * q + 1]));
+          acc[1][2 * q] = fma(a1.y, y.x, fma(a1.x, x.x, acc[1][2 * q]));
+          acc[1][2 * q + 1] = fma(a1.y, y.y, fma(a1.x, x.y, acc[1][2 * q + 1]));
+        }
+      }
+    }
+    __syncthreads();   // this stage is reissued at step k + 2
+  }
+  // X rows to shared memory (row stride 17), then Y = X T and M_b = V_b^T Y_b
+  constexpr int kX = kSB + 1;
+  double* Xs = ysm;
+  double* Ts = Xs + kSymmRows * kX;
+  double* Ys = Ts + kSB * kSB;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) Xs[(i0 + 64 * a) * kX + 8 * h + c] = acc[a][c];
+  const double* Tw = Vw + 2 * kSbrV;
+  for (int e = tid; e < kSB * kSB; e += kSymmThreads) Ts[e] = Tw[e];
+  __syncthreads();
+  for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
+    const int c = e >> 7, i = e & 127;
+    double y = 0.0;
+    for (int l = 0; l <= c; ++l) y = fma(Xs[i * kX + l], Ts[l * kSB + c], y);
+    Ys[i * kX + c] = (i < imax) ? y : 0.0;
+    if (i < imax) Yw[(int64_t)c * kSBMax + I0 + i] = y;
+  }
+  __syncthreads();
+  double* Mw = const_cast<double*>(Vw) + 2 * kSbrV + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
+  for (int e = tid; e < kSB * kSB; e += kSymmThreads) {
+    const int a = e >> 4, c = e & 15;
+    double s = 0.0;
+    for (int i = 0; i < imax; ++i) s = fma(Vw[(int64_t)a * kSBMax + I0 + i], Ys[i * kX + c], s);
+    Mw[e] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Stage 2: bulge chasing on the band, one CTA per problem.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double& bat(double* Bd, int i, int j) { return Bd[j * kSBLdb + (i - j)]; }  // i >= j
 
 // task (j, s) of sweep j on the band Bd (n x n), executed by one warp
-__device__ __forceinline__ void chase_task(double* __restrict__ Bd, int n, int j, int s) {
+// Band storage: element (i, j), i >= j, at Bd[j * kSBLdb + (i - j)] = Bd[j * (kSBLdb - 1) + i].
+constexpr int kSBRow = kSBLdb - 1;   // stride between (i, j) and (i, j + 1)
+
+// Task (j, s) of sweep j on the band Bd (n x n), executed by one warp; ps: 16 doubles of per-warp scratch.
+// Lane (l16, hh) holds row / column l16 of the three 16 x 16 blocks the task updates (B: left-applied,
+// s >= 1; D: two-sided; C: right-applied) at entries l = 8 hh + q.  The latency chain is kept short: the
+// products with the Householder vector v = (1, x_1 .. x_{L-1}) * scale are formed from x before the
+// reflector's scalars are known (v^T y = y_0 + scale * sum_{l>=1} x_l y_l), the squared norm from the two
+// half-sums, and p = tau D v is broadcast through shared memory while K = tau/2 p.v is reduced.
+template <bool FULL>
+__device__ __forceinline__ void chase_task_t(double* __restrict__ Bd, double* __restrict__ ps, int j, int s, int L,
+                                             int L2) {
   const int lane = threadIdx.x & 31;
   const int r = j + 1 + s * kSB;
-  const int L = min(kSB, n - r);
-  const int cx = (s == 0) ? j : r - kSB;    // column holding the vector to annihilate (rows r .. r + L - 1)
+  const int cx = (s == 0) ? j : r - kSB;    // column holding x (rows r .. r + L - 1)
   const int l16 = lane & 15, hh = lane >> 4;
   const int r2 = r + L;
-  const int L2 = min(kSB, n - r2);
-  // every load of the task first (the three blocks it updates are disjoint): B (s >= 1, left-apply),
-  // D (two-sided), C (right-apply); lane (l16, hh) holds column / row l16 and the 8 entries 8 hh .. 8 hh + 7
-#ifdef CMSVD_CHASE_PROF
-  long long ck0 = clock64();
-#endif
-  double x = (lane < L) ? bat(Bd, r + lane, cx) : 0.0;
-  double b[8], dd[8], cr[8];
+  const double* px = Bd + cx * kSBRow + r;
+  double* pB = Bd + (cx + l16) * kSBRow + r + 8 * hh;          // B[l][c = l16]   at pB[q]
+  double* pDlo = Bd + (r + 8 * hh) * kSBRow + r + l16;          // D[a = l16][l], a >= l, at pDlo[q * kSBRow]
+  double* pDup = Bd + (r + l16) * kSBRow + r + 8 * hh;          // D[l][a = l16], l > a,  at pDup[q]
+  double* pC = Bd + (r + 8 * hh) * kSBRow + r2 + l16;           // C[a = l16][l]   at pC[q * kSBRow]
+  double xl[8], b[8], dd[8], cr[8];
+  const double alpha = px[0];
+  const double xa = (l16 < L) ? px[l16] : 0.0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int l = 8 * hh + q;
-    b[q] = (s > 0 && l < L) ? bat(Bd, r + l, cx + l16) : 0.0;               // B[l][c = l16]
-    dd[q] = (l16 < L && l < L) ? (l16 >= l ? bat(Bd, r + l16, r + l) : bat(Bd, r + l, r + l16)) : 0.0;  // D[a][l]
-    cr[q] = (l16 < L2 && l < L) ? bat(Bd, r2 + l16, r + l) : 0.0;           // C[a][l]
+    if (FULL) {
+      xl[q] = px[l];
+      b[q] = s > 0 ? pB[q] : 0.0;
+      dd[q] = (l16 >= l) ? pDlo[q * kSBRow] : pDup[q];
+      cr[q] = pC[q * kSBRow];
+    } else {
+      xl[q] = (l < L) ? px[l] : 0.0;
+      b[q] = (s > 0 && l < L) ? pB[q] : 0.0;
+      dd[q] = (l16 < L && l < L) ? ((l16 >= l) ? pDlo[q * kSBRow] : pDup[q]) : 0.0;
+      cr[q] = (l16 < L2 && l < L) ? pC[q * kSBRow] : 0.0;
+    }
   }
-  double sq = (lane >= 1 && lane < L) ? x * x : 0.0;
-  sq = warp_sum(sq);
-  const double alpha = __shfl_sync(0xffffffffu, x, 0);
-  double tau = 0.0, beta = alpha, scale = 0.0;
-  if (sq > 0.0) {
-    const double x2 = fma(alpha, alpha, sq);
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x2));
-    const double e = fma(-(x2 * y), y, 1.0);
-    y = fma(y * e, fma(e, 0.375, 0.5), y);
-    const double xn = x2 * y;
-    beta = alpha >= 0.0 ? -xn : xn;
-    tau = (beta - alpha) * sbr_rcp(beta);
-    scale = sbr_rcp(alpha - beta);
-  }
-#ifdef CMSVD_CHASE_PROF
-  long long ck1 = clock64();
-#endif
-  if (tau == 0.0) return;   // H = I (x is already beta e_0): nothing to apply (warp-uniform)
-  // v by lane: vh[q] = v[8 hh + q], va = v[l16]
-  const double vmine = (lane == 0) ? 1.0 : ((lane < L) ? x * scale : 0.0);
-  double vh[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) vh[q] = __shfl_sync(0xffffffffu, vmine, 8 * hh + q);
-  const double va = __shfl_sync(0xffffffffu, vmine, l16);
-  // three independent dot products per lane
-  double db = 0.0, pa = 0.0, qd = 0.0;
+  // half-sums over l >= 1 (entry l = 0 is q = 0 of the hh = 0 lanes) and the l = 0 terms
+  double sq = 0.0, tb = 0.0, tp = 0.0, tq = 0.0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    db = fma(vh[q], b[q], db);
-    pa = fma(dd[q], vh[q], pa);
-    qd = fma(cr[q], vh[q], qd);
+    const double xq = (hh == 0 && q == 0) ? 0.0 : xl[q];
+    sq = fma(xq, xq, sq);
+    tb = fma(xq, b[q], tb);
+    tp = fma(xq, dd[q], tp);
+    tq = fma(xq, cr[q], tq);
   }
-  db += __shfl_xor_sync(0xffffffffu, db, 16);
-  pa += __shfl_xor_sync(0xffffffffu, pa, 16);
-  qd += __shfl_xor_sync(0xffffffffu, qd, 16);
-  db *= tau;
-  pa *= tau;
-  qd *= tau;
-  // (b) K = tau/2 p.v: lanes 0..15 and 16..31 hold the same p_a, reduce over a (4 levels)
+  double b0 = hh == 0 ? b[0] : 0.0, d0 = hh == 0 ? dd[0] : 0.0, c0 = hh == 0 ? cr[0] : 0.0;
+  sq += __shfl_xor_sync(0xffffffffu, sq, 16);
+  tb += __shfl_xor_sync(0xffffffffu, tb, 16);
+  tp += __shfl_xor_sync(0xffffffffu, tp, 16);
+  tq += __shfl_xor_sync(0xffffffffu, tq, 16);
+  b0 += __shfl_xor_sync(0xffffffffu, b0, 16);
+  d0 += __shfl_xor_sync(0xffffffffu, d0, 16);
+  c0 += __shfl_xor_sync(0xffffffffu, c0, 16);
+  if (!(sq > 0.0)) return;   // x is already alpha e_0: H = I (warp-uniform)
+  const double x2 = fma(alpha, alpha, sq);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x2));
+  const double e = fma(-(x2 * y), y, 1.0);
+  y = fma(y * e, fma(e, 0.375, 0.5), y);
+  const double xn = x2 * y;
+  const double beta = alpha >= 0.0 ? -xn : xn;
+  const double tau = (beta - alpha) * sbr_rcp(beta);
+  const double scale = sbr_rcp(alpha - beta);
+  const double db = tau * fma(scale, tb, b0);   // tau v^T B[:, l16]
+  const double pa = tau * fma(scale, tp, d0);   // p_a = tau (D v)_a, a = l16
+  const double qd = tau * fma(scale, tq, c0);   // tau (C v)_a
+  double vh[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) vh[q] = (hh == 0 && q == 0) ? 1.0 : xl[q] * scale;
+  const double va = (l16 == 0) ? 1.0 : xa * scale;
+  // broadcast p; meanwhile K = tau/2 p.v reduced over the 16 rows (lanes 0..15 and 16..31 hold the same p_a)
+  if (lane < 16) ps[lane] = (l16 < L) ? pa : 0.0;
   double pv = (l16 < L) ? pa * va : 0.0;
   pv += __shfl_xor_sync(0xffffffffu, pv, 1);
   pv += __shfl_xor_sync(0xffffffffu, pv, 2);
   pv += __shfl_xor_sync(0xffffffffu, pv, 4);
   pv += __shfl_xor_sync(0xffffffffu, pv, 8);
-  const double wa = pa - 0.5 * tau * pv * va;
-  double wh[8];
+  __syncwarp();
+  double ph[8];
+  {
+    const double2* p2 = reinterpret_cast<const double2*>(ps + 8 * hh);
 #pragma unroll
-  for (int q = 0; q < 8; ++q) wh[q] = __shfl_sync(0xffffffffu, wa, 8 * hh + q);
-#ifdef CMSVD_CHASE_PROF
-  long long ck2 = clock64();
-#endif
+    for (int q = 0; q < 4; ++q) { const double2 t = p2[q]; ph[2 * q] = t.x; ph[2 * q + 1] = t.y; }
+  }
+  const double K = 0.5 * tau * pv;
+  const double wa = fma(-K, va, pa);
   // stores (each lane writes only entries it loaded itself, or the lower entries of D it owns)
   if (s == 0) {
-    if (lane < L) bat(Bd, r + lane, j) = (lane == 0) ? beta : 0.0;
+    if (lane < L) Bd[j * kSBRow + r + lane] = (lane == 0) ? beta : 0.0;
   } else {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int l = 8 * hh + q;
-      if (l < L) bat(Bd, r + l, cx + l16) = (l16 == 0) ? (l == 0 ? beta : 0.0) : fma(-db, vh[q], b[q]);
+      if (FULL || l < L) pB[q] = (l16 == 0) ? (l == 0 ? beta : 0.0) : fma(-db, vh[q], b[q]);
     }
   }
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int l = 8 * hh + q;
-    if (l16 < L && l <= l16) bat(Bd, r + l16, r + l) = fma(-va, wh[q], fma(-wa, vh[q], dd[q]));
-    if (l16 < L2 && l < L) bat(Bd, r2 + l16, r + l) = fma(-qd, vh[q], cr[q]);
+    const double wl = fma(-K, vh[q], ph[q]);
+    if ((FULL || l16 < L) && l <= l16) pDlo[q * kSBRow] = fma(-va, wl, fma(-wa, vh[q], dd[q]));
+    if (FULL || (l16 < L2 && l < L)) pC[q * kSBRow] = fma(-qd, vh[q], cr[q]);
   }
-#ifdef CMSVD_CHASE_PROF
-  __syncwarp();
-  long long ck3 = clock64();
-  if (blockIdx.x == 0 && lane == 0 && j == 200 && s == 5)
-    printf("task (200,5): householder %lld, applies %lld, stores %lld cycles\n", ck1 - ck0, ck2 - ck1, ck3 - ck2);
-#endif
+  __syncwarp();                       // p reads done before the scratch is reused by the next task
+}
+
+__device__ __forceinline__ void chase_task(double* __restrict__ Bd, double* __restrict__ ps, int n, int j, int s) {
+  const int r = j + 1 + s * kSB;
+  const int L = min(kSB, n - r);
+  const int L2 = min(kSB, n - r - L);
+  if (L == kSB && L2 == kSB) chase_task_t<true>(Bd, ps, j, s, L, L2);
+  else chase_task_t<false>(Bd, ps, j, s, L, L2);
 }
 
 // FLAGS: per-sweep progress flags (each warp owns whole sweeps and polls its predecessor's counter)
@@ -536,6 +825,7 @@ __global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double*
   extern __shared__ __align__(16) double bsm[];
   double* Bd = bsm;                                              // [kSBMax][kSBLdb]
   volatile int* prog = reinterpret_cast<volatile int*>(Bd + kSBMax * kSBLdb);   // steps done per sweep
+  double* vsc = Bd + kSBMax * kSBLdb + kSBMax / 2 + 32 * (threadIdx.x >> 5);    // per-warp v / w scratch
   const int p = blockIdx.x;
   const int n = ns[p];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -568,7 +858,7 @@ __global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double*
         __syncwarp();
         __threadfence_block();
       }
-      chase_task(Bd, n, j, s);
+      chase_task(Bd, vsc, n, j, s);
       __threadfence_block();
       __syncwarp();
       if (lane == 0) prog[j] = s + 1;
@@ -588,7 +878,7 @@ __global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double*
       const int j = jhi - idx;
       const int s = tt - 3 * j;
       if (j < 0 || s >= (n - 3 - j) / kSB + 1) break;
-      chase_task(Bd, n, j, s);
+      chase_task(Bd, vsc, n, j, s);
     }
     __syncthreads();
   }
@@ -644,6 +934,34 @@ __global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double*
   }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
+static PFN_cuTensorMapEncodeTiled_v12000 sbr_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 3-D map over the batch of n x n Grams: dims (rows = ld, cols = ld, problems), box0 x box1 x 1 boxes
+static bool sbr_tensor_map(CUtensorMap* map, double* G, int64_t ld, int64_t stride, int nprob, int box0, int box1,
+                           CUtensorMapSwizzle swz) {
+  auto fn = sbr_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)ld, (cuuint64_t)nprob};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * sizeof(double), (cuuint64_t)stride * sizeof(double)};
+  cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, G, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 size_t sbr_ws_bytes(int nprob) { return (size_t)nprob * kSbrPer * sizeof(double); }
 
 // Stage 1 + stage 2 for nprob problems (n = ns[p] <= 512, G destroyed): writes dd, ee (e^2), gsh, cnt,
@@ -657,6 +975,20 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   const size_t ssmem = (size_t)2 * kSymmBuf * sizeof(double);
   const size_t ssmem2 = ((size_t)kSymmRows * (kSB + 1) * 2 + kSB * kSB) * sizeof(double);
   const size_t symm_smem = std::max(ssmem, ssmem2);
+  CUtensorMap tmap, tlo, tup;
+  const bool tma = c.sbr_tma && (stride * sizeof(double)) % 16 == 0 && (ld * sizeof(double)) % 16 == 0 &&
+                   ((uintptr_t)G % 16) == 0 &&
+                   sbr_tensor_map(&tmap, G, ld, stride, nprob, kSyrTile, kSyrTile, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+                   sbr_tensor_map(&tlo, G, ld, stride, nprob, kSymmRows, kSymmJB, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+                   sbr_tensor_map(&tup, G, ld, stride, nprob, 16, kSymmRows, CU_TENSOR_MAP_SWIZZLE_128B);
+  const size_t ymem = ((size_t)2 * kSymmStage + 2) * sizeof(double);
+  const size_t tsmem = ((size_t)kSyrTile * kSyrTile + 4 * kSB * kSyrTile + 2) * sizeof(double);
+  if (tma) {
+    cudaError_t e2 = cudaFuncSetAttribute(k_sbr_syr2k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+    if (e2 != cudaSuccess) return e2;
+    e2 = cudaFuncSetAttribute(k_sbr_symm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ymem);
+    if (e2 != cudaSuccess) return e2;
+  }
   cudaError_t e = cudaFuncSetAttribute(k_sbr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_sbr_symm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)symm_smem);
@@ -671,20 +1003,26 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     if (t >= npan) break;
     const int nrb = (np0 + kSymmRows - 1) / kSymmRows;
     pr = prof_begin(c, PC_SBR_SYMM);
-    k_sbr_symm<<<dim3(nprob, nrb), kSymmThreads, symm_smem, c.stream>>>(G, ld, stride, d_ns, t, ws);
+    if (tma)
+      k_sbr_symm_tma<<<dim3(nprob, nrb), kSymmThreads, ymem, c.stream>>>(tlo, tup, G, ld, stride, d_ns, t, ws);
+    else
+      k_sbr_symm<<<dim3(nprob, nrb), kSymmThreads, symm_smem, c.stream>>>(G, ld, stride, d_ns, t, ws);
     c.launches += 1;
     prof_end(c, pr);
     pr = prof_begin(c, PC_SBR_SYR2K);
     k_sbr_w<<<dim3(nprob, nrb), 256, 0, c.stream>>>(d_ns, t, ws);
     c.launches += 1;
     const int nt = (np0 + kSyrTile - 1) / kSyrTile;
-    k_sbr_syr2k<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, 0, c.stream>>>(G, ld, stride, d_ns, t, ws);
+    if (tma)
+      k_sbr_syr2k_tma<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, tsmem, c.stream>>>(tmap, d_ns, t, ws);
+    else
+      k_sbr_syr2k<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, 0, c.stream>>>(G, ld, stride, d_ns, t, ws);
     c.launches += 1;
     prof_end(c, pr);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  const size_t csmem = (size_t)kSBMax * kSBLdb * sizeof(double) + kSBMax * sizeof(int);
+  const size_t csmem = ((size_t)kSBMax * kSBLdb + kSBMax / 2 + 32 * kChaseWarps) * sizeof(double);
   const int pr = prof_begin(c, PC_SBR_CHASE);
   if (c.chase_flags) {
     e = cudaFuncSetAttribute(k_sbr_chase<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);

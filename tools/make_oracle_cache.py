@@ -14,7 +14,7 @@ Writes tests/oracle_cache/<name>.npz (compressed):
 err2 / total are float64; sigma_tilde / mu are stored as float32 (the parity
 tolerance on singular values is 1e-4 relative, float32 rounding is 6e-8).
 
-Usage: python tools/make_oracle_cache.py config2|config4|config5|greedy2|greedy3|greedy4|greedy5 [...]
+Usage: python tools/make_oracle_cache.py config2|config4|config5|greedy3|greedy5|greedy5big [...]
 """
 from __future__ import annotations
 
@@ -100,8 +100,8 @@ def main():
             greedy_cache("greedy_config3", sp, col.r,
                          [(oc.APPROX, oc.SORT_RESIDUAL, 0.1, 1), (oc.APPROX, oc.SORT_RESIDUAL, 0.3, 1),
                           (oc.APPROX, oc.SORT_FROBENIUS, 0.3, 1)], oracle.TRUNC)
-        elif what == "greedy5":
-            for N, r in ((512, 16), (512, 64), (2048, 16)):
+        elif what in ("greedy5", "greedy5big"):
+            for N, r in (((512, 16), (512, 64)) if what == "greedy5" else ((2048, 16),)):
                 col = synth.config5(N=N, r=r)
                 sp = oracle.block_spectra(col.blocks)
                 greedy_cache(f"greedy_config5_N{N}_r{r}", sp, r, [(oc.APPROX, oc.SORT_RESIDUAL, 0.1, 16)], oracle.RAW)
