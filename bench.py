@@ -214,12 +214,29 @@ def work_model(col, pairs, blk_rank, big):
     }
     # unique HBM bytes of the materialised residual R' = F - Q Z (read Q, Z, F; write R')
     nbytes = {"resid_R": float(np.sum(4.0 * (m * q + q * w + 2 * m * w)))}
+    # two-stage reduction of the core Grams with n > 160 (k_sbr.cu): per panel t the trailing block has
+    # n_p = n - 16 (t + 1) rows; the symmetric product streams the full n_p^2 block once, the rank-32 update
+    # reads and writes its lower triangle (8 B per element)
+    big_n = nG[nG > 160]
+    if big_n.size:
+        sym_b = syr_b = sym_f = syr_f = 0.0
+        for nn in np.unique(big_n):
+            cnt = float(np.sum(big_n == nn))
+            npv = nn - 16.0 * np.arange(1, int((nn - 18) // 16) + 2)
+            npv = npv[npv >= 2]
+            sym_b += cnt * float(np.sum(8.0 * npv ** 2))
+            syr_b += cnt * float(np.sum(16.0 * npv * (npv + 1) / 2))
+            sym_f += cnt * float(np.sum(2.0 * 16 * npv ** 2))
+            syr_f += cnt * float(np.sum(2.0 * 32 * npv * (npv + 1) / 2))
+        nbytes["sbr_symm"], nbytes["sbr_syr2k"] = sym_b, syr_b
+        flops["sbr_symm"], flops["sbr_syr2k"] = sym_f, syr_f
     return flops, nbytes
 
 
 def categorize(prof, flops, nbytes, total_ms, steps, tiles):
     tc_peak = tf32_fp32eq_tflops()
     peaks = {"eig_G": DFMA_TFLOPS, "eig_W": DFMA_TFLOPS, "gram_W": tc_peak if tiles else DFMA_TFLOPS,
+             "sbr_symm": DFMA_TFLOPS, "sbr_syr2k": DFMA_TFLOPS,
              "gram_ZZ": DFMA_TFLOPS, "proj_Z": tc_peak if tiles else FFMA_TFLOPS,
              "resid_R": tc_peak if tiles else FFMA_TFLOPS, "pair_tc": tc_peak}
     kernels = {}
@@ -492,12 +509,15 @@ def main():
         {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
          "traffic": None}
     others = [roofline_entry(k, kernels[k], peaks, tc_peak, traffic.get(k))
-              for k in ("proj_Z", "resid_R", "gram_W", "pair_tc") if k in kernels and k in flops and k != dom]
+              for k in ("proj_Z", "resid_R", "gram_W", "pair_tc", "sbr_symm", "sbr_syr2k")
+              if k in kernels and k in flops and k != dom]
     for o in others:
         if o["kernel"] in nbytes:
             e = kernels[o["kernel"]]
             o["hbm"] = {"achieved": e["gbs"], "peak": hbm_gbs(), "unit": "GB/s", "frac": e["frac_of_hbm"],
-                        "algorithmic": "read Q, Z, F + write R' per pair (4 B each)"}
+                        "algorithmic": "read Q, Z, F + write R' per pair (4 B each)" if o["kernel"] == "resid_R" else
+                        "per panel: the n_p^2 trailing block read once (symm) / its lower triangle read + "
+                        "written (syr2k), 8 B per element"}
     if one_time["s1_energy_gbs"]:
         others.append({"bound": "hbm", "kernel": "energy (S1, one-time)", "achieved": one_time["s1_energy_gbs"],
                        "peak": hbm_gbs(), "unit": "GB/s", "frac": one_time["s1_energy_gbs"] / hbm_gbs(),

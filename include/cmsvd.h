@@ -185,6 +185,12 @@ cmsvd_status cmsvd_pair_errors_tight(cmsvd_ctx ctx, const int32_t* pairs, int64_
 cmsvd_status cmsvd_cluster_verify(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters,
                                   double* exact_err2, double* total, int64_t* mem);
 
+/* cmsvd_cluster_verify plus the derived quantities (any may be NULL): rel[c] = sqrt(exact_err2[c] /
+ * total[c]) (0 for a zero-energy cluster; the certificate compares it with eps) and
+ * *ratio = sum_i m n_i / sum_c mem[c].  Errors as cmsvd_cluster_verify. */
+cmsvd_status cmsvd_cluster_verify_ex(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters,
+                                     double* exact_err2, double* total, int64_t* mem, double* rel, double* ratio);
+
 /* The compressed representation of a partition: for each
  * cluster c (ids 0..n_clusters-1 of assign[count], host arrays) the rank-r_c truncated SVD of the
  * concatenation M_c of its blocks in ascending block order, r_c = min(r, m, N_c), stored as

@@ -26,7 +26,7 @@ SORT_FROBENIUS, SORT_RESIDUAL = 0, 1
 
 EXPORTS = ["cmsvd_status_string", "cmsvd_last_error", "cmsvd_version", "cmsvd_create", "cmsvd_destroy",
            "cmsvd_register", "cmsvd_block_spectra", "cmsvd_pair_errors", "cmsvd_pair_errors_tight",
-           "cmsvd_cluster", "cmsvd_cluster_verify", "cmsvd_cluster_factors", "cmsvd_sequence_errors",
+           "cmsvd_cluster", "cmsvd_cluster_verify", "cmsvd_cluster_verify_ex", "cmsvd_cluster_factors", "cmsvd_sequence_errors",
            "cmsvd_launch_count", "cmsvd_sym_eigvals", "cmsvd_spectra_diagnostics",
            "cmsvd_profile_enable",
            "cmsvd_profile_read"]
@@ -81,6 +81,8 @@ def load(path: str = LIB_PATH):
     L.cmsvd_cluster_factors.argtypes = [vp, i32, vp, i32, vp, vp, vp]
     L.cmsvd_cluster_verify.restype = ctypes.c_int
     L.cmsvd_cluster_verify.argtypes = [vp, i32, vp, i32, vp, vp, vp]
+    L.cmsvd_cluster_verify_ex.restype = ctypes.c_int
+    L.cmsvd_cluster_verify_ex.argtypes = [vp, i32, vp, i32, vp, vp, vp, vp, vp]
     L.cmsvd_sym_eigvals.restype = ctypes.c_int
     L.cmsvd_sym_eigvals.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp]
     L.cmsvd_spectra_diagnostics.restype = ctypes.c_int
@@ -352,10 +354,11 @@ class Context:
         e2 = np.zeros(nc)
         tot = np.zeros(nc)
         mem = np.zeros(nc, np.int64)
-        self._check(self._L.cmsvd_cluster_verify(self._h, int(r), _ptr(assign), nc, _ptr(e2), _ptr(tot), _ptr(mem)))
-        raw = float(self.m) * float(np.sum(self._ncols)) if hasattr(self, "_ncols") else float("nan")
-        return {"exact_err2": e2, "total": tot, "rel": np.sqrt(e2 / np.maximum(tot, 1e-300)), "mem": mem,
-                "ratio": raw / float(np.sum(mem)) if nc else float("nan")}
+        rel = np.zeros(nc)
+        ratio = ctypes.c_double(float("nan"))
+        self._check(self._L.cmsvd_cluster_verify_ex(self._h, int(r), _ptr(assign), nc, _ptr(e2), _ptr(tot),
+                                                    _ptr(mem), _ptr(rel), ctypes.byref(ratio)))
+        return {"exact_err2": e2, "total": tot, "rel": rel, "mem": mem, "ratio": ratio.value}
 
     # -- cmsvd_cluster ---------------------------------------------------
     def cluster(self, algorithm: int, eps: float, r: int | None = None, sort: int = SORT_FROBENIUS,

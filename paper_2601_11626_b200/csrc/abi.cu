@@ -2,6 +2,7 @@
 // abi.cu -- the extern "C" boundary of libcmsvd (declared in include/cmsvd.h).
 // Every entry point converts C++/CUDA failures into a cmsvd_status plus a
 // per-context message; no exception crosses the ABI.
+#include <cmath>
 #include <cstring>
 #include <new>
 
@@ -162,6 +163,27 @@ cmsvd_status cmsvd_cluster_verify(cmsvd_ctx ctx, int32_t r, const int32_t* assig
   GUARD_CTX(ctx);
   try {
     return do_cluster_verify(c, r, assign, n_clusters, exact_err2, total, mem);
+  } catch (const std::bad_alloc&) {
+    return fail(c, CMSVD_E_NOMEM, "cluster_verify: host allocation failed");
+  } catch (...) {
+    return fail(c, CMSVD_E_ARG, "cluster_verify: unexpected exception");
+  }
+}
+
+cmsvd_status cmsvd_cluster_verify_ex(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters,
+                                     double* exact_err2, double* total, int64_t* mem, double* rel, double* ratio) {
+  GUARD_CTX(ctx);
+  try {
+    Status st = do_cluster_verify(c, r, assign, n_clusters, exact_err2, total, mem);
+    if (st != CMSVD_OK) return st;
+    double raw = 0.0, stored = 0.0;
+    for (int32_t i = 0; i < c.count; ++i) raw += (double)c.m * (double)c.n[i];
+    for (int32_t g = 0; g < n_clusters; ++g) {
+      stored += (double)mem[g];
+      if (rel) rel[g] = total[g] > 0.0 ? std::sqrt(std::max(exact_err2[g], 0.0) / total[g]) : 0.0;
+    }
+    if (ratio) *ratio = stored > 0.0 ? raw / stored : 0.0;
+    return CMSVD_OK;
   } catch (const std::bad_alloc&) {
     return fail(c, CMSVD_E_NOMEM, "cluster_verify: host allocation failed");
   } catch (...) {

@@ -42,24 +42,38 @@ FULL_METRICS = [
 ]
 
 
+_UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1.0, "usecond": 1e3, "msecond": 1e6}
+
+
 def launches(path, out):
+    """Per-kernel launch counts, device time (ns -> ms) and, when captured, DRAM read/write bytes."""
     rows = list(csv.reader(open(path)))
     hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr_i]
-    ik, iv, im = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name")
+    ik, iv, im, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name"), h.index("Metric Unit")
     tot = defaultdict(float)
+    rd = defaultdict(float)
+    wr = defaultdict(float)
     cnt = defaultdict(int)
     for r in rows[hdr_i + 1:]:
-        if len(r) <= iv or r[im] != "gpu__time_duration.sum":
+        if len(r) <= iv:
             continue
         name = r[ik].split("(")[0].replace("void ", "").replace("cmsvd::", "")
-        v = float(r[iv].replace(",", ""))
-        tot[name] += v
-        cnt[name] += 1
+        v = float(r[iv].replace(",", "")) * _UNIT.get(r[iu], 1.0)
+        if r[im] == "gpu__time_duration.sum":
+            tot[name] += v
+            cnt[name] += 1
+        elif r[im] == "dram__bytes_read.sum":
+            rd[name] += v
+        elif r[im] == "dram__bytes_write.sum":
+            wr[name] += v
     s = sum(tot.values())
-    lines = [f"{'kernel':40s} {'launches':>8s} {'total_ms':>10s} {'share':>7s}"]
+    dram = bool(rd)
+    lines = [f"{'kernel':40s} {'launches':>8s} {'total_ms':>10s} {'share':>7s}" +
+             (f" {'dram_rd_GB':>10s} {'dram_wr_GB':>10s}" if dram else "")]
     for k in sorted(tot, key=lambda k: -tot[k]):
-        lines.append(f"{k[:40]:40s} {cnt[k]:8d} {tot[k] / 1e6:10.3f} {100 * tot[k] / s:6.2f}%")
+        lines.append(f"{k[:40]:40s} {cnt[k]:8d} {tot[k] / 1e6:10.3f} {100 * tot[k] / s:6.2f}%" +
+                     (f" {rd[k] / 1e9:10.3f} {wr[k] / 1e9:10.3f}" if dram else ""))
     lines.append(f"{'total':40s} {sum(cnt.values()):8d} {s / 1e6:10.3f}")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
