@@ -303,12 +303,18 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __re
     Ys[i * kX + c] = (i < imax) ? y : 0.0;
     if (i < imax) Yw[(int64_t)c * kSBMax + I0 + i] = y;
   }
+  // the block's V rows in shared memory ([l][i], coalesced) for M_b = V_b^T Y_b
+  double* Vb = Ys + kSymmRows * kX;
+  for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
+    const int l = e >> 7, i = e & 127;
+    Vb[e] = i < imax ? Vw[(int64_t)l * kSBMax + I0 + i] : 0.0;
+  }
   __syncthreads();
   double* Mw = const_cast<double*>(Vw) + 2 * kSbrV + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) {
     const int a = e >> 4, c = e & 15;
     double s = 0.0;
-    for (int i = 0; i < imax; ++i) s = fma(Vw[(int64_t)a * kSBMax + I0 + i], Ys[i * kX + c], s);
+    for (int i = 0; i < imax; ++i) s = fma(Vb[a * kSymmRows + i], Ys[i * kX + c], s);
     Mw[e] = s;
   }
 }
@@ -448,8 +454,9 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int
 }
 
 __global__ void __launch_bounds__(kSyrThreads) k_sbr_syr2k_tma(const __grid_constant__ CUtensorMap tmap,
-                                                                  const int* __restrict__ ns, int t,
-                                                                  const double* __restrict__ ws) {
+                                                                  const __grid_constant__ CUtensorMap tmv,
+                                                                  const __grid_constant__ CUtensorMap tmw,
+                                                                  const int* __restrict__ ns, int t) {
   extern __shared__ __align__(128) double tsm[];
   double* At = tsm;                                   // [64 cols][64 rows] (TMA box, dense)
   double* VI = At + kSyrTile * kSyrTile;
@@ -472,19 +479,15 @@ __global__ void __launch_bounds__(kSyrThreads) k_sbr_syr2k_tma(const __grid_cons
     mbar_init(bar, 1);
     fence_mbar_init();
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"((unsigned)(kSyrTile * kSyrTile * sizeof(double)))
+                 "r"((unsigned)((kSyrTile * kSyrTile + 4 * kSB * kSyrTile) * sizeof(double)))
                  : "memory");
     tma_load_3d(At, &tmap, R0 + I0, R0 + J0, p, bar);
-  }
-  const double* Vw = ws + (int64_t)p * kSbrPer;
-  const double* Ww = Vw + kSbrV;
-  for (int e = tid; e < kSyrTile * kSB; e += kSyrThreads) {
-    const int l = e >> 6, i = e & 63;
-    const int gi = I0 + i, gj = J0 + i;
-    VI[e] = gi < np ? Vw[(int64_t)l * kSBMax + gi] : 0.0;
-    WI[e] = gi < np ? Ww[(int64_t)l * kSBMax + gi] : 0.0;
-    VJ[e] = gj < np ? Vw[(int64_t)l * kSBMax + gj] : 0.0;
-    WJ[e] = gj < np ? Ww[(int64_t)l * kSBMax + gj] : 0.0;
+    // V / W rows of the tile ([l][i] boxes of the workspace; rows >= n_p hold zeros or stale values of the
+    // unused padding, which only meet matrix entries outside the problem)
+    tma_load_3d(VI, &tmv, I0, 0, p, bar);
+    tma_load_3d(WI, &tmw, I0, 0, p, bar);
+    tma_load_3d(VJ, &tmv, J0, 0, p, bar);
+    tma_load_3d(WJ, &tmw, J0, 0, p, bar);
   }
   __syncthreads();
   mbar_wait(bar, 0);
@@ -533,16 +536,18 @@ __global__ void __launch_bounds__(kSyrThreads) k_sbr_syr2k_tma(const __grid_cons
 // (16-byte pairs (j, j+1)) is conflict-free; slices crossing the diagonal are copied element-wise by
 // cp.async.  Two stages in flight; the V slices (32 x 16) follow by cp.async.
 // ---------------------------------------------------------------------------
-constexpr int kSymmA = kSymmJB * kSymmRows;    // doubles per A slice (32 KB)
-constexpr int kSymmStage = kSymmA + kSymmJB * kSB;   // + V slice (4 KB)
+constexpr int kSymmJT = 16;                    // columns per TMA slice (one 16 x 128 swizzled box when transposed)
+constexpr int kSymmNS = 3;                     // stages in flight
+constexpr int kSymmA = kSymmJT * kSymmRows;    // doubles per A slice (16 KB)
+constexpr int kSymmStage = 2 * kSymmA + kSymmJT * kSB;   // lower box + transposed box + V slice (34 KB)
 
-__global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_tma(const __grid_constant__ CUtensorMap tlo,
+__global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_constant__ CUtensorMap tlo,
                                                                     const __grid_constant__ CUtensorMap tup,
                                                                     const double* __restrict__ G, int64_t ld,
                                                                     int64_t stride, const int* __restrict__ ns,
                                                                     int t, double* __restrict__ ws) {
   extern __shared__ __align__(1024) double ysm[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ysm + 2 * kSymmStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ysm + kSymmNS * kSymmStage);
   const int p = blockIdx.x;
   const int n = ns[p];
   if (t >= sbr_panels(n)) return;
@@ -556,40 +561,28 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_tma(const __grid_c
   const int i0 = tid & 63, h = tid >> 6;
   const int imax = min(kSymmRows, np - I0);
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+#pragma unroll
+    for (int q = 0; q < kSymmNS; ++q) mbar_init(&bars[q], 1);
     fence_mbar_init();
   }
   __syncthreads();
   auto kind = [&](int J0) {
-    const int jmax = min(kSymmJB, np - J0);
+    const int jmax = min(kSymmJT, np - J0);
     return (J0 + jmax - 1 <= I0) ? 0 : ((I0 + imax - 1 < J0) ? 1 : 2);
   };
   auto issue = [&](int J0, int st) {
-    double* As = ysm + st * kSymmStage;
-    double* Vs = As + kSymmA;
-    const int jmax = min(kSymmJB, np - J0);
+    double* As = ysm + st * kSymmStage;   // lower box [j][i] (dense), then the transposed box [i][j] (swizzled)
+    double* Vs = As + 2 * kSymmA;
+    const int jmax = min(kSymmJT, np - J0);
     const int kd = kind(J0);
-    if (kd == 2) {
-      for (int e = tid; e < kSymmJB * kSymmRows; e += kSymmThreads) {
-        const int jj = e >> 7, ii = e & 127;
-        const bool ok = jj < jmax && ii < imax;
-        const int gi = I0 + ii, gj = J0 + jj;
-        const double* src = !ok ? A : (gi >= gj ? A + (int64_t)gj * ld + gi : A + (int64_t)gi * ld + gj);
-        cp_async8(As + jj * kSymmRows + ii, src, ok);
-      }
-    } else if (tid == 0) {
+    if (tid == 0) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[st])),
-                   "r"((unsigned)(kSymmA * sizeof(double)))
+                   "r"((unsigned)((kd == 2 ? 2 : 1) * kSymmA * sizeof(double)))
                    : "memory");
-      if (kd == 0) {
-        tma_load_3d(As, &tlo, R0 + I0, R0 + J0, p, &bars[st]);
-      } else {
-        tma_load_3d(As, &tup, R0 + J0, R0 + I0, p, &bars[st]);
-        tma_load_3d(As + kSymmA / 2, &tup, R0 + J0 + 16, R0 + I0, p, &bars[st]);
-      }
+      if (kd != 1) tma_load_3d(As, &tlo, R0 + I0, R0 + J0, p, &bars[st]);
+      if (kd != 0) tma_load_3d(As + kSymmA, &tup, R0 + J0, R0 + I0, p, &bars[st]);
     }
-    for (int e = tid; e < kSymmJB * kSB; e += kSymmThreads) {
+    for (int e = tid; e < kSymmJT * kSB; e += kSymmThreads) {
       const int jj = e >> 4, c = e & 15;
       const bool ok = jj < jmax;
       cp_async8(Vs + e, ok ? Vw + (int64_t)c * kSBMax + J0 + jj : Vw, ok);
@@ -601,28 +594,45 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_tma(const __grid_c
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
-  const int nsl = (np + kSymmJB - 1) / kSymmJB;
+  const int nsl = (np + kSymmJT - 1) / kSymmJT;
   unsigned uses = 0;   // TMA completions consumed per stage (bit st: parity of the next wait)
-  issue(0, 0);
+  for (int q = 0; q < kSymmNS - 1 && q < nsl; ++q) issue(q * kSymmJT, q);
   for (int k = 0; k < nsl; ++k) {
-    const int st = k & 1;
-    const int J0 = k * kSymmJB;
-    if (k + 1 < nsl) {
-      issue((k + 1) * kSymmJB, (k + 1) & 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
+    const int st = k % kSymmNS;
+    const int J0 = k * kSymmJT;
+    if (k + kSymmNS - 1 < nsl) issue((k + kSymmNS - 1) * kSymmJT, (k + kSymmNS - 1) % kSymmNS);
+    const int pending = min(nsl, k + kSymmNS) - k - 1;   // groups committed after slice k's
+    if (pending >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else if (pending == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
     const int kd = kind(J0);
-    if (kd != 2) {
-      mbar_wait(&bars[st], (uses >> st) & 1u);
-      uses ^= 1u << st;
-    }
+    mbar_wait(&bars[st], (uses >> st) & 1u);
+    uses ^= 1u << st;
     __syncthreads();
     const double* As = ysm + st * kSymmStage;
-    const double* Vs = As + kSymmA;
-    const int jmax = min(kSymmJB, np - J0);
-    if (kd != 1) {
+    const double* Au = As + kSymmA;
+    const double* Vs = As + 2 * kSymmA;
+    const int jmax = min(kSymmJT, np - J0);
+    if (kd == 2) {
+      // slice crossing the diagonal block: A22(i, j) from the lower box if i >= j, else the transposed box
+      const int sw = i0 & 7;
+      for (int jj = 0; jj < jmax; ++jj) {
+        const int gj = J0 + jj;
+        const int cu = ((((jj >> 1) ^ sw) << 1) | (jj & 1));
+        const double a0 = (I0 + i0 >= gj) ? As[jj * kSymmRows + i0] : Au[i0 * 16 + cu];
+        const double a1 = (I0 + i0 + 64 >= gj) ? As[jj * kSymmRows + i0 + 64] : Au[(i0 + 64) * 16 + cu];
+        const double2* vr = reinterpret_cast<const double2*>(Vs + jj * kSB + 8 * h);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 v = vr[q];
+          acc[0][2 * q] = fma(a0, v.x, acc[0][2 * q]);
+          acc[0][2 * q + 1] = fma(a0, v.y, acc[0][2 * q + 1]);
+          acc[1][2 * q] = fma(a1, v.x, acc[1][2 * q]);
+          acc[1][2 * q + 1] = fma(a1, v.y, acc[1][2 * q + 1]);
+        }
+      }
+    } else if (kd == 0) {
+#pragma unroll 4
       for (int jj = 0; jj < jmax; ++jj) {
         const double a0 = As[jj * kSymmRows + i0], a1 = As[jj * kSymmRows + i0 + 64];
         const double2* vr = reinterpret_cast<const double2*>(Vs + jj * kSB + 8 * h);
@@ -636,13 +646,13 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_tma(const __grid_c
         }
       }
     } else {
-      // swizzled rows: A22(i, J0 + 2 kp .. + 1) at box (kp >> 3), row i, 16-byte chunk (kp & 7) ^ (i & 7)
+      // swizzled rows: A22(i, J0 + 2 kp .. + 1) at row i, 16-byte chunk kp ^ (i & 7)
       const int sw = i0 & 7;
+#pragma unroll 2
       for (int kp = 0; 2 * kp < jmax; ++kp) {
-        const double* box = As + (kp >> 3) * (kSymmA / 2);
-        const int ch = ((kp & 7) ^ sw) << 1;
-        double2 a0 = *reinterpret_cast<const double2*>(box + i0 * 16 + ch);
-        double2 a1 = *reinterpret_cast<const double2*>(box + (i0 + 64) * 16 + ch);
+        const int ch = (kp ^ sw) << 1;
+        double2 a0 = *reinterpret_cast<const double2*>(Au + i0 * 16 + ch);
+        double2 a1 = *reinterpret_cast<const double2*>(Au + (i0 + 64) * 16 + ch);
         if (2 * kp + 1 >= jmax) { a0.y = 0.0; a1.y = 0.0; }
         const double2* v0 = reinterpret_cast<const double2*>(Vs + (2 * kp) * kSB + 8 * h);
         const double2* v1 = reinterpret_cast<const double2*>(Vs + (2 * kp + 1) * kSB + 8 * h);
@@ -656,7 +666,7 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_tma(const __grid_c
         }
       }
     }
-    __syncthreads();   // this stage is reissued at step k + 2
+    __syncthreads();   // this stage is reissued kSymmNS - 1 steps later
   }
   // X rows to shared memory (row stride 17), then Y = X T and M_b = V_b^T Y_b
   constexpr int kX = kSB + 1;
@@ -677,12 +687,18 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_tma(const __grid_c
     Ys[i * kX + c] = (i < imax) ? y : 0.0;
     if (i < imax) Yw[(int64_t)c * kSBMax + I0 + i] = y;
   }
+  // the block's V rows in shared memory ([l][i], coalesced) for M_b = V_b^T Y_b
+  double* Vb = Ys + kSymmRows * kX;
+  for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
+    const int l = e >> 7, i = e & 127;
+    Vb[e] = i < imax ? Vw[(int64_t)l * kSBMax + I0 + i] : 0.0;
+  }
   __syncthreads();
   double* Mw = const_cast<double*>(Vw) + 2 * kSbrV + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) {
     const int a = e >> 4, c = e & 15;
     double s = 0.0;
-    for (int i = 0; i < imax; ++i) s = fma(Vw[(int64_t)a * kSBMax + I0 + i], Ys[i * kX + c], s);
+    for (int i = 0; i < imax; ++i) s = fma(Vb[a * kSymmRows + i], Ys[i * kX + c], s);
     Mw[e] = s;
   }
 }
@@ -962,6 +978,18 @@ static bool sbr_tensor_map(CUtensorMap* map, double* G, int64_t ld, int64_t stri
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static bool sbr_ws_map(CUtensorMap* map, double* base, int nprob) {
+  auto fn = sbr_encode_fn();
+  if (!fn || ((uintptr_t)base % 16) != 0) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)kSBMax, (cuuint64_t)kSB, (cuuint64_t)nprob};
+  cuuint64_t strides[2] = {(cuuint64_t)kSBMax * sizeof(double), (cuuint64_t)kSbrPer * sizeof(double)};
+  cuuint32_t box[3] = {(cuuint32_t)kSyrTile, (cuuint32_t)kSB, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 size_t sbr_ws_bytes(int nprob) { return (size_t)nprob * kSbrPer * sizeof(double); }
 
 // Stage 1 + stage 2 for nprob problems (n = ns[p] <= 512, G destroyed): writes dd, ee (e^2), gsh, cnt,
@@ -973,15 +1001,19 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   const int npan = sbr_panels(nmax);
   const size_t psmem = ((size_t)kSB * kPanelLd + 256 + 2 * kSB + 2 * kSB * kSB) * sizeof(double);
   const size_t ssmem = (size_t)2 * kSymmBuf * sizeof(double);
-  const size_t ssmem2 = ((size_t)kSymmRows * (kSB + 1) * 2 + kSB * kSB) * sizeof(double);
+  const size_t ssmem2 = ((size_t)kSymmRows * (kSB + 1) * 2 + kSB * kSB + kSymmRows * kSB) * sizeof(double);
   const size_t symm_smem = std::max(ssmem, ssmem2);
   CUtensorMap tmap, tlo, tup;
   const bool tma = c.sbr_tma && (stride * sizeof(double)) % 16 == 0 && (ld * sizeof(double)) % 16 == 0 &&
                    ((uintptr_t)G % 16) == 0 &&
                    sbr_tensor_map(&tmap, G, ld, stride, nprob, kSyrTile, kSyrTile, CU_TENSOR_MAP_SWIZZLE_NONE) &&
-                   sbr_tensor_map(&tlo, G, ld, stride, nprob, kSymmRows, kSymmJB, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+                   sbr_tensor_map(&tlo, G, ld, stride, nprob, kSymmRows, kSymmJT, CU_TENSOR_MAP_SWIZZLE_NONE) &&
                    sbr_tensor_map(&tup, G, ld, stride, nprob, 16, kSymmRows, CU_TENSOR_MAP_SWIZZLE_128B);
-  const size_t ymem = ((size_t)2 * kSymmStage + 2) * sizeof(double);
+  const size_t ymem = std::max((size_t)kSymmNS * kSymmStage + 4,
+                               (size_t)kSymmRows * (kSB + 1) * 2 + kSB * kSB + kSymmRows * kSB + 4) * sizeof(double);
+  // V and W (kSBMax x kSB per problem, column-major, problem stride kSbrPer) as 3-D maps, 64 x 16 boxes
+  CUtensorMap tmv, tmw;
+  const bool tma2 = tma && sbr_ws_map(&tmv, ws, nprob) && sbr_ws_map(&tmw, ws + kSbrV, nprob);
   const size_t tsmem = ((size_t)kSyrTile * kSyrTile + 4 * kSB * kSyrTile + 2) * sizeof(double);
   if (tma) {
     cudaError_t e2 = cudaFuncSetAttribute(k_sbr_syr2k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
@@ -1013,8 +1045,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     k_sbr_w<<<dim3(nprob, nrb), 256, 0, c.stream>>>(d_ns, t, ws);
     c.launches += 1;
     const int nt = (np0 + kSyrTile - 1) / kSyrTile;
-    if (tma)
-      k_sbr_syr2k_tma<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, tsmem, c.stream>>>(tmap, d_ns, t, ws);
+    if (tma2)
+      k_sbr_syr2k_tma<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, tsmem, c.stream>>>(tmap, tmv, tmw, d_ns, t);
     else
       k_sbr_syr2k<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, 0, c.stream>>>(G, ld, stride, d_ns, t, ws);
     c.launches += 1;
