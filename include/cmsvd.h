@@ -181,7 +181,7 @@ cmsvd_status cmsvd_pair_errors_tight(cmsvd_ctx ctx, const int32_t* pairs, int64_
  *                   is stored raw when that is smaller, cf. Table 2's 1.000*).
  * The compression ratio is sum_i m n_i / sum_c mem[c].
  * Errors: CMSVD_E_STATE (no collection), CMSVD_E_ARG (bad assign / r),
- * CMSVD_E_SHAPE (min(m, N_c) > 512), CMSVD_E_NOCONV, CMSVD_E_CUDA, CMSVD_E_NOMEM. */
+ * CMSVD_E_SHAPE (min(m, N_c) > 4096), CMSVD_E_NOCONV, CMSVD_E_CUDA, CMSVD_E_NOMEM. */
 cmsvd_status cmsvd_cluster_verify(cmsvd_ctx ctx, int32_t r, const int32_t* assign, int32_t n_clusters,
                                   double* exact_err2, double* total, int64_t* mem);
 
@@ -251,14 +251,15 @@ cmsvd_status cmsvd_cluster(cmsvd_ctx ctx, const cmsvd_cluster_opts* opts, int32_
 
 /* Diagnostic: the batched fp64 symmetric eigensolver that yields sigma~^2 from the core Grams (Lemma 1 /
  * Cor. 3), on caller matrices, for parity tests.
- *   count >= 1 problems; problem p is n[p] x n[p] (0 <= n[p] <= nmax <= 512) at G + p * nmax * nmax,
+ *   count >= 1 problems; problem p is n[p] x n[p] (0 <= n[p] <= nmax <= 4096) at G + p * nmax * nmax,
  *   column-major with leading dimension nmax, symmetric (only the lower triangle is read), host memory;
  *   ev[p * kw + l] = the l-th largest eigenvalue (l < min(kw, n[p])), non-increasing; entries l >= n[p]
  *   are unspecified; trace[p] = sum of the diagonal (may be NULL).  1 <= kw <= nmax.  The dispatch by
  *   size is the pair path's (n <= 160 register/shared-memory kernels, 160 < n <= 512 the two-stage band
- *   reduction; CMSVD_EIG_SBR=0 selects the one-stage in-place kernel).
+ *   reduction; CMSVD_EIG_SBR=0 selects the one-stage in-place kernel) and, for 512 < n <= 4096, the
+ *   cluster verification's (the two-stage reduction with the panel and the band in global memory).
  * Errors: CMSVD_E_ARG (NULL pointers, kw out of range), CMSVD_E_SHAPE (n[p] < 0, n[p] > nmax or
- * nmax > 512), CMSVD_E_CUDA, CMSVD_E_NOMEM. */
+ * nmax > 4096), CMSVD_E_CUDA, CMSVD_E_NOMEM. */
 cmsvd_status cmsvd_sym_eigvals(cmsvd_ctx ctx, int32_t count, int32_t nmax, const int32_t* n, const double* G,
                                int32_t kw, double* ev, double* trace);
 

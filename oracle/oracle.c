@@ -751,7 +751,32 @@ int or_exact_groups(int64_t m, const int32_t* n, const double* const* A, const i
       memcpy(M + col * m, A[ids[t]], sizeof(double) * m * n[ids[t]]);
       col += n[ids[t]];
     }
-    int st = or_exact_err2(m, nc, M, m, r, out + g);
+    int st;
+    const int64_t dim = m < nc ? m : nc;
+    if (dim <= 512) {
+      st = or_exact_err2(m, nc, M, m, r, out + g);
+    } else {
+      /* wide concatenations (reading A15): the smaller fp64 Gram, G = M M^T (m <= nc) or M^T M, and its
+         eigenvalues by the tridiagonalisation + bisection of or_sym_eig_topk; E_r^2 = sum_{j>r} lambda_j */
+      double* G = (double*)malloc(sizeof(double) * dim * dim);
+      for (int64_t a = 0; a < dim; ++a)
+        for (int64_t b = 0; b <= a; ++b) {
+          double t = 0.0;
+          if (m <= nc)
+            for (int64_t c2 = 0; c2 < nc; ++c2) t += M[a + c2 * m] * M[b + c2 * m];
+          else
+            for (int64_t i = 0; i < m; ++i) t += M[i + a * m] * M[i + b * m];
+          G[a + b * dim] = t;
+          G[b + a * dim] = t;
+        }
+      double* lam = (double*)malloc(sizeof(double) * dim);
+      st = or_sym_eig_topk(dim, G, dim, 0, lam, NULL, dim);
+      double t = 0.0;
+      for (int64_t j = dim - 1; j >= r; --j) t += lam[j] > 0.0 ? lam[j] : 0.0;
+      out[g] = t;
+      free(lam);
+      free(G);
+    }
     if (st) status = st;
     free(M);
   }

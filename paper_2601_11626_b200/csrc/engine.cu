@@ -869,7 +869,7 @@ Status do_pair_errors_tight(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, 
 Status do_sym_eigvals(Ctx& c, int32_t count, int32_t nmax, const int32_t* n, const double* G, int32_t kw,
                       double* ev, double* trace) {
   if (!n || !G || !ev || count < 1) return fail(c, CMSVD_E_ARG, "sym_eigvals: NULL pointer or count < 1");
-  if (nmax < 1 || nmax > kEigMax) return fail(c, CMSVD_E_SHAPE, "sym_eigvals: nmax must be in 1..512");
+  if (nmax < 1 || nmax > 4096) return fail(c, CMSVD_E_SHAPE, "sym_eigvals: nmax must be in 1..4096");
   if (kw < 1 || kw > nmax) return fail(c, CMSVD_E_ARG, "sym_eigvals: kw must be in 1..nmax");
   for (int32_t p = 0; p < count; ++p)
     if (n[p] < 0 || n[p] > nmax) return fail(c, CMSVD_E_SHAPE, "sym_eigvals: n[p] outside 0..nmax");

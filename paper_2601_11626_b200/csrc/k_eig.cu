@@ -1724,7 +1724,8 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
                                 double* trace, double* scratch, double* save, int64_t save_stride) {
   if (save && !tridiag_can_save(c, nmax)) return cudaErrorInvalidValue;
   if (nprob <= 0) return cudaSuccess;
-  if (nmax > kTriMax) return cudaErrorInvalidValue;
+  // n > 512 only through the two-stage reduction (cluster verification); the pair path stays <= 512
+  if (nmax > kTriMax && (!c.eig_sbr || save)) return cudaErrorInvalidValue;
   const size_t smem = tridiag_smem(nmax, kw);
   const int nstride = nmax;
   double* dd = scratch;
@@ -1768,7 +1769,7 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
     c.launches += 1;
   } else if (c.eig_sbr) {
     // two-stage reduction (k_sbr.cu): dense -> band (BLAS3-shaped panels) -> tridiagonal (bulge chasing)
-    e = ensure(c.ws[WS_SBR], sbr_ws_bytes(nprob));
+    e = ensure(c.ws[WS_SBR], sbr_ws_bytes(nprob, nmax));
     if (e != cudaSuccess) return e;
     e = launch_tridiag_sbr(c, const_cast<double*>(G), ld_in, stride_in, d_ns, nprob, nmax, d_thr, kw, nstride, dd, ee,
                            gsh, cnt, trace, (double*)c.ws[WS_SBR].p);

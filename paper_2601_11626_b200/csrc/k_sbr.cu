@@ -40,7 +40,8 @@ namespace cmsvd {
 #endif
 
 constexpr int kSB = 16;                 // band half-width of stage 1
-constexpr int kSBMax = 512;             // largest n
+constexpr int kSBMax = 512;             // largest n with the panel and the band in shared memory (pair path)
+constexpr int kSBBig = 4096;            // largest n (cluster verification, global-memory panel and band)
 constexpr int kSBLdb = 2 * kSB + 2;     // band storage: diagonals 0 .. 2 kSB (band + bulge), padded so that a
                                         // row walk (stride kSBLdb - 1 doubles) is free of bank conflicts
 constexpr int kSymmRows = 128;          // rows of A22 per k_sbr_symm CTA
@@ -50,11 +51,28 @@ constexpr int kSyrTile = 64;            // k_sbr_syr2k tile
 constexpr int kSyrThreads = 256;
 constexpr int kPanelThreads = 256;
 constexpr int kChaseWarps = 12;
-constexpr int kMBlocks = kSBMax / kSymmRows;   // M partials per problem
 
-// workspace per problem (doubles): V (kSBMax x kSB), Y/W (kSBMax x kSB), T (kSB x kSB), M (kMBlocks x kSB x kSB)
-constexpr int64_t kSbrV = (int64_t)kSBMax * kSB;
-constexpr int64_t kSbrPer = 2 * kSbrV + kSB * kSB + (int64_t)kMBlocks * kSB * kSB;
+// workspace per problem (doubles): V (ldv x kSB), Y/W (ldv x kSB), T (kSB x kSB), M (ceil(ldv/128) x kSB x kSB),
+// and for n > kSBMax the band of the chase (n x kSBLdb, global memory)
+struct SbrWs {
+  int ldv;            // rows of V and Y per problem (kSBMax for n <= kSBMax, else n rounded up to 128)
+  int64_t per;        // doubles per problem
+  int64_t band;       // offset of the global-memory band (0: band in shared memory)
+  __host__ __device__ int64_t vsz() const { return (int64_t)ldv * kSB; }
+};
+static SbrWs sbr_layout(int nmax) {
+  SbrWs L;
+  L.ldv = nmax <= kSBMax ? kSBMax : (nmax + 127) / 128 * 128;
+  const int64_t nmb = (L.ldv + kSymmRows - 1) / kSymmRows;
+  L.per = 2 * L.vsz() + kSB * kSB + nmb * kSB * kSB;
+  L.band = 0;
+  if (nmax > kSBMax) {
+    L.band = L.per;
+    L.per += (int64_t)nmax * kSBLdb;
+  }
+  L.per = (L.per + 15) / 16 * 16;   // 128-byte problem stride (TMA alignment)
+  return L;
+}
 
 __device__ __forceinline__ double sbr_rcp(double q) {
   double y;
@@ -73,12 +91,16 @@ __host__ __device__ __forceinline__ int sbr_panels(int n) { return n >= kSB + 2 
 // ---------------------------------------------------------------------------
 constexpr int kPanelLd = kSBMax + 1;   // column stride of the staged panel (odd: conflict-free columns)
 
+template <bool SMEM>
 __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict__ G, int64_t ld, int64_t stride,
                                                               const int* __restrict__ ns, int t,
-                                                              double* __restrict__ ws, double* __restrict__ trace) {
+                                                              double* __restrict__ ws, double* __restrict__ trace,
+                                                              const SbrWs L) {
   extern __shared__ __align__(16) double psm[];
-  double* P = psm;                                   // [kSB][kPanelLd]
-  double* red = P + kSB * kPanelLd;                  // [16][16] partial sums
+  // SMEM: the panel is staged in shared memory ([kSB][kPanelLd]); else (n > kSBMax) it is factored in place
+  // in global memory (its entries below the band hold the reflectors afterwards, which the band never reads)
+  constexpr int kPld = SMEM ? kPanelLd : 0;
+  double* red = psm + (SMEM ? kSB * kPanelLd : 0);   // [16][16] partial sums
   double* scal = red + 256;                          // beta, tau per column; S (16 x 16), T (16 x 16)
   double* S = scal + 2 * kSB;
   double* T = S + kSB * kSB;
@@ -93,16 +115,19 @@ __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict_
   }
   if (t >= sbr_panels(n)) return;
   const int c0 = t * kSB, R0 = c0 + kSB, np = n - R0;
-  // stage the panel
-  for (int e = tid; e < kSB * np; e += kPanelThreads) {
-    const int c = e / np, i = e - c * np;
-    P[c * kPanelLd + i] = A[(int64_t)(c0 + c) * ld + R0 + i];
+  double* P = SMEM ? psm : A + (int64_t)c0 * ld + R0;
+  const int64_t ldp = SMEM ? (int64_t)kPld : ld;
+  if (SMEM) {   // stage the panel
+    for (int e = tid; e < kSB * np; e += kPanelThreads) {
+      const int c = e / np, i = e - c * np;
+      P[c * ldp + i] = A[(int64_t)(c0 + c) * ld + R0 + i];
+    }
   }
   __syncthreads();
   const int g = tid >> 4, cc = tid & 15;   // 16 row groups x 16 columns
   const int kmax = min(kSB, np);
   for (int k = 0; k < kmax; ++k) {
-    double* x = P + k * kPanelLd;
+    double* x = P + k * ldp;
     // squared norm below the diagonal element
     double part = 0.0;
     for (int i = k + 1 + tid; i < np; i += kPanelThreads) part = fma(x[i], x[i], part);
@@ -128,7 +153,7 @@ __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict_
     if (tau != 0.0) {
       double d = 0.0;
       if (cc > k) {
-        const double* pc = P + cc * kPanelLd;
+        const double* pc = P + cc * ldp;
         if (g == 0) d = pc[k];
         for (int i = k + 1 + g; i < np; i += 16) d = fma(x[i], pc[i], d);
       }
@@ -139,7 +164,7 @@ __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict_
 #pragma unroll
         for (int q = 0; q < 16; ++q) s += red[q * 16 + cc];
         s *= tau;
-        double* pc = P + cc * kPanelLd;
+        double* pc = P + cc * ldp;
         if (g == 0) pc[k] -= s;
         for (int i = k + 1 + g; i < np; i += 16) pc[i] = fma(-s, x[i], pc[i]);
       }
@@ -151,8 +176,8 @@ __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict_
     const int j = tid >> 4, k = tid & 15;
     double s = 0.0;
     if (j < k && k < kmax) {
-      const double* vj = P + j * kPanelLd;
-      const double* vk = P + k * kPanelLd;
+      const double* vj = P + j * ldp;
+      const double* vk = P + k * ldp;
       s = vj[k];
       for (int i = k + 1; i < np; ++i) s = fma(vj[i], vk[i], s);
     }
@@ -174,17 +199,17 @@ __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict_
   }
   __syncthreads();
   // outputs: R into the band (rows R0 .. R0 + 15 of the panel columns, upper triangle), V, T
-  double* Vw = ws + (int64_t)p * kSbrPer;
-  double* Tw = Vw + 2 * kSbrV;
+  double* Vw = ws + (int64_t)p * L.per;
+  double* Tw = Vw + 2 * L.vsz();
   for (int e = tid; e < kSB * kSB; e += kPanelThreads) {
     const int c = e >> 4, k = e & 15;   // R[k][c], k <= c
-    if (k <= c && k < np) A[(int64_t)(c0 + c) * ld + R0 + k] = P[c * kPanelLd + k];
+    if (SMEM && k <= c && k < np) A[(int64_t)(c0 + c) * ld + R0 + k] = P[c * ldp + k];
     Tw[e] = T[e];
   }
   for (int e = tid; e < kSB * np; e += kPanelThreads) {
     const int c = e / np, i = e - c * np;
-    const double v = (i < c) ? 0.0 : (i == c ? 1.0 : P[c * kPanelLd + i]);
-    Vw[(int64_t)c * kSBMax + i] = (c < kmax) ? v : 0.0;
+    const double v = (i < c) ? 0.0 : (i == c ? 1.0 : P[c * ldp + i]);
+    Vw[(int64_t)c * L.ldv + i] = (c < kmax) ? v : 0.0;
   }
 }
 
@@ -205,7 +230,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
 
 __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __restrict__ G, int64_t ld,
                                                                 int64_t stride, const int* __restrict__ ns, int t,
-                                                                double* __restrict__ ws) {
+                                                                double* __restrict__ ws, const SbrWs L) {
   extern __shared__ __align__(16) double ssm[];
   const int p = blockIdx.x;
   const int n = ns[p];
@@ -215,8 +240,8 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __re
   if (I0 >= np) return;
   const int tid = threadIdx.x;
   const double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;   // A22(i, j) at A[j * ld + i]
-  const double* Vw = ws + (int64_t)p * kSbrPer;
-  double* Yw = const_cast<double*>(Vw) + kSbrV;
+  const double* Vw = ws + (int64_t)p * L.per;
+  double* Yw = const_cast<double*>(Vw) + L.vsz();
   const int i0 = tid & 63, h = tid >> 6;
   const int imax = min(kSymmRows, np - I0);
   // stage the slice starting at column J0 into buffer `buf` (At[j][i] = A22(I0 + i, J0 + j), Vs[j][c])
@@ -248,7 +273,7 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __re
     for (int e = tid; e < kSymmJB * kSB; e += kSymmThreads) {
       const int jj = e >> 4, c = e & 15;
       const bool ok = jj < jmax;
-      cp_async8(Vs + e, ok ? Vw + (int64_t)c * kSBMax + J0 + jj : Vw, ok);
+      cp_async8(Vs + e, ok ? Vw + (int64_t)c * L.ldv + J0 + jj : Vw, ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -293,7 +318,7 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __re
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int c = 0; c < 8; ++c) Xs[(i0 + 64 * a) * kX + 8 * h + c] = acc[a][c];
-  const double* Tw = Vw + 2 * kSbrV;
+  const double* Tw = Vw + 2 * L.vsz();
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) Ts[e] = Tw[e];
   __syncthreads();
   for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
@@ -301,16 +326,16 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __re
     double y = 0.0;
     for (int l = 0; l <= c; ++l) y = fma(Xs[i * kX + l], Ts[l * kSB + c], y);
     Ys[i * kX + c] = (i < imax) ? y : 0.0;
-    if (i < imax) Yw[(int64_t)c * kSBMax + I0 + i] = y;
+    if (i < imax) Yw[(int64_t)c * L.ldv + I0 + i] = y;
   }
   // the block's V rows in shared memory ([l][i], coalesced) for M_b = V_b^T Y_b
   double* Vb = Ys + kSymmRows * kX;
   for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
     const int l = e >> 7, i = e & 127;
-    Vb[e] = i < imax ? Vw[(int64_t)l * kSBMax + I0 + i] : 0.0;
+    Vb[e] = i < imax ? Vw[(int64_t)l * L.ldv + I0 + i] : 0.0;
   }
   __syncthreads();
-  double* Mw = const_cast<double*>(Vw) + 2 * kSbrV + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
+  double* Mw = const_cast<double*>(Vw) + 2 * L.vsz() + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) {
     const int a = e >> 4, c = e & 15;
     double s = 0.0;
@@ -322,7 +347,8 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __re
 // ---------------------------------------------------------------------------
 // Stage 1c: W = Y - V Z in place of Y, Z = 1/2 T^T sum_b M_b (16 x 16), rows [128 b, 128 b + 128).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t, double* __restrict__ ws) {
+__global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t, double* __restrict__ ws,
+                                                 const SbrWs L) {
   __shared__ double Ms[kSB * kSB], Zs[kSB * kSB];
   const int p = blockIdx.x;
   const int n = ns[p];
@@ -331,9 +357,9 @@ __global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t
   const int I0 = blockIdx.y * kSymmRows;
   if (I0 >= np) return;
   const int tid = threadIdx.x;
-  double* Vw = ws + (int64_t)p * kSbrPer;
-  double* Yw = Vw + kSbrV;
-  const double* Tw = Vw + 2 * kSbrV;
+  double* Vw = ws + (int64_t)p * L.per;
+  double* Yw = Vw + L.vsz();
+  const double* Tw = Vw + 2 * L.vsz();
   const double* Mw = Tw + kSB * kSB;
   const int nmb = (np + kSymmRows - 1) / kSymmRows;
   double s = 0.0;
@@ -352,10 +378,10 @@ __global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t
     const int c = e >> 7, i = e & 127;
     if (i >= imax) continue;
     const int64_t gi = I0 + i;
-    double w = Yw[(int64_t)c * kSBMax + gi];
+    double w = Yw[(int64_t)c * L.ldv + gi];
 #pragma unroll
-    for (int l = 0; l < kSB; ++l) w = fma(-Vw[(int64_t)l * kSBMax + gi], Zs[l * kSB + c], w);
-    Yw[(int64_t)c * kSBMax + gi] = w;
+    for (int l = 0; l < kSB; ++l) w = fma(-Vw[(int64_t)l * L.ldv + gi], Zs[l * kSB + c], w);
+    Yw[(int64_t)c * L.ldv + gi] = w;
   }
 }
 
@@ -366,7 +392,7 @@ __global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSyrThreads, 2) k_sbr_syr2k(double* __restrict__ G, int64_t ld, int64_t stride,
                                                                 const int* __restrict__ ns, int t,
-                                                                const double* __restrict__ ws) {
+                                                                const double* __restrict__ ws, const SbrWs L) {
   __shared__ __align__(16) double VI[kSB * kSyrTile], WI[kSB * kSyrTile], VJ[kSB * kSyrTile], WJ[kSB * kSyrTile];
   const int p = blockIdx.x;
   const int n = ns[p];
@@ -391,16 +417,16 @@ __global__ void __launch_bounds__(kSyrThreads, 2) k_sbr_syr2k(double* __restrict
       const bool ok = I0 + i < np && J0 + j < np && (!diag || i >= j);
       a[r2][c] = ok ? A[(int64_t)(J0 + j) * ld + I0 + i] : 0.0;
     }
-  const double* Vw = ws + (int64_t)p * kSbrPer;
-  const double* Ww = Vw + kSbrV;
+  const double* Vw = ws + (int64_t)p * L.per;
+  const double* Ww = Vw + L.vsz();
   // [l][i] layouts: column l of V / W for the tile rows (coalesced global loads)
   for (int e = tid; e < kSyrTile * kSB; e += kSyrThreads) {
     const int l = e >> 6, i = e & 63;
     const int gi = I0 + i, gj = J0 + i;
-    VI[e] = gi < np ? Vw[(int64_t)l * kSBMax + gi] : 0.0;
-    WI[e] = gi < np ? Ww[(int64_t)l * kSBMax + gi] : 0.0;
-    VJ[e] = gj < np ? Vw[(int64_t)l * kSBMax + gj] : 0.0;
-    WJ[e] = gj < np ? Ww[(int64_t)l * kSBMax + gj] : 0.0;
+    VI[e] = gi < np ? Vw[(int64_t)l * L.ldv + gi] : 0.0;
+    WI[e] = gi < np ? Ww[(int64_t)l * L.ldv + gi] : 0.0;
+    VJ[e] = gj < np ? Vw[(int64_t)l * L.ldv + gj] : 0.0;
+    WJ[e] = gj < np ? Ww[(int64_t)l * L.ldv + gj] : 0.0;
   }
   __syncthreads();
 #pragma unroll 4
@@ -545,7 +571,7 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
                                                                     const __grid_constant__ CUtensorMap tup,
                                                                     const double* __restrict__ G, int64_t ld,
                                                                     int64_t stride, const int* __restrict__ ns,
-                                                                    int t, double* __restrict__ ws) {
+                                                                    int t, double* __restrict__ ws, const SbrWs L) {
   extern __shared__ __align__(1024) double ysm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(ysm + kSymmNS * kSymmStage);
   const int p = blockIdx.x;
@@ -556,8 +582,8 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
   if (I0 >= np) return;
   const int tid = threadIdx.x;
   const double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;   // A22(i, j) at A[j * ld + i]
-  const double* Vw = ws + (int64_t)p * kSbrPer;
-  double* Yw = const_cast<double*>(Vw) + kSbrV;
+  const double* Vw = ws + (int64_t)p * L.per;
+  double* Yw = const_cast<double*>(Vw) + L.vsz();
   const int i0 = tid & 63, h = tid >> 6;
   const int imax = min(kSymmRows, np - I0);
   if (tid == 0) {
@@ -585,7 +611,7 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
     for (int e = tid; e < kSymmJT * kSB; e += kSymmThreads) {
       const int jj = e >> 4, c = e & 15;
       const bool ok = jj < jmax;
-      cp_async8(Vs + e, ok ? Vw + (int64_t)c * kSBMax + J0 + jj : Vw, ok);
+      cp_async8(Vs + e, ok ? Vw + (int64_t)c * L.ldv + J0 + jj : Vw, ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -677,7 +703,7 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int c = 0; c < 8; ++c) Xs[(i0 + 64 * a) * kX + 8 * h + c] = acc[a][c];
-  const double* Tw = Vw + 2 * kSbrV;
+  const double* Tw = Vw + 2 * L.vsz();
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) Ts[e] = Tw[e];
   __syncthreads();
   for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
@@ -685,16 +711,16 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
     double y = 0.0;
     for (int l = 0; l <= c; ++l) y = fma(Xs[i * kX + l], Ts[l * kSB + c], y);
     Ys[i * kX + c] = (i < imax) ? y : 0.0;
-    if (i < imax) Yw[(int64_t)c * kSBMax + I0 + i] = y;
+    if (i < imax) Yw[(int64_t)c * L.ldv + I0 + i] = y;
   }
   // the block's V rows in shared memory ([l][i], coalesced) for M_b = V_b^T Y_b
   double* Vb = Ys + kSymmRows * kX;
   for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
     const int l = e >> 7, i = e & 127;
-    Vb[e] = i < imax ? Vw[(int64_t)l * kSBMax + I0 + i] : 0.0;
+    Vb[e] = i < imax ? Vw[(int64_t)l * L.ldv + I0 + i] : 0.0;
   }
   __syncthreads();
-  double* Mw = const_cast<double*>(Vw) + 2 * kSbrV + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
+  double* Mw = const_cast<double*>(Vw) + 2 * L.vsz() + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) {
     const int a = e >> 4, c = e & 15;
     double s = 0.0;
@@ -830,18 +856,22 @@ __device__ __forceinline__ void chase_task(double* __restrict__ Bd, double* __re
 
 // FLAGS: per-sweep progress flags (each warp owns whole sweeps and polls its predecessor's counter)
 // instead of one CTA barrier per wavefront time step
-template <bool FLAGS>
+// GB: n > kSBMax, the band lives in the problem's global workspace (L.band) instead of shared memory
+template <bool FLAGS, bool GB>
 __global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double* __restrict__ G, int64_t ld,
                                                                     int64_t stride, const int* __restrict__ ns,
                                                                     const double* __restrict__ thr, int kw,
                                                                     int nstride, double* __restrict__ dout,
                                                                     double* __restrict__ e2out,
                                                                     double* __restrict__ gsh,
-                                                                    int* __restrict__ cnt_out) {
+                                                                    int* __restrict__ cnt_out,
+                                                                    double* __restrict__ ws, const SbrWs L, int nmax) {
   extern __shared__ __align__(16) double bsm[];
-  double* Bd = bsm;                                              // [kSBMax][kSBLdb]
-  volatile int* prog = reinterpret_cast<volatile int*>(Bd + kSBMax * kSBLdb);   // steps done per sweep
-  double* vsc = Bd + kSBMax * kSBLdb + kSBMax / 2 + 32 * (threadIdx.x >> 5);    // per-warp v / w scratch
+  const int nb = GB ? nmax : kSBMax;
+  double* Bd = GB ? ws + (int64_t)blockIdx.x * L.per + L.band : bsm;               // [n][kSBLdb]
+  double* sbase = GB ? bsm : bsm + (int64_t)kSBMax * kSBLdb;
+  volatile int* prog = reinterpret_cast<volatile int*>(sbase);                     // steps done per sweep
+  double* vsc = sbase + nb / 2 + 2 + 32 * (threadIdx.x >> 5);                      // per-warp p scratch
   const int p = blockIdx.x;
   const int n = ns[p];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -978,11 +1008,11 @@ static bool sbr_tensor_map(CUtensorMap* map, double* G, int64_t ld, int64_t stri
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static bool sbr_ws_map(CUtensorMap* map, double* base, int nprob) {
+static bool sbr_ws_map(CUtensorMap* map, double* base, int nprob, const SbrWs& L) {
   auto fn = sbr_encode_fn();
   if (!fn || ((uintptr_t)base % 16) != 0) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)kSBMax, (cuuint64_t)kSB, (cuuint64_t)nprob};
-  cuuint64_t strides[2] = {(cuuint64_t)kSBMax * sizeof(double), (cuuint64_t)kSbrPer * sizeof(double)};
+  cuuint64_t dims[3] = {(cuuint64_t)L.ldv, (cuuint64_t)kSB, (cuuint64_t)nprob};
+  cuuint64_t strides[2] = {(cuuint64_t)L.ldv * sizeof(double), (cuuint64_t)L.per * sizeof(double)};
   cuuint32_t box[3] = {(cuuint32_t)kSyrTile, (cuuint32_t)kSB, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -990,14 +1020,17 @@ static bool sbr_ws_map(CUtensorMap* map, double* base, int nprob) {
          CUDA_SUCCESS;
 }
 
-size_t sbr_ws_bytes(int nprob) { return (size_t)nprob * kSbrPer * sizeof(double); }
+size_t sbr_ws_bytes(int nprob, int nmax) { return (size_t)nprob * sbr_layout(nmax).per * sizeof(double); }
 
-// Stage 1 + stage 2 for nprob problems (n = ns[p] <= 512, G destroyed): writes dd, ee (e^2), gsh, cnt,
-// trace like k_tridiag.  ws: sbr_ws_bytes(nprob) bytes.
+// Stage 1 + stage 2 for nprob problems (n = ns[p] <= nmax <= kSBBig, G destroyed): writes dd, ee (e^2), gsh,
+// cnt, trace like k_tridiag.  ws: sbr_ws_bytes(nprob, nmax) bytes.  n <= 512 (the pair path): panel and band
+// in shared memory; larger n (N1 cluster verification): panel in place and band in global memory.
 cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, const int* d_ns, int nprob, int nmax,
                                const double* d_thr, int kw, int nstride, double* dd, double* ee, double* gsh,
                                int* cnt, double* trace, double* ws) {
-  if (nmax > kSBMax) return cudaErrorInvalidValue;
+  if (nmax > kSBBig) return cudaErrorInvalidValue;
+  const SbrWs L = sbr_layout(nmax);
+  const bool big = nmax > kSBMax;
   const int npan = sbr_panels(nmax);
   const size_t psmem = ((size_t)kSB * kPanelLd + 256 + 2 * kSB + 2 * kSB * kSB) * sizeof(double);
   const size_t ssmem = (size_t)2 * kSymmBuf * sizeof(double);
@@ -1013,7 +1046,7 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
                                (size_t)kSymmRows * (kSB + 1) * 2 + kSB * kSB + kSymmRows * kSB + 4) * sizeof(double);
   // V and W (kSBMax x kSB per problem, column-major, problem stride kSbrPer) as 3-D maps, 64 x 16 boxes
   CUtensorMap tmv, tmw;
-  const bool tma2 = tma && sbr_ws_map(&tmv, ws, nprob) && sbr_ws_map(&tmw, ws + kSbrV, nprob);
+  const bool tma2 = tma && sbr_ws_map(&tmv, ws, nprob, L) && sbr_ws_map(&tmw, ws + L.vsz(), nprob, L);
   const size_t tsmem = ((size_t)kSyrTile * kSyrTile + 4 * kSB * kSyrTile + 2) * sizeof(double);
   if (tma) {
     cudaError_t e2 = cudaFuncSetAttribute(k_sbr_syr2k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
@@ -1021,7 +1054,7 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     e2 = cudaFuncSetAttribute(k_sbr_symm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ymem);
     if (e2 != cudaSuccess) return e2;
   }
-  cudaError_t e = cudaFuncSetAttribute(k_sbr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+  cudaError_t e = cudaFuncSetAttribute(k_sbr_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_sbr_symm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)symm_smem);
   if (e != cudaSuccess) return e;
@@ -1029,44 +1062,49 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   for (int t = 0; t < std::max(npan, 1); ++t) {
     const int np0 = nmax - (t + 1) * kSB;   // largest trailing size at this panel
     int pr = prof_begin(c, PC_SBR_PANEL);
-    k_sbr_panel<<<nprob, kPanelThreads, psmem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace);
+    if (big)
+      k_sbr_panel<false><<<nprob, kPanelThreads, (256 + 2 * kSB + 2 * kSB * kSB) * sizeof(double), c.stream>>>(
+          G, ld, stride, d_ns, t, ws, trace, L);
+    else
+      k_sbr_panel<true><<<nprob, kPanelThreads, psmem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L);
     c.launches += 1;
     prof_end(c, pr);
     if (t >= npan) break;
     const int nrb = (np0 + kSymmRows - 1) / kSymmRows;
     pr = prof_begin(c, PC_SBR_SYMM);
     if (tma)
-      k_sbr_symm_tma<<<dim3(nprob, nrb), kSymmThreads, ymem, c.stream>>>(tlo, tup, G, ld, stride, d_ns, t, ws);
+      k_sbr_symm_tma<<<dim3(nprob, nrb), kSymmThreads, ymem, c.stream>>>(tlo, tup, G, ld, stride, d_ns, t, ws, L);
     else
-      k_sbr_symm<<<dim3(nprob, nrb), kSymmThreads, symm_smem, c.stream>>>(G, ld, stride, d_ns, t, ws);
+      k_sbr_symm<<<dim3(nprob, nrb), kSymmThreads, symm_smem, c.stream>>>(G, ld, stride, d_ns, t, ws, L);
     c.launches += 1;
     prof_end(c, pr);
     pr = prof_begin(c, PC_SBR_SYR2K);
-    k_sbr_w<<<dim3(nprob, nrb), 256, 0, c.stream>>>(d_ns, t, ws);
+    k_sbr_w<<<dim3(nprob, nrb), 256, 0, c.stream>>>(d_ns, t, ws, L);
     c.launches += 1;
     const int nt = (np0 + kSyrTile - 1) / kSyrTile;
     if (tma2)
       k_sbr_syr2k_tma<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, tsmem, c.stream>>>(tmap, tmv, tmw, d_ns, t);
     else
-      k_sbr_syr2k<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, 0, c.stream>>>(G, ld, stride, d_ns, t, ws);
+      k_sbr_syr2k<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, 0, c.stream>>>(G, ld, stride, d_ns, t, ws, L);
     c.launches += 1;
     prof_end(c, pr);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  const size_t csmem = ((size_t)kSBMax * kSBLdb + kSBMax / 2 + 32 * kChaseWarps) * sizeof(double);
+  const size_t csmem = ((big ? 0 : (size_t)kSBMax * kSBLdb) + (size_t)(big ? nmax : kSBMax) / 2 + 2 +
+                        32 * kChaseWarps) * sizeof(double);
   const int pr = prof_begin(c, PC_SBR_CHASE);
-  if (c.chase_flags) {
-    e = cudaFuncSetAttribute(k_sbr_chase<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
-    if (e != cudaSuccess) return e;
-    k_sbr_chase<true><<<nprob, kChaseWarps * 32, csmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd, ee,
-                                                                    gsh, cnt);
-  } else {
-    e = cudaFuncSetAttribute(k_sbr_chase<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
-    if (e != cudaSuccess) return e;
-    k_sbr_chase<false><<<nprob, kChaseWarps * 32, csmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd, ee,
-                                                                     gsh, cnt);
-  }
+#define SBR_CHASE(F_, GB_)                                                                                        \
+  do {                                                                                                            \
+    e = cudaFuncSetAttribute(k_sbr_chase<F_, GB_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);       \
+    if (e != cudaSuccess) return e;                                                                               \
+    k_sbr_chase<F_, GB_><<<nprob, kChaseWarps * 32, csmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride,  \
+                                                                        dd, ee, gsh, cnt, ws, L, nmax);           \
+  } while (0)
+  if (big) SBR_CHASE(false, true);
+  else if (c.chase_flags) SBR_CHASE(true, false);
+  else SBR_CHASE(false, false);
+#undef SBR_CHASE
   c.launches += 1;
   prof_end(c, pr);
   return cudaGetLastError();

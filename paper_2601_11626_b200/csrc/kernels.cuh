@@ -30,8 +30,8 @@ bool tridiag_can_save(const Ctx& c, int nmax);
 cudaError_t launch_topk_vectors(Ctx& c, int n, int kw, const double* d, const double* save, const double* ev,
                                 const double* gsh, double* Z);
 size_t tridiag_scratch_bytes(int nprob, int nmax);
-// two-stage (dense -> band -> tridiagonal) reduction for 160 < n <= 512 (k_sbr.cu); outputs as k_tridiag
-size_t sbr_ws_bytes(int nprob);
+// two-stage (dense -> band -> tridiagonal) reduction for 160 < n <= 4096 (k_sbr.cu); outputs as k_tridiag
+size_t sbr_ws_bytes(int nprob, int nmax);
 cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, const int* d_ns, int nprob, int nmax,
                                const double* d_thr, int kw, int nstride, double* dd, double* ee, double* gsh,
                                int* cnt, double* trace, double* ws);

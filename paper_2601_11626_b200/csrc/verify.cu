@@ -84,6 +84,8 @@ __global__ void __launch_bounds__(256) k_gram(const float* const* __restrict__ X
     if (_e != cudaSuccess) return cuda_fail(c, _e, where); \
   } while (0)
 
+constexpr int64_t kVerifyMax = 4096;
+
 Status do_cluster_verify(Ctx& c, int32_t r, const int32_t* assign, int32_t n_clusters, double* exact_err2,
                          double* total, int64_t* mem) {
   if (c.count <= 0) return fail(c, CMSVD_E_STATE, "cluster_verify: no collection registered");
@@ -104,9 +106,11 @@ Status do_cluster_verify(Ctx& c, int32_t r, const int32_t* assign, int32_t n_clu
     if (members[g].empty()) return fail(c, CMSVD_E_ARG, "cluster_verify: empty cluster " + std::to_string(g));
     for (int i : members[g]) ncol[g] += c.n[i];
     dim[g] = std::min<int64_t>(m, ncol[g]);
-    if (dim[g] > kEigMax)
+    // the Gram's eigenvalues: n <= 512 by the pair path's solvers, up to kVerifyMax by the two-stage
+    // reduction with the panel and the band in global memory (k_sbr.cu)
+    if (dim[g] > kVerifyMax)
       return fail(c, CMSVD_E_SHAPE, "cluster_verify: min(m, N_c) = " + std::to_string(dim[g]) + " > " +
-                                        std::to_string(kEigMax) + " for cluster " + std::to_string(g));
+                                        std::to_string(kVerifyMax) + " for cluster " + std::to_string(g));
     dmax = std::max<int>(dmax, (int)dim[g]);
     xoff[g + 1] = xoff[g] + ((m * ncol[g] + 31) / 32) * 32;
   }

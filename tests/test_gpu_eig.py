@@ -38,7 +38,7 @@ def check(ev, mats, kw):
         assert np.all(np.diff(ev[p, :k]) <= 1e-12 * abs(ref[0]))
 
 
-@pytest.mark.parametrize("n", [2, 3, 31, 64, 96, 128, 150, 160, 161, 176, 200, 255, 256, 300, 384, 500, 511, 512])
+@pytest.mark.parametrize("n", [2, 3, 31, 64, 96, 128, 150, 160, 161, 176, 200, 255, 256, 300, 384, 500, 511, 512, 513, 700, 1024])
 def test_eigvals_vs_lapack(cm, n):
     R = np.random.default_rng(n)
     mats = [gram(R, n), gram(R, n, decay=1.0)]

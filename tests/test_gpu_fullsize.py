@@ -133,3 +133,52 @@ def test_config5_greedy_knn(cm, N, r):
     cache = load(f"greedy_config5_N{N}_r{r}")
     col = synth.config5(N=N, r=r)
     _check_greedy(cm, col, r, cache, "a2_s1_e0.1_k16", cm.ALG_APPROX, cm.SORT_RESIDUAL, 0.1, 16, cm.RAW)
+
+
+def _clusters(assign):
+    return [sorted(np.flatnonzero(assign == c).tolist()) for c in range(int(np.max(assign)) + 1)]
+
+
+def test_verify_wide_clusters_config5(cm):
+    """N1 beyond 512: the 32 Alg. 3 clusters of config 5 (N = 512, r = 16, kNN 16) are 2048 x 1024
+    concatenations (min(m, N_c) = 1024: two-stage reduction with the panel and the band in global memory);
+    exact errors of three clusters against the oracle's Gram route, every cluster within eps (P13)."""
+    import oracle
+    from tolerances import assert_err2
+    col = synth.config5(N=512, r=16)
+    with cm.Context(0) as ctx:
+        ctx.register(torch.from_numpy(col.blocks).cuda())
+        ctx.block_spectra(col.r)
+        g = ctx.cluster(cm.ALG_APPROX, 0.1, sort=cm.SORT_RESIDUAL, knn=16)
+        assign = np.asarray(g["assign"], np.int32)
+        v = ctx.cluster_verify(assign)
+    groups = _clusters(assign)
+    assert max(len(gr) for gr in groups) * col.n > 512
+    pick = [0, len(groups) // 2, len(groups) - 1]
+    sub = sorted({b for i in pick for b in groups[i]})
+    sp = oracle.block_spectra(np.ascontiguousarray(col.blocks[sub]))
+    local = [[sub.index(b) for b in groups[i]] for i in pick]
+    ex = oracle.exact_groups(sp, local, col.r)
+    assert_err2(v["exact_err2"][pick], ex, v["total"][pick], "config5 wide cluster exact error")
+    assert np.all(v["rel"] <= 0.1 * (1 + 1e-6))
+    assert np.all(v["exact_err2"] <= np.asarray(g["err2"]) * (1 + 2e-3) + 1e-7 * v["total"])   # inc >= exact
+
+
+def test_verify_config4_clusters(cm):
+    """N1 on the headline config: the 4 Alg. 3 clusters are 4096 x 65536 concatenations (row Gram of
+    4096^2).  Exact error <= the incremental certificate (P6 / F3), rel <= eps = 0.15 (P13), compression
+    ratio sum m n_i / sum mem_c with mem_c = r_c (m + N_c) (reading A23)."""
+    col = synth.config4()
+    with cm.Context(0) as ctx:
+        ctx.register(torch.from_numpy(col.blocks).cuda())
+        ctx.block_spectra(col.r)
+        g = ctx.cluster(cm.ALG_APPROX, 0.15, sort=cm.SORT_RESIDUAL, operand=cm.TRUNC)
+        assign = np.asarray(g["assign"], np.int32)
+        v = ctx.cluster_verify(assign)
+    assert len(g["clusters"]) == 4
+    assert np.all(v["exact_err2"] <= np.asarray(g["err2"]) * (1 + 2e-3) + 1e-7 * v["total"])
+    assert np.all(v["rel"] <= 0.15)
+    ncs = np.array([col.n * len(c) for c in _clusters(assign)])
+    mem = np.minimum(col.m * ncs, np.minimum(col.r, np.minimum(col.m, ncs)) * (col.m + ncs))
+    assert np.array_equal(v["mem"], mem)
+    assert abs(v["ratio"] - col.m * col.n * col.N / mem.sum()) < 1e-12 * v["ratio"]

@@ -182,3 +182,18 @@ def test_exact_groups_vs_lapack_and_union():
     union = np.sort(np.concatenate([sa, sb]))[::-1]
     for r in range(0, 8):
         assert abs(oracle.exact_groups(sp, [[0, 1]], r)[0] - np.sum(union[r:] ** 2)) < 1e-12 * 60
+
+
+def test_exact_groups_wide_gram_route():
+    """Concatenations wider than 512 (both Gram orientations) take the Gram + own tridiagonal route:
+    against LAPACK's SVD of the explicit concatenation."""
+    R = np.random.default_rng(12)
+    for m, widths in [(560, [300, 300]), (700, [200, 350, 100])]:
+        blocks = [(R.standard_normal((m, w)) * np.linspace(2, 0.1, w)).astype(np.float32).astype(np.float64)
+                  for w in widths]
+        sp = oracle.block_spectra(blocks)
+        M = np.concatenate(blocks, axis=1)
+        s = np.linalg.svd(M, compute_uv=False)
+        for r in (1, 40, 300):
+            got = oracle.exact_groups(sp, [list(range(len(blocks)))], r)[0]
+            assert abs(got - np.sum(s[r:] ** 2)) <= 1e-10 * np.sum(s ** 2), (m, r)

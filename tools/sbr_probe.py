@@ -32,7 +32,7 @@ with cm.Context(0) as ctx:
         print(f"n={n} count={count} kw={kw} wall {wall * 1e3:.1f} ms (incl. H2D of {count * n * n * 8 / 1e9:.2f} GB):",
               {k: round(v[0], 3) for k, v in prof.items() if v[1]}, flush=True)
 err = 0.0
-for u in range(8):
+for u in range(min(8, count)):
     ref = np.linalg.eigvalsh(uniq[u])[::-1][:kw]
     err = max(err, float(np.max(np.abs(ev[u] - ref)) / ref[0]))
 print(f"max |ev - eigvalsh| / lambda_1 = {err:.3e}")
