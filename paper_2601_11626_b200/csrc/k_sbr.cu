@@ -694,38 +694,66 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
     }
     __syncthreads();   // this stage is reissued kSymmNS - 1 steps later
   }
-  // X rows to shared memory (row stride 17), then Y = X T and M_b = V_b^T Y_b
+  // epilogue: X rows to shared memory (row stride 17); Y = X T by row (thread = row, X row in registers);
+  // M_b = V_b^T Y_b = (V_b^T X_b) T with Q = V_b^T X_b as 8 row-group partials (16 independent
+  // accumulators per thread, no long serial chains), then M = Q T
   constexpr int kX = kSB + 1;
-  double* Xs = ysm;
-  double* Ts = Xs + kSymmRows * kX;
-  double* Ys = Ts + kSB * kSB;
+  double* Xs = ysm;                          // [128][17]
+  double* Ts = Xs + kSymmRows * kX;          // [16][16]
+  double* Vb = Ts + kSB * kSB;               // [16][128]
+  double* Qp = Vb + kSB * kSymmRows;         // [8][16][16] partials, then Q [16][16]
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int c = 0; c < 8; ++c) Xs[(i0 + 64 * a) * kX + 8 * h + c] = acc[a][c];
   const double* Tw = Vw + 2 * L.vsz();
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) Ts[e] = Tw[e];
-  __syncthreads();
-  for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
-    const int c = e >> 7, i = e & 127;
-    double y = 0.0;
-    for (int l = 0; l <= c; ++l) y = fma(Xs[i * kX + l], Ts[l * kSB + c], y);
-    Ys[i * kX + c] = (i < imax) ? y : 0.0;
-    if (i < imax) Yw[(int64_t)c * L.ldv + I0 + i] = y;
-  }
-  // the block's V rows in shared memory ([l][i], coalesced) for M_b = V_b^T Y_b
-  double* Vb = Ys + kSymmRows * kX;
   for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
     const int l = e >> 7, i = e & 127;
     Vb[e] = i < imax ? Vw[(int64_t)l * L.ldv + I0 + i] : 0.0;
   }
   __syncthreads();
+  {
+    const int i = tid;                       // kSymmThreads == kSymmRows: one row per thread
+    double x[kSB];
+#pragma unroll
+    for (int l = 0; l < kSB; ++l) x[l] = Xs[i * kX + l];
+    if (i < imax) {
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) {
+        double y = 0.0;
+#pragma unroll
+        for (int l = 0; l <= c; ++l) y = fma(x[l], Ts[l * kSB + c], y);
+        Yw[(int64_t)c * L.ldv + I0 + i] = y;
+      }
+    }
+    // Q partial over rows 16 g .. 16 g + 15 for row a of V_b^T: thread (g = tid >> 4, a = tid & 15)
+    const int g = tid >> 4, a = tid & 15;
+    double q[kSB];
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) q[c] = 0.0;
+    for (int ii = 16 * g; ii < 16 * g + 16; ++ii) {
+      const double v = Vb[a * kSymmRows + ii];
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) q[c] = fma(v, Xs[ii * kX + c], q[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) Qp[(g * kSB + a) * kSB + c] = q[c];
+  }
+  __syncthreads();
   double* Mw = const_cast<double*>(Vw) + 2 * L.vsz() + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
-  for (int e = tid; e < kSB * kSB; e += kSymmThreads) {
+  for (int e = tid; e < kSB * kSB; e += kSymmThreads) {     // Q = sum of the 8 partials (fixed order)
+    double t = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) t += Qp[g * kSB * kSB + e];
+    Vb[e] = t;                                               // Q [a][c] (V_b no longer needed)
+  }
+  __syncthreads();
+  for (int e = tid; e < kSB * kSB; e += kSymmThreads) {     // M = Q T  (T upper triangular)
     const int a = e >> 4, c = e & 15;
-    double s = 0.0;
-    for (int i = 0; i < imax; ++i) s = fma(Vb[a * kSymmRows + i], Ys[i * kX + c], s);
-    Mw[e] = s;
+    double m = 0.0;
+    for (int l = 0; l <= c; ++l) m = fma(Vb[a * kSB + l], Ts[l * kSB + c], m);
+    Mw[e] = m;
   }
 }
 
@@ -1043,7 +1071,7 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
                    sbr_tensor_map(&tlo, G, ld, stride, nprob, kSymmRows, kSymmJT, CU_TENSOR_MAP_SWIZZLE_NONE) &&
                    sbr_tensor_map(&tup, G, ld, stride, nprob, 16, kSymmRows, CU_TENSOR_MAP_SWIZZLE_128B);
   const size_t ymem = std::max((size_t)kSymmNS * kSymmStage + 4,
-                               (size_t)kSymmRows * (kSB + 1) * 2 + kSB * kSB + kSymmRows * kSB + 4) * sizeof(double);
+                               (size_t)kSymmRows * (kSB + 1) + kSB * kSB + 2 * kSymmRows * kSB + 4) * sizeof(double);
   // V and W (kSBMax x kSB per problem, column-major, problem stride kSbrPer) as 3-D maps, 64 x 16 boxes
   CUtensorMap tmv, tmw;
   const bool tma2 = tma && sbr_ws_map(&tmv, ws, nprob, L) && sbr_ws_map(&tmw, ws + L.vsz(), nprob, L);
