@@ -124,6 +124,8 @@ struct Ctx {
   bool use_tc = true;                  // tcgen05 contraction kernel (CMSVD_NO_TC=1 selects the SIMT path)
   bool tc_ok = true;                   // every block numerically full column rank (set by block_spectra)
   int gl_batch_mb = 1024;              // in-place global-memory eigen batches (n > 160), MB of matrices per launch
+  bool sbr_fused = false;              // band reduction: look-ahead fused update + product pass (CMSVD_SBR_FUSED=1;
+                                       // measured 24.8 vs 23.0 ms unfused at n = 512: the partials' traffic)
   bool sbr_tma = true;                 // band reduction: TMA tile loads/stores in the rank-32 update (CMSVD_SBR_TMA=0)
   bool chase_flags = false;            // band chase: per-sweep progress flags instead of time-step barriers
   bool eig_sbr = true;                 // n > 160: two-stage (band) reduction instead of the one-stage in-place kernel

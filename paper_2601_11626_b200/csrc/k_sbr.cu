@@ -52,19 +52,30 @@ constexpr int kSyrThreads = 256;
 constexpr int kPanelThreads = 256;
 constexpr int kChaseWarps = 12;
 
-// workspace per problem (doubles): V (ldv x kSB), Y/W (ldv x kSB), T (kSB x kSB), M (ceil(ldv/128) x kSB x kSB),
-// and for n > kSBMax the band of the chase (n x kSBLdb, global memory)
+// workspace per problem (doubles): two sets (panel parity t & 1) of [V (ldv x kSB) | Y/W (ldv x kSB) | T
+// (kSB x kSB)], the M partials (ceil(ldv/128) x kSB x kSB), the fused pass's product partials (one 2 x 64 x kSB
+// slot per lower 64 x 64 tile), and for n > kSBMax the band of the chase (n x kSBLdb, global memory)
 struct SbrWs {
   int ldv;            // rows of V and Y per problem (kSBMax for n <= kSBMax, else n rounded up to 128)
+  int ntm;            // 64-row tiles per side
   int64_t per;        // doubles per problem
+  int64_t set;        // doubles per V / W / T set
+  int64_t moff;       // offset of the M partials
+  int64_t poff;       // offset of the product partials
   int64_t band;       // offset of the global-memory band (0: band in shared memory)
   __host__ __device__ int64_t vsz() const { return (int64_t)ldv * kSB; }
+  __host__ __device__ double* vp(double* ws, int p, int par) const { return ws + (int64_t)p * per + par * set; }
+  __host__ __device__ double* mp(double* ws, int p) const { return ws + (int64_t)p * per + moff; }
 };
 static SbrWs sbr_layout(int nmax) {
   SbrWs L;
   L.ldv = nmax <= kSBMax ? kSBMax : (nmax + 127) / 128 * 128;
+  L.ntm = (L.ldv + 63) / 64;
   const int64_t nmb = (L.ldv + kSymmRows - 1) / kSymmRows;
-  L.per = 2 * L.vsz() + kSB * kSB + nmb * kSB * kSB;
+  L.set = (2 * L.vsz() + kSB * kSB + 15) / 16 * 16;
+  L.moff = 2 * L.set;
+  L.poff = L.moff + nmb * kSB * kSB;
+  L.per = L.poff + (int64_t)L.ntm * (L.ntm + 1) / 2 * 2 * 64 * kSB;
   L.band = 0;
   if (nmax > kSBMax) {
     L.band = L.per;
@@ -95,7 +106,7 @@ template <bool SMEM>
 __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict__ G, int64_t ld, int64_t stride,
                                                               const int* __restrict__ ns, int t,
                                                               double* __restrict__ ws, double* __restrict__ trace,
-                                                              const SbrWs L) {
+                                                              const SbrWs L, int par) {
   extern __shared__ __align__(16) double psm[];
   // SMEM: the panel is staged in shared memory ([kSB][kPanelLd]); else (n > kSBMax) it is factored in place
   // in global memory (its entries below the band hold the reflectors afterwards, which the band never reads)
@@ -199,16 +210,16 @@ __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict_
   }
   __syncthreads();
   // outputs: R into the band (rows R0 .. R0 + 15 of the panel columns, upper triangle), V, T
-  double* Vw = ws + (int64_t)p * L.per;
+  double* Vw = L.vp(ws, p, par);
   double* Tw = Vw + 2 * L.vsz();
   for (int e = tid; e < kSB * kSB; e += kPanelThreads) {
     const int c = e >> 4, k = e & 15;   // R[k][c], k <= c
     if (SMEM && k <= c && k < np) A[(int64_t)(c0 + c) * ld + R0 + k] = P[c * ldp + k];
     Tw[e] = T[e];
   }
-  for (int e = tid; e < kSB * np; e += kPanelThreads) {
-    const int c = e / np, i = e - c * np;
-    const double v = (i < c) ? 0.0 : (i == c ? 1.0 : P[c * ldp + i]);
+  for (int e = tid; e < kSB * L.ldv; e += kPanelThreads) {
+    const int c = e / L.ldv, i = e - c * L.ldv;
+    const double v = (i >= np || i < c) ? 0.0 : (i == c ? 1.0 : P[c * ldp + i]);
     Vw[(int64_t)c * L.ldv + i] = (c < kmax) ? v : 0.0;
   }
 }
@@ -230,7 +241,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
 
 __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __restrict__ G, int64_t ld,
                                                                 int64_t stride, const int* __restrict__ ns, int t,
-                                                                double* __restrict__ ws, const SbrWs L) {
+                                                                double* __restrict__ ws, const SbrWs L, int par) {
   extern __shared__ __align__(16) double ssm[];
   const int p = blockIdx.x;
   const int n = ns[p];
@@ -240,7 +251,7 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __re
   if (I0 >= np) return;
   const int tid = threadIdx.x;
   const double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;   // A22(i, j) at A[j * ld + i]
-  const double* Vw = ws + (int64_t)p * L.per;
+  const double* Vw = L.vp(ws, p, par);
   double* Yw = const_cast<double*>(Vw) + L.vsz();
   const int i0 = tid & 63, h = tid >> 6;
   const int imax = min(kSymmRows, np - I0);
@@ -335,7 +346,7 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __re
     Vb[e] = i < imax ? Vw[(int64_t)l * L.ldv + I0 + i] : 0.0;
   }
   __syncthreads();
-  double* Mw = const_cast<double*>(Vw) + 2 * L.vsz() + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
+  double* Mw = L.mp(ws, p) + (int64_t)blockIdx.y * kSB * kSB;
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) {
     const int a = e >> 4, c = e & 15;
     double s = 0.0;
@@ -348,7 +359,7 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm(const double* __re
 // Stage 1c: W = Y - V Z in place of Y, Z = 1/2 T^T sum_b M_b (16 x 16), rows [128 b, 128 b + 128).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t, double* __restrict__ ws,
-                                                 const SbrWs L) {
+                                                 const SbrWs L, int par) {
   __shared__ double Ms[kSB * kSB], Zs[kSB * kSB];
   const int p = blockIdx.x;
   const int n = ns[p];
@@ -357,10 +368,10 @@ __global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t
   const int I0 = blockIdx.y * kSymmRows;
   if (I0 >= np) return;
   const int tid = threadIdx.x;
-  double* Vw = ws + (int64_t)p * L.per;
+  double* Vw = L.vp(ws, p, par);
   double* Yw = Vw + L.vsz();
   const double* Tw = Vw + 2 * L.vsz();
-  const double* Mw = Tw + kSB * kSB;
+  const double* Mw = L.mp(ws, p);
   const int nmb = (np + kSymmRows - 1) / kSymmRows;
   double s = 0.0;
   for (int b = 0; b < nmb; ++b) s += Mw[b * kSB * kSB + tid];
@@ -392,7 +403,8 @@ __global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSyrThreads, 2) k_sbr_syr2k(double* __restrict__ G, int64_t ld, int64_t stride,
                                                                 const int* __restrict__ ns, int t,
-                                                                const double* __restrict__ ws, const SbrWs L) {
+                                                                const double* __restrict__ ws, const SbrWs L,
+                                                                int par) {
   __shared__ __align__(16) double VI[kSB * kSyrTile], WI[kSB * kSyrTile], VJ[kSB * kSyrTile], WJ[kSB * kSyrTile];
   const int p = blockIdx.x;
   const int n = ns[p];
@@ -417,7 +429,7 @@ __global__ void __launch_bounds__(kSyrThreads, 2) k_sbr_syr2k(double* __restrict
       const bool ok = I0 + i < np && J0 + j < np && (!diag || i >= j);
       a[r2][c] = ok ? A[(int64_t)(J0 + j) * ld + I0 + i] : 0.0;
     }
-  const double* Vw = ws + (int64_t)p * L.per;
+  const double* Vw = L.vp(const_cast<double*>(ws), p, par);
   const double* Ww = Vw + L.vsz();
   // [l][i] layouts: column l of V / W for the tile rows (coalesced global loads)
   for (int e = tid; e < kSyrTile * kSB; e += kSyrThreads) {
@@ -466,6 +478,14 @@ using tc::mbar_init;
 using tc::fence_mbar_init;
 using tc::mbar_wait;
 using tc::fence_proxy_async;
+
+// D = A B + D for one 8 x 8 x 4 fp64 tile (DMMA): a = A[g][t], b = B[t][g], (c0, c1) = C[g][2t .. 2t+1],
+// g = lane / 4, t = lane % 4 (measured 37.1 TF/s on B200, tools/dmma_probe.cu)
+__device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
@@ -571,7 +591,8 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
                                                                     const __grid_constant__ CUtensorMap tup,
                                                                     const double* __restrict__ G, int64_t ld,
                                                                     int64_t stride, const int* __restrict__ ns,
-                                                                    int t, double* __restrict__ ws, const SbrWs L) {
+                                                                    int t, double* __restrict__ ws, const SbrWs L,
+                                                                    int par) {
   extern __shared__ __align__(1024) double ysm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(ysm + kSymmNS * kSymmStage);
   const int p = blockIdx.x;
@@ -582,7 +603,7 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
   if (I0 >= np) return;
   const int tid = threadIdx.x;
   const double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;   // A22(i, j) at A[j * ld + i]
-  const double* Vw = ws + (int64_t)p * L.per;
+  const double* Vw = L.vp(ws, p, par);
   double* Yw = const_cast<double*>(Vw) + L.vsz();
   const int i0 = tid & 63, h = tid >> 6;
   const int imax = min(kSymmRows, np - I0);
@@ -741,7 +762,7 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
     for (int c = 0; c < kSB; ++c) Qp[(g * kSB + a) * kSB + c] = q[c];
   }
   __syncthreads();
-  double* Mw = const_cast<double*>(Vw) + 2 * L.vsz() + kSB * kSB + (int64_t)blockIdx.y * kSB * kSB;
+  double* Mw = L.mp(ws, p) + (int64_t)blockIdx.y * kSB * kSB;
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) {     // Q = sum of the 8 partials (fixed order)
     double t = 0.0;
 #pragma unroll
@@ -750,6 +771,271 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
   }
   __syncthreads();
   for (int e = tid; e < kSB * kSB; e += kSymmThreads) {     // M = Q T  (T upper triangular)
+    const int a = e >> 4, c = e & 15;
+    double m = 0.0;
+    for (int l = 0; l <= c; ++l) m = fma(Vb[a * kSB + l], Ts[l * kSB + c], m);
+    Mw[e] = m;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused stage 1 (look-ahead): one pass over the trailing matrix per panel.
+//   k_sbr_strip(t)  : A22(t)[:, 0:16] -= V_t W_t[0:16]^T + W_t V_t[0:16]^T (the strip that holds panel t + 1),
+//                     so that panel t + 1 can be factored before the rest of A22(t) is updated;
+//   k_sbr_panel(t+1): its QR (V_{t+1}, T_{t+1}, R into the band);
+//   k_sbr_fused(t)  : per lower 64 x 64 tile of A22(t) (TMA box of 66 rows: the padded pitch makes both
+//                     product orientations conflict-free), the rank-32 update with (V_t, W_t) (strip columns
+//                     excepted), then on fp64 tensor cores (DMMA) the products with V_{t+1} of the updated
+//                     tile: X_I += A V'_J and X_J += A^T V'_I, where V' is V_{t+1} shifted by the 16 strip rows
+//                     (TMA boxes starting at row -16: zero-filled), written as per-tile partials;
+//   k_sbr_reduce(t+1): X = the partials in fixed order, Y_{t+1} = X T_{t+1}, M partials;  k_sbr_w(t+1).
+// The trailing matrix is read and written once per panel (the separate symmetric product's full read is
+// gone); V/W/T of panels t and t + 1 live in the two parity sets of the workspace.
+// ---------------------------------------------------------------------------
+constexpr int kFP = 66;   // row pitch of the fused tile (TMA box rows)
+
+__global__ void __launch_bounds__(128) k_sbr_strip(double* __restrict__ G, int64_t ld, int64_t stride,
+                                                   const int* __restrict__ ns, int t, double* __restrict__ ws,
+                                                   const SbrWs L, int par) {
+  __shared__ double VS[kSB * kSB], WS[kSB * kSB];
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int i = blockIdx.y * 128 + threadIdx.x;
+  const double* Vw = L.vp(ws, p, par);
+  const double* Ww = Vw + L.vsz();
+  for (int e = threadIdx.x; e < kSB * kSB; e += 128) {   // rows 0..15 of V_t, W_t: [j][l]
+    const int j = e >> 4, l = e & 15;
+    VS[e] = Vw[(int64_t)l * L.ldv + j];
+    WS[e] = Ww[(int64_t)l * L.ldv + j];
+  }
+  __syncthreads();
+  if (i >= np) return;
+  double vi[kSB], wi[kSB];
+#pragma unroll
+  for (int l = 0; l < kSB; ++l) {
+    vi[l] = Vw[(int64_t)l * L.ldv + i];
+    wi[l] = Ww[(int64_t)l * L.ldv + i];
+  }
+  double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;
+  const int jmax = min(kSB, i + 1);   // lower storage: j <= i
+  for (int j = 0; j < jmax; ++j) {
+    double a = A[(int64_t)j * ld + i];
+#pragma unroll
+    for (int l = 0; l < kSB; ++l) a = fma(-vi[l], WS[j * kSB + l], fma(-wi[l], VS[j * kSB + l], a));
+    A[(int64_t)j * ld + i] = a;
+  }
+}
+
+__global__ void __launch_bounds__(kSyrThreads, 2) k_sbr_fused(
+    const __grid_constant__ CUtensorMap tmap66, const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmw,
+    const __grid_constant__ CUtensorMap tvn, double* __restrict__ G, int64_t ld, int64_t stride,
+    const int* __restrict__ ns, int t, double* __restrict__ ws, const SbrWs L) {
+  extern __shared__ __align__(128) double fsm[];
+  double* At = fsm;                          // [64 cols][kFP rows]
+  double* VI = At + kSyrTile * kFP;          // V_t / W_t rows of the tile: [l][64]
+  double* WI = VI + kSB * kSyrTile;
+  double* VJ = WI + kSB * kSyrTile;
+  double* WJ = VJ + kSB * kSyrTile;
+  double* PI = WJ + kSB * kSyrTile;          // V_{t+1} rows (shifted by 16): [l][kFP]
+  double* PJ = PI + kSB * kFP;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(PJ + kSB * kFP);
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const bool next = t + 1 < sbr_panels(n);
+  const int nt = (np + kSyrTile - 1) / kSyrTile;
+  int q = blockIdx.y, ti = 0;
+  while (q > ti) { ++ti; q -= ti; }
+  const int tj = q;
+  if (ti >= nt) return;
+  const int I0 = ti * kSyrTile, J0 = tj * kSyrTile;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const unsigned bytes = (unsigned)((kSyrTile * kFP + 4 * kSB * kSyrTile + (next ? 2 * kSB * kFP : 0)) *
+                                      sizeof(double));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    tma_load_3d(At, &tmap66, R0 + I0, R0 + J0, p, bar);
+    tma_load_3d(VI, &tmv, I0, 0, p, bar);
+    tma_load_3d(WI, &tmw, I0, 0, p, bar);
+    tma_load_3d(VJ, &tmv, J0, 0, p, bar);
+    tma_load_3d(WJ, &tmw, J0, 0, p, bar);
+    if (next) {
+      tma_load_3d(PI, &tvn, I0 - kSB, 0, p, bar);
+      tma_load_3d(PJ, &tvn, J0 - kSB, 0, p, bar);
+    }
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  const int tx = tid & 31, ty = tid >> 5;
+  const bool diag = ti == tj;
+  double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;
+  double a[2][8];
+#pragma unroll
+  for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) a[r2][c] = At[(8 * ty + c) * kFP + tx + 32 * r2];
+#pragma unroll 4
+  for (int l = 0; l < kSB; ++l) {
+    const double vi0 = VI[l * kSyrTile + tx], vi1 = VI[l * kSyrTile + tx + 32];
+    const double wi0 = WI[l * kSyrTile + tx], wi1 = WI[l * kSyrTile + tx + 32];
+    const double2* vj2 = reinterpret_cast<const double2*>(VJ + l * kSyrTile + 8 * ty);
+    const double2* wj2 = reinterpret_cast<const double2*>(WJ + l * kSyrTile + 8 * ty);
+#pragma unroll
+    for (int c2 = 0; c2 < 4; ++c2) {
+      const double2 vj = vj2[c2], wj = wj2[c2];
+      a[0][2 * c2] = fma(-vi0, wj.x, fma(-wi0, vj.x, a[0][2 * c2]));
+      a[1][2 * c2] = fma(-vi1, wj.x, fma(-wi1, vj.x, a[1][2 * c2]));
+      a[0][2 * c2 + 1] = fma(-vi0, wj.y, fma(-wi0, vj.y, a[0][2 * c2 + 1]));
+      a[1][2 * c2 + 1] = fma(-vi1, wj.y, fma(-wi1, vj.y, a[1][2 * c2 + 1]));
+    }
+  }
+  __syncthreads();   // every thread's tile reads are done before the updated values are written back
+#pragma unroll
+  for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int i = tx + 32 * r2, j = 8 * ty + c;
+      const bool strip = tj == 0 && j < kSB;          // updated (and partly factored) by strip / panel t+1
+      const bool ok = I0 + i < np && J0 + j < np && (!diag || i >= j) && !strip;
+      if (ok) {
+        A[(int64_t)(J0 + j) * ld + I0 + i] = a[r2][c];
+        At[j * kFP + i] = a[r2][c];
+        if (diag && i > j) At[i * kFP + j] = a[r2][c];   // full symmetric diagonal tile for the product
+      }
+    }
+  if (!next) return;
+  __syncthreads();
+  // products on fp64 tensor cores: warps 0..3 X_I rows 16 w .. + 15 (A V'_J); warps 4..7 X_J rows
+  // 16 (w - 4) .. + 15 (A^T V'_I), off-diagonal tiles only.  Fragments: a = M(g, t), b = V(t, g), c = X(g, 2t..)
+  const int lane = tid & 31, wq = tid >> 5, gq = lane >> 2, tq = lane & 3;
+  const bool tr = wq >= 4;
+  if (tr && diag) return;
+  const int rb = 16 * (wq & 3);
+  const double* Pb = tr ? PI : PJ;
+  double cx[2][2][2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ntile = 0; ntile < 2; ++ntile) cx[mt][ntile][0] = cx[mt][ntile][1] = 0.0;
+#pragma unroll 4
+  for (int ks = 0; ks < kSyrTile / 4; ++ks) {
+    const int k = 4 * ks + tq;
+    double bf[2];
+#pragma unroll
+    for (int ntile = 0; ntile < 2; ++ntile) bf[ntile] = Pb[(8 * ntile + gq) * kFP + k];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = rb + 8 * mt + gq;
+      double av = tr ? At[r * kFP + k] : At[k * kFP + r];   // A^T(r, k) = A(k, r) / A(r, k)
+      av = ((tr ? I0 : J0) + k < np) ? av : 0.0;            // columns outside the problem (stale padding)
+      dmma_f64(cx[mt][0][0], cx[mt][0][1], av, bf[0]);
+      dmma_f64(cx[mt][1][0], cx[mt][1][1], av, bf[1]);
+    }
+  }
+  double* part = ws + (int64_t)p * L.per + L.poff + ((int64_t)blockIdx.y * 2 + (tr ? 1 : 0)) * 64 * kSB;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ntile = 0; ntile < 2; ++ntile) {
+      const int r = rb + 8 * mt + gq, c = 8 * ntile + 2 * tq;
+      part[r * kSB + c] = cx[mt][ntile][0];
+      part[r * kSB + c + 1] = cx[mt][ntile][1];
+    }
+}
+
+// X_{t+1} rows [128 b, 128 b + 128) (A22(t+1) coordinates; A22(t) row i' + 16) from the partials of pass t in
+// fixed order, then Y_{t+1} = X T_{t+1} and the M partial of the block (as the symmetric-product kernel).
+__global__ void __launch_bounds__(kSymmRows) k_sbr_reduce(const int* __restrict__ ns, int t1,
+                                                          double* __restrict__ ws, const SbrWs L, int par) {
+  extern __shared__ __align__(16) double rsm[];
+  constexpr int kX = kSB + 1;
+  double* Xs = rsm;                          // [128][17]
+  double* Ts = Xs + kSymmRows * kX;          // [16][16]
+  double* Vb = Ts + kSB * kSB;               // [16][128]
+  double* Qp = Vb + kSB * kSymmRows;         // [8][16][16]
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t1 >= sbr_panels(n)) return;
+  const int R0 = (t1 + 1) * kSB, np = n - R0;    // panel t1's trailing size; pass t1 - 1 had np + 16 rows
+  const int I0 = blockIdx.y * kSymmRows;
+  if (I0 >= np) return;
+  const int tid = threadIdx.x;
+  const int imax = min(kSymmRows, np - I0);
+  const double* Vw = L.vp(ws, p, par);
+  double* Yw = const_cast<double*>(Vw) + L.vsz();
+  const double* Tw = Vw + 2 * L.vsz();
+  const double* part = ws + (int64_t)p * L.per + L.poff;
+  const int nt = (np + kSB + kSyrTile - 1) / kSyrTile;   // tiles per side of pass t1 - 1
+  {
+    const int ip = I0 + tid;                      // A22(t1) row
+    double x[kSB];
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) x[c] = 0.0;
+    if (tid < imax) {
+      const int i = ip + kSB;                     // A22(t1 - 1) row
+      const int ti = i / kSyrTile, r = i % kSyrTile;
+      for (int tj = 0; tj <= ti; ++tj) {          // X_I partials of tiles (ti, tj)
+        const double* src = part + ((int64_t)(ti * (ti + 1) / 2 + tj) * 2) * 64 * kSB + r * kSB;
+#pragma unroll
+        for (int c = 0; c < kSB; ++c) x[c] += src[c];
+      }
+      for (int tk = ti + 1; tk < nt; ++tk) {      // X_J partials of tiles (tk, ti)
+        const double* src = part + ((int64_t)(tk * (tk + 1) / 2 + ti) * 2 + 1) * 64 * kSB + r * kSB;
+#pragma unroll
+        for (int c = 0; c < kSB; ++c) x[c] += src[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) Xs[tid * kX + c] = x[c];
+  }
+  for (int e = tid; e < kSB * kSB; e += kSymmRows) Ts[e] = Tw[e];
+  for (int e = tid; e < kSymmRows * kSB; e += kSymmRows) {
+    const int l = e >> 7, i = e & 127;
+    Vb[e] = i < imax ? Vw[(int64_t)l * L.ldv + I0 + i] : 0.0;
+  }
+  __syncthreads();
+  {
+    const int i = tid;
+    double x[kSB];
+#pragma unroll
+    for (int l = 0; l < kSB; ++l) x[l] = Xs[i * kX + l];
+    if (i < imax) {
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) {
+        double y = 0.0;
+#pragma unroll
+        for (int l = 0; l <= c; ++l) y = fma(x[l], Ts[l * kSB + c], y);
+        Yw[(int64_t)c * L.ldv + I0 + i] = y;
+      }
+    }
+    const int g = tid >> 4, a = tid & 15;
+    double qv[kSB];
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) qv[c] = 0.0;
+    for (int ii = 16 * g; ii < 16 * g + 16; ++ii) {
+      const double v = Vb[a * kSymmRows + ii];
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) qv[c] = fma(v, Xs[ii * kX + c], qv[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) Qp[(g * kSB + a) * kSB + c] = qv[c];
+  }
+  __syncthreads();
+  double* Mw = L.mp(ws, p) + (int64_t)blockIdx.y * kSB * kSB;
+  for (int e = tid; e < kSB * kSB; e += kSymmRows) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) s2 += Qp[g * kSB * kSB + e];
+    Vb[e] = s2;
+  }
+  __syncthreads();
+  for (int e = tid; e < kSB * kSB; e += kSymmRows) {
     const int a = e >> 4, c = e & 15;
     double m = 0.0;
     for (int l = 0; l <= c; ++l) m = fma(Vb[a * kSB + l], Ts[l * kSB + c], m);
@@ -1036,12 +1322,12 @@ static bool sbr_tensor_map(CUtensorMap* map, double* G, int64_t ld, int64_t stri
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static bool sbr_ws_map(CUtensorMap* map, double* base, int nprob, const SbrWs& L) {
+static bool sbr_ws_map(CUtensorMap* map, double* base, int nprob, const SbrWs& L, int rows) {
   auto fn = sbr_encode_fn();
   if (!fn || ((uintptr_t)base % 16) != 0) return false;
   cuuint64_t dims[3] = {(cuuint64_t)L.ldv, (cuuint64_t)kSB, (cuuint64_t)nprob};
   cuuint64_t strides[2] = {(cuuint64_t)L.ldv * sizeof(double), (cuuint64_t)L.per * sizeof(double)};
-  cuuint32_t box[3] = {(cuuint32_t)kSyrTile, (cuuint32_t)kSB, 1};
+  cuuint32_t box[3] = {(cuuint32_t)rows, (cuuint32_t)kSB, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
@@ -1072,50 +1358,103 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
                    sbr_tensor_map(&tup, G, ld, stride, nprob, 16, kSymmRows, CU_TENSOR_MAP_SWIZZLE_128B);
   const size_t ymem = std::max((size_t)kSymmNS * kSymmStage + 4,
                                (size_t)kSymmRows * (kSB + 1) + kSB * kSB + 2 * kSymmRows * kSB + 4) * sizeof(double);
-  // V and W (kSBMax x kSB per problem, column-major, problem stride kSbrPer) as 3-D maps, 64 x 16 boxes
-  CUtensorMap tmv, tmw;
-  const bool tma2 = tma && sbr_ws_map(&tmv, ws, nprob, L) && sbr_ws_map(&tmw, ws + L.vsz(), nprob, L);
+  // V and W of both parity sets as 3-D maps (64 x 16 boxes; V of the next panel also as 66 x 16 boxes)
+  CUtensorMap tmv[2], tmw[2], tvn[2], tm66;
+  bool tma2 = tma;
+  for (int q2 = 0; q2 < 2 && tma2; ++q2)
+    tma2 = sbr_ws_map(&tmv[q2], ws + q2 * L.set, nprob, L, kSyrTile) &&
+           sbr_ws_map(&tmw[q2], ws + q2 * L.set + L.vsz(), nprob, L, kSyrTile) &&
+           sbr_ws_map(&tvn[q2], ws + q2 * L.set, nprob, L, kFP);
+  const bool fused = tma2 && c.sbr_fused &&
+                     sbr_tensor_map(&tm66, G, ld, stride, nprob, kFP, kSyrTile, CU_TENSOR_MAP_SWIZZLE_NONE);
   const size_t tsmem = ((size_t)kSyrTile * kSyrTile + 4 * kSB * kSyrTile + 2) * sizeof(double);
+  const size_t fsmem = ((size_t)kSyrTile * kFP + 4 * kSB * kSyrTile + 2 * kSB * kFP + 2) * sizeof(double);
+  const size_t rsmem = ((size_t)kSymmRows * (kSB + 1) + kSB * kSB + 2 * kSB * kSymmRows) * sizeof(double);
   if (tma) {
     cudaError_t e2 = cudaFuncSetAttribute(k_sbr_syr2k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
     if (e2 != cudaSuccess) return e2;
     e2 = cudaFuncSetAttribute(k_sbr_symm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ymem);
+    if (e2 != cudaSuccess) return e2;
+    e2 = cudaFuncSetAttribute(k_sbr_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+    if (e2 != cudaSuccess) return e2;
+    e2 = cudaFuncSetAttribute(k_sbr_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
     if (e2 != cudaSuccess) return e2;
   }
   cudaError_t e = cudaFuncSetAttribute(k_sbr_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_sbr_symm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)symm_smem);
   if (e != cudaSuccess) return e;
-  // trace (panel 0 kernel) even when there are no panels
-  for (int t = 0; t < std::max(npan, 1); ++t) {
-    const int np0 = nmax - (t + 1) * kSB;   // largest trailing size at this panel
-    int pr = prof_begin(c, PC_SBR_PANEL);
+  auto panel = [&](int t) {
+    const int pr = prof_begin(c, PC_SBR_PANEL);
     if (big)
       k_sbr_panel<false><<<nprob, kPanelThreads, (256 + 2 * kSB + 2 * kSB * kSB) * sizeof(double), c.stream>>>(
-          G, ld, stride, d_ns, t, ws, trace, L);
+          G, ld, stride, d_ns, t, ws, trace, L, t & 1);
     else
-      k_sbr_panel<true><<<nprob, kPanelThreads, psmem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L);
+      k_sbr_panel<true><<<nprob, kPanelThreads, psmem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L, t & 1);
     c.launches += 1;
     prof_end(c, pr);
-    if (t >= npan) break;
+  };
+  auto symm_w = [&](int t) {
+    const int np0 = nmax - (t + 1) * kSB;
     const int nrb = (np0 + kSymmRows - 1) / kSymmRows;
-    pr = prof_begin(c, PC_SBR_SYMM);
+    int pr = prof_begin(c, PC_SBR_SYMM);
     if (tma)
-      k_sbr_symm_tma<<<dim3(nprob, nrb), kSymmThreads, ymem, c.stream>>>(tlo, tup, G, ld, stride, d_ns, t, ws, L);
+      k_sbr_symm_tma<<<dim3(nprob, nrb), kSymmThreads, ymem, c.stream>>>(tlo, tup, G, ld, stride, d_ns, t, ws, L,
+                                                                         t & 1);
     else
-      k_sbr_symm<<<dim3(nprob, nrb), kSymmThreads, symm_smem, c.stream>>>(G, ld, stride, d_ns, t, ws, L);
+      k_sbr_symm<<<dim3(nprob, nrb), kSymmThreads, symm_smem, c.stream>>>(G, ld, stride, d_ns, t, ws, L, t & 1);
     c.launches += 1;
     prof_end(c, pr);
     pr = prof_begin(c, PC_SBR_SYR2K);
-    k_sbr_w<<<dim3(nprob, nrb), 256, 0, c.stream>>>(d_ns, t, ws, L);
-    c.launches += 1;
-    const int nt = (np0 + kSyrTile - 1) / kSyrTile;
-    if (tma2)
-      k_sbr_syr2k_tma<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, tsmem, c.stream>>>(tmap, tmv, tmw, d_ns, t);
-    else
-      k_sbr_syr2k<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, 0, c.stream>>>(G, ld, stride, d_ns, t, ws, L);
+    k_sbr_w<<<dim3(nprob, nrb), 256, 0, c.stream>>>(d_ns, t, ws, L, t & 1);
     c.launches += 1;
     prof_end(c, pr);
+  };
+  // trace (panel 0 kernel) even when there are no panels
+  panel(0);
+  if (npan > 0) symm_w(0);
+  for (int t = 0; t < npan; ++t) {
+    const int np0 = nmax - (t + 1) * kSB;   // largest trailing size at this panel
+    const int nt = (np0 + kSyrTile - 1) / kSyrTile;
+    if (fused) {
+      // look-ahead: strip of panel t + 1 first, its QR, then one pass over the rest with the product
+      int pr = prof_begin(c, PC_SBR_SYR2K);
+      k_sbr_strip<<<dim3(nprob, (np0 + 127) / 128), 128, 0, c.stream>>>(G, ld, stride, d_ns, t, ws, L, t & 1);
+      c.launches += 1;
+      prof_end(c, pr);
+      if (t + 1 < npan) panel(t + 1);
+      pr = prof_begin(c, PC_SBR_SYR2K);
+      k_sbr_fused<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, fsmem, c.stream>>>(
+          tm66, tmv[t & 1], tmw[t & 1], tvn[(t + 1) & 1], G, ld, stride, d_ns, t, ws, L);
+      c.launches += 1;
+      prof_end(c, pr);
+      if (t + 1 < npan) {
+        const int nrb1 = (np0 - kSB + kSymmRows - 1) / kSymmRows;
+        pr = prof_begin(c, PC_SBR_SYMM);
+        k_sbr_reduce<<<dim3(nprob, std::max(nrb1, 1)), kSymmRows, rsmem, c.stream>>>(d_ns, t + 1, ws, L,
+                                                                                     (t + 1) & 1);
+        c.launches += 1;
+        prof_end(c, pr);
+        pr = prof_begin(c, PC_SBR_SYR2K);
+        k_sbr_w<<<dim3(nprob, std::max(nrb1, 1)), 256, 0, c.stream>>>(d_ns, t + 1, ws, L, (t + 1) & 1);
+        c.launches += 1;
+        prof_end(c, pr);
+      }
+    } else {
+      const int pr = prof_begin(c, PC_SBR_SYR2K);
+      if (tma2)
+        k_sbr_syr2k_tma<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, tsmem, c.stream>>>(tmap, tmv[t & 1],
+                                                                                          tmw[t & 1], d_ns, t);
+      else
+        k_sbr_syr2k<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, 0, c.stream>>>(G, ld, stride, d_ns, t, ws, L,
+                                                                                 t & 1);
+      c.launches += 1;
+      prof_end(c, pr);
+      if (t + 1 < npan) {
+        panel(t + 1);
+        symm_w(t + 1);
+      }
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -76,3 +76,17 @@ def test_structured_spectra(cm):
         ev, _ = ctx.sym_eigvals([A, D, Bnd], 200)
     check(ev, [A, D, Bnd], 200)
     assert np.allclose(ev[0, :50], 9.0, atol=1e-12 * 9) and np.allclose(ev[0, 50:100], 4.0, atol=1e-12 * 9)
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_band_reduction_variants(cm, fused, monkeypatch):
+    """The look-ahead fused pass (CMSVD_SBR_FUSED=1: strip update + panel QR first, then one pass with the
+    rank-32 update and the next product on fp64 tensor cores) and the default two-pass stage 1 agree with
+    LAPACK on ragged sizes, including the global-memory panel / band above 512."""
+    monkeypatch.setenv("CMSVD_SBR_FUSED", fused)
+    R = np.random.default_rng(31)
+    sizes = [512, 400, 161, 257, 640]
+    mats = [gram(R, n, decay=0.4) for n in sizes]
+    with cm.Context(0) as ctx:
+        ev, _ = ctx.sym_eigvals(mats, 160)
+    check(ev, mats, 160)
