@@ -81,6 +81,7 @@ cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
   if (const char* env = getenv("CMSVD_BIG_TC")) h->c.big_tc = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_TC_WIDE")) h->c.tc_wide = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_TC_BIG")) h->c.tc_big = !(env[0] == '0');
+  if (const char* env = getenv("CMSVD_TC_WS")) h->c.tc_ws = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_DUO")) h->c.eig_duo = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_DUO160")) h->c.eig_duo160 = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_COMMIT_TOPK")) h->c.commit_topk = !(env[0] == '0');
@@ -101,7 +102,7 @@ cmsvd_status cmsvd_destroy(cmsvd_ctx ctx) {
   cudaSetDevice(c.device);
   cudaStreamSynchronize(c.stream);
   DevMem* bufs[] = {&c.arena, &c.d_E, &c.d_U, &c.d_sig, &c.d_Ftrunc, &c.d_sig32, &c.d_rank,
-                    &c.d_bdesc, &c.d_adesc_raw, &c.d_adesc_trunc, &c.d_meta64, &c.d_meta32};
+                    &c.d_bdesc, &c.d_adesc_raw, &c.d_adesc_trunc, &c.d_meta64, &c.d_meta32, &c.d_Qp, &c.d_Fp, &c.d_QTp};
   for (DevMem* b : bufs) release(*b);
   for (auto& b : c.ws) release(b);
   for (auto& b : c.cws) release(b);

@@ -115,12 +115,17 @@ struct Ctx {
   DevMem d_Ftrunc;               // fp32 TRUNC operands, m x min(r, k_i) each at foff
   std::vector<int64_t> foff;
   bool trunc_ready = false;
+  // tf32 hi/lo planes of the bases and TRUNC operands (A22 collections with operands wider than 128 columns):
+  // count x 2 x planes_cols x m fp32 each, fed to k_gemm_ws by TMA
+  DevMem d_Qp, d_Fp, d_QTp;   // QTp: the Q planes transposed (count x 2 x m x planes_cols), A operand of R' = F - Q Z
+  int planes_cols = 0;
+  bool planes_ok = false;
   DevMem d_sig32, d_rank, d_bdesc, d_adesc_raw, d_adesc_trunc, d_meta64, d_meta32;
 
   // workspaces (grow-only)
   DevMem ws[16];
   DevMem cws[16];  // cluster-driver state and scratch
-  size_t ws_budget = (size_t)8 << 30;  // bytes of pair workspace per chunk
+  size_t ws_budget = (size_t)24 << 30; // bytes of pair workspace per chunk (config 4: all 2016 pairs in one chunk)
   bool use_tc = true;                  // tcgen05 contraction kernel (CMSVD_NO_TC=1 selects the SIMT path)
   bool tc_ok = true;                   // every block numerically full column rank (set by block_spectra)
   int gl_batch_mb = 1024;              // in-place global-memory eigen batches (n > 160), MB of matrices per launch
@@ -132,6 +137,7 @@ struct Ctx {
   bool eig_rr = true;                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)
   bool zz_syrk = true;                 // w <= 128: Z^T Z by k_syrk_zz instead of k_gemm_tn (CMSVD_ZZ_SYRK=0: off)
   bool tc_big = true;                  // q or w > 128: tcgen05 GEMM tiles instead of SIMT (CMSVD_TC_BIG=0: off)
+  bool tc_ws = true;                   // ... by the warp-specialised TMA-fed kernel on pre-split planes (CMSVD_TC_WS=0: off)
   bool big_tc = true;                  // A22 subspace-iteration products on tcgen05 tiles (CMSVD_BIG_TC=0: SIMT fp64)
   bool tc_wide = true;                 // ... with 256-column tiles for Z = Q^T F (CMSVD_TC_WIDE=0: 128)
   bool eig_duo = true;                 // n <= 128: two problems per CTA with dedicated row warps (CMSVD_EIG_DUO=0: off)

@@ -110,6 +110,7 @@ Status do_register(Ctx& c, int64_t m, int32_t count, const int32_t* n, const flo
     if (!blocks[i]) return fail(c, CMSVD_E_ARG, "register: blocks[" + std::to_string(i) + "] is NULL");
   }
   c.spectra_r = 0;
+  c.planes_ok = false;
   c.trunc_ready = false;
   c.m = m;
   c.count = count;
@@ -431,6 +432,22 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
     c.launches += 1;
     CK(cudaGetLastError(), "spectra: trunc");
   }
+  // tf32 hi/lo planes of U_r and of the TRUNC operands, split once per block (survey K2): the operands of the
+  // TMA-fed contraction kernel k_gemm_ws (bases wider than one 128-column tile only)
+  c.planes_ok = false;
+  if (c.use_tc && c.tc_big && c.tc_ws && kc > 128 && (m & 3) == 0 && (kc & 3) == 0 && N > 0) {
+    const size_t pb = (size_t)N * 2 * kc * m * 4;
+    CK(ensure(c.d_Qp, pb), "spectra: Q planes");
+    CK(ensure(c.d_Fp, pb), "spectra: F planes");
+    CK(ensure(c.d_QTp, pb), "spectra: Q^T planes");
+    const int64_t ustride = c.uoff[1] - c.uoff[0];
+    CK(launch_split_planes(c, (const float*)c.d_U.p, ustride, m, kc, kc, N, (float*)c.d_Qp.p), "spectra: Q planes");
+    CK(launch_split_planes(c, (const float*)c.d_Ftrunc.p, ustride, m, kc, kc, N, (float*)c.d_Fp.p),
+       "spectra: F planes");
+    CK(launch_split_planes_t(c, (const float*)c.d_U.p, ustride, m, kc, N, (float*)c.d_QTp.p), "spectra: Q^T planes");
+    c.planes_cols = kc;
+    c.planes_ok = true;
+  }
   c.sig.resize((size_t)N * nmax);
   c.rank.resize(N);
   CK(cudaMemcpyAsync(c.sig.data(), c.d_sig.p, (size_t)N * nmax * 8, cudaMemcpyDeviceToHost, c.stream), "spectra: d2h");
@@ -461,6 +478,7 @@ Status do_block_spectra(Ctx& c, int32_t r, double* energy, float* sigma, int32_t
     return do_block_spectra_big(c, r, energy, sigma, rank_out);
   }
   c.big = false;
+  c.planes_ok = false;
   for (int i = 0; i < N; ++i)
     if (c.n[i] > m) return fail(c, CMSVD_E_SHAPE, "block_spectra: wide blocks (m < n_i <= 512) are not supported");
   const int nmax = c.nmax;
@@ -609,13 +627,17 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
   const bool use_tc = c.use_tc && c.tc_ok && (full ? dims.qmax : dims.rrmax) <= 128 && dims.wmax <= 128;
   const bool use_tc_big = !use_tc && c.use_tc && c.tc_ok && c.tc_big;  // same precision class, tiled
   const int WMAX = std::max(1, dims.wmax);
+  // ... by the warp-specialised TMA-fed kernel when every operand is a registered block's pre-split planes
+  const bool use_ws = use_tc_big && c.tc_ws && dims.planes && gemm_ws_supported(c, m) && (QMAX & 3) == 0 &&
+                      QMAX <= c.planes_cols && WMAX <= c.planes_cols;
   const int GMAX = std::max(1, dims.rrmax + dims.wmax);
   if (need_mat && ((!tight && GMAX > kEigMax) || WMAX > kEigMax))
     return fail(c, CMSVD_E_SHAPE, "pair_errors: core size r'+w = " + std::to_string(GMAX) + " exceeds " +
                                       std::to_string(kEigMax) + " (large-core path not built yet)");
   size_t per_pair = 0;
   if (need_mat) {
-    per_pair = align_up((size_t)QMAX * WMAX * 4, 256) + (use_tc ? 0 : align_up((size_t)m * WMAX * 4, 256)) +
+    per_pair = align_up((size_t)QMAX * WMAX * 4, 256) * (use_ws ? 3 : 1) +
+               (use_tc ? 0 : align_up((size_t)m * WMAX * 4, 256) * (use_ws ? 2 : 1)) +
                2 * align_up((size_t)WMAX * WMAX * 8, 256) + align_up((size_t)GMAX * GMAX * 8, 256) +
                4 * sizeof(GemmDesc) + 2 * (size_t)r * 8 + (size_t)(2 * GMAX + 4) * 8 + 64;
   }
@@ -632,7 +654,9 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       // carve the workspace
       size_t off = 0;
       auto carve = [&](size_t bytes) { size_t o = off; off += align_up(bytes, 256); return o; };
-      size_t oZ = carve((size_t)Pc * QMAX * WMAX * 4), oR = carve(use_tc ? 256 : (size_t)Pc * m * WMAX * 4);
+      size_t oZ = carve((size_t)Pc * QMAX * WMAX * 4);
+      size_t oR = carve(use_tc ? 256 : (size_t)Pc * m * WMAX * 4 * (use_ws ? 2 : 1));   // ws: hi/lo planes of R'
+      size_t oZp = carve(use_ws ? (size_t)Pc * QMAX * WMAX * 8 : 256);                   // ws: hi/lo planes of Z
       size_t oW = carve((size_t)Pc * WMAX * WMAX * 8), oZZ = carve((size_t)Pc * WMAX * WMAX * 8);
       size_t oG = carve((size_t)Pc * GMAX * GMAX * 8);
       size_t oD = carve((size_t)Pc * 4 * sizeof(GemmDesc));
@@ -670,7 +694,18 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
       c.launches += 1;
       CK(cudaGetLastError(), "pairs: descs");
       prof_end(c, pf);
-      if (use_tc) {
+      if (use_ws) {
+        float* Zp = (float*)(base + oZp);
+        pf = prof_begin(c, PC_PROJ);
+        CK(launch_gemm_ws(c, 0, pr, Pc, d_bd, d_ad, full ? 1 : 0, QMAX, WMAX, Z, Zp, R, W), "pairs: Z = Q^T F (ws)");
+        prof_end(c, pf);
+        pf = prof_begin(c, PC_RESID);
+        CK(launch_gemm_ws(c, 1, pr, Pc, d_bd, d_ad, full ? 1 : 0, QMAX, WMAX, Z, Zp, R, W), "pairs: R = F - Q Z (ws)");
+        prof_end(c, pf);
+        pf = prof_begin(c, PC_GRAM_W);
+        CK(launch_gemm_ws(c, 2, pr, Pc, d_bd, d_ad, full ? 1 : 0, QMAX, WMAX, Z, Zp, R, W), "pairs: W = R^T R (ws)");
+        prof_end(c, pf);
+      } else if (use_tc) {
         // fused tcgen05 3xTF32: Z = Q^T F, R' = F - Q Z (on chip), W' = R'^T R'
         // (tight: Q = U_r, the same projection as the incremental estimator)
         pf = prof_begin(c, PC_PAIR_TC);
@@ -782,7 +817,8 @@ Status do_pair_errors(Ctx& c, const int32_t* pairs, int64_t P, int32_t r, uint32
     return fail(c, CMSVD_E_ARG, "pair_errors: bad operand");
   if (where != CMSVD_HOST && where != CMSVD_DEVICE) return fail(c, CMSVD_E_ARG, "pair_errors: bad `where`");
   const AppDesc* d_ad = (const AppDesc*)(operand == CMSVD_OPERAND_TRUNC ? c.d_adesc_trunc.p : c.d_adesc_raw.p);
-  const Dims dims = block_dims(c, operand);
+  Dims dims = block_dims(c, operand);
+  dims.planes = c.planes_ok && operand == CMSVD_OPERAND_TRUNC;
   if (where == CMSVD_HOST) {
     for (int64_t p = 0; p < 2 * P; ++p)
       if (pairs[p] < 0 || pairs[p] >= c.count)

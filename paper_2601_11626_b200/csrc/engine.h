@@ -16,6 +16,8 @@ struct Dims {
   int qmax = 0;   // projection-basis columns (full range)
   int rrmax = 0;  // tracked top-r columns
   int wmax = 0;   // appended-operand columns
+  bool planes = false;  // every base / appended operand is a registered block's U_r / TRUNC factor (their tf32
+                        // planes exist: k_gemm_ws may be used)
 };
 
 Status fail(Ctx& c, cmsvd_status s, const std::string& msg);

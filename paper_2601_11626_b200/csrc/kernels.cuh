@@ -68,6 +68,15 @@ cudaError_t launch_pair_tc(Ctx& c, const int2* pairs, int64_t P, const BaseDesc*
                            int use_full_basis, int QMAX, int WMAX, float* Zws, double* Wws);
 // batched 3xTF32 tcgen05 GEMM tiles (C = A^T B, or C = C0 - A B with nnsub); out64: fp64 C
 cudaError_t launch_gemm_tc(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN, bool nnsub, bool out64);
+// warp-specialised TMA-fed 3xTF32 contractions on pre-split tf32 planes (k_gemm_ws.cu).  mode 0: Z = Q^T F
+// (fp32 Z + its planes), 1: planes of R' = F - Q Z, 2: W' = R'^T R' (fp64)
+bool gemm_ws_supported(const Ctx& c, int64_t m);
+cudaError_t launch_split_planes(Ctx& c, const float* src, int64_t sstride, int64_t rows, int cols, int cols_dst,
+                                int count, float* dst);
+cudaError_t launch_split_planes_t(Ctx& c, const float* src, int64_t sstride, int64_t rows, int cols, int count,
+                                  float* dst);
+cudaError_t launch_gemm_ws(Ctx& c, int mode, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad,
+                           int use_full, int QMAX, int WMAX, float* Zws, float* Zp, float* Rp, double* Wws);
 // C (fp64) = A B, A: M x K, B: K x N column-major fp32 (3xTF32 tiles)
 cudaError_t launch_gemm_tc_nn64(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN);
 // Y[i] = (float) X[i] for n doubles

@@ -165,17 +165,19 @@ def test_full_size_sampled_pairs(cm, name):
     compare(out, ref, 7, f"{name} full size")
 
 
-@pytest.mark.parametrize("tc_big", ["1", "0"])
-def test_c4_reduced_wide_operands(cm, tc_big, monkeypatch):
-    """r = 192 > 128: bases and TRUNC operands wider than one 128-column tile take the tcgen05 GEMM-tile
-    path (k_gemm_tc: Z = Q^T F, R' = F - Q Z, W' = R'^T R' as 3xTF32 tiles; CMSVD_TC_BIG=0: SIMT).
-    Both against the oracle."""
+@pytest.mark.parametrize("tc_big,tc_ws", [("1", "1"), ("1", "0"), ("0", "1")])
+def test_c4_reduced_wide_operands(cm, tc_big, tc_ws, monkeypatch):
+    """r = 192 > 128: bases and TRUNC operands wider than one 128-column tile take the warp-specialised
+    TMA-fed tcgen05 kernel on pre-split tf32 planes (k_gemm_ws: Z = Q^T F, R' = F - Q Z, W' = R'^T R'; ragged
+    here: 192 = 128 + 64 rows of Z, 192 of the 256 tile columns), with CMSVD_TC_WS=0 the staged GEMM tiles
+    (k_gemm_tc), with CMSVD_TC_BIG=0 the SIMT path.  All three against the oracle."""
     monkeypatch.setenv("CMSVD_TC_BIG", tc_big)
+    monkeypatch.setenv("CMSVD_TC_WS", tc_ws)
     col = synth.config4(N=4, m=1024, rank=64)
     r = 192
     sp, E, sig, rank, pairs, out = run_pairs(cm, col, r)
     orc = oracle.pair_errors(sp, pairs, r, 7, oracle.TRUNC)
-    compare(out, orc, 7, f"config4-reduced r=192 tc_big={tc_big}")
+    compare(out, orc, 7, f"config4-reduced r=192 tc_big={tc_big} tc_ws={tc_ws}")
 
 
 def _flat_block(R, m, decay):
