@@ -119,6 +119,8 @@ struct Ctx {
   // count x 2 x planes_cols x m fp32 each, fed to k_gemm_ws by TMA
   DevMem d_Qp, d_Fp, d_QTp;   // QTp: the Q planes transposed (count x 2 x m x planes_cols), A operand of R' = F - Q Z
   int planes_cols = 0;
+  const float* planes_F = nullptr;   // the fp32 TRUNC operands the F planes were split from (block i at i * planes_fstride)
+  int64_t planes_fstride = 0;
   bool planes_ok = false;
   DevMem d_sig32, d_rank, d_bdesc, d_adesc_raw, d_adesc_trunc, d_meta64, d_meta32;
 

@@ -446,6 +446,8 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
        "spectra: F planes");
     CK(launch_split_planes_t(c, (const float*)c.d_U.p, ustride, m, kc, N, (float*)c.d_QTp.p), "spectra: Q^T planes");
     c.planes_cols = kc;
+    c.planes_F = (const float*)c.d_Ftrunc.p;
+    c.planes_fstride = ustride;
     c.planes_ok = true;
   }
   c.sig.resize((size_t)N * nmax);

@@ -34,11 +34,19 @@ constexpr uint32_t kWsATile = kWsBM * kWsKT * 4;  // bytes of one A plane per st
 constexpr uint32_t kWsBTile = kWsBN * kWsKT * 4;  // bytes of one B plane per stage (32 KB)
 constexpr int kWsBlk = 128 / kWsKT;              // stages per TMEM accumulation chain (128-long K block)
 
-template <bool SHARE_A>
+// MODE 1 epilogue: the minuend F arrives by TMA in slices of kWsFC columns per column half (two slices in
+// flight), so that no epilogue thread waits on a global load
+constexpr int kWsFC = 16;
+constexpr uint32_t kWsFHalf = kWsFC * kWsBM * 4;   // one half's slice: [col][row] fp32 (8 KB)
+constexpr uint32_t kWsFBuf = 2 * kWsFHalf;         // both halves (16 KB)
+constexpr int kWsFSteps = 128 / kWsFC;             // slices per tile
+
+template <int MODE, bool SHARE_A>
 struct WsCfg {
   static constexpr int kStages = SHARE_A ? 3 : 2;
   static constexpr uint32_t kStageBytes = SHARE_A ? 2 * kWsBTile : 2 * kWsATile + 2 * kWsBTile;
-  static constexpr uint32_t kSmem = kStages * kStageBytes + 1024;
+  static constexpr uint32_t kFOff = kStages * kStageBytes;
+  static constexpr uint32_t kSmem = kFOff + (MODE == 1 ? 2 * kWsFBuf : 0) + 1024;
 };
 
 struct WsArgs {
@@ -61,6 +69,12 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
       ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_u(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
@@ -134,12 +148,13 @@ __global__ void __launch_bounds__(256) k_split_planes_t(const float* __restrict_
 template <int MODE, bool SHARE_A>
 __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant__ CUtensorMap tmA,
                                                             const __grid_constant__ CUtensorMap tmB,
+                                                            const __grid_constant__ CUtensorMap tmF,
                                                             const WsArgs a) {
-  using Cfg = WsCfg<SHARE_A>;
+  using Cfg = WsCfg<MODE, SHARE_A>;
   constexpr int kStages = Cfg::kStages;
   extern __shared__ uint8_t ws_smem_raw[];
   const uint32_t sm = (smem_u32(ws_smem_raw) + 1023u) & ~1023u;
-  __shared__ uint64_t bar_full[3], bar_empty[3], bar_accf[2], bar_acce[2];
+  __shared__ uint64_t bar_full[3], bar_empty[3], bar_accf[2], bar_acce[2], bar_ff[2], bar_fe[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
 
@@ -151,6 +166,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&bar_accf[s], 1);
       tc::mbar_init(&bar_acce[s], 8);   // one arrival per epilogue warp
+      tc::mbar_init(&bar_ff[s], 1);
+      tc::mbar_init(&bar_fe[s], 8);
     }
     tc::fence_mbar_init();
   }
@@ -269,6 +286,27 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
       }
     }
     __syncwarp();
+  } else if (wid == 2 && MODE == 1) {
+    // ------------------------------ minuend (F) loader ------------------------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const int64_t p = item / tiles;
+        const int t = (int)(item - p * tiles);
+        const int tm = t / a.tiles_n, tn = t - tm * a.tiles_n;
+        const int app = a.pairs[p].y;
+        for (int c = 0; c < kWsFSteps; ++c, ++it) {
+          const int s = it & 1;
+          mbar_wait_u32(smem_u32(&bar_fe[s]), ((it >> 1) & 1u) ^ 1u);
+          const uint32_t full = smem_u32(&bar_ff[s]);
+          mbar_expect_tx(full, kWsFBuf);
+          const uint32_t dst = sm + Cfg::kFOff + s * kWsFBuf;
+          tma_load_3d_u(dst, &tmF, kWsBM * tm, kWsBN * tn + kWsFC * c, app, full);
+          tma_load_3d_u(dst + kWsFHalf, &tmF, kWsBM * tm, kWsBN * tn + 128 + kWsFC * c, app, full);
+        }
+      }
+    }
+    __syncwarp();
   }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
@@ -277,7 +315,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
     const int half = (wid - 4) >> 2;           // column half [128 half, 128 half + 128)
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
     const int row = 32 * wq + lane;
-    uint32_t blk = 0;
+    uint32_t blk = 0, fit = 0;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
       const int64_t p = item / tiles;
       const int t = (int)(item - p * tiles);
@@ -331,28 +369,29 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
           }
         }
       } else if (MODE == 1) {
-        const AppDesc ap = a.ad[pr.y];
-        const int w = ap.w;
-        if (gi < a.m) {
-          float* Rh = a.Rp + (p * 2 + 0) * a.m * (int64_t)a.WMAX;
-          float* Rl = a.Rp + (p * 2 + 1) * a.m * (int64_t)a.WMAX;
-          const float* F = ap.F;
+        const int w = a.ad[pr.y].w;
+        float* Rh = a.Rp + (p * 2 + 0) * a.m * (int64_t)a.WMAX + gi;
+        float* Rl = a.Rp + (p * 2 + 1) * a.m * (int64_t)a.WMAX + gi;
 #pragma unroll
-          for (int c = 0; c < 128; c += 32) {
-            float f[32];
+        for (int c = 0; c < kWsFSteps; ++c, ++fit) {
+          const int s = fit & 1;
+          mbar_wait_u32(smem_u32(&bar_ff[s]), (fit >> 1) & 1u);
+          const uint32_t fb = sm + Cfg::kFOff + s * kWsFBuf + half * kWsFHalf + (uint32_t)row * 4u;
+          float f[kWsFC];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int gj = j0 + c + j;
-              f[j] = gj < w ? __ldg(F + (int64_t)gj * a.m + gi) : 0.f;
-            }
+          for (int j = 0; j < kWsFC; ++j)
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f[j]) : "r"(fb + (uint32_t)j * (kWsBM * 4)));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bar_fe[s]));
+          if (gi < a.m) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int gj = j0 + c + j;
+            for (int j = 0; j < kWsFC; ++j) {
+              const int gj = j0 + kWsFC * c + j;
               if (gj < a.WMAX) {
-                const float x = gj < w ? f[j] - sum[c + j] : 0.f;
+                const float x = gj < w ? f[j] - sum[kWsFC * c + j] : 0.f;
                 float h, l;
                 tc::split_tf32(x, h, l);
-                const int64_t o = (int64_t)gj * a.m + gi;
+                const int64_t o = (int64_t)gj * a.m;
                 Rh[o] = h;
                 Rl[o] = l;
               }
@@ -430,14 +469,15 @@ cudaError_t launch_split_planes_t(Ctx& c, const float* src, int64_t sstride, int
 bool gemm_ws_supported(const Ctx& c, int64_t m) { return ws_encode_fn() != nullptr && (m & 3) == 0 && c.planes_ok; }
 
 template <int MODE, bool SHARE_A>
-static cudaError_t launch_ws(Ctx& c, const CUtensorMap& tA, const CUtensorMap& tB, const WsArgs& a) {
-  using Cfg = WsCfg<SHARE_A>;
+static cudaError_t launch_ws(Ctx& c, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tF,
+                             const WsArgs& a) {
+  using Cfg = WsCfg<MODE, SHARE_A>;
   cudaError_t e = cudaFuncSetAttribute(k_gemm_ws<MODE, SHARE_A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)Cfg::kSmem);
   if (e != cudaSuccess) return e;
   const int64_t items = a.P * a.tiles_m * a.tiles_n;
   const unsigned grid = (unsigned)std::min<int64_t>(items, c.sm_count);
-  k_gemm_ws<MODE, SHARE_A><<<grid, kWsThreads, Cfg::kSmem, c.stream>>>(tA, tB, a);
+  k_gemm_ws<MODE, SHARE_A><<<grid, kWsThreads, Cfg::kSmem, c.stream>>>(tA, tB, tF, a);
   c.launches += 1;
   return cudaGetLastError();
 }
@@ -459,7 +499,7 @@ cudaError_t launch_gemm_ws(Ctx& c, int mode, const int2* pairs, int64_t P, const
     a.tiles_m = (QMAX + kWsBM - 1) / kWsBM;
     if (!ws_map_k(&tA, Qp, m, c.planes_cols, c.count, kWsBM) || !ws_map_k(&tB, Fp, m, c.planes_cols, c.count, kWsBN))
       return cudaErrorInvalidValue;
-    return launch_ws<0, false>(c, tA, tB, a);
+    return launch_ws<0, false>(c, tA, tB, tB, a);
   }
   if (mode == 1) {
     a.tiles_m = (int)((m + kWsBM - 1) / kWsBM);
@@ -467,13 +507,26 @@ cudaError_t launch_gemm_ws(Ctx& c, int mode, const int2* pairs, int64_t P, const
     if (!ws_map_k(&tA, (const float*)c.d_QTp.p, c.planes_cols, (int)m, c.count, kWsBM) ||
         !ws_map_k(&tB, Zp, QMAX, WMAX, P, kWsBN))
       return cudaErrorInvalidValue;
-    return launch_ws<1, false>(c, tA, tB, a);
+    // the fp32 minuend F (TRUNC operands at a uniform stride): box 128 rows x kWsFC columns, no swizzle
+    CUtensorMap tF;
+    {
+      auto fn = ws_encode_fn();
+      cuuint64_t dims[3] = {(cuuint64_t)m, (cuuint64_t)c.planes_cols, (cuuint64_t)c.count};
+      cuuint64_t strides[2] = {(cuuint64_t)m * 4, (cuuint64_t)c.planes_fstride * 4};
+      cuuint32_t box[3] = {(cuuint32_t)kWsBM, (cuuint32_t)kWsFC, 1};
+      cuuint32_t estr[3] = {1, 1, 1};
+      if (!fn || fn(&tF, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(c.planes_F), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+    return launch_ws<1, false>(c, tA, tB, tF, a);
   }
   a.tiles_m = (WMAX + kWsBM - 1) / kWsBM;
   if (!ws_map_k(&tB, Rp, m, WMAX, P, kWsBN)) return cudaErrorInvalidValue;
-  if (a.tiles_n == 1) return launch_ws<2, true>(c, tB, tB, a);
+  if (a.tiles_n == 1) return launch_ws<2, true>(c, tB, tB, tB, a);
   if (!ws_map_k(&tA, Rp, m, WMAX, P, kWsBM)) return cudaErrorInvalidValue;
-  return launch_ws<2, false>(c, tA, tB, a);
+  return launch_ws<2, false>(c, tA, tB, tB, a);
 }
 
 }  // namespace cmsvd

@@ -41,7 +41,7 @@ int main(int argc, char** argv) {
   CKC(launch_split_planes_t(c, dU, (int64_t)kc * m, m, kc, N, (float*)c.d_QTp.p));
   CKC(launch_split_planes(c, dU, (int64_t)kc * m, m, kc, kc, N, (float*)c.d_Qp.p));
   CKC(launch_split_planes(c, dF, (int64_t)kc * m, m, kc, kc, N, (float*)c.d_Fp.p));
-  c.planes_cols = kc; c.planes_ok = true;
+  c.planes_cols = kc; c.planes_ok = true; c.planes_F = dF; c.planes_fstride = (int64_t)kc * m;
   std::vector<BaseDesc> bd(N); std::vector<AppDesc> ad(N);
   const int qs[3] = {kc, kc - 5, kc - 64}, wsz[3] = {kc, kc - 3, kc - 40};
   for (int i = 0; i < N; ++i) {
