@@ -175,6 +175,200 @@ __global__ void __launch_bounds__(kCholThreads) k_chol_inv(double* __restrict__ 
   if (tid == 0) status[blockIdx.x] = s_bad;
 }
 
+// ---------------------------------------------------------------------------
+// Blocked variant of k_chol_inv (same contract; default).  The unblocked kernel applies one rank-1 update
+// of the trailing matrix per column from global memory (s^3/6 read-modify-writes: 24 ms per 512 x 512
+// problem, a quarter of S2 on config 4).  Here, per 32-column panel: the diagonal block is factored in
+// shared memory by one warp, the row panel R(kb.., j) is obtained by a forward substitution per column
+// (thread = column) and kept in shared memory, and the trailing matrix receives ONE rank-32 update in
+// 4 x 4 register tiles (warp = tile column, lanes over tile rows: coalesced).  The inverse T = R^-1 is
+// built by block columns: T(0:J0, J) = -(T(0:J0, 0:J0) R(0:J0, J)) R_JJ^-1, thread = row, the panel
+// R(0:J0, J) broadcast from shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kCB = 32;
+constexpr int kCholBlkThreads = 512;   // 128 registers per thread: the 32-long substitution / accumulator vectors stay in registers
+constexpr int kCBLd = kCB + 1;
+constexpr int kCPsLd = 512;
+constexpr size_t kCholBlkSmem = (size_t)(2 * kCB * kCBLd + kCB * kCPsLd) * sizeof(double);
+
+__global__ void __launch_bounds__(kCholBlkThreads) k_chol_inv_blk(double* __restrict__ Hs, double* __restrict__ Ts,
+                                                              int s, int64_t stride, int* __restrict__ status) {
+  extern __shared__ __align__(16) double csm[];
+  double* Dk = csm;                       // [32][33] diagonal block (upper), identity-padded
+  double* Ik = Dk + kCB * kCBLd;          // [32][33] its inverse
+  double* Ps = Ik + kCB * kCBLd;          // [32][512] row panel (Cholesky) / [J0][32] column panel (inverse)
+  __shared__ double s_shift;
+  __shared__ double red[kCholBlkThreads / 32];
+  __shared__ int s_bad;
+  double* H = Hs + (int64_t)blockIdx.x * stride;
+  double* T = Ts + (int64_t)blockIdx.x * stride;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int nw = kCholBlkThreads / 32;
+  double mx = 0.0;
+  for (int i = tid; i < s; i += kCholBlkThreads) mx = fmax(mx, fabs(H[(int64_t)i * s + i]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[wid] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m2 = 0.0;
+    for (int k = 0; k < nw; ++k) m2 = fmax(m2, red[k]);
+    s_shift = 1e-13 * m2;
+    s_bad = 0;
+  }
+  __syncthreads();
+  const double shift = s_shift;
+  for (int i = tid; i < s; i += kCholBlkThreads) H[(int64_t)i * s + i] += shift;
+  __syncthreads();
+  // ---- Cholesky H = R^T R, R upper (H(k, j), k <= j, at H[j * s + k]) ----
+  for (int kb = 0; kb < s; kb += kCB) {
+    const int nb = min(kCB, s - kb);
+    for (int e = tid; e < kCB * kCB; e += kCholBlkThreads) {
+      const int r = e & 31, cc = e >> 5;
+      double v = (r == cc) ? 1.0 : 0.0;
+      if (r < nb && cc < nb && r <= cc) v = H[(int64_t)(kb + cc) * s + kb + r];
+      Dk[r * kCBLd + cc] = v;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      for (int k = 0; k < nb; ++k) {
+        double d = Dk[k * kCBLd + k];
+        if (!(d > 0.0)) { if (lane == 0) s_bad = 1; d = fmax(shift, 1e-300); }
+        const double piv = sqrt(d), inv = 1.0 / piv;
+        const double rkc = (lane > k && lane < nb) ? Dk[k * kCBLd + lane] * inv : 0.0;
+        __syncwarp();
+        if (lane == k) Dk[k * kCBLd + k] = piv;
+        else if (lane > k && lane < nb) Dk[k * kCBLd + lane] = rkc;
+        __syncwarp();
+        if (lane > k && lane < nb)
+          for (int i = k + 1; i <= lane; ++i) Dk[i * kCBLd + lane] = fma(-Dk[k * kCBLd + i], rkc, Dk[i * kCBLd + lane]);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < nb * nb; e += kCholBlkThreads) {
+      const int r = e % nb, cc = e / nb;
+      if (r <= cc) H[(int64_t)(kb + cc) * s + kb + r] = Dk[r * kCBLd + cc];
+    }
+    const int rem = s - kb - nb;   // > 0 only when nb == kCB
+    if (rem > 0) {
+      for (int jj = tid; jj < rem; jj += kCholBlkThreads) {   // the column's x lives in Ps[:, jj] (thread-private)
+        double* col = H + (int64_t)(kb + kCB + jj) * s + kb;
+        double* xs = Ps + jj;
+#pragma unroll 4
+        for (int l = 0; l < kCB; ++l) xs[l * kCPsLd] = col[l];
+        for (int l = 0; l < kCB; ++l) {
+          double v0 = xs[l * kCPsLd], v1 = 0.0;
+          int t = 0;
+          for (; t + 1 < l; t += 2) {
+            v0 = fma(-Dk[t * kCBLd + l], xs[t * kCPsLd], v0);
+            v1 = fma(-Dk[(t + 1) * kCBLd + l], xs[(t + 1) * kCPsLd], v1);
+          }
+          if (t < l) v0 = fma(-Dk[t * kCBLd + l], xs[t * kCPsLd], v0);
+          const double v = (v0 + v1) / Dk[l * kCBLd + l];
+          xs[l * kCPsLd] = v;
+          col[l] = v;
+        }
+      }
+      for (int e = rem + tid; e < ((rem + 3) & ~3); e += kCholBlkThreads)   // pad the last 4-column tile
+        for (int l = 0; l < kCB; ++l) Ps[l * kCPsLd + e] = 0.0;
+      __syncthreads();
+      const int ntile = (rem + 3) >> 2;
+      const int base = kb + kCB;
+      for (int tj = wid; tj < ntile; tj += nw) {
+        for (int ti = lane; ti <= tj; ti += 32) {
+          double acc[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+#pragma unroll 8
+          for (int l = 0; l < kCB; ++l) {
+            const double2 a0 = *reinterpret_cast<const double2*>(Ps + l * kCPsLd + 4 * ti);
+            const double2 a1 = *reinterpret_cast<const double2*>(Ps + l * kCPsLd + 4 * ti + 2);
+            const double2 b0 = *reinterpret_cast<const double2*>(Ps + l * kCPsLd + 4 * tj);
+            const double2 b1 = *reinterpret_cast<const double2*>(Ps + l * kCPsLd + 4 * tj + 2);
+            const double a[4] = {a0.x, a0.y, a1.x, a1.y}, b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int j = base + 4 * tj + v;
+            if (j < s) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int i = base + 4 * ti + u;
+                if (i <= j) H[(int64_t)j * s + i] -= acc[u][v];
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- T = R^-1 (upper; zero below the diagonal) ----
+  for (int e = tid; e < s * s; e += kCholBlkThreads) T[e] = 0.0;
+  __syncthreads();
+  for (int J0 = 0; J0 < s; J0 += kCB) {
+    const int nb = min(kCB, s - J0);
+    for (int e = tid; e < kCB * kCB; e += kCholBlkThreads) {
+      const int r = e & 31, cc = e >> 5;
+      double v = (r == cc) ? 1.0 : 0.0;
+      if (r < nb && cc < nb && r <= cc) v = H[(int64_t)(J0 + cc) * s + J0 + r];
+      Dk[r * kCBLd + cc] = v;
+      Ik[r * kCBLd + cc] = 0.0;
+    }
+    // column panel R(0:J0, J) -> Ps[k][c]
+    for (int e = tid; e < J0 * kCB; e += kCholBlkThreads) {
+      const int k = e % J0, cc = e / J0;
+      Ps[k * kCB + cc] = cc < nb ? H[(int64_t)(J0 + cc) * s + k] : 0.0;
+    }
+    __syncthreads();
+    if (wid == 0) {   // R_JJ^-1 by back substitution, lane = column (its x lives in Ik[:, lane])
+      const int cc = lane;
+      for (int r = cc; r >= 0; --r) {
+        double v = (r == cc) ? 1.0 : 0.0;
+        for (int k = r + 1; k <= cc; ++k) v = fma(-Dk[r * kCBLd + k], Ik[k * kCBLd + cc], v);
+        Ik[r * kCBLd + cc] = v / Dk[r * kCBLd + r];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < nb * nb; e += kCholBlkThreads) {
+      const int r = e % nb, cc = e / nb;
+      if (r <= cc) T[(int64_t)(J0 + cc) * s + J0 + r] = Ik[r * kCBLd + cc];
+    }
+    for (int r = tid; r < J0; r += kCholBlkThreads) {
+      double acc[kCB];
+#pragma unroll
+      for (int cc = 0; cc < kCB; ++cc) acc[cc] = 0.0;
+      const int k0 = r & ~31;    // warp-uniform start: T(r, k) = 0 for k < r
+      for (int k = k0; k < J0; ++k) {
+        const double t = T[(int64_t)k * s + r];
+        const double2* b2 = reinterpret_cast<const double2*>(Ps + k * kCB);
+#pragma unroll
+        for (int q = 0; q < kCB / 2; ++q) {
+          const double2 b = b2[q];
+          acc[2 * q] = fma(t, b.x, acc[2 * q]);
+          acc[2 * q + 1] = fma(t, b.y, acc[2 * q + 1]);
+        }
+      }
+      // T(r, J0 + c) = -sum_{c' <= c} acc[c'] Ik[c'][c]
+#pragma unroll
+      for (int cc = 0; cc < kCB; ++cc) {
+        double v = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 <= cc; ++c2) v = fma(acc[c2], Ik[c2 * kCBLd + cc], v);
+        if (cc < nb) T[(int64_t)(J0 + cc) * s + r] = -v;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) status[blockIdx.x] = s_bad;
+}
+
 // Gaussian N(0,1) test matrix from a counter-based hash (splitmix64 + Box-Muller); deterministic.
 __global__ void k_randn(double* __restrict__ X, int64_t n, uint64_t seed) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -219,7 +413,13 @@ cudaError_t cholqr(Ctx& c, int batch, int64_t rows, int s, double* Y, double* Yt
     e = gemm_mixed<double, true>(c, batch, s, s, (int)rows, Y, rows, rows * s, Y, rows, rows * s, H, s,
                                  (int64_t)s * s);
     if (e != cudaSuccess) return e;
-    k_chol_inv<<<batch, kCholThreads, 0, c.stream>>>(H, T, s, (int64_t)s * s, status);
+    if (c.chol_blocked && s <= kCPsLd) {
+      e = cudaFuncSetAttribute(k_chol_inv_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCholBlkSmem);
+      if (e != cudaSuccess) return e;
+      k_chol_inv_blk<<<batch, kCholBlkThreads, kCholBlkSmem, c.stream>>>(H, T, s, (int64_t)s * s, status);
+    } else {
+      k_chol_inv<<<batch, kCholThreads, 0, c.stream>>>(H, T, s, (int64_t)s * s, status);
+    }
     c.launches += 1;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
