@@ -351,3 +351,23 @@ def test_duo160_ragged_vs_oracle_and_one_problem_kernel(cm, monkeypatch):
         ctx.close()
         compare_pairs(outs[-1], ref, what=f"duo160={flag}")
     assert_err2(outs[0]["err2"][:, 2], outs[1]["err2"][:, 2], ref.total, "duo160 vs one-problem kernel")
+
+
+def test_sharded_union_equals_unsharded(cm):
+    """N4 (pair-grid sharding, shard.py): the tiles of a world of 4, evaluated one after the other on this
+    GPU, reassemble bitwise to the unsharded call (the evaluations are independent of their batch)."""
+    from paper_2601_11626_b200 import shard
+    col = synth.config1()
+    with cm.Context(0) as ctx:
+        ctx.register(col.blocks)
+        E, sig, rank = ctx.block_spectra(col.r)
+        order = np.array(sorted(range(col.N), key=lambda i: (-E[i], i)))
+        pairs = synth.all_pairs_by_norm_order(order)
+        full = ctx.pair_errors(pairs)
+        err2 = np.full_like(full["err2"], np.nan)
+        total = np.full_like(full["total"], np.nan)
+        for idx in shard.partition_pairs(pairs, 4):
+            part = ctx.pair_errors(pairs[idx])
+            err2[idx] = part["err2"]
+            total[idx] = part["total"]
+    assert np.array_equal(err2, full["err2"]) and np.array_equal(total, full["total"])
