@@ -103,7 +103,7 @@ cmsvd_status cmsvd_destroy(cmsvd_ctx ctx) {
   cudaSetDevice(c.device);
   cudaStreamSynchronize(c.stream);
   DevMem* bufs[] = {&c.arena, &c.d_E, &c.d_U, &c.d_sig, &c.d_Ftrunc, &c.d_sig32, &c.d_rank,
-                    &c.d_bdesc, &c.d_adesc_raw, &c.d_adesc_trunc, &c.d_meta64, &c.d_meta32, &c.d_Qp, &c.d_Fp, &c.d_QTp};
+                    &c.d_bdesc, &c.d_adesc_raw, &c.d_adesc_trunc, &c.d_meta64, &c.d_meta32, &c.d_Qp, &c.d_Fp, &c.d_QTp, &c.d_Ap, &c.d_ATp};
   for (DevMem* b : bufs) release(*b);
   for (auto& b : c.ws) release(b);
   for (auto& b : c.cws) release(b);

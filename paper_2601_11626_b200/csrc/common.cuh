@@ -117,6 +117,7 @@ struct Ctx {
   bool trunc_ready = false;
   // tf32 hi/lo planes of the bases and TRUNC operands (A22 collections with operands wider than 128 columns):
   // count x 2 x planes_cols x m fp32 each, fed to k_gemm_ws by TMA
+  DevMem d_Ap, d_ATp;          // S2 (A22): tf32 planes of the blocks and of their transposes (k_gemm_ws MODE 3)
   DevMem d_Qp, d_Fp, d_QTp;   // QTp: the Q planes transposed (count x 2 x m x planes_cols), A operand of R' = F - Q Z
   int planes_cols = 0;
   const float* planes_F = nullptr;   // the fp32 TRUNC operands the F planes were split from (block i at i * planes_fstride)

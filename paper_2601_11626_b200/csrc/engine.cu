@@ -280,9 +280,26 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
       CK(cudaMemcpyAsync(dns, hns.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, c.stream), "spectra: h2d");
       const int64_t ms = m * s, ns_ = (int64_t)n * s;
       const bool tcp = c.big_tc && c.use_tc;
+      // ... through the TMA-fed warp-specialised kernel on pre-split tf32 planes of A and A^T (k_gemm_ws MODE 3)
+      const bool wsp = tcp && c.tc_ws && gemm_ws_available() && (m & 3) == 0 && (n & 3) == 0 && (s & 3) == 0;
       float *Y32 = nullptr, *Z32 = nullptr;
+      float *Ap = nullptr, *ATp = nullptr, *Yp = nullptr, *Zp = nullptr, *Omp = nullptr;
       GemmDesc *dAtY = nullptr, *dAZ = nullptr;
-      if (tcp) {
+      if (wsp) {
+        const size_t pa = (size_t)nb * 2 * m * n * 4;
+        CK(ensure(c.d_Ap, pa), "spectra: A planes");
+        CK(ensure(c.d_ATp, pa), "spectra: A^T planes");
+        CK(ensure(c.ws[WS_D], ((size_t)nb * 2 * (m + n) * s + (size_t)2 * n * s) * 4), "spectra: basis planes");
+        Ap = (float*)c.d_Ap.p;
+        ATp = (float*)c.d_ATp.p;
+        Yp = (float*)c.ws[WS_D].p;
+        Zp = Yp + (size_t)nb * 2 * m * s;
+        Omp = Zp + (size_t)nb * 2 * n * s;
+        CK(launch_split_planes_ptr(c, (const float* const*)dA, m, n, nb, Ap, ATp), "spectra: split A");
+        CK(launch_split_planes64(c, Om, (int64_t)n * s, 1, Omp), "spectra: split Omega");
+        CK(launch_gemm_ws_tn64(c, nb, (int)m, s, n, ATp, Omp, true, Y, m, ms), "spectra: AO (ws)");
+        CK(cholqr(c, nb, m, s, Y, Tmp, H, T, st, 1), "spectra: cholqr");
+      } else if (tcp) {
         // the products with A on tcgen05 (3xTF32 tiles, fp64 outputs for the fp64 CholQR2); the
         // orthonormal bases enter them rounded to fp32 (a 6e-8 relative perturbation of the basis,
         // which the next power iteration and CholQR absorb; the Rayleigh-Ritz values move by O(u32))
@@ -320,7 +337,12 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
       auto power = [&](int iters) -> Status {
         for (int it = 0; it < iters; ++it) {
           const int passes = it + 1 == iters ? 2 : 1;
-          if (tcp) {
+          if (wsp) {
+            CK(launch_split_planes64(c, Y, ms, nb, Yp), "spectra: Y planes");
+            CK(launch_gemm_ws_tn64(c, nb, n, s, (int)m, Ap, Yp, false, Z, n, ns_), "spectra: AtY (ws)");
+            CK(launch_split_planes64(c, Z, ns_, nb, Zp), "spectra: Z planes");
+            CK(launch_gemm_ws_tn64(c, nb, (int)m, s, n, ATp, Zp, false, Y, m, ms), "spectra: AZ (ws)");
+          } else if (tcp) {
             CK(launch_to_f32(c, Y, Y32, (int64_t)nb * ms), "spectra: Y32");
             CK(launch_gemm_tc(c, dAtY, nb, n, s, false, true), "spectra: AtY (tc)");
             CK(launch_to_f32(c, Z, Z32, (int64_t)nb * ns_), "spectra: Z32");
@@ -338,7 +360,10 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
       };
       // Rayleigh-Ritz: Bt = A^T Q, H = Bt^T Bt = W diag(lambda) W^T, U_r = Q W_r, descriptors
       auto rayleigh_ritz = [&]() -> Status {
-        if (tcp) {
+        if (wsp) {
+          CK(launch_split_planes64(c, Y, ms, nb, Yp), "spectra: Y planes");
+          CK(launch_gemm_ws_tn64(c, nb, n, s, (int)m, Ap, Yp, false, Z, n, ns_), "spectra: Bt (ws)");
+        } else if (tcp) {
           CK(launch_to_f32(c, Y, Y32, (int64_t)nb * ms), "spectra: Y32");
           CK(launch_gemm_tc(c, dAtY, nb, n, s, false, true), "spectra: Bt (tc)");
         } else {

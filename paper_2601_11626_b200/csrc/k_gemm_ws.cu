@@ -3,6 +3,8 @@
 //   MODE 0  Z  = Q^T F     (Lemma 1's projection Y = Q_t^T A)      K = m
 //   MODE 1  R' = F - Q Z   (Thm 2's residual / Lemma 1's R)  K = q
 //   MODE 2  W' = R'^T R'   (Gram of Lemma 1's R-factor)       K = m
+//   MODE 3  C = A^T B (fp64 out) on K-major planes: the products with the block of the S2 subspace iteration
+//           (Z = A^T Y, Y = A Z through the transposed planes; reading A22, block spectra PAPER.md:247-249)
 // The fp32 operands are split ONCE into tf32 hi/lo planes (hi = RN_tf32(x), lo = x - hi): the bases Q and
 // the TRUNC operands F per block after S2 (k_split_planes), Z and R' by the epilogues that produce them.
 // Planes are fed to shared memory by cp.async.bulk.tensor (TMA, 128-byte swizzle) and consumed by
@@ -62,6 +64,11 @@ struct WsArgs {
   float* Zp;       // MODE 0 out / MODE 1 in: P x 2 x (WMAX cols x QMAX rows) planes
   float* Rp;       // MODE 1 out / MODE 2 in: P x 2 x (WMAX cols x m rows) planes
   double* Wws;     // MODE 2 out: P x (WMAX x WMAX) fp64, ld WMAX
+  // MODE 3 (plain batched product, S2): C[b] (Mg x Ng fp64, ld ldc, stride sC) = sum_k A[b](k, i) B[b](k, j)
+  double* C64;
+  int64_t ldc, sC;
+  int Mg, Ng, Kg;
+  int b_shared;    // 1: every problem uses B planes of batch entry 0
 };
 
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
@@ -145,6 +152,59 @@ __global__ void __launch_bounds__(256) k_split_planes_t(const float* __restrict_
   }
 }
 
+// planes of fp32 matrices given by a pointer table (rows x cols each, ld = rows): normal [i][h][c][r] and
+// transposed [i][h][r][c] in one pass over 32 x 32 tiles
+__global__ void __launch_bounds__(256) k_split_planes_ptr(const float* const* __restrict__ srcp, int64_t rows, int cols,
+                                                          float* __restrict__ dst, float* __restrict__ dst_t) {
+  __shared__ float t[32][33];
+  const int i = blockIdx.z;
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const float* s = srcp[i];
+  float* dh = dst + ((int64_t)i * 2 + 0) * rows * cols;
+  float* dl = dst + ((int64_t)i * 2 + 1) * rows * cols;
+  for (int cc = ty; cc < 32; cc += 8) {
+    float x = 0.f;
+    if (r0 + tx < rows && c0 + cc < cols) {
+      x = s[(int64_t)(c0 + cc) * rows + r0 + tx];
+      float h, l;
+      tc::split_tf32(x, h, l);
+      dh[(int64_t)(c0 + cc) * rows + r0 + tx] = h;
+      dl[(int64_t)(c0 + cc) * rows + r0 + tx] = l;
+    }
+    t[cc][tx] = x;
+  }
+  __syncthreads();
+  float* th = dst_t + ((int64_t)i * 2 + 0) * rows * cols;
+  float* tl = dst_t + ((int64_t)i * 2 + 1) * rows * cols;
+  for (int rr = ty; rr < 32; rr += 8) {
+    if (r0 + rr < rows && c0 + tx < cols) {
+      float h, l;
+      tc::split_tf32(t[tx][rr], h, l);
+      th[(r0 + rr) * cols + c0 + tx] = h;
+      tl[(r0 + rr) * cols + c0 + tx] = l;
+    }
+  }
+}
+
+// planes of `count` fp64 matrices rounded to fp32 first (n elements each, matrix i at src + i * n):
+// dst[(i * 2 + h) * n + e]
+__global__ void __launch_bounds__(256) k_split_planes64(const double* __restrict__ src, int64_t n, int count,
+                                                        float* __restrict__ dst) {
+  const int i = blockIdx.y;
+  const double* s = src + (int64_t)i * n;
+  float* dh = dst + ((int64_t)i * 2 + 0) * n;
+  float* dl = dst + ((int64_t)i * 2 + 1) * n;
+  (void)count;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    float h, l;
+    tc::split_tf32((float)s[e], h, l);
+    dh[e] = h;
+    dl[e] = l;
+  }
+}
+
 template <int MODE, bool SHARE_A>
 __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant__ CUtensorMap tmA,
                                                             const __grid_constant__ CUtensorMap tmB,
@@ -185,6 +245,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
       const BaseDesc b = a.bd[a.pairs[p].x];
       return (a.use_full ? b.q : b.rr);
     }
+    if (MODE == 3) return a.Kg;
     return (int)a.m;
   };
 
@@ -198,7 +259,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
         const int64_t p = item / tiles;
         const int t = (int)(item - p * tiles);
         const int tm = t / a.tiles_n, tn = t - tm * a.tiles_n;
-        const int2 pr = a.pairs[p];
+        const int2 pr = MODE == 3 ? make_int2(0, 0) : a.pairs[p];
         const int K = item_k(p);
         const int nst = (K + kWsKT - 1) / kWsKT;
         for (int st = 0; st < nst; ++st, ++it) {
@@ -219,6 +280,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
               tma_load_4d(bA + kWsATile, &tmA, k0, kWsBM * tm, 1, pr.x, full);
               tma_load_4d(bB, &tmB, k0, kWsBN * tn, 0, pr.y, full);
               tma_load_4d(bB + kWsBTile, &tmB, k0, kWsBN * tn, 1, pr.y, full);
+            } else if (MODE == 3) {
+              const int bb = a.b_shared ? 0 : (int)p;
+              tma_load_4d(bA, &tmA, k0, kWsBM * tm, 0, (int)p, full);
+              tma_load_4d(bA + kWsATile, &tmA, k0, kWsBM * tm, 1, (int)p, full);
+              tma_load_4d(bB, &tmB, k0, kWsBN * tn, 0, bb, full);
+              tma_load_4d(bB + kWsBTile, &tmB, k0, kWsBN * tn, 1, bb, full);
             } else if (MODE == 1) {
               tma_load_4d(bA, &tmA, k0, kWsBM * tm, 0, pr.x, full);
               tma_load_4d(bA + kWsATile, &tmA, k0, kWsBM * tm, 1, pr.x, full);
@@ -320,7 +387,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
       const int64_t p = item / tiles;
       const int t = (int)(item - p * tiles);
       const int tm = t / a.tiles_n, tn = t - tm * a.tiles_n;
-      const int2 pr = a.pairs[p];
+      const int2 pr = MODE == 3 ? make_int2(0, 0) : a.pairs[p];
       const int K = item_k(p);
       const int nblk = (K + 127) / 128;
       float sum[128];
@@ -398,6 +465,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
             }
           }
         }
+      } else if (MODE == 3) {
+        if (gi < a.Mg) {
+          double* C = a.C64 + p * a.sC + gi;
+#pragma unroll
+          for (int j = 0; j < 128; ++j) {
+            const int gj = j0 + j;
+            if (gj < a.Ng) C[(int64_t)gj * a.ldc] = (double)sum[j];
+          }
+        }
       } else {
         const int w = a.ad[pr.y].w;
         if (gi < w) {
@@ -466,6 +542,25 @@ cudaError_t launch_split_planes_t(Ctx& c, const float* src, int64_t sstride, int
   return cudaGetLastError();
 }
 
+cudaError_t launch_split_planes_ptr(Ctx& c, const float* const* d_srcp, int64_t rows, int cols, int count, float* dst,
+                                    float* dst_t) {
+  if (count <= 0 || cols <= 0) return cudaSuccess;
+  dim3 g((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32), count);
+  k_split_planes_ptr<<<g, 256, 0, c.stream>>>(d_srcp, rows, cols, dst, dst_t);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_planes64(Ctx& c, const double* src, int64_t n, int count, float* dst) {
+  if (count <= 0 || n <= 0) return cudaSuccess;
+  dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 2048), count);
+  k_split_planes64<<<g, 256, 0, c.stream>>>(src, n, count, dst);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+bool gemm_ws_available() { return ws_encode_fn() != nullptr; }
+
 bool gemm_ws_supported(const Ctx& c, int64_t m) { return ws_encode_fn() != nullptr && (m & 3) == 0 && c.planes_ok; }
 
 template <int MODE, bool SHARE_A>
@@ -527,6 +622,21 @@ cudaError_t launch_gemm_ws(Ctx& c, int mode, const int2* pairs, int64_t P, const
   if (a.tiles_n == 1) return launch_ws<2, true>(c, tB, tB, tB, a);
   if (!ws_map_k(&tA, Rp, m, WMAX, P, kWsBM)) return cudaErrorInvalidValue;
   return launch_ws<2, false>(c, tA, tB, tB, a);
+}
+
+// C[b] (M x N fp64, ld ldc, stride sC) = A[b]^T-planes . B[b]-planes: Ap [batch][2][M][K] (K contiguous),
+// Bp [batch or 1][2][N][K]; 3xTF32 on k_gemm_ws (MODE 3)
+cudaError_t launch_gemm_ws_tn64(Ctx& c, int batch, int M, int N, int K, const float* Ap, const float* Bp, bool b_shared,
+                                double* C, int64_t ldc, int64_t sC) {
+  if (batch <= 0 || M <= 0 || N <= 0) return cudaSuccess;
+  WsArgs a{};
+  a.P = batch; a.m = K; a.Mg = M; a.Ng = N; a.Kg = K; a.C64 = C; a.ldc = ldc; a.sC = sC; a.b_shared = b_shared ? 1 : 0;
+  a.tiles_m = (M + kWsBM - 1) / kWsBM;
+  a.tiles_n = (N + kWsBN - 1) / kWsBN;
+  CUtensorMap tA, tB;
+  if (!ws_map_k(&tA, Ap, K, M, batch, kWsBM) || !ws_map_k(&tB, Bp, K, N, b_shared ? 1 : batch, kWsBN))
+    return cudaErrorInvalidValue;
+  return launch_ws<3, false>(c, tA, tB, tB, a);
 }
 
 }  // namespace cmsvd

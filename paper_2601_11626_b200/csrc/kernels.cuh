@@ -75,6 +75,12 @@ cudaError_t launch_split_planes(Ctx& c, const float* src, int64_t sstride, int64
                                 int count, float* dst);
 cudaError_t launch_split_planes_t(Ctx& c, const float* src, int64_t sstride, int64_t rows, int cols, int count,
                                   float* dst);
+cudaError_t launch_split_planes_ptr(Ctx& c, const float* const* d_srcp, int64_t rows, int cols, int count, float* dst,
+                                    float* dst_t);
+cudaError_t launch_split_planes64(Ctx& c, const double* src, int64_t n, int count, float* dst);
+cudaError_t launch_gemm_ws_tn64(Ctx& c, int batch, int M, int N, int K, const float* Ap, const float* Bp, bool b_shared,
+                                double* C, int64_t ldc, int64_t sC);
+bool gemm_ws_available();
 cudaError_t launch_gemm_ws(Ctx& c, int mode, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad,
                            int use_full, int QMAX, int WMAX, float* Zws, float* Zp, float* Rp, double* Wws);
 // C (fp64) = A B, A: M x K, B: K x N column-major fp32 (3xTF32 tiles)
