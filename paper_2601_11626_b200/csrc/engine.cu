@@ -369,7 +369,8 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
         } else {
           CK((gemm_mixed<float, true>(c, nb, n, s, (int)m, nullptr, m, 0, Y, m, ms, Z, n, ns_, 1.0, dA)), "spectra: Bt");
         }
-        CK((gemm_mixed<double, true>(c, nb, s, s, n, Z, n, ns_, Z, n, ns_, H, s, (int64_t)s * s)), "spectra: H");
+        CK((gemm_mixed<double, true>(c, nb, s, s, n, Z, n, ns_, Z, n, ns_, H, s, (int64_t)s * s, 1.0, nullptr, 1)),
+           "spectra: H");
         CK(launch_syev(c, H, s, (int64_t)s * s, dns, nb, s, (double*)c.ws[WS_V].p, (int64_t)s * s,
                        (double*)c.ws[WS_B].p, (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, s, st + nb),
            "spectra: eig(H)");

@@ -25,13 +25,18 @@ namespace cmsvd {
 //   TA = true : A is K x M column-major (lda), element (i,k) at A[i*lda + k]
 //   B: K x N column-major (ldb), C: M x N column-major (ldc).
 // Batched over blockIdx.z with strides sA, sB, sC.  64x64 tiles, BK = 16.
+// shape: 0 general; 1 the product is symmetric (C = X^T X): only tiles on or below the diagonal are
+// computed and mirrored (bitwise what the skipped tiles would compute: the same products in the same
+// order); 2 B is upper triangular (B(k, j) = 0 for k > j): the K loop of a tile stops at its last column.
 // ---------------------------------------------------------------------------
 template <typename TAe, bool TA>
 __global__ void __launch_bounds__(256) k_gemm_mixed(int M, int N, int K, const TAe* __restrict__ A,
                                                     const TAe* const* __restrict__ Ap, int64_t lda, int64_t sA,
                                                     const double* __restrict__ B, int64_t ldb, int64_t sB,
-                                                    double* __restrict__ C, int64_t ldc, int64_t sC, double alpha) {
+                                                    double* __restrict__ C, int64_t ldc, int64_t sC, double alpha,
+                                                    int shape) {
   constexpr int BM = 64, BN = 64, BK = 16;
+  if (shape == 1 && blockIdx.x < blockIdx.y) return;
   __shared__ double As[BK][BM + 1];
   __shared__ double Bs[BK][BN + 1];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -44,7 +49,8 @@ __global__ void __launch_bounds__(256) k_gemm_mixed(int M, int N, int K, const T
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (int k0 = 0; k0 < K; k0 += BK) {
+  const int Kt = shape == 2 ? min(K, j0 + BN) : K;
+  for (int k0 = 0; k0 < Kt; k0 += BK) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int e = tid + 256 * s;
@@ -83,17 +89,20 @@ __global__ void __launch_bounds__(256) k_gemm_mixed(int M, int N, int K, const T
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int i = i0 + tx + 16 * a, j = j0 + ty + 16 * b;
-      if (i < M && j < N) Cb[(int64_t)j * ldc + i] = alpha * acc[a][b];
+      if (i < M && j < N) {
+        Cb[(int64_t)j * ldc + i] = alpha * acc[a][b];
+        if (shape == 1 && blockIdx.x != blockIdx.y) Cb[(int64_t)i * ldc + j] = alpha * acc[a][b];
+      }
     }
 }
 
 template <typename TAe, bool TA>
 cudaError_t gemm_mixed(Ctx& c, int batch, int M, int N, int K, const TAe* A, int64_t lda, int64_t sA,
                        const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
-                       double alpha, const TAe* const* Ap) {
+                       double alpha, const TAe* const* Ap, int shape) {
   if (batch <= 0 || M <= 0 || N <= 0) return cudaSuccess;
   dim3 g((M + 63) / 64, (N + 63) / 64, batch);
-  k_gemm_mixed<TAe, TA><<<g, 256, 0, c.stream>>>(M, N, K, A, Ap, lda, sA, B, ldb, sB, C, ldc, sC, alpha);
+  k_gemm_mixed<TAe, TA><<<g, 256, 0, c.stream>>>(M, N, K, A, Ap, lda, sA, B, ldb, sB, C, ldc, sC, alpha, shape);
   c.launches += 1;
   return cudaGetLastError();
 }
@@ -411,7 +420,7 @@ cudaError_t cholqr(Ctx& c, int batch, int64_t rows, int s, double* Y, double* Yt
   cudaError_t e;
   for (int pass = 0; pass < passes; ++pass) {
     e = gemm_mixed<double, true>(c, batch, s, s, (int)rows, Y, rows, rows * s, Y, rows, rows * s, H, s,
-                                 (int64_t)s * s);
+                                 (int64_t)s * s, 1.0, nullptr, 1);   // H = Y^T Y: symmetric
     if (e != cudaSuccess) return e;
     if (c.chol_blocked && s <= kCPsLd) {
       e = cudaFuncSetAttribute(k_chol_inv_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCholBlkSmem);
@@ -424,7 +433,7 @@ cudaError_t cholqr(Ctx& c, int batch, int64_t rows, int s, double* Y, double* Yt
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     e = gemm_mixed<double, false>(c, batch, (int)rows, s, s, Y, rows, rows * s, T, s, (int64_t)s * s, Ytmp, rows,
-                                  rows * s);
+                                  rows * s, 1.0, nullptr, 2);        // T = R^-1: upper triangular
     if (e != cudaSuccess) return e;
     e = cudaMemcpyAsync(Y, Ytmp, sizeof(double) * (size_t)batch * rows * s, cudaMemcpyDeviceToDevice, c.stream);
     if (e != cudaSuccess) return e;
@@ -556,15 +565,15 @@ cudaError_t launch_ritz_resid(Ctx& c, int nb, int64_t m, int s, int kc, const do
 // Explicit instantiations used by the engine
 template cudaError_t gemm_mixed<float, false>(Ctx&, int, int, int, int, const float*, int64_t, int64_t,
                                               const double*, int64_t, int64_t, double*, int64_t, int64_t, double,
-                                              const float* const*);
+                                              const float* const*, int);
 template cudaError_t gemm_mixed<float, true>(Ctx&, int, int, int, int, const float*, int64_t, int64_t,
                                              const double*, int64_t, int64_t, double*, int64_t, int64_t, double,
-                                              const float* const*);
+                                              const float* const*, int);
 template cudaError_t gemm_mixed<double, false>(Ctx&, int, int, int, int, const double*, int64_t, int64_t,
                                                const double*, int64_t, int64_t, double*, int64_t, int64_t, double,
-                                               const double* const*);
+                                               const double* const*, int);
 template cudaError_t gemm_mixed<double, true>(Ctx&, int, int, int, int, const double*, int64_t, int64_t,
                                               const double*, int64_t, int64_t, double*, int64_t, int64_t, double,
-                                              const double* const*);
+                                              const double* const*, int);
 
 }  // namespace cmsvd

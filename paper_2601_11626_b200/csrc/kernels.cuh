@@ -95,7 +95,7 @@ cudaError_t launch_build_G1(Ctx& c, int rr, int w, const double* spec, const flo
 template <typename TAe, bool TA>
 cudaError_t gemm_mixed(Ctx& c, int batch, int M, int N, int K, const TAe* A, int64_t lda, int64_t sA,
                        const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
-                       double alpha = 1.0, const TAe* const* Ap = nullptr);
+                       double alpha = 1.0, const TAe* const* Ap = nullptr, int shape = 0);
 __global__ void k_big_leftvec(int64_t m, int s, int kc, const double* Y, const double* V, const int* perm,
                               float* const* Uout);
 __global__ void k_big_stats(int nb, const int* ids, int s, int r, int64_t m, int nmax_sig, const double* ev,
