@@ -586,8 +586,13 @@ constexpr int kSymmJT = 16;                    // columns per TMA slice (one 16 
 constexpr int kSymmNS = 3;                     // stages in flight
 constexpr int kSymmA = kSymmJT * kSymmRows;    // doubles per A slice (16 KB)
 constexpr int kSymmStage = 2 * kSymmA + kSymmJT * kSB;   // lower box + transposed box + V slice (34 KB)
+#ifndef CMSVD_SYMM_TT
+#define CMSVD_SYMM_TT 128   // 256 (4 columns per thread, twice the warps) measured slower: 22.8 vs 21.4 ms per config-4 pass
+#endif
+constexpr int kSymmTT = CMSVD_SYMM_TT;          // threads: 64 row pairs x (kSymmTT / 64) column groups
+constexpr int kSymmCW = kSB / (kSymmTT / 64);   // columns of Y per thread
 
-__global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_constant__ CUtensorMap tlo,
+__global__ void __launch_bounds__(kSymmTT, 2) k_sbr_symm_tma(const __grid_constant__ CUtensorMap tlo,
                                                                     const __grid_constant__ CUtensorMap tup,
                                                                     const double* __restrict__ G, int64_t ld,
                                                                     int64_t stride, const int* __restrict__ ns,
@@ -605,7 +610,7 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
   const double* A = G + (int64_t)p * stride + (int64_t)R0 * ld + R0;   // A22(i, j) at A[j * ld + i]
   const double* Vw = L.vp(ws, p, par);
   double* Yw = const_cast<double*>(Vw) + L.vsz();
-  const int i0 = tid & 63, h = tid >> 6;
+  const int i0 = tid & 63, h = tid >> 6;   // rows i0, i0 + 64; columns kSymmCW h .. + kSymmCW - 1
   const int imax = min(kSymmRows, np - I0);
   if (tid == 0) {
 #pragma unroll
@@ -629,18 +634,18 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
       if (kd != 1) tma_load_3d(As, &tlo, R0 + I0, R0 + J0, p, &bars[st]);
       if (kd != 0) tma_load_3d(As + kSymmA, &tup, R0 + J0, R0 + I0, p, &bars[st]);
     }
-    for (int e = tid; e < kSymmJT * kSB; e += kSymmThreads) {
+    for (int e = tid; e < kSymmJT * kSB; e += kSymmTT) {
       const int jj = e >> 4, c = e & 15;
       const bool ok = jj < jmax;
       cp_async8(Vs + e, ok ? Vw + (int64_t)c * L.ldv + J0 + jj : Vw, ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  double acc[2][8];
+  double acc[2][kSymmCW];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
+    for (int c = 0; c < kSymmCW; ++c) acc[a][c] = 0.0;
   const int nsl = (np + kSymmJT - 1) / kSymmJT;
   unsigned uses = 0;   // TMA completions consumed per stage (bit st: parity of the next wait)
   for (int q = 0; q < kSymmNS - 1 && q < nsl; ++q) issue(q * kSymmJT, q);
@@ -668,9 +673,9 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
         const int cu = ((((jj >> 1) ^ sw) << 1) | (jj & 1));
         const double a0 = (I0 + i0 >= gj) ? As[jj * kSymmRows + i0] : Au[i0 * 16 + cu];
         const double a1 = (I0 + i0 + 64 >= gj) ? As[jj * kSymmRows + i0 + 64] : Au[(i0 + 64) * 16 + cu];
-        const double2* vr = reinterpret_cast<const double2*>(Vs + jj * kSB + 8 * h);
+        const double2* vr = reinterpret_cast<const double2*>(Vs + jj * kSB + kSymmCW * h);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kSymmCW / 2; ++q) {
           const double2 v = vr[q];
           acc[0][2 * q] = fma(a0, v.x, acc[0][2 * q]);
           acc[0][2 * q + 1] = fma(a0, v.y, acc[0][2 * q + 1]);
@@ -682,9 +687,9 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
 #pragma unroll 4
       for (int jj = 0; jj < jmax; ++jj) {
         const double a0 = As[jj * kSymmRows + i0], a1 = As[jj * kSymmRows + i0 + 64];
-        const double2* vr = reinterpret_cast<const double2*>(Vs + jj * kSB + 8 * h);
+        const double2* vr = reinterpret_cast<const double2*>(Vs + jj * kSB + kSymmCW * h);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kSymmCW / 2; ++q) {
           const double2 v = vr[q];
           acc[0][2 * q] = fma(a0, v.x, acc[0][2 * q]);
           acc[0][2 * q + 1] = fma(a0, v.y, acc[0][2 * q + 1]);
@@ -701,10 +706,10 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
         double2 a0 = *reinterpret_cast<const double2*>(Au + i0 * 16 + ch);
         double2 a1 = *reinterpret_cast<const double2*>(Au + (i0 + 64) * 16 + ch);
         if (2 * kp + 1 >= jmax) { a0.y = 0.0; a1.y = 0.0; }
-        const double2* v0 = reinterpret_cast<const double2*>(Vs + (2 * kp) * kSB + 8 * h);
-        const double2* v1 = reinterpret_cast<const double2*>(Vs + (2 * kp + 1) * kSB + 8 * h);
+        const double2* v0 = reinterpret_cast<const double2*>(Vs + (2 * kp) * kSB + kSymmCW * h);
+        const double2* v1 = reinterpret_cast<const double2*>(Vs + (2 * kp + 1) * kSB + kSymmCW * h);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kSymmCW / 2; ++q) {
           const double2 x = v0[q], y = v1[q];
           acc[0][2 * q] = fma(a0.y, y.x, fma(a0.x, x.x, acc[0][2 * q]));
           acc[0][2 * q + 1] = fma(a0.y, y.y, fma(a0.x, x.y, acc[0][2 * q + 1]));
@@ -726,16 +731,16 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) Xs[(i0 + 64 * a) * kX + 8 * h + c] = acc[a][c];
+    for (int c = 0; c < kSymmCW; ++c) Xs[(i0 + 64 * a) * kX + kSymmCW * h + c] = acc[a][c];
   const double* Tw = Vw + 2 * L.vsz();
-  for (int e = tid; e < kSB * kSB; e += kSymmThreads) Ts[e] = Tw[e];
-  for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
+  for (int e = tid; e < kSB * kSB; e += kSymmTT) Ts[e] = Tw[e];
+  for (int e = tid; e < kSymmRows * kSB; e += kSymmTT) {
     const int l = e >> 7, i = e & 127;
     Vb[e] = i < imax ? Vw[(int64_t)l * L.ldv + I0 + i] : 0.0;
   }
   __syncthreads();
-  {
-    const int i = tid;                       // kSymmThreads == kSymmRows: one row per thread
+  if (tid < kSymmRows) {
+    const int i = tid;                       // one row per thread
     double x[kSB];
 #pragma unroll
     for (int l = 0; l < kSB; ++l) x[l] = Xs[i * kX + l];
@@ -763,14 +768,14 @@ __global__ void __launch_bounds__(kSymmThreads, 2) k_sbr_symm_tma(const __grid_c
   }
   __syncthreads();
   double* Mw = L.mp(ws, p) + (int64_t)blockIdx.y * kSB * kSB;
-  for (int e = tid; e < kSB * kSB; e += kSymmThreads) {     // Q = sum of the 8 partials (fixed order)
+  for (int e = tid; e < kSB * kSB; e += kSymmTT) {     // Q = sum of the 8 partials (fixed order)
     double t = 0.0;
 #pragma unroll
     for (int g = 0; g < 8; ++g) t += Qp[g * kSB * kSB + e];
     Vb[e] = t;                                               // Q [a][c] (V_b no longer needed)
   }
   __syncthreads();
-  for (int e = tid; e < kSB * kSB; e += kSymmThreads) {     // M = Q T  (T upper triangular)
+  for (int e = tid; e < kSB * kSB; e += kSymmTT) {     // M = Q T  (T upper triangular)
     const int a = e >> 4, c = e & 15;
     double m = 0.0;
     for (int l = 0; l <= c; ++l) m = fma(Vb[a * kSB + l], Ts[l * kSB + c], m);
@@ -1399,7 +1404,7 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     const int nrb = (np0 + kSymmRows - 1) / kSymmRows;
     int pr = prof_begin(c, PC_SBR_SYMM);
     if (tma)
-      k_sbr_symm_tma<<<dim3(nprob, nrb), kSymmThreads, ymem, c.stream>>>(tlo, tup, G, ld, stride, d_ns, t, ws, L,
+      k_sbr_symm_tma<<<dim3(nprob, nrb), kSymmTT, ymem, c.stream>>>(tlo, tup, G, ld, stride, d_ns, t, ws, L,
                                                                          t & 1);
     else
       k_sbr_symm<<<dim3(nprob, nrb), kSymmThreads, symm_smem, c.stream>>>(G, ld, stride, d_ns, t, ws, L, t & 1);
