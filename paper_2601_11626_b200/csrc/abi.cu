@@ -82,6 +82,7 @@ cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
   if (const char* env = getenv("CMSVD_TC_WIDE")) h->c.tc_wide = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_TC_BIG")) h->c.tc_big = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_TC_WS")) h->c.tc_ws = !(env[0] == '0');
+  if (const char* env = getenv("CMSVD_ZZ_FUSED")) h->c.zz_fused = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_CHOL_BLOCKED")) h->c.chol_blocked = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_DUO")) h->c.eig_duo = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_DUO160")) h->c.eig_duo160 = !(env[0] == '0');

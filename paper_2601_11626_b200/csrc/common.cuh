@@ -141,6 +141,7 @@ struct Ctx {
   bool zz_syrk = true;                 // w <= 128: Z^T Z by k_syrk_zz instead of k_gemm_tn (CMSVD_ZZ_SYRK=0: off)
   bool tc_big = true;                  // q or w > 128: tcgen05 GEMM tiles instead of SIMT (CMSVD_TC_BIG=0: off)
   bool tc_ws = true;                   // ... by the warp-specialised TMA-fed kernel on pre-split planes (CMSVD_TC_WS=0: off)
+  bool zz_fused = true;                // k_gemm_ws: Z^T Z folded into the W' contraction (CMSVD_ZZ_FUSED=0: separate fp64 Gram)
   bool chol_blocked = true;            // CholQR: blocked Cholesky + inverse kernel (CMSVD_CHOL_BLOCKED=0: unblocked)
   bool big_tc = true;                  // A22 subspace-iteration products on tcgen05 tiles (CMSVD_BIG_TC=0: SIMT fp64)
   bool tc_wide = true;                 // ... with 256-column tiles for Z = Q^T F (CMSVD_TC_WIDE=0: 128)

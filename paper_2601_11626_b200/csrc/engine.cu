@@ -658,6 +658,10 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
   // ... by the warp-specialised TMA-fed kernel when every operand is a registered block's pre-split planes
   const bool use_ws = use_tc_big && c.tc_ws && dims.planes && gemm_ws_supported(c, m) && (QMAX & 3) == 0 &&
                       QMAX <= c.planes_cols && WMAX <= c.planes_cols;
+  // ... and Z^T Z folded into the W' contraction (Z planes as leading K stages): the lower-right block of the
+  // core Gram from one tensor-core pass; the fp32 accumulation matches the precision class of Z itself.
+  // Full-range (A22) bases only: their ||F||^2 split needs only tr(Z^T Z + W')
+  const bool zz_fused = use_ws && c.big && c.zz_fused && WMAX <= 256 && !tight;
   const int GMAX = std::max(1, dims.rrmax + dims.wmax);
   if (need_mat && ((!tight && GMAX > kEigMax) || WMAX > kEigMax))
     return fail(c, CMSVD_E_SHAPE, "pair_errors: core size r'+w = " + std::to_string(GMAX) + " exceeds " +
@@ -731,7 +735,8 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
         CK(launch_gemm_ws(c, 1, pr, Pc, d_bd, d_ad, full ? 1 : 0, QMAX, WMAX, Z, Zp, R, W), "pairs: R = F - Q Z (ws)");
         prof_end(c, pf);
         pf = prof_begin(c, PC_GRAM_W);
-        CK(launch_gemm_ws(c, 2, pr, Pc, d_bd, d_ad, full ? 1 : 0, QMAX, WMAX, Z, Zp, R, W), "pairs: W = R^T R (ws)");
+        CK(launch_gemm_ws(c, 2, pr, Pc, d_bd, d_ad, full ? 1 : 0, QMAX, WMAX, Z, Zp, R, W, zz_fused),
+           "pairs: W = R^T R (ws)");
         prof_end(c, pf);
       } else if (use_tc) {
         // fused tcgen05 3xTF32: Z = Q^T F, R' = F - Q Z (on chip), W' = R'^T R'
@@ -770,13 +775,15 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
         prof_end(c, pf);
       } else {
         pf = prof_begin(c, PC_GRAM_ZZ);
-        if (c.zz_syrk && WMAX <= 128)
+        if (zz_fused) {
+        } else if (c.zz_syrk && WMAX <= 128)
           CK(launch_syrk_zz(c, pr, Pc, d_bd, d_ad, full ? 1 : 0, QMAX, WMAX, Z, ZZ), "pairs: Z^T Z");
         else
           CK(launch_gemm_tn(c, dZZ, (int)Pc, WMAX, WMAX, true), "pairs: Z^T Z");
         prof_end(c, pf);
         pf = prof_begin(c, PC_BUILD_G);
-        k_build_G<<<(unsigned)Pc, kThreads, 0, c.stream>>>(pr, d_bd, d_ad, QMAX, WMAX, GMAX, Z, W, ZZ, Gm, zn2);
+        k_build_G<<<(unsigned)Pc, kThreads, 0, c.stream>>>(pr, d_bd, d_ad, QMAX, WMAX, GMAX, Z, W,
+                                                           zz_fused ? nullptr : ZZ, Gm, zn2);
         c.launches += 1;
         CK(cudaGetLastError(), "pairs: build G");
         prof_end(c, pf);

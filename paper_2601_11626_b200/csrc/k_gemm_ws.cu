@@ -69,6 +69,8 @@ struct WsArgs {
   int64_t ldc, sC;
   int Mg, Ng, Kg;
   int b_shared;    // 1: every problem uses B planes of batch entry 0
+  int zzK;         // MODE 2 (shared-A variant): leading K elements taken from the Z planes (third map), so that
+                   // the tile is Z^T Z + R'^T R' (the lower-right block of the core Gram); 0: W' alone
 };
 
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
       return (a.use_full ? b.q : b.rr);
     }
     if (MODE == 3) return a.Kg;
+    if (MODE == 2) return (int)a.m + a.zzK;
     return (int)a.m;
   };
 
@@ -271,8 +274,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
           const uint32_t base = sm + s * Cfg::kStageBytes;
           const int k0 = st * kWsKT;
           if (SHARE_A) {
-            tma_load_4d(base, &tmB, k0, kWsBN * tn, 0, (int)p, full);
-            tma_load_4d(base + kWsBTile, &tmB, k0, kWsBN * tn, 1, (int)p, full);
+            if (k0 < a.zzK) {   // Z planes first (K = the projection index), then the rows of R'
+              tma_load_4d(base, &tmF, k0, kWsBN * tn, 0, (int)p, full);
+              tma_load_4d(base + kWsBTile, &tmF, k0, kWsBN * tn, 1, (int)p, full);
+            } else {
+              tma_load_4d(base, &tmB, k0 - a.zzK, kWsBN * tn, 0, (int)p, full);
+              tma_load_4d(base + kWsBTile, &tmB, k0 - a.zzK, kWsBN * tn, 1, (int)p, full);
+            }
           } else {
             const uint32_t bA = base, bB = base + 2 * kWsATile;
             if (MODE == 0) {
@@ -580,7 +588,8 @@ static cudaError_t launch_ws(Ctx& c, const CUtensorMap& tA, const CUtensorMap& t
 // mode 0: Z = Q^T F (+ planes of Z); 1: R' planes = split(F - Q Z); 2: W' = R'^T R' (fp64 out).
 // Qp / Fp: the per-block plane arenas of the context (c.d_Qp, c.d_Fp: count x 2 x planes_cols x m).
 cudaError_t launch_gemm_ws(Ctx& c, int mode, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad,
-                           int use_full, int QMAX, int WMAX, float* Zws, float* Zp, float* Rp, double* Wws) {
+                           int use_full, int QMAX, int WMAX, float* Zws, float* Zp, float* Rp, double* Wws,
+                           bool add_zz) {
   if (P <= 0) return cudaSuccess;
   const int64_t m = c.m;
   WsArgs a{};
@@ -619,7 +628,15 @@ cudaError_t launch_gemm_ws(Ctx& c, int mode, const int2* pairs, int64_t P, const
   }
   a.tiles_m = (WMAX + kWsBM - 1) / kWsBM;
   if (!ws_map_k(&tB, Rp, m, WMAX, P, kWsBN)) return cudaErrorInvalidValue;
-  if (a.tiles_n == 1) return launch_ws<2, true>(c, tB, tB, tB, a);
+  if (a.tiles_n == 1) {
+    CUtensorMap tZ = tB;
+    if (add_zz) {
+      if (!ws_map_k(&tZ, Zp, QMAX, WMAX, P, kWsBN)) return cudaErrorInvalidValue;
+      a.zzK = (QMAX + kWsKT - 1) / kWsKT * kWsKT;
+    }
+    return launch_ws<2, true>(c, tB, tB, tZ, a);
+  }
+  if (add_zz) return cudaErrorInvalidValue;
   if (!ws_map_k(&tA, Rp, m, WMAX, P, kWsBM)) return cudaErrorInvalidValue;
   return launch_ws<2, false>(c, tA, tB, tB, a);
 }

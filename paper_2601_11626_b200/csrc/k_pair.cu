@@ -87,13 +87,15 @@ __global__ void __launch_bounds__(kThreads) k_build_G(const int2* __restrict__ p
     if (i < rr && j < rr) v = (i == j) ? b.spec[i] * b.spec[i] : 0.0;
     else if (i < rr) v = b.spec[i] * (double)Z[(int64_t)(j - rr) * QMAX + i];
     else if (j < rr) v = b.spec[j] * (double)Z[(int64_t)(i - rr) * QMAX + j];
-    else v = ZZ[(int64_t)(j - rr) * WMAX + (i - rr)] + W[(int64_t)(j - rr) * WMAX + (i - rr)];
+    else v = (ZZws ? ZZ[(int64_t)(j - rr) * WMAX + (i - rr)] : 0.0) + W[(int64_t)(j - rr) * WMAX + (i - rr)];
     G[(int64_t)j * GMAX + i] = v;
   }
   if (threadIdx.x == 0) {
+    // ZZws == nullptr: W already holds Z^T Z + R'^T R' (fused by k_gemm_ws; full bases only)
     double s = 0.0;
-    for (int i = 0; i < w; ++i) s += ZZ[(int64_t)i * WMAX + i];
-    if (b.full)  // A22: ||F||^2 = ||U_r^T F||^2 + ||(I - U_r U_r^T) F||^2 (whole operand is "residual-free")
+    if (ZZws)
+      for (int i = 0; i < w; ++i) s += ZZ[(int64_t)i * WMAX + i];
+    if (b.full || !ZZws)  // A22: ||F||^2 = ||U_r^T F||^2 + ||(I - U_r U_r^T) F||^2 (whole operand is "residual-free")
       for (int i = 0; i < w; ++i) s += W[(int64_t)i * WMAX + i];
     zn2[p] = s;
   }

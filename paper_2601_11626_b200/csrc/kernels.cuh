@@ -82,7 +82,8 @@ cudaError_t launch_gemm_ws_tn64(Ctx& c, int batch, int M, int N, int K, const fl
                                 double* C, int64_t ldc, int64_t sC);
 bool gemm_ws_available();
 cudaError_t launch_gemm_ws(Ctx& c, int mode, const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad,
-                           int use_full, int QMAX, int WMAX, float* Zws, float* Zp, float* Rp, double* Wws);
+                           int use_full, int QMAX, int WMAX, float* Zws, float* Zp, float* Rp, double* Wws,
+                           bool add_zz = false);   // mode 2 with add_zz: Wws = Z^T Z + R'^T R' (WMAX <= 256)
 // C (fp64) = A B, A: M x K, B: K x N column-major fp32 (3xTF32 tiles)
 cudaError_t launch_gemm_tc_nn64(Ctx& c, const GemmDesc* d_descs, int nprob, int maxM, int maxN);
 // Y[i] = (float) X[i] for n doubles
