@@ -135,6 +135,8 @@ struct Ctx {
   bool sbr_fused = false;              // band reduction: look-ahead fused update + product pass (CMSVD_SBR_FUSED=1;
                                        // measured 24.8 vs 23.0 ms unfused at n = 512: the partials' traffic)
   bool sbr_tma = true;                 // band reduction: TMA tile loads/stores in the rank-32 update (CMSVD_SBR_TMA=0)
+  bool syr2k_row = false;              // band reduction: row-persistent pipelined rank-32 update (CMSVD_SYR2K_ROW=1; measured equal,
+                                       // 17.2 vs 17.3 ms: the update is bound by shared-memory wavefronts, not by its loads)
   bool chase_flags = false;            // band chase: per-sweep progress flags instead of time-step barriers
   bool eig_sbr = true;                 // n > 160: two-stage (band) reduction instead of the one-stage in-place kernel
   bool eig_rr = true;                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)

@@ -576,6 +576,125 @@ __global__ void __launch_bounds__(kSyrThreads) k_sbr_syr2k_tma(const __grid_cons
 }
 
 // ---------------------------------------------------------------------------
+// Stage 1d, row-persistent variant: one CTA per (problem, tile row I); it walks the tiles J = 0 .. I of the
+// row through a two-stage ring (tile + V_J / W_J rows per stage; V_I / W_I stay resident), with a producer
+// thread issuing the TMA loads, the bulk stores of finished tiles and the refills, so that the update of
+// one tile overlaps the load of the next and the store of the previous one.  The one-tile-per-CTA kernel
+// spends ~60% of its time waiting for its own loads (ncu: long scoreboard) and pays one CTA launch per
+// 64 x 64 tile; here 21312 short CTAs per launch become <= 8 per problem.  Two CTAs per SM.
+// ---------------------------------------------------------------------------
+constexpr int kSyrRowThreads = kSyrThreads + 32;                       // 8 consumer warps + the producer warp
+constexpr int kSyrRowStage = kSyrTile * kSyrTile + 2 * kSB * kSyrTile;  // doubles per stage (48 KB)
+constexpr size_t kSyrRowSmem = ((size_t)2 * kSB * kSyrTile + 2 * kSyrRowStage + 8) * sizeof(double);
+
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kSyrRowThreads, 2) k_sbr_syr2k_row(const __grid_constant__ CUtensorMap tmap,
+                                                                     const __grid_constant__ CUtensorMap tmv,
+                                                                     const __grid_constant__ CUtensorMap tmw,
+                                                                     const int* __restrict__ ns, int t) {
+  extern __shared__ __align__(128) double rsm[];
+  double* VI = rsm;
+  double* WI = VI + kSB * kSyrTile;
+  double* stage0 = WI + kSB * kSyrTile;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + 2 * kSyrRowStage);   // full[2], done[2], vw
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int nt = (np + kSyrTile - 1) / kSyrTile;
+  const int ti = nt - 1 - (int)blockIdx.y;   // longest rows first
+  if (ti < 0) return;
+  const int I0 = ti * kSyrTile;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], kSyrThreads);
+    mbar_init(&bars[3], kSyrThreads);
+    mbar_init(&bars[4], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  constexpr unsigned kStageTx = (unsigned)(kSyrRowStage * sizeof(double));
+  if (tid >= kSyrThreads) {
+    // ---------------- producer ----------------
+    if (tid == kSyrThreads) {
+      auto load_stage = [&](int tj) {
+        const int s = tj & 1;
+        double* At = stage0 + s * kSyrRowStage;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[s])), "r"(kStageTx)
+                     : "memory");
+        tma_load_3d(At, &tmap, R0 + I0, R0 + tj * kSyrTile, p, &bars[s]);
+        tma_load_3d(At + kSyrTile * kSyrTile, &tmv, tj * kSyrTile, 0, p, &bars[s]);
+        tma_load_3d(At + kSyrTile * kSyrTile + kSB * kSyrTile, &tmw, tj * kSyrTile, 0, p, &bars[s]);
+      };
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[4])),
+                   "r"((unsigned)(2 * kSB * kSyrTile * sizeof(double)))
+                   : "memory");
+      tma_load_3d(VI, &tmv, I0, 0, p, &bars[4]);
+      tma_load_3d(WI, &tmw, I0, 0, p, &bars[4]);
+      load_stage(0);
+      if (ti >= 1) load_stage(1);
+      for (int tj = 0; tj <= ti; ++tj) {
+        const int s = tj & 1;
+        mbar_wait(&bars[2 + s], (tj >> 1) & 1u);                 // the consumers are done with tile tj
+        tma_store_3d(&tmap, R0 + I0, R0 + tj * kSyrTile, p, stage0 + s * kSyrRowStage);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (tj + 2 <= ti) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // the store has read the stage
+          load_stage(tj + 2);
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    return;
+  }
+  // ---------------- consumers (8 warps) ----------------
+  const int tx = tid & 31, ty = tid >> 5;
+  mbar_wait(&bars[4], 0);
+  for (int tj = 0; tj <= ti; ++tj) {
+    const int s = tj & 1;
+    double* At = stage0 + s * kSyrRowStage;
+    const double* VJ = At + kSyrTile * kSyrTile;
+    const double* WJ = VJ + kSB * kSyrTile;
+    mbar_wait(&bars[s], (tj >> 1) & 1u);
+    const bool diag = ti == tj;
+    double a[2][8];
+#pragma unroll
+    for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) a[r2][c] = At[(8 * ty + c) * kSyrTile + tx + 32 * r2];
+#pragma unroll 4
+    for (int l = 0; l < kSB; ++l) {
+      const double vi0 = VI[l * kSyrTile + tx], vi1 = VI[l * kSyrTile + tx + 32];
+      const double wi0 = WI[l * kSyrTile + tx], wi1 = WI[l * kSyrTile + tx + 32];
+      const double2* vj2 = reinterpret_cast<const double2*>(VJ + l * kSyrTile + 8 * ty);
+      const double2* wj2 = reinterpret_cast<const double2*>(WJ + l * kSyrTile + 8 * ty);
+#pragma unroll
+      for (int c2 = 0; c2 < 4; ++c2) {
+        const double2 vj = vj2[c2], wj = wj2[c2];
+        a[0][2 * c2] = fma(-vi0, wj.x, fma(-wi0, vj.x, a[0][2 * c2]));
+        a[1][2 * c2] = fma(-vi1, wj.x, fma(-wi1, vj.x, a[1][2 * c2]));
+        a[0][2 * c2 + 1] = fma(-vi0, wj.y, fma(-wi0, vj.y, a[0][2 * c2 + 1]));
+        a[1][2 * c2 + 1] = fma(-vi1, wj.y, fma(-wi1, vj.y, a[1][2 * c2 + 1]));
+      }
+    }
+#pragma unroll
+    for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int i = tx + 32 * r2, j = 8 * ty + c;
+        if (!diag || i >= j) At[j * kSyrTile + i] = a[r2][c];
+      }
+    fence_proxy_async();          // generic-proxy smem writes visible to the bulk store
+    mbar_arrive_cta(&bars[2 + s]);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Stage 1b (TMA variant).  Slices below the diagonal block (all i >= j) arrive as one 128 x 32 box of the
 // lower storage (dense [j][i] in shared memory); slices right of it (all i < j, A22(i, j) = G(j, i)) as two
 // 16 x 128 boxes of the transposed region with the 128-byte swizzle, so that reading a row i of the slice
@@ -1378,6 +1497,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   if (tma) {
     cudaError_t e2 = cudaFuncSetAttribute(k_sbr_syr2k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
     if (e2 != cudaSuccess) return e2;
+    e2 = cudaFuncSetAttribute(k_sbr_syr2k_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrRowSmem);
+    if (e2 != cudaSuccess) return e2;
     e2 = cudaFuncSetAttribute(k_sbr_symm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ymem);
     if (e2 != cudaSuccess) return e2;
     e2 = cudaFuncSetAttribute(k_sbr_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
@@ -1447,7 +1568,10 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
       }
     } else {
       const int pr = prof_begin(c, PC_SBR_SYR2K);
-      if (tma2)
+      if (tma2 && c.syr2k_row)
+        k_sbr_syr2k_row<<<dim3(nprob, nt), kSyrRowThreads, kSyrRowSmem, c.stream>>>(tmap, tmv[t & 1], tmw[t & 1],
+                                                                                    d_ns, t);
+      else if (tma2)
         k_sbr_syr2k_tma<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, tsmem, c.stream>>>(tmap, tmv[t & 1],
                                                                                           tmw[t & 1], d_ns, t);
       else
