@@ -135,6 +135,8 @@ struct Ctx {
   bool sbr_fused = false;              // band reduction: look-ahead fused update + product pass (CMSVD_SBR_FUSED=1;
                                        // measured 24.8 vs 23.0 ms unfused at n = 512: the partials' traffic)
   bool sbr_tma = true;                 // band reduction: TMA tile loads/stores in the rank-32 update (CMSVD_SBR_TMA=0)
+  bool symm_dmma = true;               // band reduction: Y = A22 V T on the fp64 tensor cores (CMSVD_SYMM_DMMA=0: scalar kernel)
+  bool syr2k_dmma = true;              // band reduction: rank-32 update on the fp64 tensor cores (CMSVD_SYR2K_DMMA=0: scalar kernel)
   bool syr2k_row = false;              // band reduction: row-persistent pipelined rank-32 update (CMSVD_SYR2K_ROW=1; measured equal,
                                        // 17.2 vs 17.3 ms: the update is bound by shared-memory wavefronts, not by its loads)
   bool chase_flags = false;            // band chase: per-sweep progress flags instead of time-step barriers

@@ -576,6 +576,117 @@ __global__ void __launch_bounds__(kSyrThreads) k_sbr_syr2k_tma(const __grid_cons
 }
 
 // ---------------------------------------------------------------------------
+// Stage 1d on the fp64 tensor cores (DMMA m8n8k4), default: A22 tile (64 x 64) -= [V_I W_I] [W_J V_J]^T as a
+// K = 32 product, a warp owning 32 rows x 16 columns as 4 x 2 accumulator fragments initialised from the
+// tile.  The scalar kernel is bound by shared-memory wavefronts (73% of the SM rate); fragments cut them
+// to ~60%, given conflict-free layouts: the tile and the V / W rows arrive through 4-D views (i % 16, j or
+// l, i / 16, problem) as 16-row boxes with the 128-byte swizzle ([i / 16][j][16 i]), the tile leaves
+// through the same map, and the k index of a step is mapped to l = s + 4t (see k_sbr_symm_dmma).
+// ---------------------------------------------------------------------------
+constexpr int kSyrDTile = kSyrTile * kSyrTile;       // doubles per tile (32 KB)
+constexpr int kSyrDOp = kSB * kSyrTile;              // doubles per V / W operand (8 KB)
+constexpr size_t kSyrDSmem = ((size_t)kSyrDTile + 4 * kSyrDOp + 2) * sizeof(double) + 1024;
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kSyrThreads, 3) k_sbr_syr2k_dmma(const __grid_constant__ CUtensorMap tm4,
+                                                                   const __grid_constant__ CUtensorMap tv4,
+                                                                   const __grid_constant__ CUtensorMap tw4,
+                                                                   const int* __restrict__ ns, int t) {
+  extern __shared__ uint8_t dsm_raw[];
+  double* At = reinterpret_cast<double*>(dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u));
+  double* VI = At + kSyrDTile;                        // [i / 16][l][16 i], swizzled
+  double* WI = VI + kSyrDOp;
+  double* VJ = WI + kSyrDOp;
+  double* WJ = VJ + kSyrDOp;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(WJ + kSyrDOp);
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int nt = (np + kSyrTile - 1) / kSyrTile;
+  int q = blockIdx.y, ti = 0;
+  while (q > ti) { ++ti; q -= ti; }
+  const int tj = q;
+  if (ti >= nt) return;
+  const int I0 = ti * kSyrTile, J0 = tj * kSyrTile;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int fg = lane >> 2, ft = lane & 3;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"((unsigned)((kSyrDTile + 4 * kSyrDOp) * sizeof(double)))
+                 : "memory");
+    tma_load_4d(At, &tm4, 0, R0 + J0, (R0 + I0) >> 4, p, bar);
+    tma_load_4d(VI, &tv4, 0, 0, I0 >> 4, p, bar);
+    tma_load_4d(WI, &tw4, 0, 0, I0 >> 4, p, bar);
+    tma_load_4d(VJ, &tv4, 0, 0, J0 >> 4, p, bar);
+    tma_load_4d(WJ, &tw4, 0, 0, J0 >> 4, p, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // warp tile: rows 32 wr .. + 31, columns 16 wc .. + 15
+  const int wr = wid & 1, wc = wid >> 1;
+  const bool diag = ti == tj;
+  // swizzled offsets: element (x, y) of a [x / 16][y][16 x] block with `pitch` y rows per 16-row group
+  auto off = [](int x, int y, int pitch) {
+    const int xb = x & 15;
+    return (x >> 4) * (pitch * 16) + y * 16 + ((((xb >> 1) ^ (y & 7)) << 1) | (xb & 1));
+  };
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) {
+      const int i = 32 * wr + 8 * a + fg, j = 16 * wc + 8 * bb + 2 * ft;
+      acc[a][bb][0] = At[off(i, j, kSyrTile)];
+      acc[a][bb][1] = At[off(i, j + 1, kSyrTile)];
+    }
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const double* PI = half == 0 ? VI : WI;   // rows of the tile: V_I then W_I
+    const double* QJ = half == 0 ? WJ : VJ;   // columns: W_J then V_J
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4) {
+      const int l = s4 + 4 * ft;
+      double qb[2];
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb) qb[bb] = QJ[off(16 * wc + 8 * bb + fg, l, kSB)];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double pa = -PI[off(32 * wr + 8 * a + fg, l, kSB)];
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) dmma_f64(acc[a][bb][0], acc[a][bb][1], pa, qb[bb]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) {
+      const int i = 32 * wr + 8 * a + fg, j = 16 * wc + 8 * bb + 2 * ft;
+      if (!diag || i >= j) At[off(i, j, kSyrTile)] = acc[a][bb][0];
+      if (!diag || i >= j + 1) At[off(i, j + 1, kSyrTile)] = acc[a][bb][1];
+    }
+  fence_proxy_async();     // generic-proxy smem writes visible to the bulk copy
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+                 ::"l"(&tm4), "r"(0), "r"(R0 + J0), "r"((R0 + I0) >> 4), "r"(p), "r"(smem_u32(At))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Stage 1d, row-persistent variant: one CTA per (problem, tile row I); it walks the tiles J = 0 .. I of the
 // row through a two-stage ring (tile + V_J / W_J rows per stage; V_I / W_I stay resident), with a producer
 // thread issuing the TMA loads, the bulk stores of finished tiles and the refills, so that the update of
@@ -901,6 +1012,205 @@ __global__ void __launch_bounds__(kSymmTT, 2) k_sbr_symm_tma(const __grid_consta
     Mw[e] = m;
   }
 }
+
+// ---------------------------------------------------------------------------
+// Stage 1b on the fp64 tensor cores (DMMA m8n8k4), default.  The scalar kernel above is bound by
+// shared-memory wavefronts (81% of the SM rate: every DFMA row operand is a 64-bit load of 32 lanes = 2
+// wavefronts, 0.5 wavefronts per DFMA).  Here a warp owns 32 rows x 16 columns of Y as 4 x 2 accumulator
+// fragments and reads the 16-column slice of A22 as 8 x 4 fragments, 16 + 8 loads for 32 DMMAs (8192 FMAs):
+// 2.7x fewer wavefronts, provided every fragment load is free of bank conflicts:
+//   * slices right of the diagonal block arrive as the transposed 16 x 128 box with the 128-byte swizzle
+//     ([i][16 j], as before): fragment (rows 8a + g, k = j = 4s + t) touches 8 chunks x 2 halves exactly;
+//   * slices below it arrive through a 4-D view of the lower storage (i % 16, j, i / 16, problem) as eight
+//     16 x 16 boxes with the 128-byte swizzle ([i / 16][j][16 i]); with the k index mapped to j = s + 4t
+//     (any bijection of k is allowed as long as the V fragment uses the same one) the four j rows of a
+//     fragment fall into both halves of the swizzle: conflict-free as well;
+//   * the V slice is staged with its own swizzle (16-byte chunk ^ 4 (bit1(j) ^ bit3(j))), which serves
+//     both k mappings;
+//   * slices crossing the diagonal run both passes with complementary masks.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_dmma(const __grid_constant__ CUtensorMap tlo4,
+                                                                    const __grid_constant__ CUtensorMap tup,
+                                                                    const double* __restrict__ G, int64_t ld,
+                                                                    int64_t stride, const int* __restrict__ ns,
+                                                                    int t, double* __restrict__ ws, const SbrWs L,
+                                                                    int par) {
+  extern __shared__ __align__(1024) double ysm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ysm + kSymmNS * kSymmStage);
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int I0 = blockIdx.y * kSymmRows;
+  if (I0 >= np) return;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int fg = lane >> 2, ft = lane & 3;   // DMMA fragment coordinates
+  const double* Vw = L.vp(ws, p, par);
+  double* Yw = const_cast<double*>(Vw) + L.vsz();
+  const int imax = min(kSymmRows, np - I0);
+  (void)G; (void)ld; (void)stride;
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < kSymmNS; ++q) mbar_init(&bars[q], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto kind = [&](int J0) {
+    const int jmax = min(kSymmJT, np - J0);
+    return (J0 + jmax - 1 <= I0) ? 0 : ((I0 + imax - 1 < J0) ? 1 : 2);
+  };
+  auto issue = [&](int J0, int st) {
+    double* As = ysm + st * kSymmStage;   // lower boxes [i / 16][j][16 i], then the transposed box [i][16 j]
+    double* Vs = As + 2 * kSymmA;
+    const int jmax = min(kSymmJT, np - J0);
+    const int kd = kind(J0);
+    if (tid == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[st])),
+                   "r"((unsigned)((kd == 2 ? 2 : 1) * kSymmA * sizeof(double)))
+                   : "memory");
+      if (kd != 1)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+            ::"r"(smem_u32(As)), "l"(&tlo4), "r"(0), "r"(R0 + J0), "r"((R0 + I0) >> 4), "r"(p), "r"(smem_u32(&bars[st]))
+            : "memory");
+      if (kd != 0) tma_load_3d(As + kSymmA, &tup, R0 + J0, R0 + I0, p, &bars[st]);
+    }
+    for (int e = tid; e < kSymmJT * kSB; e += kSymmThreads) {
+      const int jj = e >> 4, c = e & 15;
+      const bool ok = jj < jmax;
+      const int sel = ((jj >> 1) ^ (jj >> 3)) & 1;
+      cp_async8(Vs + jj * kSB + ((((c >> 1) ^ (sel << 2)) << 1) | (c & 1)), ok ? Vw + (int64_t)c * L.ldv + J0 + jj : Vw,
+                ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) acc[a][bb][0] = acc[a][bb][1] = 0.0;
+  const int nsl = (np + kSymmJT - 1) / kSymmJT;
+  unsigned uses = 0;
+  for (int q = 0; q < kSymmNS - 1 && q < nsl; ++q) issue(q * kSymmJT, q);
+  for (int k = 0; k < nsl; ++k) {
+    const int st = k % kSymmNS;
+    const int J0 = k * kSymmJT;
+    if (k + kSymmNS - 1 < nsl) issue((k + kSymmNS - 1) * kSymmJT, (k + kSymmNS - 1) % kSymmNS);
+    const int pending = min(nsl, k + kSymmNS) - k - 1;
+    if (pending >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else if (pending == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    const int kd = kind(J0);
+    mbar_wait(&bars[st], (uses >> st) & 1u);
+    uses ^= 1u << st;
+    __syncthreads();
+    const double* Al = ysm + st * kSymmStage;
+    const double* Au = Al + kSymmA;
+    const double* Vs = Al + 2 * kSymmA;
+    const int jmax = min(kSymmJT, np - J0);
+    const bool full = jmax == kSymmJT && imax == kSymmRows;
+    // one pass over the slice with the k mapping of its storage: LOWER (j = s + 4t) or transposed (j = 4s + t)
+    auto pass = [&](bool lower, bool masked) {
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int jj = lower ? s4 + 4 * ft : 4 * s4 + ft;
+        const int sel = ((jj >> 1) ^ (jj >> 3)) & 1;
+        double vb[2];
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+          vb[bb] = Vs[jj * kSB + (((((8 * bb + fg) >> 1) ^ (sel << 2)) << 1) | (fg & 1))];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int i = 32 * wid + 8 * a + fg;
+          double av;
+          if (lower) {
+            const int ib = i & 15;
+            av = Al[(i >> 4) * 256 + jj * 16 + ((((ib >> 1) ^ (jj & 7)) << 1) | (ib & 1))];
+          } else {
+            av = Au[i * 16 + ((((jj >> 1) ^ (i & 7)) << 1) | (jj & 1))];
+          }
+          if (masked) {
+            const bool low = I0 + i >= J0 + jj;
+            if (low != lower || jj >= jmax || i >= imax) av = 0.0;
+          } else if (!full) {
+            if (jj >= jmax || i >= imax) av = 0.0;
+          }
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb) dmma_f64(acc[a][bb][0], acc[a][bb][1], av, vb[bb]);
+        }
+      }
+    };
+    if (kd == 0) pass(true, false);
+    else if (kd == 1) pass(false, false);
+    else { pass(true, true); pass(false, true); }
+    __syncthreads();   // this stage is reissued kSymmNS - 1 steps later
+  }
+  // epilogue: X rows to shared memory (row stride 17); Y = X T by row (thread = row, X row in registers);
+  // M_b = V_b^T Y_b = (V_b^T X_b) T with Q = V_b^T X_b as 8 row-group partials (16 independent
+  // accumulators per thread, no long serial chains), then M = Q T
+  constexpr int kX = kSB + 1;
+  double* Xs = ysm;                          // [128][17]
+  double* Ts = Xs + kSymmRows * kX;          // [16][16]
+  double* Vb = Ts + kSB * kSB;               // [16][128]
+  double* Qp = Vb + kSB * kSymmRows;         // [8][16][16] partials, then Q [16][16]
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) {
+      Xs[(32 * wid + 8 * a + fg) * kX + 8 * bb + 2 * ft] = acc[a][bb][0];
+      Xs[(32 * wid + 8 * a + fg) * kX + 8 * bb + 2 * ft + 1] = acc[a][bb][1];
+    }
+  const double* Tw = Vw + 2 * L.vsz();
+  for (int e = tid; e < kSB * kSB; e += kSymmThreads) Ts[e] = Tw[e];
+  for (int e = tid; e < kSymmRows * kSB; e += kSymmThreads) {
+    const int l = e >> 7, i = e & 127;
+    Vb[e] = i < imax ? Vw[(int64_t)l * L.ldv + I0 + i] : 0.0;
+  }
+  __syncthreads();
+  if (tid < kSymmRows) {
+    const int i = tid;                       // one row per thread
+    double x[kSB];
+#pragma unroll
+    for (int l = 0; l < kSB; ++l) x[l] = Xs[i * kX + l];
+    if (i < imax) {
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) {
+        double y = 0.0;
+#pragma unroll
+        for (int l = 0; l <= c; ++l) y = fma(x[l], Ts[l * kSB + c], y);
+        Yw[(int64_t)c * L.ldv + I0 + i] = y;
+      }
+    }
+    // Q partial over rows 16 g .. 16 g + 15 for row a of V_b^T: thread (g = tid >> 4, a = tid & 15)
+    const int g = tid >> 4, a = tid & 15;
+    double q[kSB];
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) q[c] = 0.0;
+    for (int ii = 16 * g; ii < 16 * g + 16; ++ii) {
+      const double v = Vb[a * kSymmRows + ii];
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) q[c] = fma(v, Xs[ii * kX + c], q[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) Qp[(g * kSB + a) * kSB + c] = q[c];
+  }
+  __syncthreads();
+  double* Mw = L.mp(ws, p) + (int64_t)blockIdx.y * kSB * kSB;
+  for (int e = tid; e < kSB * kSB; e += kSymmThreads) {     // Q = sum of the 8 partials (fixed order)
+    double t = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) t += Qp[g * kSB * kSB + e];
+    Vb[e] = t;                                               // Q [a][c] (V_b no longer needed)
+  }
+  __syncthreads();
+  for (int e = tid; e < kSB * kSB; e += kSymmThreads) {     // M = Q T  (T upper triangular)
+    const int a = e >> 4, c = e & 15;
+    double m = 0.0;
+    for (int l = 0; l <= c; ++l) m = fma(Vb[a * kSB + l], Ts[l * kSB + c], m);
+    Mw[e] = m;
+  }
+}
+
 
 // ---------------------------------------------------------------------------
 // Fused stage 1 (look-ahead): one pass over the trailing matrix per panel.
@@ -1446,6 +1756,45 @@ static bool sbr_tensor_map(CUtensorMap* map, double* G, int64_t ld, int64_t stri
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 4-D view of the lower storage (i % 16, j, i / 16, problem): eight 16 x 16 boxes with the 128-byte swizzle
+// per 128 x 16 slice, shared-memory order [i / 16][j][16 i] (k_sbr_symm_dmma); ld must be a multiple of 16
+static bool sbr_tensor_map_lo4(CUtensorMap* map, double* G, int64_t ld, int64_t stride, int nprob) {
+  auto fn = sbr_encode_fn();
+  if (!fn || (ld & 15) != 0) return false;
+  cuuint64_t dims[4] = {16, (cuuint64_t)ld, (cuuint64_t)(ld / 16), (cuuint64_t)nprob};
+  cuuint64_t strides[3] = {(cuuint64_t)ld * sizeof(double), 128, (cuuint64_t)stride * sizeof(double)};
+  cuuint32_t box[4] = {16, (cuuint32_t)kSymmJT, (cuuint32_t)(kSymmRows / 16), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, G, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// the same view with 64-column boxes (the 64 x 64 tile of k_sbr_syr2k_dmma: four 16-row groups)
+static bool sbr_tensor_map_tile4(CUtensorMap* map, double* G, int64_t ld, int64_t stride, int nprob) {
+  auto fn = sbr_encode_fn();
+  if (!fn || (ld & 15) != 0) return false;
+  cuuint64_t dims[4] = {16, (cuuint64_t)ld, (cuuint64_t)(ld / 16), (cuuint64_t)nprob};
+  cuuint64_t strides[3] = {(cuuint64_t)ld * sizeof(double), 128, (cuuint64_t)stride * sizeof(double)};
+  cuuint32_t box[4] = {16, (cuuint32_t)kSyrTile, (cuuint32_t)(kSyrTile / 16), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, G, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+// V / W rows of the workspace ([l][i], ld = L.ldv) as (i % 16, l, i / 16, problem): 64 rows x 16 l per box
+static bool sbr_ws_map4(CUtensorMap* map, double* base, int nprob, const SbrWs& L) {
+  auto fn = sbr_encode_fn();
+  if (!fn || ((uintptr_t)base % 16) != 0 || (L.ldv & 15) != 0) return false;
+  cuuint64_t dims[4] = {16, (cuuint64_t)kSB, (cuuint64_t)(L.ldv / 16), (cuuint64_t)nprob};
+  cuuint64_t strides[3] = {(cuuint64_t)L.ldv * sizeof(double), 128, (cuuint64_t)L.per * sizeof(double)};
+  cuuint32_t box[4] = {16, (cuuint32_t)kSB, (cuuint32_t)(kSyrTile / 16), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 static bool sbr_ws_map(CUtensorMap* map, double* base, int nprob, const SbrWs& L, int rows) {
   auto fn = sbr_encode_fn();
   if (!fn || ((uintptr_t)base % 16) != 0) return false;
@@ -1480,6 +1829,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
                    sbr_tensor_map(&tmap, G, ld, stride, nprob, kSyrTile, kSyrTile, CU_TENSOR_MAP_SWIZZLE_NONE) &&
                    sbr_tensor_map(&tlo, G, ld, stride, nprob, kSymmRows, kSymmJT, CU_TENSOR_MAP_SWIZZLE_NONE) &&
                    sbr_tensor_map(&tup, G, ld, stride, nprob, 16, kSymmRows, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tlo4;
+  const bool dmma = tma && c.symm_dmma && sbr_tensor_map_lo4(&tlo4, G, ld, stride, nprob);
   const size_t ymem = std::max((size_t)kSymmNS * kSymmStage + 4,
                                (size_t)kSymmRows * (kSB + 1) + kSB * kSB + 2 * kSymmRows * kSB + 4) * sizeof(double);
   // V and W of both parity sets as 3-D maps (64 x 16 boxes; V of the next panel also as 66 x 16 boxes)
@@ -1489,6 +1840,14 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     tma2 = sbr_ws_map(&tmv[q2], ws + q2 * L.set, nprob, L, kSyrTile) &&
            sbr_ws_map(&tmw[q2], ws + q2 * L.set + L.vsz(), nprob, L, kSyrTile) &&
            sbr_ws_map(&tvn[q2], ws + q2 * L.set, nprob, L, kFP);
+  CUtensorMap tm4, tv4[2], tw4[2];
+  bool sdm = tma2 && c.syr2k_dmma && sbr_tensor_map_tile4(&tm4, G, ld, stride, nprob);
+  for (int q2 = 0; q2 < 2 && sdm; ++q2)
+    sdm = sbr_ws_map4(&tv4[q2], ws + q2 * L.set, nprob, L) && sbr_ws_map4(&tw4[q2], ws + q2 * L.set + L.vsz(), nprob, L);
+  if (sdm) {
+    cudaError_t e3 = cudaFuncSetAttribute(k_sbr_syr2k_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrDSmem);
+    if (e3 != cudaSuccess) return e3;
+  }
   const bool fused = tma2 && c.sbr_fused &&
                      sbr_tensor_map(&tm66, G, ld, stride, nprob, kFP, kSyrTile, CU_TENSOR_MAP_SWIZZLE_NONE);
   const size_t tsmem = ((size_t)kSyrTile * kSyrTile + 4 * kSB * kSyrTile + 2) * sizeof(double);
@@ -1500,6 +1859,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     e2 = cudaFuncSetAttribute(k_sbr_syr2k_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrRowSmem);
     if (e2 != cudaSuccess) return e2;
     e2 = cudaFuncSetAttribute(k_sbr_symm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ymem);
+    if (e2 != cudaSuccess) return e2;
+    e2 = cudaFuncSetAttribute(k_sbr_symm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ymem);
     if (e2 != cudaSuccess) return e2;
     e2 = cudaFuncSetAttribute(k_sbr_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
     if (e2 != cudaSuccess) return e2;
@@ -1524,7 +1885,10 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     const int np0 = nmax - (t + 1) * kSB;
     const int nrb = (np0 + kSymmRows - 1) / kSymmRows;
     int pr = prof_begin(c, PC_SBR_SYMM);
-    if (tma)
+    if (dmma)
+      k_sbr_symm_dmma<<<dim3(nprob, nrb), kSymmThreads, ymem, c.stream>>>(tlo4, tup, G, ld, stride, d_ns, t, ws, L,
+                                                                          t & 1);
+    else if (tma)
       k_sbr_symm_tma<<<dim3(nprob, nrb), kSymmTT, ymem, c.stream>>>(tlo, tup, G, ld, stride, d_ns, t, ws, L,
                                                                          t & 1);
     else
@@ -1568,7 +1932,10 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
       }
     } else {
       const int pr = prof_begin(c, PC_SBR_SYR2K);
-      if (tma2 && c.syr2k_row)
+      if (sdm)
+        k_sbr_syr2k_dmma<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, kSyrDSmem, c.stream>>>(tm4, tv4[t & 1],
+                                                                                               tw4[t & 1], d_ns, t);
+      else if (tma2 && c.syr2k_row)
         k_sbr_syr2k_row<<<dim3(nprob, nt), kSyrRowThreads, kSyrRowSmem, c.stream>>>(tmap, tmv[t & 1], tmw[t & 1],
                                                                                     d_ns, t);
       else if (tma2)
