@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kSyrThreads, 3) k_sbr_syr2k_dmma(const __grid_
     const double* QJ = half == 0 ? WJ : VJ;   // columns: W_J then V_J
 #pragma unroll
     for (int s4 = 0; s4 < 4; ++s4) {
-      const int l = s4 + 4 * ft;
+      const int l = (s4 & 1) + 2 * ft + 8 * (s4 >> 1);   // k -> l: every half-warp covers the swizzle once
       double qb[2];
 #pragma unroll
       for (int bb = 0; bb < 2; ++bb) qb[bb] = QJ[off(16 * wc + 8 * bb + fg, l, kSB)];
@@ -805,6 +805,128 @@ __global__ void __launch_bounds__(kSyrRowThreads, 2) k_sbr_syr2k_row(const __gri
   }
 }
 
+// the row-persistent pipeline with the DMMA update and the swizzled 4-D views (default)
+__global__ void __launch_bounds__(kSyrRowThreads, 2) k_sbr_syr2k_rowd(const __grid_constant__ CUtensorMap tm4,
+                                                                     const __grid_constant__ CUtensorMap tv4,
+                                                                     const __grid_constant__ CUtensorMap tw4,
+                                                                     const int* __restrict__ ns, int t) {
+  extern __shared__ __align__(1024) double rsmd[];
+  double* VI = rsmd;
+  double* WI = VI + kSB * kSyrTile;
+  double* stage0 = WI + kSB * kSyrTile;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + 2 * kSyrRowStage);   // full[2], done[2], vw
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  if (t >= sbr_panels(n)) return;
+  const int R0 = (t + 1) * kSB, np = n - R0;
+  const int nt = (np + kSyrTile - 1) / kSyrTile;
+  const int ti = nt - 1 - (int)blockIdx.y;   // longest rows first
+  if (ti < 0) return;
+  const int I0 = ti * kSyrTile;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], kSyrThreads);
+    mbar_init(&bars[3], kSyrThreads);
+    mbar_init(&bars[4], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  constexpr unsigned kStageTx = (unsigned)(kSyrRowStage * sizeof(double));
+  if (tid >= kSyrThreads) {
+    // ---------------- producer ----------------
+    if (tid == kSyrThreads) {
+      auto load_stage = [&](int tj) {
+        const int s = tj & 1;
+        double* At = stage0 + s * kSyrRowStage;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[s])), "r"(kStageTx)
+                     : "memory");
+        tma_load_4d(At, &tm4, 0, R0 + tj * kSyrTile, (R0 + I0) >> 4, p, &bars[s]);
+        tma_load_4d(At + kSyrTile * kSyrTile, &tv4, 0, 0, (tj * kSyrTile) >> 4, p, &bars[s]);
+        tma_load_4d(At + kSyrTile * kSyrTile + kSB * kSyrTile, &tw4, 0, 0, (tj * kSyrTile) >> 4, p, &bars[s]);
+      };
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[4])),
+                   "r"((unsigned)(2 * kSB * kSyrTile * sizeof(double)))
+                   : "memory");
+      tma_load_4d(VI, &tv4, 0, 0, I0 >> 4, p, &bars[4]);
+      tma_load_4d(WI, &tw4, 0, 0, I0 >> 4, p, &bars[4]);
+      load_stage(0);
+      if (ti >= 1) load_stage(1);
+      for (int tj = 0; tj <= ti; ++tj) {
+        const int s = tj & 1;
+        mbar_wait(&bars[2 + s], (tj >> 1) & 1u);                 // the consumers are done with tile tj
+        asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+                     ::"l"(&tm4), "r"(0), "r"(R0 + tj * kSyrTile), "r"((R0 + I0) >> 4), "r"(p),
+                       "r"(smem_u32(stage0 + s * kSyrRowStage))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (tj + 2 <= ti) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // the store has read the stage
+          load_stage(tj + 2);
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    return;
+  }
+  // ---------------- consumers (8 warps) ----------------
+  const int wid = tid >> 5, lane = tid & 31;
+  const int fg = lane >> 2, ft = lane & 3;
+  const int wr = wid & 1, wc = wid >> 1;
+  auto off = [](int x, int y, int pitch) {
+    const int xb = x & 15;
+    return (x >> 4) * (pitch * 16) + y * 16 + ((((xb >> 1) ^ (y & 7)) << 1) | (xb & 1));
+  };
+  mbar_wait(&bars[4], 0);
+  for (int tj = 0; tj <= ti; ++tj) {
+    const int s = tj & 1;
+    double* At = stage0 + s * kSyrRowStage;
+    const double* VJ = At + kSyrTile * kSyrTile;
+    const double* WJ = VJ + kSB * kSyrTile;
+    mbar_wait(&bars[s], (tj >> 1) & 1u);
+    const bool diag = ti == tj;
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb) {
+        const int i = 32 * wr + 8 * a + fg, j = 16 * wc + 8 * bb + 2 * ft;
+        acc[a][bb][0] = At[off(i, j, kSyrTile)];
+        acc[a][bb][1] = At[off(i, j + 1, kSyrTile)];
+      }
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const double* PI = half == 0 ? VI : WI;
+      const double* QJ = half == 0 ? WJ : VJ;
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int l = (s4 & 1) + 2 * ft + 8 * (s4 >> 1);
+        double qb[2];
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) qb[bb] = QJ[off(16 * wc + 8 * bb + fg, l, kSB)];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const double pa = -PI[off(32 * wr + 8 * a + fg, l, kSB)];
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb) dmma_f64(acc[a][bb][0], acc[a][bb][1], pa, qb[bb]);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb) {
+        const int i = 32 * wr + 8 * a + fg, j = 16 * wc + 8 * bb + 2 * ft;
+        if (!diag || i >= j) At[off(i, j, kSyrTile)] = acc[a][bb][0];
+        if (!diag || i >= j + 1) At[off(i, j + 1, kSyrTile)] = acc[a][bb][1];
+      }
+    fence_proxy_async();          // generic-proxy smem writes visible to the bulk store
+    mbar_arrive_cta(&bars[2 + s]);
+  }
+}
+
+
 // ---------------------------------------------------------------------------
 // Stage 1b (TMA variant).  Slices below the diagonal block (all i >= j) arrive as one 128 x 32 box of the
 // lower storage (dense [j][i] in shared memory); slices right of it (all i < j, A22(i, j) = G(j, i)) as two
@@ -813,7 +935,10 @@ __global__ void __launch_bounds__(kSyrRowThreads, 2) k_sbr_syr2k_row(const __gri
 // cp.async.  Two stages in flight; the V slices (32 x 16) follow by cp.async.
 // ---------------------------------------------------------------------------
 constexpr int kSymmJT = 16;                    // columns per TMA slice (one 16 x 128 swizzled box when transposed)
-constexpr int kSymmNS = 3;                     // stages in flight
+#ifndef CMSVD_SYMM_NS
+#define CMSVD_SYMM_NS 2
+#endif
+constexpr int kSymmNS = CMSVD_SYMM_NS;         // stages in flight (2: 70 KB per CTA, three CTAs per SM)
 constexpr int kSymmA = kSymmJT * kSymmRows;    // doubles per A slice (16 KB)
 constexpr int kSymmStage = 2 * kSymmA + kSymmJT * kSB;   // lower box + transposed box + V slice (34 KB)
 #ifndef CMSVD_SYMM_TT
@@ -1023,20 +1148,26 @@ __global__ void __launch_bounds__(kSymmTT, 2) k_sbr_symm_tma(const __grid_consta
 //     ([i][16 j], as before): fragment (rows 8a + g, k = j = 4s + t) touches 8 chunks x 2 halves exactly;
 //   * slices below it arrive through a 4-D view of the lower storage (i % 16, j, i / 16, problem) as eight
 //     16 x 16 boxes with the 128-byte swizzle ([i / 16][j][16 i]); with the k index mapped to j = s + 4t
-//     (any bijection of k is allowed as long as the V fragment uses the same one) the four j rows of a
-//     fragment fall into both halves of the swizzle: conflict-free as well;
-//   * the V slice is staged with its own swizzle (16-byte chunk ^ 4 (bit1(j) ^ bit3(j))), which serves
-//     both k mappings;
+//     (any bijection of k is allowed as long as the V fragment uses the same one) ... in both cases the k
+//     index of a step is mapped to the column j so that each HALF-WARP (64-bit shared loads are served per
+//     16 lanes: 4 values of g, all t) covers the 8 chunks x 2 halves of the swizzle once: j = (t & 1) + 2 s +
+//     8 (t >> 1) for the transposed storage, j = (s & 1) + 2 t + 8 (s >> 1) for the lower storage;
+//   * the V slice is staged with its own swizzle (symm_vswz), which serves both k mappings;
 //   * slices crossing the diagonal run both passes with complementary masks.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_dmma(const __grid_constant__ CUtensorMap tlo4,
+// swizzle of the staged V slice: 2-bit value that differs between the four j of a k step under both mappings
+__device__ __forceinline__ int symm_vswz(int jj) { return ((jj & 1) | ((jj >> 2) & 2)) ^ ((jj >> 1) & 3); }
+
+constexpr int kSymmDNS = 3;                                // stages in flight
+constexpr int kSymmDStage = kSymmA + kSymmJT * kSB;        // ONE box (lower or transposed) + the V slice (18 KB)
+__global__ void __launch_bounds__(kSymmThreads, 4) k_sbr_symm_dmma(const __grid_constant__ CUtensorMap tlo4,
                                                                     const __grid_constant__ CUtensorMap tup,
                                                                     const double* __restrict__ G, int64_t ld,
                                                                     int64_t stride, const int* __restrict__ ns,
                                                                     int t, double* __restrict__ ws, const SbrWs L,
                                                                     int par) {
   extern __shared__ __align__(1024) double ysm[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ysm + kSymmNS * kSymmStage);
+  __shared__ uint64_t bars[kSymmDNS];
   const int p = blockIdx.x;
   const int n = ns[p];
   if (t >= sbr_panels(n)) return;
@@ -1051,36 +1182,48 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_dmma(const __grid_
   (void)G; (void)ld; (void)stride;
   if (tid == 0) {
 #pragma unroll
-    for (int q = 0; q < kSymmNS; ++q) mbar_init(&bars[q], 1);
+    for (int q = 0; q < kSymmDNS; ++q) mbar_init(&bars[q], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  auto kind = [&](int J0) {
-    const int jmax = min(kSymmJT, np - J0);
-    return (J0 + jmax - 1 <= I0) ? 0 : ((I0 + imax - 1 < J0) ? 1 : 2);
+  const int nsl = (np + kSymmJT - 1) / kSymmJT;
+  // slices [kc0, kc1) cross the diagonal block: each is two work items (lower box masked to i >= j, then the
+  // transposed box masked to i < j), so that a stage holds one 16 KB box and four CTAs fit per SM
+  const int kc0 = min(nsl, I0 / kSymmJT);                              // first slice with a column > I0
+  const int kc1 = min(nsl, (I0 + imax - 1) / kSymmJT + 1);             // first slice entirely right of the rows
+  const int nc = kc1 - kc0;
+  const int nitems = nsl + nc;
+  // item -> (slice, box: 0 lower, 1 transposed, masked?)
+  auto item_slice = [&](int it, int& box, bool& masked) {
+    if (it < kc0) { box = 0; masked = false; return it; }
+    if (it < kc0 + 2 * nc) { box = (it - kc0) & 1; masked = true; return kc0 + ((it - kc0) >> 1); }
+    box = 1; masked = false;
+    return it - nc;
   };
-  auto issue = [&](int J0, int st) {
-    double* As = ysm + st * kSymmStage;   // lower boxes [i / 16][j][16 i], then the transposed box [i][16 j]
-    double* Vs = As + 2 * kSymmA;
+  auto issue = [&](int it, int st) {
+    int box; bool masked;
+    const int k = item_slice(it, box, masked);
+    const int J0 = k * kSymmJT;
+    double* As = ysm + st * kSymmDStage;   // lower boxes [i / 16][j][16 i] or the transposed box [i][16 j]
+    double* Vs = As + kSymmA;
     const int jmax = min(kSymmJT, np - J0);
-    const int kd = kind(J0);
     if (tid == 0) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[st])),
-                   "r"((unsigned)((kd == 2 ? 2 : 1) * kSymmA * sizeof(double)))
+                   "r"((unsigned)(kSymmA * sizeof(double)))
                    : "memory");
-      if (kd != 1)
+      if (box == 0)
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
             ::"r"(smem_u32(As)), "l"(&tlo4), "r"(0), "r"(R0 + J0), "r"((R0 + I0) >> 4), "r"(p), "r"(smem_u32(&bars[st]))
             : "memory");
-      if (kd != 0) tma_load_3d(As + kSymmA, &tup, R0 + J0, R0 + I0, p, &bars[st]);
+      else
+        tma_load_3d(As, &tup, R0 + J0, R0 + I0, p, &bars[st]);
     }
     for (int e = tid; e < kSymmJT * kSB; e += kSymmThreads) {
       const int jj = e >> 4, c = e & 15;
       const bool ok = jj < jmax;
-      const int sel = ((jj >> 1) ^ (jj >> 3)) & 1;
-      cp_async8(Vs + jj * kSB + ((((c >> 1) ^ (sel << 2)) << 1) | (c & 1)), ok ? Vw + (int64_t)c * L.ldv + J0 + jj : Vw,
-                ok);
+      cp_async8(Vs + jj * kSB + ((((c >> 1) ^ (symm_vswz(jj) << 1)) << 1) | (c & 1)),
+                ok ? Vw + (int64_t)c * L.ldv + J0 + jj : Vw, ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -1089,47 +1232,47 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_dmma(const __grid_
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int bb = 0; bb < 2; ++bb) acc[a][bb][0] = acc[a][bb][1] = 0.0;
-  const int nsl = (np + kSymmJT - 1) / kSymmJT;
   unsigned uses = 0;
-  for (int q = 0; q < kSymmNS - 1 && q < nsl; ++q) issue(q * kSymmJT, q);
-  for (int k = 0; k < nsl; ++k) {
-    const int st = k % kSymmNS;
-    const int J0 = k * kSymmJT;
-    if (k + kSymmNS - 1 < nsl) issue((k + kSymmNS - 1) * kSymmJT, (k + kSymmNS - 1) % kSymmNS);
-    const int pending = min(nsl, k + kSymmNS) - k - 1;
+  for (int q = 0; q < kSymmDNS - 1 && q < nitems; ++q) issue(q, q);
+  for (int it = 0; it < nitems; ++it) {
+    const int st = it % kSymmDNS;
+    if (it + kSymmDNS - 1 < nitems) issue(it + kSymmDNS - 1, (it + kSymmDNS - 1) % kSymmDNS);
+    const int pending = min(nitems, it + kSymmDNS) - it - 1;   // groups committed after this item's
     if (pending >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
     else if (pending == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
     else asm volatile("cp.async.wait_group 0;" ::: "memory");
-    const int kd = kind(J0);
+    int box; bool masked;
+    const int k = item_slice(it, box, masked);
+    const int J0 = k * kSymmJT;
     mbar_wait(&bars[st], (uses >> st) & 1u);
     uses ^= 1u << st;
     __syncthreads();
-    const double* Al = ysm + st * kSymmStage;
-    const double* Au = Al + kSymmA;
-    const double* Vs = Al + 2 * kSymmA;
+    const double* Ab = ysm + st * kSymmDStage;
+    const double* Vs = Ab + kSymmA;
     const int jmax = min(kSymmJT, np - J0);
     const bool full = jmax == kSymmJT && imax == kSymmRows;
-    // one pass over the slice with the k mapping of its storage: LOWER (j = s + 4t) or transposed (j = 4s + t)
-    auto pass = [&](bool lower, bool masked) {
+    // one pass over the box; the k index t of a step is mapped to the column j of the slice so that every
+    // half-warp covers the 8 chunks x 2 halves of the swizzle once (see the kernel comment)
+    auto pass = [&](bool lower, bool msk) {
 #pragma unroll
       for (int s4 = 0; s4 < 4; ++s4) {
-        const int jj = lower ? s4 + 4 * ft : 4 * s4 + ft;
-        const int sel = ((jj >> 1) ^ (jj >> 3)) & 1;
+        const int jj = lower ? (s4 & 1) + 2 * ft + 8 * (s4 >> 1) : (ft & 1) + 2 * s4 + 8 * (ft >> 1);
+        const int vs = symm_vswz(jj) << 1;
         double vb[2];
 #pragma unroll
         for (int bb = 0; bb < 2; ++bb)
-          vb[bb] = Vs[jj * kSB + (((((8 * bb + fg) >> 1) ^ (sel << 2)) << 1) | (fg & 1))];
+          vb[bb] = Vs[jj * kSB + (((((8 * bb + fg) >> 1) ^ vs) << 1) | (fg & 1))];
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           const int i = 32 * wid + 8 * a + fg;
           double av;
           if (lower) {
             const int ib = i & 15;
-            av = Al[(i >> 4) * 256 + jj * 16 + ((((ib >> 1) ^ (jj & 7)) << 1) | (ib & 1))];
+            av = Ab[(i >> 4) * 256 + jj * 16 + ((((ib >> 1) ^ (jj & 7)) << 1) | (ib & 1))];
           } else {
-            av = Au[i * 16 + ((((jj >> 1) ^ (i & 7)) << 1) | (jj & 1))];
+            av = Ab[i * 16 + ((((jj >> 1) ^ (i & 7)) << 1) | (jj & 1))];
           }
-          if (masked) {
+          if (msk) {
             const bool low = I0 + i >= J0 + jj;
             if (low != lower || jj >= jmax || i >= imax) av = 0.0;
           } else if (!full) {
@@ -1140,10 +1283,12 @@ __global__ void __launch_bounds__(kSymmThreads, 3) k_sbr_symm_dmma(const __grid_
         }
       }
     };
-    if (kd == 0) pass(true, false);
-    else if (kd == 1) pass(false, false);
-    else { pass(true, true); pass(false, true); }
-    __syncthreads();   // this stage is reissued kSymmNS - 1 steps later
+    if (box == 0) {
+      if (masked) pass(true, true); else pass(true, false);
+    } else {
+      if (masked) pass(false, true); else pass(false, false);
+    }
+    __syncthreads();   // this stage is reissued kSymmDNS - 1 items later
   }
   // epilogue: X rows to shared memory (row stride 17); Y = X T by row (thread = row, X row in registers);
   // M_b = V_b^T Y_b = (V_b^T X_b) T with Q = V_b^T X_b as 8 row-group partials (16 independent
@@ -1831,6 +1976,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
                    sbr_tensor_map(&tup, G, ld, stride, nprob, 16, kSymmRows, CU_TENSOR_MAP_SWIZZLE_128B);
   CUtensorMap tlo4;
   const bool dmma = tma && c.symm_dmma && sbr_tensor_map_lo4(&tlo4, G, ld, stride, nprob);
+  const size_t ydmem = std::max((size_t)kSymmDNS * kSymmDStage,
+                                (size_t)kSymmRows * (kSB + 1) + kSB * kSB + 2 * kSymmRows * kSB + 4) * sizeof(double);
   const size_t ymem = std::max((size_t)kSymmNS * kSymmStage + 4,
                                (size_t)kSymmRows * (kSB + 1) + kSB * kSB + 2 * kSymmRows * kSB + 4) * sizeof(double);
   // V and W of both parity sets as 3-D maps (64 x 16 boxes; V of the next panel also as 66 x 16 boxes)
@@ -1847,6 +1994,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   if (sdm) {
     cudaError_t e3 = cudaFuncSetAttribute(k_sbr_syr2k_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrDSmem);
     if (e3 != cudaSuccess) return e3;
+    e3 = cudaFuncSetAttribute(k_sbr_syr2k_rowd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrRowSmem);
+    if (e3 != cudaSuccess) return e3;
   }
   const bool fused = tma2 && c.sbr_fused &&
                      sbr_tensor_map(&tm66, G, ld, stride, nprob, kFP, kSyrTile, CU_TENSOR_MAP_SWIZZLE_NONE);
@@ -1860,7 +2009,7 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     if (e2 != cudaSuccess) return e2;
     e2 = cudaFuncSetAttribute(k_sbr_symm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ymem);
     if (e2 != cudaSuccess) return e2;
-    e2 = cudaFuncSetAttribute(k_sbr_symm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ymem);
+    e2 = cudaFuncSetAttribute(k_sbr_symm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ydmem);
     if (e2 != cudaSuccess) return e2;
     e2 = cudaFuncSetAttribute(k_sbr_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
     if (e2 != cudaSuccess) return e2;
@@ -1886,8 +2035,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     const int nrb = (np0 + kSymmRows - 1) / kSymmRows;
     int pr = prof_begin(c, PC_SBR_SYMM);
     if (dmma)
-      k_sbr_symm_dmma<<<dim3(nprob, nrb), kSymmThreads, ymem, c.stream>>>(tlo4, tup, G, ld, stride, d_ns, t, ws, L,
-                                                                          t & 1);
+      k_sbr_symm_dmma<<<dim3(nprob, nrb), kSymmThreads, ydmem, c.stream>>>(tlo4, tup, G, ld, stride, d_ns, t, ws, L,
+                                                                           t & 1);
     else if (tma)
       k_sbr_symm_tma<<<dim3(nprob, nrb), kSymmTT, ymem, c.stream>>>(tlo, tup, G, ld, stride, d_ns, t, ws, L,
                                                                          t & 1);
@@ -1932,7 +2081,10 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
       }
     } else {
       const int pr = prof_begin(c, PC_SBR_SYR2K);
-      if (sdm)
+      if (sdm && c.syr2k_row)
+        k_sbr_syr2k_rowd<<<dim3(nprob, nt), kSyrRowThreads, kSyrRowSmem, c.stream>>>(tm4, tv4[t & 1], tw4[t & 1],
+                                                                                            d_ns, t);
+      else if (sdm)
         k_sbr_syr2k_dmma<<<dim3(nprob, nt * (nt + 1) / 2), kSyrThreads, kSyrDSmem, c.stream>>>(tm4, tv4[t & 1],
                                                                                                tw4[t & 1], d_ns, t);
       else if (tma2 && c.syr2k_row)
