@@ -29,26 +29,42 @@ namespace cmsvd {
 // computed and mirrored (bitwise what the skipped tiles would compute: the same products in the same
 // order); 2 B is upper triangular (B(k, j) = 0 for k > j): the K loop of a tile stops at its last column.
 // ---------------------------------------------------------------------------
+// D = A B + D for one 8 x 8 x 4 fp64 tile (DMMA): a = A[g][t], b = B[t][g], (c0, c1) = C[g][2t .. 2t+1],
+// g = lane / 4, t = lane % 4
+__device__ __forceinline__ void big_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// The products run on the fp64 tensor cores: a warp owns 32 x 16 of the 64 x 64 tile as 4 x 2 accumulator
+// fragments (6 fragment loads per 8 DMMAs = 2048 FMAs; the scalar form needed 8 loads per 16 DFMAs and was
+// bound by shared-memory wavefronts).  The staged operands are [k][i ^ swz(k)], swz(k) = 4 (k & 3) ^ (k >> 2):
+// the four k rows of a fragment land in four different 32-byte slots (the 16 lanes of a half-warp cover all
+// banks once), and the 16 k of a staging store (k fastest) in 16 different 8-byte slots.
 template <typename TAe, bool TA>
 __global__ void __launch_bounds__(256) k_gemm_mixed(int M, int N, int K, const TAe* __restrict__ A,
                                                     const TAe* const* __restrict__ Ap, int64_t lda, int64_t sA,
                                                     const double* __restrict__ B, int64_t ldb, int64_t sB,
                                                     double* __restrict__ C, int64_t ldc, int64_t sC, double alpha,
                                                     int shape) {
-  constexpr int BM = 64, BN = 64, BK = 16;
+  constexpr int BM = 64, BN = 64, BK = 16, PITCH = 64;
+  auto swz = [](int k) { return (4 * (k & 3)) ^ (k >> 2); };
   if (shape == 1 && blockIdx.x < blockIdx.y) return;
-  __shared__ double As[BK][BM + 1];
-  __shared__ double Bs[BK][BN + 1];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  __shared__ double As[BK][PITCH];
+  __shared__ double Bs[BK][PITCH];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int fg = lane >> 2, ft = lane & 3;
+  const int wr = wid & 1, wc = wid >> 1;   // warp tile: rows 32 wr .. + 31, columns 16 wc .. + 15
   const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
   const TAe* Ab = Ap ? Ap[blockIdx.z] : A + (int64_t)blockIdx.z * sA;
   const double* Bb = B + (int64_t)blockIdx.z * sB;
   double* Cb = C + (int64_t)blockIdx.z * sC;
-  double acc[4][4];
+  double acc[4][2][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int Kt = shape == 2 ? min(K, j0 + BN) : K;
   for (int k0 = 0; k0 < Kt; k0 += BK) {
 #pragma unroll
@@ -58,42 +74,46 @@ __global__ void __launch_bounds__(256) k_gemm_mixed(int M, int N, int K, const T
       if (TA) {  // element (i, k) at A[i*lda + k]: coalesce along k
         const int k = e & 15, i = e >> 4;
         if (i0 + i < M && k0 + k < K) va = (double)Ab[(int64_t)(i0 + i) * lda + k0 + k];
-        As[k][i] = va;
+        As[k][i ^ swz(k)] = va;
       } else {   // element (i, k) at A[k*lda + i]: coalesce along i
         const int i = e & 63, k = e >> 6;
         if (i0 + i < M && k0 + k < K) va = (double)Ab[(int64_t)(k0 + k) * lda + i0 + i];
-        As[k][i] = va;
+        As[k][i ^ swz(k)] = va;
       }
       const int kb = e & 15, j = e >> 4;  // B element (k, j) at B[j*ldb + k]: coalesce along k
       double vb = 0.0;
       if (j0 + j < N && k0 + kb < K) vb = Bb[(int64_t)(j0 + j) * ldb + k0 + kb];
-      Bs[kb][j] = vb;
+      Bs[kb][j ^ swz(kb)] = vb;
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < BK; ++k) {
-      double av[4], bv[4];
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      double bv[2];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = As[k][tx + 16 * a];
+      const int kk = 4 * ks + ft, sw = swz(kk);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = Bs[k][ty + 16 * b];
+      for (int b = 0; b < 2; ++b) bv[b] = Bs[kk][(16 * wc + 8 * b + fg) ^ sw];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 4; ++a) {
+        const double av = As[kk][(32 * wr + 8 * a + fg) ^ sw];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        for (int b = 0; b < 2; ++b) big_dmma(acc[a][b][0], acc[a][b][1], av, bv[b]);
+      }
     }
     __syncthreads();
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = i0 + tx + 16 * a, j = j0 + ty + 16 * b;
-      if (i < M && j < N) {
-        Cb[(int64_t)j * ldc + i] = alpha * acc[a][b];
-        if (shape == 1 && blockIdx.x != blockIdx.y) Cb[(int64_t)i * ldc + j] = alpha * acc[a][b];
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = i0 + 32 * wr + 8 * a + fg, j = j0 + 16 * wc + 8 * b + 2 * ft + e;
+        if (i < M && j < N) {
+          Cb[(int64_t)j * ldc + i] = alpha * acc[a][b][e];
+          if (shape == 1 && blockIdx.x != blockIdx.y) Cb[(int64_t)i * ldc + j] = alpha * acc[a][b][e];
+        }
       }
-    }
 }
 
 template <typename TAe, bool TA>
