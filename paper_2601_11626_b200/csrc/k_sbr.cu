@@ -1747,6 +1747,285 @@ __device__ __forceinline__ void chase_task(double* __restrict__ Bd, double* __re
   else chase_task_t<false>(Bd, ps, j, s, L, L2);
 }
 
+// ---------------------------------------------------------------------------
+// Stage 2, two problems in flight per CTA (CMSVD_CHASE2=1; an experiment kept for its negative result: the same
+// 26 eigensolver tests pass, but a config-4 pass takes 25.6 ms against 22.8 ms for one CTA per problem -- both
+// variants sustain ~4.7 tasks per microsecond and SM, so the chase is bound by task throughput, not by the
+// per-step latency this design hides).  A bulge chase is one latency chain per
+// time step (3 (n - 3) steps of ~1 us with at most n / 48 + 1 concurrent tasks): one problem per SM leaves
+// the SM ~70% idle, and a second resident CTA does not fit (139 KB of band per problem, 52 K registers).
+// But sweep j only touches columns >= j: once a problem has passed its middle, the first half of its band
+// is dead.  A persistent CTA therefore keeps a circular band buffer of 1.5 x 512 columns and starts the
+// next problem of its queue as soon as the previous one has freed enough columns (its finished diagonal /
+// sub-diagonal entries are written out first): two problems, half a chase apart, share every time step and
+// its barrier, and a problem completes every ~1.5 n steps instead of every 3 n.  Column c of a problem with
+// offset `off` lives at physical column (off + c) mod kCh2Cap; a task whose 32 columns do not straddle the
+// wrap point runs the plain pointer arithmetic on a shifted base, the rare straddling task goes element by
+// element.
+// ---------------------------------------------------------------------------
+constexpr int kCh2Warps = 16;
+constexpr int kCh2Cap = kSBMax + kSBMax / 2;
+
+constexpr int kCh2WrapSz = kCh2Cap * kSBLdb;
+template <bool WRAP>
+struct ChAcc {
+  double* base;   // Bd + off * kSBLdb: element (i, c) at base[c * kSBRow + i], minus kCh2WrapSz from column cw on
+  int cw;         // first logical column stored before the start of the buffer (WRAP only)
+  __device__ __forceinline__ double& at(int i, int c) const {
+    return base[c * kSBRow + i - ((WRAP && c >= cw) ? kCh2WrapSz : 0)];
+  }
+};
+
+template <bool FULL, bool WRAP>
+__device__ __forceinline__ void chase2_task_t(const ChAcc<WRAP> A, double* __restrict__ ps, int j, int s, int L,
+                                              int L2) {
+  const int lane = threadIdx.x & 31;
+  const int r = j + 1 + s * kSB;
+  const int cx = (s == 0) ? j : r - kSB;    // column holding x (rows r .. r + L - 1)
+  const int l16 = lane & 15, hh = lane >> 4;
+  const int r2 = r + L;
+  double xl[8], b[8], dd[8], cr[8];
+  const double alpha = A.at(r, cx);
+  const double xa = (l16 < L) ? A.at(r + l16, cx) : 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int l = 8 * hh + q;
+    if (FULL) {
+      xl[q] = A.at(r + l, cx);
+      b[q] = s > 0 ? A.at(r + l, cx + l16) : 0.0;
+      dd[q] = (l16 >= l) ? A.at(r + l16, r + l) : A.at(r + l, r + l16);
+      cr[q] = A.at(r2 + l16, r + l);
+    } else {
+      xl[q] = (l < L) ? A.at(r + l, cx) : 0.0;
+      b[q] = (s > 0 && l < L) ? A.at(r + l, cx + l16) : 0.0;
+      dd[q] = (l16 < L && l < L) ? ((l16 >= l) ? A.at(r + l16, r + l) : A.at(r + l, r + l16)) : 0.0;
+      cr[q] = (l16 < L2 && l < L) ? A.at(r2 + l16, r + l) : 0.0;
+    }
+  }
+  double sq = 0.0, tb = 0.0, tp = 0.0, tq = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double xq = (hh == 0 && q == 0) ? 0.0 : xl[q];
+    sq = fma(xq, xq, sq);
+    tb = fma(xq, b[q], tb);
+    tp = fma(xq, dd[q], tp);
+    tq = fma(xq, cr[q], tq);
+  }
+  double b0 = hh == 0 ? b[0] : 0.0, d0 = hh == 0 ? dd[0] : 0.0, c0 = hh == 0 ? cr[0] : 0.0;
+  sq += __shfl_xor_sync(0xffffffffu, sq, 16);
+  tb += __shfl_xor_sync(0xffffffffu, tb, 16);
+  tp += __shfl_xor_sync(0xffffffffu, tp, 16);
+  tq += __shfl_xor_sync(0xffffffffu, tq, 16);
+  b0 += __shfl_xor_sync(0xffffffffu, b0, 16);
+  d0 += __shfl_xor_sync(0xffffffffu, d0, 16);
+  c0 += __shfl_xor_sync(0xffffffffu, c0, 16);
+  if (!(sq > 0.0)) return;   // x is already alpha e_0: H = I (warp-uniform)
+  const double x2 = fma(alpha, alpha, sq);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x2));
+  const double e = fma(-(x2 * y), y, 1.0);
+  y = fma(y * e, fma(e, 0.375, 0.5), y);
+  const double xn = x2 * y;
+  const double beta = alpha >= 0.0 ? -xn : xn;
+  const double tau = (beta - alpha) * sbr_rcp(beta);
+  const double scale = sbr_rcp(alpha - beta);
+  const double db = tau * fma(scale, tb, b0);
+  const double pa = tau * fma(scale, tp, d0);
+  const double qd = tau * fma(scale, tq, c0);
+  double vh[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) vh[q] = (hh == 0 && q == 0) ? 1.0 : xl[q] * scale;
+  const double va = (l16 == 0) ? 1.0 : xa * scale;
+  if (lane < 16) ps[lane] = (l16 < L) ? pa : 0.0;
+  double pv = (l16 < L) ? pa * va : 0.0;
+  pv += __shfl_xor_sync(0xffffffffu, pv, 1);
+  pv += __shfl_xor_sync(0xffffffffu, pv, 2);
+  pv += __shfl_xor_sync(0xffffffffu, pv, 4);
+  pv += __shfl_xor_sync(0xffffffffu, pv, 8);
+  __syncwarp();
+  double ph[8];
+  {
+    const double2* p2 = reinterpret_cast<const double2*>(ps + 8 * hh);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { const double2 t = p2[q]; ph[2 * q] = t.x; ph[2 * q + 1] = t.y; }
+  }
+  const double K = 0.5 * tau * pv;
+  const double wa = fma(-K, va, pa);
+  if (s == 0) {
+    if (lane < L) A.at(r + lane, j) = (lane == 0) ? beta : 0.0;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int l = 8 * hh + q;
+      if (FULL || l < L) A.at(r + l, cx + l16) = (l16 == 0) ? (l == 0 ? beta : 0.0) : fma(-db, vh[q], b[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int l = 8 * hh + q;
+    const double wl = fma(-K, vh[q], ph[q]);
+    if ((FULL || l16 < L) && l <= l16) A.at(r + l16, r + l) = fma(-va, wl, fma(-wa, vh[q], dd[q]));
+    if (FULL || (l16 < L2 && l < L)) A.at(r2 + l16, r + l) = fma(-qd, vh[q], cr[q]);
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void chase2_task(double* __restrict__ Bd, double* __restrict__ ps, int n, int off, int j,
+                                            int s) {
+  const int r = j + 1 + s * kSB;
+  const int L = min(kSB, n - r);
+  const int L2 = min(kSB, n - r - L);
+  const bool full = L == kSB && L2 == kSB;
+  // columns touched: cx .. r + 15 with cx = j (s = 0) or r - 16
+  const int cmin = off + ((s == 0) ? j : r - kSB), cmax = off + min(n - 1, r + kSB - 1);
+  if (cmax < kCh2Cap || cmin >= kCh2Cap) {
+    const ChAcc<false> A{Bd + (cmax < kCh2Cap ? off : off - kCh2Cap) * kSBLdb, 0};
+    if (full) chase2_task_t<true, false>(A, ps, j, s, L, L2);
+    else chase2_task_t<false, false>(A, ps, j, s, L, L2);
+  } else {   // the task's columns straddle the end of the circular buffer
+    const ChAcc<true> A{Bd + off * kSBLdb, kCh2Cap - off};
+    if (full) chase2_task_t<true, true>(A, ps, j, s, L, L2);
+    else chase2_task_t<false, true>(A, ps, j, s, L, L2);
+  }
+}
+
+// d, e^2 are complete: Gershgorin data and the count above the threshold (as at the end of k_sbr_chase)
+__global__ void __launch_bounds__(128) k_sbr_chase_fin(const int* __restrict__ ns, const double* __restrict__ thr,
+                                                       int kw, int nstride, const double* __restrict__ dout,
+                                                       const double* __restrict__ e2out, double* __restrict__ gsh,
+                                                       int* __restrict__ cnt_out, int nprob) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nprob) return;
+  const int n = ns[p];
+  if (n <= 0) { cnt_out[p] = 0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; return; }
+  const double* dO = dout + (int64_t)p * nstride;
+  const double* eO = e2out + (int64_t)p * nstride;
+  double glo = 1e300, ghi = -1e300, emax = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double rr = 0.0;
+    if (i > 0) rr += sqrt(eO[i - 1]);
+    if (i + 1 < n) rr += sqrt(eO[i]);
+    const double di = dO[i];
+    glo = fmin(glo, di - rr);
+    ghi = fmax(ghi, di + rr);
+    if (i + 1 < n) emax = fmax(emax, eO[i]);
+  }
+  const double nrm = fmax(fmax(fabs(glo), fabs(ghi)), 1e-300);
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax) * 4.0;
+  glo -= 2.2e-16 * nrm * n + pivmin;
+  ghi += 2.2e-16 * nrm * n + pivmin;
+  gsh[4 * p] = glo; gsh[4 * p + 1] = ghi; gsh[4 * p + 2] = pivmin; gsh[4 * p + 3] = nrm;
+  int above = n;
+  if (thr) {
+    const double tt = thr[p];
+    if (tt >= ghi) above = 0;
+    else if (tt > glo) {
+      int c0 = 0;
+      double qd = dO[0] - tt;
+      if (fabs(qd) < pivmin) qd = -pivmin;
+      c0 += qd < 0.0;
+      for (int i = 1; i < n; ++i) {
+        qd = (dO[i] - tt) - eO[i - 1] / qd;
+        if (fabs(qd) < pivmin) qd = -pivmin;
+        c0 += qd < 0.0;
+      }
+      above = n - c0;
+    }
+  }
+  cnt_out[p] = min(kw, above);
+}
+
+// The scheduling state (two slots: problem, n, offset, start step, columns written out) is a function of
+// uniform data only, so every thread carries it in registers: no shared-memory state, no elected thread.
+__global__ void __launch_bounds__(kCh2Warps * 32, 1) k_sbr_chase2(const double* __restrict__ G, int64_t ld,
+                                                                  int64_t stride, const int* __restrict__ ns,
+                                                                  int nstride, double* __restrict__ dout,
+                                                                  double* __restrict__ e2out, int nprob) {
+  extern __shared__ __align__(16) double bsm2[];
+  double* Bd = bsm2;                                             // [kCh2Cap][kSBLdb]
+  double* vsc = bsm2 + (int64_t)kCh2Cap * kSBLdb + 32 * (threadIdx.x >> 5);   // per-warp p scratch
+  const int tid = threadIdx.x, wid = tid >> 5;
+  int act[2] = {0, 0}, sp[2] = {0, 0}, sn[2] = {0, 0}, so[2] = {0, 0}, st0[2] = {0, 0}, sx[2] = {0, 0};
+  int next = blockIdx.x;
+  int nnext = next < nprob ? ns[next] : 0;   // size of the next problem (loaded once, not once per time step)
+  auto cell = [&](int off, int c, int d) -> double& {
+    int pc = off + c;
+    if (pc >= kCh2Cap) pc -= kCh2Cap;
+    return Bd[pc * kSBLdb + d];
+  };
+  // write out the final diagonal / squared sub-diagonal entries of columns [from, upto) of slot q
+  auto extract = [&](int q, int from, int upto) {
+    double* dO = dout + (int64_t)sp[q] * nstride;
+    double* eO = e2out + (int64_t)sp[q] * nstride;
+    for (int i = from + tid; i < upto; i += blockDim.x) {
+      dO[i] = cell(so[q], i, 0);
+      if (i + 1 < sn[q]) { const double e1 = cell(so[q], i, 1); eO[i] = e1 * e1; }
+    }
+  };
+  int tau_step = 0;
+  for (;;) {
+    // ---- retire finished problems (all sweeps done) ----
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (act[q] && tau_step - st0[q] > 3 * (sn[q] - 3)) {
+        extract(q, sx[q], sn[q]);
+        act[q] = 0;
+      }
+    // ---- start the next problem of this CTA's queue when a slot and enough dead columns are available ----
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      while (!act[q] && next < nprob) {
+        const int o = 1 - q;
+        const int p = next;
+        const int n = nnext;
+        if (n <= 0) { next += gridDim.x; nnext = next < nprob ? ns[next] : 0; continue; }
+        int off = 0;
+        if (act[o]) {
+          const int To = tau_step - st0[o];
+          const int fin = min(sn[o], max(0, (To - 1) / 3));   // its final columns (sweep j: step 0 at time 3 j)
+          const int need = sn[o] + n - kCh2Cap;               // its leading columns this problem overwrites
+          if (need > fin) break;
+          if (need > sx[o]) { extract(o, sx[o], need); sx[o] = need; }
+          off = so[o] + sn[o];
+          if (off >= kCh2Cap) off -= kCh2Cap;
+        }
+        __syncthreads();   // the extract above (and the last time step) precede the overwrite
+        const double* A = G + (int64_t)p * stride;
+        for (int e = tid; e < n * kSBLdb; e += blockDim.x) {
+          const int jj = e / kSBLdb, d = e - jj * kSBLdb;
+          cell(off, jj, d) = (d <= kSB && jj + d < n) ? A[(int64_t)jj * ld + jj + d] : 0.0;
+        }
+        __syncthreads();
+        act[q] = 1; sp[q] = p; sn[q] = n; so[q] = off; st0[q] = tau_step; sx[q] = 0;
+        next += gridDim.x;
+        nnext = next < nprob ? ns[next] : 0;
+      }
+    }
+    if (!act[0] && !act[1]) break;
+    // ---- one time step of every active problem: task (j, s = T - 3 j), both problems' tasks over the warps ----
+    int cntq[2], jhiq[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      cntq[q] = 0; jhiq[q] = 0;
+      const int n = sn[q], T = tau_step - st0[q];
+      if (act[q] && n >= 3 && T <= 3 * (n - 3)) {
+        const int jhi = min(T / 3, n - 3);
+        const int num = 16 * T - n + 3;
+        const int jlo = num > 0 ? (num + 46) / 47 : 0;
+        jhiq[q] = jhi;
+        cntq[q] = max(0, jhi - jlo + 1);
+      }
+    }
+    for (int idx = wid; idx < cntq[0] + cntq[1]; idx += kCh2Warps) {
+      const int q = idx < cntq[0] ? 0 : 1;
+      const int j = jhiq[q] - (q == 0 ? idx : idx - cntq[0]);
+      chase2_task(Bd, vsc, sn[q], so[q], j, tau_step - st0[q] - 3 * j);
+    }
+    __syncthreads();
+    ++tau_step;
+  }
+}
+
 // FLAGS: per-sweep progress flags (each warp owns whole sweeps and polls its predecessor's counter)
 // instead of one CTA barrier per wavefront time step
 // GB: n > kSBMax, the band lives in the problem's global workspace (L.band) instead of shared memory
@@ -2118,7 +2397,15 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   } while (0)
   if (big) SBR_CHASE(false, true);
   else if (c.chase_flags) SBR_CHASE(true, false);
-  else SBR_CHASE(false, false);
+  else if (c.chase2) {
+    const size_t c2smem = ((size_t)kCh2Cap * kSBLdb + 32 * kCh2Warps) * sizeof(double);
+    e = cudaFuncSetAttribute(k_sbr_chase2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2smem);
+    if (e != cudaSuccess) return e;
+    k_sbr_chase2<<<std::min(nprob, c.sm_count), kCh2Warps * 32, c2smem, c.stream>>>(G, ld, stride, d_ns, nstride, dd,
+                                                                                   ee, nprob);
+    k_sbr_chase_fin<<<(nprob + 127) / 128, 128, 0, c.stream>>>(d_ns, d_thr, kw, nstride, dd, ee, gsh, cnt, nprob);
+    c.launches += 1;
+  } else SBR_CHASE(false, false);
 #undef SBR_CHASE
   c.launches += 1;
   prof_end(c, pr);
