@@ -78,15 +78,46 @@ def test_structured_spectra(cm):
     assert np.allclose(ev[0, :50], 9.0, atol=1e-12 * 9) and np.allclose(ev[0, 50:100], 4.0, atol=1e-12 * 9)
 
 
-@pytest.mark.parametrize("fused", ["0", "1"])
-def test_band_reduction_variants(cm, fused, monkeypatch):
-    """The look-ahead fused pass (CMSVD_SBR_FUSED=1: strip update + panel QR first, then one pass with the
-    rank-32 update and the next product on fp64 tensor cores) and the default two-pass stage 1 agree with
-    LAPACK on ragged sizes, including the global-memory panel / band above 512."""
-    monkeypatch.setenv("CMSVD_SBR_FUSED", fused)
+@pytest.mark.parametrize("knob", ["", "CMSVD_SBR_FUSED=1", "CMSVD_SYMM_DMMA=0", "CMSVD_SYR2K_DMMA=0", "CMSVD_SYR2K_ROW=0",
+                                  "CMSVD_SYMM_DMMA=0,CMSVD_SYR2K_DMMA=0,CMSVD_SYR2K_ROW=1", "CMSVD_CHASE2=1",
+                                  "CMSVD_CHASE_FLAGS=1", "CMSVD_SBR_TMA=0"])
+def test_band_reduction_variants(cm, knob, monkeypatch):
+    """Every selectable path of the two-stage reduction agrees with LAPACK on ragged sizes (including the
+    global-memory panel / band above 512): the default (stage 1 on the fp64 tensor cores: DMMA product and
+    row-persistent DMMA update), the scalar product / update kernels, the one-tile-per-CTA and row-persistent
+    scalar updates, the look-ahead fused pass, the chase with per-sweep flags or with two problems in flight
+    per CTA over the circular band buffer, and the non-TMA staging."""
+    for kv in filter(None, knob.split(",")):
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
     R = np.random.default_rng(31)
     sizes = [512, 400, 161, 257, 640]
     mats = [gram(R, n, decay=0.4) for n in sizes]
     with cm.Context(0) as ctx:
         ev, _ = ctx.sym_eigvals(mats, 160)
     check(ev, mats, 160)
+
+
+def test_chase_two_in_flight_queue(cm, monkeypatch):
+    """CMSVD_CHASE2=1 with more problems than SMs: every persistent CTA walks a queue of ragged problems
+    through the circular band buffer (offsets 0, n_A, n_A + n_B mod 768, ...: column wrap inside a problem,
+    early write-out of the finished columns before they are overwritten, empty and tiny problems in the
+    queue).  Same bar as the default path."""
+    monkeypatch.setenv("CMSVD_CHASE2", "1")
+    R = np.random.default_rng(41)
+    base = [512, 161, 400, 0, 512, 257, 200, 3, 333, 512, 170, 2, 480, 1]
+    sizes = (base * 32)[:420]
+    protos = {n: (gram(R, n, decay=0.3) if n else np.zeros((0, 0))) for n in set(sizes)}
+    # distinct matrices per problem (scaled copies keep the LAPACK reference cheap)
+    scale = 1.0 + 0.01 * np.arange(len(sizes))
+    mats = [protos[n] * scale[i] for i, n in enumerate(sizes)]
+    with cm.Context(0) as ctx:
+        ev, _ = ctx.sym_eigvals(mats, 64)
+    refs = {n: (np.linalg.eigvalsh(protos[n])[::-1][:64] if n else np.zeros(0)) for n in protos}
+    for i, n in enumerate(sizes):
+        k = min(64, n)
+        if k == 0:
+            continue
+        ref = refs[n][:k] * scale[i]
+        tol = 2e-11 * np.abs(ref) + 1e-12 * abs(ref[0]) * max(1.0, n / 64)
+        assert np.all(np.abs(ev[i, :k] - ref) <= tol), (i, n, np.abs(ev[i, :k] - ref).max())
