@@ -93,6 +93,7 @@ cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
   if (const char* env = getenv("CMSVD_SYR2K_DMMA")) h->c.syr2k_dmma = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_SYR2K_ROW")) h->c.syr2k_row = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_CHASE2")) h->c.chase2 = (env[0] == '1');
+  if (const char* env = getenv("CMSVD_CHASE_SMALL")) h->c.chase_small = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_CHASE_FLAGS")) h->c.chase_flags = (env[0] == '1');
   if (const char* env = getenv("CMSVD_EIG_SBR")) h->c.eig_sbr = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_RR")) h->c.eig_rr = !(env[0] == '0');

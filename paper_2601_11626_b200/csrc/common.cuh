@@ -141,6 +141,7 @@ struct Ctx {
                                        // per CTA); with the DMMA update 15.3 vs 16.8 ms, with the scalar update equal (17.2 vs 17.3)
   bool chase2 = false;                 // band chase: two problems in flight per persistent CTA (CMSVD_CHASE2=1).  Measured 25.6 vs
                                        // 22.8 ms: the chase is bound by task throughput (~4.7 tasks/us/SM in both), not by latency
+  bool chase_small = true;             // band chase, n <= 256: 6-warp CTAs with half the band, two per SM (CMSVD_CHASE_SMALL=0: off)
   bool chase_flags = false;            // band chase: per-sweep progress flags instead of time-step barriers
   bool eig_sbr = true;                 // n > 160: two-stage (band) reduction instead of the one-stage in-place kernel
   bool eig_rr = true;                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)

@@ -2029,8 +2029,10 @@ __global__ void __launch_bounds__(kCh2Warps * 32, 1) k_sbr_chase2(const double* 
 // FLAGS: per-sweep progress flags (each warp owns whole sweeps and polls its predecessor's counter)
 // instead of one CTA barrier per wavefront time step
 // GB: n > kSBMax, the band lives in the problem's global workspace (L.band) instead of shared memory
-template <bool FLAGS, bool GB>
-__global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double* __restrict__ G, int64_t ld,
+// W: warps per CTA (12; 6 for n <= 256, where a time step has at most 6 tasks and the band takes half the
+// shared memory: two CTAs per SM)
+template <bool FLAGS, bool GB, int W = kChaseWarps>
+__global__ void __launch_bounds__(W * 32, W == kChaseWarps ? 1 : 2) k_sbr_chase(const double* __restrict__ G, int64_t ld,
                                                                     int64_t stride, const int* __restrict__ ns,
                                                                     const double* __restrict__ thr, int kw,
                                                                     int nstride, double* __restrict__ dout,
@@ -2039,9 +2041,9 @@ __global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double*
                                                                     int* __restrict__ cnt_out,
                                                                     double* __restrict__ ws, const SbrWs L, int nmax) {
   extern __shared__ __align__(16) double bsm[];
-  const int nb = GB ? nmax : kSBMax;
+  const int nb = GB ? nmax : (W == kChaseWarps ? kSBMax : kSBMax / 2);
   double* Bd = GB ? ws + (int64_t)blockIdx.x * L.per + L.band : bsm;               // [n][kSBLdb]
-  double* sbase = GB ? bsm : bsm + (int64_t)kSBMax * kSBLdb;
+  double* sbase = GB ? bsm : bsm + (int64_t)nb * kSBLdb;
   volatile int* prog = reinterpret_cast<volatile int*>(sbase);                     // steps done per sweep
   double* vsc = sbase + nb / 2 + 2 + 32 * (threadIdx.x >> 5);                      // per-warp p scratch
   const int p = blockIdx.x;
@@ -2062,7 +2064,7 @@ __global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double*
   __syncthreads();
   if (FLAGS) {
   // sweeps j = wid, wid + W, ...; step s of sweep j waits until sweep j - 1 has completed step s + 2
-  for (int j = wid; j + 2 < n; j += kChaseWarps) {
+  for (int j = wid; j + 2 < n; j += W) {
     const int nsteps = (n - 3 - j) / kSB + 1;   // steps with a window of >= 2 rows
     for (int s = 0; s < nsteps; ++s) {
       if (j > 0) {
@@ -2092,7 +2094,7 @@ __global__ void __launch_bounds__(kChaseWarps * 32, 1) k_sbr_chase(const double*
 #endif
   for (int tt = 0; tt <= tmax; ++tt) {
     const int jhi = min(tt / 3, n - 3);
-    for (int idx = wid;; idx += kChaseWarps) {
+    for (int idx = wid;; idx += W) {
       const int j = jhi - idx;
       const int s = tt - 3 * j;
       if (j < 0 || s >= (n - 3 - j) / kSB + 1) break;
@@ -2397,7 +2399,14 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   } while (0)
   if (big) SBR_CHASE(false, true);
   else if (c.chase_flags) SBR_CHASE(true, false);
-  else if (c.chase2) {
+  else if (!c.chase2 && nmax <= kSBMax / 2 && c.chase_small) {
+    // n <= 256: six warps and half the band per CTA, two CTAs per SM
+    const size_t hsmem = ((size_t)(kSBMax / 2) * kSBLdb + (size_t)kSBMax / 4 + 2 + 32 * 6) * sizeof(double);
+    e = cudaFuncSetAttribute(k_sbr_chase<false, false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+    if (e != cudaSuccess) return e;
+    k_sbr_chase<false, false, 6><<<nprob, 6 * 32, hsmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd, ee,
+                                                                      gsh, cnt, ws, L, nmax);
+  } else if (c.chase2) {
     const size_t c2smem = ((size_t)kCh2Cap * kSBLdb + 32 * kCh2Warps) * sizeof(double);
     e = cudaFuncSetAttribute(k_sbr_chase2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2smem);
     if (e != cudaSuccess) return e;
