@@ -1637,12 +1637,13 @@ constexpr int kSBRow = kSBLdb - 1;   // stride between (i, j) and (i, j + 1)
 // products with the Householder vector v = (1, x_1 .. x_{L-1}) * scale are formed from x before the
 // reflector's scalars are known (v^T y = y_0 + scale * sum_{l>=1} x_l y_l), the squared norm from the two
 // half-sums, and p = tau D v is broadcast through shared memory while K = tau/2 p.v is reduced.
-template <bool FULL>
+// S0: the sweep's first step (s = 0: no block B; the annihilated column is column j itself)
+template <bool FULL, bool S0>
 __device__ __forceinline__ void chase_task_t(double* __restrict__ Bd, double* __restrict__ ps, int j, int s, int L,
                                              int L2) {
   const int lane = threadIdx.x & 31;
   const int r = j + 1 + s * kSB;
-  const int cx = (s == 0) ? j : r - kSB;    // column holding x (rows r .. r + L - 1)
+  const int cx = S0 ? j : r - kSB;    // column holding x (rows r .. r + L - 1)
   const int l16 = lane & 15, hh = lane >> 4;
   const int r2 = r + L;
   const double* px = Bd + cx * kSBRow + r;
@@ -1658,12 +1659,12 @@ __device__ __forceinline__ void chase_task_t(double* __restrict__ Bd, double* __
     const int l = 8 * hh + q;
     if (FULL) {
       xl[q] = px[l];
-      b[q] = s > 0 ? pB[q] : 0.0;
-      dd[q] = (l16 >= l) ? pDlo[q * kSBRow] : pDup[q];
+      b[q] = S0 ? 0.0 : pB[q];
+      dd[q] = *((l16 >= l) ? pDlo + q * kSBRow : pDup + q);   // one load through a selected address
       cr[q] = pC[q * kSBRow];
     } else {
       xl[q] = (l < L) ? px[l] : 0.0;
-      b[q] = (s > 0 && l < L) ? pB[q] : 0.0;
+      b[q] = (!S0 && l < L) ? pB[q] : 0.0;
       dd[q] = (l16 < L && l < L) ? ((l16 >= l) ? pDlo[q * kSBRow] : pDup[q]) : 0.0;
       cr[q] = (l16 < L2 && l < L) ? pC[q * kSBRow] : 0.0;
     }
@@ -1720,7 +1721,7 @@ __device__ __forceinline__ void chase_task_t(double* __restrict__ Bd, double* __
   const double K = 0.5 * tau * pv;
   const double wa = fma(-K, va, pa);
   // stores (each lane writes only entries it loaded itself, or the lower entries of D it owns)
-  if (s == 0) {
+  if (S0) {
     if (lane < L) Bd[j * kSBRow + r + lane] = (lane == 0) ? beta : 0.0;
   } else {
 #pragma unroll
@@ -1743,8 +1744,13 @@ __device__ __forceinline__ void chase_task(double* __restrict__ Bd, double* __re
   const int r = j + 1 + s * kSB;
   const int L = min(kSB, n - r);
   const int L2 = min(kSB, n - r - L);
-  if (L == kSB && L2 == kSB) chase_task_t<true>(Bd, ps, j, s, L, L2);
-  else chase_task_t<false>(Bd, ps, j, s, L, L2);
+  if (s == 0) {
+    if (L == kSB && L2 == kSB) chase_task_t<true, true>(Bd, ps, j, s, L, L2);
+    else chase_task_t<false, true>(Bd, ps, j, s, L, L2);
+  } else {
+    if (L == kSB && L2 == kSB) chase_task_t<true, false>(Bd, ps, j, s, L, L2);
+    else chase_task_t<false, false>(Bd, ps, j, s, L, L2);
+  }
 }
 
 // ---------------------------------------------------------------------------
