@@ -83,6 +83,9 @@ cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
   if (const char* env = getenv("CMSVD_TC_BIG")) h->c.tc_big = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_TC_WS")) h->c.tc_ws = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_ZZ_FUSED")) h->c.zz_fused = !(env[0] == '0');
+  if (const char* env = getenv("CMSVD_G_UPPER")) h->c.g_upper = atoi(env);
+  if (const char* env = getenv("CMSVD_SBR_GROUPS")) h->c.sbr_groups = std::max(1, std::min(16, atoi(env)));
+  if (const char* env = getenv("CMSVD_SBR_PANEL_RR")) h->c.sbr_panel_rr = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_CHOL_BLOCKED")) h->c.chol_blocked = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_DUO")) h->c.eig_duo = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_DUO160")) h->c.eig_duo160 = !(env[0] == '0');
@@ -115,6 +118,9 @@ cmsvd_status cmsvd_destroy(cmsvd_ctx ctx) {
   for (auto& b : c.cws) release(b);
   prof_collect(c);
   for (auto e : c.prof.pool) cudaEventDestroy(e);
+  if (c.aux_stream) cudaStreamDestroy(c.aux_stream);
+  for (auto& ev : c.aux_ev)
+    if (ev) cudaEventDestroy(ev);
   if (c.own_stream) cudaStreamDestroy(c.stream);
   delete ctx;
   return CMSVD_OK;

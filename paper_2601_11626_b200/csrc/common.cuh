@@ -143,6 +143,15 @@ struct Ctx {
                                        // 22.8 ms: the chase is bound by task throughput (~4.7 tasks/us/SM in both), not by latency
   bool chase_small = true;             // band chase, n <= 256: 6-warp CTAs with half the band, two per SM (CMSVD_CHASE_SMALL=0: off)
   bool chase_flags = false;            // band chase: per-sweep progress flags instead of time-step barriers
+  int g_upper = 1;                     // core Grams of the band reduction: 1 = strict upper triangle not written, 0 = written,
+                                       // 2 = poisoned with NaN (CMSVD_G_UPPER; the band reduction reads the lower storage only)
+  int sbr_groups = 1;                  // band reduction, n <= 512: the batch is cut into this many groups whose band chase + bisection
+                                       // run on a second stream under the next group's stage 1 (CMSVD_SBR_GROUPS; 1: one stream,
+                                       // the default: measured 89.4 ms per config-4 pass with 4 groups vs 85.7 with one -- the
+                                       // chase CTA's 139 KB of shared memory leaves one stage-1 CTA per SM instead of four)
+  cudaStream_t aux_stream = nullptr;   // second stream of the pipelined band reduction (created on first use)
+  cudaEvent_t aux_ev[17] = {};         // group hand-over events + the join
+  bool sbr_panel_rr = true;            // band reduction, n <= 512: register-resident panel QR (CMSVD_SBR_PANEL_RR=0: shared-memory kernel)
   bool eig_sbr = true;                 // n > 160: two-stage (band) reduction instead of the one-stage in-place kernel
   bool eig_rr = true;                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)
   bool zz_syrk = true;                 // w <= 128: Z^T Z by k_syrk_zz instead of k_gemm_tn (CMSVD_ZZ_SYRK=0: off)

@@ -783,7 +783,8 @@ Status pair_eval_dev(Ctx& c, const int2* d_pairs, int64_t P, int r, unsigned kin
         prof_end(c, pf);
         pf = prof_begin(c, PC_BUILD_G);
         k_build_G<<<(unsigned)Pc, kThreads, 0, c.stream>>>(pr, d_bd, d_ad, QMAX, WMAX, GMAX, Z, W,
-                                                           zz_fused ? nullptr : ZZ, Gm, zn2);
+                                                           zz_fused ? nullptr : ZZ, Gm, zn2,
+                                                           (GMAX > 160 && c.eig_sbr) ? c.g_upper : 0);
         c.launches += 1;
         CK(cudaGetLastError(), "pairs: build G");
         prof_end(c, pf);

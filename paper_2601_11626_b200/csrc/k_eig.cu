@@ -1719,6 +1719,83 @@ static bool uses_duo(const Ctx& c, int nmax) {
 }
 bool tridiag_can_save(const Ctx& c, int nmax) { return c.eig_rr && nmax <= 160 && !(nmax <= 128 && uses_duo(c, nmax)); }
 
+// top-kw eigenvalues of nprob tridiagonals (dd, ee = e^2, Gershgorin data gsh) by bisection / multisection
+static cudaError_t launch_bisect_topk(Ctx& c, int nprob, int kw, int nstride, const int* d_ns, const double* dd,
+                                      const double* ee, const double* gsh, const int* cnt, double* ev) {
+  cudaError_t e;
+  const int64_t total = (int64_t)nprob * kw;
+  const int prb = prof_begin(c, PC_BISECT);
+  if (total <= kMultisectMax)
+    k_multisect<<<(unsigned)((total + 3) / 4), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
+  else
+  {
+    // stage the block's tridiagonals when a block spans at most kBisStage problems
+    const size_t sm = (size_t)kBisStage * nstride * (2 * sizeof(double) + 2 * sizeof(float));
+    if (128 / kw + 2 <= kBisStage && sm <= 96 * 1024) {
+      e = cudaFuncSetAttribute(k_bisect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      k_bisect<true><<<(unsigned)((total + 127) / 128), 128, sm, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh,
+                                                                             cnt, ev);
+    } else {
+      k_bisect<false><<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh,
+                                                                              cnt, ev);
+    }
+  }
+  c.launches += 1;
+  prof_end(c, prb);
+  return cudaGetLastError();
+}
+
+// Pipelined two-stage reduction (n <= 512, large batches): the batch is cut into groups; stage 1 (dense -> band:
+// HBM / DMMA bound, fills the SMs) of the groups runs back to back on the context's stream, the band chase (one
+// CTA per SM, latency bound, ~1.2 IPC) and the bisection of a finished group on a second stream, i.e. under
+// the next group's stage 1.  Same kernels, same per-problem arithmetic: the results are bitwise those of the
+// one-stream path.
+static cudaError_t launch_sbr_pipelined(Ctx& c, double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
+                                        int nprob, int nmax, const double* d_thr, int kw, int nstride, double* dd,
+                                        double* ee, double* gsh, int* cnt, double* trace, double* ev, int groups) {
+  cudaError_t e;
+  if (!c.aux_stream) {
+    e = cudaStreamCreateWithFlags(&c.aux_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+  }
+  for (int g = 0; g <= groups; ++g)
+    if (!c.aux_ev[g]) {
+      e = cudaEventCreateWithFlags(&c.aux_ev[g], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+  double* ws = (double*)c.ws[WS_SBR].p;
+  const int64_t per = sbr_ws_per(nmax);
+  const int gs = (nprob + groups - 1) / groups;
+  cudaStream_t main_stream = c.stream;
+  for (int g = 0; g < groups; ++g) {
+    const int p0 = g * gs, np = std::min(gs, nprob - p0);
+    if (np <= 0) break;
+    double* Gg = G + (int64_t)p0 * stride_in;
+    const double* thr = d_thr ? d_thr + p0 : nullptr;
+    double* ddg = dd + (int64_t)p0 * nstride;
+    double* eeg = ee + (int64_t)p0 * nstride;
+    e = launch_tridiag_sbr(c, Gg, ld_in, stride_in, d_ns + p0, np, nmax, thr, kw, nstride, ddg, eeg, gsh + 4 * (int64_t)p0,
+                           cnt + p0, trace + p0, ws + (int64_t)p0 * per, 1);
+    if (e != cudaSuccess) return e;
+    e = cudaEventRecord(c.aux_ev[g], main_stream);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamWaitEvent(c.aux_stream, c.aux_ev[g], 0);
+    if (e != cudaSuccess) return e;
+    c.stream = c.aux_stream;
+    e = launch_tridiag_sbr(c, Gg, ld_in, stride_in, d_ns + p0, np, nmax, thr, kw, nstride, ddg, eeg, gsh + 4 * (int64_t)p0,
+                           cnt + p0, trace + p0, ws + (int64_t)p0 * per, 2);
+    if (e == cudaSuccess)
+      e = launch_bisect_topk(c, np, kw, nstride, d_ns + p0, ddg, eeg, gsh + 4 * (int64_t)p0, cnt + p0,
+                             ev + (int64_t)p0 * kw);
+    c.stream = main_stream;
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaEventRecord(c.aux_ev[groups], c.aux_stream);
+  if (e != cudaSuccess) return e;
+  return cudaStreamWaitEvent(main_stream, c.aux_ev[groups], 0);
+}
+
 cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
                                 int nprob, int nmax, const double* d_thr, int kw, double* ev, int* cnt,
                                 double* trace, double* scratch, double* save, int64_t save_stride) {
@@ -1771,6 +1848,11 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
     // two-stage reduction (k_sbr.cu): dense -> band (BLAS3-shaped panels) -> tridiagonal (bulge chasing)
     e = ensure(c.ws[WS_SBR], sbr_ws_bytes(nprob, nmax));
     if (e != cudaSuccess) return e;
+    // large batches of n <= 512 problems: groups of at least two CTA waves of the chase, pipelined on two streams
+    const int groups = nmax <= 512 ? std::min(c.sbr_groups, nprob / (2 * c.sm_count)) : 1;
+    if (groups >= 2)
+      return launch_sbr_pipelined(c, const_cast<double*>(G), ld_in, stride_in, d_ns, nprob, nmax, d_thr, kw, nstride,
+                                  dd, ee, gsh, cnt, trace, ev, groups);
     e = launch_tridiag_sbr(c, const_cast<double*>(G), ld_in, stride_in, d_ns, nprob, nmax, d_thr, kw, nstride, dd, ee,
                            gsh, cnt, trace, (double*)c.ws[WS_SBR].p);
     if (e != cudaSuccess) return e;
@@ -1791,27 +1873,7 @@ cudaError_t launch_tridiag_topk(Ctx& c, const double* G, int64_t ld_in, int64_t 
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int64_t total = (int64_t)nprob * kw;
-  const int prb = prof_begin(c, PC_BISECT);
-  if (total <= kMultisectMax)
-    k_multisect<<<(unsigned)((total + 3) / 4), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
-  else
-  {
-    // stage the block's tridiagonals when a block spans at most kBisStage problems
-    const size_t sm = (size_t)kBisStage * nstride * (2 * sizeof(double) + 2 * sizeof(float));
-    if (128 / kw + 2 <= kBisStage && sm <= 96 * 1024) {
-      e = cudaFuncSetAttribute(k_bisect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e != cudaSuccess) return e;
-      k_bisect<true><<<(unsigned)((total + 127) / 128), 128, sm, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh,
-                                                                             cnt, ev);
-    } else {
-      k_bisect<false><<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh,
-                                                                              cnt, ev);
-    }
-  }
-  c.launches += 1;
-  prof_end(c, prb);
-  return cudaGetLastError();
+  return launch_bisect_topk(c, nprob, kw, nstride, d_ns, dd, ee, gsh, cnt, ev);
 }
 
 size_t tridiag_scratch_bytes(int nprob, int nmax) { return ((size_t)nprob * (2 * nmax + 4)) * 8; }

@@ -65,12 +65,15 @@ __global__ void k_make_descs(const int2* __restrict__ pairs, int64_t P, const Ba
   (void)GMAX;
 }
 
-// G = [[D^2, D Z_r], [Z_r^T D, ZZ + W]] (fp64, ld GMAX) and ||Z||_F^2.
+// G = [[D^2, D Z_r], [Z_r^T D, ZZ + W]] (fp64, ld GMAX) and ||Z||_F^2.  Only the lower triangles of W and ZZ
+// are read (their producers may leave the strict upper triangle uncomputed).  upper: 0 = G written in full,
+// 1 = the strict upper triangle of G is not written (the band reduction reads the lower storage only),
+// 2 = it is poisoned with NaN (test knob CMSVD_G_POISON=1: proves that nothing downstream reads it).
 __global__ void __launch_bounds__(kThreads) k_build_G(const int2* __restrict__ pairs, const BaseDesc* __restrict__ bd,
                                                       const AppDesc* __restrict__ ad, int QMAX, int WMAX, int GMAX,
                                                       const float* __restrict__ Zws, const double* __restrict__ Wws,
                                                       const double* __restrict__ ZZws, double* __restrict__ Gws,
-                                                      double* __restrict__ zn2) {
+                                                      double* __restrict__ zn2, int upper) {
   const int64_t p = blockIdx.x;
   const int2 pr = pairs[p];
   const BaseDesc b = bd[pr.x];
@@ -83,11 +86,18 @@ __global__ void __launch_bounds__(kThreads) k_build_G(const int2* __restrict__ p
   double* G = Gws + p * (int64_t)GMAX * GMAX;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     int i = e % n, j = e / n;
+    if (i < j && upper) {
+      if (upper == 2) G[(int64_t)j * GMAX + i] = __longlong_as_double(0x7ff8000000000000ll);
+      continue;
+    }
     double v;
     if (i < rr && j < rr) v = (i == j) ? b.spec[i] * b.spec[i] : 0.0;
     else if (i < rr) v = b.spec[i] * (double)Z[(int64_t)(j - rr) * QMAX + i];
     else if (j < rr) v = b.spec[j] * (double)Z[(int64_t)(i - rr) * QMAX + j];
-    else v = (ZZws ? ZZ[(int64_t)(j - rr) * WMAX + (i - rr)] : 0.0) + W[(int64_t)(j - rr) * WMAX + (i - rr)];
+    else {
+      const int a = max(i, j) - rr, c = min(i, j) - rr;   // (row a, column c) of the lower triangle
+      v = (ZZws ? ZZ[(int64_t)c * WMAX + a] : 0.0) + W[(int64_t)c * WMAX + a];
+    }
     G[(int64_t)j * GMAX + i] = v;
   }
   if (threadIdx.x == 0) {

@@ -225,6 +225,170 @@ __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict_
 }
 
 // ---------------------------------------------------------------------------
+// Stage 1a, register-resident variant (n <= kSBMax; the default).  The shared-memory kernel above spends its
+// time in the load/store unit (two or three shared-memory wavefronts per DFMA: 16 % of the DFMA rate) and in
+// five CTA barriers per column.  Here thread tid owns ROWS tid and tid + 256 of the panel, all 16 columns in
+// registers (the column loop is fully unrolled, so every register index is static); shared memory carries
+// only the 8 x 16 warp totals, double-buffered: ONE barrier per column.  Per column k:
+//   1. every thread: partial dots of x = P[k+1:, k] (its rows below k) with all 16 columns -- columns c > k for
+//      the update, c < k for the V^T V entries that larft needs, c = k for the norm; a transposing shuffle
+//      reduction leaves the warp total of column c in lanes 2 c, 2 c + 1; the owner of row k publishes that row
+//                                                                                                -> barrier
+//   2. every warp, lane c (and c + 16): total of column c from the 8 warp totals; every lane forms beta, tau,
+//      scale (rsqrt / rcp + Newton, as in the chase) and s_c = tau (P[k][c] + scale d_c); warp 0 also stores
+//      tau, scale and S[c][k] (c < k)
+//   3. every thread updates its rows in registers with s_c shuffled from lane c:
+//      P[i][c] -= s_c scale x_i (i > k), P[k][c] -= s_c, P[k][k] = beta
+// The Householder vectors stay unscaled in the registers (v = scale x below the diagonal) until V is written.
+// ---------------------------------------------------------------------------
+constexpr int kP3Warps = kPanelThreads / 32;
+constexpr int kP3Smem = (2 * kP3Warps * 16 + 2 * 16 + 2 * kSB + 2 * kSB * kSB) * (int)sizeof(double);
+
+__global__ void __launch_bounds__(kPanelThreads, 2) k_sbr_panel3(double* __restrict__ G, int64_t ld, int64_t stride,
+                                                                 const int* __restrict__ ns, int t,
+                                                                 double* __restrict__ ws, double* __restrict__ trace,
+                                                                 const SbrWs L, int par) {
+  extern __shared__ __align__(16) double psm[];
+  double* wtot = psm;                       // [2][8 warps][16]
+  double* rowk = wtot + 2 * kP3Warps * 16;  // [2][16] row k of the panel (published by its owner)
+  double* scal = rowk + 2 * 16;             // tau per column
+  double* scl = scal + kSB;                 // scale per column
+  double* S = scl + kSB;                    // 16 x 16
+  double* T = S + kSB * kSB;                // 16 x 16
+  const int p = blockIdx.x;
+  const int n = ns[p];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* A = G + (int64_t)p * stride;
+  if (t == 0 && tid < 32) {   // trace of the original matrix (invariant, kept for the finalisation)
+    double s = 0.0;
+    for (int i = tid; i < n; i += 32) s += A[(int64_t)i * ld + i];
+    s = warp_sum(s);
+    if (tid == 0) trace[p] = s;
+  }
+  if (t >= sbr_panels(n)) return;
+  const int c0 = t * kSB, R0 = c0 + kSB, np = n - R0;
+  const int kmax = min(kSB, np);
+  const int r0 = tid, r1 = tid + kPanelThreads;
+  double p0[kSB], p1[kSB];
+#pragma unroll
+  for (int c = 0; c < kSB; ++c) {
+    const double* col = A + (int64_t)(c0 + c) * ld + R0;
+    p0[c] = r0 < np ? col[r0] : 0.0;
+    p1[c] = r1 < np ? col[r1] : 0.0;
+  }
+  S[tid] = 0.0;
+  if (tid < kSB) { scal[tid] = 0.0; scl[tid] = 0.0; }
+  const int lc = lane & 15;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+  for (int k = 0; k < kSB; ++k) {
+    if (k < kmax) {   // CTA-uniform
+      double* wt = wtot + (k & 1) * kP3Warps * 16;
+      double* rk = rowk + (k & 1) * 16;
+      // 1. partial dots of x (rows > k of column k) with every column, reduced over the warp
+      const double x0 = r0 > k ? p0[k] : 0.0;
+      const double x1 = p1[k];                 // r1 >= 256 > k; zero beyond np
+      double v[16];
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) v[c] = fma(x1, p1[c], x0 * p0[c]);
+      double w8[8], w4[4], w2[2], w1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double keep = b4 ? v[j + 8] : v[j], send = b4 ? v[j] : v[j + 8];
+        w8[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double keep = b3 ? w8[j + 4] : w8[j], send = b3 ? w8[j] : w8[j + 4];
+        w4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const double keep = b2 ? w4[j + 2] : w4[j], send = b2 ? w4[j] : w4[j + 2];
+        w2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      {
+        const double keep = b1 ? w2[1] : w2[0], send = b1 ? w2[0] : w2[1];
+        w1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      w1 += __shfl_xor_sync(0xffffffffu, w1, 1);   // warp total of column lane >> 1
+      if ((lane & 1) == 0) wt[wid * 16 + (lane >> 1)] = w1;
+      if (tid == k) {
+#pragma unroll
+        for (int c = 0; c < kSB; ++c) rk[c] = p0[c];
+      }
+      __syncthreads();
+      // 2. totals and the reflector's scalars (every warp, redundantly)
+      double d = 0.0;
+#pragma unroll
+      for (int w = 0; w < kP3Warps; ++w) d += wt[w * 16 + lc];
+      const double sig2 = __shfl_sync(0xffffffffu, d, k);
+      const double alpha = rk[k];
+      const double pkc = rk[lc];
+      double tau = 0.0, beta = alpha, scale = 0.0;
+      if (sig2 > 0.0) {
+        const double x2 = fma(alpha, alpha, sig2);
+        double y;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x2));
+        const double e = fma(-(x2 * y), y, 1.0);
+        y = fma(y * e, fma(e, 0.375, 0.5), y);
+        const double xn = x2 * y;
+        beta = alpha >= 0.0 ? -xn : xn;
+        tau = (beta - alpha) * sbr_rcp(beta);
+        scale = sbr_rcp(alpha - beta);
+      }
+      const double sc = tau * fma(scale, d, pkc);   // lane c > k: tau (P[k][c] + v^T P[k+1:, c])
+      if (wid == 0 && lane < kSB) {
+        if (lane < k) S[lane * kSB + k] = scl[lane] * fma(scale, d, pkc);   // v_c^T v_k
+        else if (lane == k) { scal[k] = tau; scl[k] = scale; }
+      }
+      // 3. update in registers
+      const double f0 = r0 > k ? scale * p0[k] : (r0 == k ? 1.0 : 0.0);   // v_i of this thread's rows
+      const double f1 = scale * p1[k];
+#pragma unroll
+      for (int c = k + 1; c < kSB; ++c) {
+        const double scc = __shfl_sync(0xffffffffu, sc, c);
+        p0[c] = fma(-scc, f0, p0[c]);
+        p1[c] = fma(-scc, f1, p1[c]);
+      }
+      if (r0 == k) p0[k] = beta;
+      // (column k + 1 writes the other halves of wtot / rowk; column k + 2 reuses these after the barrier of
+      // column k + 1, which every warp reaches only after its reads above)
+    }
+  }
+  __syncthreads();
+  // T (upper triangular): T[k][k] = tau_k, T[0:k][k] = -tau_k T[0:k][0:k] S[0:k][k]
+  if (tid < 32) {
+    const int i = tid;
+    for (int k = 0; k < kSB; ++k) {
+      const double tk = k < kmax ? scal[k] : 0.0;
+      double s = 0.0;
+      if (i < k)
+        for (int l = i; l < k; ++l) s = fma(T[i * kSB + l], S[l * kSB + k], s);
+      __syncwarp();
+      if (i < kSB) T[i * kSB + k] = (i < k) ? -tk * s : (i == k ? tk : 0.0);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // outputs: R into the band (rows R0 .. R0 + 15 of the panel columns, upper triangle), T, V (unit lower
+  // trapezoidal; zero rows from np on: the set was last written by panel t - 2, whose rows from np + 2 kSB on
+  // are zero already; zero columns from kmax on)
+  double* Vw = L.vp(ws, p, par);
+  double* Tw = Vw + 2 * L.vsz();
+  Tw[tid] = T[tid];
+  const int zend = t < 2 ? L.ldv : min(L.ldv, np + 2 * kSB);
+#pragma unroll
+  for (int c = 0; c < kSB; ++c) {
+    if (r0 < kSB && r0 <= c && r0 < np) A[(int64_t)(c0 + c) * ld + R0 + r0] = p0[c];   // R[r0][c]
+    const double sc = c < kmax ? scl[c] : 0.0;
+    double* vw = Vw + (int64_t)c * L.ldv;
+    if (r0 < zend) vw[r0] = (c < kmax && r0 < np) ? (r0 > c ? sc * p0[c] : (r0 == c ? 1.0 : 0.0)) : 0.0;
+    if (r1 < zend) vw[r1] = (c < kmax && r1 < np) ? sc * p1[c] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Stage 1b: Y = A22 V T for rows [128 b, 128 b + 128) of A22 (n_p x n_p, symmetric, lower stored),
 // M_b = V_b^T Y_b.  Thread t: rows i0 = t % 64 and i0 + 64, columns 8 (t / 64) .. + 7.  The 32-column
 // slices of the symmetric row panel are staged by cp.async into two buffers (the next slice's copies in
@@ -2240,13 +2404,16 @@ static bool sbr_ws_map(CUtensorMap* map, double* base, int nprob, const SbrWs& L
 }
 
 size_t sbr_ws_bytes(int nprob, int nmax) { return (size_t)nprob * sbr_layout(nmax).per * sizeof(double); }
+int64_t sbr_ws_per(int nmax) { return sbr_layout(nmax).per; }
 
 // Stage 1 + stage 2 for nprob problems (n = ns[p] <= nmax <= kSBBig, G destroyed): writes dd, ee (e^2), gsh,
 // cnt, trace like k_tridiag.  ws: sbr_ws_bytes(nprob, nmax) bytes.  n <= 512 (the pair path): panel and band
 // in shared memory; larger n (N1 cluster verification): panel in place and band in global memory.
 cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, const int* d_ns, int nprob, int nmax,
                                const double* d_thr, int kw, int nstride, double* dd, double* ee, double* gsh,
-                               int* cnt, double* trace, double* ws) {
+                               int* cnt, double* trace, double* ws, int phase) {
+  // phase: bit 0 = stage 1 (dense -> band), bit 1 = stage 2 (band -> tridiagonal); the pipelined caller
+  // (launch_tridiag_topk) issues the two stages of a group of problems on different streams
   if (nmax > kSBBig) return cudaErrorInvalidValue;
   const SbrWs L = sbr_layout(nmax);
   const bool big = nmax > kSBMax;
@@ -2305,6 +2472,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   }
   cudaError_t e = cudaFuncSetAttribute(k_sbr_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_sbr_panel3, cudaFuncAttributeMaxDynamicSharedMemorySize, kP3Smem);
+  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_sbr_symm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)symm_smem);
   if (e != cudaSuccess) return e;
   auto panel = [&](int t) {
@@ -2312,6 +2481,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     if (big)
       k_sbr_panel<false><<<nprob, kPanelThreads, (256 + 2 * kSB + 2 * kSB * kSB) * sizeof(double), c.stream>>>(
           G, ld, stride, d_ns, t, ws, trace, L, t & 1);
+    else if (c.sbr_panel_rr)
+      k_sbr_panel3<<<nprob, kPanelThreads, kP3Smem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L, t & 1);
     else
       k_sbr_panel<true><<<nprob, kPanelThreads, psmem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L, t & 1);
     c.launches += 1;
@@ -2336,6 +2507,7 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     c.launches += 1;
     prof_end(c, pr);
   };
+  if (phase & 1) {
   // trace (panel 0 kernel) even when there are no panels
   panel(0);
   if (npan > 0) symm_w(0);
@@ -2393,6 +2565,8 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+  }
+  if (!(phase & 2)) return cudaGetLastError();
   const size_t csmem = ((big ? 0 : (size_t)kSBMax * kSBLdb) + (size_t)(big ? nmax : kSBMax) / 2 + 2 +
                         32 * kChaseWarps) * sizeof(double);
   const int pr = prof_begin(c, PC_SBR_CHASE);

@@ -34,7 +34,8 @@ size_t tridiag_scratch_bytes(int nprob, int nmax);
 size_t sbr_ws_bytes(int nprob, int nmax);
 cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, const int* d_ns, int nprob, int nmax,
                                const double* d_thr, int kw, int nstride, double* dd, double* ee, double* gsh,
-                               int* cnt, double* trace, double* ws);
+                               int* cnt, double* trace, double* ws, int phase = 3);
+int64_t sbr_ws_per(int nmax);   // doubles of band-reduction workspace per problem
 // top-kw eigenpairs of one n x n symmetric matrix (n <= 160, kw <= 64): Z (n x kw, ld n), evals[kw]
 // non-increasing; G is read only.  d_n: device int holding n.
 size_t syev_topk_scratch_bytes(int n, int kw);
@@ -47,7 +48,8 @@ __global__ void k_make_descs(const int2* pairs, int64_t P, const BaseDesc* bd, c
                              double* ZZws, GemmDesc* dZ, GemmDesc* dR, GemmDesc* dW, GemmDesc* dZZ, int* nG, int* nW,
                              double* thrW, int r);
 __global__ void k_build_G(const int2* pairs, const BaseDesc* bd, const AppDesc* ad, int QMAX, int WMAX, int GMAX,
-                          const float* Zws, const double* Wws, const double* ZZws, double* Gws, double* zn2);
+                          const float* Zws, const double* Wws, const double* ZZws, double* Gws, double* zn2,
+                          int upper);
 __global__ void k_finalize_tight(const int2* pairs, int64_t P, const BaseDesc* bd, const AppDesc* ad, int r,
                                  const double* evW, const int* cntW, const double* trW, const double* zn2,
                                  double* err2x, double* total);

@@ -180,6 +180,26 @@ def test_c4_reduced_wide_operands(cm, tc_big, tc_ws, monkeypatch):
     compare(out, orc, 7, f"config4-reduced r=192 tc_big={tc_big} tc_ws={tc_ws}")
 
 
+def test_core_gram_lower_storage_only(cm, monkeypatch):
+    """Core Grams above n = 160 are built in lower storage only (k_build_G leaves the strict upper triangle of
+    G unwritten, and reads only the lower triangles of W' and Z^T Z).  Poisoning the upper triangle with NaN
+    (CMSVD_G_UPPER=2) or writing it in full (=0) must not change a single output bit: nothing downstream of
+    k_build_G reads it.  Checked against the oracle as well."""
+    col = synth.config4(N=4, m=1024, rank=64)
+    r = 192
+    outs = {}
+    for mode in ("1", "2", "0"):
+        monkeypatch.setenv("CMSVD_G_UPPER", mode)
+        sp, E, sig, rank, pairs, outs[mode] = run_pairs(cm, col, r)
+    for mode in ("2", "0"):
+        for key in ("err2", "total", "sigma_tilde", "mu"):
+            a, b = outs["1"][key], outs[mode][key]
+            if a is not None:
+                assert np.array_equal(np.asarray(a), np.asarray(b), equal_nan=True), (mode, key)
+    orc = oracle.pair_errors(sp, pairs, r, 7, oracle.TRUNC)
+    compare(outs["1"], orc, 7, "config4-reduced r=192, lower-storage core Grams")
+
+
 def _flat_block(R, m, decay):
     U = np.linalg.qr(R.standard_normal((m, m)))[0]
     V = np.linalg.qr(R.standard_normal((m, m)))[0]

@@ -80,13 +80,14 @@ def test_structured_spectra(cm):
 
 @pytest.mark.parametrize("knob", ["", "CMSVD_SBR_FUSED=1", "CMSVD_SYMM_DMMA=0", "CMSVD_SYR2K_DMMA=0", "CMSVD_SYR2K_ROW=0",
                                   "CMSVD_SYMM_DMMA=0,CMSVD_SYR2K_DMMA=0,CMSVD_SYR2K_ROW=1", "CMSVD_CHASE2=1",
-                                  "CMSVD_CHASE_FLAGS=1", "CMSVD_SBR_TMA=0"])
+                                  "CMSVD_CHASE_FLAGS=1", "CMSVD_SBR_TMA=0", "CMSVD_SBR_PANEL_RR=0"])
 def test_band_reduction_variants(cm, knob, monkeypatch):
     """Every selectable path of the two-stage reduction agrees with LAPACK on ragged sizes (including the
     global-memory panel / band above 512): the default (stage 1 on the fp64 tensor cores: DMMA product and
     row-persistent DMMA update), the scalar product / update kernels, the one-tile-per-CTA and row-persistent
     scalar updates, the look-ahead fused pass, the chase with per-sweep flags or with two problems in flight
-    per CTA over the circular band buffer, and the non-TMA staging."""
+    per CTA over the circular band buffer, the non-TMA staging, and the shared-memory panel QR (the default
+    panel kernel keeps the panel in registers)."""
     for kv in filter(None, knob.split(",")):
         k, v = kv.split("=")
         monkeypatch.setenv(k, v)
@@ -96,6 +97,28 @@ def test_band_reduction_variants(cm, knob, monkeypatch):
     with cm.Context(0) as ctx:
         ev, _ = ctx.sym_eigvals(mats, 160)
     check(ev, mats, 160)
+
+
+@pytest.mark.parametrize("groups", ["1", "3"])
+def test_pipelined_groups_bitwise(cm, groups, monkeypatch):
+    """CMSVD_SBR_GROUPS: the batch cut into groups whose chase + bisection run on a second stream under the
+    next group's stage 1.  Same kernels per problem: the eigenvalues are bitwise those of the one-stream path
+    (and within the LAPACK bar), on a ragged batch large enough for three groups (>= 2 x SM count each)."""
+    R = np.random.default_rng(43)
+    base = [300, 161, 256, 0, 200, 257, 170, 3]
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    sizes = (base * ((6 * nsm + 40) // len(base) + 1))[:6 * nsm + 37]
+    protos = {n: (gram(R, n, decay=0.3) if n else np.zeros((0, 0))) for n in set(sizes)}
+    mats = [protos[n] for n in sizes]
+    monkeypatch.setenv("CMSVD_SBR_GROUPS", "1")
+    with cm.Context(0) as ctx:
+        ev1, tr1 = ctx.sym_eigvals(mats, 64)
+    monkeypatch.setenv("CMSVD_SBR_GROUPS", groups)
+    with cm.Context(0) as ctx:
+        ev, tr = ctx.sym_eigvals(mats, 64)
+        ev_b, _ = ctx.sym_eigvals(mats, 64)   # second call on the same context: streams and events reused
+    assert np.array_equal(ev, ev1) and np.array_equal(tr, tr1) and np.array_equal(ev_b, ev1)
+    check(ev[:len(base)], mats[:len(base)], 64)
 
 
 def test_chase_two_in_flight_queue(cm, monkeypatch):
