@@ -145,10 +145,9 @@ struct Ctx {
   bool chase_flags = false;            // band chase: per-sweep progress flags instead of time-step barriers
   int g_upper = 1;                     // core Grams of the band reduction: 1 = strict upper triangle not written, 0 = written,
                                        // 2 = poisoned with NaN (CMSVD_G_UPPER; the band reduction reads the lower storage only)
-  int sbr_groups = 1;                  // band reduction, n <= 512: the batch is cut into this many groups whose band chase + bisection
-                                       // run on a second stream under the next group's stage 1 (CMSVD_SBR_GROUPS; 1: one stream,
-                                       // the default: measured 89.4 ms per config-4 pass with 4 groups vs 85.7 with one -- the
-                                       // chase CTA's 139 KB of shared memory leaves one stage-1 CTA per SM instead of four)
+  int sbr_groups = 1;                  // band reduction, n <= 512: the band chase runs in this many groups of whole CTA waves, the
+                                       // bisection of a finished group on a second stream under the next group's chase
+                                       // (CMSVD_SBR_GROUPS; 1: one stream)
   cudaStream_t aux_stream = nullptr;   // second stream of the pipelined band reduction (created on first use)
   cudaEvent_t aux_ev[17] = {};         // group hand-over events + the join
   bool sbr_panel_rr = true;            // band reduction, n <= 512: register-resident panel QR (CMSVD_SBR_PANEL_RR=0: shared-memory kernel)

@@ -1746,11 +1746,15 @@ static cudaError_t launch_bisect_topk(Ctx& c, int nprob, int kw, int nstride, co
   return cudaGetLastError();
 }
 
-// Pipelined two-stage reduction (n <= 512, large batches): the batch is cut into groups; stage 1 (dense -> band:
-// HBM / DMMA bound, fills the SMs) of the groups runs back to back on the context's stream, the band chase (one
-// CTA per SM, latency bound, ~1.2 IPC) and the bisection of a finished group on a second stream, i.e. under
-// the next group's stage 1.  Same kernels, same per-problem arithmetic: the results are bitwise those of the
-// one-stream path.
+// Pipelined two-stage reduction (n <= 512, large batches).  Stage 1 (dense -> band: HBM / DMMA bound, several CTAs
+// per SM) runs for the whole batch; the band chase (one CTA per SM: 139 KB of shared memory, latency bound at
+// ~1.2 IPC) then runs in groups of whole CTA waves on the context's stream, and the bisection of a finished
+// group (issue bound, little shared memory: co-resident with a chase CTA) on a second stream, i.e. under the
+// next group's chase.  Same kernels, same per-problem arithmetic: the results are bitwise those of the
+// one-stream path.  Measured on config 4 (2016 problems of n = 512): 85.2 / 84.3 / 85.0 ms per pass with 2 / 3 /
+// 5 groups vs 86.0 with one stream -- the co-running bisection takes 2.2x as long and the chase is not
+// faster, so the default stays one stream (CMSVD_SBR_GROUPS).  Cutting stage 1 into groups as well was
+// measured slower (89.4 ms with 4 groups: a chase CTA leaves room for one stage-1 CTA per SM instead of four).
 static cudaError_t launch_sbr_pipelined(Ctx& c, double* G, int64_t ld_in, int64_t stride_in, const int* d_ns,
                                         int nprob, int nmax, const double* d_thr, int kw, int nstride, double* dd,
                                         double* ee, double* gsh, int* cnt, double* trace, double* ev, int groups) {
@@ -1766,7 +1770,10 @@ static cudaError_t launch_sbr_pipelined(Ctx& c, double* G, int64_t ld_in, int64_
     }
   double* ws = (double*)c.ws[WS_SBR].p;
   const int64_t per = sbr_ws_per(nmax);
-  const int gs = (nprob + groups - 1) / groups;
+  e = launch_tridiag_sbr(c, G, ld_in, stride_in, d_ns, nprob, nmax, d_thr, kw, nstride, dd, ee, gsh, cnt, trace, ws, 1);
+  if (e != cudaSuccess) return e;
+  const int waves = (nprob + c.sm_count - 1) / c.sm_count;
+  const int gs = (waves + groups - 1) / groups * c.sm_count;   // whole waves of one chase CTA per SM
   cudaStream_t main_stream = c.stream;
   for (int g = 0; g < groups; ++g) {
     const int p0 = g * gs, np = std::min(gs, nprob - p0);
@@ -1776,18 +1783,15 @@ static cudaError_t launch_sbr_pipelined(Ctx& c, double* G, int64_t ld_in, int64_
     double* ddg = dd + (int64_t)p0 * nstride;
     double* eeg = ee + (int64_t)p0 * nstride;
     e = launch_tridiag_sbr(c, Gg, ld_in, stride_in, d_ns + p0, np, nmax, thr, kw, nstride, ddg, eeg, gsh + 4 * (int64_t)p0,
-                           cnt + p0, trace + p0, ws + (int64_t)p0 * per, 1);
+                           cnt + p0, trace + p0, ws + (int64_t)p0 * per, 2);
     if (e != cudaSuccess) return e;
     e = cudaEventRecord(c.aux_ev[g], main_stream);
     if (e != cudaSuccess) return e;
     e = cudaStreamWaitEvent(c.aux_stream, c.aux_ev[g], 0);
     if (e != cudaSuccess) return e;
     c.stream = c.aux_stream;
-    e = launch_tridiag_sbr(c, Gg, ld_in, stride_in, d_ns + p0, np, nmax, thr, kw, nstride, ddg, eeg, gsh + 4 * (int64_t)p0,
-                           cnt + p0, trace + p0, ws + (int64_t)p0 * per, 2);
-    if (e == cudaSuccess)
-      e = launch_bisect_topk(c, np, kw, nstride, d_ns + p0, ddg, eeg, gsh + 4 * (int64_t)p0, cnt + p0,
-                             ev + (int64_t)p0 * kw);
+    e = launch_bisect_topk(c, np, kw, nstride, d_ns + p0, ddg, eeg, gsh + 4 * (int64_t)p0, cnt + p0,
+                           ev + (int64_t)p0 * kw);
     c.stream = main_stream;
     if (e != cudaSuccess) return e;
   }
