@@ -85,6 +85,8 @@ cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
   if (const char* env = getenv("CMSVD_ZZ_FUSED")) h->c.zz_fused = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_G_UPPER")) h->c.g_upper = atoi(env);
   if (const char* env = getenv("CMSVD_SBR_GROUPS")) h->c.sbr_groups = std::max(1, std::min(16, atoi(env)));
+  if (const char* env = getenv("CMSVD_CHASE_SPLIT")) h->c.chase_split = !(env[0] == '0');
+  if (const char* env = getenv("CMSVD_BISECT_P")) h->c.bisect_p = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_SBR_PANEL_RR")) h->c.sbr_panel_rr = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_CHOL_BLOCKED")) h->c.chol_blocked = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_EIG_DUO")) h->c.eig_duo = !(env[0] == '0');

@@ -142,6 +142,8 @@ struct Ctx {
   bool chase2 = false;                 // band chase: two problems in flight per persistent CTA (CMSVD_CHASE2=1).  Measured 25.6 vs
                                        // 22.8 ms: the chase is bound by task throughput (~4.7 tasks/us/SM in both), not by latency
   bool chase_small = true;             // band chase, n <= 256: 6-warp CTAs with half the band, two per SM (CMSVD_CHASE_SMALL=0: off)
+  bool chase_split = true;             // band chase, 256 < n <= 512: sweeps 0 .. n - 257 on the full band, the trailing 256 x 256 band
+                                       // matrix with the half-band two-CTAs-per-SM variant (CMSVD_CHASE_SPLIT=0: one kernel)
   bool chase_flags = false;            // band chase: per-sweep progress flags instead of time-step barriers
   int g_upper = 1;                     // core Grams of the band reduction: 1 = strict upper triangle not written, 0 = written,
                                        // 2 = poisoned with NaN (CMSVD_G_UPPER; the band reduction reads the lower storage only)
@@ -150,6 +152,8 @@ struct Ctx {
                                        // (CMSVD_SBR_GROUPS; 1: one stream)
   cudaStream_t aux_stream = nullptr;   // second stream of the pipelined band reduction (created on first use)
   cudaEvent_t aux_ev[17] = {};         // group hand-over events + the join
+  bool bisect_p = true;                // bisection on the division-free polynomial Sturm recurrence (CMSVD_BISECT_P=0: pivot form
+                                       // with the fp32 coarse phase)
   bool sbr_panel_rr = true;            // band reduction, n <= 512: register-resident panel QR (CMSVD_SBR_PANEL_RR=0: shared-memory kernel)
   bool eig_sbr = true;                 // n > 160: two-stage (band) reduction instead of the one-stage in-place kernel
   bool eig_rr = true;                  // register-resident tridiagonalisation for n <= 160 (CMSVD_EIG_RR=0: smem kernel)

@@ -1364,6 +1364,95 @@ __global__ void __launch_bounds__(128) k_bisect(int P, int kw, int nstride, cons
   *out = 0.5 * (lo + hi);
 }
 
+// ---------------------------------------------------------------------------
+// Division-free bisection (the default): Sturm counts from the polynomial recurrence
+//   p_0 = 1, p_1 = d_0 - x, p_i = (d_{i-1} - x) p_{i-1} - e^2_{i-2} p_{i-2},  count(x) = sign changes of (p_i),
+// on the matrix normalised by its Gershgorin norm (|d| <= 1, e^2 <= 1).  The pivot form above carries a
+// reciprocal on its dependency chain (MUFU + 3 dependent DFMA + product + clamp per step: ncu shows the kernel
+// waiting on fixed-latency dependencies at 54 % issue utilisation); here the chain is ONE DFMA per step (the
+// product e^2 p_{i-2} and the shift d - x are off the chain) and a step is 3 fp64 instructions instead of 7, so
+// the fp32 coarse phase is no longer worth its widening and all steps run in fp64.
+//   * range: |p_i| grows by at most 2^1.3 per step; every 8 steps both running values are rescaled by the power
+//     of two that brings the larger to [1, 2) (exponent arithmetic: exact, signs untouched);
+//   * zeros: e^2 is floored at 2^-200 when staged (a relative perturbation of 2^-100 of an off-diagonal entry),
+//     so p_{i+1} = -e^2 p_{i-1} != 0 after an exact zero p_i, and the sign-bit count over the two steps is 1
+//     whichever sign bit the zero carries: no per-step test;
+//   * Wilkinson's analysis of this recurrence (AEP ch. 5) gives the same backward stability as the pivot form.
+// Stopping rule and output as k_bisect.
+// ---------------------------------------------------------------------------
+constexpr int kBisPStage = 6;
+template <bool STAGE>
+__global__ void __launch_bounds__(128) k_bisect_p(int P, int kw, int nstride, const int* __restrict__ ns,
+                                                  const double* __restrict__ dd, const double* __restrict__ ee2,
+                                                  const double* __restrict__ gsh, const int* __restrict__ cnt,
+                                                  double* __restrict__ ev) {
+  extern __shared__ double bis_sm[];
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+  const int p0 = (int)(g0 / kw);
+  constexpr double kE2Floor = 6.223015277861142e-61;   // 2^-200
+  if (STAGE) {  // problems p0 .. p0 + np - 1 of this block: normalised (d_i, e2_{i-1}) pairs
+    const int64_t glast = min((int64_t)P * kw, g0 + blockDim.x) - 1;
+    const int np = glast >= g0 ? (int)(glast / kw) - p0 + 1 : 0;
+    for (int q = 0; q < np; ++q) {
+      const int pq = p0 + q;
+      const int n = ns[pq];
+      const double inv = 1.0 / gsh[4 * pq + 3];
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double di = dd[(int64_t)pq * nstride + i];
+        const double ei = i > 0 ? ee2[(int64_t)pq * nstride + i - 1] : 0.0;
+        bis_sm[(size_t)q * 2 * nstride + 2 * i] = di * inv;
+        bis_sm[(size_t)q * 2 * nstride + 2 * i + 1] = fmax((ei * inv) * inv, kE2Floor);
+      }
+    }
+    __syncthreads();
+  }
+  if (g >= (int64_t)P * kw) return;
+  const int p = (int)(g / kw), l = (int)(g % kw);
+  double* out = ev + (int64_t)p * kw + l;
+  if (l >= cnt[p]) { *out = 0.0; return; }
+  const int n = ns[p];
+  const double* d = dd + (int64_t)p * nstride;
+  const double* e2 = ee2 + (int64_t)p * nstride;
+  const double nrm = gsh[4 * p + 3];
+  const double inv = 1.0 / nrm;
+  const double2* de = reinterpret_cast<const double2*>(bis_sm + (size_t)2 * (p - p0) * nstride);
+  auto ld = [&](int i) -> double2 {   // (d_i, e2_{i-1}) normalised, i >= 1
+    return STAGE ? de[i] : make_double2(__ldg(d + i) * inv, fmax((__ldg(e2 + i - 1) * inv) * inv, kE2Floor));
+  };
+  const double d0 = STAGE ? de[0].x : d[0] * inv;
+  const int target = n - 1 - l;
+  double lo = gsh[4 * p] * inv, hi = gsh[4 * p + 1] * inv;
+  // stop at 1e-13 ||T|| absolute (the floor that resolves sigma = sqrt(lambda) near zero, A13) or 1e-11
+  // relative, whichever is looser (as k_bisect); normalised: ||T|| = 1
+  for (int it = 0; it < 120 && (hi - lo) > fmax(1e-13, 1e-11 * fmax(fabs(lo), fabs(hi))) + 4.4e-16 * fmax(fabs(lo), fabs(hi)); ++it) {
+    const double x = 0.5 * (lo + hi);
+    double pp = 1.0, pc = d0 - x;
+    int c = (int)((unsigned)__double2hiint(pc) >> 31);
+    auto step = [&](int i) {
+      const double2 v = ld(i);
+      const double t = v.y * pp;
+      const double pn = fma(v.x - x, pc, -t);
+      c += (int)((unsigned)(__double2hiint(pn) ^ __double2hiint(pc)) >> 31);
+      pp = pc;
+      pc = pn;
+    };
+    int i = 1;
+    for (; i + 8 <= n; i += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) step(i + u);
+      const unsigned ha = (unsigned)__double2hiint(pc) & 0x7fffffffu, hb = (unsigned)__double2hiint(pp) & 0x7fffffffu;
+      const unsigned ex = max(ha, hb) >> 20;                        // biased exponent of the larger
+      const double f = __hiloint2double((int)((2046u - ex) << 20), 0);   // 2^(1023 - ex)
+      pc *= f;
+      pp *= f;
+    }
+    for (; i < n; ++i) step(i);
+    if (c <= target) lo = x; else hi = x;
+  }
+  *out = 0.5 * (lo + hi) * nrm;
+}
+
 // Multisection for small batches (latency-bound: e.g. one greedy evaluation or
 // commit): one warp per wanted eigenvalue, the 32 lanes evaluate Sturm counts
 // at 32 interior points of the bracket, so each fp64 step narrows it 33x.
@@ -1731,7 +1820,16 @@ static cudaError_t launch_bisect_topk(Ctx& c, int nprob, int kw, int nstride, co
   {
     // stage the block's tridiagonals when a block spans at most kBisStage problems
     const size_t sm = (size_t)kBisStage * nstride * (2 * sizeof(double) + 2 * sizeof(float));
-    if (128 / kw + 2 <= kBisStage && sm <= 96 * 1024) {
+    const size_t smp = (size_t)kBisPStage * nstride * 2 * sizeof(double);
+    if (c.bisect_p && 128 / kw + 2 <= kBisPStage && smp <= 96 * 1024) {
+      e = cudaFuncSetAttribute(k_bisect_p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+      if (e != cudaSuccess) return e;
+      k_bisect_p<true><<<(unsigned)((total + 127) / 128), 128, smp, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh,
+                                                                                cnt, ev);
+    } else if (c.bisect_p) {
+      k_bisect_p<false><<<(unsigned)((total + 127) / 128), 128, 0, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh,
+                                                                                cnt, ev);
+    } else if (128 / kw + 2 <= kBisStage && sm <= 96 * 1024) {
       e = cudaFuncSetAttribute(k_bisect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
       k_bisect<true><<<(unsigned)((total + 127) / 128), 128, sm, c.stream>>>(nprob, kw, nstride, d_ns, dd, ee, gsh,

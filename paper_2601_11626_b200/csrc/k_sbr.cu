@@ -2209,7 +2209,13 @@ __global__ void __launch_bounds__(W * 32, W == kChaseWarps ? 1 : 2) k_sbr_chase(
                                                                     double* __restrict__ e2out,
                                                                     double* __restrict__ gsh,
                                                                     int* __restrict__ cnt_out,
-                                                                    double* __restrict__ ws, const SbrWs L, int nmax) {
+                                                                    double* __restrict__ ws, const SbrWs L, int nmax,
+                                                                    int joff, int jstop, int fin) {
+  // Two-phase use (256 < nmax <= 512, launch_tridiag_sbr): phase A (joff = 0, jstop = J = nmax - 256, fin = 0)
+  // runs sweeps 0 .. J - 1 on the full band, writes d, e^2 of rows < J and the trailing band with the fill its
+  // sweeps have left (rows >= J, diagonals 0 .. 2 kSB) back into the lower storage of G; phase B (joff = J, fin = 0) is the chase of that
+  // trailing (n - J) x (n - J) band matrix, which fits the half-band variant (two CTAs per SM); k_sbr_chase_fin
+  // follows.  One-phase use: joff = 0, jstop >= n, fin = 1.
   extern __shared__ __align__(16) double bsm[];
   const int nb = GB ? nmax : (W == kChaseWarps ? kSBMax : kSBMax / 2);
   double* Bd = GB ? ws + (int64_t)blockIdx.x * L.per + L.band : bsm;               // [n][kSBLdb]
@@ -2217,24 +2223,35 @@ __global__ void __launch_bounds__(W * 32, W == kChaseWarps ? 1 : 2) k_sbr_chase(
   volatile int* prog = reinterpret_cast<volatile int*>(sbase);                     // steps done per sweep
   double* vsc = sbase + nb / 2 + 2 + 32 * (threadIdx.x >> 5);                      // per-warp p scratch
   const int p = blockIdx.x;
-  const int n = ns[p];
+  int n = ns[p];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double* A = G + (int64_t)p * stride;
   double* dO = dout + (int64_t)p * nstride;
   double* eO = e2out + (int64_t)p * nstride;
   if (n <= 0) {
-    if (tid == 0) { cnt_out[p] = 0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; }
+    if (tid == 0 && fin) { cnt_out[p] = 0; gsh[4 * p] = 0; gsh[4 * p + 1] = 0; gsh[4 * p + 2] = 1e-300; gsh[4 * p + 3] = 1e-300; }
     return;
   }
+  if (joff > 0) {   // phase B: the trailing band matrix (phase A has finished problems with n - joff <= 2 itself)
+    if (n - joff <= 2) return;
+    A += (int64_t)joff * ld + joff;
+    dO += joff;
+    eO += joff;
+    n -= joff;
+  }
+  const int nsw = min(n - 2, jstop);   // sweeps run here (a complete reduction has n - 2)
+  // a sweep annihilates only the first column of each fill block: between sweeps the matrix carries the rest of
+  // the fill on diagonals kSB + 1 .. 2 kSB, so the hand-over between the phases is the band WITH its bulges
+  const int dmax = joff > 0 ? 2 * kSB : kSB;
   for (int e = tid; e < n * kSBLdb; e += blockDim.x) {
     const int jj = e / kSBLdb, d = e - jj * kSBLdb;
-    Bd[e] = (d <= kSB && jj + d < n) ? A[(int64_t)jj * ld + jj + d] : 0.0;
+    Bd[e] = (d <= dmax && jj + d < n) ? A[(int64_t)jj * ld + jj + d] : 0.0;
   }
   for (int e = tid; e < n; e += blockDim.x) prog[e] = 0;
   __syncthreads();
   if (FLAGS) {
   // sweeps j = wid, wid + W, ...; step s of sweep j waits until sweep j - 1 has completed step s + 2
-  for (int j = wid; j + 2 < n; j += W) {
+  for (int j = wid; j < nsw; j += W) {
     const int nsteps = (n - 3 - j) / kSB + 1;   // steps with a window of >= 2 rows
     for (int s = 0; s < nsteps; ++s) {
       if (j > 0) {
@@ -2258,12 +2275,13 @@ __global__ void __launch_bounds__(W * 32, W == kChaseWarps ? 1 : 2) k_sbr_chase(
   // time-stepped wavefront: task (j, s) runs at time 3 j + s, so that step s of sweep j follows step s + 2
   // of sweep j - 1 (their blocks are then disjoint); the tasks of one time step are independent and
   // spread over the warps, one CTA barrier per time step (no polling)
-  const int tmax = 3 * (n - 3);
+  const int jlast = nsw - 1;
+  const int tmax = jlast >= 0 ? 3 * jlast + (n - 3 - jlast) / kSB : -1;   // last step of the last sweep
 #ifdef CMSVD_CHASE_PROF
   long long ct0 = clock64();
 #endif
   for (int tt = 0; tt <= tmax; ++tt) {
-    const int jhi = min(tt / 3, n - 3);
+    const int jhi = min(tt / 3, jlast);
     for (int idx = wid;; idx += W) {
       const int j = jhi - idx;
       const int s = tt - 3 * j;
@@ -2280,10 +2298,20 @@ __global__ void __launch_bounds__(W * 32, W == kChaseWarps ? 1 : 2) k_sbr_chase(
   (void)prog;
   __syncthreads();
   // outputs (as k_tridiag): d, e^2, Gershgorin data, threshold count
-  for (int i = tid; i < n; i += blockDim.x) {
+  const bool partial = nsw < n - 2;
+  const int nout = partial ? nsw : n;
+  for (int i = tid; i < nout; i += blockDim.x) {
     dO[i] = Bd[i * kSBLdb];
     if (i + 1 < n) { const double e1 = Bd[i * kSBLdb + 1]; eO[i] = e1 * e1; }
   }
+  if (partial) {   // the trailing band back into the lower storage of G (phase B reads it from there)
+    double* Aw = const_cast<double*>(A);
+    for (int e = nsw * kSBLdb + tid; e < n * kSBLdb; e += blockDim.x) {
+      const int jj = e / kSBLdb, d = e - jj * kSBLdb;
+      if (d <= 2 * kSB && jj + d < n) Aw[(int64_t)jj * ld + jj + d] = Bd[e];
+    }
+  }
+  if (!fin) return;
   __syncthreads();
   if (tid == 0) {
     double glo = 1e300, ghi = -1e300, emax = 0.0;
@@ -2575,7 +2603,7 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     e = cudaFuncSetAttribute(k_sbr_chase<F_, GB_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);       \
     if (e != cudaSuccess) return e;                                                                               \
     k_sbr_chase<F_, GB_><<<nprob, kChaseWarps * 32, csmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride,  \
-                                                                        dd, ee, gsh, cnt, ws, L, nmax);           \
+                                                                        dd, ee, gsh, cnt, ws, L, nmax, 0, 1 << 30, 1); \
   } while (0)
   if (big) SBR_CHASE(false, true);
   else if (c.chase_flags) SBR_CHASE(true, false);
@@ -2585,7 +2613,22 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     e = cudaFuncSetAttribute(k_sbr_chase<false, false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
     if (e != cudaSuccess) return e;
     k_sbr_chase<false, false, 6><<<nprob, 6 * 32, hsmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd, ee,
-                                                                      gsh, cnt, ws, L, nmax);
+                                                                      gsh, cnt, ws, L, nmax, 0, 1 << 30, 1);
+  } else if (!c.chase2 && nmax <= kSBMax && c.chase_split) {
+    // 256 < n <= 512: sweeps 0 .. J - 1 on the full band (one CTA per SM), the trailing 256 x 256 band matrix
+    // with the half-band variant (two CTAs per SM), then the Gershgorin / threshold-count pass
+    const int J = nmax - kSBMax / 2;
+    const size_t hsmem = ((size_t)(kSBMax / 2) * kSBLdb + (size_t)kSBMax / 4 + 2 + 32 * 6) * sizeof(double);
+    e = cudaFuncSetAttribute(k_sbr_chase<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_sbr_chase<false, false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+    if (e != cudaSuccess) return e;
+    k_sbr_chase<false, false><<<nprob, kChaseWarps * 32, csmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd,
+                                                                             ee, gsh, cnt, ws, L, nmax, 0, J, 0);
+    k_sbr_chase<false, false, 6><<<nprob, 6 * 32, hsmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd, ee,
+                                                                      gsh, cnt, ws, L, nmax, J, 1 << 30, 0);
+    k_sbr_chase_fin<<<(nprob + 127) / 128, 128, 0, c.stream>>>(d_ns, d_thr, kw, nstride, dd, ee, gsh, cnt, nprob);
+    c.launches += 2;
   } else if (c.chase2) {
     const size_t c2smem = ((size_t)kCh2Cap * kSBLdb + 32 * kCh2Warps) * sizeof(double);
     e = cudaFuncSetAttribute(k_sbr_chase2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2smem);

@@ -80,14 +80,15 @@ def test_structured_spectra(cm):
 
 @pytest.mark.parametrize("knob", ["", "CMSVD_SBR_FUSED=1", "CMSVD_SYMM_DMMA=0", "CMSVD_SYR2K_DMMA=0", "CMSVD_SYR2K_ROW=0",
                                   "CMSVD_SYMM_DMMA=0,CMSVD_SYR2K_DMMA=0,CMSVD_SYR2K_ROW=1", "CMSVD_CHASE2=1",
-                                  "CMSVD_CHASE_FLAGS=1", "CMSVD_SBR_TMA=0", "CMSVD_SBR_PANEL_RR=0"])
+                                  "CMSVD_CHASE_FLAGS=1", "CMSVD_SBR_TMA=0", "CMSVD_SBR_PANEL_RR=0", "CMSVD_BISECT_P=0"])
 def test_band_reduction_variants(cm, knob, monkeypatch):
     """Every selectable path of the two-stage reduction agrees with LAPACK on ragged sizes (including the
     global-memory panel / band above 512): the default (stage 1 on the fp64 tensor cores: DMMA product and
     row-persistent DMMA update), the scalar product / update kernels, the one-tile-per-CTA and row-persistent
     scalar updates, the look-ahead fused pass, the chase with per-sweep flags or with two problems in flight
     per CTA over the circular band buffer, the non-TMA staging, and the shared-memory panel QR (the default
-    panel kernel keeps the panel in registers)."""
+    panel kernel keeps the panel in registers), and the pivot-form bisection with its fp32 coarse phase (the
+    default is the division-free polynomial recurrence)."""
     for kv in filter(None, knob.split(",")):
         k, v = kv.split("=")
         monkeypatch.setenv(k, v)
@@ -97,6 +98,21 @@ def test_band_reduction_variants(cm, knob, monkeypatch):
     with cm.Context(0) as ctx:
         ev, _ = ctx.sym_eigvals(mats, 160)
     check(ev, mats, 160)
+
+
+@pytest.mark.parametrize("split", ["1", "0"])
+def test_chase_split_boundaries(cm, split, monkeypatch):
+    """256 < nmax <= 512: the chase runs sweeps 0 .. nmax - 257 on the full band and hands the trailing band
+    matrix (written back into the lower storage) to the half-band kernel.  Sizes around the hand-over: problems
+    that phase A finishes alone (n - 2 <= J), a trailing matrix of 3 rows (one sweep), one window step more,
+    and the full size; nmax = 500 moves J off a multiple of the band width."""
+    monkeypatch.setenv("CMSVD_CHASE_SPLIT", split)
+    R = np.random.default_rng(47)
+    for sizes in ([512, 259, 258, 257, 260, 273, 274, 290, 511, 3, 2, 0], [500, 245, 246, 247, 248, 263, 499, 300]):
+        mats = [gram(R, n, decay=0.4) if n else np.zeros((0, 0)) for n in sizes]
+        with cm.Context(0) as ctx:
+            ev, tr = ctx.sym_eigvals(mats, 200)
+        check(ev, mats, 200)
 
 
 @pytest.mark.parametrize("groups", ["1", "3"])
