@@ -142,8 +142,8 @@ struct Ctx {
   bool chase2 = false;                 // band chase: two problems in flight per persistent CTA (CMSVD_CHASE2=1).  Measured 25.6 vs
                                        // 22.8 ms: the chase is bound by task throughput (~4.7 tasks/us/SM in both), not by latency
   bool chase_small = true;             // band chase, n <= 256: 6-warp CTAs with half the band, two per SM (CMSVD_CHASE_SMALL=0: off)
-  bool chase_split = true;             // band chase, 256 < n <= 512: sweeps 0 .. n - 257 on the full band, the trailing 256 x 256 band
-                                       // matrix with the half-band two-CTAs-per-SM variant (CMSVD_CHASE_SPLIT=0: one kernel)
+  bool chase_split = true;             // band chase, n <= 512: phases on ever smaller bands as the active part shrinks (512 / 384 /
+                                       // 256 / 128 rows: 1 / 2 / 2 / 4 CTAs per SM; CMSVD_CHASE_SPLIT=0: one kernel)
   bool chase_flags = false;            // band chase: per-sweep progress flags instead of time-step barriers
   int g_upper = 1;                     // core Grams of the band reduction: 1 = strict upper triangle not written, 0 = written,
                                        // 2 = poisoned with NaN (CMSVD_G_UPPER; the band reduction reads the lower storage only)

@@ -2201,8 +2201,9 @@ __global__ void __launch_bounds__(kCh2Warps * 32, 1) k_sbr_chase2(const double* 
 // GB: n > kSBMax, the band lives in the problem's global workspace (L.band) instead of shared memory
 // W: warps per CTA (12; 6 for n <= 256, where a time step has at most 6 tasks and the band takes half the
 // shared memory: two CTAs per SM)
-template <bool FLAGS, bool GB, int W = kChaseWarps>
-__global__ void __launch_bounds__(W * 32, W == kChaseWarps ? 1 : 2) k_sbr_chase(const double* __restrict__ G, int64_t ld,
+// W warps, band rows NB (shared memory): (12, 512) one CTA per SM, (8, 384) two, (6, 256) two, (3, 128) four
+template <bool FLAGS, bool GB, int W = kChaseWarps, int NB = kSBMax>
+__global__ void __launch_bounds__(W * 32, NB >= 512 ? 1 : (NB >= 384 ? 2 : (NB >= 256 ? 3 : 6))) k_sbr_chase(const double* __restrict__ G, int64_t ld,
                                                                     int64_t stride, const int* __restrict__ ns,
                                                                     const double* __restrict__ thr, int kw,
                                                                     int nstride, double* __restrict__ dout,
@@ -2217,7 +2218,7 @@ __global__ void __launch_bounds__(W * 32, W == kChaseWarps ? 1 : 2) k_sbr_chase(
   // trailing (n - J) x (n - J) band matrix, which fits the half-band variant (two CTAs per SM); k_sbr_chase_fin
   // follows.  One-phase use: joff = 0, jstop >= n, fin = 1.
   extern __shared__ __align__(16) double bsm[];
-  const int nb = GB ? nmax : (W == kChaseWarps ? kSBMax : kSBMax / 2);
+  const int nb = GB ? nmax : NB;
   double* Bd = GB ? ws + (int64_t)blockIdx.x * L.per + L.band : bsm;               // [n][kSBLdb]
   double* sbase = GB ? bsm : bsm + (int64_t)nb * kSBLdb;
   volatile int* prog = reinterpret_cast<volatile int*>(sbase);                     // steps done per sweep
@@ -2607,28 +2608,40 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   } while (0)
   if (big) SBR_CHASE(false, true);
   else if (c.chase_flags) SBR_CHASE(true, false);
-  else if (!c.chase2 && nmax <= kSBMax / 2 && c.chase_small) {
-    // n <= 256: six warps and half the band per CTA, two CTAs per SM
-    const size_t hsmem = ((size_t)(kSBMax / 2) * kSBLdb + (size_t)kSBMax / 4 + 2 + 32 * 6) * sizeof(double);
-    e = cudaFuncSetAttribute(k_sbr_chase<false, false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
-    if (e != cudaSuccess) return e;
-    k_sbr_chase<false, false, 6><<<nprob, 6 * 32, hsmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd, ee,
-                                                                      gsh, cnt, ws, L, nmax, 0, 1 << 30, 1);
-  } else if (!c.chase2 && nmax <= kSBMax && c.chase_split) {
-    // 256 < n <= 512: sweeps 0 .. J - 1 on the full band (one CTA per SM), the trailing 256 x 256 band matrix
-    // with the half-band variant (two CTAs per SM), then the Gershgorin / threshold-count pass
-    const int J = nmax - kSBMax / 2;
-    const size_t hsmem = ((size_t)(kSBMax / 2) * kSBLdb + (size_t)kSBMax / 4 + 2 + 32 * 6) * sizeof(double);
-    e = cudaFuncSetAttribute(k_sbr_chase<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_sbr_chase<false, false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
-    if (e != cudaSuccess) return e;
-    k_sbr_chase<false, false><<<nprob, kChaseWarps * 32, csmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd,
-                                                                             ee, gsh, cnt, ws, L, nmax, 0, J, 0);
-    k_sbr_chase<false, false, 6><<<nprob, 6 * 32, hsmem, c.stream>>>(G, ld, stride, d_ns, d_thr, kw, nstride, dd, ee,
-                                                                      gsh, cnt, ws, L, nmax, J, 1 << 30, 0);
-    k_sbr_chase_fin<<<(nprob + 127) / 128, 128, 0, c.stream>>>(d_ns, d_thr, kw, nstride, dd, ee, gsh, cnt, nprob);
-    c.launches += 2;
+  else if (!c.chase2 && (c.chase_split || (nmax <= kSBMax / 2 && c.chase_small))) {
+    // The chase is latency bound (a time step lasts one task, ~1.1 us, whatever the number of tasks), and its
+    // shared memory (the band with its fill, 34 diagonals) decides how many problems an SM holds.  The active
+    // part of the matrix shrinks by one row per sweep, so the reduction is cut into phases that run on ever
+    // smaller bands: active size <= 512 one CTA per SM, <= 384 two, <= 256 two (registers), <= 128 four; a
+    // phase writes d, e^2 of its finished rows and hands the trailing band with its fill through the lower
+    // storage of G to the next one; k_sbr_chase_fin (Gershgorin data, threshold count) follows.
+    // CMSVD_CHASE_SPLIT=0: one kernel (the half-band one for n <= 256).
+    int cur = 0, nph = 0;
+#define SBR_PHASE(W_, NB_, JSTOP_, FIN_)                                                                           \
+  do {                                                                                                             \
+    const size_t sm_ = ((size_t)(NB_) * kSBLdb + (size_t)(NB_) / 2 + 2 + 32 * (W_)) * sizeof(double);              \
+    e = cudaFuncSetAttribute(k_sbr_chase<false, false, W_, NB_>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                             (int)sm_);                                                                            \
+    if (e != cudaSuccess) return e;                                                                                \
+    k_sbr_chase<false, false, W_, NB_><<<nprob, (W_) * 32, sm_, c.stream>>>(G, ld, stride, d_ns, d_thr, kw,        \
+                                                                            nstride, dd, ee, gsh, cnt, ws, L,      \
+                                                                            nmax, cur, JSTOP_, FIN_);              \
+    ++nph;                                                                                                         \
+  } while (0)
+    if (!c.chase_split) {
+      SBR_PHASE(6, 256, 1 << 30, 1);
+    } else {
+      while (true) {
+        const int a = nmax - cur;   // largest active size
+        if (a > 384) { SBR_PHASE(12, 512, a - 384, 0); cur += a - 384; }
+        else if (a > 256) { SBR_PHASE(8, 384, a - 256, 0); cur += a - 256; }
+        else if (a > 128) { SBR_PHASE(6, 256, a - 128, 0); cur += a - 128; }
+        else { SBR_PHASE(3, 128, 1 << 30, 0); break; }
+      }
+      k_sbr_chase_fin<<<(nprob + 127) / 128, 128, 0, c.stream>>>(d_ns, d_thr, kw, nstride, dd, ee, gsh, cnt, nprob);
+    }
+#undef SBR_PHASE
+    c.launches += nph - (c.chase_split ? 0 : 1);
   } else if (c.chase2) {
     const size_t c2smem = ((size_t)kCh2Cap * kSBLdb + 32 * kCh2Warps) * sizeof(double);
     e = cudaFuncSetAttribute(k_sbr_chase2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2smem);
