@@ -241,15 +241,18 @@ __global__ void __launch_bounds__(kPanelThreads) k_sbr_panel(double* __restrict_
 //      P[i][c] -= s_c scale x_i (i > k), P[k][c] -= s_c, P[k][k] = beta
 // The Householder vectors stay unscaled in the registers (v = scale x below the diagonal) until V is written.
 // ---------------------------------------------------------------------------
-constexpr int kP3Warps = kPanelThreads / 32;
-constexpr int kP3Smem = (2 * kP3Warps * 16 + 2 * 16 + 2 * kSB + 2 * kSB * kSB) * (int)sizeof(double);
+// NT threads own rows tid and tid + NT: 256 threads for panels of up to 512 rows, 128 for up to 256, 64 for up to
+// 128 (half / a quarter of the warps and of the reduction's instructions, twice / four times the CTAs per SM)
+constexpr int kP3Smem = (2 * (kPanelThreads / 32) * 16 + 2 * 16 + 2 * kSB + 2 * kSB * kSB) * (int)sizeof(double);
 
-__global__ void __launch_bounds__(kPanelThreads, 2) k_sbr_panel3(double* __restrict__ G, int64_t ld, int64_t stride,
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_sbr_panel3(double* __restrict__ G, int64_t ld, int64_t stride,
                                                                  const int* __restrict__ ns, int t,
                                                                  double* __restrict__ ws, double* __restrict__ trace,
                                                                  const SbrWs L, int par) {
   extern __shared__ __align__(16) double psm[];
   double* wtot = psm;                       // [2][8 warps][16]
+  constexpr int kP3Warps = NT / 32;
   double* rowk = wtot + 2 * kP3Warps * 16;  // [2][16] row k of the panel (published by its owner)
   double* scal = rowk + 2 * 16;             // tau per column
   double* scl = scal + kSB;                 // scale per column
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(kPanelThreads, 2) k_sbr_panel3(double* __restr
   if (t >= sbr_panels(n)) return;
   const int c0 = t * kSB, R0 = c0 + kSB, np = n - R0;
   const int kmax = min(kSB, np);
-  const int r0 = tid, r1 = tid + kPanelThreads;
+  const int r0 = tid, r1 = tid + NT;
   double p0[kSB], p1[kSB];
 #pragma unroll
   for (int c = 0; c < kSB; ++c) {
@@ -276,8 +279,9 @@ __global__ void __launch_bounds__(kPanelThreads, 2) k_sbr_panel3(double* __restr
     p0[c] = r0 < np ? col[r0] : 0.0;
     p1[c] = r1 < np ? col[r1] : 0.0;
   }
-  S[tid] = 0.0;
+  for (int i = tid; i < kSB * kSB; i += NT) S[i] = 0.0;
   if (tid < kSB) { scal[tid] = 0.0; scl[tid] = 0.0; }
+  __syncthreads();
   const int lc = lane & 15;
   const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
 #pragma unroll
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(kPanelThreads, 2) k_sbr_panel3(double* __restr
       double* rk = rowk + (k & 1) * 16;
       // 1. partial dots of x (rows > k of column k) with every column, reduced over the warp
       const double x0 = r0 > k ? p0[k] : 0.0;
-      const double x1 = p1[k];                 // r1 >= 256 > k; zero beyond np
+      const double x1 = p1[k];                 // r1 >= NT > k; zero beyond np
       double v[16];
 #pragma unroll
       for (int c = 0; c < kSB; ++c) v[c] = fma(x1, p1[c], x0 * p0[c]);
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(kPanelThreads, 2) k_sbr_panel3(double* __restr
   // are zero already; zero columns from kmax on)
   double* Vw = L.vp(ws, p, par);
   double* Tw = Vw + 2 * L.vsz();
-  Tw[tid] = T[tid];
+  for (int i = tid; i < kSB * kSB; i += NT) Tw[i] = T[i];
   const int zend = t < 2 ? L.ldv : min(L.ldv, np + 2 * kSB);
 #pragma unroll
   for (int c = 0; c < kSB; ++c) {
@@ -385,6 +389,7 @@ __global__ void __launch_bounds__(kPanelThreads, 2) k_sbr_panel3(double* __restr
     double* vw = Vw + (int64_t)c * L.ldv;
     if (r0 < zend) vw[r0] = (c < kmax && r0 < np) ? (r0 > c ? sc * p0[c] : (r0 == c ? 1.0 : 0.0)) : 0.0;
     if (r1 < zend) vw[r1] = (c < kmax && r1 < np) ? sc * p1[c] : 0.0;
+    for (int i = 2 * NT + tid; i < zend; i += NT) vw[i] = 0.0;   // rows beyond this layout (np <= 2 NT): zero
   }
 }
 
@@ -2501,8 +2506,7 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
   }
   cudaError_t e = cudaFuncSetAttribute(k_sbr_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_sbr_panel3, cudaFuncAttributeMaxDynamicSharedMemorySize, kP3Smem);
-  if (e != cudaSuccess) return e;
+
   e = cudaFuncSetAttribute(k_sbr_symm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)symm_smem);
   if (e != cudaSuccess) return e;
   auto panel = [&](int t) {
@@ -2510,8 +2514,12 @@ cudaError_t launch_tridiag_sbr(Ctx& c, double* G, int64_t ld, int64_t stride, co
     if (big)
       k_sbr_panel<false><<<nprob, kPanelThreads, (256 + 2 * kSB + 2 * kSB * kSB) * sizeof(double), c.stream>>>(
           G, ld, stride, d_ns, t, ws, trace, L, t & 1);
-    else if (c.sbr_panel_rr)
-      k_sbr_panel3<<<nprob, kPanelThreads, kP3Smem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L, t & 1);
+    else if (c.sbr_panel_rr) {
+      const int np0 = nmax - (t + 1) * kSB;   // largest panel height of this launch
+      if (np0 > 256) k_sbr_panel3<256><<<nprob, 256, kP3Smem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L, t & 1);
+      else if (np0 > 128) k_sbr_panel3<128><<<nprob, 128, kP3Smem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L, t & 1);
+      else k_sbr_panel3<64><<<nprob, 64, kP3Smem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L, t & 1);
+    }
     else
       k_sbr_panel<true><<<nprob, kPanelThreads, psmem, c.stream>>>(G, ld, stride, d_ns, t, ws, trace, L, t & 1);
     c.launches += 1;
