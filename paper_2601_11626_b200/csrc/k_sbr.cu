@@ -553,15 +553,22 @@ __global__ void __launch_bounds__(256) k_sbr_w(const int* __restrict__ ns, int t
     Zs[tid] = 0.5 * z;
   }
   __syncthreads();
+  // thread (i, h): row I0 + i, columns 8 h .. 8 h + 7; the row of V is loaded once into registers
   const int imax = min(kSymmRows, np - I0);
-  for (int e = tid; e < kSymmRows * kSB; e += 256) {
-    const int c = e >> 7, i = e & 127;
-    if (i >= imax) continue;
-    const int64_t gi = I0 + i;
-    double w = Yw[(int64_t)c * L.ldv + gi];
+  const int i = tid & 127, h = tid >> 7;
+  if (i >= imax) return;
+  const int64_t gi = I0 + i;
+  double v[kSB], y[8];
 #pragma unroll
-    for (int l = 0; l < kSB; ++l) w = fma(-Vw[(int64_t)l * L.ldv + gi], Zs[l * kSB + c], w);
-    Yw[(int64_t)c * L.ldv + gi] = w;
+  for (int l = 0; l < kSB; ++l) v[l] = Vw[(int64_t)l * L.ldv + gi];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) y[c] = Yw[(int64_t)(8 * h + c) * L.ldv + gi];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    double w = y[c];
+#pragma unroll
+    for (int l = 0; l < kSB; ++l) w = fma(-v[l], Zs[l * kSB + 8 * h + c], w);
+    Yw[(int64_t)(8 * h + c) * L.ldv + gi] = w;
   }
 }
 
