@@ -319,3 +319,23 @@ def _c2_spectra():
     if "sp" not in _C2:
         _C2["sp"] = oracle.block_spectra(synth.config2().blocks)
     return _C2["sp"]
+
+
+def _axis_keys():
+    import axis_example as ax
+    return sorted(ax.RUNS)
+
+
+@pytest.mark.parametrize("key", _axis_keys())
+def test_hand_traced_greedy_run(cm, key):
+    """The hand-traced axis-aligned run of tests/axis_example.py (ragged widths 1-2, m = 6): compositions,
+    append orders, number of tentative evaluations and certificates, against values derived by hand
+    (not the oracle's output); fp32 inputs, so the integers hold to ~1e-6 of the cluster energy."""
+    import axis_example as ax
+    alg, sort, eps, knn = key
+    clusters, err2, total, evals = ax.RUNS[key]
+    g = run_gpu(cm, ax.blocks(np.float32), ax.R, alg, eps, sort, knn=knn)
+    assert [list(c) for c in g["clusters"]] == clusters
+    assert g["n_evals"] == len(evals)
+    assert np.allclose(g["total"], total, rtol=1e-6)
+    assert np.allclose(g["err2"], err2, rtol=0, atol=1e-5 * max(total))

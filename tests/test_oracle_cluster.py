@@ -130,3 +130,30 @@ def test_sequence_errors_pins():
         if len(seq) == 1:
             tail = float(np.sum(sp.sig[seq[0]][r:] ** 2))
             assert np.allclose(e2[s], tail, rtol=1e-9, atol=1e-9 * tot[s])
+
+
+def _axis_runs():
+    import axis_example as ax
+    return ax, sorted(ax.RUNS)
+
+
+@pytest.mark.parametrize("key", _axis_runs()[1])
+def test_hand_traced_greedy_run(key):
+    """Exact compositions, append orders, certificates and every tentative evaluation of Algs 2-3 on the
+    axis-aligned collection of tests/axis_example.py, whose run is traced by hand there (candidate order
+    of both sort modes, stop on the first rejection, the kNN window, the commit's truncation, and the
+    point where Alg. 2 and Alg. 3 part)."""
+    ax, _ = _axis_runs()
+    alg, sort, eps, knn = key
+    clusters, err2, total, evals = ax.RUNS[key]
+    sp = oracle.block_spectra(ax.blocks())
+    res = oc.cluster(sp, alg, ax.R, eps, sort, knn)
+    assert res.clusters == clusters
+    check_cover(res, 5)
+    assert np.allclose(res.total, total, rtol=1e-12)
+    assert np.allclose(res.err2, err2, rtol=0, atol=1e-10)
+    assert res.n_evals == len(evals)
+    got = [(c, b, e2, tot, ok) for (c, b, _, e2, tot, ok) in res.decisions]
+    for g, e in zip(got, evals):
+        assert g[0] == e[0] and g[1] == e[1] and g[4] == e[4], (g, e)
+        assert abs(g[2] - e[2]) <= 1e-10 and abs(g[3] - e[3]) <= 1e-10, (g, e)
