@@ -15,9 +15,9 @@ the SURVEY.md §8(c) readings (A1..A21) and DESIGN.md's A22, restated in DESIGN.
 
 Pins: tests/test_oracle_pins.py, tests/test_oracle_big_pins.py and
 tests/test_oracle_cluster.py (closed forms, LAPACK cross-checks, brute force,
-invariants).  Parity unpinned: the exact cluster compositions
-of greedy runs on synthetic data are bound only by the certified-error
-property (P12) and decision replay.
+invariants, and a greedy run traced by hand: tests/axis_example.py fixes the
+exact compositions, append orders and every tentative evaluation of Algs 2-3).
+No function here is left without a pin.
 """
 from __future__ import annotations
 
