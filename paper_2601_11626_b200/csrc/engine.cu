@@ -403,9 +403,16 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
            "spectra: guard gather");
         CK((gemm_mixed<double, false>(c, nb, n, kc, s, Z, n, ns_, Wg, s, (int64_t)s * kc, BW, n, (int64_t)n * kc)),
            "spectra: guard A^T U");
-        CK((gemm_mixed<float, false>(c, nb, (int)m, kc, n, nullptr, m, 0, BW, n, (int64_t)n * kc, Pm, m,
-                                     (int64_t)m * kc, 1.0, dA)),
-           "spectra: guard A A^T U");
+        if (wsp && (kc & 3) == 0) {
+          // on the TMA-fed tcgen05 kernel like the power steps (3xTF32: ~1e-7 relative, the guard resolves 1e-4)
+          CK(launch_split_planes64(c, BW, (int64_t)n * kc, nb, Zp), "spectra: guard planes");
+          CK(launch_gemm_ws_tn64(c, nb, (int)m, kc, n, ATp, Zp, false, Pm, m, (int64_t)m * kc),
+             "spectra: guard A A^T U (ws)");
+        } else {
+          CK((gemm_mixed<float, false>(c, nb, (int)m, kc, n, nullptr, m, 0, BW, n, (int64_t)n * kc, Pm, m,
+                                       (int64_t)m * kc, 1.0, dA)),
+             "spectra: guard A A^T U");
+        }
         CK(launch_ritz_resid(c, nb, m, s, kc, Pm, (const double*)c.ws[WS_EV].p, (const float* const*)dU,
                              (double*)(st + 2 * nb)),
            "spectra: guard residual");

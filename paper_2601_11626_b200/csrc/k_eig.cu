@@ -99,6 +99,9 @@ __device__ __forceinline__ void sturm2(const T* __restrict__ d, const T* __restr
 #define CMSVD_TRI_WARPS 8
 #endif
 constexpr int kTriWarps = CMSVD_TRI_WARPS;
+#ifndef CMSVD_QL_BATCH
+#define CMSVD_QL_BATCH 16   // columns of Z per load batch of the in-place QL rotation sweep (k_syev_ql<true>)
+#endif
 constexpr int kTriThreads = 32 * kTriWarps;
 constexpr int kTriMax = 512;      // up to 16 row chunks of 32 lanes (n > 160: matrix in global memory)
 constexpr int kEigSmemMax = 160;  // largest n staged entirely in shared memory
@@ -1512,7 +1515,7 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
                                                             double* __restrict__ Vws, int64_t stride_v,
                                                             double* __restrict__ VHws, double* __restrict__ evals,
                                                             int* __restrict__ perm, int64_t stride_out,
-                                                            int* __restrict__ status, int max_iter) {
+                                                            int* __restrict__ status, int max_iter, int col_bt) {
   extern __shared__ double sm[];
   const int p = blockIdx.x;
   const int n = ns[p];
@@ -1662,29 +1665,39 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
       const int lo_i = s_l;
       // apply rotations i = m-1 .. lo_i to columns (i, i+1) of Z: each thread owns rows
       if (GL) {
-        for (int row = tid; row < n; row += kTriThreads) {
-          double* z = A + row;
-          // the rotated column i is carried in a register to the next rotation; the original values of
-          // the next 8 columns are loaded ahead in one batch (every load precedes the stores that follow
-          // it), which hides the global-memory latency of the in-place (n > 160) variant
-          double f = z[(int64_t)m * ldz];
+        // a thread rotates two rows (tid, tid + kTriThreads) at once: the rotated column i of each row is
+        // carried in a register to the next rotation; the original values of the next kQB columns of both rows
+        // are loaded ahead in one batch (every load precedes the stores that follow it) -- 2 kQB loads in
+        // flight per thread hide the global-memory latency of the in-place (n > 160) variant
+        constexpr int kQB = CMSVD_QL_BATCH;
+        for (int row = tid; row < n; row += 2 * kTriThreads) {
+          const bool two = row + kTriThreads < n;
+          double* za = A + row;
+          double* zb = A + (two ? row + kTriThreads : row);
+          double fa = za[(int64_t)m * ldz], fb = zb[(int64_t)m * ldz];
           int i = m - 1;
           while (i >= lo_i) {
-            const int cnt = min(8, i - lo_i + 1);
-            double zc[8];
+            const int cnt = min(kQB, i - lo_i + 1);
+            double ca[kQB], cb[kQB];
   #pragma unroll
-            for (int t = 0; t < 8; ++t) zc[t] = (t < cnt) ? z[(int64_t)(i - t) * ldz] : 0.0;
+            for (int t = 0; t < kQB; ++t) {
+              ca[t] = (t < cnt) ? za[(int64_t)(i - t) * ldz] : 0.0;
+              cb[t] = (t < cnt) ? zb[(int64_t)(i - t) * ldz] : 0.0;
+            }
   #pragma unroll
-            for (int t = 0; t < 8; ++t)
+            for (int t = 0; t < kQB; ++t)
               if (t < cnt) {
                 const int ii = i - t;
                 const double c_ = rc[ii], s_ = rs[ii];
-                z[(int64_t)(ii + 1) * ldz] = s_ * zc[t] + c_ * f;
-                f = c_ * zc[t] - s_ * f;
+                za[(int64_t)(ii + 1) * ldz] = s_ * ca[t] + c_ * fa;
+                fa = c_ * ca[t] - s_ * fa;
+                if (two) zb[(int64_t)(ii + 1) * ldz] = s_ * cb[t] + c_ * fb;
+                fb = c_ * cb[t] - s_ * fb;
               }
             i -= cnt;
           }
-          z[(int64_t)lo_i * ldz] = f;
+          za[(int64_t)lo_i * ldz] = fa;
+          if (two) zb[(int64_t)lo_i * ldz] = fb;
         }
       } else {
         for (int row = tid; row < n; row += kTriThreads) {
@@ -1712,7 +1725,64 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
   unsigned long long t2 = clock64();
 #endif
   // ---- back-transformation Z <- H_0 H_1 ... H_{n-3} Z ----
-  // shared memory: thread per column; global memory (GL): warp per column, lanes over rows (coalesced)
+  // shared memory: thread per column; global memory (GL): a warp keeps two columns of Z in registers (row
+  // 32 t + lane in slot t) and applies every reflector to them -- Z is read and written once instead of once
+  // per reflector (2 GB of L2 / DRAM traffic per 512 x 512 problem), no barrier between reflectors; the
+  // reflector vectors are shared by the CTA's warps through L1, the next one is loaded ahead
+  if (GL && col_bt) {
+    for (int c0 = wid; c0 < n; c0 += 2 * kTriWarps) {
+      const int c1 = c0 + kTriWarps;
+      const bool two = c1 < n;
+      double* za = A + (int64_t)c0 * ldz;
+      double* zb = A + (int64_t)(two ? c1 : c0) * ldz;
+      double z0[16], z1[16], vr[16], vn[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int j = 32 * t + lane;
+        z0[t] = j < n ? za[j] : 0.0;
+        z1[t] = j < n ? zb[j] : 0.0;
+        vn[t] = 0.0;
+      }
+      auto loadv = [&](int k) {
+        const double* v = VH + (int64_t)k * n;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const int j = 32 * t + lane;
+          vn[t] = (32 * t + 31 > k && j > k && j < n) ? v[j] : 0.0;
+        }
+      };
+      if (n >= 3) loadv(n - 3);
+      for (int k = n - 3; k >= 0; --k) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) vr[t] = vn[t];
+        if (k > 0) loadv(k - 1);
+        const double tk = tauH[k];
+        if (tk == 0.0) continue;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          d0 = fma(vr[t], z0[t], d0);
+          d1 = fma(vr[t], z1[t], d1);
+        }
+        d0 = warp_sum(d0) * tk;
+        d1 = warp_sum(d1) * tk;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          z0[t] = fma(-d0, vr[t], z0[t]);
+          z1[t] = fma(-d1, vr[t], z1[t]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int j = 32 * t + lane;
+        if (j < n) {
+          za[j] = z0[t];
+          if (two) zb[j] = z1[t];
+        }
+      }
+    }
+    __syncthreads();
+  } else
   for (int k = n - 3; k >= 0; --k) {
     const double tk = tauH[k];
     if (tk != 0.0) {
@@ -1772,10 +1842,12 @@ cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_i
     cudaError_t e = cudaFuncSetAttribute(k_syev_ql<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_syev_ql<false><<<nprob, kTriThreads, smem, c.stream>>>(G, ld_in, stride_in, d_ns, Vws, stride_v, VHws, evals,
-                                                             perm, stride_out, status, 60);
+                                                             perm, stride_out, status, 60, 0);
     c.launches += 1;
     return cudaGetLastError();
   }
+  // CMSVD_SYEV_COLBT=0: the per-reflector back-transformation (one pass over Z per reflector)
+  static const int col_bt = [] { const char* e = getenv("CMSVD_SYEV_COLBT"); return (e && e[0] == '0') ? 0 : 1; }();
   // in place in global memory (G is destroyed); batches sized to stay L2-resident
   cudaError_t e = cudaFuncSetAttribute(k_syev_ql<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -1785,7 +1857,8 @@ cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_i
     k_syev_ql<true><<<nb, kTriThreads, smem, c.stream>>>(G + (int64_t)p0 * stride_in, ld_in, stride_in, d_ns + p0,
                                                          Vws + (int64_t)p0 * stride_v, stride_v,
                                                          VHws + (int64_t)p0 * stride_v, evals + (int64_t)p0 * stride_out,
-                                                         perm + (int64_t)p0 * stride_out, stride_out, status + p0, 60);
+                                                         perm + (int64_t)p0 * stride_out, stride_out, status + p0, 60,
+                                                         col_bt);
     c.launches += 1;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
