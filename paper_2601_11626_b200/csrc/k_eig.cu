@@ -1499,6 +1499,69 @@ __global__ void __launch_bounds__(128) k_multisect(int P, int kw, int nstride, c
   if (lane == 0) *out = 0.5 * (lo + hi);
 }
 
+// One implicit QL sweep (tql2, Wilkinson-type shift) on the unreduced block l .. m of the tridiagonal (dd, ee):
+// the rotations i = m-1 .. lo are left in rc[i], rs[i]; returns lo, the lowest rotation index generated (l, or
+// the stop index + 1 after an underflow).  Sequential: one thread.
+__device__ __forceinline__ int ql_sweep(double* __restrict__ dd, double* __restrict__ ee, int l, int m,
+                                        double* __restrict__ rc, double* __restrict__ rs) {
+  double g = (dd[l + 1] - dd[l]) / (2.0 * ee[l]);
+  double r = hypot(g, 1.0);
+  g = dd[m] - dd[l] + ee[l] / (g + copysign(r, g));
+  double sn = 1.0, cs = 1.0, pp = 0.0;
+  int i = m - 1;
+  bool underflow = false;
+  // every d/e value read below is an original one (the sweep writes ee[i+1], dd[i+1] behind the
+  // read front), so the next iteration's operands are prefetched into registers
+  double e_i = ee[i], d_i1 = dd[i + 1], d_i = dd[i];
+  for (; i >= l; --i) {
+    const double e_n = (i > l) ? ee[i - 1] : 0.0;
+    const double d_n = (i > l) ? dd[i - 1] : 0.0;
+    double f = sn * e_i;
+    const double b = cs * e_i;
+    // r = hypot(f, g), sn = f / r, cs = g / r: one MUFU.RSQ64H + a cubic step instead of the
+    // IEEE hypot and two divisions on this sequential chain; scaled fallback near under/overflow
+    const double x2 = fma(f, f, g * g);
+    const double gq = d_i1 - pp;
+    if (x2 > 1e-280 && x2 < 1e280) {
+      // (d_i - gq) sn + 2 cs b = y ((d_i - gq) f + 2 g b): the bracket is formed while the
+      // reciprocal square root is in flight, so one multiply follows it on the chain
+      const double T = fma(d_i - gq, f, 2.0 * g * b);
+      const double y = rsqrt_cubic(x2);
+      ee[i + 1] = x2 * y;
+      sn = f * y;
+      cs = g * y;
+      r = T * y;
+    } else {
+      r = hypot(f, g);
+      ee[i + 1] = r;
+      if (r == 0.0) {
+        dd[i + 1] = gq;
+        ee[m] = 0.0;
+        underflow = true;
+        break;
+      }
+      sn = f / r;
+      cs = g / r;
+      r = (d_i - gq) * sn + 2.0 * cs * b;
+    }
+    pp = sn * r;
+    dd[i + 1] = gq + pp;
+    g = cs * r - b;
+    rc[i] = cs;
+    rs[i] = sn;
+    e_i = e_n;
+    d_i1 = d_i;
+    d_i = d_n;
+  }
+  // rotations actually generated: indices i_stop+1 .. m-1 (i_stop = i)
+  if (!underflow) {
+    dd[l] -= pp;
+    ee[l] = g;
+    ee[m] = 0.0;
+  }
+  return underflow ? i + 1 : l;
+}
+
 // ---------------------------------------------------------------------------
 // Symmetric eigen-decomposition with vectors (block spectra S2, cluster-state
 // commits S10): the tridiagonal reduction above with the reflectors saved,
@@ -1515,7 +1578,7 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
                                                             double* __restrict__ Vws, int64_t stride_v,
                                                             double* __restrict__ VHws, double* __restrict__ evals,
                                                             int* __restrict__ perm, int64_t stride_out,
-                                                            int* __restrict__ status, int max_iter, int col_bt) {
+                                                            int* __restrict__ status, int max_iter, int flags) {
   extern __shared__ double sm[];
   const int p = blockIdx.x;
   const int n = ns[p];
@@ -1576,6 +1639,99 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
   // deflate when |e_m| <= eps (|d_m| + |d_m+1|) or |e_m| <= 8 eps ||T|| (absolute accuracy ~ eps ||T||,
   // the same as the reduction's backward error; needed when both neighbours are ~0)
   const double defl_abs = 8.0 * 2.220446049250313e-16 * s_anorm;
+  if (GL && (flags & 2)) {
+    // Fused sweeps (in-place variant): warp 0 runs the QL iteration on (dd, ee) alone -- the rotations do not
+    // depend on Z -- and leaves up to kQF consecutive sweeps in tables padded with identity rotations over
+    // the union range [L, H]; every thread then passes its two rows of Z ONCE through the kQF rotation stages
+    // (sweep k trails sweep k-1 by one column: the value leaving stage k-1 at column i+k is what stage k
+    // rotates next; an identity stage is a one-column delay), so Z is read and written once per kQF sweeps.
+    // Per element the same rotations in the same order as the sweep-by-sweep loop below.
+    constexpr int kQF = 4, kQB = CMSVD_QL_BATCH;
+    const int tl = n + 2 * kQF;                 // table row: index kQF + i for rotation i in [-kQF, n + kQF)
+    double* __restrict__ tc = vA;               // kQF rows of cosines, then kQF rows of sines (vA .. e2 are dead)
+    double* __restrict__ ts = vA + kQF * tl;
+    __shared__ int s_cnt, s_L, s_H, s_lcur, s_itcur;
+    if (tid == 0) { s_lcur = 0; s_itcur = 0; }
+    for (;;) {
+      for (int e = tid; e < kQF * tl; e += kTriThreads) { tc[e] = 1.0; ts[e] = 0.0; }
+      __syncthreads();
+      if (wid == 0) {
+        int l = s_lcur, iter = s_itcur, cnt = 0, L = n, H = -1, fail = 0, its = 0;
+        while (cnt < kQF && l < n) {
+          int mq = n - 1;
+          for (int base = l; base < n - 1; base += 32) {
+            const int mm = base + lane;
+            bool neg = false;
+            if (mm < n - 1) {
+              const double dsum = fabs(dd[mm]) + fabs(dd[mm + 1]);
+              neg = fabs(ee[mm]) <= 2.220446049250313e-16 * dsum || fabs(ee[mm]) <= defl_abs;
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, neg);
+            if (bal) { mq = base + __ffs(bal) - 1; break; }
+          }
+          if (mq == l) { ++l; iter = 0; continue; }
+          if (iter >= max_iter) { fail = 1; break; }
+          int lo = 0;
+          if (lane == 0) lo = ql_sweep(dd, ee, l, mq, tc + cnt * tl + kQF, ts + cnt * tl + kQF);
+          lo = __shfl_sync(0xffffffffu, lo, 0);
+          __syncwarp();
+          L = min(L, lo);
+          H = max(H, mq);
+          ++cnt; ++iter; ++its;
+        }
+        if (lane == 0) {
+          s_cnt = cnt; s_L = L; s_H = H; s_lcur = l; s_itcur = iter;
+          s_iters += its;
+          if (fail) s_fail = 1;
+        }
+      }
+      __syncthreads();
+      if (s_fail || s_cnt == 0) break;
+      const int L = s_L, H = s_H;
+      for (int row = tid; row < n; row += 2 * kTriThreads) {
+        const bool two = row + kTriThreads < n;
+        double* za = A + row;
+        double* zb = A + (two ? row + kTriThreads : row);
+        double fa[kQF], fb[kQF];
+#pragma unroll
+        for (int k = 0; k < kQF; ++k) fa[k] = fb[k] = 0.0;
+        int i0 = H;
+        while (i0 >= L - kQF) {
+          const int nb = min(kQB, i0 - (L - kQF) + 1);
+          double ca[kQB], cb[kQB];
+#pragma unroll
+          for (int t = 0; t < kQB; ++t) {
+            const bool ld = t < nb && i0 - t >= L;
+            ca[t] = ld ? za[(int64_t)(i0 - t) * ldz] : 0.0;
+            cb[t] = ld ? zb[(int64_t)(i0 - t) * ldz] : 0.0;
+          }
+#pragma unroll
+          for (int t = 0; t < kQB; ++t)
+            if (t < nb) {
+              const int ii = i0 - t;
+              double va = ca[t], vb = cb[t];
+#pragma unroll
+              for (int k = 0; k < kQF; ++k) {
+                const double c_ = tc[k * tl + kQF + ii + k], s_ = ts[k * tl + kQF + ii + k];
+                const double oa = s_ * va + c_ * fa[k];
+                fa[k] = c_ * va - s_ * fa[k];
+                va = oa;
+                const double ob = s_ * vb + c_ * fb[k];
+                fb[k] = c_ * vb - s_ * fb[k];
+                vb = ob;
+              }
+              const int io = ii + kQF;
+              if (io >= L && io <= H) {
+                za[(int64_t)io * ldz] = va;
+                if (two) zb[(int64_t)io * ldz] = vb;
+              }
+            }
+          i0 -= nb;
+        }
+      }
+      __syncthreads();
+    }
+  } else
   for (int l = 0; l < n; ++l) {
     int iter = 0;
     while (true) {
@@ -1599,62 +1755,7 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
         if (m != l) {
           if (iter >= max_iter) { s_fail = 1; s_m = l; }
           else {
-            double g = (dd[l + 1] - dd[l]) / (2.0 * ee[l]);
-            double r = hypot(g, 1.0);
-            g = dd[m] - dd[l] + ee[l] / (g + copysign(r, g));
-            double sn = 1.0, cs = 1.0, pp = 0.0;
-            int i = m - 1;
-            bool underflow = false;
-            // every d/e value read below is an original one (the sweep writes ee[i+1], dd[i+1] behind the
-            // read front), so the next iteration's operands are prefetched into registers
-            double e_i = ee[i], d_i1 = dd[i + 1], d_i = dd[i];
-            for (; i >= l; --i) {
-              const double e_n = (i > l) ? ee[i - 1] : 0.0;
-              const double d_n = (i > l) ? dd[i - 1] : 0.0;
-              double f = sn * e_i;
-              const double b = cs * e_i;
-              // r = hypot(f, g), sn = f / r, cs = g / r: one MUFU.RSQ64H + a cubic step instead of the
-              // IEEE hypot and two divisions on this sequential chain; scaled fallback near under/overflow
-              const double x2 = fma(f, f, g * g);
-              const double gq = d_i1 - pp;
-              if (x2 > 1e-280 && x2 < 1e280) {
-                // (d_i - gq) sn + 2 cs b = y ((d_i - gq) f + 2 g b): the bracket is formed while the
-                // reciprocal square root is in flight, so one multiply follows it on the chain
-                const double T = fma(d_i - gq, f, 2.0 * g * b);
-                const double y = rsqrt_cubic(x2);
-                ee[i + 1] = x2 * y;
-                sn = f * y;
-                cs = g * y;
-                r = T * y;
-              } else {
-                r = hypot(f, g);
-                ee[i + 1] = r;
-                if (r == 0.0) {
-                  dd[i + 1] = gq;
-                  ee[m] = 0.0;
-                  underflow = true;
-                  break;
-                }
-                sn = f / r;
-                cs = g / r;
-                r = (d_i - gq) * sn + 2.0 * cs * b;
-              }
-              pp = sn * r;
-              dd[i + 1] = gq + pp;
-              g = cs * r - b;
-              rc[i] = cs;
-              rs[i] = sn;
-              e_i = e_n;
-              d_i1 = d_i;
-              d_i = d_n;
-            }
-            // rotations actually generated: indices i_stop+1 .. m-1 (i_stop = i)
-            s_l = underflow ? i + 1 : l;   // lowest rotation index applied
-            if (!underflow) {
-              dd[l] -= pp;
-              ee[l] = g;
-              ee[m] = 0.0;
-            }
+            s_l = ql_sweep(dd, ee, l, m, rc, rs);   // lowest rotation index applied
             s_iters += 1;
           }
         }
@@ -1729,7 +1830,7 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_syev_ql(const double* __rest
   // 32 t + lane in slot t) and applies every reflector to them -- Z is read and written once instead of once
   // per reflector (2 GB of L2 / DRAM traffic per 512 x 512 problem), no barrier between reflectors; the
   // reflector vectors are shared by the CTA's warps through L1, the next one is loaded ahead
-  if (GL && col_bt) {
+  if (GL && (flags & 1)) {
     for (int c0 = wid; c0 < n; c0 += 2 * kTriWarps) {
       const int c1 = c0 + kTriWarps;
       const bool two = c1 < n;
@@ -1847,7 +1948,12 @@ cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_i
     return cudaGetLastError();
   }
   // CMSVD_SYEV_COLBT=0: the per-reflector back-transformation (one pass over Z per reflector)
-  static const int col_bt = [] { const char* e = getenv("CMSVD_SYEV_COLBT"); return (e && e[0] == '0') ? 0 : 1; }();
+  // CMSVD_SYEV_QLF=1: fused QL sweeps (Z read and written once per 4 sweeps)
+  static const int col_bt = [] {
+    const char* e = getenv("CMSVD_SYEV_COLBT");
+    const char* f = getenv("CMSVD_SYEV_QLF");
+    return ((e && e[0] == '0') ? 0 : 1) | ((f && f[0] == '1') ? 2 : 0);
+  }();
   // in place in global memory (G is destroyed); batches sized to stay L2-resident
   cudaError_t e = cudaFuncSetAttribute(k_syev_ql<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
