@@ -77,6 +77,8 @@ cmsvd_status cmsvd_create(int device, void* cuda_stream, cmsvd_ctx* out) {
   if (const char* env = getenv("CMSVD_WS_BYTES")) h->c.ws_budget = (size_t)atoll(env);
   if (const char* env = getenv("CMSVD_NO_TC")) h->c.use_tc = !(env[0] == '1');
   if (const char* env = getenv("CMSVD_GL_BATCH_MB")) h->c.gl_batch_mb = std::max(1, atoi(env));
+  if (const char* env = getenv("CMSVD_SYEV_COLBT")) if (env[0] == '0') h->c.syev_flags &= ~1;
+  if (const char* env = getenv("CMSVD_SYEV_QLF")) if (env[0] == '0') h->c.syev_flags &= ~2;
   if (const char* env = getenv("CMSVD_ZZ_SYRK")) h->c.zz_syrk = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_BIG_TC")) h->c.big_tc = !(env[0] == '0');
   if (const char* env = getenv("CMSVD_TC_WIDE")) h->c.tc_wide = !(env[0] == '0');

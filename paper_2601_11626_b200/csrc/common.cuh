@@ -132,6 +132,7 @@ struct Ctx {
   bool use_tc = true;                  // tcgen05 contraction kernel (CMSVD_NO_TC=1 selects the SIMT path)
   bool tc_ok = true;                   // every block numerically full column rank (set by block_spectra)
   int gl_batch_mb = 1024;              // in-place global-memory eigen batches (n > 160), MB of matrices per launch
+  int syev_flags = 3;                  // k_syev_ql<true>: bit 0 column-resident back-transformation (CMSVD_SYEV_COLBT=0 clears), bit 1 fused QL sweeps (CMSVD_SYEV_QLF=0 clears)
   bool sbr_fused = false;              // band reduction: look-ahead fused update + product pass (CMSVD_SBR_FUSED=1;
                                        // measured 24.8 vs 23.0 ms unfused at n = 512: the partials' traffic)
   bool sbr_tma = true;                 // band reduction: TMA tile loads/stores in the rank-32 update (CMSVD_SBR_TMA=0)

@@ -1947,13 +1947,9 @@ cudaError_t launch_syev(Ctx& c, const double* G, int64_t ld_in, int64_t stride_i
     c.launches += 1;
     return cudaGetLastError();
   }
-  // CMSVD_SYEV_COLBT=0: the per-reflector back-transformation (one pass over Z per reflector)
-  // CMSVD_SYEV_QLF=1: fused QL sweeps (Z read and written once per 4 sweeps)
-  static const int col_bt = [] {
-    const char* e = getenv("CMSVD_SYEV_COLBT");
-    const char* f = getenv("CMSVD_SYEV_QLF");
-    return ((e && e[0] == '0') ? 0 : 1) | ((f && f[0] == '1') ? 2 : 0);
-  }();
+  // c.syev_flags: CMSVD_SYEV_COLBT=0 keeps the per-reflector back-transformation (one pass over Z per reflector),
+  // CMSVD_SYEV_QLF=0 the sweep-by-sweep QL rotations instead of the fused pass (Z read and written once per 4 sweeps)
+  const int col_bt = c.syev_flags;
   // in place in global memory (G is destroyed); batches sized to stay L2-resident
   cudaError_t e = cudaFuncSetAttribute(k_syev_ql<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -160,3 +160,33 @@ def test_chase_two_in_flight_queue(cm, monkeypatch):
         ref = refs[n][:k] * scale[i]
         tol = 2e-11 * np.abs(ref) + 1e-12 * abs(ref[0]) * max(1.0, n / 64)
         assert np.all(np.abs(ev[i, :k] - ref) <= tol), (i, n, np.abs(ev[i, :k] - ref).max())
+
+
+@pytest.mark.parametrize("colbt,qlf", [("1", "1"), ("0", "1"), ("1", "0"), ("0", "0")])
+def test_syev_inplace_variants(cm, colbt, qlf, monkeypatch):
+    """k_syev_ql<true> (160 < n <= 512, Z in place in global memory): the column-resident back-transformation
+    and the fused four-sweep QL pass, and their one-at-a-time forms (CMSVD_SYEV_COLBT=0, CMSVD_SYEV_QLF=0),
+    through the N1 codec (cmsvd_cluster_factors on a 300-column cluster, Thm EYM): the
+    reconstruction from the returned factors has exactly the rank-r tail energy that LAPACK's singular
+    values of the explicit concatenation give, and V has orthonormal columns."""
+    monkeypatch.setenv("CMSVD_SYEV_COLBT", colbt)
+    monkeypatch.setenv("CMSVD_SYEV_QLF", qlf)
+    R = np.random.default_rng(300)
+    m, n, r = 600, 150, 40
+    dec = np.exp(-0.03 * np.arange(2 * n))
+    X = (np.linalg.qr(R.standard_normal((m, 2 * n)))[0] * dec) @ np.linalg.qr(R.standard_normal((2 * n, 2 * n)))[0]
+    blocks = np.ascontiguousarray(np.stack([X[:, :n].T, X[:, n:].T, R.standard_normal((n, m))]), dtype=np.float32)
+    with cm.Context(0) as ctx:
+        ctx.register(blocks)
+        ctx.block_spectra(r)
+        fac = ctx.cluster_factors(np.array([0, 0, 1], np.int32))
+    members, Ut, V = fac[0]
+    assert list(members) == [0, 1]
+    X32 = np.concatenate([blocks[0].T, blocks[1].T], axis=1).astype(np.float64)
+    s = np.linalg.svd(X32, compute_uv=False)
+    tail = float(np.sum(s[r:] ** 2))
+    Xh = Ut.astype(np.float64) @ V.astype(np.float64).T
+    err2 = float(np.sum((X32 - Xh) ** 2))
+    assert abs(err2 - tail) <= 1e-4 * tail + 1e-9 * float(np.sum(s ** 2)), (err2, tail)
+    G = V.astype(np.float64).T @ V.astype(np.float64)
+    assert np.allclose(G, np.eye(G.shape[0]), atol=1e-5)
