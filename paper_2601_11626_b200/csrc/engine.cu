@@ -374,7 +374,7 @@ Status do_block_spectra_big(Ctx& c, int32_t r, double* energy, float* sigma, int
         CK(launch_syev(c, H, s, (int64_t)s * s, dns, nb, s, (double*)c.ws[WS_V].p, (int64_t)s * s,
                        (double*)c.ws[WS_B].p, (double*)c.ws[WS_EV].p, (int*)c.ws[WS_PERM].p, s, st + nb),
            "spectra: eig(H)");
-        dim3 g((unsigned)((m + 255) / 256), kc, nb);
+        dim3 g((unsigned)((m + 255) / 256), (unsigned)((kc + 7) / 8), nb);   // kLvCols = 8 Ritz vectors per CTA
         k_big_leftvec<<<g, 256, 0, c.stream>>>(m, s, kc, Y, (const double*)c.ws[WS_V].p, (const int*)c.ws[WS_PERM].p,
                                                (float* const*)dU);
         c.launches += 1;

@@ -463,17 +463,40 @@ cudaError_t cholqr(Ctx& c, int batch, int64_t rows, int s, double* Y, double* Yt
 
 // U[:, l] = Y W[:, perm[l]] (fp32 out) for l < kc: the top-kc left singular
 // vectors from the Rayleigh-Ritz step (Y = orthonormal range basis, m x s).
+// A CTA stages kLvCols Ritz vectors in shared memory and every thread carries
+// its row through all of them (Y is read once per kLvCols columns instead of
+// once per column; each output is the same sequential fp64 fma chain over k).
+constexpr int kLvCols = 8, kLvChunk = 512;
 __global__ void __launch_bounds__(256) k_big_leftvec(int64_t m, int s, int kc, const double* __restrict__ Y,
                                                      const double* __restrict__ V, const int* __restrict__ perm,
                                                      float* const* __restrict__ Uout) {
-  const int b = blockIdx.z, l = blockIdx.y;
+  __shared__ double sv[kLvCols][kLvChunk];
+  const int b = blockIdx.z, l0 = blockIdx.y * kLvCols;
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= m || l >= kc) return;
   const double* y = Y + (int64_t)b * m * s;
-  const double* v = V + (int64_t)b * s * s + (int64_t)perm[(int64_t)b * s + l] * s;
-  double acc = 0.0;
-  for (int k = 0; k < s; ++k) acc = fma(y[(int64_t)k * m + row], v[k], acc);
-  Uout[b][(int64_t)l * m + row] = (float)acc;
+  const int nl = min(kLvCols, kc - l0);
+  double acc[kLvCols];
+#pragma unroll
+  for (int j = 0; j < kLvCols; ++j) acc[j] = 0.0;
+  for (int k0 = 0; k0 < s; k0 += kLvChunk) {
+    const int kn = min(kLvChunk, s - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kLvCols * kn; e += blockDim.x) {
+      const int j = e / kn, k = e - j * kn;
+      sv[j][k] = j < nl ? V[(int64_t)b * s * s + (int64_t)perm[(int64_t)b * s + l0 + j] * s + k0 + k] : 0.0;
+    }
+    __syncthreads();
+    if (row < m)
+      for (int k = 0; k < kn; ++k) {
+        const double yk = y[(int64_t)(k0 + k) * m + row];
+#pragma unroll
+        for (int j = 0; j < kLvCols; ++j) acc[j] = fma(yk, sv[j][k], acc[j]);
+      }
+  }
+  if (row < m)
+#pragma unroll
+    for (int j = 0; j < kLvCols; ++j)
+      if (j < nl) Uout[b][(int64_t)(l0 + j) * m + row] = (float)acc[j];
 }
 
 // Spectrum statistics + descriptors for "big" blocks (A22): only the top
